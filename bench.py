@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""bench.py -- paged decode-attention step on B200: achieved HBM GB/s, us/step.
+
+One step = copy_blocks (when the step has copy-on-write pairs) +
+reshape_and_cache + paged_attention (+ its split-context reduce) for ONE attention
+layer over the whole batch, all on one stream; at N > 1 GPUs heads are sharded
+tensor-parallel style and the per-rank output head slices are all-gathered
+with NCCL (+ permute to [S][H][D]).
+
+value = logical K/V bytes read per step by all ranks / device step time (GB/s); the
+roofline object reports the dominant call (pa_paged_attention) against
+MEASURED_PEAKS.json's HBM copy bandwidth.  Inputs are seeded synthetic data with the
+BASELINE.json shapes (synth/), resident in HBM; the 2+ GB KV working set is > 15x the
+126 MB L2, so consecutive steps stream from HBM (no flush needed; stated in config).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_sharegpt] [--impl ours|reference]
+Under torchrun (N > 1) every rank runs its head shard; rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "paged decode-attention achieved HBM GB/s (% of peak), us/step"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(config: str, n: int):
+    """ncu dram bytes per launch of the dominant kernel, from the committed profile summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(config, {}).get(str(n))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML samples of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="c2_sharegpt")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--partition-tokens", type=int, default=0)
+    ap.add_argument("--block-size", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--extra", action="store_true", help="also print per-config lines for the other configs")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------- reference arm ---
+
+def oracle_sample(wl, budget_s: float, steps_total: int):
+    """Pick a bounded sample (sequences x heads) of the workload for the oracle."""
+    import oracle
+    from synth import materialize_numpy, shard, subset
+    rs = np.random.default_rng(wl.seed)
+    order = rs.permutation(wl.S)
+    # heads: a slice of the heads keeps input generation small
+    world = 1
+    for w in (10, 8, 6, 5, 4, 3, 2, 1):
+        if wl.H % w == 0 and wl.H_kv % w == 0 and wl.H // w >= 2:
+            world = w
+            break
+    nseq = 8
+    while True:
+        sub = shard(subset(wl, sorted(order[:nseq].tolist())), 0, world)
+        x = materialize_numpy(sub)
+        args = (x["query"], x["key_cache"], x["value_cache"], sub.block_tables, sub.context_lens, sub.scale, sub.B,
+                sub.H_kv, sub.dtype)
+        t0 = time.perf_counter()
+        oracle.paged_attention(*args)
+        dt = time.perf_counter() - t0
+        if dt * steps_total <= budget_s or nseq == 1:
+            return sub, args, dt
+        nseq = max(1, nseq // 2)
+
+
+def run_reference(a, wl, world, rank):
+    if rank != 0:
+        return
+    import oracle
+    threads = oracle.max_threads()
+    sub, args, dt = oracle_sample(wl, budget_s=150.0, steps_total=a.steps + a.warmup)
+    for _ in range(a.warmup):
+        oracle.paged_attention(*args)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        oracle.paged_attention(*args)
+    el = time.perf_counter() - t0
+    kv = sub.logical_kv_bytes()
+    gbs = kv * a.steps / el / 1e9
+    sample = f"{sub.S} of {wl.S} sequences x {sub.H} of {wl.H} heads per step (ctx sum {int(sub.context_lens.sum())})"
+    line = {"impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": el / a.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl.name, "seqs": wl.S, "heads": wl.H, "head_dim": wl.D, "block_size": wl.B,
+                       "kv_dtype": wl.dtype},
+            "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- our arm ---------
+
+def run_ours(a, wl_full, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2309_06180_b200 as pa
+    from synth import materialize_torch, shard, tables_torch
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    wl = shard(wl_full, rank, world) if world > 1 else wl_full
+    x = materialize_torch(wl, dev)
+    tb = tables_torch(wl, dev)
+    q, kn, vn, kc, vc = x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"]
+    bt, cl, sm, bm = tb["block_tables"], tb["context_lens"], tb["slot_mapping"], tb["block_mapping"]
+    out = torch.empty_like(q)
+    mcl = wl.max_context_len
+    ws_n = pa.paged_attention_workspace_size(wl.S, wl.H, wl.D, mcl, a.partition_tokens)
+    ws = torch.empty(max(ws_n, 16), dtype=torch.uint8, device=dev)
+    gathered = torch.empty((world, wl.S, wl.H, wl.D), dtype=q.dtype, device=dev) if world > 1 else None
+    full_out = torch.empty((wl.S, wl.H * world, wl.D), dtype=q.dtype, device=dev) if world > 1 else None
+    has_pairs = len(wl.block_mapping) > 0
+    stream = torch.cuda.current_stream(dev)
+    ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+
+    def step(i=None):
+        if has_pairs:
+            pa.copy_blocks([kc], [vc], bm)
+        pa.reshape_and_cache(kn, vn, kc, vc, sm)
+        if i is not None:
+            ev_a0[i].record(stream)
+        pa.paged_attention(out, q, kc, vc, bt, cl, wl.scale, max_context_len=mcl,
+                           partition_tokens=a.partition_tokens, workspace=ws)
+        if i is not None:
+            ev_a1[i].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, out)
+            full_out.copy_(gathered.permute(1, 0, 2, 3).reshape(wl.S, world * wl.H, wl.D))
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    pa.take_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for i in range(a.steps):
+            step(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = pa.take_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_total = e0.elapsed_time(e1)
+    attn_ms = float(np.mean([ev_a0[i].elapsed_time(ev_a1[i]) for i in range(a.steps)]))
+    t = torch.tensor([ms_total, attn_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total, attn_ms = float(t[0]), float(t[1])
+    ms_step = ms_total / a.steps
+
+    # ---- e2e: the same step through pa_decode_step with pinned host buffers ----------
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, wl, world, dev, {"query": q, "key": kn, "value": vn}, kc, vc, mcl, ws, stream)
+
+    if rank != 0:
+        return
+    peak, peak_src = load_peaks()
+    kv_all = wl_full.logical_kv_bytes()
+    sb = wl.step_bytes()
+    attn_bytes = sb["kv_logical"] + sb["q_out"] + sb["tables"]   # per launch of pa_paged_attention, this rank
+    achieved = attn_bytes / (attn_ms * 1e-3) / 1e9
+    value = kv_all / (ms_step * 1e-3) / 1e9
+    traffic = load_traffic(wl_full.name, world)
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms_step, "us_per_step": ms_step * 1e3, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "strong",
+        "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic (seeded; shapes of BASELINE.json configs)",
+        "config": {"workload": wl_full.name, "seqs": wl_full.S, "heads": wl_full.H, "kv_heads": wl_full.H_kv,
+                   "head_dim": wl_full.D, "block_size": wl_full.B, "kv_dtype": wl_full.dtype,
+                   "mean_ctx": float(wl_full.context_lens.mean()), "max_ctx": int(wl_full.max_context_len),
+                   "cow_pairs": int(len(wl_full.block_mapping)), "parallelism": f"tp{world}",
+                   "partition_tokens": a.partition_tokens or pa.DEFAULT_PARTITION_TOKENS,
+                   "l2": "inputs larger than L2 (KV %.2f GB vs 126 MB L2); no flush" % (kv_all / 1e9)},
+        "tokens_per_s": wl_full.S / (ms_step * 1e-3),
+        "kv_tokens_per_s": float(wl_full.context_lens.sum()) / (ms_step * 1e-3),
+        "frac_of_peak": value / peak,
+        "roofline": {"bound": "hbm", "kernel": "pa_paged_attention (paged_attention_kernel + reduce)",
+                     "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes_per_launch": attn_bytes,
+                     "avg_launch_ms": attn_ms},
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if not a.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(wl_full)
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(a, wl, world, dev, x, kc, vc, mcl, ws, stream):
+    """Same metric measured through pa_decode_step: per step H2D of the step's inputs
+    from pinned host memory, the kernels, and D2H of the output."""
+    import torch
+
+    import paper_2309_06180_b200 as pa
+    pin = {k: x[k].cpu().pin_memory() for k in ("query", "key", "value")}
+    host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in
+            dict(slot=wl.slot_mapping, bt=wl.block_tables, cl=wl.context_lens,
+                 bm=wl.block_mapping.reshape(-1, 2)).items()}
+    out = torch.empty(pin["query"].shape, dtype=pin["query"].dtype).pin_memory()
+    st = torch.empty(pa.decode_step_staging_size(wl.S, wl.H, wl.H_kv, wl.D, wl.W, len(wl.block_mapping),
+                                                 pin["query"].dtype), dtype=torch.uint8, device=dev)
+    h2d = sum(t.numel() * t.element_size() for t in list(pin.values()) + list(host.values()))
+    d2h = out.numel() * out.element_size()
+    steps = max(10, min(a.steps, 200))
+
+    def one():
+        pa.decode_step(out, pin["query"], pin["key"], pin["value"], host["slot"], host["bt"], host["cl"], host["bm"],
+                       kc, vc, wl.scale, st, ws, max_context_len=mcl, stream=stream)
+
+    for _ in range(3):
+        one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    kv_all = wl.logical_kv_bytes() * world
+    return {"value": kv_all / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms, "steps": steps,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "pa_decode_step (C ABI, pinned host buffers)"}
+
+
+def cpu_baseline(wl):
+    import oracle
+    sub, args, dt = oracle_sample(wl, budget_s=20.0, steps_total=1)
+    reps = max(1, int(10.0 / max(dt, 1e-3)))
+    reps = min(reps, 20)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.paged_attention(*args)
+    el = (time.perf_counter() - t0) / reps
+    return {"value": sub.logical_kv_bytes() / el / 1e9, "unit": "GB/s", "cores": oracle.max_threads(),
+            "kind": "oracle", "sample": f"{sub.S} of {wl.S} sequences x {sub.H} of {wl.H} heads, {reps} reps, "
+                                        f"{el:.3f} s each (fp64 C, OpenMP)"}
+
+
+def main():
+    a = parse()
+    world, rank, local = dist_env()
+    from synth import make_config
+    over = {"B": a.block_size} if a.block_size else {}
+    wl = make_config(a.config, **over)
+    if a.impl == "reference":
+        run_reference(a, wl, world, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        run_ours(a, wl, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,209 @@
+/*
+ * pa.h -- C ABI of libpagedattn.so, the B200 (sm_100a) PagedAttention decode hot path.
+ *
+ * Paper: Kwon et al., "Efficient Memory Management for Large Language Model Serving
+ * with PagedAttention", SOSP'23 (arXiv 2309.06180).  P:N = PAPER.md line N.
+ *
+ * Conventions for every entry point
+ *  - Tensor pointers are DEVICE pointers owned by the caller unless a parameter says
+ *    HOST.  The library never allocates or frees device memory on these calls and
+ *    never synchronises the stream (except the pa_debug_* / pa_validate_* helpers and
+ *    pa_decode_step's documented D2H copy, which is stream-ordered).
+ *  - Element type of query/out/key/value/caches is `dtype` (fp32, fp16 or bf16);
+ *    arithmetic is fp32 with round-to-nearest-even output.
+ *  - KV cache layout ("optimized for block read"; reading c7):
+ *        key_cache, value_cache: [num_blocks][num_kv_heads][block_size][head_dim]
+ *    so one (block, kv head) chunk is block_size*head_dim contiguous elements.
+ *  - block_tables: int32 [num_seqs][max_blocks_per_seq] row-major (row stride W);
+ *    entry j < ceil(ctx/B) of row s is the physical block of logical block j
+ *    (P:254-256).  Entries beyond are never read.  context_lens: int32 [num_seqs],
+ *    the number of tokens INCLUDING the current one (written before attention).
+ *  - Errors are detected on the host before any launch and returned as a status;
+ *    pa_last_error() gives a thread-local message.  Checked: null pointers, 16-byte
+ *    alignment of every tensor pointer, dims <= 0, num_heads % num_kv_heads,
+ *    head_dim in {64, 128}, block_size a power of two in [1, 256], workspace size.
+ *    Device-side contract violations (a block id outside [0, num_blocks), ctx >
+ *    W*block_size, repeated slots) are undefined behaviour; pa_validate_tables()
+ *    checks them in tests.  A failed launch returns PA_ERR_CUDA.
+ */
+#ifndef PAGED_ATTN_PA_H_
+#define PAGED_ATTN_PA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* pa_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum { PA_F32 = 0, PA_F16 = 1, PA_BF16 = 2 } pa_dtype_t;
+
+typedef enum {
+    PA_OK = 0,
+    PA_ERR_INVALID_ARG = 1,
+    PA_ERR_UNSUPPORTED = 2,
+    PA_ERR_WORKSPACE = 3,
+    PA_ERR_CUDA = 4,
+    PA_ERR_OUT_OF_BLOCKS = 5
+} pa_status_t;
+
+/* Library default partition size (tokens) of the split-context variant. */
+#define PA_DEFAULT_PARTITION_TOKENS 512
+
+/* ------------------------------------------------------------------------------------
+ * pa_paged_attention -- single-query decode attention over the paged KV cache.
+ *
+ * Eq.4: for every sequence s and query head h, with kv head
+ * kvh = h / (num_heads / num_kv_heads) and n = context_lens[s]:
+ *     l_t = scale * q[s][h] . K[t],   t = 0..n-1, K[t] = key_cache[bt[s][t/B]][kvh][t%B]
+ *     out[s][h] = sum_t softmax(l)_t * V[t]                 (n == 0 -> out = 0)
+ * out, query: [num_seqs][num_heads][head_dim].  `scale` is the caller's (1/sqrt(D)
+ * in every config, reading c1).
+ *
+ * Contexts longer than PA_DEFAULT_PARTITION_TOKENS use the split-context variant
+ * (BJ:north_star): partitions of that many logical tokens each produce (m, L, o~)
+ * into `workspace`, then a log-sum-exp reduce kernel merges them.  The partition
+ * size depends on nothing but the context length, so results are bitwise identical
+ * for any batch composition, block size, physical placement or head sharding.
+ * max_context_len: host upper bound of context_lens (<= 0 -> W * block_size); it
+ * only sizes the grid.  workspace: device, >= pa_paged_attention_workspace_size(),
+ * 16-byte aligned; may be NULL when that size is 0.
+ * ---------------------------------------------------------------------------------- */
+pa_status_t pa_paged_attention(void* out, const void* query, const void* key_cache,
+                               const void* value_cache, const int32_t* block_tables,
+                               const int32_t* context_lens, float scale, int block_size,
+                               int num_kv_heads, int num_seqs, int num_heads, int head_dim,
+                               int max_blocks_per_seq, int max_context_len, pa_dtype_t dtype,
+                               void* workspace, size_t workspace_bytes, pa_stream_t stream);
+
+/* Same, with an explicit partition size in tokens (a positive multiple of 16;
+ * 0 -> PA_DEFAULT_PARTITION_TOKENS).  A partition size >= max_context_len runs the
+ * single-pass kernel only.  Used by tests (split vs single-pass) and ablations. */
+pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_cache,
+                                  const void* value_cache, const int32_t* block_tables,
+                                  const int32_t* context_lens, float scale, int block_size,
+                                  int num_kv_heads, int num_seqs, int num_heads, int head_dim,
+                                  int max_blocks_per_seq, int max_context_len, pa_dtype_t dtype,
+                                  int partition_tokens, void* workspace, size_t workspace_bytes,
+                                  pa_stream_t stream);
+
+/* Bytes of workspace pa_paged_attention(_ex) needs (0 if no context is split).
+ * partition_tokens as in pa_paged_attention_ex. */
+size_t pa_paged_attention_workspace_size(int num_seqs, int num_heads, int head_dim,
+                                         int max_context_len, int partition_tokens);
+
+/* ------------------------------------------------------------------------------------
+ * pa_reshape_and_cache -- fused reshape + block write.
+ * For token i with slot = slot_mapping[i] >= 0: b = slot / B, o = slot % B and
+ *     key_cache[b][h][o][:] = key[i][h][:],  value_cache[b][h][o][:] = value[i][h][:]
+ * for every kv head h.  slot < 0 skips the token (reading c11).  Bit-exact copy.
+ * key, value: [num_tokens][num_kv_heads][head_dim]; slot_mapping: int64 [num_tokens].
+ * Slots must be distinct and < num_blocks * block_size.  num_tokens == 0 is a no-op.
+ * ---------------------------------------------------------------------------------- */
+pa_status_t pa_reshape_and_cache(const void* key, const void* value, void* key_cache,
+                                 void* value_cache, const int64_t* slot_mapping, int num_tokens,
+                                 int num_kv_heads, int head_dim, int block_size, pa_dtype_t dtype,
+                                 pa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * pa_copy_blocks -- fused block copy for copy-on-write.
+ * For every layer l < num_layers and pair p: key_caches[l][dst] <- key_caches[l][src]
+ * and the same for value_caches, whole blocks (num_kv_heads*block_size*head_dim
+ * elements), in ONE launch.  key_caches / value_caches: HOST arrays of num_layers
+ * device pointers.  block_mapping: device int64 [num_pairs][2] = (src, dst).
+ * Precondition (reading c12): dst ids distinct and disjoint from every src id (a CoW
+ * destination is always a fresh block); src ids may repeat.  num_pairs == 0
+ * is a no-op.  num_layers <= 256.
+ * ---------------------------------------------------------------------------------- */
+pa_status_t pa_copy_blocks(void* const* key_caches, void* const* value_caches, int num_layers,
+                           const int64_t* block_mapping, int num_pairs, int num_kv_heads,
+                           int block_size, int head_dim, pa_dtype_t dtype, pa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * pa_decode_step -- one decode step of one attention layer from HOST inputs: the
+ * end-to-end call of bench.py's "e2e" number.  Stream-ordered:
+ *   H2D  query/key/value/slot_mapping/block_tables/context_lens/block_mapping
+ *        (HOST, ideally pinned) into the device staging buffer `staging`
+ *   pa_copy_blocks (if num_pairs > 0) on (key_cache, value_cache)
+ *   pa_reshape_and_cache, pa_paged_attention (default partitioning)
+ *   D2H  out -> host_out (HOST)
+ * key_cache/value_cache/workspace/staging: DEVICE.  staging must hold
+ * pa_decode_step_staging_size() bytes.  The call returns after enqueueing; the
+ * caller synchronises the stream before reading host_out.
+ * ---------------------------------------------------------------------------------- */
+size_t pa_decode_step_staging_size(int num_seqs, int num_heads, int num_kv_heads, int head_dim,
+                                   int max_blocks_per_seq, int num_pairs, pa_dtype_t dtype);
+pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* host_key,
+                           const void* host_value, const int64_t* host_slot_mapping,
+                           const int32_t* host_block_tables, const int32_t* host_context_lens,
+                           const int64_t* host_block_mapping, int num_pairs,
+                           void* key_cache, void* value_cache, float scale, int block_size,
+                           int num_kv_heads, int num_seqs, int num_heads, int head_dim,
+                           int max_blocks_per_seq, int max_context_len, pa_dtype_t dtype,
+                           void* staging, size_t staging_bytes, void* workspace,
+                           size_t workspace_bytes, pa_stream_t stream);
+
+/* Thread-local message for the last non-OK status of this thread ("" if none). */
+const char* pa_last_error(void);
+
+/* Number of kernel launches the library issued on this thread since the last call
+ * (bench.py's gpu_launches evidence).  Resets the counter. */
+long long pa_take_launch_count(void);
+
+/* ------------------------------------------------------------------------------------
+ * Test-only helpers (synchronising).
+ * pa_debug_gather_kv: k_out/v_out [num_seqs][num_kv_heads][max_ctx][head_dim] (DEVICE)
+ * receive the K/V rows of logical tokens t < context_lens[s] through the SAME tile
+ * loader the attention kernel uses (block-table lookup + bulk copy into shared memory),
+ * rows t >= ctx untouched.  For the bitwise block-table indexing check.
+ * pa_validate_tables: every live entry bt[s][j], j < ceil(ctx[s]/B), in [0,NB);
+ * 0 <= ctx[s] <= W*B.  *first_bad_out (HOST) = first bad flat index s*W+j (or
+ * -(s+1) for a bad ctx) or -1 when all valid.
+ * ---------------------------------------------------------------------------------- */
+pa_status_t pa_debug_gather_kv(void* k_out, void* v_out, const void* key_cache,
+                               const void* value_cache, const int32_t* block_tables,
+                               const int32_t* context_lens, int block_size, int num_kv_heads,
+                               int num_seqs, int head_dim, int max_blocks_per_seq, int max_ctx,
+                               pa_dtype_t dtype, pa_stream_t stream);
+pa_status_t pa_validate_tables(const int32_t* block_tables, const int32_t* context_lens,
+                               int num_seqs, int max_blocks_per_seq, int block_size,
+                               int num_blocks, int64_t* first_bad_out, pa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * Host block allocator -- the paper's KV block manager (P:249-256, P:295-332,
+ * P:451-458), used only on the host to generate block tables, slot mappings and
+ * copy-on-write pairs.  Single-threaded per allocator object.
+ *  - physical blocks 0..num_blocks-1, handed out in `initial_order` (HOST int32
+ *    [num_blocks], a permutation; NULL = 0,1,2,...); freed blocks join the BACK of
+ *    the FIFO free list (Fig.9: after freeing 2,4,5,8 the next blocks are 9-12).
+ *  - allocate(n): ceil(n/B) fresh blocks, filled left to right.
+ *  - append_slot: the slot (block*B + offset) of one new token; a new block when the
+ *    last is full; copy-on-write when the last block is partial and shared
+ *    (refcount > 1): cow_src_out / cow_dst_out receive (old, new), else -1.
+ *  - fork: a child sharing every block (refcount + 1).
+ *  - free: drop the sequence; blocks whose refcount reaches 0 are freed.
+ * Errors: PA_ERR_OUT_OF_BLOCKS (free list empty), PA_ERR_INVALID_ARG (unknown or
+ * freed handle = double free, bad sizes).
+ * ---------------------------------------------------------------------------------- */
+typedef struct pa_alloc pa_alloc_t;
+pa_alloc_t* pa_alloc_create(int num_blocks, int block_size, const int32_t* initial_order);
+void pa_alloc_destroy(pa_alloc_t* a);
+pa_status_t pa_alloc_allocate(pa_alloc_t* a, int num_tokens, int* seq_out);
+pa_status_t pa_alloc_append_slot(pa_alloc_t* a, int seq, int64_t* slot_out, int* cow_src_out,
+                                 int* cow_dst_out);
+pa_status_t pa_alloc_fork(pa_alloc_t* a, int parent, int* child_out);
+pa_status_t pa_alloc_free(pa_alloc_t* a, int seq, int* freed_out);
+/* Rows of the given sequences into block_tables_out (HOST int32 [n][W], padded -1)
+ * and their token counts into context_lens_out (HOST int32 [n]). */
+pa_status_t pa_alloc_export(const pa_alloc_t* a, const int* seqs, int n, int W,
+                            int32_t* block_tables_out, int32_t* context_lens_out);
+int pa_alloc_refcount(const pa_alloc_t* a, int block);
+int pa_alloc_num_free(const pa_alloc_t* a);
+int pa_alloc_num_blocks_of(const pa_alloc_t* a, int seq); /* -1 if unknown */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAGED_ATTN_PA_H_ */

@@ -1,0 +1,380 @@
+// pa_api.cpp -- the C ABI of libpagedattn.so (include/pa.h): argument validation on the
+// host, launch configuration, workspace sizing, error strings.  No allocation and no
+// synchronisation on the hot path.
+#include "../../include/pa.h"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "pa_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local long long g_launches = 0;
+
+pa_status_t fail(pa_status_t st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+pa_status_t fail(pa_status_t st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+pa_status_t cuda_fail(cudaError_t e, const char* where) {
+    return fail(PA_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int elem_bytes(pa_dtype_t d) { return d == PA_F32 ? 4 : 2; }
+
+bool valid_dtype(pa_dtype_t d) { return d == PA_F32 || d == PA_F16 || d == PA_BF16; }
+
+int log2_pow2(int b) {  // -1 if not a power of two in [1, 256]
+    if (b < 1 || b > 256 || (b & (b - 1))) return -1;
+    int l = 0;
+    while ((1 << l) < b) ++l;
+    return l;
+}
+
+#define REQUIRE(cond, ...)                                   \
+    do {                                                     \
+        if (!(cond)) return fail(PA_ERR_INVALID_ARG, __VA_ARGS__); \
+    } while (0)
+
+#define REQUIRE_PTR(p, align)                                                                  \
+    do {                                                                                       \
+        if ((p) == nullptr) return fail(PA_ERR_INVALID_ARG, "%s is NULL", #p);                \
+        if (!aligned((p), (align)))                                                            \
+            return fail(PA_ERR_INVALID_ARG, "%s is not %d-byte aligned", #p, (int)(align));   \
+    } while (0)
+
+int effective_partition(int partition_tokens) {
+    return partition_tokens == 0 ? PA_DEFAULT_PARTITION_TOKENS : partition_tokens;
+}
+
+size_t workspace_bytes_for(int64_t S, int64_t H, int64_t D, int max_ctx, int PT) {
+    if (S <= 0 || H <= 0 || D <= 0 || max_ctx <= 0 || PT <= 0) return 0;
+    const int64_t NP = (max_ctx + PT - 1) / PT;
+    if (NP <= 1) return 0;
+    // part_o [S][H][NP][D] fp32, then part_ml [S][H][NP] float2
+    return (size_t)(S * H * NP * D * 4 + S * H * NP * 8);
+}
+
+}  // namespace
+
+namespace pa {
+void count_launch() { ++g_launches; }
+}  // namespace pa
+
+extern "C" {
+
+const char* pa_last_error(void) { return g_err.c_str(); }
+
+long long pa_take_launch_count(void) {
+    long long n = g_launches;
+    g_launches = 0;
+    return n;
+}
+
+size_t pa_paged_attention_workspace_size(int num_seqs, int num_heads, int head_dim, int max_context_len,
+                                         int partition_tokens) {
+    return workspace_bytes_for(num_seqs, num_heads, head_dim, max_context_len, effective_partition(partition_tokens));
+}
+
+pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_cache, const void* value_cache,
+                                  const int32_t* block_tables, const int32_t* context_lens, float scale,
+                                  int block_size, int num_kv_heads, int num_seqs, int num_heads, int head_dim,
+                                  int max_blocks_per_seq, int max_context_len, pa_dtype_t dtype,
+                                  int partition_tokens, void* workspace, size_t workspace_bytes,
+                                  pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
+    REQUIRE(num_seqs >= 0, "num_seqs must be >= 0 (got %d)", num_seqs);
+    REQUIRE(num_heads > 0 && num_kv_heads > 0, "num_heads and num_kv_heads must be positive");
+    REQUIRE(num_heads % num_kv_heads == 0, "num_heads (%d) must be a multiple of num_kv_heads (%d)", num_heads,
+            num_kv_heads);
+    if (head_dim != 64 && head_dim != 128)
+        return fail(PA_ERR_UNSUPPORTED, "head_dim must be 64 or 128 (got %d)", head_dim);
+    const int log2B = log2_pow2(block_size);
+    if (log2B < 0) return fail(PA_ERR_UNSUPPORTED, "block_size must be a power of two in [1,256] (got %d)", block_size);
+    REQUIRE(max_blocks_per_seq > 0, "max_blocks_per_seq must be positive");
+    REQUIRE(std::isfinite(scale), "scale must be finite");
+    const int PT = effective_partition(partition_tokens);
+    REQUIRE(PT > 0 && PT % 16 == 0, "partition_tokens must be a positive multiple of 16 (got %d)", partition_tokens);
+    REQUIRE(num_seqs <= 65535 && num_heads <= 65535, "num_seqs and num_heads must be <= 65535");
+    if (num_seqs == 0) return PA_OK;
+    REQUIRE_PTR(out, 16);
+    REQUIRE_PTR(query, 16);
+    REQUIRE_PTR(key_cache, 16);
+    REQUIRE_PTR(value_cache, 16);
+    REQUIRE_PTR(block_tables, 4);
+    REQUIRE_PTR(context_lens, 4);
+    const int64_t cap = (int64_t)max_blocks_per_seq * block_size;
+    int64_t mcl = max_context_len > 0 ? max_context_len : cap;
+    if (mcl > cap) mcl = cap;
+    REQUIRE(mcl <= (1 << 30), "max_context_len too large");
+    const int NP = (int)((mcl + PT - 1) / PT);
+    const size_t need = workspace_bytes_for(num_seqs, num_heads, head_dim, (int)mcl, PT);
+    if (need > 0) {
+        if (workspace == nullptr || workspace_bytes < need)
+            return fail(PA_ERR_WORKSPACE, "workspace of %zu bytes required (got %zu)", need,
+                        workspace ? workspace_bytes : (size_t)0);
+        REQUIRE_PTR(workspace, 16);
+    }
+    const size_t smem = pa::attention_smem_bytes((int)dtype, head_dim, PT, block_size);
+    if (smem > 227 * 1024)
+        return fail(PA_ERR_UNSUPPORTED, "partition_tokens %d with block_size %d needs %zu B of shared memory", PT,
+                    block_size, smem);
+
+    pa::AttnParams p{};
+    p.out = out;
+    p.query = query;
+    p.key_cache = key_cache;
+    p.value_cache = value_cache;
+    p.block_tables = block_tables;
+    p.context_lens = context_lens;
+    if (need > 0) {
+        const int64_t n = (int64_t)num_seqs * num_heads * NP;
+        p.part_o = static_cast<float*>(workspace);
+        p.part_ml = reinterpret_cast<float2*>(static_cast<char*>(workspace) + n * head_dim * 4);
+    }
+    p.scale_log2 = (float)((double)scale * 1.4426950408889634);
+    p.log2B = log2B;
+    p.H = num_heads;
+    p.H_kv = num_kv_heads;
+    p.G = num_heads / num_kv_heads;
+    p.W = max_blocks_per_seq;
+    p.PT = PT;
+    p.NP = NP;
+    cudaError_t e = pa::launch_attention(p, (int)dtype, head_dim, num_seqs, num_heads, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pa_paged_attention");
+    return PA_OK;
+}
+
+pa_status_t pa_paged_attention(void* out, const void* query, const void* key_cache, const void* value_cache,
+                               const int32_t* block_tables, const int32_t* context_lens, float scale, int block_size,
+                               int num_kv_heads, int num_seqs, int num_heads, int head_dim, int max_blocks_per_seq,
+                               int max_context_len, pa_dtype_t dtype, void* workspace, size_t workspace_bytes,
+                               pa_stream_t stream) {
+    return pa_paged_attention_ex(out, query, key_cache, value_cache, block_tables, context_lens, scale, block_size,
+                                 num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq, max_context_len,
+                                 dtype, 0, workspace, workspace_bytes, stream);
+}
+
+pa_status_t pa_reshape_and_cache(const void* key, const void* value, void* key_cache, void* value_cache,
+                                 const int64_t* slot_mapping, int num_tokens, int num_kv_heads, int head_dim,
+                                 int block_size, pa_dtype_t dtype, pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
+    REQUIRE(num_tokens >= 0, "num_tokens must be >= 0");
+    REQUIRE(num_kv_heads > 0, "num_kv_heads must be positive");
+    if (head_dim != 64 && head_dim != 128)
+        return fail(PA_ERR_UNSUPPORTED, "head_dim must be 64 or 128 (got %d)", head_dim);
+    const int log2B = log2_pow2(block_size);
+    if (log2B < 0) return fail(PA_ERR_UNSUPPORTED, "block_size must be a power of two in [1,256] (got %d)", block_size);
+    if (num_tokens == 0) return PA_OK;
+    REQUIRE_PTR(key, 16);
+    REQUIRE_PTR(value, 16);
+    REQUIRE_PTR(key_cache, 16);
+    REQUIRE_PTR(value_cache, 16);
+    REQUIRE_PTR(slot_mapping, 8);
+    pa::CacheWriteParams p{key, value, key_cache, value_cache, slot_mapping, num_tokens, num_kv_heads,
+                           head_dim * elem_bytes(dtype), log2B};
+    cudaError_t e = pa::launch_reshape_and_cache(p, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pa_reshape_and_cache");
+    return PA_OK;
+}
+
+pa_status_t pa_copy_blocks(void* const* key_caches, void* const* value_caches, int num_layers,
+                           const int64_t* block_mapping, int num_pairs, int num_kv_heads, int block_size,
+                           int head_dim, pa_dtype_t dtype, pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
+    REQUIRE(num_layers >= 1 && num_layers <= pa::kMaxLayers, "num_layers must be in [1, %d]", pa::kMaxLayers);
+    REQUIRE(num_pairs >= 0, "num_pairs must be >= 0");
+    REQUIRE(num_kv_heads > 0, "num_kv_heads must be positive");
+    if (head_dim != 64 && head_dim != 128)
+        return fail(PA_ERR_UNSUPPORTED, "head_dim must be 64 or 128 (got %d)", head_dim);
+    if (log2_pow2(block_size) < 0)
+        return fail(PA_ERR_UNSUPPORTED, "block_size must be a power of two in [1,256] (got %d)", block_size);
+    REQUIRE(key_caches != nullptr && value_caches != nullptr, "key_caches/value_caches host arrays are NULL");
+    if (num_pairs == 0) return PA_OK;
+    REQUIRE_PTR(block_mapping, 8);
+    pa::CopyBlocksParams p;
+    std::memset(&p, 0, sizeof(p));
+    for (int l = 0; l < num_layers; ++l) {
+        REQUIRE(key_caches[l] && value_caches[l], "layer %d cache pointer is NULL", l);
+        REQUIRE(aligned(key_caches[l], 16) && aligned(value_caches[l], 16), "layer %d cache not 16-byte aligned", l);
+        p.key_caches[l] = key_caches[l];
+        p.value_caches[l] = value_caches[l];
+    }
+    p.block_mapping = block_mapping;
+    p.block_bytes = (int64_t)num_kv_heads * block_size * head_dim * elem_bytes(dtype);
+    cudaError_t e = pa::launch_copy_blocks(p, num_layers, num_pairs, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pa_copy_blocks");
+    return PA_OK;
+}
+
+// ---- end-to-end step from host buffers ----------------------------------------------
+
+namespace {
+struct StagingLayout {
+    size_t q, k, v, out, slot, bt, ctx, bm, total;
+};
+size_t up256(size_t x) { return (x + 255) & ~(size_t)255; }
+StagingLayout staging_layout(int S, int H, int Hkv, int D, int W, int P, pa_dtype_t dt) {
+    StagingLayout L{};
+    const size_t e = (size_t)elem_bytes(dt);
+    size_t o = 0;
+    L.q = o;    o += up256((size_t)S * H * D * e);
+    L.k = o;    o += up256((size_t)S * Hkv * D * e);
+    L.v = o;    o += up256((size_t)S * Hkv * D * e);
+    L.out = o;  o += up256((size_t)S * H * D * e);
+    L.slot = o; o += up256((size_t)S * 8);
+    L.bt = o;   o += up256((size_t)S * W * 4);
+    L.ctx = o;  o += up256((size_t)S * 4);
+    L.bm = o;   o += up256((size_t)(P > 0 ? P : 0) * 16);
+    L.total = o;
+    return L;
+}
+}  // namespace
+
+size_t pa_decode_step_staging_size(int num_seqs, int num_heads, int num_kv_heads, int head_dim,
+                                   int max_blocks_per_seq, int num_pairs, pa_dtype_t dtype) {
+    if (num_seqs < 0 || num_heads <= 0 || num_kv_heads <= 0 || head_dim <= 0 || max_blocks_per_seq <= 0) return 0;
+    return staging_layout(num_seqs, num_heads, num_kv_heads, head_dim, max_blocks_per_seq, num_pairs, dtype).total;
+}
+
+pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* host_key, const void* host_value,
+                           const int64_t* host_slot_mapping, const int32_t* host_block_tables,
+                           const int32_t* host_context_lens, const int64_t* host_block_mapping, int num_pairs,
+                           void* key_cache, void* value_cache, float scale, int block_size, int num_kv_heads,
+                           int num_seqs, int num_heads, int head_dim, int max_blocks_per_seq, int max_context_len,
+                           pa_dtype_t dtype, void* staging, size_t staging_bytes, void* workspace,
+                           size_t workspace_bytes, pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
+    REQUIRE(num_seqs >= 0 && num_heads > 0 && num_kv_heads > 0 && max_blocks_per_seq > 0, "bad sizes");
+    REQUIRE(num_pairs >= 0, "num_pairs must be >= 0");
+    if (num_seqs == 0 && num_pairs == 0) return PA_OK;
+    REQUIRE(host_out && host_query && host_key && host_value && host_slot_mapping && host_block_tables &&
+                host_context_lens,
+            "a host input pointer is NULL");
+    REQUIRE(num_pairs == 0 || host_block_mapping, "host_block_mapping is NULL");
+    const StagingLayout L =
+        staging_layout(num_seqs, num_heads, num_kv_heads, head_dim, max_blocks_per_seq, num_pairs, dtype);
+    if (staging == nullptr || staging_bytes < L.total)
+        return fail(PA_ERR_WORKSPACE, "staging of %zu bytes required (got %zu)", L.total,
+                    staging ? staging_bytes : (size_t)0);
+    REQUIRE_PTR(staging, 256);
+    char* st = static_cast<char*>(staging);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t e = (size_t)elem_bytes(dtype);
+    struct Cp {
+        size_t off;
+        const void* src;
+        size_t n;
+    } cps[] = {{L.q, host_query, (size_t)num_seqs * num_heads * head_dim * e},
+               {L.k, host_key, (size_t)num_seqs * num_kv_heads * head_dim * e},
+               {L.v, host_value, (size_t)num_seqs * num_kv_heads * head_dim * e},
+               {L.slot, host_slot_mapping, (size_t)num_seqs * 8},
+               {L.bt, host_block_tables, (size_t)num_seqs * max_blocks_per_seq * 4},
+               {L.ctx, host_context_lens, (size_t)num_seqs * 4},
+               {L.bm, host_block_mapping, (size_t)num_pairs * 16}};
+    for (const Cp& c : cps) {
+        if (c.n == 0) continue;
+        cudaError_t err = cudaMemcpyAsync(st + c.off, c.src, c.n, cudaMemcpyHostToDevice, s);
+        if (err != cudaSuccess) return cuda_fail(err, "pa_decode_step H2D");
+    }
+    pa_status_t r;
+    if (num_pairs > 0) {
+        void* kcs[1] = {key_cache};
+        void* vcs[1] = {value_cache};
+        r = pa_copy_blocks(kcs, vcs, 1, reinterpret_cast<const int64_t*>(st + L.bm), num_pairs, num_kv_heads,
+                           block_size, head_dim, dtype, stream);
+        if (r != PA_OK) return r;
+    }
+    r = pa_reshape_and_cache(st + L.k, st + L.v, key_cache, value_cache, reinterpret_cast<const int64_t*>(st + L.slot),
+                             num_seqs, num_kv_heads, head_dim, block_size, dtype, stream);
+    if (r != PA_OK) return r;
+    r = pa_paged_attention(st + L.out, st + L.q, key_cache, value_cache, reinterpret_cast<const int32_t*>(st + L.bt),
+                           reinterpret_cast<const int32_t*>(st + L.ctx), scale, block_size, num_kv_heads, num_seqs,
+                           num_heads, head_dim, max_blocks_per_seq, max_context_len, dtype, workspace,
+                           workspace_bytes, stream);
+    if (r != PA_OK) return r;
+    cudaError_t err =
+        cudaMemcpyAsync(host_out, st + L.out, (size_t)num_seqs * num_heads * head_dim * e, cudaMemcpyDeviceToHost, s);
+    if (err != cudaSuccess) return cuda_fail(err, "pa_decode_step D2H");
+    return PA_OK;
+}
+
+// ---- test-only helpers -------------------------------------------------------------
+
+pa_status_t pa_debug_gather_kv(void* k_out, void* v_out, const void* key_cache, const void* value_cache,
+                               const int32_t* block_tables, const int32_t* context_lens, int block_size,
+                               int num_kv_heads, int num_seqs, int head_dim, int max_blocks_per_seq, int max_ctx,
+                               pa_dtype_t dtype, pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
+    if (head_dim != 64 && head_dim != 128) return fail(PA_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+    const int log2B = log2_pow2(block_size);
+    if (log2B < 0) return fail(PA_ERR_UNSUPPORTED, "block_size must be a power of two in [1,256]");
+    REQUIRE(num_seqs > 0 && num_kv_heads > 0 && max_blocks_per_seq > 0 && max_ctx > 0, "bad sizes");
+    REQUIRE_PTR(k_out, 16);
+    REQUIRE_PTR(v_out, 16);
+    REQUIRE_PTR(key_cache, 16);
+    REQUIRE_PTR(value_cache, 16);
+    REQUIRE_PTR(block_tables, 4);
+    REQUIRE_PTR(context_lens, 4);
+    pa::GatherParams p{k_out, v_out, key_cache, value_cache, block_tables, context_lens, log2B, num_kv_heads,
+                       max_blocks_per_seq, max_ctx};
+    cudaError_t e = pa::launch_debug_gather(p, (int)dtype, head_dim, num_seqs, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pa_debug_gather_kv");
+    return PA_OK;
+}
+
+pa_status_t pa_validate_tables(const int32_t* block_tables, const int32_t* context_lens, int num_seqs,
+                               int max_blocks_per_seq, int block_size, int num_blocks, int64_t* first_bad_out,
+                               pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(first_bad_out != nullptr, "first_bad_out is NULL");
+    REQUIRE(num_seqs >= 0 && max_blocks_per_seq > 0 && block_size > 0 && num_blocks > 0, "bad sizes");
+    *first_bad_out = -1;
+    if (num_seqs == 0) return PA_OK;
+    REQUIRE_PTR(block_tables, 4);
+    REQUIRE_PTR(context_lens, 4);
+    unsigned long long* d = nullptr;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMallocAsync(&d, sizeof(*d), s);
+    if (e != cudaSuccess) return cuda_fail(e, "pa_validate_tables alloc");
+    unsigned long long h = ~0ull;
+    e = cudaMemcpyAsync(d, &h, sizeof(h), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = pa::launch_validate_tables(block_tables, context_lens, num_seqs, max_blocks_per_seq, block_size,
+                                       num_blocks, d, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(d, s);
+    if (e != cudaSuccess) return cuda_fail(e, "pa_validate_tables");
+    const unsigned long long total = (unsigned long long)num_seqs * max_blocks_per_seq;
+    if (h == ~0ull)
+        *first_bad_out = -1;
+    else if (h >= total)
+        *first_bad_out = -(int64_t)(h - total) - 1;
+    else
+        *first_bad_out = (int64_t)h;
+    return PA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// pa_cache.cu -- the two kernels that maintain the paged KV cache (sm_100a).
+//
+//  reshape_and_cache  fused reshape + block write: each new token's K/V row
+//                     per kv head goes to (slot / B, head, slot % B) of the
+//                     [NB][H_kv][B][D] cache; 16-byte vector copies, bit-exact.
+//  copy_blocks        fused block copy: every copy-on-write (src, dst) pair
+//                     of every layer in ONE launch instead of many cudaMemcpyAsync calls.
+//  validate_tables    test helper: block ids in range, ctx <= W*B.
+#include "pa_common.cuh"
+#include "pa_internal.h"
+
+namespace pa {
+
+__global__ void __launch_bounds__(128) reshape_and_cache_kernel(const CacheWriteParams p) {
+    const int i = blockIdx.x;
+    const int64_t slot = p.slot_mapping[i];
+    if (slot < 0) return;  // padding token (reading c11)
+    const int64_t b = slot >> p.log2B;
+    const int o = (int)(slot & ((1 << p.log2B) - 1));
+    const int cpr = p.row_bytes >> 4;  // 16-byte chunks per row
+    const int nvec = p.H_kv * cpr;
+    const uint4* ks = static_cast<const uint4*>(p.key) + (int64_t)i * nvec;
+    const uint4* vs = static_cast<const uint4*>(p.value) + (int64_t)i * nvec;
+    uint4* kc = static_cast<uint4*>(p.key_cache);
+    uint4* vc = static_cast<uint4*>(p.value_cache);
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+        const int h = v / cpr, cc = v - h * cpr;
+        const int64_t dst = ((((b * p.H_kv + h) << p.log2B) + o) * cpr) + cc;
+        const uint4 kv = __ldg(ks + v), vv = __ldg(vs + v);
+        kc[dst] = kv;
+        vc[dst] = vv;
+    }
+}
+
+__global__ void __launch_bounds__(256) copy_blocks_kernel(const __grid_constant__ CopyBlocksParams p) {
+    const int pair = blockIdx.x, layer = blockIdx.y, which = blockIdx.z;
+    const int64_t src = p.block_mapping[2 * pair], dst = p.block_mapping[2 * pair + 1];
+    char* base = static_cast<char*>(which == 0 ? p.key_caches[layer] : p.value_caches[layer]);
+    const uint4* s = reinterpret_cast<const uint4*>(base + src * p.block_bytes);
+    uint4* d = reinterpret_cast<uint4*>(base + dst * p.block_bytes);
+    const int n = (int)(p.block_bytes >> 4);
+    constexpr int U = 4;
+    int i = threadIdx.x;
+    for (; i + (U - 1) * 256 < n; i += U * 256) {
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) r[u] = s[i + u * 256];
+#pragma unroll
+        for (int u = 0; u < U; ++u) d[i + u * 256] = r[u];
+    }
+    for (; i < n; i += 256) d[i] = s[i];
+}
+
+__global__ void validate_tables_kernel(const int32_t* bt, const int32_t* ctx, int S, int W, int B, int NB,
+                                       unsigned long long* first_bad) {
+    const int64_t total = (int64_t)S * W;
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total; f += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(f / W), j = (int)(f % W);
+        const int n = ctx[s];
+        unsigned long long code = ~0ull;
+        if (j == 0 && (n < 0 || (int64_t)n > (int64_t)W * B)) {
+            code = (unsigned long long)(total + s);  // bad context length: coded past every entry
+        } else if ((int64_t)j * B < n) {
+            const int b = bt[f];
+            if (b < 0 || b >= NB) code = (unsigned long long)f;
+        }
+        if (code != ~0ull) atomicMin(first_bad, code);
+    }
+}
+
+cudaError_t launch_reshape_and_cache(const CacheWriteParams& p, cudaStream_t stream) {
+    reshape_and_cache_kernel<<<p.num_tokens, 128, 0, stream>>>(p);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_copy_blocks(const CopyBlocksParams& p, int num_layers, int num_pairs, cudaStream_t stream) {
+    copy_blocks_kernel<<<dim3(num_pairs, num_layers, 2), 256, 0, stream>>>(p);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_validate_tables(const int32_t* bt, const int32_t* ctx, int S, int W, int B, int NB,
+                                   unsigned long long* d_first_bad, cudaStream_t stream) {
+    validate_tables_kernel<<<148, 256, 0, stream>>>(bt, ctx, S, W, B, NB, d_first_bad);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace pa

@@ -1,0 +1,206 @@
+"""Torch-tensor front end of libpagedattn.so -- argument marshalling only.
+
+Same names as the C ABI (include/pa.h) without the ``pa_`` prefix.  Shapes are read
+from the tensors, pointers and the current CUDA stream are passed through; every
+computation happens in the library's sm_100a kernels.  P:N = PAPER.md line N.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import check
+
+_DT = {torch.float32: _lib.PA_F32, torch.float16: _lib.PA_F16, torch.bfloat16: _lib.PA_BF16}
+
+
+def _code(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {t.dtype}") from None
+
+
+def _dev(t: torch.Tensor, name: str) -> int:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def paged_attention_workspace_size(num_seqs: int, num_heads: int, head_dim: int, max_context_len: int,
+                                   partition_tokens: int = 0) -> int:
+    return int(_lib.raw().pa_paged_attention_workspace_size(num_seqs, num_heads, head_dim, max_context_len,
+                                                           partition_tokens))
+
+
+def paged_attention(out, query, key_cache, value_cache, block_tables, context_lens, scale: float,
+                    block_size: int | None = None, num_kv_heads: int | None = None, max_context_len: int = 0,
+                    partition_tokens: int = 0, workspace: torch.Tensor | None = None, stream=None):
+    """Eq.4 decode attention: out[s][h] = softmax(scale q.K^T) V over the
+    block-table-addressed cache.  out/query [S][H][D]; caches [NB][H_kv][B][D];
+    block_tables int32 [S][W]; context_lens int32 [S]."""
+    S, H, D = query.shape
+    _, hk, B, _ = key_cache.shape
+    block_size = B if block_size is None else block_size
+    num_kv_heads = hk if num_kv_heads is None else num_kv_heads
+    W = block_tables.shape[1]
+    mcl = max_context_len if max_context_len > 0 else W * block_size
+    need = paged_attention_workspace_size(S, H, D, mcl, partition_tokens)
+    if workspace is None and need > 0:
+        workspace = torch.empty(need, dtype=torch.uint8, device=query.device)
+    ws_ptr = _dev(workspace, "workspace") if workspace is not None else None
+    ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    check(_lib.raw().pa_paged_attention_ex(
+        _dev(out, "out"), _dev(query, "query"), _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"),
+        _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"), float(scale), int(block_size),
+        int(num_kv_heads), S, H, D, W, int(mcl), _code(query), int(partition_tokens), ws_ptr, ws_bytes,
+        _stream(stream)), "pa_paged_attention")
+    return out
+
+
+def reshape_and_cache(key, value, key_cache, value_cache, slot_mapping, stream=None):
+    """Fused reshape + block write: key/value [T][H_kv][D] into the caches at
+    slot_mapping (int64 [T], -1 = skip)."""
+    T, hk, D = key.shape
+    B = key_cache.shape[2]
+    check(_lib.raw().pa_reshape_and_cache(
+        _dev(key, "key"), _dev(value, "value"), _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"),
+        _dev(slot_mapping, "slot_mapping"), T, hk, D, B, _code(key), _stream(stream)), "pa_reshape_and_cache")
+
+
+def copy_blocks(key_caches, value_caches, block_mapping, stream=None):
+    """Fused copy-on-write block copy over every layer in one launch.
+    block_mapping: int64 [P][2] (src, dst) on the device."""
+    L = len(key_caches)
+    kp = (ctypes.c_void_p * L)(*[_dev(k, "key_caches[i]") for k in key_caches])
+    vp = (ctypes.c_void_p * L)(*[_dev(v, "value_caches[i]") for v in value_caches])
+    _, hk, B, D = key_caches[0].shape
+    P = block_mapping.shape[0] if block_mapping.numel() else 0
+    bm = _dev(block_mapping, "block_mapping") if P else None
+    check(_lib.raw().pa_copy_blocks(kp, vp, L, bm, P, hk, B, D, _code(key_caches[0]), _stream(stream)),
+          "pa_copy_blocks")
+
+
+def decode_step_staging_size(num_seqs, num_heads, num_kv_heads, head_dim, max_blocks_per_seq, num_pairs, dtype):
+    return int(_lib.raw().pa_decode_step_staging_size(num_seqs, num_heads, num_kv_heads, head_dim,
+                                                     max_blocks_per_seq, num_pairs, _DT[dtype]))
+
+
+def _host(t: torch.Tensor, name: str) -> int:
+    if t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous host tensor")
+    return t.data_ptr()
+
+
+def decode_step(host_out, host_query, host_key, host_value, host_slot_mapping, host_block_tables,
+                host_context_lens, host_block_mapping, key_cache, value_cache, scale: float, staging, workspace=None,
+                max_context_len: int = 0, stream=None):
+    """One decode step from HOST (pinned) inputs: H2D, copy_blocks, reshape_and_cache,
+    paged_attention, D2H of out -- all enqueued on one stream (pa_decode_step)."""
+    S, H, D = host_query.shape
+    _, hk, B, _ = key_cache.shape
+    W = host_block_tables.shape[1]
+    P = host_block_mapping.shape[0] if host_block_mapping is not None and host_block_mapping.numel() else 0
+    ws_ptr = _dev(workspace, "workspace") if workspace is not None else None
+    ws_bytes = workspace.numel() if workspace is not None else 0
+    check(_lib.raw().pa_decode_step(
+        _host(host_out, "host_out"), _host(host_query, "host_query"), _host(host_key, "host_key"),
+        _host(host_value, "host_value"), _host(host_slot_mapping, "host_slot_mapping"),
+        _host(host_block_tables, "host_block_tables"), _host(host_context_lens, "host_context_lens"),
+        _host(host_block_mapping, "host_block_mapping") if P else None, P,
+        _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"), float(scale), B, hk, S, H, D, W,
+        int(max_context_len), _code(host_query), _dev(staging, "staging"), staging.numel(), ws_ptr, ws_bytes,
+        _stream(stream)), "pa_decode_step")
+
+
+def debug_gather_kv(key_cache, value_cache, block_tables, context_lens, max_ctx: int, stream=None):
+    """Test-only: the logical K/V rows [S][H_kv][max_ctx][D] fetched by the attention
+    kernel's own tile loader (block-table lookup + bulk copy)."""
+    NB, hk, B, D = key_cache.shape
+    S, W = block_tables.shape
+    k_out = torch.zeros((S, hk, max_ctx, D), dtype=key_cache.dtype, device=key_cache.device)
+    v_out = torch.zeros_like(k_out)
+    check(_lib.raw().pa_debug_gather_kv(
+        _dev(k_out, "k_out"), _dev(v_out, "v_out"), _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"),
+        _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"), B, hk, S, D, W, max_ctx,
+        _code(key_cache), _stream(stream)), "pa_debug_gather_kv")
+    return k_out, v_out
+
+
+def validate_tables(block_tables, context_lens, block_size: int, num_blocks: int, stream=None) -> int:
+    S, W = block_tables.shape
+    bad = ctypes.c_int64(-2)
+    check(_lib.raw().pa_validate_tables(_dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"), S, W,
+                                        block_size, num_blocks, ctypes.byref(bad), _stream(stream)),
+          "pa_validate_tables")
+    return int(bad.value)
+
+
+class BlockAllocator:
+    """The paper's KV block manager in C++ (pa_alloc_*):
+    allocate / append_slot / fork / free on a FIFO free list of physical block ids."""
+
+    def __init__(self, num_blocks: int, block_size: int, initial_order=None):
+        self.num_blocks, self.block_size = num_blocks, block_size
+        arr = None
+        if initial_order is not None:
+            arr = (ctypes.c_int32 * num_blocks)(*[int(b) for b in initial_order])
+        self._h = _lib.raw().pa_alloc_create(num_blocks, block_size, arr)
+        if not self._h:
+            raise ValueError("pa_alloc_create failed (bad sizes or initial_order not a permutation)")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.raw().pa_alloc_destroy(h)
+            self._h = None
+
+    def allocate(self, num_tokens: int) -> int:
+        out = ctypes.c_int(-1)
+        check(_lib.raw().pa_alloc_allocate(self._h, num_tokens, ctypes.byref(out)), "pa_alloc_allocate")
+        return out.value
+
+    def append_slot(self, seq: int):
+        """Returns (slot, cow) with cow = (src, dst) or None."""
+        slot, src, dst = ctypes.c_int64(), ctypes.c_int(), ctypes.c_int()
+        check(_lib.raw().pa_alloc_append_slot(self._h, seq, ctypes.byref(slot), ctypes.byref(src), ctypes.byref(dst)),
+              "pa_alloc_append_slot")
+        return slot.value, ((src.value, dst.value) if src.value >= 0 else None)
+
+    def fork(self, parent: int) -> int:
+        out = ctypes.c_int(-1)
+        check(_lib.raw().pa_alloc_fork(self._h, parent, ctypes.byref(out)), "pa_alloc_fork")
+        return out.value
+
+    def free(self, seq: int) -> int:
+        out = ctypes.c_int(0)
+        check(_lib.raw().pa_alloc_free(self._h, seq, ctypes.byref(out)), "pa_alloc_free")
+        return out.value
+
+    def export(self, seqs, W: int):
+        import numpy as np
+        seqs = np.ascontiguousarray(seqs, dtype=np.int32)
+        bt = np.empty((len(seqs), W), dtype=np.int32)
+        cl = np.empty(len(seqs), dtype=np.int32)
+        check(_lib.raw().pa_alloc_export(self._h, seqs.ctypes.data, len(seqs), W, bt.ctypes.data, cl.ctypes.data),
+              "pa_alloc_export")
+        return bt, cl
+
+    def refcount(self, block: int) -> int:
+        return int(_lib.raw().pa_alloc_refcount(self._h, block))
+
+    def num_free(self) -> int:
+        return int(_lib.raw().pa_alloc_num_free(self._h))
+
+    def num_blocks_of(self, seq: int) -> int:
+        return int(_lib.raw().pa_alloc_num_blocks_of(self._h, seq))

@@ -1,0 +1,190 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/pa.h
+declares, rejects bad arguments on the host before any launch, and its host block
+allocator matches the reference block manager (oracle/block_manager.py) and the
+paper's worked examples (P:N = PAPER.md line N)."""
+import ctypes
+import os
+import random
+import re
+
+import numpy as np
+import pytest
+
+from oracle.block_manager import BlockManager, OutOfBlocks
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pa = pytest.importorskip("paper_2309_06180_b200")
+from paper_2309_06180_b200 import _lib  # noqa: E402
+
+L = _lib.raw()
+OK, INVALID, UNSUPPORTED, WORKSPACE, OOB = 0, 1, 2, 3, 5
+
+
+def header_functions():
+    txt = open(os.path.join(ROOT, "include", "pa.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(pa_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_every_declared_symbol_is_exported():
+    names = header_functions()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(L, n), f"{n} declared in pa.h but not exported"
+
+
+def test_library_is_sm100a_only():
+    """The shared library carries sm_100a SASS (no PTX JIT fallback for other archs)."""
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UBLKCP" in sass          # bulk async copies global -> shared
+    assert "FHFMA" in sass           # mixed-precision FMA for q.k
+    assert "FFMA2" in sass           # packed fp32x2 FMA for p*V
+
+
+FAKE = 0x100000  # aligned, never dereferenced: every call below fails validation first
+
+
+def attn(**kw):
+    a = dict(out=FAKE, q=FAKE, kc=FAKE, vc=FAKE, bt=FAKE, cl=FAKE, scale=0.125, B=16, hkv=2, S=4, H=2, D=64, W=8,
+             mcl=100, dt=0, pt=0, ws=None, wsb=0)
+    a.update(kw)
+    return L.pa_paged_attention_ex(a["out"], a["q"], a["kc"], a["vc"], a["bt"], a["cl"], a["scale"], a["B"], a["hkv"],
+                                   a["S"], a["H"], a["D"], a["W"], a["mcl"], a["dt"], a["pt"], a["ws"], a["wsb"], None)
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(D=96), UNSUPPORTED),
+    (dict(B=3), UNSUPPORTED),
+    (dict(B=512), UNSUPPORTED),
+    (dict(H=3, hkv=2), INVALID),
+    (dict(hkv=0), INVALID),
+    (dict(out=None), INVALID),
+    (dict(q=FAKE + 8), INVALID),
+    (dict(bt=FAKE + 2), INVALID),
+    (dict(dt=7), INVALID),
+    (dict(pt=24), INVALID),
+    (dict(scale=float("nan")), INVALID),
+    (dict(mcl=2048, W=128), WORKSPACE),
+    (dict(mcl=2048, W=128, ws=FAKE, wsb=16), WORKSPACE),
+])
+def test_attention_argument_validation(kw, status):
+    assert attn(**kw) == status
+    assert _lib.last_error() != ""
+
+
+def test_attention_zero_seqs_is_noop():
+    assert attn(S=0, out=None) == OK
+
+
+def test_workspace_size():
+    f = L.pa_paged_attention_workspace_size
+    assert f(4, 2, 64, 100, 0) == 0
+    assert f(4, 2, 64, 512, 0) == 0
+    S, H, D = 256, 40, 128
+    assert f(S, H, D, 2048, 0) == S * H * 4 * (D * 4 + 8)
+    assert f(S, H, D, 2048, 4096) == 0
+
+
+def test_cache_kernels_argument_validation():
+    r = L.pa_reshape_and_cache
+    assert r(FAKE, FAKE, FAKE, FAKE, FAKE, 4, 2, 96, 16, 1, None) == UNSUPPORTED
+    assert r(FAKE, FAKE, FAKE, FAKE, FAKE + 4, 4, 2, 64, 16, 1, None) == INVALID
+    assert r(None, FAKE, FAKE, FAKE, FAKE, 4, 2, 64, 16, 1, None) == INVALID
+    assert r(None, None, None, None, None, 0, 2, 64, 16, 1, None) == OK
+    c = L.pa_copy_blocks
+    arr = (ctypes.c_void_p * 1)(FAKE)
+    assert c(arr, arr, 0, FAKE, 1, 2, 16, 64, 1, None) == INVALID
+    assert c(arr, arr, 300, FAKE, 1, 2, 16, 64, 1, None) == INVALID
+    assert c(arr, arr, 1, None, 0, 2, 16, 64, 1, None) == OK
+    bad = (ctypes.c_void_p * 1)(FAKE + 8)
+    assert c(bad, arr, 1, FAKE, 1, 2, 16, 64, 1, None) == INVALID
+
+
+def test_decode_step_staging_validation():
+    need = L.pa_decode_step_staging_size(4, 2, 2, 64, 8, 0, 0)
+    assert need > 0
+    st = L.pa_decode_step
+    r = st(FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, None, 0, FAKE, FAKE, 0.1, 16, 2, 4, 2, 64, 8, 100, 0,
+           FAKE, need - 1, None, 0, None)
+    assert r == WORKSPACE
+
+
+# ------------------------------------------------------------- host block allocator ----
+
+def test_allocator_fig6_and_cow():
+    """Fig.6 and the parallel-sampling copy-on-write."""
+    a = pa.BlockAllocator(8, 4, [7, 1, 3, 0, 2, 4, 5, 6])
+    h = a.allocate(7)
+    bt, cl = a.export([h], 3)
+    assert bt.tolist() == [[7, 1, -1]] and cl.tolist() == [7]
+    c = a.fork(h)
+    assert a.refcount(7) == 2 and a.refcount(1) == 2
+    slot, cow = a.append_slot(h)
+    assert cow == (1, 3) and slot == 3 * 4 + 3
+    assert a.refcount(1) == 1
+    assert a.append_slot(c) == (1 * 4 + 3, None)
+    assert a.free(c) == 1 and a.free(h) == 2
+    with pytest.raises(pa.PagedAttnError):
+        a.free(h)
+    with pytest.raises(ValueError):
+        pa.BlockAllocator(4, 4, [0, 0, 1, 2])
+
+
+def test_allocator_out_of_blocks():
+    a = pa.BlockAllocator(2, 4)
+    h = a.allocate(8)
+    with pytest.raises(pa.PagedAttnError) as e:
+        a.append_slot(h)
+    assert e.value.status == OOB
+
+
+def test_allocator_matches_reference_fuzz():
+    """Same random op sequence on the C++ allocator and the reference block manager:
+    identical handles, slots, copy-on-write pairs, refcounts and tables."""
+    rs = random.Random(5)
+    order = rs.sample(range(96), 96)
+    a = pa.BlockAllocator(96, 4, order)
+    m = BlockManager(96, 4, initial_order=order)
+    live = []
+    for step in range(6000):
+        op = rs.random()
+        if op < 0.15 or not live:
+            n = rs.randint(1, 14)
+            try:
+                hm = m.allocate(n)
+            except OutOfBlocks:
+                with pytest.raises(pa.PagedAttnError):
+                    a.allocate(n)
+                h = live.pop(rs.randrange(len(live))) if live else None
+                if h is not None:
+                    assert a.free(h) == m.free(h)
+                continue
+            assert a.allocate(n) == hm
+            live.append(hm)
+        elif op < 0.7:
+            h = rs.choice(live)
+            try:
+                kind, slot, cow = m.append_slot(h)
+            except OutOfBlocks:
+                with pytest.raises(pa.PagedAttnError):
+                    a.append_slot(h)
+                continue
+            assert a.append_slot(h) == (slot, cow)
+        elif op < 0.85:
+            p = rs.choice(live)
+            c = m.fork(p)
+            assert a.fork(p) == c
+            live.append(c)
+        else:
+            h = live.pop(rs.randrange(len(live)))
+            assert a.free(h) == m.free(h)
+        if step % 100 == 0:
+            assert [a.refcount(b) for b in range(96)] == m.ref
+            assert a.num_free() == m.num_free()
+            if live:
+                bt, cl = a.export(live, 64)
+                rows, lens = m.export(live, 64)
+                assert bt.tolist() == rows and cl.tolist() == lens

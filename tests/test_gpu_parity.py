@@ -1,0 +1,324 @@
+"""GPU parity: the CUDA path (libpagedattn.so through its C ABI) against the fp64 oracle
+on identical generated inputs, plus the invariants BJ:north_star names.
+
+Bars: cache writes, copy_blocks and block-table indexing bit-exact; attention max-abs
+<= 1e-5 (fp32), 2e-3 (fp16), 1e-2 (bf16).  P:N = PAPER.md line N.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import make_config, materialize_numpy, materialize_torch, shard, subset, tables_torch
+from synth import rng as R
+from synth.workload import place_private
+from tests.pathutil import TOL, as_f64, bits, gpu_step, max_abs, oracle_step
+
+pytestmark = pytest.mark.gpu
+pa = pytest.importorskip("paper_2309_06180_b200")
+
+SMALL = {
+    "c1_tiny": {},
+    "c2_sharegpt": dict(S=24, H=4, H_kv=4),
+    "c2_alpaca": dict(S=40, H=4, H_kv=4),
+    "c3_parallel": dict(S=24, H=2, H_kv=2),
+    "c3_fork": dict(S=24, H=2, H_kv=2),
+    "c4_sharegpt": dict(S=16, H=3, H_kv=3),
+    "c4_long": dict(S=8, H=2, H_kv=2),
+    "c5_beam": dict(S=16, H=2, H_kv=2),
+}
+
+
+def test_device_inputs_equal_oracle_inputs():
+    wl = make_config("c3_fork", S=12, H=2, H_kv=2)
+    n = materialize_numpy(wl)
+    t = materialize_torch(wl, "cuda")
+    for k in n:
+        assert np.array_equal(n[k], bits(t[k])), k
+
+
+@pytest.mark.parametrize("name", list(SMALL))
+def test_step_parity_small(name):
+    """copy_blocks + reshape_and_cache bitwise over the WHOLE cache (untouched slots
+    included); attention within tolerance; no NaN from poisoned slots."""
+    wl = make_config(name, **SMALL[name])
+    out, kc, vc, _ = gpu_step(wl)
+    ref, rkc, rvc = oracle_step(wl)
+    assert np.array_equal(bits(kc), rkc) and np.array_equal(bits(vc), rvc)
+    err = max_abs(out, ref)
+    assert err <= TOL[wl.dtype], f"{name}: max-abs {err}"
+
+
+@pytest.mark.parametrize("pt", [16, 32, 128, 512, 4096])
+def test_partition_sizes(pt):
+    wl = make_config("c2_sharegpt", S=24, H=4, H_kv=4)
+    out, *_ = gpu_step(wl, partition_tokens=pt)
+    ref, *_ = oracle_step(wl)
+    assert max_abs(out, ref) <= TOL[wl.dtype]
+
+
+def test_split_vs_single_pass():
+    """Sequences with one partition are bitwise identical under any partition size;
+    split ones agree within tolerance with the single-pass kernel."""
+    wl = make_config("c2_sharegpt", S=32, H=4, H_kv=4)
+    x = materialize_torch(wl, "cuda")
+    a, *_ = gpu_step(wl, partition_tokens=512, inputs={k: v.clone() for k, v in x.items()})
+    b, *_ = gpu_step(wl, partition_tokens=4096, inputs={k: v.clone() for k, v in x.items()})
+    short = wl.context_lens <= 512
+    assert short.any() and (~short).any()
+    assert torch.equal(a[torch.as_tensor(short)], b[torch.as_tensor(short)])
+    assert float((a.double() - b.double()).abs().max()) <= TOL[wl.dtype]
+
+
+def test_determinism_bitwise():
+    wl = make_config("c4_long", S=8, H=4, H_kv=4)
+    x = materialize_torch(wl, "cuda")
+    a, *_ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()})
+    b, *_ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()})
+    assert torch.equal(a, b)
+
+
+# ------------------------------------------------ logical caches: B and placement ----
+
+def logical_problem(ctx, B, place_seed, H, H_kv, D, dtype, seed=77):
+    """The same LOGICAL q, K, V (drawn per (seq, head, token, dim)) placed into a
+    [NB][H_kv][B][D] cache with block size B on shuffled blocks (test-side placement)."""
+    ctx = np.asarray(ctx, np.int64)
+    bt, NB, _, _ = place_private(ctx, B, place_seed, pool_factor=2.0, min_extra=3)
+    S, T = len(ctx), int(max(1, ctx.max()))
+    dev = "cuda"
+    s = torch.arange(S, device=dev).view(S, 1, 1, 1)
+    h = torch.arange(H_kv, device=dev).view(1, H_kv, 1, 1)
+    t = torch.arange(T, device=dev).view(1, 1, T, 1)
+    d = torch.arange(D, device=dev).view(1, 1, 1, D)
+    idx = ((s * H_kv + h) * T + t) * D + d
+    K = R.f32_to_dtype_t(R.uniform_f32_t(R.key(seed, R.STREAM_KCACHE), idx), dtype)
+    V = R.f32_to_dtype_t(R.uniform_f32_t(R.key(seed, R.STREAM_VCACHE), idx), dtype)
+    qi = (torch.arange(S, device=dev).view(S, 1, 1) * H + torch.arange(H, device=dev).view(1, H, 1)) * D + \
+        torch.arange(D, device=dev).view(1, 1, D)
+    q = R.f32_to_dtype_t(R.uniform_f32_t(R.key(seed, R.STREAM_Q), qi), dtype).contiguous()
+    kc = torch.full((NB, H_kv, B, D), float("nan"), dtype=K.dtype, device=dev)
+    vc = torch.full_like(kc, float("nan"))
+    btt = torch.as_tensor(bt, device=dev)
+    for si in range(S):
+        n = int(ctx[si])
+        if n == 0:
+            continue
+        tt = torch.arange(n, device=dev)
+        blocks = btt[si, tt // B].long()
+        kc[blocks, :, tt % B, :] = K[si, :, :n, :].permute(1, 0, 2)
+        vc[blocks, :, tt % B, :] = V[si, :, :n, :].permute(1, 0, 2)
+    cl = torch.as_tensor(ctx.astype(np.int32), device=dev)
+    return q, kc, vc, btt, cl
+
+
+def attend(q, kc, vc, bt, cl, scale, pt=0):
+    out = torch.empty_like(q)
+    pa.paged_attention(out, q, kc, vc, bt, cl, scale, max_context_len=int(cl.max()), partition_tokens=pt)
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("dtype,D", [("f16", 128), ("bf16", 128), ("f32", 64), ("f16", 64), ("bf16", 64),
+                                     ("f32", 128)])
+def test_block_size_and_permutation_invariance_bitwise(dtype, D):
+    """Same logical K/V, B in {1,2,4,8,16,32,64} and two physical placements: bitwise
+    identical outputs (the kernel computes on 16-token logical tiles), and within
+    tolerance of the oracle."""
+    ctx = [1, 2, 15, 16, 17, 33, 100, 511, 512, 513, 700, 1100]
+    H = H_kv = 2
+    scale = 1.0 / np.sqrt(D)
+    outs = []
+    for B in (1, 2, 4, 8, 16, 32, 64):
+        for ps in (11, 12):
+            q, kc, vc, bt, cl = logical_problem(ctx, B, ps, H, H_kv, D, dtype)
+            outs.append(attend(q, kc, vc, bt, cl, scale))
+            if B in (1, 16) and ps == 11:
+                ref = oracle.paged_attention(bits(q), bits(kc), bits(vc), bt.cpu().numpy(), cl.cpu().numpy(), scale,
+                                             B, H_kv, dtype)
+                assert max_abs(outs[-1], ref) <= TOL[dtype]
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
+def test_context_edge_cases():
+    """ctx = 0 -> zeros; ctx = 1 -> the (just written) V row bit for bit; tile and
+    partition boundaries within tolerance."""
+    ctx = [0, 1, 2, 15, 16, 17, 31, 32, 33, 511, 512, 513, 1023, 1024, 1025, 2047, 2048]
+    wl = make_config("explicit", ctx=ctx, H=4, H_kv=4, D=128, B=16, dtype="f16", seed=5)
+    out, kc, vc, x = gpu_step(wl)
+    ref, *_ = oracle_step(wl)
+    assert max_abs(out, ref) <= TOL["f16"]
+    assert torch.equal(out[0], torch.zeros_like(out[0]))
+    assert torch.equal(out[1], x["value"][1])
+
+
+def test_gqa():
+    wl = make_config("c1_tiny", H=4, H_kv=2)
+    out, *_ = gpu_step(wl)
+    ref, *_ = oracle_step(wl)
+    assert max_abs(out, ref) <= TOL["f32"]
+    wl = make_config("c2_sharegpt", S=8, H=8, H_kv=2)
+    out, *_ = gpu_step(wl)
+    ref, *_ = oracle_step(wl)
+    assert max_abs(out, ref) <= TOL["f16"]
+
+
+def test_peaked_softmax_and_large_scores():
+    """q x 8 (peaked softmax) within tolerance; scores spanning +-700 stay finite
+    and within the bound derived in DESIGN.md (fp32 score rounding x max|v|)."""
+    wl = make_config("c1_tiny", scale=8.0 / 8.0)
+    out, *_ = gpu_step(wl)
+    ref, *_ = oracle_step(wl)
+    assert max_abs(out, ref) <= TOL["f32"]
+    wl = make_config("c1_tiny", scale=60.0)
+    out, *_ = gpu_step(wl)
+    ref, *_ = oracle_step(wl)
+    g = as_f64(out)
+    assert np.isfinite(g).all()
+    assert np.max(np.abs(g - ref)) <= 5e-2
+
+
+# ------------------------------------------------------------ cache kernels ---------
+
+def test_reshape_and_cache_prefill_shaped():
+    """A multi-token slot_mapping (all prompt tokens of several sequences, as in the
+    prompt phase) plus padding slots (-1): bitwise vs the oracle."""
+    alloc = pa.BlockAllocator(64, 16, list(np.random.default_rng(3).permutation(64)))
+    prompts = [7, 40, 16, 1, 33]
+    slots = []
+    for n in prompts:
+        h = alloc.allocate(n)
+        bt, _ = alloc.export([h], 8)
+        slots += [int(bt[0, t // 16]) * 16 + t % 16 for t in range(n)]
+    slots = np.array(slots[:30] + [-1] + slots[30:] + [-1], np.int64)
+    T, H_kv, D = len(slots), 4, 64
+    for dtype in ("f16", "bf16", "f32"):
+        r = np.random.default_rng(4)
+        npdt = np.uint32 if dtype == "f32" else np.uint16
+        hi = 1 << (32 if dtype == "f32" else 16)
+        key = r.integers(0, hi, (T, H_kv, D), dtype=np.uint64).astype(npdt)
+        val = r.integers(0, hi, (T, H_kv, D), dtype=np.uint64).astype(npdt)
+        kc0 = r.integers(0, hi, (64, H_kv, 16, D), dtype=np.uint64).astype(npdt)
+        vc0 = r.integers(0, hi, (64, H_kv, 16, D), dtype=np.uint64).astype(npdt)
+        ek, ev = oracle.reshape_and_cache(key, val, kc0, vc0, slots, 16, dtype)
+        tdt = {"f32": torch.int32, "f16": torch.int16, "bf16": torch.int16}[dtype]
+        view = R.torch_dtype(dtype)
+
+        def dev(a):
+            return torch.from_numpy(a.view(np.int32 if dtype == "f32" else np.int16)).to(tdt).cuda().view(view)
+        kc, vc = dev(kc0), dev(vc0)
+        pa.reshape_and_cache(dev(key), dev(val), kc, vc, torch.from_numpy(slots).cuda())
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(kc), ek) and np.array_equal(bits(vc), ev), dtype
+
+
+def test_copy_blocks_multilayer_bitwise():
+    wl = make_config("c3_fork", S=30, H=2, H_kv=2)
+    layers = [materialize_torch(wl, "cuda", layer=l) for l in range(3)]
+    nl = [materialize_numpy(wl, layer=l) for l in range(3)]
+    kcs = [x["key_cache"] for x in layers]
+    vcs = [x["value_cache"] for x in layers]
+    pa.copy_blocks(kcs, vcs, tables_torch(wl, "cuda")["block_mapping"])
+    torch.cuda.synchronize()
+    ek, ev = oracle.copy_blocks([n["key_cache"] for n in nl], [n["value_cache"] for n in nl], wl.block_mapping,
+                                wl.dtype)
+    for l in range(3):
+        assert np.array_equal(bits(kcs[l]), ek[l]) and np.array_equal(bits(vcs[l]), ev[l])
+
+
+@pytest.mark.parametrize("B", [1, 8, 16, 32])
+def test_block_table_indexing_bitwise(B):
+    """The attention kernel's own tile loader (block-table lookup + bulk copy) fetches
+    exactly the oracle's logical rows (Fig.6)."""
+    wl = make_config("c2_sharegpt", S=10, H=3, H_kv=3, B=B)
+    x = materialize_torch(wl, "cuda")
+    tb = tables_torch(wl, "cuda")
+    mc = wl.max_context_len
+    ko, vo = pa.debug_gather_kv(x["key_cache"], x["value_cache"], tb["block_tables"], tb["context_lens"], mc)
+    n = materialize_numpy(wl)
+    kb, vb = bits(ko), bits(vo)
+    for s in range(wl.S):
+        c = int(wl.context_lens[s])
+        for h in range(wl.H_kv):
+            rk, rv = oracle.gather_kv_bits(n["key_cache"], n["value_cache"], wl.block_tables[s], c, h, B, wl.dtype)
+            assert np.array_equal(kb[s, h, :c], rk) and np.array_equal(vb[s, h, :c], rv)
+
+
+def test_validate_tables():
+    wl = make_config("c2_alpaca", S=16, H=2, H_kv=2)
+    tb = tables_torch(wl, "cuda")
+    assert pa.validate_tables(tb["block_tables"], tb["context_lens"], wl.B, wl.num_blocks) == -1
+    bt = tb["block_tables"].clone()
+    bt[3, 0] = wl.num_blocks
+    assert pa.validate_tables(bt, tb["context_lens"], wl.B, wl.num_blocks) == 3 * wl.W
+    cl = tb["context_lens"].clone()
+    cl[5] = wl.W * wl.B + 1
+    assert pa.validate_tables(tb["block_tables"], cl, wl.B, wl.num_blocks) == -6
+
+
+def test_decode_step_host_api_matches_device_api():
+    wl = make_config("c3_fork", S=24, H=2, H_kv=2)
+    x = materialize_torch(wl, "cuda")
+    ref, *_ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()})
+    kc, vc = x["key_cache"].clone(), x["value_cache"].clone()
+    pin = {k: x[k].cpu().pin_memory() for k in ("query", "key", "value")}
+    host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in
+            dict(slot=wl.slot_mapping, bt=wl.block_tables, cl=wl.context_lens, bm=wl.block_mapping).items()}
+    out = torch.empty(pin["query"].shape, dtype=pin["query"].dtype).pin_memory()
+    st = torch.empty(pa.decode_step_staging_size(wl.S, wl.H, wl.H_kv, wl.D, wl.W, len(wl.block_mapping),
+                                                 pin["query"].dtype), dtype=torch.uint8, device="cuda")
+    ws_n = pa.paged_attention_workspace_size(wl.S, wl.H, wl.D, wl.max_context_len)
+    ws = torch.empty(max(ws_n, 16), dtype=torch.uint8, device="cuda")
+    pa.decode_step(out, pin["query"], pin["key"], pin["value"], host["slot"], host["bt"], host["cl"], host["bm"],
+                   kc, vc, wl.scale, st, ws, max_context_len=wl.max_context_len)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref.cpu())
+
+
+def test_cow_parent_unchanged():
+    """Copy-on-write: the sample that keeps the shared block (writes in place)
+    gets bitwise the same output whether or not its siblings copied and wrote."""
+    wl = make_config("c3_fork", S=36, H=2, H_kv=2)
+    full, *_ = gpu_step(wl)
+    n = wl.meta["n"]
+    keepers = [r * n + n - 1 for r in range(wl.S // n)]
+    sub = subset(wl, keepers)
+    alone, *_ = gpu_step(sub)
+    assert torch.equal(full[keepers], alone)
+
+
+def test_launch_counter():
+    pa.take_launch_count()
+    wl = make_config("c3_fork", S=12, H=2, H_kv=2)
+    gpu_step(wl)
+    assert pa.take_launch_count() >= 3
+
+
+# ------------------------------------------------------------ full-size sampled -----
+
+FULL = ["c2_sharegpt", "c2_alpaca", "c3_parallel", "c3_fork", "c4_long", "c5_beam"]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_size_sampled_parity(name):
+    """BASELINE.json sizes in bench.py's launch configuration (default partitioning):
+    sampled sequences x a head slice against the oracle; whole output NaN-free; the new
+    token's K/V landed bit for bit."""
+    wl = make_config(name)
+    out, kc, vc, x = gpu_step(wl)
+    assert not torch.isnan(out).any()
+    rs = np.random.default_rng(len(name))
+    seqs = sorted(set([int(np.argmax(wl.context_lens)), int(np.argmin(wl.context_lens))] +
+                      rs.choice(wl.S, 4, replace=False).tolist()))
+    world = wl.H // 4 if wl.H % 4 == 0 else 1
+    rank = int(rs.integers(world))
+    sub = shard(subset(wl, seqs), rank, world)
+    ref, *_ = oracle_step(sub)
+    h0 = sub.q_head0
+    got = out[seqs][:, h0:h0 + sub.H]
+    assert max_abs(got, ref) <= TOL[wl.dtype]
+    slots = torch.as_tensor(wl.slot_mapping, device="cuda")
+    B = wl.B
+    assert torch.equal(kc[slots // B, :, slots % B, :], x["key"]) and torch.equal(vc[slots // B, :, slots % B, :],
+                                                                                   x["value"])
