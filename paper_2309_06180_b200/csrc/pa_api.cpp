@@ -367,13 +367,13 @@ pa_status_t pa_validate_tables(const int32_t* block_tables, const int32_t* conte
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     cudaFreeAsync(d, s);
     if (e != cudaSuccess) return cuda_fail(e, "pa_validate_tables");
-    const unsigned long long total = (unsigned long long)num_seqs * max_blocks_per_seq;
-    if (h == ~0ull)
+    if (h == ~0ull) {
         *first_bad_out = -1;
-    else if (h >= total)
-        *first_bad_out = -(int64_t)(h - total) - 1;
-    else
-        *first_bad_out = (int64_t)h;
+    } else {
+        const int64_t row = (int64_t)(h / (unsigned long long)(max_blocks_per_seq + 1));
+        const int64_t pos = (int64_t)(h % (unsigned long long)(max_blocks_per_seq + 1));
+        *first_bad_out = pos == 0 ? -(row + 1) : row * max_blocks_per_seq + pos - 1;
+    }
     return PA_OK;
 }
 

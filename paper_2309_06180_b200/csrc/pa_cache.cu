@@ -51,18 +51,21 @@ __global__ void __launch_bounds__(256) copy_blocks_kernel(const __grid_constant_
     for (; i < n; i += 256) d[i] = s[i];
 }
 
+// Codes are row-major over (row s, position 0 = ctx, 1 + j = entry j) so atomicMin
+// yields the first problem in row order; entries of a row with a bad ctx are skipped.
 __global__ void validate_tables_kernel(const int32_t* bt, const int32_t* ctx, int S, int W, int B, int NB,
                                        unsigned long long* first_bad) {
     const int64_t total = (int64_t)S * W;
     for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total; f += (int64_t)gridDim.x * blockDim.x) {
         const int s = (int)(f / W), j = (int)(f % W);
         const int n = ctx[s];
+        const bool bad_ctx = n < 0 || (int64_t)n > (int64_t)W * B;
         unsigned long long code = ~0ull;
-        if (j == 0 && (n < 0 || (int64_t)n > (int64_t)W * B)) {
-            code = (unsigned long long)(total + s);  // bad context length: coded past every entry
+        if (bad_ctx) {
+            if (j == 0) code = (unsigned long long)s * (W + 1);
         } else if ((int64_t)j * B < n) {
             const int b = bt[f];
-            if (b < 0 || b >= NB) code = (unsigned long long)f;
+            if (b < 0 || b >= NB) code = (unsigned long long)s * (W + 1) + 1 + j;
         }
         if (code != ~0ull) atomicMin(first_bad, code);
     }
