@@ -2,8 +2,10 @@
 """bench.py -- paged decode-attention step on B200: achieved HBM GB/s, us/step.
 
 One step = copy_blocks (when the step has copy-on-write pairs) +
-reshape_and_cache + paged_attention (+ its split-context reduce) for ONE attention
-layer over the whole batch, all on one stream; at N > 1 GPUs heads are sharded
+reshape_and_cache + paged_attention (with its split-context merge) for ONE attention
+layer over the whole batch, all on one stream; by default the cache write is fused
+into the attention kernel (pa_paged_attention_decode; --unfused runs the separate
+reshape_and_cache launch); at N > 1 GPUs heads are sharded
 tensor-parallel style and the per-rank output head slices are all-gathered
 with NCCL (+ permute to [S][H][D]).
 
@@ -113,6 +115,7 @@ def parse():
     ap.add_argument("--partition-tokens", type=int, default=0)
     ap.add_argument("--block-size", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--unfused", action="store_true", help="separate reshape_and_cache launch (ablation)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also print per-config lines for the other configs")
     return ap.parse_args()
@@ -197,7 +200,7 @@ def run_ours(a, wl_full, world, rank, local):
     out = torch.empty_like(q)
     mcl = wl.max_context_len
     ws_n = pa.paged_attention_workspace_size(wl.S, wl.H, wl.D, mcl, a.partition_tokens)
-    ws = torch.empty(max(ws_n, 16), dtype=torch.uint8, device=dev)
+    ws = torch.zeros(max(ws_n, 16), dtype=torch.uint8, device=dev)
     gathered = torch.empty((world, wl.S, wl.H, wl.D), dtype=q.dtype, device=dev) if world > 1 else None
     full_out = torch.empty((wl.S, wl.H * world, wl.D), dtype=q.dtype, device=dev) if world > 1 else None
     has_pairs = len(wl.block_mapping) > 0
@@ -208,11 +211,15 @@ def run_ours(a, wl_full, world, rank, local):
     def step(i=None):
         if has_pairs:
             pa.copy_blocks([kc], [vc], bm)
-        pa.reshape_and_cache(kn, vn, kc, vc, sm)
+        if a.unfused:
+            pa.reshape_and_cache(kn, vn, kc, vc, sm)
         if i is not None:
             ev_a0[i].record(stream)
-        pa.paged_attention(out, q, kc, vc, bt, cl, wl.scale, max_context_len=mcl,
-                           partition_tokens=a.partition_tokens, workspace=ws)
+        if a.unfused:
+            pa.paged_attention(out, q, kc, vc, bt, cl, wl.scale, max_context_len=mcl,
+                               partition_tokens=a.partition_tokens, workspace=ws)
+        else:  # the decode step's cache write fused into the attention kernel
+            pa.paged_attention_decode(out, q, kn, vn, kc, vc, bt, cl, wl.scale, max_context_len=mcl, workspace=ws)
         if i is not None:
             ev_a1[i].record(stream)
         if world > 1:
@@ -255,7 +262,8 @@ def run_ours(a, wl_full, world, rank, local):
     peak, peak_src = load_peaks()
     kv_all = wl_full.logical_kv_bytes()
     sb = wl.step_bytes()
-    attn_bytes = sb["kv_logical"] + sb["q_out"] + sb["tables"]   # per launch of pa_paged_attention, this rank
+    # per launch of the attention call on this rank: K/V read + q/out + tables (+ the fused new-token write)
+    attn_bytes = sb["kv_logical"] + sb["q_out"] + sb["tables"] + (0 if a.unfused else sb["cache_write"] // 2)
     achieved = attn_bytes / (attn_ms * 1e-3) / 1e9
     value = kv_all / (ms_step * 1e-3) / 1e9
     traffic = load_traffic(wl_full.name, world)
@@ -273,7 +281,9 @@ def run_ours(a, wl_full, world, rank, local):
         "tokens_per_s": wl_full.S / (ms_step * 1e-3),
         "kv_tokens_per_s": float(wl_full.context_lens.sum()) / (ms_step * 1e-3),
         "frac_of_peak": value / peak,
-        "roofline": {"bound": "hbm", "kernel": "pa_paged_attention (paged_attention_kernel + reduce)",
+        "roofline": {"bound": "hbm", "kernel": "paged_attention_kernel (pa_paged_attention_decode: cache write + "
+                                                "attention + split-context merge in one launch)"
+                     if not a.unfused else "paged_attention_kernel (pa_paged_attention)",
                      "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes_per_launch": attn_bytes,
                      "avg_launch_ms": attn_ms},

@@ -64,12 +64,16 @@ typedef enum {
  *
  * Contexts longer than PA_DEFAULT_PARTITION_TOKENS use the split-context variant
  * (BJ:north_star): partitions of that many logical tokens each produce (m, L, o~)
- * into `workspace`, then a log-sum-exp reduce kernel merges them.  The partition
- * size depends on nothing but the context length, so results are bitwise identical
- * for any batch composition, block size, physical placement or head sharding.
- * max_context_len: host upper bound of context_lens (<= 0 -> W * block_size); it
- * only sizes the grid.  workspace: device, >= pa_paged_attention_workspace_size(),
- * 16-byte aligned; may be NULL when that size is 0.
+ * into `workspace`; the last partition of each (sequence, head group) to finish
+ * merges them by log-sum-exp in partition order (one kernel launch per call).  The
+ * partition size depends on nothing but the context length, so results are bitwise
+ * identical for any batch composition, block size, physical placement or head
+ * sharding.  max_context_len: host upper bound of context_lens (<= 0 -> W *
+ * block_size); it only sizes the grid.  workspace: device, >=
+ * pa_paged_attention_workspace_size(), 16-byte aligned, any content (its completion
+ * counters are zeroed on the stream by the call; do not share one workspace between
+ * calls running concurrently on different streams);
+ * may be NULL when that size is 0.
  * ---------------------------------------------------------------------------------- */
 pa_status_t pa_paged_attention(void* out, const void* query, const void* key_cache,
                                const void* value_cache, const int32_t* block_tables,
@@ -88,6 +92,24 @@ pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_
                                   int max_blocks_per_seq, int max_context_len, pa_dtype_t dtype,
                                   int partition_tokens, void* workspace, size_t workspace_bytes,
                                   pa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * pa_paged_attention_decode -- the decode step's cache write fused into the attention
+ * kernel ("saves the newly generated KV cache" and attends in one pass).
+ * key, value: [num_seqs][num_kv_heads][head_dim], the new token of every sequence,
+ * whose logical position is context_lens[s] - 1 (so its slot is
+ * block_tables[s][(ctx-1)/B]*B + (ctx-1)%B).  Equivalent to pa_reshape_and_cache with
+ * that slot_mapping followed by pa_paged_attention, bit for bit: the cache receives the
+ * same bytes and the output is identical.  Sequences with ctx == 0 write nothing and
+ * output 0.  Default partitioning; workspace as for pa_paged_attention.
+ * ---------------------------------------------------------------------------------- */
+pa_status_t pa_paged_attention_decode(void* out, const void* query, const void* key,
+                                      const void* value, void* key_cache, void* value_cache,
+                                      const int32_t* block_tables, const int32_t* context_lens,
+                                      float scale, int block_size, int num_kv_heads, int num_seqs,
+                                      int num_heads, int head_dim, int max_blocks_per_seq,
+                                      int max_context_len, pa_dtype_t dtype, void* workspace,
+                                      size_t workspace_bytes, pa_stream_t stream);
 
 /* Bytes of workspace pa_paged_attention(_ex) needs (0 if no context is split).
  * partition_tokens as in pa_paged_attention_ex. */
@@ -124,10 +146,11 @@ pa_status_t pa_copy_blocks(void* const* key_caches, void* const* value_caches, i
 /* ------------------------------------------------------------------------------------
  * pa_decode_step -- one decode step of one attention layer from HOST inputs: the
  * end-to-end call of bench.py's "e2e" number.  Stream-ordered:
- *   H2D  query/key/value/slot_mapping/block_tables/context_lens/block_mapping
+ *   H2D  query/key/value/block_tables/context_lens/block_mapping
  *        (HOST, ideally pinned) into the device staging buffer `staging`
  *   pa_copy_blocks (if num_pairs > 0) on (key_cache, value_cache)
- *   pa_reshape_and_cache, pa_paged_attention (default partitioning)
+ *   pa_paged_attention_decode (cache write + attention).  host_slot_mapping may be
+ *   NULL and is not read: a decode token's slot follows from its block table row.
  *   D2H  out -> host_out (HOST)
  * key_cache/value_cache/workspace/staging: DEVICE.  staging must hold
  * pa_decode_step_staging_size() bytes.  The call returns after enqueueing; the

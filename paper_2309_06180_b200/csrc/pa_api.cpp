@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -66,14 +67,18 @@ size_t workspace_bytes_for(int64_t S, int64_t H, int64_t D, int max_ctx, int PT)
     if (S <= 0 || H <= 0 || D <= 0 || max_ctx <= 0 || PT <= 0) return 0;
     const int64_t NP = (max_ctx + PT - 1) / PT;
     if (NP <= 1) return 0;
-    // part_o [S][H][NP][D] fp32, then part_ml [S][H][NP] float2
-    return (size_t)(S * H * NP * D * 4 + S * H * NP * 8);
+    // counters [S][H] int32 (16-byte padded), part_o [S][H][NP][D] fp32, part_ml [S][H][NP] float2
+    return (size_t)(((S * H * 4 + 15) / 16) * 16 + S * H * NP * D * 4 + S * H * NP * 8);
 }
 
 }  // namespace
 
 namespace pa {
 void count_launch() { ++g_launches; }
+bool pdl_enabled() {
+    const char* e = getenv("PA_PDL");
+    return !(e && e[0] == '0');
+}
 }  // namespace pa
 
 extern "C" {
@@ -91,13 +96,17 @@ size_t pa_paged_attention_workspace_size(int num_seqs, int num_heads, int head_d
     return workspace_bytes_for(num_seqs, num_heads, head_dim, max_context_len, effective_partition(partition_tokens));
 }
 
-pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_cache, const void* value_cache,
-                                  const int32_t* block_tables, const int32_t* context_lens, float scale,
-                                  int block_size, int num_kv_heads, int num_seqs, int num_heads, int head_dim,
-                                  int max_blocks_per_seq, int max_context_len, pa_dtype_t dtype,
-                                  int partition_tokens, void* workspace, size_t workspace_bytes,
-                                  pa_stream_t stream) {
-    g_err.clear();
+}  // extern "C"
+
+namespace {
+// Shared body of pa_paged_attention(_ex) and pa_paged_attention_decode (new_key != NULL:
+// the decode step's token s is written at logical position ctx[s]-1 by the kernel).
+pa_status_t attention_impl(void* out, const void* query, const void* new_key, const void* new_value,
+                           const void* key_cache, const void* value_cache, const int32_t* block_tables,
+                           const int32_t* context_lens, float scale, int block_size, int num_kv_heads, int num_seqs,
+                           int num_heads, int head_dim, int max_blocks_per_seq, int max_context_len,
+                           pa_dtype_t dtype, int partition_tokens, void* workspace, size_t workspace_bytes,
+                           pa_stream_t stream) {
     REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
     REQUIRE(num_seqs >= 0, "num_seqs must be >= 0 (got %d)", num_seqs);
     REQUIRE(num_heads > 0 && num_kv_heads > 0, "num_heads and num_kv_heads must be positive");
@@ -119,6 +128,10 @@ pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_
     REQUIRE_PTR(value_cache, 16);
     REQUIRE_PTR(block_tables, 4);
     REQUIRE_PTR(context_lens, 4);
+    if (new_key != nullptr || new_value != nullptr) {
+        REQUIRE_PTR(new_key, 16);
+        REQUIRE_PTR(new_value, 16);
+    }
     const int64_t cap = (int64_t)max_blocks_per_seq * block_size;
     int64_t mcl = max_context_len > 0 ? max_context_len : cap;
     if (mcl > cap) mcl = cap;
@@ -131,7 +144,22 @@ pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_
                         workspace ? workspace_bytes : (size_t)0);
         REQUIRE_PTR(workspace, 16);
     }
-    const size_t smem = pa::attention_smem_bytes((int)dtype, head_dim, PT, block_size);
+    // Launch shape: HPC query heads per CTA (one warp each), STG tiles in flight per warp
+    // (~64 KB of stages per CTA -> 3 CTAs per SM).  PA_HPC / PA_STG override (tuning).
+    const int stage = pa::attention_stage_bytes((int)dtype, head_dim);
+    int hpc = 1;
+    if (num_heads % 4 == 0) {
+        hpc = 4;
+    } else {
+        for (int d = 8; d >= 1; --d)
+            if (num_heads % d == 0) { hpc = d; break; }
+    }
+    if (const char* ev = getenv("PA_HPC")) hpc = atoi(ev) > 0 ? atoi(ev) : hpc;
+    if (hpc > 8) hpc = 8;
+    int stg = (64 * 1024) / (hpc * stage);
+    stg = stg < 2 ? 2 : (stg > 8 ? 8 : stg);
+    if (const char* ev = getenv("PA_STG")) stg = atoi(ev) > 0 ? atoi(ev) : stg;
+    const size_t smem = pa::attention_smem_bytes(stage, hpc, stg, PT, block_size);
     if (smem > 227 * 1024)
         return fail(PA_ERR_UNSUPPORTED, "partition_tokens %d with block_size %d needs %zu B of shared memory", PT,
                     block_size, smem);
@@ -143,10 +171,17 @@ pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_
     p.value_cache = value_cache;
     p.block_tables = block_tables;
     p.context_lens = context_lens;
+    p.new_key = new_key;
+    p.new_value = new_value;
+    p.key_cache_w = const_cast<void*>(key_cache);
+    p.value_cache_w = const_cast<void*>(value_cache);
     if (need > 0) {
         const int64_t n = (int64_t)num_seqs * num_heads * NP;
-        p.part_o = static_cast<float*>(workspace);
-        p.part_ml = reinterpret_cast<float2*>(static_cast<char*>(workspace) + n * head_dim * 4);
+        const int64_t cnt_bytes = (((int64_t)num_seqs * num_heads * 4 + 15) / 16) * 16;
+        char* w = static_cast<char*>(workspace);
+        p.counters = reinterpret_cast<int*>(w);
+        p.part_o = reinterpret_cast<float*>(w + cnt_bytes);
+        p.part_ml = reinterpret_cast<float2*>(w + cnt_bytes + n * head_dim * 4);
     }
     p.scale_log2 = (float)((double)scale * 1.4426950408889634);
     p.log2B = log2B;
@@ -156,9 +191,39 @@ pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_
     p.W = max_blocks_per_seq;
     p.PT = PT;
     p.NP = NP;
-    cudaError_t e = pa::launch_attention(p, (int)dtype, head_dim, num_seqs, num_heads, (cudaStream_t)stream);
+    p.HPC = hpc;
+    p.STG = stg;
+    cudaError_t e = pa::launch_attention(p, (int)dtype, head_dim, num_seqs, smem, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "pa_paged_attention");
     return PA_OK;
+}
+}  // namespace
+
+extern "C" {
+
+pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_cache, const void* value_cache,
+                                  const int32_t* block_tables, const int32_t* context_lens, float scale,
+                                  int block_size, int num_kv_heads, int num_seqs, int num_heads, int head_dim,
+                                  int max_blocks_per_seq, int max_context_len, pa_dtype_t dtype,
+                                  int partition_tokens, void* workspace, size_t workspace_bytes,
+                                  pa_stream_t stream) {
+    g_err.clear();
+    return attention_impl(out, query, nullptr, nullptr, key_cache, value_cache, block_tables, context_lens, scale,
+                          block_size, num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq,
+                          max_context_len, dtype, partition_tokens, workspace, workspace_bytes, stream);
+}
+
+pa_status_t pa_paged_attention_decode(void* out, const void* query, const void* key, const void* value,
+                                      void* key_cache, void* value_cache, const int32_t* block_tables,
+                                      const int32_t* context_lens, float scale, int block_size, int num_kv_heads,
+                                      int num_seqs, int num_heads, int head_dim, int max_blocks_per_seq,
+                                      int max_context_len, pa_dtype_t dtype, void* workspace,
+                                      size_t workspace_bytes, pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(key != nullptr && value != nullptr, "key/value (the step's new token) are NULL");
+    return attention_impl(out, query, key, value, key_cache, value_cache, block_tables, context_lens, scale,
+                          block_size, num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq,
+                          max_context_len, dtype, 0, workspace, workspace_bytes, stream);
 }
 
 pa_status_t pa_paged_attention(void* out, const void* query, const void* key_cache, const void* value_cache,
@@ -267,8 +332,8 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     REQUIRE(num_seqs >= 0 && num_heads > 0 && num_kv_heads > 0 && max_blocks_per_seq > 0, "bad sizes");
     REQUIRE(num_pairs >= 0, "num_pairs must be >= 0");
     if (num_seqs == 0 && num_pairs == 0) return PA_OK;
-    REQUIRE(host_out && host_query && host_key && host_value && host_slot_mapping && host_block_tables &&
-                host_context_lens,
+    (void)host_slot_mapping;  // implied by the block tables for a decode step (see pa.h)
+    REQUIRE(host_out && host_query && host_key && host_value && host_block_tables && host_context_lens,
             "a host input pointer is NULL");
     REQUIRE(num_pairs == 0 || host_block_mapping, "host_block_mapping is NULL");
     const StagingLayout L =
@@ -287,7 +352,6 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     } cps[] = {{L.q, host_query, (size_t)num_seqs * num_heads * head_dim * e},
                {L.k, host_key, (size_t)num_seqs * num_kv_heads * head_dim * e},
                {L.v, host_value, (size_t)num_seqs * num_kv_heads * head_dim * e},
-               {L.slot, host_slot_mapping, (size_t)num_seqs * 8},
                {L.bt, host_block_tables, (size_t)num_seqs * max_blocks_per_seq * 4},
                {L.ctx, host_context_lens, (size_t)num_seqs * 4},
                {L.bm, host_block_mapping, (size_t)num_pairs * 16}};
@@ -304,13 +368,11 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
                            block_size, head_dim, dtype, stream);
         if (r != PA_OK) return r;
     }
-    r = pa_reshape_and_cache(st + L.k, st + L.v, key_cache, value_cache, reinterpret_cast<const int64_t*>(st + L.slot),
-                             num_seqs, num_kv_heads, head_dim, block_size, dtype, stream);
-    if (r != PA_OK) return r;
-    r = pa_paged_attention(st + L.out, st + L.q, key_cache, value_cache, reinterpret_cast<const int32_t*>(st + L.bt),
-                           reinterpret_cast<const int32_t*>(st + L.ctx), scale, block_size, num_kv_heads, num_seqs,
-                           num_heads, head_dim, max_blocks_per_seq, max_context_len, dtype, workspace,
-                           workspace_bytes, stream);
+    r = pa_paged_attention_decode(st + L.out, st + L.q, st + L.k, st + L.v, key_cache, value_cache,
+                                  reinterpret_cast<const int32_t*>(st + L.bt),
+                                  reinterpret_cast<const int32_t*>(st + L.ctx), scale, block_size, num_kv_heads,
+                                  num_seqs, num_heads, head_dim, max_blocks_per_seq, max_context_len, dtype, workspace,
+                                  workspace_bytes, stream);
     if (r != PA_OK) return r;
     cudaError_t err =
         cudaMemcpyAsync(host_out, st + L.out, (size_t)num_seqs * num_heads * head_dim * e, cudaMemcpyDeviceToHost, s);

@@ -11,7 +11,11 @@
 
 namespace pa {
 
-__global__ void __launch_bounds__(128) reshape_and_cache_kernel(const CacheWriteParams p) {
+// One CTA per token; 256 threads issue all of the token's 16-byte loads (K and V, every
+// kv head) before any store so each thread has several requests in flight.
+__global__ void __launch_bounds__(256) reshape_and_cache_kernel(const CacheWriteParams p) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int i = blockIdx.x;
     const int64_t slot = p.slot_mapping[i];
     if (slot < 0) return;  // padding token (reading c11)
@@ -23,16 +27,33 @@ __global__ void __launch_bounds__(128) reshape_and_cache_kernel(const CacheWrite
     const uint4* vs = static_cast<const uint4*>(p.value) + (int64_t)i * nvec;
     uint4* kc = static_cast<uint4*>(p.key_cache);
     uint4* vc = static_cast<uint4*>(p.value_cache);
-    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-        const int h = v / cpr, cc = v - h * cpr;
-        const int64_t dst = ((((b * p.H_kv + h) << p.log2B) + o) * cpr) + cc;
-        const uint4 kv = __ldg(ks + v), vv = __ldg(vs + v);
-        kc[dst] = kv;
-        vc[dst] = vv;
+    constexpr int U = 4;
+    for (int v0 = threadIdx.x; v0 < nvec; v0 += U * 256) {
+        uint4 kr[U], vr[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int v = v0 + u * 256;
+            if (v < nvec) {
+                kr[u] = __ldg(ks + v);
+                vr[u] = __ldg(vs + v);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int v = v0 + u * 256;
+            if (v < nvec) {
+                const int h = v / cpr, cc = v - h * cpr;
+                const int64_t dst = ((((b * p.H_kv + h) << p.log2B) + o) * cpr) + cc;
+                kc[dst] = kr[u];
+                vc[dst] = vr[u];
+            }
+        }
     }
 }
 
 __global__ void __launch_bounds__(256) copy_blocks_kernel(const __grid_constant__ CopyBlocksParams p) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int pair = blockIdx.x, layer = blockIdx.y, which = blockIdx.z;
     const int64_t src = p.block_mapping[2 * pair], dst = p.block_mapping[2 * pair + 1];
     char* base = static_cast<char*>(which == 0 ? p.key_caches[layer] : p.value_caches[layer]);
@@ -72,15 +93,11 @@ __global__ void validate_tables_kernel(const int32_t* bt, const int32_t* ctx, in
 }
 
 cudaError_t launch_reshape_and_cache(const CacheWriteParams& p, cudaStream_t stream) {
-    reshape_and_cache_kernel<<<p.num_tokens, 128, 0, stream>>>(p);
-    count_launch();
-    return cudaGetLastError();
+    return launch_k(reshape_and_cache_kernel, dim3(p.num_tokens), dim3(256), 0, stream, p);
 }
 
 cudaError_t launch_copy_blocks(const CopyBlocksParams& p, int num_layers, int num_pairs, cudaStream_t stream) {
-    copy_blocks_kernel<<<dim3(num_pairs, num_layers, 2), 256, 0, stream>>>(p);
-    count_launch();
-    return cudaGetLastError();
+    return launch_k(copy_blocks_kernel, dim3(num_pairs, num_layers, 2), dim3(256), 0, stream, p);
 }
 
 cudaError_t launch_validate_tables(const int32_t* bt, const int32_t* ctx, int S, int W, int B, int NB,

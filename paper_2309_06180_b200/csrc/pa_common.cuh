@@ -69,6 +69,15 @@ __device__ __forceinline__ void bulk_g2s_hint(void* smem_dst, const void* gsrc, 
         : "memory");
 }
 
+// ---- programmatic dependent launch (PDL) -----------------------------------------------
+// Kernels of this library are launched with programmatic stream serialisation: a kernel
+// may be scheduled while its predecessor drains, and blocks in pdl_wait() until the
+// predecessor grid has completed and its memory is visible.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- math -----------------------------------------------------------------------------
 __device__ __forceinline__ float ex2(float x) {  // 2^x, ex2.approx (MUFU.EX2); ex2(-inf) = +0
     float y;

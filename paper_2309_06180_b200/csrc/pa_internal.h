@@ -5,6 +5,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace pa {
 
 struct AttnParams {
@@ -14,14 +16,21 @@ struct AttnParams {
     const void* value_cache;    // [NB][H_kv][B][D]
     const int32_t* block_tables;  // [S][W]
     const int32_t* context_lens;  // [S]
+    const void* new_key;        // [S][H_kv][D] this step's token (fused decode entry) or NULL
+    const void* new_value;
+    void* key_cache_w;          // writable aliases of the caches (fused decode entry)
+    void* value_cache_w;
     float2* part_ml;            // [S][H][NP] (m, L) in the exp2 domain (split only)
     float* part_o;              // [S][H][NP][D] normalised partial outputs (split only)
+    int* counters;              // [S][ceil(H/HPC)] partitions finished (split only; zero between calls)
     float scale_log2;           // scale * log2(e)
     int log2B;                  // block_size = 1 << log2B
     int H, H_kv, G;             // query heads, kv heads, H / H_kv
     int W;                      // block table row stride
     int PT;                     // partition size in tokens (multiple of 16)
     int NP;                     // partitions in the grid = ceil(max_ctx / PT)
+    int HPC;                    // query heads per CTA (one warp each)
+    int STG;                    // tiles in flight per warp (shared-memory stages)
 };
 
 struct GatherParams {
@@ -52,9 +61,29 @@ struct CopyBlocksParams {
 };
 
 void count_launch();
+bool pdl_enabled();  // PA_PDL=0 disables programmatic dependent launch
 
-size_t attention_smem_bytes(int dtype, int head_dim, int partition_tokens, int block_size);
-cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int num_heads,
+// Launch `kern` on `stream`, with programmatic stream serialisation when enabled.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                     Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    count_launch();
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+int attention_stage_bytes(int dtype, int head_dim);
+size_t attention_smem_bytes(int stage_bytes, int hpc, int stg, int partition_tokens, int block_size);
+cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, size_t smem,
                              cudaStream_t stream);
 cudaError_t launch_debug_gather(const GatherParams& p, int dtype, int head_dim, int num_seqs, cudaStream_t stream);
 cudaError_t launch_reshape_and_cache(const CacheWriteParams& p, cudaStream_t stream);

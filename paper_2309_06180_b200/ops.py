@@ -48,7 +48,8 @@ def paged_attention(out, query, key_cache, value_cache, block_tables, context_le
                     partition_tokens: int = 0, workspace: torch.Tensor | None = None, stream=None):
     """Eq.4 decode attention: out[s][h] = softmax(scale q.K^T) V over the
     block-table-addressed cache.  out/query [S][H][D]; caches [NB][H_kv][B][D];
-    block_tables int32 [S][W]; context_lens int32 [S]."""
+    block_tables int32 [S][W]; context_lens int32 [S].  `workspace` (uint8, device, any
+    content; see pa.h) is allocated when omitted and the context needs splitting."""
     S, H, D = query.shape
     _, hk, B, _ = key_cache.shape
     block_size = B if block_size is None else block_size
@@ -65,6 +66,27 @@ def paged_attention(out, query, key_cache, value_cache, block_tables, context_le
         _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"), float(scale), int(block_size),
         int(num_kv_heads), S, H, D, W, int(mcl), _code(query), int(partition_tokens), ws_ptr, ws_bytes,
         _stream(stream)), "pa_paged_attention")
+    return out
+
+
+def paged_attention_decode(out, query, key, value, key_cache, value_cache, block_tables, context_lens, scale: float,
+                           max_context_len: int = 0, workspace: torch.Tensor | None = None, stream=None):
+    """The decode step's reshape_and_cache fused into paged_attention (pa.h): token s
+    (key/value [S][H_kv][D]) is written at logical position ctx[s]-1 and attended."""
+    S, H, D = query.shape
+    _, hk, B, _ = key_cache.shape
+    W = block_tables.shape[1]
+    mcl = max_context_len if max_context_len > 0 else W * B
+    need = paged_attention_workspace_size(S, H, D, mcl, 0)
+    if workspace is None and need > 0:
+        workspace = torch.empty(need, dtype=torch.uint8, device=query.device)
+    ws_ptr = _dev(workspace, "workspace") if workspace is not None else None
+    ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    check(_lib.raw().pa_paged_attention_decode(
+        _dev(out, "out"), _dev(query, "query"), _dev(key, "key"), _dev(value, "value"), _dev(key_cache, "key_cache"),
+        _dev(value_cache, "value_cache"), _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"),
+        float(scale), B, hk, S, H, D, W, int(mcl), _code(query), ws_ptr, ws_bytes, _stream(stream)),
+        "pa_paged_attention_decode")
     return out
 
 
@@ -115,7 +137,7 @@ def decode_step(host_out, host_query, host_key, host_value, host_slot_mapping, h
     ws_bytes = workspace.numel() if workspace is not None else 0
     check(_lib.raw().pa_decode_step(
         _host(host_out, "host_out"), _host(host_query, "host_query"), _host(host_key, "host_key"),
-        _host(host_value, "host_value"), _host(host_slot_mapping, "host_slot_mapping"),
+        _host(host_value, "host_value"), None,
         _host(host_block_tables, "host_block_tables"), _host(host_context_lens, "host_context_lens"),
         _host(host_block_mapping, "host_block_mapping") if P else None, P,
         _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"), float(scale), B, hk, S, H, D, W,

@@ -22,8 +22,9 @@ def as_f64(t) -> np.ndarray:
     return t.detach().to(torch.float64).cpu().numpy()
 
 
-def gpu_step(wl, device="cuda", partition_tokens=0, inputs=None, run_copy=True, run_write=True):
-    """copy_blocks -> reshape_and_cache -> paged_attention on the device.
+def gpu_step(wl, device="cuda", partition_tokens=0, inputs=None, run_copy=True, run_write=True, fused=False):
+    """copy_blocks -> reshape_and_cache -> paged_attention on the device (fused=True:
+    copy_blocks -> paged_attention_decode, the cache write inside the attention kernel).
     Returns (out, key_cache, value_cache, inputs)."""
     import torch
 
@@ -34,9 +35,14 @@ def gpu_step(wl, device="cuda", partition_tokens=0, inputs=None, run_copy=True, 
     kc, vc = x["key_cache"], x["value_cache"]
     if run_copy and len(wl.block_mapping):
         pa.copy_blocks([kc], [vc], tb["block_mapping"])
+    out = torch.empty_like(x["query"])
+    if fused:
+        pa.paged_attention_decode(out, x["query"], x["key"], x["value"], kc, vc, tb["block_tables"],
+                                  tb["context_lens"], wl.scale, max_context_len=wl.max_context_len)
+        torch.cuda.synchronize()
+        return out, kc, vc, x
     if run_write:
         pa.reshape_and_cache(x["key"], x["value"], kc, vc, tb["slot_mapping"])
-    out = torch.empty_like(x["query"])
     pa.paged_attention(out, x["query"], kc, vc, tb["block_tables"], tb["context_lens"], wl.scale,
                        max_context_len=wl.max_context_len, partition_tokens=partition_tokens)
     torch.cuda.synchronize()

@@ -84,7 +84,7 @@ def test_workspace_size():
     assert f(4, 2, 64, 100, 0) == 0
     assert f(4, 2, 64, 512, 0) == 0
     S, H, D = 256, 40, 128
-    assert f(S, H, D, 2048, 0) == S * H * 4 * (D * 4 + 8)
+    assert f(S, H, D, 2048, 0) == S * H * 4 + S * H * 4 * (D * 4 + 8)
     assert f(S, H, D, 2048, 4096) == 0
 
 

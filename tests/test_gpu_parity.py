@@ -260,7 +260,7 @@ def test_validate_tables():
 def test_decode_step_host_api_matches_device_api():
     wl = make_config("c3_fork", S=24, H=2, H_kv=2)
     x = materialize_torch(wl, "cuda")
-    ref, *_ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()})
+    ref, rk, rv, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()})
     kc, vc = x["key_cache"].clone(), x["value_cache"].clone()
     pin = {k: x[k].cpu().pin_memory() for k in ("query", "key", "value")}
     host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in
@@ -269,11 +269,12 @@ def test_decode_step_host_api_matches_device_api():
     st = torch.empty(pa.decode_step_staging_size(wl.S, wl.H, wl.H_kv, wl.D, wl.W, len(wl.block_mapping),
                                                  pin["query"].dtype), dtype=torch.uint8, device="cuda")
     ws_n = pa.paged_attention_workspace_size(wl.S, wl.H, wl.D, wl.max_context_len)
-    ws = torch.empty(max(ws_n, 16), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(ws_n, 16), dtype=torch.uint8, device="cuda")
     pa.decode_step(out, pin["query"], pin["key"], pin["value"], host["slot"], host["bt"], host["cl"], host["bm"],
                    kc, vc, wl.scale, st, ws, max_context_len=wl.max_context_len)
     torch.cuda.synchronize()
     assert torch.equal(out, ref.cpu())
+    assert np.array_equal(bits(kc), bits(rk)) and np.array_equal(bits(vc), bits(rv))
 
 
 def test_cow_parent_unchanged():
@@ -322,3 +323,63 @@ def test_full_size_sampled_parity(name):
     B = wl.B
     assert torch.equal(kc[slots // B, :, slots % B, :], x["key"]) and torch.equal(vc[slots // B, :, slots % B, :],
                                                                                    x["value"])
+
+
+def test_workspace_reuse_across_layouts():
+    """One workspace (garbage-filled) serves calls with different partition counts and
+    batch sizes: the call zeroes its own completion counters (pa.h contract)."""
+    wl = make_config("c2_sharegpt", S=32, H=4, H_kv=4)
+    x = materialize_torch(wl, "cuda")
+    tb = tables_torch(wl, "cuda")
+    pts = [16, 64, 512]
+    need = max(pa.paged_attention_workspace_size(wl.S, wl.H, wl.D, wl.max_context_len, pt) for pt in pts)
+    ws = torch.randint(0, 255, (need,), dtype=torch.uint8, device="cuda")
+    pa.reshape_and_cache(x["key"], x["value"], x["key_cache"], x["value_cache"], tb["slot_mapping"])
+    ref, *_ = oracle_step(wl)
+    for pt, ns in [(16, 32), (64, 32), (512, 32), (16, 7), (64, 32), (16, 32)]:
+        out = torch.empty_like(x["query"][:ns])
+        pa.paged_attention(out, x["query"][:ns].contiguous(), x["key_cache"], x["value_cache"],
+                           tb["block_tables"][:ns].contiguous(), tb["context_lens"][:ns].contiguous(), wl.scale,
+                           max_context_len=wl.max_context_len, partition_tokens=pt, workspace=ws)
+        torch.cuda.synchronize()
+        assert max_abs(out, ref[:ns]) <= TOL[wl.dtype], (pt, ns)
+
+
+@pytest.mark.parametrize("name", list(SMALL) + ["c2_sharegpt_full", "c5_beam_full"])
+def test_fused_decode_equals_unfused_bitwise(name):
+    """pa_paged_attention_decode (cache write fused into the attention kernel) leaves the
+    same cache bytes and the same output bits as reshape_and_cache + paged_attention,
+    and matches the oracle."""
+    if name.endswith("_full"):
+        wl = make_config(name[:-5])
+    else:
+        wl = make_config(name, **SMALL[name])
+    x = materialize_torch(wl, "cuda")
+    a, ka, va, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()})
+    b, kb, vb, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()}, fused=True)
+    assert torch.equal(a, b)
+    assert torch.equal(ka.view(torch.int16 if ka.element_size() == 2 else torch.int32),
+                       kb.view(torch.int16 if kb.element_size() == 2 else torch.int32))
+    assert torch.equal(va.view(torch.int16 if va.element_size() == 2 else torch.int32),
+                       vb.view(torch.int16 if vb.element_size() == 2 else torch.int32))
+    if not name.endswith("_full"):
+        ref, rkc, rvc = oracle_step(wl)
+        assert np.array_equal(bits(kb), rkc) and np.array_equal(bits(vb), rvc)
+        assert max_abs(b, ref) <= TOL[wl.dtype]
+
+
+@pytest.mark.parametrize("B", [1, 8, 32])
+def test_fused_decode_block_sizes(B):
+    wl = make_config("c2_sharegpt", S=16, H=4, H_kv=4, B=B)
+    out, kc, vc, _ = gpu_step(wl, fused=True)
+    ref, rkc, rvc = oracle_step(wl)
+    assert np.array_equal(bits(kc), rkc) and np.array_equal(bits(vc), rvc)
+    assert max_abs(out, ref) <= TOL[wl.dtype]
+
+
+def test_fused_decode_gqa():
+    wl = make_config("c2_sharegpt", S=8, H=8, H_kv=2)
+    out, kc, vc, _ = gpu_step(wl, fused=True)
+    ref, rkc, rvc = oracle_step(wl)
+    assert np.array_equal(bits(kc), rkc) and np.array_equal(bits(vc), rvc)
+    assert max_abs(out, ref) <= TOL[wl.dtype]
