@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -63,12 +64,29 @@ int effective_partition(int partition_tokens) {
     return partition_tokens == 0 ? PA_DEFAULT_PARTITION_TOKENS : partition_tokens;
 }
 
+int64_t pad16(int64_t x) { return (x + 15) / 16 * 16; }
+
+// Workspace layout: counters [S][H] int32 | control (work counter, unit count) 16 B |
+// work list [S][NP] int4 | (split only) part_o [S][H][NP][D] fp32 | part_ml [S][H][NP] float2
+struct WsLayout {
+    int64_t counters, ctrl, items, part_o, part_ml, total;
+};
+WsLayout ws_layout(int64_t S, int64_t H, int64_t D, int64_t NP) {
+    WsLayout L{};
+    int64_t o = 0;
+    L.counters = o; o += pad16(S * H * 4);
+    L.ctrl = o;     o += 16;
+    L.items = o;    o += pad16(S * NP * 16);
+    L.part_o = o;   if (NP > 1) o += S * H * NP * D * 4;
+    L.part_ml = o;  if (NP > 1) o += S * H * NP * 8;
+    L.total = o;
+    return L;
+}
+
 size_t workspace_bytes_for(int64_t S, int64_t H, int64_t D, int max_ctx, int PT) {
-    if (S <= 0 || H <= 0 || D <= 0 || max_ctx <= 0 || PT <= 0) return 0;
-    const int64_t NP = (max_ctx + PT - 1) / PT;
-    if (NP <= 1) return 0;
-    // counters [S][H] int32 (16-byte padded), part_o [S][H][NP][D] fp32, part_ml [S][H][NP] float2
-    return (size_t)(((S * H * 4 + 15) / 16) * 16 + S * H * NP * D * 4 + S * H * NP * 8);
+    if (S <= 0 || H <= 0 || D <= 0 || PT <= 0) return 0;
+    const int64_t NP = max_ctx > 0 ? (max_ctx + PT - 1) / PT : 1;
+    return (size_t)ws_layout(S, H, D, NP).total;
 }
 
 }  // namespace
@@ -136,30 +154,38 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     int64_t mcl = max_context_len > 0 ? max_context_len : cap;
     if (mcl > cap) mcl = cap;
     REQUIRE(mcl <= (1 << 30), "max_context_len too large");
-    const int NP = (int)((mcl + PT - 1) / PT);
+    const int NP = std::max<int>(1, (int)((mcl + PT - 1) / PT));
     const size_t need = workspace_bytes_for(num_seqs, num_heads, head_dim, (int)mcl, PT);
-    if (need > 0) {
-        if (workspace == nullptr || workspace_bytes < need)
-            return fail(PA_ERR_WORKSPACE, "workspace of %zu bytes required (got %zu)", need,
-                        workspace ? workspace_bytes : (size_t)0);
-        REQUIRE_PTR(workspace, 16);
-    }
-    // Launch shape: HPC query heads per CTA (one warp each), STG tiles in flight per warp
-    // (~64 KB of stages per CTA -> 3 CTAs per SM).  PA_HPC / PA_STG override (tuning).
-    const int stage = pa::attention_stage_bytes((int)dtype, head_dim);
-    int hpc = 1;
-    if (num_heads % 4 == 0) {
-        hpc = 4;
-    } else {
+    if (workspace == nullptr || workspace_bytes < need)
+        return fail(PA_ERR_WORKSPACE, "workspace of %zu bytes required (got %zu)", need,
+                    workspace ? workspace_bytes : (size_t)0);
+    REQUIRE_PTR(workspace, 16);
+    // Scheduler (PA_SCHED): "coop" (default) -- one CTA per (partition, group of 4 query
+    // heads, sequence), one producer warp filling shared K/V stages for 4 consumer warps;
+    // "grid" -- same CTAs, every warp loading its own head's tiles; "persistent" --
+    // warps streaming a longest-first work list.  ~64 KB of stages per CTA (3 CTAs per
+    // SM), measured best (scripts/sweep.py).  PA_HPC / PA_STG / PA_HPW override.
+    const char* sched_env = getenv("PA_SCHED");
+    int sched = 2;  // coop
+    if (sched_env && std::strcmp(sched_env, "grid") == 0) sched = 0;
+    if (sched_env && std::strcmp(sched_env, "persistent") == 0) sched = 1;
+    const bool persistent = sched == 1;
+    const int rb = pa::attention_row_bytes((int)dtype, head_dim);
+    const int G = num_heads / num_kv_heads;
+    int nw = 4;
+    if (sched != 1 && num_heads % 4 != 0) {
         for (int d = 8; d >= 1; --d)
-            if (num_heads % d == 0) { hpc = d; break; }
+            if (num_heads % d == 0) { nw = d; break; }
     }
-    if (const char* ev = getenv("PA_HPC")) hpc = atoi(ev) > 0 ? atoi(ev) : hpc;
-    if (hpc > 8) hpc = 8;
-    int stg = (64 * 1024) / (hpc * stage);
+    if (const char* ev = getenv("PA_HPC")) nw = atoi(ev) > 0 ? atoi(ev) : nw;
+    if (nw > 8) nw = 8;
+    const int nkv_max = nw % G == 0 ? nw / G : (nw + G - 1) / G + 1;
+    const int stage = sched == 2 ? 2 * nkv_max * 16 * rb : 2 * 16 * rb;
+    int stg = sched == 2 ? (64 * 1024) / stage : (64 * 1024) / (nw * stage);
     stg = stg < 2 ? 2 : (stg > 8 ? 8 : stg);
     if (const char* ev = getenv("PA_STG")) stg = atoi(ev) > 0 ? atoi(ev) : stg;
-    const size_t smem = pa::attention_smem_bytes(stage, hpc, stg, PT, block_size);
+    const size_t smem = sched == 2 ? pa::attention_smem_bytes_coop(rb, nw, G, stg, PT, block_size)
+                                   : pa::attention_smem_bytes(persistent, rb, nw, stg, PT, block_size);
     if (smem > 227 * 1024)
         return fail(PA_ERR_UNSUPPORTED, "partition_tokens %d with block_size %d needs %zu B of shared memory", PT,
                     block_size, smem);
@@ -175,13 +201,15 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     p.new_value = new_value;
     p.key_cache_w = const_cast<void*>(key_cache);
     p.value_cache_w = const_cast<void*>(value_cache);
-    if (need > 0) {
-        const int64_t n = (int64_t)num_seqs * num_heads * NP;
-        const int64_t cnt_bytes = (((int64_t)num_seqs * num_heads * 4 + 15) / 16) * 16;
+    {
+        const WsLayout L = ws_layout(num_seqs, num_heads, head_dim, NP);
         char* w = static_cast<char*>(workspace);
-        p.counters = reinterpret_cast<int*>(w);
-        p.part_o = reinterpret_cast<float*>(w + cnt_bytes);
-        p.part_ml = reinterpret_cast<float2*>(w + cnt_bytes + n * head_dim * 4);
+        p.counters = reinterpret_cast<int*>(w + L.counters);
+        p.work_counter = reinterpret_cast<int*>(w + L.ctrl);
+        p.n_items = reinterpret_cast<int*>(w + L.ctrl + 4);
+        p.items = reinterpret_cast<int4*>(w + L.items);
+        p.part_o = reinterpret_cast<float*>(w + L.part_o);
+        p.part_ml = reinterpret_cast<float2*>(w + L.part_ml);
     }
     p.scale_log2 = (float)((double)scale * 1.4426950408889634);
     p.log2B = log2B;
@@ -191,9 +219,11 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     p.W = max_blocks_per_seq;
     p.PT = PT;
     p.NP = NP;
-    p.HPC = hpc;
+    p.HPC = nw;
     p.STG = stg;
-    cudaError_t e = pa::launch_attention(p, (int)dtype, head_dim, num_seqs, smem, (cudaStream_t)stream);
+    p.HPW = 1;
+    if (const char* ev = getenv("PA_HPW")) p.HPW = atoi(ev) > 0 ? atoi(ev) : 1;
+    cudaError_t e = pa::launch_attention(p, (int)dtype, head_dim, num_seqs, sched, smem, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "pa_paged_attention");
     return PA_OK;
 }

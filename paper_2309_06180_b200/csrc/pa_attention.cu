@@ -5,15 +5,21 @@
 // l_t = scale * q.K_t, a numerically stable softmax and sum_t softmax_t * V_t.
 //
 // B200 design:
-//  * One CTA per (partition, group of HPC query heads, sequence); warp w owns one query
-//    head and walks the partition's 16-token LOGICAL tiles in order (the arithmetic
-//    never depends on block_size, physical placement, head grouping or grid shape ->
-//    bitwise invariance).  The partition's block ids are prefetched into shared memory
-//    once per CTA (shared by its heads), so no copy waits on a dependent global load
-//    (the paper's "extra overhead of accessing the block table").
+//  * Work unit = (sequence, query head, partition of <= PT logical tokens); one WARP
+//    walks the unit's 16-token LOGICAL tiles in order, so the arithmetic never depends
+//    on block_size, physical placement, head grouping, scheduling or grid shape ->
+//    bitwise invariance (BJ:north_star's permutation / block-size properties).
 //  * Tiles are staged into shared memory by 1-D bulk async copies (cp.async.bulk,
-//    SASS UBLKCP) completing on a per-stage mbarrier; each warp keeps STG tiles in flight
-//    (lane 0 issues; for block_size < 16 lanes issue one piece each).
+//    SASS UBLKCP) completing on per-stage mbarriers; each warp keeps STG tiles in
+//    flight.  For block_size < 16 a tile is several pieces issued by several lanes.
+//  * Default scheduler ("persistent"): a tiny build kernel counting-sorts the
+//    (sequence, partition) units by length, longest first, into a work list; a
+//    persistent grid (occupancy x SMs) of independent warps takes units from it in a
+//    static zig-zag deal and streams their tiles back to back -- the bulk copies of
+//    the next unit (its q row included) are issued while the current one is being
+//    computed, so no warp idles in a prologue and the tail is made of the shortest
+//    units.
+//    Alternative ("grid", PA_SCHED=grid): one CTA per (partition, head group, seq).
 //  * Lane mapping: a K/V row of RB = D*e bytes is covered by LT = RB/32 lanes, each
 //    owning two 16-byte chunks (c and c+LT: conflict-free 128-byte phases); a warp
 //    handles TG = 32/LT tokens at once.  q.k uses the sm_100 mixed-precision FMA
@@ -22,13 +28,19 @@
 //    keeps its own online-softmax state (m, l, acc[]) in the exp2 domain, and p*V is
 //    accumulated with packed fp32x2 FMAs (FFMA2).  No tensor cores: a one-query decode
 //    step is a memory-bound GEMV (BJ:north_star).
-//  * End: token groups merge by shuffles (log-sum-exp, fixed order).  A sequence whose
-//    context fits one partition writes `out` directly (16-byte stores); otherwise each
-//    partition writes (m, L, o~) and paged_attention_reduce merges them (split-context
-//    variant, BJ:north_star).
+//  * End of a unit: token groups merge by shuffles (log-sum-exp, fixed order).  A
+//    context that fits one partition writes `out` directly (16-byte stores); otherwise
+//    each partition publishes (m, L, o~) and the LAST partition of the (sequence,
+//    head) to finish -- an atomic counter -- merges them in partition order
+//    (split-context variant, BJ:north_star).
+//  * Fused decode entry (pa_paged_attention_decode): the step's new token (logical
+//    position ctx-1) is bulk-copied from the key/value inputs straight into its tile
+//    row, and one warp per (sequence, kv head) stores it to its cache slot
+//    (reshape_and_cache) -- no separate launch.
 #include "pa_common.cuh"
 #include "pa_internal.h"
 
+#include <algorithm>
 #include <cfloat>
 
 namespace pa {
@@ -43,25 +55,190 @@ struct AttnCfg {
     static constexpr int TPL = kTile / TG;   // tokens per lane per tile
     static constexpr int EPC = 16 / E;       // elements per chunk
     static constexpr int STAGE_BYTES = 2 * kTile * RB;
+    static constexpr int PSTAGE_BYTES = STAGE_BYTES + RB;  // persistent stage: K | V | q row
     static_assert(LT >= 1 && LT <= 16 && TG * LT == 32, "row must span 2..32 lanes");
     static_assert(TPL >= 1 && TPL * TG == kTile, "tile must split evenly over token groups");
 };
 
-// Issue the bulk copies of logical tile `tok0` (nv valid tokens, nv <= 16) of kv head
-// `kvh` into (sK, sV).  sbt holds the block ids of logical blocks jb0, jb0+1, ...
-// Called by a whole warp (lanes 0..pieces-1 issue).  Only rows t < p1 are copied, so
-// slots past the context are never read (reading c3).
+// ===================================================================== per-tile math ===
+
+// Online-softmax update of one 16-token tile (nv valid rows) for the calling lane's
+// token group g and chunks (c, c+LT).  State in the exp2 domain.
+template <typename T, int D>
+__device__ __forceinline__ void tile_update(const char* sK, const char* sV, int nv, const uint4& q0, const uint4& q1,
+                                            float scale_log2, int g, int c, float& m, float& l,
+                                            float2 (&acc)[AttnCfg<T, D>::EPC]) {
+    using C = AttnCfg<T, D>;
+    constexpr int RB = C::RB, LT = C::LT, TG = C::TG, TPL = C::TPL, EPC = C::EPC;
+    float sc[TPL];
+#pragma unroll
+    for (int jj = 0; jj < TPL; ++jj) {
+        const char* row = sK + (jj * TG + g) * RB;
+        const uint4 k0 = lds128(row + c * 16), k1 = lds128(row + (c + LT) * 16);
+        float x = dot16<T>(q0, k0, 0.f) + dot16<T>(q1, k1, 0.f);
+#pragma unroll
+        for (int off = LT / 2; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+        sc[jj] = x * scale_log2;
+    }
+    if (nv < kTile) {
+#pragma unroll
+        for (int jj = 0; jj < TPL; ++jj)
+            if (jj * TG + g >= nv) sc[jj] = -INFINITY;
+    }
+    float mt = sc[0];
+#pragma unroll
+    for (int jj = 1; jj < TPL; ++jj) mt = fmaxf(mt, sc[jj]);
+    const float mn = fmaxf(m, mt);
+    const float ms = (mn == -INFINITY) ? 0.f : mn;
+    const float alpha = ex2(m - ms);
+    float ps[TPL], psum = 0.f;
+#pragma unroll
+    for (int jj = 0; jj < TPL; ++jj) {
+        ps[jj] = ex2(sc[jj] - ms);
+        psum += ps[jj];
+    }
+    l = l * alpha + psum;
+    const float2 aa = make_float2(alpha, alpha);
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) acc[e] = fmul2(acc[e], aa);
+    if (nv == kTile) {
+#pragma unroll
+        for (int jj = 0; jj < TPL; ++jj) {
+            const char* row = sV + (jj * TG + g) * RB;
+            const uint4 v0 = lds128(row + c * 16), v1 = lds128(row + (c + LT) * 16);
+            axpy16<T>(acc, ps[jj], v0);
+            axpy16<T>(acc + EPC / 2, ps[jj], v1);
+        }
+    } else {
+#pragma unroll
+        for (int jj = 0; jj < TPL; ++jj) {
+            if (jj * TG + g < nv) {  // rows past the context were never loaded (reading c3)
+                const char* row = sV + (jj * TG + g) * RB;
+                const uint4 v0 = lds128(row + c * 16), v1 = lds128(row + (c + LT) * 16);
+                axpy16<T>(acc, ps[jj], v0);
+                axpy16<T>(acc + EPC / 2, ps[jj], v1);
+            }
+        }
+    }
+    m = mn;
+}
+
+// Merge the warp's token groups (log-sum-exp, fixed butterfly order).
+template <typename T, int D>
+__device__ __forceinline__ void merge_token_groups(float& m, float& l, float2 (&acc)[AttnCfg<T, D>::EPC]) {
+    using C = AttnCfg<T, D>;
+    constexpr int LT = C::LT, EPC = C::EPC;
+#pragma unroll
+    for (int off = LT; off < 32; off <<= 1) {
+        const float mo = __shfl_xor_sync(0xffffffffu, m, off);
+        const float lo = __shfl_xor_sync(0xffffffffu, l, off);
+        const float mn = fmaxf(m, mo);
+        const float ms = (mn == -INFINITY) ? 0.f : mn;
+        const float a = ex2(m - ms), b = ex2(mo - ms);
+        l = l * a + lo * b;
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+            const float ox = __shfl_xor_sync(0xffffffffu, acc[e].x, off);
+            const float oy = __shfl_xor_sync(0xffffffffu, acc[e].y, off);
+            acc[e] = make_float2(acc[e].x * a + ox * b, acc[e].y * a + oy * b);
+        }
+        m = mn;
+    }
+}
+
+// Lanes of token group 0: out row = acc / l (0 for an empty context), 16-byte stores.
+template <typename T, int D>
+__device__ __forceinline__ void store_out(T* o, float l, const float2 (&acc)[AttnCfg<T, D>::EPC], int c) {
+    using C = AttnCfg<T, D>;
+    constexpr int LT = C::LT, EPC = C::EPC;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        alignas(16) T v[EPC];
+#pragma unroll
+        for (int e = 0; e < EPC / 2; ++e) {
+            v[2 * e] = Elem<T>::from_f32(l > 0.f ? acc[half * EPC / 2 + e].x / l : 0.f);
+            v[2 * e + 1] = Elem<T>::from_f32(l > 0.f ? acc[half * EPC / 2 + e].y / l : 0.f);
+        }
+        *reinterpret_cast<uint4*>(o + (c + half * LT) * EPC) = *reinterpret_cast<const uint4*>(v);
+    }
+}
+
+// Lanes of token group 0: normalised partial o~ = acc / l (fp32).
+template <typename T, int D>
+__device__ __forceinline__ void store_partial(float* o, float l, const float2 (&acc)[AttnCfg<T, D>::EPC], int c) {
+    using C = AttnCfg<T, D>;
+    constexpr int LT = C::LT, EPC = C::EPC;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+#pragma unroll
+        for (int e = 0; e < EPC / 2; e += 2) {
+            const float2 a0 = acc[half * EPC / 2 + e], a1 = acc[half * EPC / 2 + e + 1];
+            *reinterpret_cast<float4*>(o + (c + half * LT) * EPC + 2 * e) =
+                make_float4(a0.x / l, a0.y / l, a1.x / l, a1.y / l);
+        }
+    }
+}
+
+// Split-context merge of (sequence, head) sh over its np partitions, in partition order:
+//   M = max m_p;  out = sum_p 2^(m_p - M) L_p o~_p / sum_p 2^(m_p - M) L_p
+template <typename T, int D>
+__device__ __forceinline__ void merge_partitions(const AttnParams& p, int64_t sh, int np, int lane) {
+    const float2* ml = p.part_ml + sh * p.NP;
+    float M = -INFINITY;
+    for (int i = 0; i < np; ++i) M = fmaxf(M, __ldcg(&ml[i]).x);
+    float L = 0.f;
+    constexpr int DPL = D / 32;  // dims per lane
+    float o[DPL];
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) o[e] = 0.f;
+    const float* po = p.part_o + sh * p.NP * D;
+    for (int i = 0; i < np; ++i) {
+        const float2 mi = __ldcg(&ml[i]);
+        const float w = mi.y * ex2(mi.x - M);
+        L += w;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) o[e] += w * __ldcg(po + (int64_t)i * D + lane * DPL + e);
+    }
+    T* out = static_cast<T*>(p.out) + sh * D + lane * DPL;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) out[e] = Elem<T>::from_f32(o[e] / L);
+}
+
+// Publish this partition's (m, L, o~); the last partition to finish merges.  Whole warp.
+template <typename T, int D>
+__device__ __forceinline__ void finish_split(const AttnParams& p, int64_t sh, int part, int nparts, float m, float l,
+                                             const float2 (&acc)[AttnCfg<T, D>::EPC], int g, int c, int lane) {
+    if (g == 0) store_partial<T, D>(p.part_o + (sh * p.NP + part) * D, l, acc, c);
+    if (lane == 0) p.part_ml[sh * p.NP + part] = make_float2(m, l);
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+        __threadfence();
+        const int old = atomicAdd(p.counters + sh, 1);
+        last = (old == min(nparts, p.NP) - 1);
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+        __threadfence();
+        merge_partitions<T, D>(p, sh, min(nparts, p.NP), lane);
+    }
+}
+
+// ===================================================================== tile loaders ===
+
+// Grid scheduler: block ids of the partition prefetched in shared memory (sbt, from
+// logical block jb0).  Copies rows [tok0, tok0 + nv) (nv may be 0) of kv head `head_off`.
 __device__ __forceinline__ void issue_tile(char* sK, char* sV, uint64_t* bar, const char* kc, const char* vc,
                                            const int* sbt, int jb0, int tok0, int nv, int p1, int log2B,
                                            int64_t blk_stride, int64_t head_off, int RB, int lane) {
     const int B = 1 << log2B;
     if (B >= kTile) {
         if (lane == 0) {
-            const int blk = nv > 0 ? sbt[(tok0 >> log2B) - jb0] : 0;
-            const int64_t off = (int64_t)blk * blk_stride + head_off + (int64_t)(tok0 & (B - 1)) * RB;
             const uint32_t bytes = (uint32_t)(nv * RB);
             mbar_arrive_expect_tx(bar, 2 * bytes);
             if (bytes) {
+                const int blk = sbt[(tok0 >> log2B) - jb0];
+                const int64_t off = (int64_t)blk * blk_stride + head_off + (int64_t)(tok0 & (B - 1)) * RB;
                 bulk_g2s(sK, kc + off, bytes, bar);
                 bulk_g2s(sV, vc + off, bytes, bar);
             }
@@ -85,195 +262,461 @@ __device__ __forceinline__ void issue_tile(char* sK, char* sV, uint64_t* bar, co
     __syncwarp();
 }
 
-// One warp walks the logical tiles [p0, p1) of (sequence s, query head h) and leaves
-// the online-softmax state of its token groups merged: every lane ends with (m, l) of
-// the whole range (exp2 domain) and acc[] = unnormalised sum p*V for its two chunks.
-//
-// Fused cache write (decode entry point): when t_new >= 0 the token at logical position
-// t_new (= ctx - 1, the last row of this partition) is this step's new token.  Its K/V
-// row comes from new_key/new_value in registers; one warp per (sequence, kv head)
-// stores it into the cache slot (reshape_and_cache), and the tile loader
-// copies only the rows before it, the row itself being written into shared memory.
+// Persistent scheduler: block id prefetched (blk_pre >= 0) or read straight from the
+// block-table row (L1/L2 resident); optional extra rows (the unit's q row, the new token's K/V) ride on the
+// same mbarrier.  Copies cache rows [tok0, pc) of the tile.
+__device__ __forceinline__ void issue_tile_p(char* sK, char* sV, uint64_t* bar, const char* kc, const char* vc,
+                                             const int32_t* btrow, int tok0, int pc, int log2B, int64_t blk_stride,
+                                             int64_t head_off, int RB, int lane, const char* q_src, char* q_dst,
+                                             const char* nk_src, const char* nv_src, int new_row, int blk_pre) {
+    const int B = 1 << log2B;
+    const int nv = max(0, min(kTile, pc - tok0));
+    if (lane == 0) {
+        uint32_t tx = (uint32_t)(2 * nv * RB);
+        if (q_src) tx += RB;
+        if (nk_src) tx += 2 * RB;
+        mbar_arrive_expect_tx(bar, tx);
+        if (q_src) bulk_g2s(q_dst, q_src, RB, bar);
+        if (nk_src) {
+            bulk_g2s(sK + new_row * RB, nk_src, RB, bar);
+            bulk_g2s(sV + new_row * RB, nv_src, RB, bar);
+        }
+        if (B >= kTile && nv > 0) {
+            const int blk = blk_pre >= 0 ? blk_pre : __ldg(btrow + (tok0 >> log2B));
+            const int64_t off = (int64_t)blk * blk_stride + head_off + (int64_t)(tok0 & (B - 1)) * RB;
+            bulk_g2s(sK, kc + off, (uint32_t)(nv * RB), bar);
+            bulk_g2s(sV, vc + off, (uint32_t)(nv * RB), bar);
+        }
+    }
+    if (B < kTile) {
+        __syncwarp();
+        const int pieces = kTile >> log2B;
+        if (lane < pieces) {
+            const int tk = tok0 + (lane << log2B);
+            if (tk < pc) {
+                const int blk = __ldg(btrow + (tk >> log2B));
+                const int nvp = min(B, pc - tk);
+                const int64_t off = (int64_t)blk * blk_stride + head_off;
+                bulk_g2s(sK + (lane << log2B) * RB, kc + off, (uint32_t)(nvp * RB), bar);
+                bulk_g2s(sV + (lane << log2B) * RB, vc + off, (uint32_t)(nvp * RB), bar);
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// Store the new token's row (already in shared memory) to its cache slot: lanes of
+// token group 0, two 16-byte chunks of K and of V each.
 template <typename T, int D>
-__device__ __forceinline__ void walk_partition(const AttnParams& p, int s, int h, int p0, int p1, int t_new,
-                                               const int* sbt, int jb0, char* stage0, uint64_t* wbars, int lane,
-                                               float& m_out, float& l_out, float2 (&acc)[AttnCfg<T, D>::EPC]) {
+__device__ __forceinline__ void write_new_token(const AttnParams& p, const char* sKrow, const char* sVrow, int s,
+                                                int kvh, int t_new, int c) {
     using C = AttnCfg<T, D>;
-    constexpr int RB = C::RB, LT = C::LT, TG = C::TG, TPL = C::TPL, EPC = C::EPC;
+    constexpr int RB = C::RB, LT = C::LT;
+    const int blk = __ldg(p.block_tables + (int64_t)s * p.W + (t_new >> p.log2B));
+    const int64_t off = (int64_t)blk * (((int64_t)p.H_kv << p.log2B) * RB) + (((int64_t)kvh << p.log2B) * RB) +
+                        (int64_t)(t_new & ((1 << p.log2B) - 1)) * RB;
+    uint4* dk = reinterpret_cast<uint4*>(static_cast<char*>(p.key_cache_w) + off);
+    uint4* dv = reinterpret_cast<uint4*>(static_cast<char*>(p.value_cache_w) + off);
+    dk[c] = lds128(sKrow + c * 16);
+    dk[c + LT] = lds128(sKrow + (c + LT) * 16);
+    dv[c] = lds128(sVrow + c * 16);
+    dv[c + LT] = lds128(sVrow + (c + LT) * 16);
+}
+
+// ============================================================ persistent scheduler ===
+
+// Stable counting sort of the (sequence, partition) units by tile count, longest first
+// (ties keep sequence order, so sibling sequences that share blocks -- parallel
+// sampling, beam search -- stay adjacent and hit in L2), and zero the split counters
+// and the work counter.  One CTA of 1024 threads.  items[i] = (s, part, ctx, 0).
+constexpr int kBuckets = 256;
+
+__device__ __forceinline__ int unit_key(int ctx, int part, int PT) {
+    const int len = max(0, min(ctx, (part + 1) * PT) - part * PT);
+    return kBuckets - 1 - min((len + kTile - 1) / kTile, kBuckets - 1);  // 0 = longest
+}
+
+__global__ void __launch_bounds__(1024) build_worklist_kernel(const AttnParams p, int S) {
+    pdl_launch_dependents();
+    pdl_wait();
+    __shared__ int base[kBuckets];
+    __shared__ int wcnt[32][kBuckets];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t ncnt = (int64_t)S * p.H;
+    for (int64_t i = tid; i < ncnt; i += 1024) p.counters[i] = 0;
+    if (tid == 0) *p.work_counter = 0;
+    if (tid < kBuckets) base[tid] = 0;
+    __syncthreads();
+    for (int s = tid; s < S; s += 1024) {  // histogram
+        const int ctx = p.context_lens[s];
+        const int np = min(ctx > 0 ? (ctx + p.PT - 1) / p.PT : 1, p.NP);
+        for (int part = 0; part < np; ++part) atomicAdd(&base[unit_key(ctx, part, p.PT)], 1);
+    }
+    __syncthreads();
+    if (w == 0) {  // exclusive scan over the buckets (8 per lane)
+        int v[kBuckets / 32], sum = 0;
+#pragma unroll
+        for (int i = 0; i < kBuckets / 32; ++i) {
+            v[i] = base[lane * (kBuckets / 32) + i];
+            sum += v[i];
+        }
+        int x = sum;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, off);
+            if (lane >= off) x += y;
+        }
+        int run = x - sum;
+#pragma unroll
+        for (int i = 0; i < kBuckets / 32; ++i) {
+            base[lane * (kBuckets / 32) + i] = run;
+            run += v[i];
+        }
+        if (lane == 31) *p.n_items = run;
+    }
+    __syncthreads();
+    // stable scatter, in rounds of (1024 sequences, partition index)
+    for (int s0 = 0; s0 < S; s0 += 1024) {
+        const int s = s0 + tid;
+        const int ctx = s < S ? p.context_lens[s] : 0;
+        const int np = s < S ? min(ctx > 0 ? (ctx + p.PT - 1) / p.PT : 1, p.NP) : 0;
+        for (int part = 0; part < p.NP; ++part) {
+            const bool has = part < np;
+            const int b = has ? unit_key(ctx, part, p.PT) : -1;
+            for (int i = tid; i < 32 * kBuckets; i += 1024) (&wcnt[0][0])[i] = 0;
+            __syncthreads();
+            const unsigned peers = __match_any_sync(0xffffffffu, b);
+            const int rank = __popc(peers & ((1u << lane) - 1u));
+            if (has && rank == 0) wcnt[w][b] = __popc(peers);
+            __syncthreads();
+            if (tid < kBuckets) {
+                int run = base[tid];
+                for (int ww = 0; ww < 32; ++ww) {
+                    const int t = wcnt[ww][tid];
+                    wcnt[ww][tid] = run;
+                    run += t;
+                }
+                base[tid] = run;
+            }
+            __syncthreads();
+            if (has) p.items[wcnt[w][b] + rank] = make_int4(s, part, ctx, 0);
+            __syncthreads();
+        }
+    }
+}
+
+// Persistent warps.  Each warp runs a producer (issue the bulk copies of its units'
+// tiles -- up to STG in flight, across unit boundaries) and a consumer (wait, compute,
+// finish the unit) in one loop.  Unit fetching is software-pipelined so no latency is
+// exposed at unit boundaries (see below).  Unit descriptors travel from producer to
+// consumer through a small per-warp ring in shared memory.
+template <typename T, int D>
+__global__ void __launch_bounds__(256) paged_attention_persistent_kernel(const AttnParams p) {
+    using C = AttnCfg<T, D>;
+    constexpr int RB = C::RB, LT = C::LT, EPC = C::EPC;
+    constexpr int SB = C::PSTAGE_BYTES;
+    constexpr int DESC = 8;
+    extern __shared__ __align__(128) unsigned char smem[];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int NW = blockDim.x >> 5, STG = p.STG, RING = STG + 2;
+    char* wst = reinterpret_cast<char*>(smem) + (size_t)warp * STG * SB;
+    uint64_t* bars_all = reinterpret_cast<uint64_t*>(smem + (size_t)NW * STG * SB);
+    uint64_t* bars = bars_all + warp * STG;
+    int* ring = reinterpret_cast<int*>(bars_all + NW * STG) + warp * RING * DESC;
+    if (lane < STG) mbar_init(&bars[lane], 1);
+    fence_mbar_init();
+    __syncwarp();
+    pdl_wait();  // work list, counters, copy_blocks of this step: all complete
+
+    const int H = p.H, PT = p.PT, log2B = p.log2B;
+    const int total = __ldcg(p.n_items) * H;
+    const char* kc = static_cast<const char*>(p.key_cache);
+    const char* vc = static_cast<const char*>(p.value_cache);
+    const int64_t blk_stride = ((int64_t)p.H_kv << log2B) * RB;
+    const int g = lane / LT, c = lane % LT;
+
+    // ---- unit-fetch pipeline -------------------------------------------------------------
+    // Static zig-zag assignment of the longest-first list: round r gives warp wg the unit
+    // r*NWT + wg (r even) or r*NWT + NWT-1-wg (r odd) -- an LPT-like deal that balances
+    // the warps' totals and, being known in advance, lets every fetch be prefetched: the
+    // block ids of the next unit C sit in lane registers and the descriptor of the unit
+    // after it is in flight while unit P is being issued.  (An atomic work queue would
+    // either expose its round trip at every unit boundary or, with lookahead, commit the
+    // longest units to the warps that start first.)
+    const int NWT = gridDim.x * NW;
+    const int wg = blockIdx.x * NW + warp;
+    auto unit_of = [&](int r) -> int { return r * NWT + ((r & 1) ? NWT - 1 - wg : wg); };
+    auto load_desc = [&](int gi) -> int4 {
+        return gi < total ? __ldcg(&p.items[gi / H]) : make_int4(-1, 0, 0, 0);
+    };
+    // block id of logical block jb0 + lane of the unit (s, p0, p1); -1 past the range
+    auto load_bids = [&](int s, int p0, int p1) -> int {
+        const int jb0 = p0 >> log2B;
+        const int nb = p1 > p0 ? ((p1 - 1) >> log2B) - jb0 + 1 : 0;
+        return lane < nb ? __ldg(p.block_tables + (int64_t)s * p.W + jb0 + lane) : -1;
+    };
+    int round = 0;
+    // unit C (the next one for P) and unit N (the one after C; descriptor in flight)
+    int cg = unit_of(0);
+    int4 cd = load_desc(cg);
+    int ng = unit_of(1);
+    int4 nd = load_desc(ng);
+    int cs = cd.x, cpart = cd.y, cctx = cd.z;
+    int cbid = cs >= 0 ? load_bids(cs, cpart * PT, min(cctx, cpart * PT + PT)) : -1;
+
+    // producer state: current unit P
+    bool pr_done = false, pr_have = false;
+    int pr_slot = 0, queued = 0, pr_tile = 0, pr_ntiles = 0, st_issue = 0, in_flight = 0;
+    int pr_s = 0, pr_h = 0, pr_p0 = 0, pr_pc = 0, pr_tnew = -1, pr_bid = -1;
+    // consumer state
+    bool c_have = false;
+    int cs_slot = 0, c_tile = 0, st_cons = 0;
+    uint32_t phase = 0;
+    int c_s = 0, c_h = 0, c_part = 0, c_p0 = 0, c_p1 = 0, c_tnew = -1, c_nparts = 1, c_ntiles = 0;
+    float m = -INFINITY, l = 0.f;
+    float2 acc[EPC];
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
+    uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
+
+    while (true) {
+        // ---------------- producer: keep up to STG tiles in flight -------------------
+        while (!pr_done && in_flight < STG) {
+            if (!pr_have || pr_tile == pr_ntiles) {
+                pr_have = false;
+                if (queued == RING) break;
+                if (cs < 0) {  // no unit left
+                    pr_done = true;
+                    break;
+                }
+                // P <- C
+                const int s = cs, part = cpart, ctx = cctx, h = cg - (cg / H) * H;
+                const int p0 = part * PT, p1 = min(ctx, p0 + PT);
+                const int ntiles = p1 > p0 ? (p1 - p0 + kTile - 1) / kTile : 0;
+                const int nparts = ctx > 0 ? (ctx + PT - 1) / PT : 1;
+                const int t_new = (p.new_key != nullptr && ctx > 0 && p1 == ctx) ? ctx - 1 : -1;
+                pr_bid = cbid;
+                // C <- N (descriptor loaded one switch ago); its block ids start loading now
+                cg = ng;
+                cs = nd.x; cpart = nd.y; cctx = nd.z;
+                cbid = cs >= 0 ? load_bids(cs, cpart * PT, min(cctx, cpart * PT + PT)) : -1;
+                // N <- the unit after; its descriptor starts loading now
+                ++round;
+                ng = unit_of(round + 1);
+                nd = load_desc(ng);
+                if (lane == 0) {
+                    int* d = ring + pr_slot * DESC;
+                    d[0] = s; d[1] = h; d[2] = part; d[3] = p0; d[4] = p1; d[5] = t_new; d[6] = nparts; d[7] = ntiles;
+                }
+                __syncwarp();
+                pr_slot = (pr_slot + 1 == RING) ? 0 : pr_slot + 1;
+                ++queued;
+                pr_have = true;
+                pr_tile = 0;
+                pr_ntiles = ntiles;
+                pr_s = s; pr_h = h; pr_p0 = p0; pr_tnew = t_new; pr_pc = t_new >= 0 ? t_new : p1;
+                continue;
+            }
+            const int tok0 = pr_p0 + pr_tile * kTile;
+            const int kvh = pr_h / p.G;
+            char* sK = wst + st_issue * SB;
+            char* sV = sK + kTile * RB;
+            const bool has_new = pr_tnew >= tok0 && pr_tnew < tok0 + kTile;
+            const char* q_src = pr_tile == 0 ? static_cast<const char*>(p.query) + ((int64_t)pr_s * H + pr_h) * RB
+                                             : nullptr;
+            const char* nk = has_new ? static_cast<const char*>(p.new_key) + ((int64_t)pr_s * p.H_kv + kvh) * RB : nullptr;
+            const char* nvp = has_new ? static_cast<const char*>(p.new_value) + ((int64_t)pr_s * p.H_kv + kvh) * RB
+                                      : nullptr;
+            // block id of this tile from the prefetched lane registers (B >= 16: one block per tile)
+            const int bidx = (tok0 >> log2B) - (pr_p0 >> log2B);
+            const int blk = __shfl_sync(0xffffffffu, pr_bid, bidx & 31);
+            issue_tile_p(sK, sV, &bars[st_issue], kc, vc, p.block_tables + (int64_t)pr_s * p.W, tok0, pr_pc, log2B,
+                         blk_stride, ((int64_t)kvh << log2B) * RB, RB, lane, q_src, sV + kTile * RB, nk, nvp,
+                         pr_tnew - tok0, (bidx < 32 && blk >= 0) ? blk : -1);
+            ++pr_tile;
+            st_issue = (st_issue + 1 == STG) ? 0 : st_issue + 1;
+            ++in_flight;
+        }
+
+        // ---------------- consumer ----------------------------------------------------
+        if (!c_have) {
+            if (queued == 0) {
+                if (pr_done) break;
+                continue;
+            }
+            const int* d = ring + cs_slot * DESC;
+            c_s = d[0]; c_h = d[1]; c_part = d[2]; c_p0 = d[3]; c_p1 = d[4]; c_tnew = d[5]; c_nparts = d[6];
+            c_ntiles = d[7];
+            c_have = true;
+            c_tile = 0;
+            m = -INFINITY;
+            l = 0.f;
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
+        }
+        if (c_tile < c_ntiles) {
+            const int tok0 = c_p0 + c_tile * kTile;
+            const int nv = min(kTile, c_p1 - tok0);
+            const char* sK = wst + st_cons * SB;
+            const char* sV = sK + kTile * RB;
+            mbar_wait(&bars[st_cons], phase);
+            if (c_tile == 0) {
+                const char* sQ = sV + kTile * RB;
+                q0 = lds128(sQ + c * 16);
+                q1 = lds128(sQ + (c + LT) * 16);
+            }
+            tile_update<T, D>(sK, sV, nv, q0, q1, p.scale_log2, g, c, m, l, acc);
+            if (c_tnew >= tok0 && c_tnew < tok0 + kTile && c_h % p.G == 0 && g == 0)
+                write_new_token<T, D>(p, sK + (c_tnew - tok0) * RB, sV + (c_tnew - tok0) * RB, c_s, c_h / p.G, c_tnew,
+                                      c);
+            __syncwarp();
+            ++c_tile;
+            --in_flight;
+            if (++st_cons == STG) {
+                st_cons = 0;
+                phase ^= 1u;
+            }
+        }
+        if (c_tile == c_ntiles) {
+            merge_token_groups<T, D>(m, l, acc);
+            const int64_t sh = (int64_t)c_s * H + c_h;
+            if (c_nparts == 1) {
+                if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
+            } else {
+                finish_split<T, D>(p, sh, c_part, c_nparts, m, l, acc, g, c, lane);
+            }
+            c_have = false;
+            cs_slot = (cs_slot + 1 == RING) ? 0 : cs_slot + 1;
+            --queued;
+        }
+    }
+}
+
+// ================================================================== grid scheduler ===
+
+// One warp streams the partition [p0, p1) of nu query heads h_first + u*h_step of
+// sequence s, tile after tile with no break between heads: the copies of the next
+// head's first tiles are in flight while the current head finishes (its q row is
+// prefetched into registers one head ahead).  Block ids come from shared memory.
+template <typename T, int D>
+__device__ __forceinline__ void stream_heads(const AttnParams& p, int s, int part, int nparts, int p0, int p1,
+                                             int t_new, const int* sbt, int jb0, char* stage0, uint64_t* wbars,
+                                             int lane, int h_first, int h_step, int nu) {
+    using C = AttnCfg<T, D>;
+    constexpr int RB = C::RB, LT = C::LT, EPC = C::EPC;
     const int STG = p.STG;
     const int ntiles = p1 > p0 ? (p1 - p0 + kTile - 1) / kTile : 0;
-    const int kvh = h / p.G;
     const int g = lane / LT, c = lane % LT;
-    const uint4* qrow = reinterpret_cast<const uint4*>(static_cast<const char*>(p.query) +
-                                                        ((int64_t)s * p.H + h) * RB);
-    const uint4 q0 = __ldg(qrow + c), q1 = __ldg(qrow + c + LT);
-
     const char* kc = static_cast<const char*>(p.key_cache);
     const char* vc = static_cast<const char*>(p.value_cache);
     const int64_t blk_bytes = ((int64_t)p.H_kv << p.log2B) * RB;
-    const int64_t head_off = ((int64_t)kvh << p.log2B) * RB;
+    const int pc = t_new >= 0 ? t_new : p1;  // cache rows copied end before the new token
+    float m, l;
+    float2 acc[EPC];
 
-    // rows copied from the cache end at pc (the new token's row is supplied directly)
-    const int pc = t_new >= 0 ? t_new : p1;
-    uint4 nk0 = make_uint4(0, 0, 0, 0), nk1 = nk0, nv0 = nk0, nv1 = nk0;
-    if (t_new >= 0) {
-        const uint4* kr = reinterpret_cast<const uint4*>(static_cast<const char*>(p.new_key) +
-                                                          ((int64_t)s * p.H_kv + kvh) * RB);
-        const uint4* vr = reinterpret_cast<const uint4*>(static_cast<const char*>(p.new_value) +
-                                                          ((int64_t)s * p.H_kv + kvh) * RB);
-        nk0 = __ldg(kr + c);
-        nk1 = __ldg(kr + c + LT);
-        nv0 = __ldg(vr + c);
-        nv1 = __ldg(vr + c + LT);
-        if (g == 0 && h % p.G == 0) {  // the one writer of (s, kvh)
-            const int blk = sbt[(t_new >> p.log2B) - jb0];
-            const int64_t off = (int64_t)blk * blk_bytes + head_off + (int64_t)(t_new & ((1 << p.log2B) - 1)) * RB;
-            uint4* dk = reinterpret_cast<uint4*>(static_cast<char*>(p.key_cache_w) + off);
-            uint4* dv = reinterpret_cast<uint4*>(static_cast<char*>(p.value_cache_w) + off);
-            dk[c] = nk0;
-            dk[c + LT] = nk1;
-            dv[c] = nv0;
-            dv[c + LT] = nv1;
+    if (ntiles == 0) {  // empty context: zeros
+        if (g == 0)
+            for (int u = 0; u < nu; ++u)
+                store_out<T, D>(static_cast<T*>(p.out) + ((int64_t)s * p.H + h_first + u * h_step) * D, 0.f, acc, c);
+        return;
+    }
+    const int total = nu * ntiles;
+    // issue cursor (unit iu, tile ju)
+    int iu = 0, ju = 0;
+    auto issue_next = [&](int k) {
+        const int h = h_first + iu * h_step;
+        const int tok0 = p0 + ju * kTile;
+        issue_tile(stage0 + k * C::STAGE_BYTES, stage0 + k * C::STAGE_BYTES + kTile * RB, &wbars[k], kc, vc, sbt,
+                   jb0, tok0, max(0, min(kTile, pc - tok0)), pc, p.log2B, blk_bytes,
+                   ((int64_t)(h / p.G) << p.log2B) * RB, RB, lane);
+        if (++ju == ntiles) {
+            ju = 0;
+            ++iu;
         }
-    }
+    };
+    for (int i = 0; i < STG && i < total; ++i) issue_next(i);
 
-    for (int j = 0; j < STG && j < ntiles; ++j) {
-        const int tok0 = p0 + j * kTile;
-        issue_tile(stage0 + j * C::STAGE_BYTES, stage0 + j * C::STAGE_BYTES + kTile * RB, &wbars[j], kc, vc, sbt,
-                   jb0, tok0, max(0, min(kTile, pc - tok0)), pc, p.log2B, blk_bytes, head_off, RB, lane);
-    }
-
-    float m = -INFINITY, l = 0.f;
-#pragma unroll
-    for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
-
-    int k = 0;
+    auto qrow = [&](int h) {
+        return reinterpret_cast<const uint4*>(static_cast<const char*>(p.query) + ((int64_t)s * p.H + h) * RB);
+    };
+    uint4 qn0 = __ldg(qrow(h_first) + c), qn1 = __ldg(qrow(h_first) + c + LT);
+    uint4 q0 = qn0, q1 = qn1;
+    int k = 0, u = 0, j = 0, h = h_first;
     uint32_t phase = 0;
-    for (int j = 0; j < ntiles; ++j) {
+    for (int i = 0; i < total; ++i) {
+        if (j == 0) {  // a new head
+            h = h_first + u * h_step;
+            q0 = qn0;
+            q1 = qn1;
+            if (u + 1 < nu) {
+                const uint4* qr = qrow(h + h_step);
+                qn0 = __ldg(qr + c);
+                qn1 = __ldg(qr + c + LT);
+            }
+            m = -INFINITY;
+            l = 0.f;
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
+        }
         const int tok0 = p0 + j * kTile;
         const int nv = min(kTile, p1 - tok0);
-        const char* sK = stage0 + k * C::STAGE_BYTES;
-        const char* sV = sK + kTile * RB;
+        char* sK = stage0 + k * C::STAGE_BYTES;
+        char* sV = sK + kTile * RB;
         mbar_wait(&wbars[k], phase);
-        if (t_new >= tok0 && t_new < tok0 + kTile) {  // place the new token's row (last tile)
+        if (t_new >= tok0 && t_new < tok0 + kTile) {  // the new token's row (last tile)
+            const int kvh = h / p.G;
             if (g == 0) {
-                char* rk = const_cast<char*>(sK) + (t_new - tok0) * RB;
-                char* rv = const_cast<char*>(sV) + (t_new - tok0) * RB;
-                reinterpret_cast<uint4*>(rk)[c] = nk0;
-                reinterpret_cast<uint4*>(rk)[c + LT] = nk1;
-                reinterpret_cast<uint4*>(rv)[c] = nv0;
-                reinterpret_cast<uint4*>(rv)[c + LT] = nv1;
+                const uint4* kr = reinterpret_cast<const uint4*>(static_cast<const char*>(p.new_key) +
+                                                                  ((int64_t)s * p.H_kv + kvh) * RB);
+                const uint4* vr = reinterpret_cast<const uint4*>(static_cast<const char*>(p.new_value) +
+                                                                  ((int64_t)s * p.H_kv + kvh) * RB);
+                uint4* rk = reinterpret_cast<uint4*>(sK + (t_new - tok0) * RB);
+                uint4* rv = reinterpret_cast<uint4*>(sV + (t_new - tok0) * RB);
+                rk[c] = __ldg(kr + c);
+                rk[c + LT] = __ldg(kr + c + LT);
+                rv[c] = __ldg(vr + c);
+                rv[c + LT] = __ldg(vr + c + LT);
             }
             __syncwarp();
+            if (h % p.G == 0 && g == 0)
+                write_new_token<T, D>(p, sK + (t_new - tok0) * RB, sV + (t_new - tok0) * RB, s, kvh, t_new, c);
         }
-
-        float sc[TPL];
-#pragma unroll
-        for (int jj = 0; jj < TPL; ++jj) {
-            const char* row = sK + (jj * TG + g) * RB;
-            const uint4 k0 = lds128(row + c * 16), k1 = lds128(row + (c + LT) * 16);
-            float x = dot16<T>(q0, k0, 0.f) + dot16<T>(q1, k1, 0.f);
-#pragma unroll
-            for (int off = LT / 2; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-            sc[jj] = x * p.scale_log2;
-        }
-        if (nv < kTile) {
-#pragma unroll
-            for (int jj = 0; jj < TPL; ++jj)
-                if (jj * TG + g >= nv) sc[jj] = -INFINITY;
-        }
-        float mt = sc[0];
-#pragma unroll
-        for (int jj = 1; jj < TPL; ++jj) mt = fmaxf(mt, sc[jj]);
-        const float mn = fmaxf(m, mt);
-        const float ms = (mn == -INFINITY) ? 0.f : mn;
-        const float alpha = ex2(m - ms);
-        float ps[TPL], psum = 0.f;
-#pragma unroll
-        for (int jj = 0; jj < TPL; ++jj) {
-            ps[jj] = ex2(sc[jj] - ms);
-            psum += ps[jj];
-        }
-        l = l * alpha + psum;
-        const float2 aa = make_float2(alpha, alpha);
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) acc[e] = fmul2(acc[e], aa);
-        if (nv == kTile) {
-#pragma unroll
-            for (int jj = 0; jj < TPL; ++jj) {
-                const char* row = sV + (jj * TG + g) * RB;
-                const uint4 v0 = lds128(row + c * 16), v1 = lds128(row + (c + LT) * 16);
-                axpy16<T>(acc, ps[jj], v0);
-                axpy16<T>(acc + EPC / 2, ps[jj], v1);
-            }
-        } else {
-#pragma unroll
-            for (int jj = 0; jj < TPL; ++jj) {
-                if (jj * TG + g < nv) {  // rows past the context were never loaded
-                    const char* row = sV + (jj * TG + g) * RB;
-                    const uint4 v0 = lds128(row + c * 16), v1 = lds128(row + (c + LT) * 16);
-                    axpy16<T>(acc, ps[jj], v0);
-                    axpy16<T>(acc + EPC / 2, ps[jj], v1);
-                }
-            }
-        }
-        m = mn;
+        tile_update<T, D>(sK, sV, nv, q0, q1, p.scale_log2, g, c, m, l, acc);
         __syncwarp();
-        if (j + STG < ntiles) {
-            const int t2 = p0 + (j + STG) * kTile;
-            issue_tile(stage0 + k * C::STAGE_BYTES, stage0 + k * C::STAGE_BYTES + kTile * RB, &wbars[k], kc, vc, sbt,
-                       jb0, t2, max(0, min(kTile, pc - t2)), pc, p.log2B, blk_bytes, head_off, RB, lane);
-        }
+        if (i + STG < total) issue_next(k);
         if (++k == STG) {
             k = 0;
             phase ^= 1u;
         }
-    }
-
-    // merge the token groups of the warp (log-sum-exp, fixed order)
-#pragma unroll
-    for (int off = LT; off < 32; off <<= 1) {
-        const float mo = __shfl_xor_sync(0xffffffffu, m, off);
-        const float lo = __shfl_xor_sync(0xffffffffu, l, off);
-        const float mn = fmaxf(m, mo);
-        const float ms = (mn == -INFINITY) ? 0.f : mn;
-        const float a = ex2(m - ms), b = ex2(mo - ms);
-        l = l * a + lo * b;
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) {
-            const float ox = __shfl_xor_sync(0xffffffffu, acc[e].x, off);
-            const float oy = __shfl_xor_sync(0xffffffffu, acc[e].y, off);
-            acc[e] = make_float2(acc[e].x * a + ox * b, acc[e].y * a + oy * b);
+        if (++j == ntiles) {  // head finished
+            j = 0;
+            ++u;
+            merge_token_groups<T, D>(m, l, acc);
+            const int64_t sh = (int64_t)s * p.H + h;
+            if (nparts == 1) {
+                if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
+            } else {
+                finish_split<T, D>(p, sh, part, nparts, m, l, acc, g, c, lane);
+            }
         }
-        m = mn;
     }
-    m_out = m;
-    l_out = l;
 }
 
-// One CTA = (partition, group of HPC query heads, sequence); warp w owns query head
-// hg*HPC + w for the whole partition and keeps STG tiles in flight; warps do not
-// synchronise with each other between the prologue and the epilogue.
-//
-// Split-context epilogue (BJ:north_star): every partition writes its (m_p, L_p, o~_p);
-// the LAST partition CTA of the (sequence, head group) to finish -- detected with an
-// atomic counter in the workspace -- merges them in partition order:
-//   M = max m_p;  out = sum_p 2^(m_p - M) L_p o~_p / sum_p 2^(m_p - M) L_p
-// (the counters are zeroed on the stream right before the launch).
+// One CTA = (partition, group of HPC*HPW query heads, sequence).  Warp w streams heads
+// base + w, base + w + HPC, ... (HPW of them), so at any moment the CTA's warps read
+// neighbouring heads of the same blocks.
 template <typename T, int D>
-__global__ void __launch_bounds__(256)
-paged_attention_kernel(const AttnParams p) {
+__global__ void __launch_bounds__(256) paged_attention_kernel(const AttnParams p) {
     using C = AttnCfg<T, D>;
-    constexpr int LT = C::LT, EPC = C::EPC;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ int s_last;
 
     const int part = blockIdx.x, hg = blockIdx.y, s = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int HPC = p.HPC, STG = p.STG;
-    const int h = hg * HPC + warp;
-    const bool active = h < p.H;  // ragged last head group
-    pdl_wait();  // the step's copy_blocks / reshape_and_cache have landed
+    const int h_first = hg * HPC * p.HPW + warp;
+    const int nu = h_first < p.H ? min(p.HPW, (p.H - h_first + HPC - 1) / HPC) : 0;
+    pdl_wait();
     const int ctx = p.context_lens[s];
     const int p0 = part * p.PT;
     if (part > 0 && p0 >= ctx) return;  // this sequence has fewer partitions (CTA-uniform)
@@ -282,8 +725,6 @@ paged_attention_kernel(const AttnParams p) {
 
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)HPC * STG * C::STAGE_BYTES);
     int* sbt = reinterpret_cast<int*>(bars + HPC * STG);
-
-    // ---- prologue: block ids of this partition (shared by the CTA's heads), barriers -
     const int jb0 = p0 >> p.log2B;
     const int nb = p1 > p0 ? ((p1 - 1) >> p.log2B) - jb0 + 1 : 0;
     const int32_t* btrow = p.block_tables + (int64_t)s * p.W;
@@ -291,83 +732,148 @@ paged_attention_kernel(const AttnParams p) {
     if (threadIdx.x < HPC * STG) mbar_init(&bars[threadIdx.x], 1);
     fence_mbar_init();
     __syncthreads();
-
-    float m = -INFINITY, l = 0.f;
-    float2 acc[EPC];
+    if (nu == 0) return;
     const int t_new = (p.new_key != nullptr && ctx > 0 && p1 == ctx) ? ctx - 1 : -1;
-    if (active)
-        walk_partition<T, D>(p, s, h, p0, p1, t_new, sbt, jb0,
-                             reinterpret_cast<char*>(smem) + (size_t)warp * STG * C::STAGE_BYTES, bars + warp * STG,
-                             lane, m, l, acc);
-    pdl_launch_dependents();  // the next kernel may be scheduled during our last wave
-    const int g = lane / LT, c = lane % LT;
-    const int64_t sh = (int64_t)s * p.H + h;
+    stream_heads<T, D>(p, s, part, nparts, p0, p1, t_new, sbt, jb0,
+                       reinterpret_cast<char*>(smem) + (size_t)warp * STG * C::STAGE_BYTES, bars + warp * STG, lane,
+                       h_first, HPC, nu);
+}
 
-    if (nparts == 1) {  // whole context in this CTA: write the output directly
-        if (!active || g != 0) return;
-        T* o = static_cast<T*>(p.out) + sh * D;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            alignas(16) T v[EPC];
-#pragma unroll
-            for (int e = 0; e < EPC / 2; ++e) {
-                v[2 * e] = Elem<T>::from_f32(l > 0.f ? acc[half * EPC / 2 + e].x / l : 0.f);
-                v[2 * e + 1] = Elem<T>::from_f32(l > 0.f ? acc[half * EPC / 2 + e].y / l : 0.f);
+// ================================================================== coop scheduler ===
+//
+// One CTA = (partition, group of HPC query heads, sequence) with HPC consumer warps (one
+// query head each) and one producer warp.  A tile stage holds the K and V rows of the
+// group's NKV kv heads for 16 logical tokens: with block_size 16 the NKV head slabs of
+// a block are contiguous, so a full tile is ONE bulk copy of NKV*B*D*e bytes for K and
+// one for V (16 KB each for 4 fp16 heads of D=128).  Consumers wait on full[k], compute
+// their head, and release the stage with one arrive per warp on empty[k]; the producer
+// waits on empty[k] before refilling it.  The CTA's warps therefore stay in lockstep on
+// the same blocks (contiguous DRAM reads), and no consumer ever issues a copy.
+template <typename T, int D>
+__global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnParams p) {
+    using C = AttnCfg<T, D>;
+    constexpr int RB = C::RB, LT = C::LT, EPC = C::EPC;
+    extern __shared__ __align__(128) unsigned char smem[];
+
+    const int part = blockIdx.x, hg = blockIdx.y, s = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int HPC = p.HPC, STG = p.STG, G = p.G;
+    const int h0 = hg * HPC;
+    const int nh = min(HPC, p.H - h0);          // consumer warps with a head
+    const int kvh0 = h0 / G;
+    const int NKV = (h0 + nh - 1) / G - kvh0 + 1;  // kv heads the group reads
+    const int NKVmax = HPC % G == 0 ? HPC / G : (HPC + G - 1) / G + 1;  // stage layout stride (host-sized)
+    const int slab = kTile * RB;                   // one kv head x 16 rows
+    const int stage_bytes = 2 * NKVmax * slab;
+    pdl_wait();
+    const int ctx = p.context_lens[s];
+    const int p0 = part * p.PT;
+    if (part > 0 && p0 >= ctx) return;  // this sequence has fewer partitions (CTA-uniform)
+    const int p1 = min(ctx, p0 + p.PT);
+    const int nparts = ctx > 0 ? (ctx + p.PT - 1) / p.PT : 1;
+    const int ntiles = p1 > p0 ? (p1 - p0 + kTile - 1) / kTile : 0;
+    const int t_new = (p.new_key != nullptr && ctx > 0 && p1 == ctx) ? ctx - 1 : -1;
+    const int pc = t_new >= 0 ? t_new : p1;
+
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STG * stage_bytes);
+    uint64_t* empty = full + STG;
+    int* sbt = reinterpret_cast<int*>(empty + STG);
+    const int jb0 = p0 >> p.log2B;
+    const int nb = p1 > p0 ? ((p1 - 1) >> p.log2B) - jb0 + 1 : 0;
+    const int32_t* btrow = p.block_tables + (int64_t)s * p.W;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) sbt[i] = __ldg(btrow + jb0 + i);
+    if (threadIdx.x < STG) {
+        mbar_init(&full[threadIdx.x], 1);
+        mbar_init(&empty[threadIdx.x], nh);
+    }
+    fence_mbar_init();
+    __syncthreads();
+
+    if (warp == HPC) {  // ------------------------------------------------ producer warp
+        const int B = 1 << p.log2B;
+        const char* kc = static_cast<const char*>(p.key_cache);
+        const char* vc = static_cast<const char*>(p.value_cache);
+        const int64_t blk_bytes = ((int64_t)p.H_kv << p.log2B) * RB;
+        const int pieces = B >= kTile ? 1 : kTile / B;
+        for (int j = 0; j < ntiles; ++j) {
+            const int k = j % STG;
+            if (j >= STG) mbar_wait(&empty[k], ((j / STG) - 1) & 1);
+            char* sK = reinterpret_cast<char*>(smem) + (size_t)k * stage_bytes;
+            char* sV = sK + NKVmax * slab;
+            const int tok0 = p0 + j * kTile;
+            const int nvc = max(0, min(kTile, pc - tok0));
+            const bool has_new = t_new >= tok0 && t_new < tok0 + kTile;
+            if (lane == 0)
+                mbar_arrive_expect_tx(&full[k], (uint32_t)(2 * NKV * (nvc + (has_new ? 1 : 0)) * RB));
+            __syncwarp();
+            if (B >= kTile && nvc == kTile && B == kTile) {
+                // whole tile of the group = NKV contiguous head slabs of one block
+                if (lane == 0) {
+                    const int blk = sbt[(tok0 >> p.log2B) - jb0];
+                    const int64_t off = (int64_t)blk * blk_bytes + (int64_t)kvh0 * slab;
+                    bulk_g2s(sK, kc + off, (uint32_t)(NKV * slab), &full[k]);
+                    bulk_g2s(sV, vc + off, (uint32_t)(NKV * slab), &full[k]);
+                }
+            } else if (nvc > 0) {
+                for (int it = lane; it < NKV * pieces; it += 32) {
+                    const int kh = it / pieces, pi = it - kh * pieces;
+                    const int tk = tok0 + pi * min(B, kTile);
+                    if (tk >= pc) continue;
+                    const int blk = sbt[(tk >> p.log2B) - jb0];
+                    const int rows = min(min(B, kTile), pc - tk);
+                    const int64_t off = (int64_t)blk * blk_bytes + ((int64_t)(kvh0 + kh) << p.log2B) * RB +
+                                        (int64_t)(tk & (B - 1)) * RB;
+                    const int dst = kh * slab + (tk - tok0) * RB;
+                    bulk_g2s(sK + dst, kc + off, (uint32_t)(rows * RB), &full[k]);
+                    bulk_g2s(sV + dst, vc + off, (uint32_t)(rows * RB), &full[k]);
+                }
             }
-            *reinterpret_cast<uint4*>(o + (c + half * LT) * EPC) = *reinterpret_cast<const uint4*>(v);
+            if (has_new && lane < NKV) {  // the new token's rows come from the step's inputs
+                const int64_t src = ((int64_t)s * p.H_kv + kvh0 + lane) * RB;
+                const int dst = lane * slab + (t_new - tok0) * RB;
+                bulk_g2s(sK + dst, static_cast<const char*>(p.new_key) + src, RB, &full[k]);
+                bulk_g2s(sV + dst, static_cast<const char*>(p.new_value) + src, RB, &full[k]);
+            }
+            __syncwarp();
         }
         return;
     }
+    if (warp >= nh) return;  // ragged last head group
 
-    // ---- split: publish this partition's (m, L, o~) --------------------------------
-    if (active && g == 0) {
-        float* o = p.part_o + (sh * p.NP + part) * D;
+    // ------------------------------------------------------------------ consumer warps
+    const int h = h0 + warp;
+    const int kh = h / G - kvh0;
+    const int g = lane / LT, c = lane % LT;
+    const uint4* qrow = reinterpret_cast<const uint4*>(static_cast<const char*>(p.query) + ((int64_t)s * p.H + h) * RB);
+    const uint4 q0 = __ldg(qrow + c), q1 = __ldg(qrow + c + LT);
+    float m = -INFINITY, l = 0.f;
+    float2 acc[EPC];
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-#pragma unroll
-            for (int e = 0; e < EPC / 2; e += 2) {
-                const float2 a0 = acc[half * EPC / 2 + e], a1 = acc[half * EPC / 2 + e + 1];
-                *reinterpret_cast<float4*>(o + (c + half * LT) * EPC + 2 * e) =
-                    make_float4(a0.x / l, a0.y / l, a1.x / l, a1.y / l);
-            }
-        }
-        if (lane == 0) p.part_ml[sh * p.NP + part] = make_float2(m, l);
+    for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
+    for (int j = 0; j < ntiles; ++j) {
+        const int k = j % STG;
+        mbar_wait(&full[k], (j / STG) & 1);
+        const char* sK = reinterpret_cast<const char*>(smem) + (size_t)k * stage_bytes + kh * slab;
+        const char* sV = sK + NKVmax * slab;
+        const int tok0 = p0 + j * kTile;
+        if (t_new >= tok0 && t_new < tok0 + kTile && h % G == 0 && g == 0)
+            write_new_token<T, D>(p, sK + (t_new - tok0) * RB, sV + (t_new - tok0) * RB, s, h / G, t_new, c);
+        tile_update<T, D>(sK, sV, min(kTile, p1 - tok0), q0, q1, p.scale_log2, g, c, m, l, acc);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[k]);
     }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int* cnt = p.counters + (int64_t)s * gridDim.y + hg;
-        const int old = atomicAdd(cnt, 1);
-        s_last = (old == min(nparts, p.NP) - 1);
+    merge_token_groups<T, D>(m, l, acc);
+    const int64_t sh = (int64_t)s * p.H + h;
+    if (nparts == 1) {
+        if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
+    } else {
+        finish_split<T, D>(p, sh, part, nparts, m, l, acc, g, c, lane);
     }
-    __syncthreads();
-    if (!s_last || !active) return;
-    __threadfence();
-
-    // ---- last partition: merge all partitions of this head, in partition order -----
-    const int np = min(nparts, p.NP);
-    const float2* ml = p.part_ml + sh * p.NP;
-    float M = -INFINITY;
-    for (int i = 0; i < np; ++i) M = fmaxf(M, __ldcg(&ml[i]).x);
-    float L = 0.f;
-    constexpr int DPL = D / 32;  // dims per lane
-    float o[DPL];
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) o[e] = 0.f;
-    const float* po = p.part_o + sh * p.NP * D;
-    for (int i = 0; i < np; ++i) {
-        const float2 mi = __ldcg(&ml[i]);
-        const float w = mi.y * ex2(mi.x - M);
-        L += w;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) o[e] += w * __ldcg(po + (int64_t)i * D + lane * DPL + e);
-    }
-    T* out = static_cast<T*>(p.out) + sh * D + lane * DPL;
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) out[e] = Elem<T>::from_f32(o[e] / L);
 }
 
-// Test-only: copy the logical K/V rows of (s, kvh) through the same tile loader.
+// ==================================================================== debug gather ===
+
+// Test-only: copy the logical K/V rows of (s, kvh) through the grid scheduler's loader.
 template <typename T, int D>
 __global__ void __launch_bounds__(32) debug_gather_kernel(GatherParams p) {
     constexpr int RB = D * Elem<T>::kBytes;
@@ -410,43 +916,99 @@ __global__ void __launch_bounds__(32) debug_gather_kernel(GatherParams p) {
     }
 }
 
-// ---------------------------------------------------------------- host launchers -----
+// ================================================================== host launchers ===
 
-int attention_stage_bytes(int dtype, int head_dim) { return 2 * kTile * head_dim * (dtype == 0 ? 4 : 2); }
+int attention_row_bytes(int dtype, int head_dim) { return head_dim * (dtype == 0 ? 4 : 2); }
 
-size_t attention_smem_bytes(int stage_bytes, int hpc, int stg, int partition_tokens, int block_size) {
+size_t attention_smem_bytes_coop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size) {
+    const int nkv_max = hpc % G == 0 ? hpc / G : (hpc + G - 1) / G + 1;
     const size_t tbl = 4 * (size_t)(partition_tokens / block_size + 2);
-    return (size_t)hpc * stg * stage_bytes + 8 * (size_t)hpc * stg + tbl;
+    return (size_t)stg * 2 * nkv_max * kTile * (size_t)row_bytes + 16 * (size_t)stg + tbl;
+}
+
+size_t attention_smem_bytes(bool persistent, int row_bytes, int nw, int stg, int partition_tokens, int block_size) {
+    if (persistent) {
+        const size_t sb = 2 * kTile * (size_t)row_bytes + row_bytes;
+        return (size_t)nw * stg * sb + 8 * (size_t)nw * stg + 4 * 8 * (size_t)nw * (stg + 2);
+    }
+    const size_t tbl = 4 * (size_t)(partition_tokens / block_size + 2);
+    return (size_t)nw * stg * (2 * kTile * (size_t)row_bytes) + 8 * (size_t)nw * stg + tbl;
 }
 
 template <typename T, int D>
-static cudaError_t launch_attention_t(const AttnParams& p, int num_seqs, size_t smem, cudaStream_t stream) {
-    auto kern = paged_attention_kernel<T, D>;
-    static size_t configured = 0;  // per instantiation; only grows
+static cudaError_t launch_attention_t(const AttnParams& p, int num_seqs, int sched, size_t smem,
+                                      cudaStream_t stream) {
+    const bool persistent = sched == 1;
+    if (sched == 2) {  // coop: HPC consumer warps + 1 producer warp per CTA
+        auto kern = paged_attention_coop_kernel<T, D>;
+        static size_t configured = 0;
+        if (smem > configured) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            configured = smem;
+        }
+        if (p.NP > 1) {
+            cudaError_t e = cudaMemsetAsync(p.counters, 0, sizeof(int) * (size_t)num_seqs * p.H, stream);
+            if (e != cudaSuccess) return e;
+        }
+        const int groups = (p.H + p.HPC - 1) / p.HPC;
+        return launch_k(kern, dim3(p.NP, groups, num_seqs), dim3((p.HPC + 1) * 32), smem, stream, p);
+    }
+    if (!persistent) {
+        auto kern = paged_attention_kernel<T, D>;
+        static size_t configured = 0;
+        if (smem > configured) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            configured = smem;
+        }
+        if (p.NP > 1) {
+            cudaError_t e = cudaMemsetAsync(p.counters, 0, sizeof(int) * (size_t)num_seqs * p.H, stream);
+            if (e != cudaSuccess) return e;
+        }
+        const int groups = (p.H + p.HPC * p.HPW - 1) / (p.HPC * p.HPW);
+        return launch_k(kern, dim3(p.NP, groups, num_seqs), dim3(p.HPC * 32), smem, stream, p);
+    }
+    auto kern = paged_attention_persistent_kernel<T, D>;
+    static size_t configured = 0;
+    static int cached_blocks = 0, cached_smem = -1, cached_threads = -1;
     if (smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    const int groups = (p.H + p.HPC - 1) / p.HPC;
-    if (p.NP > 1) {
-        cudaError_t e = cudaMemsetAsync(p.counters, 0, sizeof(int) * (size_t)num_seqs * groups, stream);
+    const int threads = p.HPC * 32;
+    if ((int)smem != cached_smem || threads != cached_threads) {
+        int nb = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
         if (e != cudaSuccess) return e;
+        cached_blocks = nb > 0 ? nb : 1;
+        cached_smem = (int)smem;
+        cached_threads = threads;
     }
-    return launch_k(kern, dim3(p.NP, groups, num_seqs), dim3(p.HPC * 32), smem, stream, p);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t units = (int64_t)num_seqs * p.NP * p.H;
+    const int64_t warps_wanted = (units + 1) / 2;  // >= 2 units per warp on average
+    int64_t grid = (int64_t)cached_blocks * sms;
+    grid = std::min<int64_t>(grid, std::max<int64_t>(1, (warps_wanted + p.HPC - 1) / p.HPC));
+    cudaError_t e = launch_k(build_worklist_kernel, dim3(1), dim3(1024), 0, stream, p, num_seqs);
+    if (e != cudaSuccess) return e;
+    return launch_k(kern, dim3((unsigned)grid), dim3(threads), smem, stream, p);
 }
 
-cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, size_t smem,
+cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int sched, size_t smem,
                              cudaStream_t stream) {
     if (dtype == 0) {
-        return head_dim == 64 ? launch_attention_t<float, 64>(p, num_seqs, smem, stream)
-                              : launch_attention_t<float, 128>(p, num_seqs, smem, stream);
+        return head_dim == 64 ? launch_attention_t<float, 64>(p, num_seqs, sched, smem, stream)
+                              : launch_attention_t<float, 128>(p, num_seqs, sched, smem, stream);
     } else if (dtype == 1) {
-        return head_dim == 64 ? launch_attention_t<__half, 64>(p, num_seqs, smem, stream)
-                              : launch_attention_t<__half, 128>(p, num_seqs, smem, stream);
+        return head_dim == 64 ? launch_attention_t<__half, 64>(p, num_seqs, sched, smem, stream)
+                              : launch_attention_t<__half, 128>(p, num_seqs, sched, smem, stream);
     }
-    return head_dim == 64 ? launch_attention_t<__nv_bfloat16, 64>(p, num_seqs, smem, stream)
-                          : launch_attention_t<__nv_bfloat16, 128>(p, num_seqs, smem, stream);
+    return head_dim == 64 ? launch_attention_t<__nv_bfloat16, 64>(p, num_seqs, sched, smem, stream)
+                          : launch_attention_t<__nv_bfloat16, 128>(p, num_seqs, sched, smem, stream);
 }
 
 cudaError_t launch_debug_gather(const GatherParams& p, int dtype, int head_dim, int num_seqs, cudaStream_t stream) {

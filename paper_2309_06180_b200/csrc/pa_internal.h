@@ -22,14 +22,18 @@ struct AttnParams {
     void* value_cache_w;
     float2* part_ml;            // [S][H][NP] (m, L) in the exp2 domain (split only)
     float* part_o;              // [S][H][NP][D] normalised partial outputs (split only)
-    int* counters;              // [S][ceil(H/HPC)] partitions finished (split only; zero between calls)
+    int* counters;              // [S][H] partitions finished (split only; zeroed by each call)
+    int* work_counter;          // persistent scheduler: next work unit
+    int* n_items;               // persistent scheduler: (sequence, partition) units in the list
+    int4* items;                // persistent scheduler: units (s, part, ctx, 0), longest first
     float scale_log2;           // scale * log2(e)
     int log2B;                  // block_size = 1 << log2B
     int H, H_kv, G;             // query heads, kv heads, H / H_kv
     int W;                      // block table row stride
     int PT;                     // partition size in tokens (multiple of 16)
     int NP;                     // partitions in the grid = ceil(max_ctx / PT)
-    int HPC;                    // query heads per CTA (one warp each)
+    int HPC;                    // warps per CTA
+    int HPW;                    // grid scheduler: query heads streamed by each warp
     int STG;                    // tiles in flight per warp (shared-memory stages)
 };
 
@@ -81,9 +85,11 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
-int attention_stage_bytes(int dtype, int head_dim);
-size_t attention_smem_bytes(int stage_bytes, int hpc, int stg, int partition_tokens, int block_size);
-cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, size_t smem,
+int attention_row_bytes(int dtype, int head_dim);
+size_t attention_smem_bytes(bool persistent, int row_bytes, int nw, int stg, int partition_tokens, int block_size);
+size_t attention_smem_bytes_coop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size);
+// sched: 0 = grid, 1 = persistent, 2 = coop
+cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int sched, size_t smem,
                              cudaStream_t stream);
 cudaError_t launch_debug_gather(const GatherParams& p, int dtype, int head_dim, int num_seqs, cudaStream_t stream);
 cudaError_t launch_reshape_and_cache(const CacheWriteParams& p, cudaStream_t stream);

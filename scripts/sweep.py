@@ -17,10 +17,15 @@ import torch  # noqa: E402
 import paper_2309_06180_b200 as pa  # noqa: E402
 from synth import make_config, materialize_torch, tables_torch  # noqa: E402
 
-SHAPES = [(4, 3), (4, 2), (4, 4), (2, 4), (2, 6), (8, 2), (8, 3), (1, 8), (1, 4)]
-PTS = [256, 512, 1024]
+# (scheduler, warps per CTA, stages per warp, heads per warp)
+SHAPES = [("grid", 4, 2, 1), ("grid", 4, 2, 2), ("grid", 4, 2, 5), ("grid", 4, 3, 2), ("grid", 2, 2, 2),
+          ("persistent", 4, 2, 1)]
+PTS = [512]
 if os.environ.get("SWEEP_SHAPES"):
-    SHAPES = [tuple(int(v) for v in x.split(",")) for x in os.environ["SWEEP_SHAPES"].split(";")]
+    SHAPES = []
+    for x in os.environ["SWEEP_SHAPES"].split(";"):
+        f = x.split(",")
+        SHAPES.append((f[0], int(f[1]), int(f[2]), int(f[3])))
 if os.environ.get("SWEEP_PTS"):
     PTS = [int(x) for x in os.environ["SWEEP_PTS"].split(",")]
 
@@ -32,21 +37,23 @@ def main():
         tb = tables_torch(wl, "cuda")
         out = torch.empty_like(x["query"])
         kv = wl.logical_kv_bytes()
-        for (hpc, stg), pt in itertools.product(SHAPES, PTS):
-            os.environ["PA_HPC"], os.environ["PA_STG"] = str(hpc), str(stg)
+        for (sched, hpc, stg, hpw), pt in itertools.product(SHAPES, PTS):
+            os.environ["PA_SCHED"], os.environ["PA_HPC"], os.environ["PA_STG"] = sched, str(hpc), str(stg)
+            os.environ["PA_HPW"] = str(hpw)
             ws = torch.zeros(max(16, pa.paged_attention_workspace_size(wl.S, wl.H, wl.D, wl.max_context_len, pt)),
                              dtype=torch.uint8, device="cuda")
 
             def call():
-                pa.paged_attention(out, x["query"], x["key_cache"], x["value_cache"], tb["block_tables"],
-                                   tb["context_lens"], wl.scale, max_context_len=wl.max_context_len,
-                                   partition_tokens=pt, workspace=ws)
+                pa.paged_attention_decode(out, x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"],
+                                          tb["block_tables"], tb["context_lens"], wl.scale,
+                                          max_context_len=wl.max_context_len, workspace=ws)
             try:
                 for _ in range(5):
                     call()
                 torch.cuda.synchronize()
             except Exception as e:  # unsupported shape (smem)
-                print(json.dumps({"config": name, "hpc": hpc, "stg": stg, "pt": pt, "error": str(e)[:120]}))
+                print(json.dumps({"config": name, "sched": sched, "hpc": hpc, "stg": stg, "hpw": hpw, "pt": pt,
+                                  "error": str(e)[:120]}))
                 continue
             n = 50
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -56,10 +63,11 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / n * 1e3
-            print(json.dumps({"config": name, "hpc": hpc, "stg": stg, "pt": pt, "us": round(us, 2),
+            print(json.dumps({"config": name, "sched": sched, "hpc": hpc, "stg": stg, "hpw": hpw, "pt": pt,
+                              "us": round(us, 2),
                               "kv_GBps": round(kv / us / 1e3, 1)}), flush=True)
-        os.environ.pop("PA_HPC", None)
-        os.environ.pop("PA_STG", None)
+        for k in ("PA_HPC", "PA_STG", "PA_HPW", "PA_SCHED"):
+            os.environ.pop(k, None)
         del x
 
 

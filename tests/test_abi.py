@@ -79,13 +79,21 @@ def test_attention_zero_seqs_is_noop():
     assert attn(S=0, out=None) == OK
 
 
+def test_attention_requires_workspace():
+    assert attn() == WORKSPACE
+
+
 def test_workspace_size():
+    """Counters + work list always; split partials only when a context needs > 1 partition."""
     f = L.pa_paged_attention_workspace_size
-    assert f(4, 2, 64, 100, 0) == 0
-    assert f(4, 2, 64, 512, 0) == 0
+    assert 0 < f(4, 2, 64, 100, 0) < 1024
+    assert f(4, 2, 64, 512, 0) == f(4, 2, 64, 100, 0)
     S, H, D = 256, 40, 128
-    assert f(S, H, D, 2048, 0) == S * H * 4 + S * H * 4 * (D * 4 + 8)
-    assert f(S, H, D, 2048, 4096) == 0
+    single = f(S, H, D, 512, 0)
+    split = f(S, H, D, 2048, 0)
+    assert split - single >= S * H * 4 * (D * 4 + 8)        # 4 partitions of o~ and (m, L)
+    assert split - single < S * H * 4 * (D * 4 + 8) + S * 4 * 16 + 64
+    assert f(S, H, D, 2048, 4096) == single
 
 
 def test_cache_kernels_argument_validation():
