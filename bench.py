@@ -188,6 +188,7 @@ def run_ours(a, wl_full, world, rank, local):
     import torch.distributed as dist
 
     import paper_2309_06180_b200 as pa
+    from paper_2309_06180_b200.tp import gather_heads
     from synth import materialize_torch, shard, tables_torch
 
     dev = torch.device("cuda", local)
@@ -201,7 +202,7 @@ def run_ours(a, wl_full, world, rank, local):
     mcl = wl.max_context_len
     ws_n = pa.paged_attention_workspace_size(wl.S, wl.H, wl.D, mcl, a.partition_tokens)
     ws = torch.zeros(max(ws_n, 16), dtype=torch.uint8, device=dev)
-    gathered = torch.empty((world, wl.S, wl.H, wl.D), dtype=q.dtype, device=dev) if world > 1 else None
+    gathered = torch.empty((world * wl.S, wl.H, wl.D), dtype=q.dtype, device=dev) if world > 1 else None
     full_out = torch.empty((wl.S, wl.H * world, wl.D), dtype=q.dtype, device=dev) if world > 1 else None
     has_pairs = len(wl.block_mapping) > 0
     stream = torch.cuda.current_stream(dev)
@@ -222,9 +223,8 @@ def run_ours(a, wl_full, world, rank, local):
             pa.paged_attention_decode(out, q, kn, vn, kc, vc, bt, cl, wl.scale, max_context_len=mcl, workspace=ws)
         if i is not None:
             ev_a1[i].record(stream)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, out)
-            full_out.copy_(gathered.permute(1, 0, 2, 3).reshape(wl.S, world * wl.H, wl.D))
+        if world > 1:  # the one exchange: all-gather of the output head slices (NCCL / NVLink)
+            full_out.copy_(gather_heads(out, buffer=gathered))
 
     for _ in range(max(3, a.warmup)):
         step()
