@@ -257,6 +257,7 @@ def run_ours(a, wl_full, world, rank, local):
     if not a.no_e2e:
         e2e = run_e2e(a, wl, world, dev, {"query": q, "key": kn, "value": vn}, kc, vc, mcl, ws, stream)
 
+    probe = read_probe(dev)
     if rank != 0:
         return
     peak, peak_src = load_peaks()
@@ -287,6 +288,7 @@ def run_ours(a, wl_full, world, rank, local):
                      "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes_per_launch": attn_bytes,
                      "avg_launch_ms": attn_ms},
+        "read_probe_gbs": probe,
         "clocks": clk.summary(),
         "gpu_launches": launches,
     }
@@ -295,6 +297,23 @@ def run_ours(a, wl_full, world, rank, local):
     if not a.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(wl_full)
     print(json.dumps(line), flush=True)
+
+
+def read_probe(dev, gib: float = 4.0):
+    """Same-run read-only HBM probe: torch's sum over a 4 GiB fp16 buffer, best of 5
+    (context for the copy-based MEASURED_PEAKS number; never the roofline peak)."""
+    import torch
+    x = torch.ones(int(gib * (1 << 30)) // 2, dtype=torch.float16, device=dev)
+    best = 0.0
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        x.sum(dtype=torch.float32)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, x.numel() * 2 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del x
+    return round(best, 1)
 
 
 def run_e2e(a, wl, world, dev, x, kc, vc, mcl, ws, stream):

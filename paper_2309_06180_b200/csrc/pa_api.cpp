@@ -169,6 +169,7 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     int sched = 2;  // coop
     if (sched_env && std::strcmp(sched_env, "grid") == 0) sched = 0;
     if (sched_env && std::strcmp(sched_env, "persistent") == 0) sched = 1;
+    if (sched_env && std::strcmp(sched_env, "pcoop") == 0) sched = 3;
     const bool persistent = sched == 1;
     const int rb = pa::attention_row_bytes((int)dtype, head_dim);
     const int G = num_heads / num_kv_heads;
@@ -180,12 +181,13 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     if (const char* ev = getenv("PA_HPC")) nw = atoi(ev) > 0 ? atoi(ev) : nw;
     if (nw > 8) nw = 8;
     const int nkv_max = nw % G == 0 ? nw / G : (nw + G - 1) / G + 1;
-    const int stage = sched == 2 ? 2 * nkv_max * 16 * rb : 2 * 16 * rb;
-    int stg = sched == 2 ? (64 * 1024) / stage : (64 * 1024) / (nw * stage);
+    const int stage = sched >= 2 ? 2 * nkv_max * 16 * rb : 2 * 16 * rb;
+    int stg = sched >= 2 ? (64 * 1024) / stage : (64 * 1024) / (nw * stage);
     stg = stg < 2 ? 2 : (stg > 8 ? 8 : stg);
     if (const char* ev = getenv("PA_STG")) stg = atoi(ev) > 0 ? atoi(ev) : stg;
-    const size_t smem = sched == 2 ? pa::attention_smem_bytes_coop(rb, nw, G, stg, PT, block_size)
-                                   : pa::attention_smem_bytes(persistent, rb, nw, stg, PT, block_size);
+    const size_t smem = sched == 2   ? pa::attention_smem_bytes_coop(rb, nw, G, stg, PT, block_size)
+                        : sched == 3 ? pa::attention_smem_bytes_pcoop(rb, nw, G, stg, PT, block_size)
+                                     : pa::attention_smem_bytes(persistent, rb, nw, stg, PT, block_size);
     if (smem > 227 * 1024)
         return fail(PA_ERR_UNSUPPORTED, "partition_tokens %d with block_size %d needs %zu B of shared memory", PT,
                     block_size, smem);

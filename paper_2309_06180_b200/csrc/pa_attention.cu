@@ -788,6 +788,7 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
     }
     fence_mbar_init();
     __syncthreads();
+    pdl_launch_dependents();  // the next kernel may become resident during our last wave
 
     if (warp == HPC) {  // ------------------------------------------------ producer warp
         const int B = 1 << p.log2B;
@@ -871,6 +872,217 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
     }
 }
 
+// ======================================================= persistent coop scheduler ===
+//
+// The coop CTA made persistent: a grid of occupancy x SMs CTAs, each with one producer
+// warp and HPC consumer warps, walks the longest-first work list of (sequence,
+// partition, head group) items (build_worklist_kernel).  The producer claims items with
+// one atomic each (the next claim is in flight while the current item's tiles are
+// issued), prefetches the item's block ids, and streams its tiles into the shared
+// stages; each stage carries the item descriptor and, for an item's first tile, the
+// group's q rows, so consumers never touch global memory before computing.  Consumers
+// see one continuous stream of tiles across items -- no CTA prologue or epilogue
+// bubbles -- and the list order makes the tail the shortest items.
+struct StageMeta {
+    int s, h0, nh, part, p0, p1, t_new, nparts, j, ntiles, kvh0, pad[5];
+};
+
+template <typename T, int D>
+__global__ void __launch_bounds__(288) paged_attention_pcoop_kernel(const AttnParams p) {
+    using C = AttnCfg<T, D>;
+    constexpr int RB = C::RB, LT = C::LT, EPC = C::EPC;
+    extern __shared__ __align__(128) unsigned char smem[];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int HPC = p.HPC, STG = p.STG, G = p.G, H = p.H, PT = p.PT;
+    const int NKVmax = HPC % G == 0 ? HPC / G : (HPC + G - 1) / G + 1;
+    const int slab = kTile * RB;
+    const int kv_bytes = 2 * NKVmax * slab;
+    const int stage_bytes = (kv_bytes + HPC * RB + (int)sizeof(StageMeta) + 127) / 128 * 128;  // K | V | q | meta
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STG * stage_bytes);
+    uint64_t* empty = full + STG;
+    int* sbt = reinterpret_cast<int*>(empty + STG);
+    if (threadIdx.x < STG) {
+        mbar_init(&full[threadIdx.x], 1);
+        mbar_init(&empty[threadIdx.x], HPC);
+    }
+    fence_mbar_init();
+    __syncthreads();
+    pdl_wait();  // work list and counters built, this step's copy_blocks done
+
+    auto stage_ptr = [&](int k) { return reinterpret_cast<char*>(smem) + (size_t)k * stage_bytes; };
+    auto meta_ptr = [&](int k) { return reinterpret_cast<StageMeta*>(stage_ptr(k) + kv_bytes + HPC * RB); };
+    const int NG = (H + HPC - 1) / HPC;
+
+    if (warp == HPC) {  // ================================================ producer warp
+        const int total = __ldcg(p.n_items) * NG;
+        const int B = 1 << p.log2B;
+        const char* kc = static_cast<const char*>(p.key_cache);
+        const char* vc = static_cast<const char*>(p.value_cache);
+        const int64_t blk_bytes = ((int64_t)p.H_kv << p.log2B) * RB;
+        const int pieces = B >= kTile ? 1 : kTile / B;
+        int k = 0, uses = 0;  // stage cursor, stages issued so far
+        auto next_stage = [&](uint64_t*& fb) -> char* {
+            if (uses >= STG) mbar_wait(&empty[k], ((uses / STG) - 1) & 1);
+            fb = &full[k];
+            return stage_ptr(k);
+        };
+        auto advance = [&]() {
+            ++uses;
+            if (++k == STG) k = 0;
+        };
+        // Item pipeline: while item `cur` is being issued, the descriptor and block ids
+        // of the next item are fetched (right after cur's first tile is queued) and
+        // the claim of the one after is in flight.  sbt is double-buffered.
+        const int tbl = PT / B + 2;
+        auto fetch = [&](int g, int buf, int4& d) {  // descriptor + block ids of item g
+            d = __ldcg(&p.items[g / NG]);
+            const int p0 = d.y * PT, p1 = min(d.z, p0 + PT);
+            const int jb0 = p0 >> p.log2B;
+            const int nb = p1 > p0 ? ((p1 - 1) >> p.log2B) - jb0 + 1 : 0;
+            const int32_t* btrow = p.block_tables + (int64_t)d.x * p.W;
+            for (int i = lane; i < nb; i += 32) sbt[buf * tbl + i] = __ldg(btrow + jb0 + i);
+            __syncwarp();
+        };
+        int gi = 0, gn = 0, buf = 0;
+        if (lane == 0) gi = atom_add_global(p.work_counter, 1);
+        gi = __shfl_sync(0xffffffffu, gi, 0);
+        int4 it = make_int4(-1, 0, 0, 0);
+        if (gi < total) fetch(gi, 0, it);
+        if (lane == 0) gn = atom_add_global(p.work_counter, 1);  // in flight
+        while (gi < total) {
+            const int hg = gi - (gi / NG) * NG;
+            const int s = it.x, part = it.y, ctx = it.z;
+            const int p0 = part * PT, p1 = min(ctx, p0 + PT);
+            const int ntiles = p1 > p0 ? (p1 - p0 + kTile - 1) / kTile : 0;
+            const int nparts = ctx > 0 ? (ctx + PT - 1) / PT : 1;
+            const int t_new = (p.new_key != nullptr && ctx > 0 && p1 == ctx) ? ctx - 1 : -1;
+            const int pc = t_new >= 0 ? t_new : p1;
+            const int h0 = hg * HPC, nh = min(HPC, H - h0);
+            const int kvh0 = h0 / G, NKV = (h0 + nh - 1) / G - kvh0 + 1;
+            const int jb0 = p0 >> p.log2B;
+            const int* cbt = sbt + buf * tbl;
+            StageMeta meta{s, h0, nh, part, p0, p1, t_new, nparts, 0, ntiles, kvh0, {0, 0, 0, 0, 0}};
+            int gnext = total;
+            int4 itn = make_int4(-1, 0, 0, 0);
+            for (int j = 0; j < max(ntiles, 1); ++j) {  // an empty context still posts one stage
+                uint64_t* fb;
+                char* sK = next_stage(fb);
+                char* sV = sK + NKVmax * slab;
+                char* sQ = sK + kv_bytes;
+                const int tok0 = p0 + j * kTile;
+                const int nvc = ntiles ? max(0, min(kTile, pc - tok0)) : 0;
+                const bool has_new = ntiles && t_new >= tok0 && t_new < tok0 + kTile;
+                if (lane == 0) {
+                    meta.j = j;
+                    *meta_ptr(k) = meta;
+                    mbar_arrive_expect_tx(fb, (uint32_t)(2 * NKV * (nvc + (has_new ? 1 : 0)) * RB +
+                                                         (j == 0 && ntiles ? nh * RB : 0)));
+                }
+                __syncwarp();
+                if (j == 0 && ntiles && lane < nh)
+                    bulk_g2s(sQ + lane * RB, static_cast<const char*>(p.query) + ((int64_t)s * H + h0 + lane) * RB, RB,
+                             fb);
+                if (B == kTile && nvc == kTile) {
+                    if (lane == 0) {
+                        const int64_t off = (int64_t)cbt[(tok0 >> p.log2B) - jb0] * blk_bytes + (int64_t)kvh0 * slab;
+                        bulk_g2s(sK, kc + off, (uint32_t)(NKV * slab), fb);
+                        bulk_g2s(sV, vc + off, (uint32_t)(NKV * slab), fb);
+                    }
+                } else if (nvc > 0) {
+                    for (int w = lane; w < NKV * pieces; w += 32) {
+                        const int kh = w / pieces, pi = w - kh * pieces;
+                        const int tk = tok0 + pi * min(B, kTile);
+                        if (tk >= pc) continue;
+                        const int rows = min(min(B, kTile), pc - tk);
+                        const int64_t off = (int64_t)cbt[(tk >> p.log2B) - jb0] * blk_bytes +
+                                            ((int64_t)(kvh0 + kh) << p.log2B) * RB + (int64_t)(tk & (B - 1)) * RB;
+                        const int dst = kh * slab + (tk - tok0) * RB;
+                        bulk_g2s(sK + dst, kc + off, (uint32_t)(rows * RB), fb);
+                        bulk_g2s(sV + dst, vc + off, (uint32_t)(rows * RB), fb);
+                    }
+                }
+                if (has_new && lane < NKV) {
+                    const int64_t src = ((int64_t)s * p.H_kv + kvh0 + lane) * RB;
+                    const int dst = lane * slab + (t_new - tok0) * RB;
+                    bulk_g2s(sK + dst, static_cast<const char*>(p.new_key) + src, RB, fb);
+                    bulk_g2s(sV + dst, static_cast<const char*>(p.new_value) + src, RB, fb);
+                }
+                __syncwarp();
+                advance();
+                if (j == 0) {  // the first tile is queued: fetch the next item meanwhile
+                    gnext = __shfl_sync(0xffffffffu, gn, 0);
+                    if (gnext < total) fetch(gnext, buf ^ 1, itn);
+                    if (lane == 0) gn = atom_add_global(p.work_counter, 1);
+                }
+            }
+            gi = gnext;
+            it = itn;
+            buf ^= 1;
+        }
+        // termination marker for the consumers
+        uint64_t* fb;
+        next_stage(fb);
+        if (lane == 0) {
+            meta_ptr(k)->s = -1;
+            mbar_arrive_expect_tx(fb, 0);
+        }
+        return;
+    }
+
+    // ============================================================== consumer warps
+    const int g = lane / LT, c = lane % LT;
+    int k = 0;
+    uint32_t phase = 0;
+    float m = -INFINITY, l = 0.f;
+    float2 acc[EPC];
+    uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
+    while (true) {
+        mbar_wait(&full[k], phase);
+        const StageMeta* mp = meta_ptr(k);
+        const int s = mp->s;
+        if (s < 0) break;
+        const int nh = mp->nh, j = mp->j, ntiles = mp->ntiles;
+        const bool active = warp < nh;
+        const int h = mp->h0 + warp;
+        const char* sK = stage_ptr(k) + (h / G - mp->kvh0) * slab;
+        const char* sV = sK + NKVmax * slab;
+        if (j == 0) {
+            m = -INFINITY;
+            l = 0.f;
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
+            if (active && ntiles) {
+                const char* sQ = stage_ptr(k) + kv_bytes + warp * RB;
+                q0 = lds128(sQ + c * 16);
+                q1 = lds128(sQ + (c + LT) * 16);
+            }
+        }
+        const int p0 = mp->p0, p1 = mp->p1, t_new = mp->t_new, part = mp->part, nparts = mp->nparts;
+        if (active && ntiles) {
+            const int tok0 = p0 + j * kTile;
+            if (t_new >= tok0 && t_new < tok0 + kTile && h % G == 0 && g == 0)
+                write_new_token<T, D>(p, sK + (t_new - tok0) * RB, sV + (t_new - tok0) * RB, s, h / G, t_new, c);
+            tile_update<T, D>(sK, sV, min(kTile, p1 - tok0), q0, q1, p.scale_log2, g, c, m, l, acc);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[k]);
+        if (++k == STG) {
+            k = 0;
+            phase ^= 1u;
+        }
+        if (active && j >= ntiles - 1) {  // last tile of the item (or an empty context)
+            merge_token_groups<T, D>(m, l, acc);
+            const int64_t sh = (int64_t)s * H + h;
+            if (nparts == 1) {
+                if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
+            } else {
+                finish_split<T, D>(p, sh, part, nparts, m, l, acc, g, c, lane);
+            }
+        }
+    }
+}
+
 // ==================================================================== debug gather ===
 
 // Test-only: copy the logical K/V rows of (s, kvh) through the grid scheduler's loader.
@@ -926,6 +1138,14 @@ size_t attention_smem_bytes_coop(int row_bytes, int hpc, int G, int stg, int par
     return (size_t)stg * 2 * nkv_max * kTile * (size_t)row_bytes + 16 * (size_t)stg + tbl;
 }
 
+size_t attention_smem_bytes_pcoop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size) {
+    const int nkv_max = hpc % G == 0 ? hpc / G : (hpc + G - 1) / G + 1;
+    const size_t stage = (2 * nkv_max * kTile * (size_t)row_bytes + (size_t)hpc * row_bytes + sizeof(StageMeta) + 127) /
+                         128 * 128;
+    const size_t tbl = 2 * 4 * (size_t)(partition_tokens / block_size + 2);  // double-buffered block ids
+    return (size_t)stg * stage + 16 * (size_t)stg + tbl;
+}
+
 size_t attention_smem_bytes(bool persistent, int row_bytes, int nw, int stg, int partition_tokens, int block_size) {
     if (persistent) {
         const size_t sb = 2 * kTile * (size_t)row_bytes + row_bytes;
@@ -939,6 +1159,33 @@ template <typename T, int D>
 static cudaError_t launch_attention_t(const AttnParams& p, int num_seqs, int sched, size_t smem,
                                       cudaStream_t stream) {
     const bool persistent = sched == 1;
+    if (sched == 3) {  // persistent coop
+        auto kern = paged_attention_pcoop_kernel<T, D>;
+        static size_t configured = 0;
+        static int cached_blocks = 0, cached_smem = -1, cached_threads = -1;
+        if (smem > configured) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            configured = smem;
+        }
+        const int threads = (p.HPC + 1) * 32;
+        if ((int)smem != cached_smem || threads != cached_threads) {
+            int nb = 0;
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
+            if (e != cudaSuccess) return e;
+            cached_blocks = nb > 0 ? nb : 1;
+            cached_smem = (int)smem;
+            cached_threads = threads;
+        }
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t items = (int64_t)num_seqs * p.NP * ((p.H + p.HPC - 1) / p.HPC);
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)cached_blocks * sms, items));
+        cudaError_t e = launch_k(build_worklist_kernel, dim3(1), dim3(1024), 0, stream, p, num_seqs);
+        if (e != cudaSuccess) return e;
+        return launch_k(kern, dim3((unsigned)grid), dim3(threads), smem, stream, p);
+    }
     if (sched == 2) {  // coop: HPC consumer warps + 1 producer warp per CTA
         auto kern = paged_attention_coop_kernel<T, D>;
         static size_t configured = 0;
