@@ -125,6 +125,8 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PA_BENCH_SAME_DEVICE") == "1":  # test only: every rank on cuda:0 (gloo)
+        local = 0
     return world, rank, local
 
 
@@ -398,7 +400,11 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("PA_BENCH_BACKEND", "nccl")  # gloo: multi-rank test on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(a, wl, world, rank, local)
     finally:

@@ -383,3 +383,22 @@ def test_fused_decode_gqa():
     ref, rkc, rvc = oracle_step(wl)
     assert np.array_equal(bits(kc), rkc) and np.array_equal(bits(vc), rvc)
     assert max_abs(out, ref) <= TOL[wl.dtype]
+
+
+@pytest.mark.parametrize("name", ["c2_sharegpt", "c3_fork", "c4_long"])
+def test_schedulers_bitwise_identical(name, monkeypatch):
+    """coop (default), grid, persistent and pcoop run the same per-(sequence, head) tile
+    arithmetic in the same order, so their outputs and cache writes are bit-identical;
+    a stage-reuse race in any pipeline would break this (full-size c2/c4, repeated)."""
+    wl = make_config(name)
+    x = materialize_torch(wl, "cuda")
+    ref = None
+    for sched in ("coop", "grid", "persistent", "pcoop", "coop"):
+        monkeypatch.setenv("PA_SCHED", sched)
+        out, kc, vc, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()}, fused=True)
+        if ref is None:
+            ref = (out, kc, vc)
+        else:
+            assert torch.equal(out, ref[0]), sched
+            assert torch.equal(kc.view(torch.int16), ref[1].view(torch.int16)), sched
+            assert torch.equal(vc.view(torch.int16), ref[2].view(torch.int16)), sched
