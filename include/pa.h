@@ -144,6 +144,33 @@ pa_status_t pa_copy_blocks(void* const* key_caches, void* const* value_caches, i
                            int block_size, int head_dim, pa_dtype_t dtype, pa_stream_t stream);
 
 /* ------------------------------------------------------------------------------------
+ * pa_swap_blocks -- block transfers between two block pools: swapping evicted KV blocks
+ * to CPU memory and back.  For every layer l < num_layers
+ * and pair p = (src, dst): dst_key_caches[l][dst] <- src_key_caches[l][src] and the same
+ * for values, whole blocks (num_kv_heads*block_size*head_dim elements), in ONE launch.
+ * Each cache pointer may be device memory or pinned, mapped host memory (cudaHostAlloc /
+ * torch pin_memory; with unified addressing the GPU reads and writes it over the host
+ * link directly), so a GPU->CPU swap-out and a CPU->GPU swap-in are both one kernel
+ * instead of one cudaMemcpyAsync per block (the small-transfer penalty of P:708-710).
+ * The four cache arrays are HOST arrays of num_layers pointers.  block_mapping:
+ * int64 [num_pairs][2], device or mapped host memory.  dst ids distinct; a pool is
+ * never both source and destination of one call.  num_pairs == 0 is a no-op.
+ * ---------------------------------------------------------------------------------- */
+pa_status_t pa_swap_blocks(void* const* dst_key_caches, void* const* dst_value_caches,
+                           const void* const* src_key_caches, const void* const* src_value_caches,
+                           int num_layers, const int64_t* block_mapping, int num_pairs,
+                           int num_kv_heads, int block_size, int head_dim, pa_dtype_t dtype,
+                           pa_stream_t stream);
+/* Benchmark baseline only: the same transfer as one cudaMemcpyAsync per (pair, layer,
+ * K/V) -- what a per-block swap costs (Fig.19 analogue, scripts/swap_bench.py). */
+pa_status_t pa_swap_blocks_memcpy(void* const* dst_key_caches, void* const* dst_value_caches,
+                                  const void* const* src_key_caches,
+                                  const void* const* src_value_caches, int num_layers,
+                                  const int64_t* host_block_mapping, int num_pairs,
+                                  int num_kv_heads, int block_size, int head_dim,
+                                  pa_dtype_t dtype, pa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
  * pa_decode_step -- one decode step of one attention layer from HOST inputs: the
  * end-to-end call of bench.py's "e2e" number.  Stream-ordered:
  *   H2D  query/key/value/block_tables/context_lens/block_mapping

@@ -16,6 +16,7 @@ Functions and the passage they follow (P:N = PAPER.md line N):
 - ``split_attention``       per-partition (m, L, o~) + log-sum-exp merge (BJ:north_star).
 - ``reshape_and_cache``     fused reshape + block write.
 - ``copy_blocks``           fused block copy for copy-on-write.
+- ``swap_blocks``           block transfers between the GPU pool and the CPU swap pool.
 - ``decode``                storage dtype -> fp64, bit-exact (own fp16/bf16 decoders).
 
 Parity pins: see tests/test_oracle.py; a function without a pin would be marked
@@ -64,6 +65,7 @@ def lib():
         L.oracle_gather_kv_bits.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32]
         L.oracle_reshape_and_cache.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32]
         L.oracle_copy_blocks.argtypes = [vp, vp, i32, vp, i32, i32, i32, i32, i32, i32]
+        L.oracle_swap_blocks.argtypes = [vp, vp, vp, vp, i32, vp, i32, i64]
         _lib = L
     return _lib
 
@@ -185,3 +187,17 @@ def copy_blocks(key_caches, value_caches, block_mapping, dtype):
     lib().oracle_copy_blocks(kp, vp, L, _p(bm), int(bm.shape[0]), int(H_kv), int(B), int(D), int(NB),
                              _dt(dtype))
     return kcs, vcs
+
+
+def swap_blocks(dst_key, dst_value, src_key, src_value, block_mapping):
+    """Lists (one per layer) of pools: returns new dst lists with dst[d] <- src[s] per pair."""
+    dk = [np.array(x, copy=True) for x in dst_key]
+    dv = [np.array(x, copy=True) for x in dst_value]
+    sk = [np.ascontiguousarray(x) for x in src_key]
+    sv = [np.ascontiguousarray(x) for x in src_value]
+    bm = np.ascontiguousarray(np.asarray(block_mapping, dtype=np.int64).reshape(-1, 2))
+    L = len(dk)
+    block_bytes = dk[0][0].nbytes
+    arr = lambda xs: (ctypes.c_void_p * L)(*[x.ctypes.data for x in xs])  # noqa: E731
+    lib().oracle_swap_blocks(arr(dk), arr(dv), arr(sk), arr(sv), L, _p(bm), int(bm.shape[0]), int(block_bytes))
+    return dk, dv

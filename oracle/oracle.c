@@ -14,6 +14,7 @@
  *                     the block table; blocks need not be contiguous.
  *   P:418-419         fused reshape + block write  -> oracle_reshape_and_cache
  *   P:424-427         fused block copy (CoW) -> oracle_copy_blocks
+ *   P:363-366         swapping blocks to the CPU pool and back -> oracle_swap_blocks
  *
  * Readings of the paper: the caller passes `scale` (c1); the
  * Eq.4 denominator is the sum of element-wise exponentials (c2); only t < ctx is read
@@ -348,4 +349,21 @@ void oracle_copy_blocks(void** key_caches, void** value_caches, int num_layers,
         }
     }
     free(snap);
+}
+
+/* ---- swapping between block pools -------------------------------------- */
+
+/* For every layer l and pair (src, dst): dst_cache_l[dst] <- src_cache_l[src] (whole
+ * blocks of block_bytes), for K and V.  The two pools are distinct arrays (GPU pool and
+ * CPU swap pool), so there is no aliasing between sources and destinations. */
+void oracle_swap_blocks(void** dst_key, void** dst_value, void** src_key, void** src_value, int num_layers,
+                        const int64_t* block_mapping, int num_pairs, int64_t block_bytes) {
+    for (int l = 0; l < num_layers; ++l)
+        for (int p = 0; p < num_pairs; ++p) {
+            int64_t src = block_mapping[2 * p], dst = block_mapping[2 * p + 1];
+            memcpy((char*)dst_key[l] + dst * block_bytes, (const char*)src_key[l] + src * block_bytes,
+                   (size_t)block_bytes);
+            memcpy((char*)dst_value[l] + dst * block_bytes, (const char*)src_value[l] + src * block_bytes,
+                   (size_t)block_bytes);
+        }
 }

@@ -322,6 +322,70 @@ pa_status_t pa_copy_blocks(void* const* key_caches, void* const* value_caches, i
     return PA_OK;
 }
 
+pa_status_t pa_swap_blocks(void* const* dst_key_caches, void* const* dst_value_caches,
+                           const void* const* src_key_caches, const void* const* src_value_caches, int num_layers,
+                           const int64_t* block_mapping, int num_pairs, int num_kv_heads, int block_size,
+                           int head_dim, pa_dtype_t dtype, pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
+    REQUIRE(num_layers >= 1 && num_layers <= pa::kMaxLayers, "num_layers must be in [1, %d]", pa::kMaxLayers);
+    REQUIRE(num_pairs >= 0, "num_pairs must be >= 0");
+    REQUIRE(num_kv_heads > 0, "num_kv_heads must be positive");
+    if (head_dim != 64 && head_dim != 128)
+        return fail(PA_ERR_UNSUPPORTED, "head_dim must be 64 or 128 (got %d)", head_dim);
+    if (log2_pow2(block_size) < 0)
+        return fail(PA_ERR_UNSUPPORTED, "block_size must be a power of two in [1,256] (got %d)", block_size);
+    REQUIRE(dst_key_caches && dst_value_caches && src_key_caches && src_value_caches,
+            "cache pointer arrays are NULL");
+    if (num_pairs == 0) return PA_OK;
+    REQUIRE_PTR(block_mapping, 8);
+    static thread_local pa::SwapBlocksParams tp;  // ~8 KB of kernel parameters, kept off the stack
+    std::memset(&tp, 0, sizeof(tp));
+    for (int l = 0; l < num_layers; ++l) {
+        REQUIRE(dst_key_caches[l] && dst_value_caches[l] && src_key_caches[l] && src_value_caches[l],
+                "layer %d cache pointer is NULL", l);
+        REQUIRE(aligned(dst_key_caches[l], 16) && aligned(dst_value_caches[l], 16) && aligned(src_key_caches[l], 16) &&
+                    aligned(src_value_caches[l], 16),
+                "layer %d cache not 16-byte aligned", l);
+        tp.dst_key[l] = dst_key_caches[l];
+        tp.dst_value[l] = dst_value_caches[l];
+        tp.src_key[l] = src_key_caches[l];
+        tp.src_value[l] = src_value_caches[l];
+    }
+    tp.block_mapping = block_mapping;
+    tp.block_bytes = (int64_t)num_kv_heads * block_size * head_dim * elem_bytes(dtype);
+    cudaError_t e = pa::launch_swap_blocks(tp, num_layers, num_pairs, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pa_swap_blocks");
+    return PA_OK;
+}
+
+pa_status_t pa_swap_blocks_memcpy(void* const* dst_key_caches, void* const* dst_value_caches,
+                                  const void* const* src_key_caches, const void* const* src_value_caches,
+                                  int num_layers, const int64_t* host_block_mapping, int num_pairs, int num_kv_heads,
+                                  int block_size, int head_dim, pa_dtype_t dtype, pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(valid_dtype(dtype) && num_layers >= 1 && num_pairs >= 0 && num_kv_heads > 0 && block_size > 0 &&
+                head_dim > 0,
+            "bad arguments");
+    if (num_pairs == 0) return PA_OK;
+    REQUIRE(host_block_mapping != nullptr, "host_block_mapping is NULL");
+    const size_t bytes = (size_t)num_kv_heads * block_size * head_dim * elem_bytes(dtype);
+    for (int i = 0; i < num_pairs; ++i) {
+        const int64_t src = host_block_mapping[2 * i], dst = host_block_mapping[2 * i + 1];
+        for (int l = 0; l < num_layers; ++l) {
+            cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst_key_caches[l]) + dst * bytes,
+                                            static_cast<const char*>(src_key_caches[l]) + src * bytes, bytes,
+                                            cudaMemcpyDefault, (cudaStream_t)stream);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(static_cast<char*>(dst_value_caches[l]) + dst * bytes,
+                                    static_cast<const char*>(src_value_caches[l]) + src * bytes, bytes,
+                                    cudaMemcpyDefault, (cudaStream_t)stream);
+            if (e != cudaSuccess) return cuda_fail(e, "pa_swap_blocks_memcpy");
+        }
+    }
+    return PA_OK;
+}
+
 // ---- end-to-end step from host buffers ----------------------------------------------
 
 namespace {

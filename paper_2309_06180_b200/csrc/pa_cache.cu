@@ -5,6 +5,9 @@
 //                     [NB][H_kv][B][D] cache; 16-byte vector copies, bit-exact.
 //  copy_blocks        fused block copy: every copy-on-write (src, dst) pair
 //                     of every layer in ONE launch instead of many cudaMemcpyAsync calls.
+//  swap_blocks        block transfers between pools (GPU <-> pinned CPU memory),
+//                     one launch for every pair and layer; host memory is read/written
+//                     over the host link directly (mapped pinned memory).
 //  validate_tables    test helper: block ids in range, ctx <= W*B.
 #include "pa_common.cuh"
 #include "pa_internal.h"
@@ -74,6 +77,28 @@ __global__ void __launch_bounds__(256) copy_blocks_kernel(const __grid_constant_
 
 // Codes are row-major over (row s, position 0 = ctx, 1 + j = entry j) so atomicMin
 // yields the first problem in row order; entries of a row with a bad ctx are skipped.
+__global__ void __launch_bounds__(256) swap_blocks_kernel(const __grid_constant__ SwapBlocksParams p) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const int pair = blockIdx.x, layer = blockIdx.y, which = blockIdx.z;
+    const int64_t src = p.block_mapping[2 * pair], dst = p.block_mapping[2 * pair + 1];
+    const char* sb = static_cast<const char*>(which == 0 ? p.src_key[layer] : p.src_value[layer]);
+    char* db = static_cast<char*>(which == 0 ? p.dst_key[layer] : p.dst_value[layer]);
+    const uint4* s = reinterpret_cast<const uint4*>(sb + src * p.block_bytes);
+    uint4* d = reinterpret_cast<uint4*>(db + dst * p.block_bytes);
+    const int n = (int)(p.block_bytes >> 4);
+    constexpr int U = 8;  // host-link latency is long: more 16-byte requests in flight per thread
+    int i = threadIdx.x;
+    for (; i + (U - 1) * 256 < n; i += U * 256) {
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) r[u] = s[i + u * 256];
+#pragma unroll
+        for (int u = 0; u < U; ++u) d[i + u * 256] = r[u];
+    }
+    for (; i < n; i += 256) d[i] = s[i];
+}
+
 __global__ void validate_tables_kernel(const int32_t* bt, const int32_t* ctx, int S, int W, int B, int NB,
                                        unsigned long long* first_bad) {
     const int64_t total = (int64_t)S * W;
@@ -98,6 +123,10 @@ cudaError_t launch_reshape_and_cache(const CacheWriteParams& p, cudaStream_t str
 
 cudaError_t launch_copy_blocks(const CopyBlocksParams& p, int num_layers, int num_pairs, cudaStream_t stream) {
     return launch_k(copy_blocks_kernel, dim3(num_pairs, num_layers, 2), dim3(256), 0, stream, p);
+}
+
+cudaError_t launch_swap_blocks(const SwapBlocksParams& p, int num_layers, int num_pairs, cudaStream_t stream) {
+    return launch_k(swap_blocks_kernel, dim3(num_pairs, num_layers, 2), dim3(256), 0, stream, p);
 }
 
 cudaError_t launch_validate_tables(const int32_t* bt, const int32_t* ctx, int S, int W, int B, int NB,

@@ -64,6 +64,15 @@ struct CopyBlocksParams {
     int64_t block_bytes;
 };
 
+struct SwapBlocksParams {
+    void* dst_key[kMaxLayers];
+    void* dst_value[kMaxLayers];
+    const void* src_key[kMaxLayers];
+    const void* src_value[kMaxLayers];
+    const int64_t* block_mapping;
+    int64_t block_bytes;
+};
+
 void count_launch();
 bool pdl_enabled();  // PA_PDL=0 disables programmatic dependent launch
 
@@ -95,6 +104,7 @@ cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int n
 cudaError_t launch_debug_gather(const GatherParams& p, int dtype, int head_dim, int num_seqs, cudaStream_t stream);
 cudaError_t launch_reshape_and_cache(const CacheWriteParams& p, cudaStream_t stream);
 cudaError_t launch_copy_blocks(const CopyBlocksParams& p, int num_layers, int num_pairs, cudaStream_t stream);
+cudaError_t launch_swap_blocks(const SwapBlocksParams& p, int num_layers, int num_pairs, cudaStream_t stream);
 cudaError_t launch_validate_tables(const int32_t* bt, const int32_t* ctx, int S, int W, int B, int NB,
                                    unsigned long long* d_first_bad, cudaStream_t stream);
 

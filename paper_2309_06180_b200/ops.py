@@ -113,6 +113,41 @@ def copy_blocks(key_caches, value_caches, block_mapping, stream=None):
           "pa_copy_blocks")
 
 
+def _dev_or_pinned(t: torch.Tensor, name: str) -> int:
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.is_cuda or t.is_pinned():
+        return t.data_ptr()
+    raise ValueError(f"{name} must be a CUDA tensor or pinned host memory")
+
+
+def swap_blocks(dst_key_caches, dst_value_caches, src_key_caches, src_value_caches, block_mapping, stream=None):
+    """Swap blocks between pools: dst[l][d] <- src[l][s] for every (s, d) pair in
+    block_mapping (int64 [P][2], device or pinned host) and layer, one launch.  Pools may be
+    device tensors or pinned host tensors (the CPU swap pool)."""
+    L = len(dst_key_caches)
+    arr = lambda xs, n: (ctypes.c_void_p * L)(*[_dev_or_pinned(x, n) for x in xs])  # noqa: E731
+    _, hk, B, D = dst_key_caches[0].shape
+    P = block_mapping.shape[0] if block_mapping.numel() else 0
+    bm = _dev_or_pinned(block_mapping, "block_mapping") if P else None
+    check(_lib.raw().pa_swap_blocks(arr(dst_key_caches, "dst_key"), arr(dst_value_caches, "dst_value"),
+                                    arr(src_key_caches, "src_key"), arr(src_value_caches, "src_value"), L, bm, P, hk,
+                                    B, D, _code(dst_key_caches[0]), _stream(stream)), "pa_swap_blocks")
+
+
+def swap_blocks_memcpy(dst_key_caches, dst_value_caches, src_key_caches, src_value_caches, host_block_mapping,
+                       stream=None):
+    """Benchmark baseline: the same transfer as one cudaMemcpyAsync per (pair, layer, K/V)."""
+    L = len(dst_key_caches)
+    arr = lambda xs, n: (ctypes.c_void_p * L)(*[_dev_or_pinned(x, n) for x in xs])  # noqa: E731
+    _, hk, B, D = dst_key_caches[0].shape
+    bm = host_block_mapping.contiguous()
+    check(_lib.raw().pa_swap_blocks_memcpy(arr(dst_key_caches, "dst_key"), arr(dst_value_caches, "dst_value"),
+                                           arr(src_key_caches, "src_key"), arr(src_value_caches, "src_value"), L,
+                                           bm.data_ptr(), bm.shape[0], hk, B, D, _code(dst_key_caches[0]),
+                                           _stream(stream)), "pa_swap_blocks_memcpy")
+
+
 def decode_step_staging_size(num_seqs, num_heads, num_kv_heads, head_dim, max_blocks_per_seq, num_pairs, dtype):
     return int(_lib.raw().pa_decode_step_staging_size(num_seqs, num_heads, num_kv_heads, head_dim,
                                                      max_blocks_per_seq, num_pairs, _DT[dtype]))

@@ -299,3 +299,26 @@ def test_copy_blocks_paper_cow_and_snapshot_semantics():
     kcs, vcs = oracle.copy_blocks(layers, vals, [[1, 3], [1, 4], [0, 5]], "f32")
     e = layers[0].copy(); e[3] = layers[0][1]; e[4] = layers[0][1]; e[5] = layers[0][0]
     assert np.array_equal(kcs[0], e)
+
+
+def test_swap_blocks_round_trip_and_placement():
+    """Swap-out then swap-in restores the GPU pool's live blocks; every
+    destination block equals its source, every other block is untouched."""
+    r = rng(18)
+    gpu = [r.integers(0, 1 << 16, (10, 2, 4, 8), dtype=np.uint16) for _ in range(2)]
+    gpuv = [r.integers(0, 1 << 16, (10, 2, 4, 8), dtype=np.uint16) for _ in range(2)]
+    cpu = [np.zeros((6, 2, 4, 8), np.uint16) for _ in range(2)]
+    cpuv = [np.zeros((6, 2, 4, 8), np.uint16) for _ in range(2)]
+    out_pairs = [[3, 0], [7, 5], [1, 2]]
+    ck, cv = oracle.swap_blocks(cpu, cpuv, gpu, gpuv, out_pairs)
+    for l in range(2):
+        e = cpu[l].copy(); e[0] = gpu[l][3]; e[5] = gpu[l][7]; e[2] = gpu[l][1]
+        assert np.array_equal(ck[l], e)
+    wiped = [np.zeros_like(g) for g in gpu]
+    wipedv = [np.zeros_like(g) for g in gpuv]
+    back = [[0, 4], [5, 9], [2, 6]]
+    gk, gv = oracle.swap_blocks(wiped, wipedv, ck, cv, back)
+    for l in range(2):
+        assert np.array_equal(gk[l][4], gpu[l][3]) and np.array_equal(gk[l][9], gpu[l][7])
+        assert np.array_equal(gv[l][6], gpuv[l][1])
+        assert not gk[l][[0, 1, 2, 3, 5, 7, 8]].any()
