@@ -185,7 +185,13 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     int stg = sched >= 2 ? (64 * 1024) / stage : (64 * 1024) / (nw * stage);
     stg = stg < 2 ? 2 : (stg > 8 ? 8 : stg);
     if (const char* ev = getenv("PA_STG")) stg = atoi(ev) > 0 ? atoi(ev) : stg;
-    const size_t smem = sched == 2   ? pa::attention_smem_bytes_coop(rb, nw, G, stg, PT, block_size)
+    // coop: partitions per CTA (scheduling only: the arithmetic partition stays PT and a
+    // CTA owning all partitions merges them in shared memory, bit-identically).  Measured
+    // neutral on c4 and worse on c2 (longer tail), so 1 unless PA_PPC says otherwise.
+    int ppc = 1;
+    if (const char* ev = getenv("PA_PPC")) ppc = atoi(ev) > 0 ? atoi(ev) : ppc;
+    ppc = std::max(1, std::min(ppc, NP));
+    const size_t smem = sched == 2   ? pa::attention_smem_bytes_coop(rb, nw, G, stg, PT * ppc, block_size, ppc, head_dim)
                         : sched == 3 ? pa::attention_smem_bytes_pcoop(rb, nw, G, stg, PT, block_size)
                                      : pa::attention_smem_bytes(persistent, rb, nw, stg, PT, block_size);
     if (smem > 227 * 1024)
@@ -224,6 +230,7 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     p.HPC = nw;
     p.STG = stg;
     p.HPW = 1;
+    p.PPC = ppc;
     if (const char* ev = getenv("PA_HPW")) p.HPW = atoi(ev) > 0 ? atoi(ev) : 1;
     cudaError_t e = pa::launch_attention(p, (int)dtype, head_dim, num_seqs, sched, smem, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "pa_paged_attention");

@@ -181,27 +181,35 @@ __device__ __forceinline__ void store_partial(float* o, float l, const float2 (&
 
 // Split-context merge of (sequence, head) sh over its np partitions, in partition order:
 //   M = max m_p;  out = sum_p 2^(m_p - M) L_p o~_p / sum_p 2^(m_p - M) L_p
-template <typename T, int D>
-__device__ __forceinline__ void merge_partitions(const AttnParams& p, int64_t sh, int np, int lane) {
-    const float2* ml = p.part_ml + sh * p.NP;
+// ml[p] = (m_p, L_p), po[p*D + d] = o~_p[d]: the global workspace (written by other CTAs,
+// read through L2) or this CTA's shared memory -- the arithmetic is the same either way.
+template <typename T, int D, bool kGlobal>
+__device__ __forceinline__ void merge_partitions_from(const float2* ml, const float* po, T* out_row, int np,
+                                                      int lane) {
+    auto ld2 = [](const float2* a) { return kGlobal ? __ldcg(a) : *a; };
+    auto ld1 = [](const float* a) { return kGlobal ? __ldcg(a) : *a; };
     float M = -INFINITY;
-    for (int i = 0; i < np; ++i) M = fmaxf(M, __ldcg(&ml[i]).x);
+    for (int i = 0; i < np; ++i) M = fmaxf(M, ld2(&ml[i]).x);
     float L = 0.f;
     constexpr int DPL = D / 32;  // dims per lane
     float o[DPL];
 #pragma unroll
     for (int e = 0; e < DPL; ++e) o[e] = 0.f;
-    const float* po = p.part_o + sh * p.NP * D;
     for (int i = 0; i < np; ++i) {
-        const float2 mi = __ldcg(&ml[i]);
+        const float2 mi = ld2(&ml[i]);
         const float w = mi.y * ex2(mi.x - M);
         L += w;
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) o[e] += w * __ldcg(po + (int64_t)i * D + lane * DPL + e);
+        for (int e = 0; e < DPL; ++e) o[e] += w * ld1(po + (int64_t)i * D + lane * DPL + e);
     }
-    T* out = static_cast<T*>(p.out) + sh * D + lane * DPL;
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) out[e] = Elem<T>::from_f32(o[e] / L);
+    for (int e = 0; e < DPL; ++e) out_row[lane * DPL + e] = Elem<T>::from_f32(o[e] / L);
+}
+
+template <typename T, int D>
+__device__ __forceinline__ void merge_partitions(const AttnParams& p, int64_t sh, int np, int lane) {
+    merge_partitions_from<T, D, true>(p.part_ml + sh * p.NP, p.part_o + sh * p.NP * D,
+                                      static_cast<T*>(p.out) + sh * D, np, lane);
 }
 
 // Publish this partition's (m, L, o~); the last partition to finish merges.  Whole warp.
@@ -755,9 +763,9 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
     constexpr int RB = C::RB, LT = C::LT, EPC = C::EPC;
     extern __shared__ __align__(128) unsigned char smem[];
 
-    const int part = blockIdx.x, hg = blockIdx.y, s = blockIdx.z;
+    const int hg = blockIdx.y, s = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int HPC = p.HPC, STG = p.STG, G = p.G;
+    const int HPC = p.HPC, STG = p.STG, G = p.G, PT = p.PT;
     const int h0 = hg * HPC;
     const int nh = min(HPC, p.H - h0);          // consumer warps with a head
     const int kvh0 = h0 / G;
@@ -767,10 +775,13 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
     const int stage_bytes = 2 * NKVmax * slab;
     pdl_wait();
     const int ctx = p.context_lens[s];
-    const int p0 = part * p.PT;
-    if (part > 0 && p0 >= ctx) return;  // this sequence has fewer partitions (CTA-uniform)
-    const int p1 = min(ctx, p0 + p.PT);
-    const int nparts = ctx > 0 ? (ctx + p.PT - 1) / p.PT : 1;
+    const int nparts = ctx > 0 ? (ctx + PT - 1) / PT : 1;
+    // this CTA walks the arithmetic partitions [c0, c0 + PPC) of the context back to back;
+    // each partition is finished exactly as if it had its own CTA (bitwise identical)
+    const int c0 = blockIdx.x * p.PPC;
+    if (c0 > 0 && c0 >= nparts) return;  // this sequence has fewer partitions (CTA-uniform)
+    const int p0 = c0 * PT;
+    const int p1 = min(ctx, p0 + p.PPC * PT);
     const int ntiles = p1 > p0 ? (p1 - p0 + kTile - 1) / kTile : 0;
     const int t_new = (p.new_key != nullptr && ctx > 0 && p1 == ctx) ? ctx - 1 : -1;
     const int pc = t_new >= 0 ? t_new : p1;
@@ -845,7 +856,19 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
     const int h = h0 + warp;
     const int kh = h / G - kvh0;
     const int g = lane / LT, c = lane % LT;
-    const uint4* qrow = reinterpret_cast<const uint4*>(static_cast<const char*>(p.query) + ((int64_t)s * p.H + h) * RB);
+    const int64_t sh = (int64_t)s * p.H + h;
+    // a CTA that owns every partition of a split context merges them itself, in shared
+    // memory (same arithmetic as the workspace path, no counters, no global round trip)
+    const bool whole = nparts > 1 && c0 == 0 && p1 == ctx;
+    float* my_po = reinterpret_cast<float*>(
+                       smem + (((size_t)STG * stage_bytes + 16 * STG + 4 * (size_t)(p.PPC * PT / (1 << p.log2B) + 2) +
+                                15) & ~(size_t)15)) +
+                   (size_t)warp * p.PPC * D;
+    float2* my_ml = reinterpret_cast<float2*>(
+                        smem + (((size_t)STG * stage_bytes + 16 * STG + 4 * (size_t)(p.PPC * PT / (1 << p.log2B) + 2) +
+                                 15) & ~(size_t)15) + (size_t)HPC * p.PPC * D * 4) +
+                    (size_t)warp * p.PPC;
+    const uint4* qrow = reinterpret_cast<const uint4*>(static_cast<const char*>(p.query) + sh * RB);
     const uint4 q0 = __ldg(qrow + c), q1 = __ldg(qrow + c + LT);
     float m = -INFINITY, l = 0.f;
     float2 acc[EPC];
@@ -862,13 +885,28 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
         tile_update<T, D>(sK, sV, min(kTile, p1 - tok0), q0, q1, p.scale_log2, g, c, m, l, acc);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[k]);
+        const int part = tok0 / PT;
+        if (tok0 + kTile >= min(p1, (part + 1) * PT)) {  // last tile of this partition
+            merge_token_groups<T, D>(m, l, acc);
+            if (nparts == 1) {
+                if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
+            } else if (whole) {  // keep (m, L, o~) in shared memory; merged below
+                if (g == 0) store_partial<T, D>(my_po + (part - c0) * D, l, acc, c);
+                if (lane == 0) my_ml[part - c0] = make_float2(m, l);
+            } else {
+                finish_split<T, D>(p, sh, part, nparts, m, l, acc, g, c, lane);
+            }
+            m = -INFINITY;
+            l = 0.f;
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
+        }
     }
-    merge_token_groups<T, D>(m, l, acc);
-    const int64_t sh = (int64_t)s * p.H + h;
-    if (nparts == 1) {
-        if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
-    } else {
-        finish_split<T, D>(p, sh, part, nparts, m, l, acc, g, c, lane);
+    if (ntiles == 0 && g == 0)  // empty context
+        store_out<T, D>(static_cast<T*>(p.out) + sh * D, 0.f, acc, c);
+    if (whole) {
+        __syncwarp();
+        merge_partitions_from<T, D, false>(my_ml, my_po, static_cast<T*>(p.out) + sh * D, nparts, lane);
     }
 }
 
@@ -1132,10 +1170,13 @@ __global__ void __launch_bounds__(32) debug_gather_kernel(GatherParams p) {
 
 int attention_row_bytes(int dtype, int head_dim) { return head_dim * (dtype == 0 ? 4 : 2); }
 
-size_t attention_smem_bytes_coop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size) {
+size_t attention_smem_bytes_coop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size,
+                                 int ppc, int head_dim) {
+    // partition_tokens here = tokens one CTA walks (PPC partitions)
     const int nkv_max = hpc % G == 0 ? hpc / G : (hpc + G - 1) / G + 1;
     const size_t tbl = 4 * (size_t)(partition_tokens / block_size + 2);
-    return (size_t)stg * 2 * nkv_max * kTile * (size_t)row_bytes + 16 * (size_t)stg + tbl;
+    const size_t head = (((size_t)stg * 2 * nkv_max * kTile * (size_t)row_bytes + 16 * (size_t)stg + tbl) + 15) & ~(size_t)15;
+    return head + (size_t)hpc * ppc * ((size_t)head_dim * 4 + 8);  // in-CTA partials
 }
 
 size_t attention_smem_bytes_pcoop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size) {
@@ -1199,7 +1240,8 @@ static cudaError_t launch_attention_t(const AttnParams& p, int num_seqs, int sch
             if (e != cudaSuccess) return e;
         }
         const int groups = (p.H + p.HPC - 1) / p.HPC;
-        return launch_k(kern, dim3(p.NP, groups, num_seqs), dim3((p.HPC + 1) * 32), smem, stream, p);
+        return launch_k(kern, dim3((p.NP + p.PPC - 1) / p.PPC, groups, num_seqs), dim3((p.HPC + 1) * 32), smem,
+                        stream, p);
     }
     if (!persistent) {
         auto kern = paged_attention_kernel<T, D>;

@@ -34,6 +34,7 @@ struct AttnParams {
     int NP;                     // partitions in the grid = ceil(max_ctx / PT)
     int HPC;                    // warps per CTA
     int HPW;                    // grid scheduler: query heads streamed by each warp
+    int PPC;                    // coop scheduler: partitions walked by one CTA (scheduling only)
     int STG;                    // tiles in flight per warp (shared-memory stages)
 };
 
@@ -96,7 +97,8 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 
 int attention_row_bytes(int dtype, int head_dim);
 size_t attention_smem_bytes(bool persistent, int row_bytes, int nw, int stg, int partition_tokens, int block_size);
-size_t attention_smem_bytes_coop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size);
+size_t attention_smem_bytes_coop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size,
+                                 int ppc, int head_dim);
 size_t attention_smem_bytes_pcoop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size);
 // sched: 0 = grid, 1 = persistent, 2 = coop, 3 = persistent coop
 cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int sched, size_t smem,

@@ -40,13 +40,19 @@ def main():
         for (sched, hpc, stg, hpw), pt in itertools.product(SHAPES, PTS):
             os.environ["PA_SCHED"], os.environ["PA_HPC"], os.environ["PA_STG"] = sched, str(hpc), str(stg)
             os.environ["PA_HPW"] = str(hpw)
+            os.environ["PA_PPC"] = str(hpw)  # 4th field doubles as coop partitions-per-CTA
             ws = torch.zeros(max(16, pa.paged_attention_workspace_size(wl.S, wl.H, wl.D, wl.max_context_len, pt)),
                              dtype=torch.uint8, device="cuda")
 
             def call():
-                pa.paged_attention_decode(out, x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"],
-                                          tb["block_tables"], tb["context_lens"], wl.scale,
-                                          max_context_len=wl.max_context_len, workspace=ws)
+                if os.environ.get("SWEEP_PTS"):  # explicit partition size: unfused entry
+                    pa.paged_attention(out, x["query"], x["key_cache"], x["value_cache"], tb["block_tables"],
+                                       tb["context_lens"], wl.scale, max_context_len=wl.max_context_len,
+                                       partition_tokens=pt, workspace=ws)
+                else:
+                    pa.paged_attention_decode(out, x["query"], x["key"], x["value"], x["key_cache"],
+                                              x["value_cache"], tb["block_tables"], tb["context_lens"], wl.scale,
+                                              max_context_len=wl.max_context_len, workspace=ws)
             try:
                 for _ in range(5):
                     call()
@@ -66,7 +72,7 @@ def main():
             print(json.dumps({"config": name, "sched": sched, "hpc": hpc, "stg": stg, "hpw": hpw, "pt": pt,
                               "us": round(us, 2),
                               "kv_GBps": round(kv / us / 1e3, 1)}), flush=True)
-        for k in ("PA_HPC", "PA_STG", "PA_HPW", "PA_SCHED"):
+        for k in ("PA_HPC", "PA_STG", "PA_HPW", "PA_SCHED", "PA_PPC"):
             os.environ.pop(k, None)
         del x
 

@@ -440,3 +440,22 @@ def test_swap_blocks_gpu_cpu_round_trip(B):
 
 def bits_t(t):
     return t.view(torch.int16) if t.element_size() == 2 else t.view(torch.int32)
+
+
+@pytest.mark.parametrize("name", ["c2_sharegpt", "c4_long"])
+def test_partitions_per_cta_bitwise_identical(name, monkeypatch):
+    """The coop scheduler may walk several 512-token partitions in one CTA (PA_PPC): each
+    is finished and merged exactly as with one CTA per partition, so outputs and cache
+    bytes are bit-identical for any PPC (TP / batch-composition invariance is kept)."""
+    wl = make_config(name)
+    x = materialize_torch(wl, "cuda")
+    ref = None
+    for ppc in ("1", "2", "3", "4"):
+        monkeypatch.setenv("PA_SCHED", "coop")
+        monkeypatch.setenv("PA_PPC", ppc)
+        out, kc, vc, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()}, fused=True)
+        if ref is None:
+            ref = (out, kc)
+        else:
+            assert torch.equal(out, ref[0]), ppc
+            assert torch.equal(kc.view(torch.int16), ref[1].view(torch.int16)), ppc
