@@ -111,6 +111,26 @@ pa_status_t pa_paged_attention_decode(void* out, const void* query, const void* 
                                       int max_context_len, pa_dtype_t dtype, void* workspace,
                                       size_t workspace_bytes, pa_stream_t stream);
 
+/* ------------------------------------------------------------------------------------
+ * pa_paged_attention_decode_shared -- pa_paged_attention_decode for batches whose
+ * sequences come in groups that share physical blocks (parallel sampling, beam search,
+ * P:295-332).  Sequences [g*group_size, (g+1)*group_size) form group
+ * g (the last group may be smaller); each distinct physical block a group reads at a
+ * logical position is brought into shared memory once and used by every member.
+ * Outputs and cache bytes are bit-identical to pa_paged_attention_decode; only the
+ * traffic changes.  group_size in [1, 8] (larger values are processed in groups of 8;
+ * 1 is the plain decode entry).  Other arguments as pa_paged_attention_decode.
+ * ---------------------------------------------------------------------------------- */
+pa_status_t pa_paged_attention_decode_shared(void* out, const void* query, const void* key,
+                                             const void* value, void* key_cache, void* value_cache,
+                                             const int32_t* block_tables,
+                                             const int32_t* context_lens, float scale,
+                                             int block_size, int num_kv_heads, int num_seqs,
+                                             int num_heads, int head_dim, int max_blocks_per_seq,
+                                             int max_context_len, int group_size, pa_dtype_t dtype,
+                                             void* workspace, size_t workspace_bytes,
+                                             pa_stream_t stream);
+
 /* Bytes of workspace pa_paged_attention(_ex) needs (0 if no context is split).
  * partition_tokens as in pa_paged_attention_ex. */
 size_t pa_paged_attention_workspace_size(int num_seqs, int num_heads, int head_dim,

@@ -124,7 +124,7 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
                            const int32_t* context_lens, float scale, int block_size, int num_kv_heads, int num_seqs,
                            int num_heads, int head_dim, int max_blocks_per_seq, int max_context_len,
                            pa_dtype_t dtype, int partition_tokens, void* workspace, size_t workspace_bytes,
-                           pa_stream_t stream) {
+                           pa_stream_t stream, int group_size = 1) {
     REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
     REQUIRE(num_seqs >= 0, "num_seqs must be >= 0 (got %d)", num_seqs);
     REQUIRE(num_heads > 0 && num_kv_heads > 0, "num_heads and num_kv_heads must be positive");
@@ -170,6 +170,10 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     if (sched_env && std::strcmp(sched_env, "grid") == 0) sched = 0;
     if (sched_env && std::strcmp(sched_env, "persistent") == 0) sched = 1;
     if (sched_env && std::strcmp(sched_env, "pcoop") == 0) sched = 3;
+    if (sched_env && std::strcmp(sched_env, "lcoop") == 0) sched = 5;
+    REQUIRE(group_size >= 1, "group_size must be >= 1");
+    const int gm = std::min(group_size, 8);
+    if (gm > 1) sched = 4;  // sharing-aware: groups of gm consecutive sequences
     const bool persistent = sched == 1;
     const int rb = pa::attention_row_bytes((int)dtype, head_dim);
     const int G = num_heads / num_kv_heads;
@@ -181,7 +185,10 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     if (const char* ev = getenv("PA_HPC")) nw = atoi(ev) > 0 ? atoi(ev) : nw;
     if (nw > 8) nw = 8;
     const int nkv_max = nw % G == 0 ? nw / G : (nw + G - 1) / G + 1;
-    const int stage = sched >= 2 ? 2 * nkv_max * 16 * rb : 2 * 16 * rb;
+    if (sched == 4) nw = std::max(1, 4 / gm);  // gm * nw consumer warps per CTA
+    const int nkv_max4 = nw % G == 0 ? nw / G : (nw + G - 1) / G + 1;
+    const int stage = sched == 4 ? gm * 2 * nkv_max4 * 16 * rb : sched >= 2 ? 2 * nkv_max * 16 * rb : 2 * 16 * rb;
+    // (sched 5 = listed coop shares the coop kernel and its shared-memory layout)
     int stg = sched >= 2 ? (64 * 1024) / stage : (64 * 1024) / (nw * stage);
     stg = stg < 2 ? 2 : (stg > 8 ? 8 : stg);
     if (const char* ev = getenv("PA_STG")) stg = atoi(ev) > 0 ? atoi(ev) : stg;
@@ -191,7 +198,10 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     int ppc = 1;
     if (const char* ev = getenv("PA_PPC")) ppc = atoi(ev) > 0 ? atoi(ev) : ppc;
     ppc = std::max(1, std::min(ppc, NP));
-    const size_t smem = sched == 2   ? pa::attention_smem_bytes_coop(rb, nw, G, stg, PT * ppc, block_size, ppc, head_dim)
+    if (sched == 5) ppc = 1;  // listed CTAs take single partitions
+    const size_t smem = sched == 4   ? pa::attention_smem_bytes_shared(rb, nw, G, stg, gm)
+                        : (sched == 2 || sched == 5)
+                            ? pa::attention_smem_bytes_coop(rb, nw, G, stg, PT * ppc, block_size, ppc, head_dim)
                         : sched == 3 ? pa::attention_smem_bytes_pcoop(rb, nw, G, stg, PT, block_size)
                                      : pa::attention_smem_bytes(persistent, rb, nw, stg, PT, block_size);
     if (smem > 227 * 1024)
@@ -231,6 +241,9 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     p.STG = stg;
     p.HPW = 1;
     p.PPC = ppc;
+    p.GM = gm;
+    p.S = num_seqs;
+    p.listed = sched == 5;
     if (const char* ev = getenv("PA_HPW")) p.HPW = atoi(ev) > 0 ? atoi(ev) : 1;
     cudaError_t e = pa::launch_attention(p, (int)dtype, head_dim, num_seqs, sched, smem, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "pa_paged_attention");
@@ -250,6 +263,20 @@ pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_
     return attention_impl(out, query, nullptr, nullptr, key_cache, value_cache, block_tables, context_lens, scale,
                           block_size, num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq,
                           max_context_len, dtype, partition_tokens, workspace, workspace_bytes, stream);
+}
+
+pa_status_t pa_paged_attention_decode_shared(void* out, const void* query, const void* key, const void* value,
+                                             void* key_cache, void* value_cache, const int32_t* block_tables,
+                                             const int32_t* context_lens, float scale, int block_size,
+                                             int num_kv_heads, int num_seqs, int num_heads, int head_dim,
+                                             int max_blocks_per_seq, int max_context_len, int group_size,
+                                             pa_dtype_t dtype, void* workspace, size_t workspace_bytes,
+                                             pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(key != nullptr && value != nullptr, "key/value (the step's new token) are NULL");
+    return attention_impl(out, query, key, value, key_cache, value_cache, block_tables, context_lens, scale,
+                          block_size, num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq,
+                          max_context_len, dtype, 0, workspace, workspace_bytes, stream, group_size);
 }
 
 pa_status_t pa_paged_attention_decode(void* out, const void* query, const void* key, const void* value,

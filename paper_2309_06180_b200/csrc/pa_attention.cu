@@ -763,22 +763,35 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
     constexpr int RB = C::RB, LT = C::LT, EPC = C::EPC;
     extern __shared__ __align__(128) unsigned char smem[];
 
-    const int hg = blockIdx.y, s = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int HPC = p.HPC, STG = p.STG, G = p.G, PT = p.PT;
-    const int h0 = hg * HPC;
-    const int nh = min(HPC, p.H - h0);          // consumer warps with a head
-    const int kvh0 = h0 / G;
-    const int NKV = (h0 + nh - 1) / G - kvh0 + 1;  // kv heads the group reads
     const int NKVmax = HPC % G == 0 ? HPC / G : (HPC + G - 1) / G + 1;  // stage layout stride (host-sized)
     const int slab = kTile * RB;                   // one kv head x 16 rows
     const int stage_bytes = 2 * NKVmax * slab;
     pdl_wait();
-    const int ctx = p.context_lens[s];
+    int hg, s, ctx, c0;
+    if (p.listed) {  // CTA = one entry of the longest-first work list x head group
+        const int NG = (p.H + HPC - 1) / HPC;
+        const int idx = blockIdx.x;
+        if (idx >= __ldcg(p.n_items) * NG) return;  // past the list (CTA-uniform)
+        const int4 it = __ldcg(&p.items[idx / NG]);
+        hg = idx - (idx / NG) * NG;
+        s = it.x;
+        c0 = it.y;
+        ctx = it.z;
+    } else {
+        hg = blockIdx.y;
+        s = blockIdx.z;
+        ctx = p.context_lens[s];
+        // this CTA walks the arithmetic partitions [c0, c0 + PPC) of the context back to
+        // back; each is finished exactly as if it had its own CTA (bitwise identical)
+        c0 = blockIdx.x * p.PPC;
+    }
+    const int h0 = hg * HPC;
+    const int nh = min(HPC, p.H - h0);          // consumer warps with a head
+    const int kvh0 = h0 / G;
+    const int NKV = (h0 + nh - 1) / G - kvh0 + 1;  // kv heads the group reads
     const int nparts = ctx > 0 ? (ctx + PT - 1) / PT : 1;
-    // this CTA walks the arithmetic partitions [c0, c0 + PPC) of the context back to back;
-    // each partition is finished exactly as if it had its own CTA (bitwise identical)
-    const int c0 = blockIdx.x * p.PPC;
     if (c0 > 0 && c0 >= nparts) return;  // this sequence has fewer partitions (CTA-uniform)
     const int p0 = c0 * PT;
     const int p1 = min(ctx, p0 + p.PPC * PT);
@@ -807,12 +820,13 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
         const char* vc = static_cast<const char*>(p.value_cache);
         const int64_t blk_bytes = ((int64_t)p.H_kv << p.log2B) * RB;
         const int pieces = B >= kTile ? 1 : kTile / B;
-        for (int j = 0; j < ntiles; ++j) {
-            const int k = j % STG;
-            if (j >= STG) mbar_wait(&empty[k], ((j / STG) - 1) & 1);
-            char* sK = reinterpret_cast<char*>(smem) + (size_t)k * stage_bytes;
+        // stage cursor and phases kept incrementally (no per-tile integer division)
+        int k = 0;
+        uint32_t ephase = 0;
+        char* sK = reinterpret_cast<char*>(smem);
+        for (int j = 0, tok0 = p0; j < ntiles; ++j, tok0 += kTile) {
+            if (j >= STG) mbar_wait(&empty[k], ephase);
             char* sV = sK + NKVmax * slab;
-            const int tok0 = p0 + j * kTile;
             const int nvc = max(0, min(kTile, pc - tok0));
             const bool has_new = t_new >= tok0 && t_new < tok0 + kTile;
             if (lane == 0)
@@ -847,6 +861,13 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
                 bulk_g2s(sV + dst, static_cast<const char*>(p.new_value) + src, RB, &full[k]);
             }
             __syncwarp();
+            if (++k == STG) {
+                k = 0;
+                sK = reinterpret_cast<char*>(smem);
+                if (j >= STG) ephase ^= 1u;  // wrapped past a round that waited on empty
+            } else {
+                sK += stage_bytes;
+            }
         }
         return;
     }
@@ -874,19 +895,29 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
     float2 acc[EPC];
 #pragma unroll
     for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
-    for (int j = 0; j < ntiles; ++j) {
-        const int k = j % STG;
-        mbar_wait(&full[k], (j / STG) & 1);
-        const char* sK = reinterpret_cast<const char*>(smem) + (size_t)k * stage_bytes + kh * slab;
+    // incremental cursors: stage k / phase, stage pointer, current partition and its end,
+    // the tile holding the new token (-1: none or not written by this warp)
+    int k = 0, part = c0, part_end = min(p1, (c0 + 1) * PT);
+    uint32_t fphase = 0;
+    const char* sKb = reinterpret_cast<const char*>(smem) + kh * slab;
+    const int j_new = (t_new >= 0 && h % G == 0) ? (t_new - p0) / kTile : -1;
+    for (int j = 0, tok0 = p0; j < ntiles; ++j, tok0 += kTile) {
+        mbar_wait(&full[k], fphase);
+        const char* sK = sKb;
         const char* sV = sK + NKVmax * slab;
-        const int tok0 = p0 + j * kTile;
-        if (t_new >= tok0 && t_new < tok0 + kTile && h % G == 0 && g == 0)
+        if (j == j_new && g == 0)
             write_new_token<T, D>(p, sK + (t_new - tok0) * RB, sV + (t_new - tok0) * RB, s, h / G, t_new, c);
         tile_update<T, D>(sK, sV, min(kTile, p1 - tok0), q0, q1, p.scale_log2, g, c, m, l, acc);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[k]);
-        const int part = tok0 / PT;
-        if (tok0 + kTile >= min(p1, (part + 1) * PT)) {  // last tile of this partition
+        if (++k == STG) {
+            k = 0;
+            fphase ^= 1u;
+            sKb = reinterpret_cast<const char*>(smem) + kh * slab;
+        } else {
+            sKb += stage_bytes;
+        }
+        if (tok0 + kTile >= part_end) {  // last tile of this partition
             merge_token_groups<T, D>(m, l, acc);
             if (nparts == 1) {
                 if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
@@ -900,6 +931,8 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
             l = 0.f;
 #pragma unroll
             for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
+            ++part;
+            part_end = min(p1, part_end + PT);
         }
     }
     if (ntiles == 0 && g == 0)  // empty context
@@ -1121,6 +1154,186 @@ __global__ void __launch_bounds__(288) paged_attention_pcoop_kernel(const AttnPa
     }
 }
 
+// ========================================= sharing-aware scheduler ===
+//
+// Sequences of one sequence group (the n samples of a request, the k beams of a beam
+// search) share physical blocks.  One CTA = (partition, group of HPC query
+// heads, group of M consecutive sequences); consumer warp (member m, head i) runs the
+// standard per-(sequence, head) tile arithmetic, so outputs are bit-identical to the
+// other schedulers.  The producer warp looks up the M members' physical blocks for each
+// 16-token logical tile, copies every DISTINCT block once into a slot of the stage and
+// publishes the member -> slot map with the stage: a block shared by the whole group
+// crosses L2 -> SM once instead of M times.  Tiles holding a member's new token are
+// never shared (copy-on-write made that block private).
+template <typename T, int D>
+__global__ void __launch_bounds__(288) paged_attention_shared_kernel(const AttnParams p) {
+    using C = AttnCfg<T, D>;
+    constexpr int RB = C::RB, LT = C::LT, EPC = C::EPC;
+    extern __shared__ __align__(128) unsigned char smem[];
+
+    const int hg = blockIdx.y, grp = blockIdx.z, part = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int HPC = p.HPC, STG = p.STG, G = p.G, PT = p.PT, M = p.GM;
+    const int NC = M * HPC;                               // consumer warps
+    const int h0 = hg * HPC, nh = min(HPC, p.H - h0);
+    const int kvh0 = h0 / G, NKV = (h0 + nh - 1) / G - kvh0 + 1;
+    const int NKVmax = HPC % G == 0 ? HPC / G : (HPC + G - 1) / G + 1;
+    const int slab = kTile * RB;                          // one kv head x 16 rows
+    const int slot_bytes = 2 * NKVmax * slab;             // K | V of the head group
+    const int stage_bytes = M * slot_bytes + 16 * ((M + 15) / 16) * 4;  // slots | member->slot map
+    const int s0 = grp * M, nm = min(M, p.S - s0);        // members of this group
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STG * stage_bytes);
+    uint64_t* empty = full + STG;
+    if (threadIdx.x < STG) {
+        mbar_init(&full[threadIdx.x], 1);
+        mbar_init(&empty[threadIdx.x], NC);
+    }
+    fence_mbar_init();
+    __syncthreads();
+    pdl_wait();
+    // the group's partition: tiles [part*PT, part*PT + PT) of every member still active
+    int gmax = 0;  // longest member context
+    for (int m = 0; m < nm; ++m) gmax = max(gmax, __ldg(p.context_lens + s0 + m));
+    const int p0 = part * PT;
+    if (part > 0 && p0 >= gmax) return;  // no member reaches this partition (CTA-uniform)
+    const int ntiles = (min(gmax, p0 + PT) - p0 + kTile - 1) / kTile;
+    auto slot_map = [&](int k) { return reinterpret_cast<int*>(smem + (size_t)k * stage_bytes + M * slot_bytes); };
+
+    if (warp == NC) {  // ================================================ producer warp
+        const int B = 1 << p.log2B;
+        const char* kc = static_cast<const char*>(p.key_cache);
+        const char* vc = static_cast<const char*>(p.value_cache);
+        const int64_t blk_bytes = ((int64_t)p.H_kv << p.log2B) * RB;
+        // lane m < nm: member m's context, copy limit and new-token position
+        const int my_s = s0 + min(lane, nm - 1);
+        const int my_ctx = lane < nm ? __ldg(p.context_lens + my_s) : 0;
+        const int my_p1 = min(my_ctx, p0 + PT);
+        const int my_tnew = (p.new_key != nullptr && lane < nm && my_ctx > 0 && my_p1 == my_ctx) ? my_ctx - 1 : -1;
+        const int my_pc = my_tnew >= 0 ? my_tnew : my_p1;
+        const int32_t* btrow = p.block_tables + (int64_t)my_s * p.W;
+        for (int j = 0; j < ntiles; ++j) {
+            const int k = j % STG;
+            if (j >= STG) mbar_wait(&empty[k], ((j / STG) - 1) & 1);
+            char* st = reinterpret_cast<char*>(smem) + (size_t)k * stage_bytes;
+            const int tok0 = p0 + j * kTile;
+            // per member: block id, rows needed, whether the tile holds its new token
+            const bool act = lane < nm && tok0 < my_p1;
+            const int rows = act ? max(0, min(kTile, my_pc - tok0)) : 0;
+            const bool has_new = act && my_tnew >= tok0 && my_tnew < tok0 + kTile;
+            // B >= 16: one block per tile; B < 16: a tile spans several blocks -> no sharing
+            const int blk = (act && rows > 0 && B >= kTile) ? __ldg(btrow + (tok0 >> p.log2B)) : -1;
+            const bool shareable = act && !has_new && B >= kTile && rows > 0;
+            // leader = first member with the same block (shareable tiles only)
+            int leader = lane;
+            for (int m = 0; m < nm; ++m) {
+                const int bm = __shfl_sync(0xffffffffu, blk, m);
+                const bool sm = __shfl_sync(0xffffffffu, shareable, m);
+                if (shareable && sm && bm == blk && m < leader) leader = m;
+            }
+            const bool is_leader = act && leader == lane;
+            const unsigned leaders = __ballot_sync(0xffffffffu, is_leader);
+            const int my_slot_if_leader = __popc(leaders & ((1u << lane) - 1u));
+            const int slot = __shfl_sync(0xffffffffu, my_slot_if_leader, leader);
+            // rows a shared slot must hold: the largest need among its members
+            int need = rows;
+            for (int m = 0; m < nm; ++m) {
+                const int lm = __shfl_sync(0xffffffffu, leader, m);
+                const int rm = __shfl_sync(0xffffffffu, rows, m);
+                if (is_leader && lm == lane) need = max(need, rm);
+            }
+            const uint32_t my_tx = is_leader ? (uint32_t)(2 * NKV * (need + (has_new ? 1 : 0)) * RB) : 0u;
+            uint32_t tx = my_tx;
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, off);
+            if (lane < M) slot_map(k)[lane] = act ? slot : -1;
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(&full[k], tx);  // also publishes the slot map
+            __syncwarp();
+            if (is_leader) {
+                char* sK = st + (size_t)my_slot_if_leader * slot_bytes;
+                char* sV = sK + NKVmax * slab;
+                if (need > 0) {
+                    if (B >= kTile) {
+                        if (B == kTile && need == kTile) {  // NKV contiguous head slabs of one block
+                            const int64_t off = (int64_t)blk * blk_bytes + (int64_t)kvh0 * slab;
+                            bulk_g2s(sK, kc + off, (uint32_t)(NKV * slab), &full[k]);
+                            bulk_g2s(sV, vc + off, (uint32_t)(NKV * slab), &full[k]);
+                        } else {
+                            for (int kh = 0; kh < NKV; ++kh) {
+                                const int64_t off = (int64_t)blk * blk_bytes + ((int64_t)(kvh0 + kh) << p.log2B) * RB +
+                                                    (int64_t)(tok0 & (B - 1)) * RB;
+                                bulk_g2s(sK + kh * slab, kc + off, (uint32_t)(need * RB), &full[k]);
+                                bulk_g2s(sV + kh * slab, vc + off, (uint32_t)(need * RB), &full[k]);
+                            }
+                        }
+                    } else {
+                        for (int kh = 0; kh < NKV; ++kh)
+                            for (int tk = tok0; tk < tok0 + need; tk += B) {
+                                const int b2 = __ldg(btrow + (tk >> p.log2B));
+                                const int r2 = min(B, tok0 + need - tk);
+                                const int64_t off = (int64_t)b2 * blk_bytes + ((int64_t)(kvh0 + kh) << p.log2B) * RB;
+                                bulk_g2s(sK + kh * slab + (tk - tok0) * RB, kc + off, (uint32_t)(r2 * RB), &full[k]);
+                                bulk_g2s(sV + kh * slab + (tk - tok0) * RB, vc + off, (uint32_t)(r2 * RB), &full[k]);
+                            }
+                    }
+                }
+                if (has_new)
+                    for (int kh = 0; kh < NKV; ++kh) {
+                        const int64_t src = ((int64_t)my_s * p.H_kv + kvh0 + kh) * RB;
+                        const int dst = kh * slab + (my_tnew - tok0) * RB;
+                        bulk_g2s(sK + dst, static_cast<const char*>(p.new_key) + src, RB, &full[k]);
+                        bulk_g2s(sV + dst, static_cast<const char*>(p.new_value) + src, RB, &full[k]);
+                    }
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    // ============================================================== consumer warps
+    const int mem = warp / HPC, hi = warp - mem * HPC;
+    const bool active = mem < nm && hi < nh;
+    const int s = s0 + min(mem, nm - 1), h = h0 + min(hi, nh - 1);
+    const int ctx = __ldg(p.context_lens + s);
+    const int nparts = ctx > 0 ? (ctx + PT - 1) / PT : 1;
+    const int p1 = min(ctx, p0 + PT);
+    const int t_new = (p.new_key != nullptr && ctx > 0 && p1 == ctx) ? ctx - 1 : -1;
+    const int kh = h / G - kvh0;
+    const int g = lane / LT, c = lane % LT;
+    const int64_t sh = (int64_t)s * p.H + h;
+    const uint4* qrow = reinterpret_cast<const uint4*>(static_cast<const char*>(p.query) + sh * RB);
+    const uint4 q0 = __ldg(qrow + c), q1 = __ldg(qrow + c + LT);
+    const int my_ntiles = p1 > p0 ? (p1 - p0 + kTile - 1) / kTile : 0;
+    float m = -INFINITY, l = 0.f;
+    float2 acc[EPC];
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
+    for (int j = 0; j < ntiles; ++j) {
+        const int k = j % STG;
+        mbar_wait(&full[k], (j / STG) & 1);
+        if (active && j < my_ntiles) {
+            const int slot = slot_map(k)[mem];
+            const char* sK = reinterpret_cast<const char*>(smem) + (size_t)k * stage_bytes + (size_t)slot * slot_bytes +
+                             kh * slab;
+            const char* sV = sK + NKVmax * slab;
+            const int tok0 = p0 + j * kTile;
+            if (t_new >= tok0 && t_new < tok0 + kTile && h % G == 0 && g == 0)
+                write_new_token<T, D>(p, sK + (t_new - tok0) * RB, sV + (t_new - tok0) * RB, s, h / G, t_new, c);
+            tile_update<T, D>(sK, sV, min(kTile, p1 - tok0), q0, q1, p.scale_log2, g, c, m, l, acc);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[k]);
+    }
+    if (!active) return;
+    if (part > 0 && p0 >= ctx) return;  // this member has no tokens in the partition
+    merge_token_groups<T, D>(m, l, acc);
+    if (nparts == 1) {
+        if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
+    } else {
+        finish_split<T, D>(p, sh, part, nparts, m, l, acc, g, c, lane);
+    }
+}
+
 // ==================================================================== debug gather ===
 
 // Test-only: copy the logical K/V rows of (s, kvh) through the grid scheduler's loader.
@@ -1187,6 +1400,12 @@ size_t attention_smem_bytes_pcoop(int row_bytes, int hpc, int G, int stg, int pa
     return (size_t)stg * stage + 16 * (size_t)stg + tbl;
 }
 
+size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int gm) {
+    const int nkv_max = hpc % G == 0 ? hpc / G : (hpc + G - 1) / G + 1;
+    const size_t stage = (size_t)gm * 2 * nkv_max * kTile * row_bytes + 16 * (size_t)((gm + 15) / 16) * 4;
+    return (size_t)stg * stage + 16 * (size_t)stg;
+}
+
 size_t attention_smem_bytes(bool persistent, int row_bytes, int nw, int stg, int partition_tokens, int block_size) {
     if (persistent) {
         const size_t sb = 2 * kTile * (size_t)row_bytes + row_bytes;
@@ -1200,6 +1419,22 @@ template <typename T, int D>
 static cudaError_t launch_attention_t(const AttnParams& p, int num_seqs, int sched, size_t smem,
                                       cudaStream_t stream) {
     const bool persistent = sched == 1;
+    if (sched == 4) {  // sharing-aware: groups of GM consecutive sequences
+        auto kern = paged_attention_shared_kernel<T, D>;
+        static size_t configured = 0;
+        if (smem > configured) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            configured = smem;
+        }
+        if (p.NP > 1) {
+            cudaError_t e = cudaMemsetAsync(p.counters, 0, sizeof(int) * (size_t)num_seqs * p.H, stream);
+            if (e != cudaSuccess) return e;
+        }
+        const int groups = (p.H + p.HPC - 1) / p.HPC;
+        const int sgroups = (num_seqs + p.GM - 1) / p.GM;
+        return launch_k(kern, dim3(p.NP, groups, sgroups), dim3((p.GM * p.HPC + 1) * 32), smem, stream, p);
+    }
     if (sched == 3) {  // persistent coop
         auto kern = paged_attention_pcoop_kernel<T, D>;
         static size_t configured = 0;
@@ -1226,6 +1461,20 @@ static cudaError_t launch_attention_t(const AttnParams& p, int num_seqs, int sch
         cudaError_t e = launch_k(build_worklist_kernel, dim3(1), dim3(1024), 0, stream, p, num_seqs);
         if (e != cudaSuccess) return e;
         return launch_k(kern, dim3((unsigned)grid), dim3(threads), smem, stream, p);
+    }
+    if (sched == 5) {  // listed coop: one CTA per (work-list entry, head group), longest first
+        auto kern = paged_attention_coop_kernel<T, D>;
+        static size_t configured = 0;
+        if (smem > configured) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            configured = smem;
+        }
+        const int groups = (p.H + p.HPC - 1) / p.HPC;
+        cudaError_t e = launch_k(build_worklist_kernel, dim3(1), dim3(1024), 0, stream, p, num_seqs);
+        if (e != cudaSuccess) return e;
+        return launch_k(kern, dim3((unsigned)((int64_t)num_seqs * p.NP * groups)), dim3((p.HPC + 1) * 32), smem,
+                        stream, p);
     }
     if (sched == 2) {  // coop: HPC consumer warps + 1 producer warp per CTA
         auto kern = paged_attention_coop_kernel<T, D>;

@@ -35,6 +35,9 @@ struct AttnParams {
     int HPC;                    // warps per CTA
     int HPW;                    // grid scheduler: query heads streamed by each warp
     int PPC;                    // coop scheduler: partitions walked by one CTA (scheduling only)
+    int GM;                     // sharing-aware scheduler: sequences per group
+    int S;                      // number of sequences
+    int listed;                 // coop: CTAs take (sequence, partition) from the work list
     int STG;                    // tiles in flight per warp (shared-memory stages)
 };
 
@@ -100,7 +103,8 @@ size_t attention_smem_bytes(bool persistent, int row_bytes, int nw, int stg, int
 size_t attention_smem_bytes_coop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size,
                                  int ppc, int head_dim);
 size_t attention_smem_bytes_pcoop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size);
-// sched: 0 = grid, 1 = persistent, 2 = coop, 3 = persistent coop
+size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int gm);
+// sched: 0 = grid, 1 = persistent, 2 = coop, 3 = persistent coop, 4 = sharing-aware groups, 5 = listed coop
 cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int sched, size_t smem,
                              cudaStream_t stream);
 cudaError_t launch_debug_gather(const GatherParams& p, int dtype, int head_dim, int num_seqs, cudaStream_t stream);

@@ -90,6 +90,28 @@ def paged_attention_decode(out, query, key, value, key_cache, value_cache, block
     return out
 
 
+def paged_attention_decode_shared(out, query, key, value, key_cache, value_cache, block_tables, context_lens,
+                                  scale: float, group_size: int, max_context_len: int = 0,
+                                  workspace: torch.Tensor | None = None, stream=None):
+    """paged_attention_decode for sequence groups sharing blocks (parallel samples, beams):
+    each distinct block of a group is read once per logical tile (pa.h)."""
+    S, H, D = query.shape
+    _, hk, B, _ = key_cache.shape
+    W = block_tables.shape[1]
+    mcl = max_context_len if max_context_len > 0 else W * B
+    need = paged_attention_workspace_size(S, H, D, mcl, 0)
+    if workspace is None and need > 0:
+        workspace = torch.empty(need, dtype=torch.uint8, device=query.device)
+    ws_ptr = _dev(workspace, "workspace") if workspace is not None else None
+    ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    check(_lib.raw().pa_paged_attention_decode_shared(
+        _dev(out, "out"), _dev(query, "query"), _dev(key, "key"), _dev(value, "value"), _dev(key_cache, "key_cache"),
+        _dev(value_cache, "value_cache"), _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"),
+        float(scale), B, hk, S, H, D, W, int(mcl), int(group_size), _code(query), ws_ptr, ws_bytes, _stream(stream)),
+        "pa_paged_attention_decode_shared")
+    return out
+
+
 def reshape_and_cache(key, value, key_cache, value_cache, slot_mapping, stream=None):
     """Fused reshape + block write: key/value [T][H_kv][D] into the caches at
     slot_mapping (int64 [T], -1 = skip)."""

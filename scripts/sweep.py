@@ -38,14 +38,20 @@ def main():
         out = torch.empty_like(x["query"])
         kv = wl.logical_kv_bytes()
         for (sched, hpc, stg, hpw), pt in itertools.product(SHAPES, PTS):
-            os.environ["PA_SCHED"], os.environ["PA_HPC"], os.environ["PA_STG"] = sched, str(hpc), str(stg)
+            os.environ["PA_SCHED"] = "coop" if sched.startswith("shared") else sched
+            os.environ["PA_HPC"], os.environ["PA_STG"] = str(hpc), str(stg)
             os.environ["PA_HPW"] = str(hpw)
             os.environ["PA_PPC"] = str(hpw)  # 4th field doubles as coop partitions-per-CTA
             ws = torch.zeros(max(16, pa.paged_attention_workspace_size(wl.S, wl.H, wl.D, wl.max_context_len, pt)),
                              dtype=torch.uint8, device="cuda")
 
             def call():
-                if os.environ.get("SWEEP_PTS"):  # explicit partition size: unfused entry
+                if sched.startswith("shared"):  # sharing-aware entry, group size in the name
+                    pa.paged_attention_decode_shared(out, x["query"], x["key"], x["value"], x["key_cache"],
+                                                     x["value_cache"], tb["block_tables"], tb["context_lens"],
+                                                     wl.scale, int(sched[6:] or 4),
+                                                     max_context_len=wl.max_context_len, workspace=ws)
+                elif os.environ.get("SWEEP_PTS"):  # explicit partition size: unfused entry
                     pa.paged_attention(out, x["query"], x["key_cache"], x["value_cache"], tb["block_tables"],
                                        tb["context_lens"], wl.scale, max_context_len=wl.max_context_len,
                                        partition_tokens=pt, workspace=ws)

@@ -387,13 +387,13 @@ def test_fused_decode_gqa():
 
 @pytest.mark.parametrize("name", ["c2_sharegpt", "c3_fork", "c4_long"])
 def test_schedulers_bitwise_identical(name, monkeypatch):
-    """coop (default), grid, persistent and pcoop run the same per-(sequence, head) tile
+    """coop (default), grid, persistent, pcoop and lcoop run the same per-(sequence, head) tile
     arithmetic in the same order, so their outputs and cache writes are bit-identical;
     a stage-reuse race in any pipeline would break this (full-size c2/c4, repeated)."""
     wl = make_config(name)
     x = materialize_torch(wl, "cuda")
     ref = None
-    for sched in ("coop", "grid", "persistent", "pcoop", "coop"):
+    for sched in ("coop", "grid", "persistent", "pcoop", "lcoop", "coop"):
         monkeypatch.setenv("PA_SCHED", sched)
         out, kc, vc, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()}, fused=True)
         if ref is None:
@@ -459,3 +459,44 @@ def test_partitions_per_cta_bitwise_identical(name, monkeypatch):
         else:
             assert torch.equal(out, ref[0]), ppc
             assert torch.equal(kc.view(torch.int16), ref[1].view(torch.int16)), ppc
+
+
+@pytest.mark.parametrize("name,gs", [("c5_beam", 4), ("c3_parallel", 6), ("c3_fork", 6), ("c2_sharegpt", 4),
+                                     ("c5_beam", 3), ("c3_parallel", 8)])
+def test_shared_decode_bitwise_equals_decode(name, gs):
+    """N1 sharing-aware entry: every distinct block of a sequence group is loaded once;
+    outputs and cache bytes bit-identical to pa_paged_attention_decode at full size,
+    including groups that do not align with the requests (gs 3 / 8)."""
+    import paper_2309_06180_b200 as pa
+    wl = make_config(name)
+    x = materialize_torch(wl, "cuda")
+    tb = tables_torch(wl, "cuda")
+    a, ka, va, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()}, fused=True)
+    y = {k: v.clone() for k, v in x.items()}
+    if len(wl.block_mapping):
+        pa.copy_blocks([y["key_cache"]], [y["value_cache"]], tb["block_mapping"])
+    b = torch.empty_like(y["query"])
+    pa.paged_attention_decode_shared(b, y["query"], y["key"], y["value"], y["key_cache"], y["value_cache"],
+                                     tb["block_tables"], tb["context_lens"], wl.scale, gs,
+                                     max_context_len=wl.max_context_len)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert torch.equal(bits_t(ka), bits_t(y["key_cache"])) and torch.equal(bits_t(va), bits_t(y["value_cache"]))
+
+
+@pytest.mark.parametrize("B", [1, 16, 32])
+def test_shared_decode_small_vs_oracle(B):
+    import paper_2309_06180_b200 as pa
+    wl = make_config("c5_beam", S=14, H=4, H_kv=4, B=B)
+    x = materialize_torch(wl, "cuda")
+    tb = tables_torch(wl, "cuda")
+    if len(wl.block_mapping):
+        pa.copy_blocks([x["key_cache"]], [x["value_cache"]], tb["block_mapping"])
+    out = torch.empty_like(x["query"])
+    pa.paged_attention_decode_shared(out, x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"],
+                                     tb["block_tables"], tb["context_lens"], wl.scale, 4,
+                                     max_context_len=wl.max_context_len)
+    torch.cuda.synchronize()
+    ref, rkc, rvc = oracle_step(wl)
+    assert np.array_equal(bits(x["key_cache"]), rkc) and np.array_equal(bits(x["value_cache"]), rvc)
+    assert max_abs(out, ref) <= TOL[wl.dtype]
