@@ -16,6 +16,8 @@ Functions and the passage they follow (P:N = PAPER.md line N):
 - ``split_attention``       per-partition (m, L, o~) + log-sum-exp merge (BJ:north_star).
 - ``reshape_and_cache``     fused reshape + block write.
 - ``copy_blocks``           fused block copy for copy-on-write.
+- ``prefill_attention``     causal multi-token attention of the prompt phase / a shared
+                            prefix's suffix over the paged cache.
 - ``swap_blocks``           block transfers between the GPU pool and the CPU swap pool.
 - ``decode``                storage dtype -> fp64, bit-exact (own fp16/bf16 decoders).
 
@@ -66,6 +68,8 @@ def lib():
         L.oracle_reshape_and_cache.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32]
         L.oracle_copy_blocks.argtypes = [vp, vp, i32, vp, i32, i32, i32, i32, i32, i32]
         L.oracle_swap_blocks.argtypes = [vp, vp, vp, vp, i32, vp, i32, i64]
+        L.oracle_prefill_attention.argtypes = [vp, vp, vp, vp, vp, vp, vp, d, i32, i32, i32, i32, i32,
+                                               i32, i32]
         _lib = L
     return _lib
 
@@ -123,6 +127,25 @@ def paged_attention(query, key_cache, value_cache, block_tables, context_lens, s
     lib().oracle_paged_attention(_p(out), _p(query), _p(key_cache), _p(value_cache), _p(bt), _p(cl),
                                  float(scale), int(block_size), int(num_kv_heads), S, H, D,
                                  int(bt.shape[1]), _dt(dtype))
+    return out
+
+
+def prefill_attention(query, key_cache, value_cache, block_tables, context_lens, query_start, scale,
+                      block_size, num_kv_heads, dtype) -> np.ndarray:
+    """Causal multi-token attention (P:140-147, P:334-338 with Eq.4).  query [T][H][D] rows
+    of sequence s in [query_start[s], query_start[s+1]); those are the last q_len tokens of its
+    context_lens[s].  Returns fp64 [T][H][D]."""
+    query, key_cache, value_cache = _raw(query), _raw(key_cache), _raw(value_cache)
+    bt = np.ascontiguousarray(block_tables, dtype=np.int32)
+    cl = np.ascontiguousarray(context_lens, dtype=np.int32)
+    qs = np.ascontiguousarray(query_start, dtype=np.int32)
+    T, H, D = query.shape
+    S = cl.shape[0]
+    assert qs.shape[0] == S + 1 and qs[-1] == T
+    out = np.empty((T, H, D), dtype=np.float64)
+    lib().oracle_prefill_attention(_p(out), _p(query), _p(key_cache), _p(value_cache), _p(bt), _p(cl),
+                                   _p(qs), float(scale), int(block_size), int(num_kv_heads), S, H, D,
+                                   int(bt.shape[1]), _dt(dtype))
     return out
 
 

@@ -15,6 +15,8 @@
  *   P:418-419         fused reshape + block write  -> oracle_reshape_and_cache
  *   P:424-427         fused block copy (CoW) -> oracle_copy_blocks
  *   P:363-366         swapping blocks to the CPU pool and back -> oracle_swap_blocks
+ *   P:140-147,334-338 prompt-phase / shared-prefix-suffix causal attention over the
+ *                     paged cache -> oracle_prefill_attention
  *
  * Readings of the paper: the caller passes `scale` (c1); the
  * Eq.4 denominator is the sum of element-wise exponentials (c2); only t < ctx is read
@@ -188,6 +190,34 @@ void oracle_paged_attention(double* out, const void* query, const void* key_cach
         int s = (int)(i / num_heads), h = (int)(i % num_heads);
         paged_one(out + i * head_dim, query, key_cache, value_cache,
                   block_tables + (int64_t)s * W, context_lens[s], s, h, scale, block_size,
+                  num_kv_heads, num_heads, head_dim, dtype);
+    }
+}
+
+/* Multi-token (prompt / chunked-prompt / shared-prefix suffix) attention, P:145-147,
+ * P:334-338 with Eq.4.  Sequence s owns query rows [query_start[s], query_start[s+1])
+ * of query [T][H][D]; its q_len = query_start[s+1]-query_start[s] new tokens are the LAST
+ * q_len of its context_lens[s] cached tokens (reading c22), so query row i sits at
+ * position p = ctx - q_len + i and attends causally to tokens 0..p (the autoregressive
+ * mask of P:140-142).  That is Eq.4 with n = p + 1 -- computed here by the same per-row
+ * routine as decode.  out: fp64 [T][H][D]. */
+void oracle_prefill_attention(double* out, const void* query, const void* key_cache,
+                              const void* value_cache, const int32_t* block_tables,
+                              const int32_t* context_lens, const int32_t* query_start,
+                              double scale, int block_size, int num_kv_heads, int num_seqs,
+                              int num_heads, int head_dim, int W, int dtype) {
+    int64_t T = query_start[num_seqs];
+    int64_t total = T * num_heads;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < total; ++i) {
+        int64_t row = i / num_heads;
+        int h = (int)(i % num_heads);
+        int s = 0;
+        while (query_start[s + 1] <= row) ++s;
+        int q_len = query_start[s + 1] - query_start[s];
+        int pos = context_lens[s] - q_len + (int)(row - query_start[s]);
+        paged_one(out + i * head_dim, query, key_cache, value_cache,
+                  block_tables + (int64_t)s * W, pos + 1, (int)row, h, scale, block_size,
                   num_kv_heads, num_heads, head_dim, dtype);
     }
 }

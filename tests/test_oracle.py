@@ -322,3 +322,98 @@ def test_swap_blocks_round_trip_and_placement():
         assert np.array_equal(gk[l][4], gpu[l][3]) and np.array_equal(gk[l][9], gpu[l][7])
         assert np.array_equal(gv[l][6], gpuv[l][1])
         assert not gk[l][[0, 1, 2, 3, 5, 7, 8]].any()
+
+
+# ------------------------------------ prompt phase / shared-prefix suffix (N4) --------
+
+def _prefill_case(r, ctxs, qlens, H, H_kv, D, B):
+    """Seeded fp32 case: per sequence a contiguous K/V [ctx][H_kv][D] placed on shuffled
+    blocks (NaN elsewhere), query rows [T][H][D]."""
+    S = len(ctxs)
+    W = max(-(-c // B) for c in ctxs)
+    NB = S * W + 5
+    perm = r.permutation(NB)
+    kc = np.full((NB, H_kv, B, D), np.nan, np.float32)
+    vc = np.full((NB, H_kv, B, D), np.nan, np.float32)
+    bt = np.zeros((S, W), np.int32)
+    Ks, Vs = [], []
+    for s, c in enumerate(ctxs):
+        K = r.uniform(-1, 1, (c, H_kv, D)).astype(np.float32)
+        V = r.uniform(-1, 1, (c, H_kv, D)).astype(np.float32)
+        bt[s] = perm[s * W:(s + 1) * W]
+        for t in range(c):
+            kc[bt[s, t // B], :, t % B] = K[t]
+            vc[bt[s, t // B], :, t % B] = V[t]
+        Ks.append(K)
+        Vs.append(V)
+    qs = np.concatenate([[0], np.cumsum(qlens)]).astype(np.int32)
+    Q = r.uniform(-1, 1, (int(qs[-1]), H, D)).astype(np.float32)
+    return Q, kc, vc, bt, np.asarray(ctxs, np.int32), qs, Ks, Vs
+
+
+def test_prefill_pure_prompt_equals_torch_causal_sdpa():
+    """ctx == q_len (the prompt phase): the result is textbook causal
+    self-attention -- pinned to torch's scaled_dot_product_attention(is_causal=True) in fp64
+    (a library routine independent of the oracle's loops), GQA via repeat_interleave."""
+    torch = pytest.importorskip("torch")
+    r = rng(30)
+    H, H_kv, D, B = 4, 2, 16, 8
+    ctxs = [37, 1, 64]
+    Q, kc, vc, bt, cl, qs, Ks, Vs = _prefill_case(r, ctxs, ctxs, H, H_kv, D, B)
+    scale = 1.0 / math.sqrt(D)
+    out = oracle.prefill_attention(Q.view(np.uint32), kc.view(np.uint32), vc.view(np.uint32), bt, cl, qs,
+                                   scale, B, H_kv, "f32")
+    for s, c in enumerate(ctxs):
+        q = torch.from_numpy(Q[qs[s]:qs[s + 1]].astype(np.float64)).permute(1, 0, 2)  # [H][c][D]
+        k = torch.from_numpy(Ks[s].astype(np.float64)).permute(1, 0, 2).repeat_interleave(H // H_kv, 0)
+        v = torch.from_numpy(Vs[s].astype(np.float64)).permute(1, 0, 2).repeat_interleave(H // H_kv, 0)
+        ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, scale=scale)
+        np.testing.assert_allclose(out[qs[s]:qs[s + 1]], ref.permute(1, 0, 2).numpy(), rtol=0, atol=1e-13)
+
+
+def test_prefill_shared_prefix_suffix_rows_equal_decode():
+    """ctx > q_len (suffix after a cached shared prefix): query row i equals the
+    decode oracle (Eq.4) run with context length ctx - q_len + i + 1 -- bitwise, since a
+    one-token step is the q_len == 1 case."""
+    r = rng(31)
+    H, H_kv, D, B = 4, 4, 8, 16
+    ctxs, qlens = [50, 20, 33], [7, 20, 1]
+    Q, kc, vc, bt, cl, qs, _, _ = _prefill_case(r, ctxs, qlens, H, H_kv, D, B)
+    out = oracle.prefill_attention(Q.view(np.uint32), kc.view(np.uint32), vc.view(np.uint32), bt, cl, qs,
+                                   0.3, B, H_kv, "f32")
+    for s in range(len(ctxs)):
+        for i in range(qlens[s]):
+            row = qs[s] + i
+            n = ctxs[s] - qlens[s] + i + 1
+            ref = oracle.paged_attention(Q[row:row + 1].view(np.uint32), kc.view(np.uint32),
+                                         vc.view(np.uint32), bt[s:s + 1], np.array([n], np.int32), 0.3, B,
+                                         H_kv, "f32")
+            assert np.array_equal(out[row], ref[0])
+
+
+def test_prefill_first_prompt_row_is_v0_and_block_invariance():
+    """Row 0 of a prompt attends to exactly one token: out = v_0 (closed form).  The
+    result does not depend on block size or placement, bitwise."""
+    H, H_kv, D = 2, 1, 8
+    outs = []
+    for B in (1, 4, 16):
+        for seed in (40, 41):
+            r = rng(32)  # same logical data
+            Q, kc, vc, bt, cl, qs, Ks, Vs = _prefill_case(r, [29], [29], H, H_kv, D, 32)
+            # re-place the same logical rows with block size B on a different permutation
+            K, V = Ks[0], Vs[0]
+            nb = -(-29 // B)
+            NB = nb + 7
+            phys = np.random.default_rng(seed).permutation(NB)[:nb].astype(np.int32)
+            kc2 = np.full((NB, H_kv, B, D), np.nan, np.float32)
+            vc2 = np.full((NB, H_kv, B, D), np.nan, np.float32)
+            for t in range(29):
+                kc2[phys[t // B], :, t % B] = K[t]
+                vc2[phys[t // B], :, t % B] = V[t]
+            out = oracle.prefill_attention(Q.view(np.uint32), kc2.view(np.uint32), vc2.view(np.uint32),
+                                           phys[None, :], cl, qs, 0.35, B, H_kv, "f32")
+            assert np.array_equal(out[0, 0], V[0, 0].astype(np.float64))
+            assert np.array_equal(out[0, 1], V[0, 0].astype(np.float64))
+            outs.append(out)
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
