@@ -131,6 +131,37 @@ pa_status_t pa_paged_attention_decode_shared(void* out, const void* query, const
                                              void* workspace, size_t workspace_bytes,
                                              pa_stream_t stream);
 
+/* ------------------------------------------------------------------------------------
+ * pa_paged_prefill_attention -- multi-token causal attention over the paged cache: the
+ * prompt phase, a chunk of a long prompt, or the user-specific suffix after
+ * a cached shared prefix ("the prompt phase computation only needs to execute
+ * on the user's task input").  SURVEY §8(f) N4; runs on the tcgen05 tensor cores.
+ *
+ * Sequence s owns query rows [query_start[s], query_start[s+1]) of query [T][H][D]
+ * (T = num_query_tokens); its q_len new tokens are the LAST q_len of its context_lens[s]
+ * cached tokens (they must already be in the cache -- pa_reshape_and_cache with the
+ * multi-token slot mapping, reading c5/c22).  Row i (position p = ctx - q_len + i)
+ * attends causally to tokens 0..p through block_tables (Eq.4 with n = p + 1, the
+ * autoregressive mask of P:140-142):
+ *     out[row][h][:] = sum_{t<=p} softmax_t(scale * q . k_t) v_t
+ * Rows with p < 0 (ctx < q_len) are 0.
+ *
+ * out, query: [T][H][D] (16-byte aligned); caches [num_blocks][H_kv][B][D];
+ * block_tables [S][max_blocks_per_seq]; context_lens [S]; query_start [S+1] int32 with
+ * query_start[0] = 0, non-decreasing, query_start[S] = T; max_query_len >= every q_len
+ * (sizes the grid).  All device pointers; the caller owns every buffer.  f16/bf16,
+ * head_dim 128 only (PA_ERR_UNSUPPORTED otherwise).  Softmax weights are rounded to the
+ * storage dtype before the P.V product.  T == 0 or S == 0 is a no-op.
+ * Asynchronous on `stream`; no workspace.
+ * ---------------------------------------------------------------------------------- */
+pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void* key_cache,
+                                       const void* value_cache, const int32_t* block_tables,
+                                       const int32_t* context_lens, const int32_t* query_start,
+                                       float scale, int block_size, int num_kv_heads,
+                                       int num_blocks, int num_seqs, int num_heads, int head_dim,
+                                       int max_blocks_per_seq, int num_query_tokens,
+                                       int max_query_len, pa_dtype_t dtype, pa_stream_t stream);
+
 /* Bytes of workspace pa_paged_attention(_ex) needs (0 if no context is split).
  * partition_tokens as in pa_paged_attention_ex. */
 size_t pa_paged_attention_workspace_size(int num_seqs, int num_heads, int head_dim,

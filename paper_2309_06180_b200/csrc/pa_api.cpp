@@ -3,6 +3,8 @@
 // synchronisation on the hot path.
 #include "../../include/pa.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -300,6 +302,94 @@ pa_status_t pa_paged_attention(void* out, const void* query, const void* key_cac
     return pa_paged_attention_ex(out, query, key_cache, value_cache, block_tables, context_lens, scale, block_size,
                                  num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq, max_context_len,
                                  dtype, 0, workspace, workspace_bytes, stream);
+}
+
+namespace {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    return fn;
+}
+
+// rank-2/3 tiled map, 2-byte elements, 128-byte swizzle, zero fill out of bounds
+bool encode_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base, const cuuint64_t* dims,
+                const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, dt, (cuuint32_t)rank, const_cast<void*>(base), dims, strides_bytes, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void* key_cache, const void* value_cache,
+                                       const int32_t* block_tables, const int32_t* context_lens,
+                                       const int32_t* query_start, float scale, int block_size, int num_kv_heads,
+                                       int num_blocks, int num_seqs, int num_heads, int head_dim,
+                                       int max_blocks_per_seq, int num_query_tokens, int max_query_len,
+                                       pa_dtype_t dtype, pa_stream_t stream) {
+    REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
+    if (dtype == PA_F32) return fail(PA_ERR_UNSUPPORTED, "prefill attention supports f16 and bf16 only");
+    if (head_dim != 128) return fail(PA_ERR_UNSUPPORTED, "prefill attention supports head_dim 128 only (got %d)", head_dim);
+    REQUIRE(num_seqs >= 0 && num_seqs <= 65535, "num_seqs must be in [0, 65535] (got %d)", num_seqs);
+    REQUIRE(num_heads > 0 && num_kv_heads > 0 && num_heads <= 65535, "num_heads/num_kv_heads out of range");
+    REQUIRE(num_heads % num_kv_heads == 0, "num_heads (%d) must be a multiple of num_kv_heads (%d)", num_heads,
+            num_kv_heads);
+    const int log2B = log2_pow2(block_size);
+    if (log2B < 0) return fail(PA_ERR_UNSUPPORTED, "block_size must be a power of two in [1,256] (got %d)", block_size);
+    REQUIRE(max_blocks_per_seq > 0, "max_blocks_per_seq must be positive");
+    REQUIRE(num_blocks > 0, "num_blocks must be positive");
+    REQUIRE((int64_t)num_blocks * num_kv_heads * block_size < (1LL << 31), "cache rows must fit in int32");
+    REQUIRE(std::isfinite(scale), "scale must be finite");
+    REQUIRE(num_query_tokens >= 0 && max_query_len >= 0, "token counts must be >= 0");
+    if (num_seqs == 0 || num_query_tokens == 0 || max_query_len == 0) return PA_OK;
+    REQUIRE_PTR(out, 16);
+    REQUIRE_PTR(query, 16);
+    REQUIRE_PTR(key_cache, 16);
+    REQUIRE_PTR(value_cache, 16);
+    REQUIRE_PTR(block_tables, 4);
+    REQUIRE_PTR(context_lens, 4);
+    REQUIRE_PTR(query_start, 4);
+    pa::PrefillParams p{};
+    const CUtensorMapDataType dt =
+        dtype == PA_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    {
+        const cuuint64_t dims[3] = {(cuuint64_t)head_dim, (cuuint64_t)num_heads, (cuuint64_t)num_query_tokens};
+        const cuuint64_t str[2] = {(cuuint64_t)head_dim * 2, (cuuint64_t)num_heads * head_dim * 2};
+        const cuuint32_t box[3] = {64, 1, 128};
+        if (!encode_map(&p.tmap_q, dt, 3, query, dims, str, box))
+            return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the query map");
+    }
+    p.box_rows = std::min(block_size, 16);
+    {
+        const cuuint64_t dims[2] = {(cuuint64_t)head_dim, (cuuint64_t)num_blocks * num_kv_heads * block_size};
+        const cuuint64_t str[1] = {(cuuint64_t)head_dim * 2};
+        const cuuint32_t box[2] = {64, (cuuint32_t)p.box_rows};
+        if (!encode_map(&p.tmap_k, dt, 2, key_cache, dims, str, box) ||
+            !encode_map(&p.tmap_v, dt, 2, value_cache, dims, str, box))
+            return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the cache maps");
+    }
+    p.out = out;
+    p.block_tables = block_tables;
+    p.context_lens = context_lens;
+    p.query_start = query_start;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    p.log2B = log2B;
+    p.H = num_heads;
+    p.H_kv = num_kv_heads;
+    p.G = num_heads / num_kv_heads;
+    p.W = max_blocks_per_seq;
+    cudaError_t e = pa::launch_prefill(p, (int)dtype, num_seqs, max_query_len, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "paged_prefill_kernel launch");
+    return PA_OK;
 }
 
 pa_status_t pa_reshape_and_cache(const void* key, const void* value, void* key_cache, void* value_cache,

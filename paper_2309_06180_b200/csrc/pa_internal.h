@@ -1,6 +1,7 @@
 // pa_internal.h -- host/device interface between the C ABI layer and the kernels.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -8,6 +9,21 @@
 #include <utility>
 
 namespace pa {
+
+// Multi-token causal attention over the paged cache (pa_prefill.cu, N4).  TMA tensor maps
+// are built by the host for every call (they hold the tensors' base addresses).
+struct PrefillParams {
+    CUtensorMap tmap_q;           // query [T][H][D], box {64, 1, 128}, 128-byte swizzle
+    CUtensorMap tmap_k;           // key cache as [NB*H_kv*B][D], box {64, box_rows}
+    CUtensorMap tmap_v;           // value cache, same
+    void* out;                    // [T][H][D]
+    const int32_t* block_tables;  // [S][W]
+    const int32_t* context_lens;  // [S]
+    const int32_t* query_start;   // [S+1]
+    float scale_log2;
+    int log2B, H, H_kv, G, W;
+    int box_rows;                 // min(block_size, 16) tokens per TMA box
+};
 
 struct AttnParams {
     void* out;                  // [S][H][D]
@@ -107,6 +123,8 @@ size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int g
 // sched: 0 = grid, 1 = persistent, 2 = coop, 3 = persistent coop, 4 = sharing-aware groups, 5 = listed coop
 cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int sched, size_t smem,
                              cudaStream_t stream);
+size_t prefill_smem_bytes();
+cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, cudaStream_t stream);
 cudaError_t launch_debug_gather(const GatherParams& p, int dtype, int head_dim, int num_seqs, cudaStream_t stream);
 cudaError_t launch_reshape_and_cache(const CacheWriteParams& p, cudaStream_t stream);
 cudaError_t launch_copy_blocks(const CopyBlocksParams& p, int num_layers, int num_pairs, cudaStream_t stream);

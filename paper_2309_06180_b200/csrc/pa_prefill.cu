@@ -1,0 +1,379 @@
+// pa_prefill.cu -- multi-token (prefill / chunked-prefill / shared-prefix suffix) paged
+// attention on the sm_100 tensor cores.
+//
+// Query token i of sequence s (i < q_len_s) sits at logical position
+// ctx_s - q_len_s + i and attends causally to every cached token t <= that position,
+// read through the block table (Eq.3/Eq.4; prompt phase P:145-147,
+// shared prefix P:334-338: "the prompt phase computation only needs to execute on the
+// user's task input").  The new tokens' K/V are already in the cache
+// (pa_reshape_and_cache with a multi-token slot mapping, reading c5).
+//
+// One CTA = (tile of 128 query tokens, query head, sequence), 128 threads.  Thread 0
+// drives the Tensor Memory Accelerator and the tensor cores; every thread owns one
+// query row for the softmax:
+//   * Q tile [128 x 128] and, per 128-token KV tile, K and V ([128 x 128] each) are
+//     brought into shared memory by TMA tensor copies with the 128-byte swizzle (K and V
+//     gathered block by block through the block table), double-buffered;
+//   * S = Q K^T by 8 tcgen05.mma (M=128, N=128, K=16) into tensor memory (fp32);
+//   * threads read S rows back with tcgen05.ld, apply scale + causal mask, online
+//     softmax in the exp2 domain, and write P (storage dtype) to shared memory in the
+//     swizzled K-major layout;
+//   * O_t = P V by 8 tcgen05.mma (B operand V read MN-major) into tensor memory; threads
+//     fold it into their fp32 O row: O = O*alpha + O_t.
+// P is rounded to the storage dtype before the second product (the FlashAttention
+// convention); the parity tolerance covers it.
+#include <cuda.h>
+
+#include "pa_common.cuh"
+#include "pa_internal.h"
+
+namespace pa {
+
+namespace {
+
+// ---- tcgen05 / TMA wrappers ------------------------------------------------------------
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// D[tmem] (+)= A[smem desc] * B[smem desc], kind::f16 (fp16/bf16 in, fp32 accumulate)
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive on `bar` when every tcgen05.mma issued so far by this thread has completed
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+// 32 consecutive fp32 columns of this thread's TMEM lane (32x32b shape, x32)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15])),
+        "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])), "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])),
+        "r"(__float_as_uint(v[20])), "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+        "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])), "r"(__float_as_uint(v[27])),
+        "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])), "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_u32(smem_dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(smem_dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// UMMA shared-memory descriptor, 128-byte swizzle (layout type 2), Blackwell version 1.
+//   K-major:  8-row x 128-byte atoms, SBO = 1024 B between 8-row groups, LBO unused (1).
+//   MN-major: 64-element (128-byte) rows along N, SBO = 1024 B between 8-row K groups,
+//             LBO = byte stride between 64-element N chunks.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor, kind::f16: fp32 accumulate, M=128, N=128.
+__host__ __device__ constexpr uint32_t umma_idesc(bool bf16, bool b_mn_major) {
+    return (1u << 4)                        // c_format = F32
+           | ((bf16 ? 1u : 0u) << 7)        // a_format
+           | ((bf16 ? 1u : 0u) << 10)       // b_format
+           | (0u << 15)                     // a K-major
+           | ((b_mn_major ? 1u : 0u) << 16) // b major
+           | ((128u >> 3) << 17)            // N
+           | ((128u >> 4) << 24);           // M
+}
+
+constexpr int kQ = 128;        // query rows per CTA
+constexpr int kN = 128;        // KV tokens per tile
+constexpr int kHalf = 128 * 128;  // bytes of one [128 rows][64 elements] swizzled half (2-byte elements)
+
+}  // namespace
+
+template <typename T>
+__global__ void __launch_bounds__(128, 1) paged_prefill_kernel(const __grid_constant__ PrefillParams p) {
+    constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment for the swizzle atoms
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* sQ = smem;                   // [2 halves][128][64]
+    unsigned char* sK = smem + 2 * kHalf;       // [2 stages][2 halves][128][64]
+    unsigned char* sV = sK + 4 * kHalf;         // [2 stages][2 halves][128][64]
+    unsigned char* sP = sV + 4 * kHalf;         // [2 halves][128][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kHalf);  // q, kv[2], mma
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+
+    const int qt = blockIdx.x, h = blockIdx.y, s = blockIdx.z;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    pdl_wait();
+    const int qs = p.query_start[s], qlen = p.query_start[s + 1] - qs;
+    const int q0 = qt * kQ;
+    if (q0 >= qlen) return;  // CTA-uniform
+    const int ctx = p.context_lens[s];
+    const int base_pos = ctx - qlen;  // logical position of query token 0
+    const int kv_len = base_pos + min(q0 + kQ, qlen);  // tokens this tile may attend to
+    const int ntiles = (kv_len + kN - 1) / kN;
+    const int kvh = h / p.G;
+    const int B = 1 << p.log2B;
+    const int32_t* btrow = p.block_tables + (int64_t)s * p.W;
+
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc(tmem_slot, 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem_S = tmem, tmem_O = tmem + 128;  // columns [0,128) S, [128,256) O_t
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+
+    auto load_kv = [&](int j, int st) {  // thread 0 only
+        unsigned char* k0 = sK + st * 2 * kHalf;
+        unsigned char* v0 = sV + st * 2 * kHalf;
+        const int br = p.box_rows;
+        uint32_t bytes = 0;
+        for (int t = j * kN; t < min(kv_len, (j + 1) * kN); t += br) bytes += 2u * 2u * br * 128u;
+        mbar_arrive_expect_tx(&bars[1 + st], bytes);
+        for (int t = j * kN; t < min(kv_len, (j + 1) * kN); t += br) {
+            const int blk = __ldg(btrow + (t >> p.log2B));
+            const int row = (blk * p.H_kv + kvh) * B + (t & (B - 1));
+            const int r = (t - j * kN) * 128;  // byte offset of the row inside a half
+            tma_load_2d(k0 + r, &p.tmap_k, 0, row, &bars[1 + st]);
+            tma_load_2d(k0 + kHalf + r, &p.tmap_k, 64, row, &bars[1 + st]);
+            tma_load_2d(v0 + r, &p.tmap_v, 0, row, &bars[1 + st]);
+            tma_load_2d(v0 + kHalf + r, &p.tmap_v, 64, row, &bars[1 + st]);
+        }
+    };
+
+    if (tid == 0) {
+        mbar_arrive_expect_tx(&bars[0], 2u * kHalf);
+        tma_load_3d(sQ, &p.tmap_q, 0, h, qs + q0, &bars[0]);
+        tma_load_3d(sQ + kHalf, &p.tmap_q, 64, h, qs + q0, &bars[0]);
+        if (ntiles > 0) load_kv(0, 0);
+    }
+
+    // this thread's query row
+    const int r = tid;
+    const bool row_valid = q0 + r < qlen;
+    const int pos = row_valid ? base_pos + q0 + r : -1;
+    float m = -INFINITY, l = 0.f;
+    const uint32_t idesc_s = umma_idesc(kBF16, false), idesc_o = umma_idesc(kBF16, true);
+    uint32_t mma_phase = 0;
+
+    mbar_wait(&bars[0], 0);
+    for (int j = 0; j < ntiles; ++j) {
+        const int st = j & 1;
+        if (tid == 0 && j + 1 < ntiles) load_kv(j + 1, st ^ 1);
+        mbar_wait(&bars[1 + st], (j >> 1) & 1);
+        unsigned char* kst = sK + st * 2 * kHalf;
+        unsigned char* vst = sV + st * 2 * kHalf;
+        const int tile0 = j * kN;
+        if (tile0 + kN > kv_len) {  // last tile: zero V rows past the attended range
+            const int first = kv_len - tile0;
+            for (int i = tid; i < (kN - first) * 16; i += 128) {
+                const int rr = first + i / 16, ch = i % 16;
+                uint4* dst = reinterpret_cast<uint4*>(vst + (ch >> 3) * kHalf + rr * 128 + (ch & 7) * 16);
+                *dst = make_uint4(0, 0, 0, 0);
+            }
+            fence_proxy_async_smem();
+        }
+        __syncthreads();
+        // ---- S = Q K^T ------------------------------------------------------------------
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t half = (k >> 2) * kHalf, koff = (k & 3) * 32;
+                const uint64_t a = umma_desc_sw128(smem_u32(sQ) + half + koff, 16, 1024);
+                const uint64_t b = umma_desc_sw128(smem_u32(kst) + half + koff, 16, 1024);
+                umma_f16(tmem_S, a, b, idesc_s, k > 0);
+            }
+            umma_commit(&bars[3]);
+        }
+        mbar_wait(&bars[3], mma_phase);
+        mma_phase ^= 1u;
+        tc_fence_after();
+        // ---- softmax on this row: pass 1 row max, pass 2 exp / sum / P -------------------
+        const int lim = row_valid ? min(pos + 1, kv_len) - tile0 : 0;  // valid columns [0, lim)
+        float mt = -INFINITY;
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+            float v[32];
+            tmem_ld32(tmem_S + lane_off + c0, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (c0 + i < lim) mt = fmaxf(mt, v[i] * p.scale_log2);
+        }
+        const float mn = fmaxf(m, mt);
+        const float ms = (mn == -INFINITY) ? 0.f : mn;
+        const float alpha = ex2(m - ms);
+        float rs = 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+            float v[32];
+            tmem_ld32(tmem_S + lane_off + c0, v);
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+                const float a0 = (c0 + i < lim) ? ex2(v[i] * p.scale_log2 - ms) : 0.f;
+                const float a1 = (c0 + i + 1 < lim) ? ex2(v[i + 1] * p.scale_log2 - ms) : 0.f;
+                T t0 = Elem<T>::from_f32(a0), t1 = Elem<T>::from_f32(a1);
+                rs += Elem<T>::to_f32(t0) + Elem<T>::to_f32(t1);  // l sums what P V actually uses
+                pk[i / 2] = (uint32_t)(*reinterpret_cast<uint16_t*>(&t0)) |
+                            ((uint32_t)(*reinterpret_cast<uint16_t*>(&t1)) << 16);
+            }
+            // columns c0..c0+31 of row r -> half (c0/64), chunks (c0%64)/8 .. +3, swizzled
+            unsigned char* prow = sP + (c0 >> 6) * kHalf + r * 128;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int ch = ((c0 & 63) >> 3) + q;
+                *reinterpret_cast<uint4*>(prow + ((ch ^ (r & 7)) << 4)) =
+                    make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            }
+        }
+        l = l * alpha + rs;
+        m = mn;
+        // O (tensor memory, fp32) *= alpha before this tile's P V accumulates into it;
+        // skipped when no row of the warp changed its max
+        if (j > 0 && !__all_sync(0xffffffffu, alpha == 1.f)) {
+#pragma unroll
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+                float v[32];
+                tmem_ld32(tmem_O + lane_off + c0, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] *= alpha;
+                tmem_st32(tmem_O + lane_off + c0, v);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        // ---- O_t = P V -------------------------------------------------------------------
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {  // K = tokens, 16 per step
+                const uint64_t a = umma_desc_sw128(smem_u32(sP) + (k >> 2) * kHalf + (k & 3) * 32, 16, 1024);
+                const uint64_t b = umma_desc_sw128(smem_u32(vst) + k * 2048, kHalf, 1024);
+                umma_f16(tmem_O, a, b, idesc_o, (j > 0) | (k > 0));
+            }
+            umma_commit(&bars[3]);
+        }
+        mbar_wait(&bars[3], mma_phase);
+        mma_phase ^= 1u;
+        tc_fence_after();
+    }
+
+    // ---- epilogue: out row = O / l -----------------------------------------------------
+    {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        T* orow = static_cast<T*>(p.out) + ((int64_t)(qs + q0 + r) * p.H + h) * 128;
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+            float v[32];
+            if (ntiles > 0) {
+                tmem_ld32(tmem_O + lane_off + c0, v);  // warp-collective: every lane loads
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            }
+            if (row_valid) {
+#pragma unroll
+                for (int c1 = 0; c1 < 32; c1 += 8) {
+                    alignas(16) T w[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) w[i] = Elem<T>::from_f32(v[c1 + i] * inv);
+                    *reinterpret_cast<uint4*>(orow + c0 + c1) = *reinterpret_cast<const uint4*>(w);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 256);
+    }
+}
+
+size_t prefill_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 64; }
+
+cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, cudaStream_t stream) {
+    const size_t smem = prefill_smem_bytes();
+    const dim3 grid((max_query_len + kQ - 1) / kQ, p.H, num_seqs);
+    if (dtype == 1) {
+        static bool configured = false;
+        if (!configured) {
+            cudaError_t e = cudaFuncSetAttribute(paged_prefill_kernel<__half>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            configured = true;
+        }
+        return launch_k(paged_prefill_kernel<__half>, grid, dim3(128), smem, stream, p);
+    }
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(paged_prefill_kernel<__nv_bfloat16>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    return launch_k(paged_prefill_kernel<__nv_bfloat16>, grid, dim3(128), smem, stream, p);
+}
+
+}  // namespace pa

@@ -112,6 +112,25 @@ def paged_attention_decode_shared(out, query, key, value, key_cache, value_cache
     return out
 
 
+def paged_prefill_attention(out, query, key_cache, value_cache, block_tables, context_lens, query_start,
+                            scale: float, max_query_len: int = 0, stream=None):
+    """Causal multi-token attention over the paged cache (pa.h):
+    query/out [T][H][D] with sequence s's rows in [query_start[s], query_start[s+1]), the
+    last q_len of its context_lens[s] cached tokens.  tcgen05 tensor cores, f16/bf16, D=128.
+    max_query_len sizes the grid; 0 reads it from query_start (a device->host sync)."""
+    T, H, D = query.shape
+    NB, hk, B, _ = key_cache.shape
+    S, W = block_tables.shape
+    if max_query_len <= 0:
+        max_query_len = int((query_start[1:] - query_start[:-1]).max().item()) if S > 0 else 0
+    check(_lib.raw().pa_paged_prefill_attention(
+        _dev(out, "out"), _dev(query, "query"), _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"),
+        _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"), _dev(query_start, "query_start"),
+        float(scale), B, hk, NB, S, H, D, W, T, int(max_query_len), _code(query), _stream(stream)),
+        "pa_paged_prefill_attention")
+    return out
+
+
 def reshape_and_cache(key, value, key_cache, value_cache, slot_mapping, stream=None):
     """Fused reshape + block write: key/value [T][H_kv][D] into the caches at
     slot_mapping (int64 [T], -1 = skip)."""

@@ -42,6 +42,9 @@ def test_library_is_sm100a_only():
     assert "UBLKCP" in sass          # bulk async copies global -> shared
     assert "FHFMA" in sass           # mixed-precision FMA for q.k
     assert "FFMA2" in sass           # packed fp32x2 FMA for p*V
+    assert "UTCHMMA" in sass         # tcgen05.mma kind::f16 (prefill attention, N4)
+    assert "UTMALDG" in sass         # TMA tensor loads (prefill attention)
+    assert "LDTM" in sass            # tcgen05.ld tensor memory -> registers
 
 
 FAKE = 0x100000  # aligned, never dereferenced: every call below fails validation first
@@ -73,6 +76,38 @@ def attn(**kw):
 def test_attention_argument_validation(kw, status):
     assert attn(**kw) == status
     assert _lib.last_error() != ""
+
+
+def prefill(**kw):
+    a = dict(out=FAKE, q=FAKE, kc=FAKE, vc=FAKE, bt=FAKE, cl=FAKE, qs=FAKE, scale=0.125, B=16, hkv=2, NB=64, S=4, H=2,
+             D=128, W=8, T=100, mql=40, dt=2)
+    a.update(kw)
+    return L.pa_paged_prefill_attention(a["out"], a["q"], a["kc"], a["vc"], a["bt"], a["cl"], a["qs"], a["scale"],
+                                        a["B"], a["hkv"], a["NB"], a["S"], a["H"], a["D"], a["W"], a["T"], a["mql"],
+                                        a["dt"], None)
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(D=64), UNSUPPORTED),
+    (dict(dt=0), UNSUPPORTED),
+    (dict(B=3), UNSUPPORTED),
+    (dict(H=3, hkv=2), INVALID),
+    (dict(NB=0), INVALID),
+    (dict(out=None), INVALID),
+    (dict(q=FAKE + 8), INVALID),
+    (dict(qs=FAKE + 2), INVALID),
+    (dict(dt=7), INVALID),
+    (dict(scale=float("inf")), INVALID),
+    (dict(NB=1 << 28, hkv=8, H=8), INVALID),
+])
+def test_prefill_argument_validation(kw, status):
+    assert prefill(**kw) == status
+    assert _lib.last_error() != ""
+
+
+def test_prefill_empty_is_noop():
+    assert prefill(T=0, out=None, q=None) == OK
+    assert prefill(S=0, out=None) == OK
 
 
 def test_attention_zero_seqs_is_noop():
