@@ -1,0 +1,101 @@
+"""Prompt-phase (N4) benchmark: pa_paged_prefill_attention on the synth.prefill workloads.
+
+Per config, one JSON line: kernel time (CUDA events on the launching stream, mean over
+`--iters` back-to-back launches after warm-up), algorithmic TFLOP/s (4*D flops per
+(query row, head, attended token), causal) against the measured dense bf16 peak of
+MEASURED_PEAKS.json (f16 has the same nominal tensor rate), query tokens/s, and as
+context torch's scaled_dot_product_attention on the same prompts with CONTIGUOUS K/V
+(no paging; library kernels, padded batch) where the prompts are uniform (p_2k).
+Caches hold U(-1,1) values; unused slots are NaN.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2309_06180_b200 as pa  # noqa: E402
+from synth.prefill import PREFILL_CONFIGS, algorithmic_flops, make_prefill  # noqa: E402
+
+D = 128
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["bf16_tflops"]), "MEASURED_PEAKS.json bf16_tflops (burst)"
+    except Exception:
+        return 2250.0, "nominal dense bf16 (B200_PROFILING.md fallback)"
+
+
+def time_it(fn, iters, warmup=5):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(iters):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / iters
+
+
+def build(c, dev="cuda"):
+    dt = torch.float16 if c["dtype"] == "f16" else torch.bfloat16
+    g = torch.Generator(device=dev)
+    g.manual_seed(c["seed"])
+    H, Hk, B, NB = c["H"], c["H_kv"], c["B"], c["num_blocks"]
+    kc = (torch.rand((NB, Hk, B, D), generator=g, device=dev) * 2 - 1).to(dt)
+    vc = (torch.rand((NB, Hk, B, D), generator=g, device=dev) * 2 - 1).to(dt)
+    T = int(c["qlen"].sum())
+    q = (torch.rand((T, H, D), generator=g, device=dev) * 2 - 1).to(dt)
+    qs = torch.as_tensor(np.concatenate([[0], np.cumsum(c["qlen"])]).astype(np.int32), device=dev)
+    return q, kc, vc, torch.as_tensor(c["block_tables"], device=dev), \
+        torch.as_tensor(c["ctx"].astype(np.int32), device=dev), qs
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default=",".join(PREFILL_CONFIGS))
+    ap.add_argument("--iters", type=int, default=50)
+    args = ap.parse_args()
+    peak, peak_src = peaks()
+    for name in args.configs.split(","):
+        c = make_prefill(name)
+        q, kc, vc, bt, cl, qs = build(c)
+        out = torch.empty_like(q)
+        mql = int(c["qlen"].max())
+        scale = 1.0 / np.sqrt(D)
+        fn = lambda: pa.paged_prefill_attention(out, q, kc, vc, bt, cl, qs, scale, max_query_len=mql)  # noqa: E731
+        pa.take_launch_count()
+        t = time_it(fn, args.iters)
+        launches = pa.take_launch_count() / (args.iters + 5)
+        flops = algorithmic_flops(c["ctx"], c["qlen"], c["H"], D)
+        tf = flops / t / 1e12
+        res = {"config": name, "seqs": len(c["ctx"]), "query_tokens": int(c["qlen"].sum()),
+               "mean_ctx": round(float(c["ctx"].mean()), 1), "ms": round(t * 1e3, 4),
+               "tflops": round(tf, 1), "peak_tflops": peak, "peak_src": peak_src, "frac": round(tf / peak, 3),
+               "query_tokens_per_s": round(c["qlen"].sum() / t, 0), "launches_per_call": launches}
+        if name == "p_2k":  # library context: contiguous causal SDPA, same flops
+            S, n = len(c["ctx"]), int(c["ctx"][0])
+            qq = q.view(S, n, c["H"], D).transpose(1, 2).contiguous()
+            kk = torch.rand_like(qq)
+            vv = torch.rand_like(qq)
+            ts = time_it(lambda: torch.nn.functional.scaled_dot_product_attention(qq, kk, vv, is_causal=True),
+                         args.iters)
+            res["sdpa_contiguous_ms"] = round(ts * 1e3, 4)
+            res["sdpa_contiguous_tflops"] = round(flops / ts / 1e12, 1)
+        print(json.dumps(res), flush=True)
+        del q, kc, vc, out
+
+
+if __name__ == "__main__":
+    main()
