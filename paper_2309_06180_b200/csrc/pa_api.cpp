@@ -373,8 +373,11 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
         const cuuint64_t dims[2] = {(cuuint64_t)head_dim, (cuuint64_t)num_blocks * num_kv_heads * block_size};
         const cuuint64_t str[1] = {(cuuint64_t)head_dim * 2};
         const cuuint32_t box[2] = {64, (cuuint32_t)p.box_rows};
+        const cuuint32_t box1[2] = {64, 1};
         if (!encode_map(&p.tmap_k, dt, 2, key_cache, dims, str, box) ||
-            !encode_map(&p.tmap_v, dt, 2, value_cache, dims, str, box))
+            !encode_map(&p.tmap_v, dt, 2, value_cache, dims, str, box) ||
+            !encode_map(&p.tmap_k1, dt, 2, key_cache, dims, str, box1) ||
+            !encode_map(&p.tmap_v1, dt, 2, value_cache, dims, str, box1))
             return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the cache maps");
     }
     p.out = out;

@@ -16,6 +16,8 @@ struct PrefillParams {
     CUtensorMap tmap_q;           // query [T][H][D], box {64, 1, 128}, 128-byte swizzle
     CUtensorMap tmap_k;           // key cache as [NB*H_kv*B][D], box {64, box_rows}
     CUtensorMap tmap_v;           // value cache, same
+    CUtensorMap tmap_k1;          // key cache, box {64, 1} (tails shorter than box_rows)
+    CUtensorMap tmap_v1;          // value cache, box {64, 1}
     void* out;                    // [T][H][D]
     const int32_t* block_tables;  // [S][W]
     const int32_t* context_lens;  // [S]

@@ -95,6 +95,42 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
         : "memory");
 }
 
+// D[tmem] (+)= A[tmem] * B[smem desc]: A (16-bit, K-major) read from tensor memory, two
+// elements per 32-bit column (the "TS" form)
+__device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
+// 32 consecutive fp32 columns without the trailing wait (caller issues tmem_ld_wait)
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, float (&v)[32]) {
+    uint32_t* r = reinterpret_cast<uint32_t*>(v);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
@@ -351,29 +387,316 @@ __global__ void __launch_bounds__(128, 1) paged_prefill_kernel(const __grid_cons
     }
 }
 
+// ---- v2: warp-specialised, two query tiles per CTA ---------------------------------------
+// Warps 0-3 / 4-7: softmax of query tile 0 / 1 (thread = row = TMEM lane); warp 8: TMA
+// producer; warp 9: tcgen05.mma issuer.  Tensor memory (512 columns): S_0, S_1, O_0, O_1
+// (128 fp32 columns each); P_t (storage dtype, packed two per column) overwrites the first
+// 64 columns of S_t and feeds O_t += P_t V as the tensor-memory A operand.  K and V are
+// double-buffered separately, so S_t(j+1) = Q_t K_{j+1}^T runs on the tensor cores while
+// the other warp group's softmax of tile j runs on the SM.  Arithmetic is identical to v1.
+constexpr int kWarpsV2 = 10;
+constexpr int kThreadsV2 = kWarpsV2 * 32;
+
+template <typename T>
+__global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const __grid_constant__ PrefillParams p) {
+    constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* sQ = smem;                // [2 tiles][2 halves][128][64]
+    unsigned char* sK = smem + 4 * kHalf;    // [2 stages][2 halves][128][64]
+    unsigned char* sV = sK + 4 * kHalf;      // [2 stages][2 halves][128][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 4 * kHalf);
+    uint64_t* q_full = bars;         // 1
+    uint64_t* k_full = bars + 1;     // 2
+    uint64_t* k_empty = bars + 3;    // 2
+    uint64_t* v_full = bars + 5;     // 2
+    uint64_t* v_empty = bars + 7;    // 2
+    uint64_t* s_full = bars + 9;     // 2 (per query tile)
+    uint64_t* p_full = bars + 11;    // 2
+    uint64_t* o_done = bars + 13;    // 2
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+    // longest work first: the slowest grid dimension walks query-tile pairs backwards
+    const int h = blockIdx.x, s = blockIdx.y, qp = gridDim.z - 1 - blockIdx.z;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    pdl_wait();
+    const int qs = p.query_start[s], qlen = p.query_start[s + 1] - qs;
+    const int q0 = qp * 2 * kQ;
+    if (q0 >= qlen) return;  // CTA-uniform
+    const int ctx = p.context_lens[s];
+    const int base_pos = ctx - qlen;
+    // tokens query tile t may attend to, and its number of 128-token KV tiles
+    const int kv0 = base_pos + min(q0 + kQ, qlen);
+    const int kv1 = q0 + kQ < qlen ? base_pos + min(q0 + 2 * kQ, qlen) : 0;
+    const int n0 = kv0 > 0 ? (kv0 + kN - 1) / kN : 0;
+    const int n1 = kv1 > 0 ? (kv1 + kN - 1) / kN : 0;
+    const int kv_len = max(kv0, kv1);
+    const int n = max(n0, n1);
+
+    if (tid == 0) {
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], kQ);
+            mbar_init(&o_done[i], 1);
+        }
+        fence_mbar_init();
+    }
+    // V stages start zeroed: rows past kv_len of the last tile are never loaded and must
+    // not hold NaN bit patterns (P = 0 there, but 0 * NaN = NaN in the MMA)
+    for (int i = tid; i < 4 * kHalf / 16; i += kThreadsV2)
+        reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+    if (warp == 0) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int kvh = h / p.G;
+    const int B = 1 << p.log2B;
+
+    if (warp == 8) {
+        // ---------------- TMA producer ----------------
+        const int32_t* btrow = p.block_tables + (int64_t)s * p.W;
+        auto load_tile = [&](unsigned char* dst0, const CUtensorMap* map, const CUtensorMap* map1, int j,
+                             uint64_t* bar) {
+            const int t0 = j * kN, t1 = min(kv_len, t0 + kN);
+            const int br = p.box_rows;
+            const int full_end = t0 + (t1 - t0) / br * br;
+            const uint32_t bytes = (uint32_t)(t1 - t0) * 256u;
+            if (lane == 0) {
+                mbar_arrive_expect_tx(bar, bytes);
+                for (int t = t0; t < t1;) {
+                    const int blk = __ldg(btrow + (t >> p.log2B));
+                    const int row = (blk * p.H_kv + kvh) * B + (t & (B - 1));
+                    const int off = (t - t0) * 128;
+                    const CUtensorMap* m = t < full_end ? map : map1;
+                    tma_load_2d(dst0 + off, m, 0, row, bar);
+                    tma_load_2d(dst0 + kHalf + off, m, 64, row, bar);
+                    t += t < full_end ? br : 1;
+                }
+            }
+            __syncwarp();
+        };
+        if (lane == 0) {
+            mbar_arrive_expect_tx(q_full, 4u * kHalf);
+            tma_load_3d(sQ, &p.tmap_q, 0, h, qs + q0, q_full);
+            tma_load_3d(sQ + kHalf, &p.tmap_q, 64, h, qs + q0, q_full);
+            tma_load_3d(sQ + 2 * kHalf, &p.tmap_q, 0, h, qs + q0 + kQ, q_full);
+            tma_load_3d(sQ + 3 * kHalf, &p.tmap_q, 64, h, qs + q0 + kQ, q_full);
+        }
+        for (int j = 0; j < n; ++j) {
+            const int st = j & 1;
+            if (j >= 2) mbar_wait(&k_empty[st], ((j - 2) >> 1) & 1);
+            load_tile(sK + st * 2 * kHalf, &p.tmap_k, &p.tmap_k1, j, &k_full[st]);
+            if (j >= 2) mbar_wait(&v_empty[st], ((j - 2) >> 1) & 1);
+            load_tile(sV + st * 2 * kHalf, &p.tmap_v, &p.tmap_v1, j, &v_full[st]);
+        }
+    } else if (warp == 9) {
+        // ---------------- MMA issuer ----------------
+        const uint32_t idesc_s = umma_idesc(kBF16, false), idesc_o = umma_idesc(kBF16, true);
+        auto issue_S = [&](int t, int j) {  // S_t = Q_t K_j^T
+            if (lane == 0) {
+                const uint32_t q = smem_u32(sQ) + t * 2 * kHalf, k = smem_u32(sK) + (j & 1) * 2 * kHalf;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+                    umma_f16(tmem + t * 128, umma_desc_sw128(q + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024),
+                             idesc_s, kk > 0);
+                }
+                umma_commit(&s_full[t]);
+            }
+            __syncwarp();
+        };
+        auto issue_PV = [&](int t, int j) {  // O_t (+)= P_t V_j, P_t in tensor memory
+            if (lane == 0) {
+                const uint32_t v = smem_u32(sV) + (j & 1) * 2 * kHalf;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                                umma_desc_sw128(v + kk * 2048, kHalf, 1024), idesc_o, (j > 0) | (kk > 0));
+                umma_commit(&o_done[t]);
+            }
+            __syncwarp();
+        };
+        mbar_wait(q_full, 0);
+        if (n > 0) {
+            mbar_wait(&k_full[0], 0);
+            tc_fence_after();
+            if (n0 > 0) issue_S(0, 0);
+            if (n1 > 0) issue_S(1, 0);
+            if (lane == 0) umma_commit(&k_empty[0]);
+        }
+        for (int j = 0; j < n; ++j) {
+            const int st = j & 1;
+            mbar_wait(&v_full[st], (j >> 1) & 1);
+            if (j < n0) {
+                mbar_wait(&p_full[0], j & 1);
+                tc_fence_after();
+                issue_PV(0, j);
+            }
+            const bool more = j + 1 < n;
+            if (more) {
+                mbar_wait(&k_full[st ^ 1], ((j + 1) >> 1) & 1);
+                tc_fence_after();
+                if (j + 1 < n0) issue_S(0, j + 1);
+            }
+            if (j < n1) {
+                mbar_wait(&p_full[1], j & 1);
+                tc_fence_after();
+                issue_PV(1, j);
+            }
+            if (lane == 0) umma_commit(&v_empty[st]);
+            if (more) {
+                if (j + 1 < n1) issue_S(1, j + 1);
+                if (lane == 0) umma_commit(&k_empty[st ^ 1]);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ---------------- softmax warp groups ----------------
+        const int t = warp >> 2;
+        const int r = tid & (kQ - 1);
+        const int nt = t == 0 ? n0 : n1;
+        const int kvt = t == 0 ? kv0 : kv1;
+        const int row = q0 + t * kQ + r;
+        const bool row_valid = row < qlen;
+        const int pos = row_valid ? base_pos + row : -1;
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + 256 + t * 128 + lane_off;
+        float m = -INFINITY, l = 0.f;
+        for (int j = 0; j < nt; ++j) {
+            mbar_wait(&s_full[t], j & 1);
+            tc_fence_after();
+            float sa[32], sb[32], sc[32], sd[32];
+            tmem_ld32_nw(tS + 0, sa);
+            tmem_ld32_nw(tS + 32, sb);
+            tmem_ld32_nw(tS + 64, sc);
+            tmem_ld32_nw(tS + 96, sd);
+            tmem_ld_wait();
+            const int lim = row_valid ? min(pos + 1, kvt) - j * kN : 0;
+            float mt = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                if (i < lim) mt = fmaxf(mt, sa[i] * p.scale_log2);
+                if (i + 32 < lim) mt = fmaxf(mt, sb[i] * p.scale_log2);
+                if (i + 64 < lim) mt = fmaxf(mt, sc[i] * p.scale_log2);
+                if (i + 96 < lim) mt = fmaxf(mt, sd[i] * p.scale_log2);
+            }
+            const float mn = fmaxf(m, mt);
+            const float ms = (mn == -INFINITY) ? 0.f : mn;
+            const float alpha = ex2(m - ms);
+            float rs = 0.f;
+            auto emit = [&](const float (&x)[32], int c0) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    const float a0 = (c0 + i < lim) ? ex2(x[i] * p.scale_log2 - ms) : 0.f;
+                    const float a1 = (c0 + i + 1 < lim) ? ex2(x[i + 1] * p.scale_log2 - ms) : 0.f;
+                    T t0 = Elem<T>::from_f32(a0), t1 = Elem<T>::from_f32(a1);
+                    rs += Elem<T>::to_f32(t0) + Elem<T>::to_f32(t1);
+                    pk[i / 2] = (uint32_t)(*reinterpret_cast<uint16_t*>(&t0)) |
+                                ((uint32_t)(*reinterpret_cast<uint16_t*>(&t1)) << 16);
+                }
+                tmem_st16(tS + c0 / 2, pk);
+            };
+            emit(sa, 0);
+            emit(sb, 32);
+            emit(sc, 64);
+            emit(sd, 96);
+            // P_t is out; now O_t *= alpha (PV_t(j-1) has completed: S_t(j) was issued after it)
+            if (j > 0) {
+                mbar_wait(&o_done[t], (j - 1) & 1);  // O_t complete up to tile j-1
+                tc_fence_after();
+                if (!__all_sync(0xffffffffu, alpha == 1.f)) {
+#pragma unroll
+                    for (int c0 = 0; c0 < 128; c0 += 32) {
+                        float v[32];
+                        tmem_ld32_nw(tO + c0, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] *= alpha;
+                        tmem_st32(tO + c0, v);
+                    }
+                }
+            }
+            l = l * alpha + rs;
+            m = mn;
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&p_full[t]);
+        }
+        // epilogue: out row = O_t / l
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        T* orow = static_cast<T*>(p.out) + ((int64_t)(qs + row) * p.H + h) * 128;
+        if (nt > 0) {
+            mbar_wait(&o_done[t], (nt - 1) & 1);
+            tc_fence_after();
+        }
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+            float v[32];
+            if (nt > 0) {
+                tmem_ld32_nw(tO + c0, v);
+                tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            }
+            if (row_valid) {
+#pragma unroll
+                for (int c1 = 0; c1 < 32; c1 += 8) {
+                    alignas(16) T w[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) w[i] = Elem<T>::from_f32(v[c1 + i] * inv);
+                    *reinterpret_cast<uint4*>(orow + c0 + c1) = *reinterpret_cast<const uint4*>(w);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 size_t prefill_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 64; }
+size_t prefill_ws_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 160; }
+
+namespace {
+template <typename Kern>
+cudaError_t set_smem(Kern k, size_t smem) {
+    return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+int prefill_variant() {
+    const char* e = getenv("PA_PREFILL");
+    return (e && e[0] == '1') ? 1 : 2;
+}
+}  // namespace
 
 cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, cudaStream_t stream) {
-    const size_t smem = prefill_smem_bytes();
-    const dim3 grid((max_query_len + kQ - 1) / kQ, p.H, num_seqs);
-    if (dtype == 1) {
-        static bool configured = false;
-        if (!configured) {
-            cudaError_t e = cudaFuncSetAttribute(paged_prefill_kernel<__half>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            configured = true;
-        }
-        return launch_k(paged_prefill_kernel<__half>, grid, dim3(128), smem, stream, p);
-    }
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(paged_prefill_kernel<__nv_bfloat16>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (prefill_variant() == 1) {
+        const size_t smem = prefill_smem_bytes();
+        const dim3 grid((max_query_len + kQ - 1) / kQ, p.H, num_seqs);
+        cudaError_t e = dtype == 1 ? set_smem(paged_prefill_kernel<__half>, smem)
+                                   : set_smem(paged_prefill_kernel<__nv_bfloat16>, smem);
         if (e != cudaSuccess) return e;
-        configured = true;
+        return dtype == 1 ? launch_k(paged_prefill_kernel<__half>, grid, dim3(128), smem, stream, p)
+                          : launch_k(paged_prefill_kernel<__nv_bfloat16>, grid, dim3(128), smem, stream, p);
     }
-    return launch_k(paged_prefill_kernel<__nv_bfloat16>, grid, dim3(128), smem, stream, p);
+    const size_t smem = prefill_ws_smem_bytes();
+    const dim3 grid(p.H, num_seqs, (max_query_len + 2 * kQ - 1) / (2 * kQ));
+    cudaError_t e = dtype == 1 ? set_smem(paged_prefill_ws_kernel<__half>, smem)
+                               : set_smem(paged_prefill_ws_kernel<__nv_bfloat16>, smem);
+    if (e != cudaSuccess) return e;
+    return dtype == 1 ? launch_k(paged_prefill_ws_kernel<__half>, grid, dim3(kThreadsV2), smem, stream, p)
+                      : launch_k(paged_prefill_ws_kernel<__nv_bfloat16>, grid, dim3(kThreadsV2), smem, stream, p);
 }
 
 }  // namespace pa

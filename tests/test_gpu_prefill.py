@@ -164,3 +164,24 @@ def test_prefill_sharegpt_sized_sampled_rows():
         r = oracle.paged_attention(qb[row:row + 1], kb, vb, btn[s:s + 1], np.array([pos + 1], np.int32), scale, B,
                                    H_kv, "f16")
         assert max_abs(out[row:row + 1], r) <= TOL["f16"]
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_v1_and_warp_specialised_v2_agree(dtype, monkeypatch):
+    """The single-tile kernel (PA_PREFILL=1, P from shared memory) and the warp-specialised
+    two-tile kernel (default, P from tensor memory) perform the same softmax arithmetic; the
+    tensor cores' internal accumulation of the two operand sources may round differently,
+    so they agree to a few output ulps (and each is within TOL of the oracle)."""
+    ctx = [600, 130, 1500, 64, 257, 1000, 300]
+    qlen = [64, 130, 1, 17, 200, 300, 300]
+    q, kc, vc, bt, cl, qs = prefill_problem(ctx, qlen, 16, 8, 2, dtype, seed=91)
+    monkeypatch.setenv("PA_PREFILL", "1")
+    a = run(q, kc, vc, bt, cl, qs, 0.09)
+    monkeypatch.setenv("PA_PREFILL", "2")
+    b = run(q, kc, vc, bt, cl, qs, 0.09)
+    ulp = 2.0 ** -10 if dtype == "f16" else 2.0 ** -7  # output ulp at |o| < 1
+    diff = (a.float() - b.float()).abs().max().item()
+    print(f"v1 vs v2 max |diff| = {diff:.3g}")
+    assert diff <= 2 * ulp
+    r = ref(q, kc, vc, bt, cl, qs, 0.09, 16, 2, dtype)
+    assert max_abs(a, r) <= TOL[dtype] and max_abs(b, r) <= TOL[dtype]
