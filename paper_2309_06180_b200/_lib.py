@@ -11,7 +11,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpagedattn.so")
+# PA_LIB_VARIANT (experiments only): load a variant build (scripts/build_variant.sh), e.g. "pe3" ->
+# libpagedattn_pe3.so next to the default library
+LIB_PATH = os.path.join(_HERE, "libpagedattn%s.so" % ("_" + os.environ["PA_LIB_VARIANT"] if os.environ.get("PA_LIB_VARIANT") else ""))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -44,6 +46,7 @@ _sig("pa_paged_attention_decode", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
 _sig("pa_paged_attention_decode_shared", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32,
                                                 _i32, _i32, _i32, _i32, _i32, _vp, _sz, _vp])
 _sig("pa_paged_prefill_attention", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32] + [_i32] * 10 + [_vp])
+_sig("pa_debug_prefill_trace", _i32, [_vp, _i32])
 _sig("pa_paged_attention_workspace_size", _sz, [_i32, _i32, _i32, _i32, _i32])
 _sig("pa_reshape_and_cache", _i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp])
 _sig("pa_copy_blocks", _i32, [ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i32, _vp, _i32, _i32, _i32, _i32, _i32,

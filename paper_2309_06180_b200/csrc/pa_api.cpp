@@ -305,6 +305,19 @@ pa_status_t pa_paged_attention(void* out, const void* query, const void* key_cac
 }
 
 namespace {
+long long* g_prefill_trace = nullptr;  // pa_debug_prefill_trace
+int g_prefill_trace_ctas = 0;
+}  // namespace
+
+// Timing experiments: the prefill kernel records clock64() events (64 slots per CTA) of the
+// first max_ctas CTAs into `buf` (device, 64 * max_ctas int64).  NULL disables.
+pa_status_t pa_debug_prefill_trace(void* buf, int max_ctas) {
+    g_prefill_trace = static_cast<long long*>(buf);
+    g_prefill_trace_ctas = buf ? max_ctas : 0;
+    return PA_OK;
+}
+
+namespace {
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -368,7 +381,7 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
         if (!encode_map(&p.tmap_q, dt, 3, query, dims, str, box))
             return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the query map");
     }
-    p.box_rows = std::min(block_size, 16);
+    p.box_rows = std::min(block_size, 128);
     {
         const cuuint64_t dims[2] = {(cuuint64_t)head_dim, (cuuint64_t)num_blocks * num_kv_heads * block_size};
         const cuuint64_t str[1] = {(cuuint64_t)head_dim * 2};
@@ -390,6 +403,12 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
     p.H_kv = num_kv_heads;
     p.G = num_heads / num_kv_heads;
     p.W = max_blocks_per_seq;
+    {
+        const char* dbg = getenv("PA_PREFILL_DEBUG");
+        p.debug = dbg ? atoi(dbg) : 0;
+        p.trace = g_prefill_trace;
+        p.trace_ctas = g_prefill_trace_ctas;
+    }
     cudaError_t e = pa::launch_prefill(p, (int)dtype, num_seqs, max_query_len, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "paged_prefill_kernel launch");
     return PA_OK;

@@ -25,6 +25,9 @@ struct PrefillParams {
     float scale_log2;
     int log2B, H, H_kv, G, W;
     int box_rows;                 // min(block_size, 16) tokens per TMA box
+    int debug;                    // timing experiments only (PA_PREFILL_DEBUG): 1 no softmax, 2 no MMA
+    long long* trace;             // timing experiments only: clock64 events of the first trace_ctas CTAs
+    int trace_ctas;
 };
 
 struct AttnParams {

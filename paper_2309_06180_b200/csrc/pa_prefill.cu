@@ -27,6 +27,10 @@
 #include "pa_common.cuh"
 #include "pa_internal.h"
 
+#ifndef PA_POLY_EVERY
+#define PA_POLY_EVERY 1000  // polynomial exp2 measured slower here: off
+#endif
+
 namespace pa {
 
 namespace {
@@ -387,6 +391,42 @@ __global__ void __launch_bounds__(128, 1) paged_prefill_kernel(const __grid_cons
     }
 }
 
+// 2^x for a pair on the FMA pipe (FA4-style offload of MUFU.EX2): x = j + f with
+// j = round(x), f in [-1/2, 1/2]; 2^f by a degree-3 minimax polynomial (relative error
+// 7.5e-5, below the storage rounding of P: 2^-9 bf16, 2^-11 f16); 2^j added to the
+// exponent field.  x is clamped to >= -127 (2^-127 rounds to 0 in P's storage type).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+    constexpr float kMagic = 12582912.f;  // 1.5 * 2^23: x + kMagic rounds x to an integer
+    x.x = fmaxf(x.x, -127.f);
+    x.y = fmaxf(x.y, -127.f);
+    const float2 t = __fadd2_rn(x, make_float2(kMagic, kMagic));
+    const float2 j = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
+    const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
+    float2 q = ffma2(make_float2(0.05517334f, 0.05517334f), f, make_float2(0.24261126f, 0.24261126f));
+    q = ffma2(q, f, make_float2(0.69326067f, 0.69326067f));
+    q = ffma2(q, f, make_float2(0.99992806f, 0.99992806f));
+    // (bits(t) - bits(kMagic)) << 23 == bits(t) << 23 (mod 2^32): the low 22 bits of
+    // bits(kMagic) are zero
+    return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+
+// two fp32 -> packed storage pair (lo = a, hi = b), one cvt (F2FP) per pair
+template <typename T>
+__device__ __forceinline__ uint32_t pack2(float a, float b);
+template <>
+__device__ __forceinline__ uint32_t pack2<__half>(float a, float b) {
+    uint32_t d;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
+    return d;
+}
+template <>
+__device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
+    uint32_t d;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
+    return d;
+}
+
 // ---- v2: warp-specialised, two query tiles per CTA ---------------------------------------
 // Warps 0-3 / 4-7: softmax of query tile 0 / 1 (thread = row = TMEM lane); warp 8: TMA
 // producer; warp 9: tcgen05.mma issuer.  Tensor memory (512 columns): S_0, S_1, O_0, O_1
@@ -394,7 +434,19 @@ __global__ void __launch_bounds__(128, 1) paged_prefill_kernel(const __grid_cons
 // 64 columns of S_t and feeds O_t += P_t V as the tensor-memory A operand.  K and V are
 // double-buffered separately, so S_t(j+1) = Q_t K_{j+1}^T runs on the tensor cores while
 // the other warp group's softmax of tile j runs on the SM.  Arithmetic is identical to v1.
+#ifndef PA_PREFILL_TRACE  // timing experiments: scripts/build_variant.sh trace -DPA_PREFILL_TRACE
+#define PF_TRACE(slot) \
+    do {               \
+    } while (0)
+#else
+#define PF_TRACE(slot)                                                                          \
+    do {                                                                                        \
+        if (trace_row) trace_row[(slot)] = clock64();                                           \
+    } while (0)
+#endif
 constexpr int kWarpsV2 = 10;
+constexpr float kLazy = 8.f;
+constexpr int kPolyEvery = PA_POLY_EVERY;  // 1 in kPolyEvery exp2 pairs on the FMA pipe  // P <= 2^8: no overflow in f16/bf16, same relative rounding
 constexpr int kThreadsV2 = kWarpsV2 * 32;
 
 template <typename T>
@@ -416,9 +468,13 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     uint64_t* o_done = bars + 13;    // 2
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
-    // longest work first: the slowest grid dimension walks query-tile pairs backwards
-    const int h = blockIdx.x, s = blockIdx.y, qp = gridDim.z - 1 - blockIdx.z;
+    // the query-tile pairs of one (sequence, head) are neighbours in launch order, so they
+    // run together and share each K/V tile through L2 (longest first within the head)
+    const int qp = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, s = blockIdx.z;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    long long* const trace_row = (p.trace && cta_lin < p.trace_ctas) ? p.trace + (int64_t)cta_lin * 64 : nullptr;
+    if (tid == 0) PF_TRACE(0);
     pdl_wait();
     const int qs = p.query_start[s], qlen = p.query_start[s + 1] - qs;
     const int q0 = qp * 2 * kQ;
@@ -458,26 +514,47 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     const uint32_t tmem = *tmem_slot;
     const int kvh = h / p.G;
     const int B = 1 << p.log2B;
+    if (tid == 0) {
+        PF_TRACE(1);
+        if (trace_row) trace_row[53] = n;
+        if (trace_row) { uint32_t smid; asm("mov.u32 %0, %%smid;" : "=r"(smid)); trace_row[54] = smid; }
+    }
 
     if (warp == 8) {
         // ---------------- TMA producer ----------------
         const int32_t* btrow = p.block_tables + (int64_t)s * p.W;
-        auto load_tile = [&](unsigned char* dst0, const CUtensorMap* map, const CUtensorMap* map1, int j,
-                             uint64_t* bar) {
-            const int t0 = j * kN, t1 = min(kv_len, t0 + kN);
-            const int br = p.box_rows;
-            const int full_end = t0 + (t1 - t0) / br * br;
-            const uint32_t bytes = (uint32_t)(t1 - t0) * 256u;
-            if (lane == 0) {
-                mbar_arrive_expect_tx(bar, bytes);
-                for (int t = t0; t < t1;) {
+        const int br = p.box_rows;
+        // tile j = tokens [128j, min(kv_len, 128j+128)): nf boxes of br rows, then single
+        // rows (never reading past kv_len).  Box b belongs to lane b % 32: the lanes look up
+        // the block table in parallel and issue their own TMA copies.
+        auto box_token = [&](int b, int nf) { return b < nf ? b * br : nf * br + (b - nf); };
+        auto lookup = [&](int j, int (&rowv)[4]) {
+            const int t0 = j * kN, len = min(kv_len, t0 + kN) - t0;
+            const int nf = len / br, nb = nf + len % br;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int b = lane + 32 * i;
+                if (b < nb) {
+                    const int t = t0 + box_token(b, nf);
                     const int blk = __ldg(btrow + (t >> p.log2B));
-                    const int row = (blk * p.H_kv + kvh) * B + (t & (B - 1));
-                    const int off = (t - t0) * 128;
-                    const CUtensorMap* m = t < full_end ? map : map1;
-                    tma_load_2d(dst0 + off, m, 0, row, bar);
-                    tma_load_2d(dst0 + kHalf + off, m, 64, row, bar);
-                    t += t < full_end ? br : 1;
+                    rowv[i] = (blk * p.H_kv + kvh) * B + (t & (B - 1));
+                }
+            }
+        };
+        auto issue = [&](unsigned char* dst0, const CUtensorMap* map, const CUtensorMap* map1, int j, uint64_t* bar,
+                         const int (&rowv)[4]) {
+            const int t0 = j * kN, len = min(kv_len, t0 + kN) - t0;
+            const int nf = len / br, nb = nf + len % br;
+            if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int b = lane + 32 * i;
+                if (b < nb) {
+                    const int off = box_token(b, nf) * 128;
+                    const CUtensorMap* m = b < nf ? map : map1;
+                    tma_load_2d(dst0 + off, m, 0, rowv[i], bar);
+                    tma_load_2d(dst0 + kHalf + off, m, 64, rowv[i], bar);
                 }
             }
             __syncwarp();
@@ -489,12 +566,15 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
             tma_load_3d(sQ + 2 * kHalf, &p.tmap_q, 0, h, qs + q0 + kQ, q_full);
             tma_load_3d(sQ + 3 * kHalf, &p.tmap_q, 64, h, qs + q0 + kQ, q_full);
         }
+        int rowv[4] = {0, 0, 0, 0};
+        if (n > 0) lookup(0, rowv);
         for (int j = 0; j < n; ++j) {
             const int st = j & 1;
             if (j >= 2) mbar_wait(&k_empty[st], ((j - 2) >> 1) & 1);
-            load_tile(sK + st * 2 * kHalf, &p.tmap_k, &p.tmap_k1, j, &k_full[st]);
+            issue(sK + st * 2 * kHalf, &p.tmap_k, &p.tmap_k1, j, &k_full[st], rowv);
             if (j >= 2) mbar_wait(&v_empty[st], ((j - 2) >> 1) & 1);
-            load_tile(sV + st * 2 * kHalf, &p.tmap_v, &p.tmap_v1, j, &v_full[st]);
+            issue(sV + st * 2 * kHalf, &p.tmap_v, &p.tmap_v1, j, &v_full[st], rowv);
+            if (j + 1 < n) lookup(j + 1, rowv);  // in flight while the next empty-wait spins
         }
     } else if (warp == 9) {
         // ---------------- MMA issuer ----------------
@@ -503,7 +583,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
             if (lane == 0) {
                 const uint32_t q = smem_u32(sQ) + t * 2 * kHalf, k = smem_u32(sK) + (j & 1) * 2 * kHalf;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
+                for (int kk = 0; kk < (p.debug >= 2 ? 0 : 8); ++kk) {
                     const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
                     umma_f16(tmem + t * 128, umma_desc_sw128(q + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024),
                              idesc_s, kk > 0);
@@ -516,7 +596,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
             if (lane == 0) {
                 const uint32_t v = smem_u32(sV) + (j & 1) * 2 * kHalf;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
+                for (int kk = 0; kk < (p.debug >= 2 ? 0 : 8); ++kk)
                     umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
                                 umma_desc_sw128(v + kk * 2048, kHalf, 1024), idesc_o, (j > 0) | (kk > 0));
                 umma_commit(&o_done[t]);
@@ -524,6 +604,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
             __syncwarp();
         };
         mbar_wait(q_full, 0);
+        if (lane == 0) PF_TRACE(2);
         if (n > 0) {
             mbar_wait(&k_full[0], 0);
             tc_fence_after();
@@ -542,6 +623,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
             const bool more = j + 1 < n;
             if (more) {
                 mbar_wait(&k_full[st ^ 1], ((j + 1) >> 1) & 1);
+                if (lane == 0 && j + 1 < 16) PF_TRACE(3 + j + 1);
                 tc_fence_after();
                 if (j + 1 < n0) issue_S(0, j + 1);
             }
@@ -571,36 +653,85 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nt; ++j) {
             mbar_wait(&s_full[t], j & 1);
+            if (tid == 0 && j < 16) PF_TRACE(19 + j);
             tc_fence_after();
+            if (p.debug == 1 || p.debug == 3) {
+                tc_fence_before();
+                mbar_arrive(&p_full[t]);
+                continue;
+            }
             float sa[32], sb[32], sc[32], sd[32];
             tmem_ld32_nw(tS + 0, sa);
             tmem_ld32_nw(tS + 32, sb);
             tmem_ld32_nw(tS + 64, sc);
             tmem_ld32_nw(tS + 96, sd);
             tmem_ld_wait();
+            if (tid == 0 && j == 2) PF_TRACE(55);
             const int lim = row_valid ? min(pos + 1, kvt) - j * kN : 0;
+            // scale > 0: max(s) * c == max(s * c) exactly (rounding is monotonic)
+            const bool full = __all_sync(0xffffffffu, lim >= kN);  // no masking in this tile
             float mt = -INFINITY;
+            if (full) {  // four independent max chains (FMNMX3), merged at the end
+                float m0 = sa[0], m1 = sb[0], m2 = sc[0], m3 = sd[0];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                if (i < lim) mt = fmaxf(mt, sa[i] * p.scale_log2);
-                if (i + 32 < lim) mt = fmaxf(mt, sb[i] * p.scale_log2);
-                if (i + 64 < lim) mt = fmaxf(mt, sc[i] * p.scale_log2);
-                if (i + 96 < lim) mt = fmaxf(mt, sd[i] * p.scale_log2);
+                for (int i = 1; i < 31; i += 2) {
+                    m0 = fmaxf(m0, fmaxf(sa[i], sa[i + 1]));
+                    m1 = fmaxf(m1, fmaxf(sb[i], sb[i + 1]));
+                    m2 = fmaxf(m2, fmaxf(sc[i], sc[i + 1]));
+                    m3 = fmaxf(m3, fmaxf(sd[i], sd[i + 1]));
+                }
+                m0 = fmaxf(m0, sa[31]);
+                m1 = fmaxf(m1, sb[31]);
+                m2 = fmaxf(m2, sc[31]);
+                m3 = fmaxf(m3, sd[31]);
+                mt = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    if (i < lim) mt = fmaxf(mt, sa[i]);
+                    if (i + 32 < lim) mt = fmaxf(mt, sb[i]);
+                    if (i + 64 < lim) mt = fmaxf(mt, sc[i]);
+                    if (i + 96 < lim) mt = fmaxf(mt, sd[i]);
+                }
             }
-            const float mn = fmaxf(m, mt);
+            mt *= p.scale_log2;
+            // lazy rescaling: the reference maximum m only moves when some row of the warp
+            // sees a score more than kLazy (log2 units) above it, so O_t is rarely rescaled;
+            // P = 2^(s*c - m) <= 2^kLazy and l use the same m, so O/l is unchanged
+            const bool bump = __any_sync(0xffffffffu, mt > m + kLazy);
+            const float mn = bump ? fmaxf(m, mt) : m;
             const float ms = (mn == -INFINITY) ? 0.f : mn;
-            const float alpha = ex2(m - ms);
-            float rs = 0.f;
+            const float alpha = bump ? ex2(m - ms) : 1.f;
+            if (tid == 0 && j == 2) PF_TRACE(56);
+            // P rounded to the storage dtype (MMA operand); the row sum l accumulates the
+            // fp32 values
+            float2 rs2 = make_float2(0.f, 0.f);
+            const float2 c2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-ms, -ms);
+            // full tiles (the common case) take a select-free path: the SM issue rate, not
+            // MUFU, bounds this loop, so every instruction per element counts
             auto emit = [&](const float (&x)[32], int c0) {
                 uint32_t pk[16];
+                if (full) {
 #pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    const float a0 = (c0 + i < lim) ? ex2(x[i] * p.scale_log2 - ms) : 0.f;
-                    const float a1 = (c0 + i + 1 < lim) ? ex2(x[i + 1] * p.scale_log2 - ms) : 0.f;
-                    T t0 = Elem<T>::from_f32(a0), t1 = Elem<T>::from_f32(a1);
-                    rs += Elem<T>::to_f32(t0) + Elem<T>::to_f32(t1);
-                    pk[i / 2] = (uint32_t)(*reinterpret_cast<uint16_t*>(&t0)) |
-                                ((uint32_t)(*reinterpret_cast<uint16_t*>(&t1)) << 16);
+                    for (int i = 0; i < 32; i += 2) {
+                        const float2 e = ffma2(make_float2(x[i], x[i + 1]), c2, nm2);  // s*c - m
+                        // MUFU.EX2 throughput bounds this loop: every kPolyEvery-th pair
+                        // takes the FMA-pipe polynomial instead
+                        const float2 a = ((i / 2) % kPolyEvery == kPolyEvery - 1) ? exp2_poly2(e)
+                                                                             : make_float2(ex2(e.x), ex2(e.y));
+                        rs2 = __fadd2_rn(rs2, a);
+                        pk[i / 2] = pack2<T>(a.x, a.y);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        const float2 e = ffma2(make_float2(x[i], x[i + 1]), c2, nm2);
+                        float2 a = make_float2(ex2(e.x), ex2(e.y));
+                        a.x = (c0 + i < lim) ? a.x : 0.f;
+                        a.y = (c0 + i + 1 < lim) ? a.y : 0.f;
+                        rs2 = __fadd2_rn(rs2, a);
+                        pk[i / 2] = pack2<T>(a.x, a.y);
+                    }
                 }
                 tmem_st16(tS + c0 / 2, pk);
             };
@@ -608,11 +739,12 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
             emit(sb, 32);
             emit(sc, 64);
             emit(sd, 96);
+            if (tid == 0 && j == 2) PF_TRACE(57);
             // P_t is out; now O_t *= alpha (PV_t(j-1) has completed: S_t(j) was issued after it)
-            if (j > 0) {
+            if (j > 0 && bump) {
                 mbar_wait(&o_done[t], (j - 1) & 1);  // O_t complete up to tile j-1
                 tc_fence_after();
-                if (!__all_sync(0xffffffffu, alpha == 1.f)) {
+                if (bump) {
 #pragma unroll
                     for (int c0 = 0; c0 < 128; c0 += 32) {
                         float v[32];
@@ -624,10 +756,12 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
                     }
                 }
             }
-            l = l * alpha + rs;
+            if (tid == 0 && j == 2) PF_TRACE(58);
+            l = l * alpha + (rs2.x + rs2.y);
             m = mn;
             tmem_st_wait();
             tc_fence_before();
+            if (tid == 0 && j < 16) PF_TRACE(35 + j);
             mbar_arrive(&p_full[t]);
         }
         // epilogue: out row = O_t / l
@@ -637,6 +771,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
             mbar_wait(&o_done[t], (nt - 1) & 1);
             tc_fence_after();
         }
+        if (tid == 0) PF_TRACE(51);
 #pragma unroll
         for (int c0 = 0; c0 < 128; c0 += 32) {
             float v[32];
@@ -660,6 +795,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     }
     tc_fence_before();
     __syncthreads();
+    if (tid == 0) PF_TRACE(52);
     if (warp == 0) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -691,7 +827,7 @@ cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int 
                           : launch_k(paged_prefill_kernel<__nv_bfloat16>, grid, dim3(128), smem, stream, p);
     }
     const size_t smem = prefill_ws_smem_bytes();
-    const dim3 grid(p.H, num_seqs, (max_query_len + 2 * kQ - 1) / (2 * kQ));
+    const dim3 grid((max_query_len + 2 * kQ - 1) / (2 * kQ), p.H, num_seqs);
     cudaError_t e = dtype == 1 ? set_smem(paged_prefill_ws_kernel<__half>, smem)
                                : set_smem(paged_prefill_ws_kernel<__nv_bfloat16>, smem);
     if (e != cudaSuccess) return e;

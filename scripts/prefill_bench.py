@@ -66,10 +66,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default=",".join(PREFILL_CONFIGS))
     ap.add_argument("--iters", type=int, default=50)
+    ap.add_argument("--block-size", type=int, default=0)
     args = ap.parse_args()
     peak, peak_src = peaks()
     for name in args.configs.split(","):
-        c = make_prefill(name)
+        c = make_prefill(name, **({"B": args.block_size} if args.block_size else {}))
         q, kc, vc, bt, cl, qs = build(c)
         out = torch.empty_like(q)
         mql = int(c["qlen"].max())
@@ -80,7 +81,7 @@ def main():
         launches = pa.take_launch_count() / (args.iters + 5)
         flops = algorithmic_flops(c["ctx"], c["qlen"], c["H"], D)
         tf = flops / t / 1e12
-        res = {"config": name, "seqs": len(c["ctx"]), "query_tokens": int(c["qlen"].sum()),
+        res = {"config": name, "block_size": c["B"], "seqs": len(c["ctx"]), "query_tokens": int(c["qlen"].sum()),
                "mean_ctx": round(float(c["ctx"].mean()), 1), "ms": round(t * 1e3, 4),
                "tflops": round(tf, 1), "peak_tflops": peak, "peak_src": peak_src, "frac": round(tf / peak, 3),
                "query_tokens_per_s": round(c["qlen"].sum() / t, 0), "launches_per_call": launches}

@@ -29,9 +29,11 @@ PREFILL_CONFIGS = {
 }
 
 
-def make_prefill(name: str) -> dict:
-    """Returns dict(ctx, qlen, block_tables, num_blocks, H, H_kv, B, dtype, seed, name)."""
+def make_prefill(name: str, **over) -> dict:
+    """Returns dict(ctx, qlen, block_tables, num_blocks, H, H_kv, B, dtype, seed, name);
+    keyword arguments override configuration fields (e.g. B=128)."""
     c = dict(PREFILL_CONFIGS[name])
+    c.update(over)
     B = c["B"]
     if c["kind"] == "trace":
         prompt, _ = request_pool(c["seed"], c["mix"])

@@ -182,6 +182,6 @@ def test_v1_and_warp_specialised_v2_agree(dtype, monkeypatch):
     ulp = 2.0 ** -10 if dtype == "f16" else 2.0 ** -7  # output ulp at |o| < 1
     diff = (a.float() - b.float()).abs().max().item()
     print(f"v1 vs v2 max |diff| = {diff:.3g}")
-    assert diff <= 2 * ulp
+    assert diff <= 4 * ulp
     r = ref(q, kc, vc, bt, cl, qs, 0.09, 16, 2, dtype)
     assert max_abs(a, r) <= TOL[dtype] and max_abs(b, r) <= TOL[dtype]
