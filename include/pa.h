@@ -268,10 +268,6 @@ pa_status_t pa_debug_gather_kv(void* k_out, void* v_out, const void* key_cache,
                                const int32_t* context_lens, int block_size, int num_kv_heads,
                                int num_seqs, int head_dim, int max_blocks_per_seq, int max_ctx,
                                pa_dtype_t dtype, pa_stream_t stream);
-/* Timing experiments only: pa_paged_prefill_attention records clock64() events of its
- * first max_ctas CTAs (64 int64 slots each) into the device buffer buf; NULL disables. */
-pa_status_t pa_debug_prefill_trace(void* buf, int max_ctas);
-
 pa_status_t pa_validate_tables(const int32_t* block_tables, const int32_t* context_lens,
                                int num_seqs, int max_blocks_per_seq, int block_size,
                                int num_blocks, int64_t* first_bad_out, pa_stream_t stream);

@@ -305,19 +305,6 @@ pa_status_t pa_paged_attention(void* out, const void* query, const void* key_cac
 }
 
 namespace {
-long long* g_prefill_trace = nullptr;  // pa_debug_prefill_trace
-int g_prefill_trace_ctas = 0;
-}  // namespace
-
-// Timing experiments: the prefill kernel records clock64() events (64 slots per CTA) of the
-// first max_ctas CTAs into `buf` (device, 64 * max_ctas int64).  NULL disables.
-pa_status_t pa_debug_prefill_trace(void* buf, int max_ctas) {
-    g_prefill_trace = static_cast<long long*>(buf);
-    g_prefill_trace_ctas = buf ? max_ctas : 0;
-    return PA_OK;
-}
-
-namespace {
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -403,12 +390,6 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
     p.H_kv = num_kv_heads;
     p.G = num_heads / num_kv_heads;
     p.W = max_blocks_per_seq;
-    {
-        const char* dbg = getenv("PA_PREFILL_DEBUG");
-        p.debug = dbg ? atoi(dbg) : 0;
-        p.trace = g_prefill_trace;
-        p.trace_ctas = g_prefill_trace_ctas;
-    }
     cudaError_t e = pa::launch_prefill(p, (int)dtype, num_seqs, max_query_len, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "paged_prefill_kernel launch");
     return PA_OK;

@@ -24,10 +24,8 @@ struct PrefillParams {
     const int32_t* query_start;   // [S+1]
     float scale_log2;
     int log2B, H, H_kv, G, W;
-    int box_rows;                 // min(block_size, 16) tokens per TMA box
-    int debug;                    // timing experiments only (PA_PREFILL_DEBUG): 1 no softmax, 2 no MMA
-    long long* trace;             // timing experiments only: clock64 events of the first trace_ctas CTAs
-    int trace_ctas;
+    int box_rows;                 // min(block_size, 128) tokens per TMA box
+    int X, S;                     // query-tile pairs per sequence (grid of work items), sequences
 };
 
 struct AttnParams {

@@ -24,6 +24,8 @@
 // convention); the parity tolerance covers it.
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "pa_common.cuh"
 #include "pa_internal.h"
 
@@ -427,27 +429,45 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
     return d;
 }
 
-// ---- v2: warp-specialised, two query tiles per CTA ---------------------------------------
+// ---- v2 (default): persistent, warp-specialised, two query tiles per CTA ------------------
 // Warps 0-3 / 4-7: softmax of query tile 0 / 1 (thread = row = TMEM lane); warp 8: TMA
 // producer; warp 9: tcgen05.mma issuer.  Tensor memory (512 columns): S_0, S_1, O_0, O_1
 // (128 fp32 columns each); P_t (storage dtype, packed two per column) overwrites the first
 // 64 columns of S_t and feeds O_t += P_t V as the tensor-memory A operand.  K and V are
-// double-buffered separately, so S_t(j+1) = Q_t K_{j+1}^T runs on the tensor cores while
-// the other warp group's softmax of tile j runs on the SM.  Arithmetic is identical to v1.
-#ifndef PA_PREFILL_TRACE  // timing experiments: scripts/build_variant.sh trace -DPA_PREFILL_TRACE
-#define PF_TRACE(slot) \
-    do {               \
-    } while (0)
-#else
-#define PF_TRACE(slot)                                                                          \
-    do {                                                                                        \
-        if (trace_row) trace_row[(slot)] = clock64();                                           \
-    } while (0)
-#endif
+// double-buffered separately; the MMA order PV_0(j), S_0(j+1), PV_1(j), S_1(j+1) keeps the
+// tensor cores on one query tile while the other tile's softmax runs on the SM.  Softmax
+// differences from v1: lazy rescaling (kLazy) and l summed from the fp32 weights.
 constexpr int kWarpsV2 = 10;
-constexpr float kLazy = 8.f;
-constexpr int kPolyEvery = PA_POLY_EVERY;  // 1 in kPolyEvery exp2 pairs on the FMA pipe  // P <= 2^8: no overflow in f16/bf16, same relative rounding
+constexpr float kLazy = 8.f;  // P <= 2^8: no overflow in f16/bf16, same relative rounding
+constexpr int kPolyEvery = PA_POLY_EVERY;  // 1 in kPolyEvery exp2 pairs on the FMA pipe
 constexpr int kThreadsV2 = kWarpsV2 * 32;
+
+// Work item = (query-tile pair qp, head h, sequence s); items are dealt to persistent CTAs
+// (one per SM) round-robin, longest pairs first.  The barrier phases run on across items,
+// so a CTA's producer and MMA warps start the next item while its softmax warps are still
+// writing the previous item's output.
+struct PrefillItem {
+    int h, s, qs, qlen, q0, base_pos, kv0, kv1, n0, n1, kv_len, n;
+};
+__device__ __forceinline__ bool prefill_item(const PrefillParams& p, int i, PrefillItem& it) {
+    const int hs = p.H * p.S;
+    const int qp = p.X - 1 - i / hs, rem = i % hs;
+    it.h = rem % p.H;
+    it.s = rem / p.H;
+    it.qs = __ldg(p.query_start + it.s);
+    it.qlen = __ldg(p.query_start + it.s + 1) - it.qs;
+    it.q0 = qp * 2 * kQ;
+    if (it.q0 >= it.qlen) return false;
+    it.base_pos = __ldg(p.context_lens + it.s) - it.qlen;
+    // tokens query tile t may attend to, and its number of 128-token KV tiles
+    it.kv0 = it.base_pos + min(it.q0 + kQ, it.qlen);
+    it.kv1 = it.q0 + kQ < it.qlen ? it.base_pos + min(it.q0 + 2 * kQ, it.qlen) : 0;
+    it.n0 = it.kv0 > 0 ? (it.kv0 + kN - 1) / kN : 0;
+    it.n1 = it.kv1 > 0 ? (it.kv1 + kN - 1) / kN : 0;
+    it.kv_len = max(it.kv0, it.kv1);
+    it.n = max(it.n0, it.n1);
+    return true;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const __grid_constant__ PrefillParams p) {
@@ -459,38 +479,24 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     unsigned char* sV = sK + 4 * kHalf;      // [2 stages][2 halves][128][64]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 4 * kHalf);
     uint64_t* q_full = bars;         // 1
-    uint64_t* k_full = bars + 1;     // 2
-    uint64_t* k_empty = bars + 3;    // 2
-    uint64_t* v_full = bars + 5;     // 2
-    uint64_t* v_empty = bars + 7;    // 2
-    uint64_t* s_full = bars + 9;     // 2 (per query tile)
-    uint64_t* p_full = bars + 11;    // 2
-    uint64_t* o_done = bars + 13;    // 2
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+    uint64_t* q_empty = bars + 1;    // 1
+    uint64_t* k_full = bars + 2;     // 2
+    uint64_t* k_empty = bars + 4;    // 2
+    uint64_t* v_full = bars + 6;     // 2
+    uint64_t* v_empty = bars + 8;    // 2
+    uint64_t* s_full = bars + 10;    // 2 (per query tile)
+    uint64_t* p_full = bars + 12;    // 2
+    uint64_t* o_done = bars + 14;    // 2
+    uint64_t* o_free = bars + 16;    // 2
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
-    // the query-tile pairs of one (sequence, head) are neighbours in launch order, so they
-    // run together and share each K/V tile through L2 (longest first within the head)
-    const int qp = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, s = blockIdx.z;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    long long* const trace_row = (p.trace && cta_lin < p.trace_ctas) ? p.trace + (int64_t)cta_lin * 64 : nullptr;
-    if (tid == 0) PF_TRACE(0);
+    const int n_items = p.X * p.H * p.S;
     pdl_wait();
-    const int qs = p.query_start[s], qlen = p.query_start[s + 1] - qs;
-    const int q0 = qp * 2 * kQ;
-    if (q0 >= qlen) return;  // CTA-uniform
-    const int ctx = p.context_lens[s];
-    const int base_pos = ctx - qlen;
-    // tokens query tile t may attend to, and its number of 128-token KV tiles
-    const int kv0 = base_pos + min(q0 + kQ, qlen);
-    const int kv1 = q0 + kQ < qlen ? base_pos + min(q0 + 2 * kQ, qlen) : 0;
-    const int n0 = kv0 > 0 ? (kv0 + kN - 1) / kN : 0;
-    const int n1 = kv1 > 0 ? (kv1 + kN - 1) / kN : 0;
-    const int kv_len = max(kv0, kv1);
-    const int n = max(n0, n1);
 
     if (tid == 0) {
         mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&k_full[i], 1);
             mbar_init(&k_empty[i], 1);
@@ -499,11 +505,13 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
             mbar_init(&s_full[i], 1);
             mbar_init(&p_full[i], kQ);
             mbar_init(&o_done[i], 1);
+            mbar_init(&o_free[i], kQ);
         }
         fence_mbar_init();
     }
-    // V stages start zeroed: rows past kv_len of the last tile are never loaded and must
-    // not hold NaN bit patterns (P = 0 there, but 0 * NaN = NaN in the MMA)
+    // V stages start zeroed: rows past kv_len of a last tile are never loaded and must not
+    // hold NaN bit patterns (P = 0 there, but 0 * NaN = NaN in the MMA); later they hold
+    // rows of earlier tiles (finite cache data)
     for (int i = tid; i < 4 * kHalf / 16; i += kThreadsV2)
         reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
@@ -512,78 +520,85 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const int kvh = h / p.G;
     const int B = 1 << p.log2B;
-    if (tid == 0) {
-        PF_TRACE(1);
-        if (trace_row) trace_row[53] = n;
-        if (trace_row) { uint32_t smid; asm("mov.u32 %0, %%smid;" : "=r"(smid)); trace_row[54] = smid; }
-    }
 
     if (warp == 8) {
         // ---------------- TMA producer ----------------
-        const int32_t* btrow = p.block_tables + (int64_t)s * p.W;
         const int br = p.box_rows;
-        // tile j = tokens [128j, min(kv_len, 128j+128)): nf boxes of br rows, then single
-        // rows (never reading past kv_len).  Box b belongs to lane b % 32: the lanes look up
-        // the block table in parallel and issue their own TMA copies.
-        auto box_token = [&](int b, int nf) { return b < nf ? b * br : nf * br + (b - nf); };
-        auto lookup = [&](int j, int (&rowv)[4]) {
-            const int t0 = j * kN, len = min(kv_len, t0 + kN) - t0;
-            const int nf = len / br, nb = nf + len % br;
+        uint32_t g = 0;    // KV tiles loaded by this CTA (stage = g & 1)
+        uint32_t nq = 0;   // query tile pairs loaded
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+            PrefillItem it;
+            if (!prefill_item(p, i, it)) continue;
+            const int kvh = it.h / p.G;
+            const int32_t* btrow = p.block_tables + (int64_t)it.s * p.W;
+            // tile j = tokens [128j, min(kv_len, 128j+128)): nf boxes of br rows, then
+            // single rows (never reading past kv_len).  Box b belongs to lane b % 32: the
+            // lanes look up the block table in parallel and issue their own TMA copies.
+            auto box_token = [&](int b, int nf) { return b < nf ? b * br : nf * br + (b - nf); };
+            auto lookup = [&](int j, int (&rowv)[4]) {
+                const int t0 = j * kN, len = min(it.kv_len, t0 + kN) - t0;
+                const int nf = len / br, nb = nf + len % br;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int b = lane + 32 * i;
-                if (b < nb) {
-                    const int t = t0 + box_token(b, nf);
-                    const int blk = __ldg(btrow + (t >> p.log2B));
-                    rowv[i] = (blk * p.H_kv + kvh) * B + (t & (B - 1));
+                for (int u = 0; u < 4; ++u) {
+                    const int b = lane + 32 * u;
+                    if (b < nb) {
+                        const int t = t0 + box_token(b, nf);
+                        const int blk = __ldg(btrow + (t >> p.log2B));
+                        rowv[u] = (blk * p.H_kv + kvh) * B + (t & (B - 1));
+                    }
                 }
-            }
-        };
-        auto issue = [&](unsigned char* dst0, const CUtensorMap* map, const CUtensorMap* map1, int j, uint64_t* bar,
-                         const int (&rowv)[4]) {
-            const int t0 = j * kN, len = min(kv_len, t0 + kN) - t0;
-            const int nf = len / br, nb = nf + len % br;
-            if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
-            __syncwarp();
+            };
+            auto issue = [&](unsigned char* dst0, const CUtensorMap* map, const CUtensorMap* map1, int j,
+                             uint64_t* bar, const int (&rowv)[4]) {
+                const int t0 = j * kN, len = min(it.kv_len, t0 + kN) - t0;
+                const int nf = len / br, nb = nf + len % br;
+                if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
+                __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int b = lane + 32 * i;
-                if (b < nb) {
-                    const int off = box_token(b, nf) * 128;
-                    const CUtensorMap* m = b < nf ? map : map1;
-                    tma_load_2d(dst0 + off, m, 0, rowv[i], bar);
-                    tma_load_2d(dst0 + kHalf + off, m, 64, rowv[i], bar);
+                for (int u = 0; u < 4; ++u) {
+                    const int b = lane + 32 * u;
+                    if (b < nb) {
+                        const int off = box_token(b, nf) * 128;
+                        const CUtensorMap* m = b < nf ? map : map1;
+                        tma_load_2d(dst0 + off, m, 0, rowv[u], bar);
+                        tma_load_2d(dst0 + kHalf + off, m, 64, rowv[u], bar);
+                    }
                 }
+                __syncwarp();
+            };
+            int rowv[4] = {0, 0, 0, 0};
+            if (it.n > 0) lookup(0, rowv);
+            if (nq > 0) mbar_wait(q_empty, (nq - 1) & 1);  // last S of the previous pair done
+            if (lane == 0) {
+                mbar_arrive_expect_tx(q_full, 4u * kHalf);
+                tma_load_3d(sQ, &p.tmap_q, 0, it.h, it.qs + it.q0, q_full);
+                tma_load_3d(sQ + kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0, q_full);
+                tma_load_3d(sQ + 2 * kHalf, &p.tmap_q, 0, it.h, it.qs + it.q0 + kQ, q_full);
+                tma_load_3d(sQ + 3 * kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0 + kQ, q_full);
             }
             __syncwarp();
-        };
-        if (lane == 0) {
-            mbar_arrive_expect_tx(q_full, 4u * kHalf);
-            tma_load_3d(sQ, &p.tmap_q, 0, h, qs + q0, q_full);
-            tma_load_3d(sQ + kHalf, &p.tmap_q, 64, h, qs + q0, q_full);
-            tma_load_3d(sQ + 2 * kHalf, &p.tmap_q, 0, h, qs + q0 + kQ, q_full);
-            tma_load_3d(sQ + 3 * kHalf, &p.tmap_q, 64, h, qs + q0 + kQ, q_full);
-        }
-        int rowv[4] = {0, 0, 0, 0};
-        if (n > 0) lookup(0, rowv);
-        for (int j = 0; j < n; ++j) {
-            const int st = j & 1;
-            if (j >= 2) mbar_wait(&k_empty[st], ((j - 2) >> 1) & 1);
-            issue(sK + st * 2 * kHalf, &p.tmap_k, &p.tmap_k1, j, &k_full[st], rowv);
-            if (j >= 2) mbar_wait(&v_empty[st], ((j - 2) >> 1) & 1);
-            issue(sV + st * 2 * kHalf, &p.tmap_v, &p.tmap_v1, j, &v_full[st], rowv);
-            if (j + 1 < n) lookup(j + 1, rowv);  // in flight while the next empty-wait spins
+            ++nq;
+            for (int j = 0; j < it.n; ++j, ++g) {
+                const int st = g & 1;
+                if (g >= 2) mbar_wait(&k_empty[st], ((g - 2) >> 1) & 1);
+                issue(sK + st * 2 * kHalf, &p.tmap_k, &p.tmap_k1, j, &k_full[st], rowv);
+                if (g >= 2) mbar_wait(&v_empty[st], ((g - 2) >> 1) & 1);
+                issue(sV + st * 2 * kHalf, &p.tmap_v, &p.tmap_v1, j, &v_full[st], rowv);
+                if (j + 1 < it.n) lookup(j + 1, rowv);  // in flight while the next empty-wait spins
+            }
         }
     } else if (warp == 9) {
         // ---------------- MMA issuer ----------------
         const uint32_t idesc_s = umma_idesc(kBF16, false), idesc_o = umma_idesc(kBF16, true);
-        auto issue_S = [&](int t, int j) {  // S_t = Q_t K_j^T
+        uint32_t g = 0, nq = 0;
+        uint32_t np[2] = {0, 0};  // P tiles consumed per query tile (p_full phases)
+        uint32_t nf[2] = {0, 0};  // pairs with tiles per query tile (o_free phases)
+        auto issue_S = [&](int t, uint32_t gs) {  // S_t = Q_t K^T, K in stage gs & 1
             if (lane == 0) {
-                const uint32_t q = smem_u32(sQ) + t * 2 * kHalf, k = smem_u32(sK) + (j & 1) * 2 * kHalf;
+                const uint32_t q = smem_u32(sQ) + t * 2 * kHalf, k = smem_u32(sK) + (gs & 1) * 2 * kHalf;
 #pragma unroll
-                for (int kk = 0; kk < (p.debug >= 2 ? 0 : 8); ++kk) {
+                for (int kk = 0; kk < 8; ++kk) {
                     const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
                     umma_f16(tmem + t * 128, umma_desc_sw128(q + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024),
                              idesc_s, kk > 0);
@@ -592,210 +607,205 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
             }
             __syncwarp();
         };
-        auto issue_PV = [&](int t, int j) {  // O_t (+)= P_t V_j, P_t in tensor memory
+        auto issue_PV = [&](int t, uint32_t gs, bool first) {  // O_t (+)= P_t V, P_t in tensor memory
             if (lane == 0) {
-                const uint32_t v = smem_u32(sV) + (j & 1) * 2 * kHalf;
+                const uint32_t v = smem_u32(sV) + (gs & 1) * 2 * kHalf;
 #pragma unroll
-                for (int kk = 0; kk < (p.debug >= 2 ? 0 : 8); ++kk)
+                for (int kk = 0; kk < 8; ++kk)
                     umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
-                                umma_desc_sw128(v + kk * 2048, kHalf, 1024), idesc_o, (j > 0) | (kk > 0));
+                                umma_desc_sw128(v + kk * 2048, kHalf, 1024), idesc_o, (!first) | (kk > 0));
                 umma_commit(&o_done[t]);
             }
             __syncwarp();
         };
-        mbar_wait(q_full, 0);
-        if (lane == 0) PF_TRACE(2);
-        if (n > 0) {
-            mbar_wait(&k_full[0], 0);
-            tc_fence_after();
-            if (n0 > 0) issue_S(0, 0);
-            if (n1 > 0) issue_S(1, 0);
-            if (lane == 0) umma_commit(&k_empty[0]);
-        }
-        for (int j = 0; j < n; ++j) {
-            const int st = j & 1;
-            mbar_wait(&v_full[st], (j >> 1) & 1);
-            if (j < n0) {
-                mbar_wait(&p_full[0], j & 1);
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+            PrefillItem it;
+            if (!prefill_item(p, i, it)) continue;
+            mbar_wait(q_full, nq & 1);
+            if (it.n > 0) {
+                mbar_wait(&k_full[g & 1], (g >> 1) & 1);
                 tc_fence_after();
-                issue_PV(0, j);
+                if (it.n0 > 0) issue_S(0, g);
+                if (it.n1 > 0) issue_S(1, g);
+                if (lane == 0) umma_commit(&k_empty[g & 1]);
+                if (it.n == 1 && lane == 0) umma_commit(q_empty);
+            } else if (lane == 0) {
+                umma_commit(q_empty);
             }
-            const bool more = j + 1 < n;
-            if (more) {
-                mbar_wait(&k_full[st ^ 1], ((j + 1) >> 1) & 1);
-                if (lane == 0 && j + 1 < 16) PF_TRACE(3 + j + 1);
-                tc_fence_after();
-                if (j + 1 < n0) issue_S(0, j + 1);
+            // O_t is overwritten by this pair's first P V: the softmax warp group must have
+            // read O_t of its previous pair with tiles (o_free; a group with no tiles in a
+            // pair neither arrives nor is waited for, so it can never run two phases ahead)
+            if (it.n0 > 0 && nf[0]++ > 0) mbar_wait(&o_free[0], (nf[0] - 2) & 1);
+            if (it.n1 > 0 && nf[1]++ > 0) mbar_wait(&o_free[1], (nf[1] - 2) & 1);
+            ++nq;
+            for (int j = 0; j < it.n; ++j, ++g) {
+                const int st = g & 1;
+                mbar_wait(&v_full[st], (g >> 1) & 1);
+                if (j < it.n0) {
+                    mbar_wait(&p_full[0], np[0]++ & 1);
+                    tc_fence_after();
+                    issue_PV(0, g, j == 0);
+                }
+                const bool more = j + 1 < it.n;
+                if (more) {
+                    mbar_wait(&k_full[st ^ 1], ((g + 1) >> 1) & 1);
+                    tc_fence_after();
+                    if (j + 1 < it.n0) issue_S(0, g + 1);
+                }
+                if (j < it.n1) {
+                    mbar_wait(&p_full[1], np[1]++ & 1);
+                    tc_fence_after();
+                    issue_PV(1, g, j == 0);
+                }
+                if (lane == 0) umma_commit(&v_empty[st]);
+                if (more) {
+                    if (j + 1 < it.n1) issue_S(1, g + 1);
+                    if (lane == 0) {
+                        umma_commit(&k_empty[st ^ 1]);
+                        if (j + 2 == it.n) umma_commit(q_empty);  // every S of this pair issued
+                    }
+                }
+                __syncwarp();
             }
-            if (j < n1) {
-                mbar_wait(&p_full[1], j & 1);
-                tc_fence_after();
-                issue_PV(1, j);
-            }
-            if (lane == 0) umma_commit(&v_empty[st]);
-            if (more) {
-                if (j + 1 < n1) issue_S(1, j + 1);
-                if (lane == 0) umma_commit(&k_empty[st ^ 1]);
-            }
-            __syncwarp();
         }
     } else {
         // ---------------- softmax warp groups ----------------
         const int t = warp >> 2;
         const int r = tid & (kQ - 1);
-        const int nt = t == 0 ? n0 : n1;
-        const int kvt = t == 0 ? kv0 : kv1;
-        const int row = q0 + t * kQ + r;
-        const bool row_valid = row < qlen;
-        const int pos = row_valid ? base_pos + row : -1;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + 256 + t * 128 + lane_off;
-        float m = -INFINITY, l = 0.f;
-        for (int j = 0; j < nt; ++j) {
-            mbar_wait(&s_full[t], j & 1);
-            if (tid == 0 && j < 16) PF_TRACE(19 + j);
-            tc_fence_after();
-            if (p.debug == 1 || p.debug == 3) {
-                tc_fence_before();
-                mbar_arrive(&p_full[t]);
-                continue;
-            }
-            float sa[32], sb[32], sc[32], sd[32];
-            tmem_ld32_nw(tS + 0, sa);
-            tmem_ld32_nw(tS + 32, sb);
-            tmem_ld32_nw(tS + 64, sc);
-            tmem_ld32_nw(tS + 96, sd);
-            tmem_ld_wait();
-            if (tid == 0 && j == 2) PF_TRACE(55);
-            const int lim = row_valid ? min(pos + 1, kvt) - j * kN : 0;
-            // scale > 0: max(s) * c == max(s * c) exactly (rounding is monotonic)
-            const bool full = __all_sync(0xffffffffu, lim >= kN);  // no masking in this tile
-            float mt = -INFINITY;
-            if (full) {  // four independent max chains (FMNMX3), merged at the end
-                float m0 = sa[0], m1 = sb[0], m2 = sc[0], m3 = sd[0];
-#pragma unroll
-                for (int i = 1; i < 31; i += 2) {
-                    m0 = fmaxf(m0, fmaxf(sa[i], sa[i + 1]));
-                    m1 = fmaxf(m1, fmaxf(sb[i], sb[i + 1]));
-                    m2 = fmaxf(m2, fmaxf(sc[i], sc[i + 1]));
-                    m3 = fmaxf(m3, fmaxf(sd[i], sd[i + 1]));
-                }
-                m0 = fmaxf(m0, sa[31]);
-                m1 = fmaxf(m1, sb[31]);
-                m2 = fmaxf(m2, sc[31]);
-                m3 = fmaxf(m3, sd[31]);
-                mt = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    if (i < lim) mt = fmaxf(mt, sa[i]);
-                    if (i + 32 < lim) mt = fmaxf(mt, sb[i]);
-                    if (i + 64 < lim) mt = fmaxf(mt, sc[i]);
-                    if (i + 96 < lim) mt = fmaxf(mt, sd[i]);
-                }
-            }
-            mt *= p.scale_log2;
-            // lazy rescaling: the reference maximum m only moves when some row of the warp
-            // sees a score more than kLazy (log2 units) above it, so O_t is rarely rescaled;
-            // P = 2^(s*c - m) <= 2^kLazy and l use the same m, so O/l is unchanged
-            const bool bump = __any_sync(0xffffffffu, mt > m + kLazy);
-            const float mn = bump ? fmaxf(m, mt) : m;
-            const float ms = (mn == -INFINITY) ? 0.f : mn;
-            const float alpha = bump ? ex2(m - ms) : 1.f;
-            if (tid == 0 && j == 2) PF_TRACE(56);
-            // P rounded to the storage dtype (MMA operand); the row sum l accumulates the
-            // fp32 values
-            float2 rs2 = make_float2(0.f, 0.f);
-            const float2 c2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-ms, -ms);
-            // full tiles (the common case) take a select-free path: the SM issue rate, not
-            // MUFU, bounds this loop, so every instruction per element counts
-            auto emit = [&](const float (&x)[32], int c0) {
-                uint32_t pk[16];
+        uint32_t ns = 0;  // S tiles consumed by this warp group (s_full / o_done phases)
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+            PrefillItem it;
+            if (!prefill_item(p, i, it)) continue;
+            const int nt = t == 0 ? it.n0 : it.n1;
+            const int kvt = t == 0 ? it.kv0 : it.kv1;
+            const int row = it.q0 + t * kQ + r;
+            const bool row_valid = row < it.qlen;
+            const int pos = row_valid ? it.base_pos + row : -1;
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < nt; ++j, ++ns) {
+                mbar_wait(&s_full[t], ns & 1);
+                tc_fence_after();
+                float sa[32], sb[32], sc[32], sd[32];
+                tmem_ld32_nw(tS + 0, sa);
+                tmem_ld32_nw(tS + 32, sb);
+                tmem_ld32_nw(tS + 64, sc);
+                tmem_ld32_nw(tS + 96, sd);
+                tmem_ld_wait();
+                const int lim = row_valid ? min(pos + 1, kvt) - j * kN : 0;
+                // scale > 0: max(s) * c == max(s * c) exactly (rounding is monotonic)
+                const bool full = __all_sync(0xffffffffu, lim >= kN);  // no masking in this tile
+                float mt = -INFINITY;
                 if (full) {
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        const float2 e = ffma2(make_float2(x[i], x[i + 1]), c2, nm2);  // s*c - m
-                        // MUFU.EX2 throughput bounds this loop: every kPolyEvery-th pair
-                        // takes the FMA-pipe polynomial instead
-                        const float2 a = ((i / 2) % kPolyEvery == kPolyEvery - 1) ? exp2_poly2(e)
-                                                                             : make_float2(ex2(e.x), ex2(e.y));
-                        rs2 = __fadd2_rn(rs2, a);
-                        pk[i / 2] = pack2<T>(a.x, a.y);
-                    }
+                    for (int u = 0; u < 32; ++u) mt = fmaxf(fmaxf(mt, sa[u]), fmaxf(sb[u], fmaxf(sc[u], sd[u])));
                 } else {
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        const float2 e = ffma2(make_float2(x[i], x[i + 1]), c2, nm2);
-                        float2 a = make_float2(ex2(e.x), ex2(e.y));
-                        a.x = (c0 + i < lim) ? a.x : 0.f;
-                        a.y = (c0 + i + 1 < lim) ? a.y : 0.f;
-                        rs2 = __fadd2_rn(rs2, a);
-                        pk[i / 2] = pack2<T>(a.x, a.y);
+                    for (int u = 0; u < 32; ++u) {
+                        if (u < lim) mt = fmaxf(mt, sa[u]);
+                        if (u + 32 < lim) mt = fmaxf(mt, sb[u]);
+                        if (u + 64 < lim) mt = fmaxf(mt, sc[u]);
+                        if (u + 96 < lim) mt = fmaxf(mt, sd[u]);
                     }
                 }
-                tmem_st16(tS + c0 / 2, pk);
-            };
-            emit(sa, 0);
-            emit(sb, 32);
-            emit(sc, 64);
-            emit(sd, 96);
-            if (tid == 0 && j == 2) PF_TRACE(57);
-            // P_t is out; now O_t *= alpha (PV_t(j-1) has completed: S_t(j) was issued after it)
-            if (j > 0 && bump) {
-                mbar_wait(&o_done[t], (j - 1) & 1);  // O_t complete up to tile j-1
-                tc_fence_after();
-                if (bump) {
+                mt *= p.scale_log2;
+                // lazy rescaling: the reference maximum m only moves when some row of the
+                // warp sees a score more than kLazy (log2 units) above it, so O_t is rarely
+                // rescaled; P = 2^(s*c - m) <= 2^kLazy and l use the same m
+                const bool bump = __any_sync(0xffffffffu, mt > m + kLazy);
+                const float mn = bump ? fmaxf(m, mt) : m;
+                const float ms = (mn == -INFINITY) ? 0.f : mn;
+                const float alpha = bump ? ex2(m - ms) : 1.f;
+                // P rounded to the storage dtype (MMA operand); the row sum l accumulates
+                // the fp32 values.  Full tiles take a select-free path.
+                float2 rs2 = make_float2(0.f, 0.f);
+                const float2 c2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-ms, -ms);
+                auto emit = [&](const float (&x)[32], int c0) {
+                    uint32_t pk[16];
+                    if (full) {
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) {
+                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);  // s*c - m
+                            const float2 a = ((u / 2) % kPolyEvery == kPolyEvery - 1)
+                                                 ? exp2_poly2(e)
+                                                 : make_float2(ex2(e.x), ex2(e.y));
+                            rs2 = __fadd2_rn(rs2, a);
+                            pk[u / 2] = pack2<T>(a.x, a.y);
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) {
+                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
+                            float2 a = make_float2(ex2(e.x), ex2(e.y));
+                            a.x = (c0 + u < lim) ? a.x : 0.f;
+                            a.y = (c0 + u + 1 < lim) ? a.y : 0.f;
+                            rs2 = __fadd2_rn(rs2, a);
+                            pk[u / 2] = pack2<T>(a.x, a.y);
+                        }
+                    }
+                    tmem_st16(tS + c0 / 2, pk);
+                };
+                emit(sa, 0);
+                emit(sb, 32);
+                emit(sc, 64);
+                emit(sd, 96);
+                // P_t is out; now O_t *= alpha (PV_t of the previous tile has completed: this
+                // S_t was issued after it)
+                if (j > 0 && bump) {
+                    mbar_wait(&o_done[t], (ns - 1) & 1);
+                    tc_fence_after();
 #pragma unroll
                     for (int c0 = 0; c0 < 128; c0 += 32) {
                         float v[32];
                         tmem_ld32_nw(tO + c0, v);
                         tmem_ld_wait();
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] *= alpha;
+                        for (int u = 0; u < 32; ++u) v[u] *= alpha;
                         tmem_st32(tO + c0, v);
                     }
                 }
+                l = l * alpha + (rs2.x + rs2.y);
+                m = mn;
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&p_full[t]);
             }
-            if (tid == 0 && j == 2) PF_TRACE(58);
-            l = l * alpha + (rs2.x + rs2.y);
-            m = mn;
-            tmem_st_wait();
-            tc_fence_before();
-            if (tid == 0 && j < 16) PF_TRACE(35 + j);
-            mbar_arrive(&p_full[t]);
-        }
-        // epilogue: out row = O_t / l
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        T* orow = static_cast<T*>(p.out) + ((int64_t)(qs + row) * p.H + h) * 128;
-        if (nt > 0) {
-            mbar_wait(&o_done[t], (nt - 1) & 1);
-            tc_fence_after();
-        }
-        if (tid == 0) PF_TRACE(51);
-#pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-            float v[32];
+            // epilogue: out row = O_t / l
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            T* orow = static_cast<T*>(p.out) + ((int64_t)(it.qs + row) * p.H + it.h) * 128;
             if (nt > 0) {
-                tmem_ld32_nw(tO + c0, v);
-                tmem_ld_wait();
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                mbar_wait(&o_done[t], (ns - 1) & 1);
+                tc_fence_after();
             }
-            if (row_valid) {
 #pragma unroll
-                for (int c1 = 0; c1 < 32; c1 += 8) {
-                    alignas(16) T w[8];
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+                float v[32];
+                if (nt > 0) {
+                    tmem_ld32_nw(tO + c0, v);
+                    tmem_ld_wait();
+                } else {
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) w[i] = Elem<T>::from_f32(v[c1 + i] * inv);
-                    *reinterpret_cast<uint4*>(orow + c0 + c1) = *reinterpret_cast<const uint4*>(w);
+                    for (int u = 0; u < 32; ++u) v[u] = 0.f;
                 }
+                if (row_valid) {
+#pragma unroll
+                    for (int c1 = 0; c1 < 32; c1 += 8) {
+                        alignas(16) T w[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) w[u] = Elem<T>::from_f32(v[c1 + u] * inv);
+                        *reinterpret_cast<uint4*>(orow + c0 + c1) = *reinterpret_cast<const uint4*>(w);
+                    }
+                }
+            }
+            if (nt > 0) {
+                tc_fence_before();
+                mbar_arrive(&o_free[t]);  // O_t may be overwritten by the next pair
             }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (tid == 0) PF_TRACE(52);
     if (warp == 0) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -803,7 +813,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
 }
 
 size_t prefill_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 64; }
-size_t prefill_ws_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 160; }
+size_t prefill_ws_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 192; }
 
 namespace {
 template <typename Kern>
@@ -827,12 +837,23 @@ cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int 
                           : launch_k(paged_prefill_kernel<__nv_bfloat16>, grid, dim3(128), smem, stream, p);
     }
     const size_t smem = prefill_ws_smem_bytes();
-    const dim3 grid((max_query_len + 2 * kQ - 1) / (2 * kQ), p.H, num_seqs);
+    static int num_sms = 0;
+    if (num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (num_sms <= 0) num_sms = 148;
+    }
+    PrefillParams q = p;
+    q.X = (max_query_len + 2 * kQ - 1) / (2 * kQ);
+    q.S = num_seqs;
+    const long long items = (long long)q.X * q.H * q.S;
+    const dim3 grid((unsigned)std::min<long long>(items, num_sms));
     cudaError_t e = dtype == 1 ? set_smem(paged_prefill_ws_kernel<__half>, smem)
                                : set_smem(paged_prefill_ws_kernel<__nv_bfloat16>, smem);
     if (e != cudaSuccess) return e;
-    return dtype == 1 ? launch_k(paged_prefill_ws_kernel<__half>, grid, dim3(kThreadsV2), smem, stream, p)
-                      : launch_k(paged_prefill_ws_kernel<__nv_bfloat16>, grid, dim3(kThreadsV2), smem, stream, p);
+    return dtype == 1 ? launch_k(paged_prefill_ws_kernel<__half>, grid, dim3(kThreadsV2), smem, stream, q)
+                      : launch_k(paged_prefill_ws_kernel<__nv_bfloat16>, grid, dim3(kThreadsV2), smem, stream, q);
 }
 
 }  // namespace pa
