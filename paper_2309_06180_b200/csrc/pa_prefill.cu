@@ -812,6 +812,354 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     }
 }
 
+// ---- v3 (default): persistent, one query tile per item, softmax split by columns ----------
+// The two softmax warp groups share the 128 rows of ONE query tile: group 0 takes key
+// columns [0,64), group 1 [64,128) of every 128-key tile (warps w and w+4 address the same
+// TMEM lanes).  Row maxima are exchanged through shared memory (named barrier, 256
+// threads); each group keeps its own partial row sum with the same reference maximum, and
+// the two sums are added in the epilogue.  Tensor memory: two S buffers (columns 0 and
+// 128, P aliased in the first 64 columns of its buffer) and O (256..383), so the MMA warp
+// computes S(j+1) = Q K_{j+1}^T while the softmax of tile j runs, and P V for tile j-1;
+// the per-tile softmax is half as long as in v2 and off the tensor-core critical path.
+// Shared memory: Q double-buffered (the next item's Q loads during this item), K and V in
+// two stages each (192 KB).
+constexpr int kKStages = 2, kVStages = 2;
+
+struct PrefillItem1 {
+    int h, s, qs, qlen, q0, base_pos, kv_len, n;
+};
+__device__ __forceinline__ bool prefill_item1(const PrefillParams& p, int i, PrefillItem1& it) {
+    const int hs = p.H * p.S;
+    const int qt = p.X - 1 - i / hs, rem = i % hs;  // longest query tiles first
+    it.h = rem % p.H;
+    it.s = rem / p.H;
+    it.qs = __ldg(p.query_start + it.s);
+    it.qlen = __ldg(p.query_start + it.s + 1) - it.qs;
+    it.q0 = qt * kQ;
+    if (it.q0 >= it.qlen) return false;
+    it.base_pos = __ldg(p.context_lens + it.s) - it.qlen;
+    it.kv_len = it.base_pos + min(it.q0 + kQ, it.qlen);
+    it.n = it.kv_len > 0 ? (it.kv_len + kN - 1) / kN : 0;
+    return true;
+}
+
+__device__ __forceinline__ void named_bar_sync_256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+template <typename T>
+__global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_split_kernel(const __grid_constant__ PrefillParams p) {
+    constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* sQ = smem;                          // [2 buffers][2 halves][128][64]
+    unsigned char* sK = smem + 4 * kHalf;              // [3 stages][2 halves][128][64]
+    unsigned char* sV = sK + 2 * kKStages * kHalf;     // [2 stages][2 halves][128][64]
+    float* red = reinterpret_cast<float*>(sV + 2 * kVStages * kHalf);  // [2 parity][2 groups][128] row maxima
+    float* lsum = red + 512;                                            // [2 groups][128] row sums
+    uint64_t* bars = reinterpret_cast<uint64_t*>(lsum + 256);
+    uint64_t* q_full = bars;                 // 2
+    uint64_t* q_empty = bars + 2;            // 2
+    uint64_t* k_full = bars + 4;             // 3
+    uint64_t* k_empty = bars + 7;            // 3
+    uint64_t* v_full = bars + 10;            // 2
+    uint64_t* v_empty = bars + 12;           // 2
+    uint64_t* s_full = bars + 14;            // 2 (per S buffer)
+    uint64_t* p_full = bars + 16;            // 1
+    uint64_t* o_done = bars + 17;            // 1
+    uint64_t* o_free = bars + 18;            // 1
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n_items = p.X * p.H * p.S;
+    pdl_wait();
+
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+        }
+        for (int i = 0; i < kKStages; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+        }
+        mbar_init(p_full, 2 * kQ);
+        mbar_init(o_done, 1);
+        mbar_init(o_free, 2 * kQ);
+        fence_mbar_init();
+    }
+    // V stages start zeroed (see v2)
+    for (int i = tid; i < 2 * kVStages * kHalf / 16; i += kThreadsV2)
+        reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+    if (warp == 0) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int B = 1 << p.log2B;
+
+    if (warp == 8) {
+        // ---------------- TMA producer ----------------
+        const int br = p.box_rows;
+        uint32_t g = 0, nq = 0;
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+            PrefillItem1 it;
+            if (!prefill_item1(p, i, it)) continue;
+            const int kvh = it.h / p.G;
+            const int32_t* btrow = p.block_tables + (int64_t)it.s * p.W;
+            auto box_token = [&](int b, int nf) { return b < nf ? b * br : nf * br + (b - nf); };
+            auto lookup = [&](int j, int (&rowv)[4]) {
+                const int t0 = j * kN, len = min(it.kv_len, t0 + kN) - t0;
+                const int nf = len / br, nb = nf + len % br;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int b = lane + 32 * u;
+                    if (b < nb) {
+                        const int t = t0 + box_token(b, nf);
+                        const int blk = __ldg(btrow + (t >> p.log2B));
+                        rowv[u] = (blk * p.H_kv + kvh) * B + (t & (B - 1));
+                    }
+                }
+            };
+            auto issue = [&](unsigned char* dst0, const CUtensorMap* map, const CUtensorMap* map1, int j,
+                             uint64_t* bar, const int (&rowv)[4]) {
+                const int t0 = j * kN, len = min(it.kv_len, t0 + kN) - t0;
+                const int nf = len / br, nb = nf + len % br;
+                if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int b = lane + 32 * u;
+                    if (b < nb) {
+                        const int off = box_token(b, nf) * 128;
+                        const CUtensorMap* m = b < nf ? map : map1;
+                        tma_load_2d(dst0 + off, m, 0, rowv[u], bar);
+                        tma_load_2d(dst0 + kHalf + off, m, 64, rowv[u], bar);
+                    }
+                }
+                __syncwarp();
+            };
+            int rowv[4] = {0, 0, 0, 0};
+            if (it.n > 0) lookup(0, rowv);
+            const int qb = nq & 1;
+            if (nq >= 2) mbar_wait(&q_empty[qb], ((nq - 2) >> 1) & 1);
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&q_full[qb], 2u * kHalf);
+                tma_load_3d(sQ + qb * 2 * kHalf, &p.tmap_q, 0, it.h, it.qs + it.q0, &q_full[qb]);
+                tma_load_3d(sQ + qb * 2 * kHalf + kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0, &q_full[qb]);
+            }
+            __syncwarp();
+            ++nq;
+            for (int j = 0; j < it.n; ++j, ++g) {
+                const uint32_t ks = g % kKStages, vs = g & 1;
+                if (g >= kKStages) mbar_wait(&k_empty[ks], ((g - kKStages) / kKStages) & 1);
+                issue(sK + ks * 2 * kHalf, &p.tmap_k, &p.tmap_k1, j, &k_full[ks], rowv);
+                if (g >= 2) mbar_wait(&v_empty[vs], ((g - 2) >> 1) & 1);
+                issue(sV + vs * 2 * kHalf, &p.tmap_v, &p.tmap_v1, j, &v_full[vs], rowv);
+                if (j + 1 < it.n) lookup(j + 1, rowv);
+            }
+        }
+    } else if (warp == 9) {
+        // ---------------- MMA issuer ----------------
+        const uint32_t idesc_s = umma_idesc(kBF16, false), idesc_o = umma_idesc(kBF16, true);
+        uint32_t gk = 0, gv = 0, nq = 0, np = 0, nf = 0;
+        auto issue_S = [&](uint32_t qb) {  // S(gk) = Q K(gk)^T into S buffer gk & 1
+            const uint32_t ks = gk % kKStages;
+            mbar_wait(&k_full[ks], (gk / kKStages) & 1);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t q = smem_u32(sQ) + qb * 2 * kHalf, k = smem_u32(sK) + ks * 2 * kHalf;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+                    umma_f16(tmem + (gk & 1) * 128, umma_desc_sw128(q + off, 16, 1024),
+                             umma_desc_sw128(k + off, 16, 1024), idesc_s, kk > 0);
+                }
+                umma_commit(&s_full[gk & 1]);
+                umma_commit(&k_empty[ks]);
+            }
+            __syncwarp();
+            ++gk;
+        };
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+            PrefillItem1 it;
+            if (!prefill_item1(p, i, it)) continue;
+            const uint32_t qb = nq & 1;
+            mbar_wait(&q_full[qb], (nq >> 1) & 1);
+            ++nq;
+            // S runs up to two tiles ahead of P V (two S buffers)
+            for (int j = 0; j < min(it.n, 2); ++j) issue_S(qb);
+            if (it.n <= 2 && lane == 0) umma_commit(&q_empty[qb]);  // every S of this item issued
+            if (it.n > 0 && nf++ > 0) mbar_wait(o_free, (nf - 2) & 1);  // O read by the epilogue
+            for (int j = 0; j < it.n; ++j) {
+                mbar_wait(&v_full[gv & 1], (gv >> 1) & 1);
+                mbar_wait(p_full, np++ & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t v = smem_u32(sV) + (gv & 1) * 2 * kHalf;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        umma_f16_ts(tmem + 256, tmem + (gv & 1) * 128 + kk * 8,
+                                    umma_desc_sw128(v + kk * 2048, kHalf, 1024), idesc_o, (j > 0) | (kk > 0));
+                    umma_commit(o_done);
+                    umma_commit(&v_empty[gv & 1]);
+                }
+                __syncwarp();
+                ++gv;
+                if (j + 2 < it.n) {
+                    issue_S(qb);  // overwrites the P just consumed (in issue order)
+                    if (j + 3 == it.n && lane == 0) umma_commit(&q_empty[qb]);
+                }
+            }
+        }
+    } else {
+        // ---------------- softmax warp groups (column halves) ----------------
+        const int hf = warp >> 2;              // key columns [64 hf, 64 hf + 64) of each tile
+        const int r = tid & (kQ - 1);
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t tO = tmem + 256 + hf * 64 + lane_off;
+        uint32_t ns = 0;
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+            PrefillItem1 it;
+            if (!prefill_item1(p, i, it)) continue;
+            const int row = it.q0 + r;
+            const bool row_valid = row < it.qlen;
+            const int pos = row_valid ? it.base_pos + row : -1;
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < it.n; ++j, ++ns) {
+                const uint32_t b = ns & 1;
+                const uint32_t tS = tmem + b * 128 + lane_off;
+                mbar_wait(&s_full[b], (ns >> 1) & 1);
+                tc_fence_after();
+                float sa[32], sb[32];
+                tmem_ld32_nw(tS + hf * 64, sa);
+                tmem_ld32_nw(tS + hf * 64 + 32, sb);
+                tmem_ld_wait();
+                const int lim = row_valid ? min(pos + 1, it.kv_len) - j * kN - hf * 64 : 0;
+                const bool full = __all_sync(0xffffffffu, lim >= 64);
+                float mo = -INFINITY;
+                if (full) {
+#pragma unroll
+                    for (int u = 0; u < 32; u += 2)
+                        mo = fmaxf(fmaxf(mo, fmaxf(sa[u], sa[u + 1])), fmaxf(sb[u], sb[u + 1]));
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) {
+                        if (u < lim) mo = fmaxf(mo, sa[u]);
+                        if (u + 32 < lim) mo = fmaxf(mo, sb[u]);
+                    }
+                }
+                // row maximum over both halves (the S reads above complete before the other
+                // group overwrites columns of this buffer with P)
+                float* rd = red + (ns & 1) * 256;
+                rd[hf * 128 + r] = mo;
+                named_bar_sync_256();
+                float mt = fmaxf(mo, rd[(hf ^ 1) * 128 + r]);
+                mt *= p.scale_log2;
+                // lazy rescaling, decided identically by both groups (same rows, same mt)
+                const bool bump = __any_sync(0xffffffffu, mt > m + kLazy);
+                const float mn = bump ? fmaxf(m, mt) : m;
+                const float ms = (mn == -INFINITY) ? 0.f : mn;
+                const float alpha = bump ? ex2(m - ms) : 1.f;
+                float2 rs2 = make_float2(0.f, 0.f);
+                const float2 c2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-ms, -ms);
+                auto emit = [&](const float (&x)[32], int c0) {
+                    uint32_t pk[16];
+                    if (full) {
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) {
+                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
+                            const float2 a = ((u / 2) % kPolyEvery == kPolyEvery - 1)
+                                                 ? exp2_poly2(e)
+                                                 : make_float2(ex2(e.x), ex2(e.y));
+                            rs2 = __fadd2_rn(rs2, a);
+                            pk[u / 2] = pack2<T>(a.x, a.y);
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) {
+                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
+                            float2 a = make_float2(ex2(e.x), ex2(e.y));
+                            a.x = (c0 + u < lim) ? a.x : 0.f;
+                            a.y = (c0 + u + 1 < lim) ? a.y : 0.f;
+                            rs2 = __fadd2_rn(rs2, a);
+                            pk[u / 2] = pack2<T>(a.x, a.y);
+                        }
+                    }
+                    tmem_st16(tS + hf * 32 + c0 / 2, pk);  // P columns of this half
+                };
+                emit(sa, 0);
+                emit(sb, 32);
+                if (j > 0 && bump) {  // O columns of this half *= alpha
+                    mbar_wait(o_done, (ns - 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
+                        float v[32];
+                        tmem_ld32_nw(tO + c0, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) v[u] *= alpha;
+                        tmem_st32(tO + c0, v);
+                    }
+                }
+                l = l * alpha + (rs2.x + rs2.y);
+                m = mn;
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(p_full);
+            }
+            // epilogue: both partial row sums, then this half's 64 output columns
+            lsum[hf * 128 + r] = l;
+            named_bar_sync_256();
+            const float lt = l + lsum[(hf ^ 1) * 128 + r];
+            named_bar_sync_256();  // lsum may be rewritten by the next item
+            const float inv = lt > 0.f ? 1.f / lt : 0.f;
+            T* orow = static_cast<T*>(p.out) + ((int64_t)(it.qs + row) * p.H + it.h) * 128 + hf * 64;
+            if (it.n > 0) {
+                mbar_wait(o_done, (ns - 1) & 1);
+                tc_fence_after();
+            }
+#pragma unroll
+            for (int c0 = 0; c0 < 64; c0 += 32) {
+                float v[32];
+                if (it.n > 0) {
+                    tmem_ld32_nw(tO + c0, v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) v[u] = 0.f;
+                }
+                if (row_valid) {
+#pragma unroll
+                    for (int c1 = 0; c1 < 32; c1 += 8) {
+                        alignas(16) T w[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) w[u] = Elem<T>::from_f32(v[c1 + u] * inv);
+                        *reinterpret_cast<uint4*>(orow + c0 + c1) = *reinterpret_cast<const uint4*>(w);
+                    }
+                }
+            }
+            if (it.n > 0) {
+                tc_fence_before();
+                mbar_arrive(o_free);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+size_t prefill_split_smem_bytes() {
+    return 1024 + (4 + 2 * kKStages + 2 * kVStages) * (size_t)kHalf + (512 + 256) * 4 + 20 * 8;
+}
+
 size_t prefill_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 64; }
 size_t prefill_ws_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 192; }
 
@@ -820,14 +1168,19 @@ template <typename Kern>
 cudaError_t set_smem(Kern k, size_t smem) {
     return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
-int prefill_variant() {
+// PA_PREFILL=1/2/3 forces a kernel (ablations).  Default: v3 when every query fits one
+// 128-row tile (v2 would leave its second softmax group idle), else v2 (whose two query
+// tiles share each K/V tile: half the TMA copies per flop).
+int prefill_variant(int max_query_len) {
     const char* e = getenv("PA_PREFILL");
-    return (e && e[0] == '1') ? 1 : 2;
+    if (e && e[0] >= '1' && e[0] <= '3') return e[0] - '0';
+    return max_query_len <= kQ ? 3 : 2;
 }
 }  // namespace
 
 cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, cudaStream_t stream) {
-    if (prefill_variant() == 1) {
+    const int variant = prefill_variant(max_query_len);
+    if (variant == 1) {
         const size_t smem = prefill_smem_bytes();
         const dim3 grid((max_query_len + kQ - 1) / kQ, p.H, num_seqs);
         cudaError_t e = dtype == 1 ? set_smem(paged_prefill_kernel<__half>, smem)
@@ -836,7 +1189,6 @@ cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int 
         return dtype == 1 ? launch_k(paged_prefill_kernel<__half>, grid, dim3(128), smem, stream, p)
                           : launch_k(paged_prefill_kernel<__nv_bfloat16>, grid, dim3(128), smem, stream, p);
     }
-    const size_t smem = prefill_ws_smem_bytes();
     static int num_sms = 0;
     if (num_sms == 0) {
         int dev = 0;
@@ -845,15 +1197,27 @@ cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int 
         if (num_sms <= 0) num_sms = 148;
     }
     PrefillParams q = p;
-    q.X = (max_query_len + 2 * kQ - 1) / (2 * kQ);
     q.S = num_seqs;
+    if (variant == 2) {
+        const size_t smem = prefill_ws_smem_bytes();
+        q.X = (max_query_len + 2 * kQ - 1) / (2 * kQ);
+        const long long items = (long long)q.X * q.H * q.S;
+        const dim3 grid((unsigned)std::min<long long>(items, num_sms));
+        cudaError_t e = dtype == 1 ? set_smem(paged_prefill_ws_kernel<__half>, smem)
+                                   : set_smem(paged_prefill_ws_kernel<__nv_bfloat16>, smem);
+        if (e != cudaSuccess) return e;
+        return dtype == 1 ? launch_k(paged_prefill_ws_kernel<__half>, grid, dim3(kThreadsV2), smem, stream, q)
+                          : launch_k(paged_prefill_ws_kernel<__nv_bfloat16>, grid, dim3(kThreadsV2), smem, stream, q);
+    }
+    const size_t smem = prefill_split_smem_bytes();
+    q.X = (max_query_len + kQ - 1) / kQ;
     const long long items = (long long)q.X * q.H * q.S;
     const dim3 grid((unsigned)std::min<long long>(items, num_sms));
-    cudaError_t e = dtype == 1 ? set_smem(paged_prefill_ws_kernel<__half>, smem)
-                               : set_smem(paged_prefill_ws_kernel<__nv_bfloat16>, smem);
+    cudaError_t e = dtype == 1 ? set_smem(paged_prefill_split_kernel<__half>, smem)
+                               : set_smem(paged_prefill_split_kernel<__nv_bfloat16>, smem);
     if (e != cudaSuccess) return e;
-    return dtype == 1 ? launch_k(paged_prefill_ws_kernel<__half>, grid, dim3(kThreadsV2), smem, stream, q)
-                      : launch_k(paged_prefill_ws_kernel<__nv_bfloat16>, grid, dim3(kThreadsV2), smem, stream, q);
+    return dtype == 1 ? launch_k(paged_prefill_split_kernel<__half>, grid, dim3(kThreadsV2), smem, stream, q)
+                      : launch_k(paged_prefill_split_kernel<__nv_bfloat16>, grid, dim3(kThreadsV2), smem, stream, q);
 }
 
 }  // namespace pa

@@ -106,10 +106,12 @@ def test_block_size_and_placement_invariance_bitwise():
         assert torch.equal(o, outs[0])
 
 
-def test_chunked_prompt_equals_whole_prompt_bitwise():
+@pytest.mark.parametrize("variant", ["2", "3"])
+def test_chunked_prompt_equals_whole_prompt_bitwise(variant, monkeypatch):
     """Prefilling a prompt in chunks (each chunk attends to the cached earlier chunks)
-    gives the rows of the whole-prompt prefill bit for bit: a row's result depends only on
-    its position, never on which launch computes it."""
+    gives the rows of the whole-prompt prefill bit for bit: with a given kernel, a row's
+    result depends only on its position, never on which launch computes it."""
+    monkeypatch.setenv("PA_PREFILL", variant)
     n, B, H, H_kv = 700, 16, 4, 4
     q, kc, vc, bt, cl, qs = prefill_problem([n], [n], B, H, H_kv, "f16")
     whole = run(q, kc, vc, bt, cl, qs, 0.088)
@@ -167,21 +169,21 @@ def test_prefill_sharegpt_sized_sampled_rows():
 
 
 @pytest.mark.parametrize("dtype", ["f16", "bf16"])
-def test_v1_and_warp_specialised_v2_agree(dtype, monkeypatch):
-    """The single-tile kernel (PA_PREFILL=1, P from shared memory) and the warp-specialised
-    two-tile kernel (default, P from tensor memory) perform the same softmax arithmetic; the
-    tensor cores' internal accumulation of the two operand sources may round differently,
-    so they agree to a few output ulps (and each is within TOL of the oracle)."""
+def test_kernel_variants_agree(dtype, monkeypatch):
+    """v1 (one query tile, P via shared memory), v2 (persistent, two query tiles per CTA)
+    and v3 (persistent, one query tile, softmax split by key columns) each match the oracle
+    and agree with one another to a few output ulps (the tensor cores' accumulation of
+    the operand sources and the split row sums round differently)."""
     ctx = [600, 130, 1500, 64, 257, 1000, 300]
     qlen = [64, 130, 1, 17, 200, 300, 300]
     q, kc, vc, bt, cl, qs = prefill_problem(ctx, qlen, 16, 8, 2, dtype, seed=91)
-    monkeypatch.setenv("PA_PREFILL", "1")
-    a = run(q, kc, vc, bt, cl, qs, 0.09)
-    monkeypatch.setenv("PA_PREFILL", "2")
-    b = run(q, kc, vc, bt, cl, qs, 0.09)
-    ulp = 2.0 ** -10 if dtype == "f16" else 2.0 ** -7  # output ulp at |o| < 1
-    diff = (a.float() - b.float()).abs().max().item()
-    print(f"v1 vs v2 max |diff| = {diff:.3g}")
-    assert diff <= 4 * ulp
     r = ref(q, kc, vc, bt, cl, qs, 0.09, 16, 2, dtype)
-    assert max_abs(a, r) <= TOL[dtype] and max_abs(b, r) <= TOL[dtype]
+    outs = []
+    for v in ("1", "2", "3"):
+        monkeypatch.setenv("PA_PREFILL", v)
+        outs.append(run(q, kc, vc, bt, cl, qs, 0.09))
+        assert max_abs(outs[-1], r) <= TOL[dtype], f"variant {v}"
+    ulp = 2.0 ** -10 if dtype == "f16" else 2.0 ** -7  # output ulp at |o| < 1
+    for o in outs[1:]:
+        diff = (o.float() - outs[0].float()).abs().max().item()
+        assert diff <= 4 * ulp
