@@ -1168,13 +1168,13 @@ template <typename Kern>
 cudaError_t set_smem(Kern k, size_t smem) {
     return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
-// PA_PREFILL=1/2/3 forces a kernel (ablations).  Default: v3 when every query fits one
-// 128-row tile (v2 would leave its second softmax group idle), else v2 (whose two query
-// tiles share each K/V tile: half the TMA copies per flop).
+// PA_PREFILL=1/2/3 forces a kernel (ablations).  Default: v3 when no query needs more than
+// 1.5 tiles of 128 rows (v2's pairs would mostly leave the second softmax group idle),
+// else v2, whose two query tiles share each K/V tile (measured).
 int prefill_variant(int max_query_len) {
     const char* e = getenv("PA_PREFILL");
     if (e && e[0] >= '1' && e[0] <= '3') return e[0] - '0';
-    return max_query_len <= kQ ? 3 : 2;
+    return max_query_len <= kQ + kQ / 2 ? 3 : 2;
 }
 }  // namespace
 

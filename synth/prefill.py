@@ -8,6 +8,8 @@ Configurations (reading c23):
               fit of synth.workload) until the batch holds >= 8192 query tokens;
               LLaMA-13B attention shape H = H_kv = 40, D = 128, f16, B = 16.
   p_2k        8 prompts of 2048 tokens (the model's maximum context), same shape.
+  p_chunk256  chunked prefill: 64 prompts whose next 256 tokens are computed after 768
+              already cached ones (a 1024-token prompt in four chunks).
   p_prefix1 / p_prefix5
               the shared-prefix translation workload of P:604-618: a cached prefix of 80
               (one-shot) / 341 (five-shot) tokens reserved once, 256 requests whose
@@ -26,6 +28,7 @@ PREFILL_CONFIGS = {
     "p_2k": dict(kind="uniform", n=8, length=2048, H=40, H_kv=40, B=16, dtype="f16", seed=1102),
     "p_prefix1": dict(kind="prefix", prefix=80, n=256, H=40, H_kv=40, B=16, dtype="f16", seed=1103),
     "p_prefix5": dict(kind="prefix", prefix=341, n=256, H=40, H_kv=40, B=16, dtype="f16", seed=1104),
+    "p_chunk256": dict(kind="chunk", n=64, chunk=256, done=768, H=40, H_kv=40, B=16, dtype="f16", seed=1105),
 }
 
 
@@ -40,6 +43,9 @@ def make_prefill(name: str, **over) -> dict:
         n = int(np.searchsorted(np.cumsum(prompt), c["tokens"]) + 1)
         ctx = prompt[:n].astype(np.int64)
         qlen = ctx.copy()
+    elif c["kind"] == "chunk":  # chunked prefill: the next `chunk` prompt tokens after `done` cached ones
+        ctx = np.full(c["n"], c["done"] + c["chunk"], np.int64)
+        qlen = np.full(c["n"], c["chunk"], np.int64)
     elif c["kind"] == "uniform":
         ctx = np.full(c["n"], c["length"], np.int64)
         qlen = ctx.copy()
