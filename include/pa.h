@@ -162,6 +162,51 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
                                        int max_blocks_per_seq, int num_query_tokens,
                                        int max_query_len, pa_dtype_t dtype, pa_stream_t stream);
 
+/* ------------------------------------------------------------------------------------
+ * Fused tensor-parallel all-gather.  Rank r of `world`
+ * computes heads [r*H_loc, (r+1)*H_loc) of the decode step (its own kv-head slice of the
+ * caches, the same block tables on every rank) and the attention kernel stores
+ * every output row straight into EVERY rank's gather buffer [S][H_total][D] (peer memory
+ * over NVLink; pointers opened with pa_ipc_open_handle), then a one-warp kernel exchanges
+ * completion flags: no NCCL call, no permute.
+ *
+ * pa_tp_comm_create: gather_a/gather_b/flags are HOST arrays of `world` DEVICE pointers
+ * as seen from this process (index k = rank k's buffer: gather buffers S*H_total*D*e
+ * bytes, 16-byte aligned; flag arrays int32[world], zero-initialised before first use);
+ * status: this rank's device int32, set to 1 if a flag wait times out (PA_TP_TIMEOUT_MS,
+ * default 10000) instead of hanging.  Returns NULL on invalid arguments (pa_last_error).
+ * The comm does not own any buffer.
+ *
+ * pa_paged_attention_decode_tp: arguments as pa_paged_attention_decode with the LOCAL
+ * head counts (num_heads * world == num_heads_total).  Calls alternate between the two
+ * gather buffers; *buffer_out (0 = gather_a, 1 = gather_b) names the one holding this
+ * call's full [S][H_total][D] output once the stream reaches the end of the call.  A
+ * result stays valid until this rank issues the call after next.  Every rank must make
+ * the same sequence of calls.  Output bits equal the single-GPU decode's.
+ * ---------------------------------------------------------------------------------- */
+typedef struct pa_tp_comm pa_tp_comm_t;
+pa_tp_comm_t* pa_tp_comm_create(int world, int rank, int num_heads_total, void* const* gather_a,
+                                void* const* gather_b, int32_t* const* flags, int32_t* status);
+void pa_tp_comm_destroy(pa_tp_comm_t* comm);
+pa_status_t pa_paged_attention_decode_tp(pa_tp_comm_t* comm, int* buffer_out, const void* query,
+                                         const void* key, const void* value, void* key_cache,
+                                         void* value_cache, const int32_t* block_tables,
+                                         const int32_t* context_lens, float scale, int block_size,
+                                         int num_kv_heads, int num_seqs, int num_heads,
+                                         int head_dim, int max_blocks_per_seq,
+                                         int max_context_len, pa_dtype_t dtype, void* workspace,
+                                         size_t workspace_bytes, pa_stream_t stream);
+
+/* CUDA IPC of device allocations between the ranks' processes (for the gather buffers and
+ * flags above).  Handles are pa_ipc_handle_bytes() opaque bytes; pa_device_alloc /
+ * pa_device_free give whole allocations whose handle maps to offset 0. */
+size_t pa_ipc_handle_bytes(void);
+pa_status_t pa_ipc_get_handle(const void* dev_ptr, void* handle_out);
+pa_status_t pa_ipc_open_handle(const void* handle, void** dev_ptr_out);
+pa_status_t pa_ipc_close_handle(void* dev_ptr);
+pa_status_t pa_device_alloc(size_t bytes, void** dev_ptr_out);
+pa_status_t pa_device_free(void* dev_ptr);
+
 /* Bytes of workspace pa_paged_attention(_ex) needs (0 if no context is split).
  * partition_tokens as in pa_paged_attention_ex. */
 size_t pa_paged_attention_workspace_size(int num_seqs, int num_heads, int head_dim,

@@ -59,6 +59,17 @@ _sig("pa_last_error", ctypes.c_char_p, [])
 _sig("pa_take_launch_count", ctypes.c_longlong, [])
 _sig("pa_debug_gather_kv", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp])
 _sig("pa_validate_tables", _i32, [_vp, _vp, _i32, _i32, _i32, _i32, ctypes.POINTER(_i64), _vp])
+_sig("pa_tp_comm_create", _vp, [_i32, _i32, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                _vp])
+_sig("pa_tp_comm_destroy", None, [_vp])
+_sig("pa_paged_attention_decode_tp", _i32, [_vp, ctypes.POINTER(ctypes.c_int), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                            _f32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _sz, _vp])
+_sig("pa_ipc_handle_bytes", _sz, [])
+_sig("pa_ipc_get_handle", _i32, [_vp, _vp])
+_sig("pa_ipc_open_handle", _i32, [_vp, ctypes.POINTER(_vp)])
+_sig("pa_ipc_close_handle", _i32, [_vp])
+_sig("pa_device_alloc", _i32, [_sz, ctypes.POINTER(_vp)])
+_sig("pa_device_free", _i32, [_vp])
 _sig("pa_alloc_create", _vp, [_i32, _i32, _vp])
 _sig("pa_alloc_destroy", None, [_vp])
 _sig("pa_alloc_allocate", _i32, [_vp, _i32, ctypes.POINTER(_i32)])

@@ -119,6 +119,13 @@ size_t pa_paged_attention_workspace_size(int num_seqs, int num_heads, int head_d
 }  // extern "C"
 
 namespace {
+// Fused TP all-gather destination (N2): rows of local head h go to every peer's gather
+// buffer at global head h0 + h of H_total.
+struct TpOut {
+    int n, H_total, h0;
+    void* peers[pa::kMaxTpPeers];
+};
+
 // Shared body of pa_paged_attention(_ex) and pa_paged_attention_decode (new_key != NULL:
 // the decode step's token s is written at logical position ctx[s]-1 by the kernel).
 pa_status_t attention_impl(void* out, const void* query, const void* new_key, const void* new_value,
@@ -126,7 +133,7 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
                            const int32_t* context_lens, float scale, int block_size, int num_kv_heads, int num_seqs,
                            int num_heads, int head_dim, int max_blocks_per_seq, int max_context_len,
                            pa_dtype_t dtype, int partition_tokens, void* workspace, size_t workspace_bytes,
-                           pa_stream_t stream, int group_size = 1) {
+                           pa_stream_t stream, int group_size = 1, const TpOut* tp = nullptr) {
     REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
     REQUIRE(num_seqs >= 0, "num_seqs must be >= 0 (got %d)", num_seqs);
     REQUIRE(num_heads > 0 && num_kv_heads > 0, "num_heads and num_kv_heads must be positive");
@@ -142,7 +149,7 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     REQUIRE(PT > 0 && PT % 16 == 0, "partition_tokens must be a positive multiple of 16 (got %d)", partition_tokens);
     REQUIRE(num_seqs <= 65535 && num_heads <= 65535, "num_seqs and num_heads must be <= 65535");
     if (num_seqs == 0) return PA_OK;
-    REQUIRE_PTR(out, 16);
+    if (tp == nullptr) REQUIRE_PTR(out, 16);
     REQUIRE_PTR(query, 16);
     REQUIRE_PTR(key_cache, 16);
     REQUIRE_PTR(value_cache, 16);
@@ -247,6 +254,12 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     p.S = num_seqs;
     p.listed = sched == 5;
     if (const char* ev = getenv("PA_HPW")) p.HPW = atoi(ev) > 0 ? atoi(ev) : 1;
+    if (tp != nullptr) {
+        p.n_out_peers = tp->n;
+        p.out_H = tp->H_total;
+        p.out_h0 = tp->h0;
+        for (int k = 0; k < tp->n; ++k) p.out_peers[k] = tp->peers[k];
+    }
     cudaError_t e = pa::launch_attention(p, (int)dtype, head_dim, num_seqs, sched, smem, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "pa_paged_attention");
     return PA_OK;
@@ -392,6 +405,125 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
     p.W = max_blocks_per_seq;
     cudaError_t e = pa::launch_prefill(p, (int)dtype, num_seqs, max_query_len, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "paged_prefill_kernel launch");
+    return PA_OK;
+}
+
+// ---- N2: fused tensor-parallel all-gather ------------------------------------------------
+struct pa_tp_comm {
+    int world, rank, H_total;
+    void* gather[2][pa::kMaxTpPeers];
+    int32_t* flags[pa::kMaxTpPeers];
+    int32_t* status;
+    int32_t epoch;
+    long long timeout_ns;
+};
+
+pa_tp_comm_t* pa_tp_comm_create(int world, int rank, int num_heads_total, void* const* gather_a,
+                                void* const* gather_b, int32_t* const* flags, int32_t* status) {
+    g_err.clear();
+    if (world < 1 || world > pa::kMaxTpPeers || rank < 0 || rank >= world || num_heads_total <= 0 ||
+        num_heads_total % world != 0 || !gather_a || !gather_b || !flags || !status) {
+        fail(PA_ERR_INVALID_ARG, "pa_tp_comm_create: world in [1,%d], 0 <= rank < world, heads divisible by world, "
+             "non-NULL buffers", pa::kMaxTpPeers);
+        return nullptr;
+    }
+    for (int k = 0; k < world; ++k) {
+        if (!gather_a[k] || !gather_b[k] || !flags[k] || !aligned(gather_a[k], 16) || !aligned(gather_b[k], 16) ||
+            !aligned(flags[k], 4)) {
+            fail(PA_ERR_INVALID_ARG, "pa_tp_comm_create: peer %d buffers NULL or misaligned", k);
+            return nullptr;
+        }
+    }
+    auto* c = new pa_tp_comm{};
+    c->world = world;
+    c->rank = rank;
+    c->H_total = num_heads_total;
+    for (int k = 0; k < world; ++k) {
+        c->gather[0][k] = gather_a[k];
+        c->gather[1][k] = gather_b[k];
+        c->flags[k] = flags[k];
+    }
+    c->status = status;
+    c->epoch = 0;
+    const char* ev = getenv("PA_TP_TIMEOUT_MS");
+    c->timeout_ns = (ev && atoll(ev) > 0 ? atoll(ev) : 10000) * 1000000LL;
+    return c;
+}
+
+void pa_tp_comm_destroy(pa_tp_comm_t* comm) { delete comm; }
+
+pa_status_t pa_paged_attention_decode_tp(pa_tp_comm_t* comm, int* buffer_out, const void* query, const void* key,
+                                         const void* value, void* key_cache, void* value_cache,
+                                         const int32_t* block_tables, const int32_t* context_lens, float scale,
+                                         int block_size, int num_kv_heads, int num_seqs, int num_heads, int head_dim,
+                                         int max_blocks_per_seq, int max_context_len, pa_dtype_t dtype,
+                                         void* workspace, size_t workspace_bytes, pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(comm != nullptr, "comm is NULL");
+    REQUIRE(num_heads * comm->world == comm->H_total, "local heads (%d) x world (%d) != total heads (%d)", num_heads,
+            comm->world, comm->H_total);
+    REQUIRE(key != nullptr && value != nullptr, "key/value (the step's new token) are NULL");
+    const int32_t epoch = comm->epoch + 1;
+    const int buf = (epoch - 1) & 1;  // the two gather buffers alternate (result valid until call +2)
+    TpOut tp{};
+    tp.n = comm->world;
+    tp.H_total = comm->H_total;
+    tp.h0 = comm->rank * num_heads;
+    for (int k = 0; k < comm->world; ++k) tp.peers[k] = comm->gather[buf][k];
+    pa_status_t st = attention_impl(nullptr, query, key, value, key_cache, value_cache, block_tables, context_lens,
+                                    scale, block_size, num_kv_heads, num_seqs, num_heads, head_dim,
+                                    max_blocks_per_seq, max_context_len, dtype, 0, workspace, workspace_bytes,
+                                    stream, 1, &tp);
+    if (st != PA_OK) return st;
+    cudaError_t e = pa::launch_tp_signal_wait(comm->flags, comm->world, comm->rank, epoch, comm->status,
+                                              comm->timeout_ns, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "tp_signal_wait launch");
+    comm->epoch = epoch;
+    if (buffer_out) *buffer_out = buf;
+    return PA_OK;
+}
+
+size_t pa_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+pa_status_t pa_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+    g_err.clear();
+    REQUIRE(dev_ptr != nullptr && handle_out != nullptr, "NULL argument");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    std::memcpy(handle_out, &h, sizeof(h));
+    return PA_OK;
+}
+
+pa_status_t pa_ipc_open_handle(const void* handle, void** dev_ptr_out) {
+    g_err.clear();
+    REQUIRE(handle != nullptr && dev_ptr_out != nullptr, "NULL argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    return PA_OK;
+}
+
+pa_status_t pa_ipc_close_handle(void* dev_ptr) {
+    g_err.clear();
+    cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+    return PA_OK;
+}
+
+pa_status_t pa_device_alloc(size_t bytes, void** dev_ptr_out) {
+    g_err.clear();
+    REQUIRE(dev_ptr_out != nullptr && bytes > 0, "bad argument");
+    cudaError_t e = cudaMalloc(dev_ptr_out, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    return PA_OK;
+}
+
+pa_status_t pa_device_free(void* dev_ptr) {
+    g_err.clear();
+    cudaError_t e = cudaFree(dev_ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFree");
     return PA_OK;
 }
 

@@ -163,6 +163,20 @@ __device__ __forceinline__ void store_out(T* o, float l, const float2 (&acc)[Att
     }
 }
 
+// store_out to this (sequence, head)'s output row: `out`, or with the fused TP all-gather
+// (N2) the row of global head out_h0 + h in every rank's gather buffer.
+template <typename T, int D>
+__device__ __forceinline__ void store_out_p(const AttnParams& p, int64_t sh, float l,
+                                            const float2 (&acc)[AttnCfg<T, D>::EPC], int c) {
+    if (p.n_out_peers == 0) {
+        store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
+        return;
+    }
+    const int64_t s = sh / p.H, h = sh - s * p.H;
+    const int64_t off = (s * p.out_H + p.out_h0 + h) * D;
+    for (int k = 0; k < p.n_out_peers; ++k) store_out<T, D>(static_cast<T*>(p.out_peers[k]) + off, l, acc, c);
+}
+
 // Lanes of token group 0: normalised partial o~ = acc / l (fp32).
 template <typename T, int D>
 __device__ __forceinline__ void store_partial(float* o, float l, const float2 (&acc)[AttnCfg<T, D>::EPC], int c) {
@@ -184,8 +198,8 @@ __device__ __forceinline__ void store_partial(float* o, float l, const float2 (&
 // ml[p] = (m_p, L_p), po[p*D + d] = o~_p[d]: the global workspace (written by other CTAs,
 // read through L2) or this CTA's shared memory -- the arithmetic is the same either way.
 template <typename T, int D, bool kGlobal>
-__device__ __forceinline__ void merge_partitions_from(const float2* ml, const float* po, T* out_row, int np,
-                                                      int lane) {
+__device__ __forceinline__ void merge_partitions_from(const AttnParams& p, int64_t sh, const float2* ml,
+                                                      const float* po, int np, int lane) {
     auto ld2 = [](const float2* a) { return kGlobal ? __ldcg(a) : *a; };
     auto ld1 = [](const float* a) { return kGlobal ? __ldcg(a) : *a; };
     float M = -INFINITY;
@@ -202,14 +216,22 @@ __device__ __forceinline__ void merge_partitions_from(const float2* ml, const fl
 #pragma unroll
         for (int e = 0; e < DPL; ++e) o[e] += w * ld1(po + (int64_t)i * D + lane * DPL + e);
     }
+    auto store_row = [&](T* out_row) {
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) out_row[lane * DPL + e] = Elem<T>::from_f32(o[e] / L);
+        for (int e = 0; e < DPL; ++e) out_row[lane * DPL + e] = Elem<T>::from_f32(o[e] / L);
+    };
+    if (p.n_out_peers == 0) {
+        store_row(static_cast<T*>(p.out) + sh * D);
+    } else {
+        const int64_t s = sh / p.H, h = sh - s * p.H;
+        const int64_t off = (s * p.out_H + p.out_h0 + h) * D;
+        for (int k = 0; k < p.n_out_peers; ++k) store_row(static_cast<T*>(p.out_peers[k]) + off);
+    }
 }
 
 template <typename T, int D>
 __device__ __forceinline__ void merge_partitions(const AttnParams& p, int64_t sh, int np, int lane) {
-    merge_partitions_from<T, D, true>(p.part_ml + sh * p.NP, p.part_o + sh * p.NP * D,
-                                      static_cast<T*>(p.out) + sh * D, np, lane);
+    merge_partitions_from<T, D, true>(p, sh, p.part_ml + sh * p.NP, p.part_o + sh * p.NP * D, np, lane);
 }
 
 // Publish this partition's (m, L, o~); the last partition to finish merges.  Whole warp.
@@ -590,7 +612,7 @@ __global__ void __launch_bounds__(256) paged_attention_persistent_kernel(const A
             merge_token_groups<T, D>(m, l, acc);
             const int64_t sh = (int64_t)c_s * H + c_h;
             if (c_nparts == 1) {
-                if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
+                if (g == 0) store_out_p<T, D>(p, sh, l, acc, c);
             } else {
                 finish_split<T, D>(p, sh, c_part, c_nparts, m, l, acc, g, c, lane);
             }
@@ -626,7 +648,7 @@ __device__ __forceinline__ void stream_heads(const AttnParams& p, int s, int par
     if (ntiles == 0) {  // empty context: zeros
         if (g == 0)
             for (int u = 0; u < nu; ++u)
-                store_out<T, D>(static_cast<T*>(p.out) + ((int64_t)s * p.H + h_first + u * h_step) * D, 0.f, acc, c);
+                store_out_p<T, D>(p, (int64_t)s * p.H + h_first + u * h_step, 0.f, acc, c);
         return;
     }
     const int total = nu * ntiles;
@@ -703,7 +725,7 @@ __device__ __forceinline__ void stream_heads(const AttnParams& p, int s, int par
             merge_token_groups<T, D>(m, l, acc);
             const int64_t sh = (int64_t)s * p.H + h;
             if (nparts == 1) {
-                if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
+                if (g == 0) store_out_p<T, D>(p, sh, l, acc, c);
             } else {
                 finish_split<T, D>(p, sh, part, nparts, m, l, acc, g, c, lane);
             }
@@ -920,7 +942,7 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
         if (tok0 + kTile >= part_end) {  // last tile of this partition
             merge_token_groups<T, D>(m, l, acc);
             if (nparts == 1) {
-                if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
+                if (g == 0) store_out_p<T, D>(p, sh, l, acc, c);
             } else if (whole) {  // keep (m, L, o~) in shared memory; merged below
                 if (g == 0) store_partial<T, D>(my_po + (part - c0) * D, l, acc, c);
                 if (lane == 0) my_ml[part - c0] = make_float2(m, l);
@@ -936,10 +958,10 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
         }
     }
     if (ntiles == 0 && g == 0)  // empty context
-        store_out<T, D>(static_cast<T*>(p.out) + sh * D, 0.f, acc, c);
+        store_out_p<T, D>(p, sh, 0.f, acc, c);
     if (whole) {
         __syncwarp();
-        merge_partitions_from<T, D, false>(my_ml, my_po, static_cast<T*>(p.out) + sh * D, nparts, lane);
+        merge_partitions_from<T, D, false>(p, sh, my_ml, my_po, nparts, lane);
     }
 }
 
@@ -1146,7 +1168,7 @@ __global__ void __launch_bounds__(288) paged_attention_pcoop_kernel(const AttnPa
             merge_token_groups<T, D>(m, l, acc);
             const int64_t sh = (int64_t)s * H + h;
             if (nparts == 1) {
-                if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
+                if (g == 0) store_out_p<T, D>(p, sh, l, acc, c);
             } else {
                 finish_split<T, D>(p, sh, part, nparts, m, l, acc, g, c, lane);
             }
@@ -1328,7 +1350,7 @@ __global__ void __launch_bounds__(288) paged_attention_shared_kernel(const AttnP
     if (part > 0 && p0 >= ctx) return;  // this member has no tokens in the partition
     merge_token_groups<T, D>(m, l, acc);
     if (nparts == 1) {
-        if (g == 0) store_out<T, D>(static_cast<T*>(p.out) + sh * D, l, acc, c);
+        if (g == 0) store_out_p<T, D>(p, sh, l, acc, c);
     } else {
         finish_split<T, D>(p, sh, part, nparts, m, l, acc, g, c, lane);
     }

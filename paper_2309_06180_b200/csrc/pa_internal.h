@@ -28,6 +28,8 @@ struct PrefillParams {
     int X, S;                     // query-tile pairs per sequence (grid of work items), sequences
 };
 
+constexpr int kMaxTpPeers = 8;
+
 struct AttnParams {
     void* out;                  // [S][H][D]
     const void* query;          // [S][H][D]
@@ -58,6 +60,12 @@ struct AttnParams {
     int S;                      // number of sequences
     int listed;                 // coop: CTAs take (sequence, partition) from the work list
     int STG;                    // tiles in flight per warp (shared-memory stages)
+    // fused tensor-parallel all-gather (N2): when n_out_peers > 0 every output row of local
+    // head h is stored to out_peers[k] + ((s * out_H) + out_h0 + h) * D for every rank k
+    // (peer memory over NVLink) instead of `out`
+    int n_out_peers;
+    int out_H, out_h0;
+    void* out_peers[kMaxTpPeers];
 };
 
 struct GatherParams {
@@ -128,6 +136,10 @@ cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int n
                              cudaStream_t stream);
 size_t prefill_smem_bytes();
 cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, cudaStream_t stream);
+// N2: rank `rank` publishes `epoch` to every peer's flag array, then waits (bounded) until
+// every peer has published it to this rank; status = 1 on timeout
+cudaError_t launch_tp_signal_wait(int32_t* const* flag_peers, int world, int rank, int32_t epoch, int32_t* status,
+                                  long long timeout_ns, cudaStream_t stream);
 cudaError_t launch_debug_gather(const GatherParams& p, int dtype, int head_dim, int num_seqs, cudaStream_t stream);
 cudaError_t launch_reshape_and_cache(const CacheWriteParams& p, cudaStream_t stream);
 cudaError_t launch_copy_blocks(const CopyBlocksParams& p, int num_layers, int num_pairs, cudaStream_t stream);
