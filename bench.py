@@ -118,6 +118,10 @@ def parse():
     ap.add_argument("--unfused", action="store_true", help="separate reshape_and_cache launch (ablation)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also print per-config lines for the other configs")
+    ap.add_argument("--tp-gather", default="auto", choices=["auto", "fused", "nccl"],
+                    help="N>1 output exchange: fused (attention stores into every rank's buffer over "
+                         "CUDA IPC / NVLink, pa_paged_attention_decode_tp) or an NCCL all-gather; auto = fused "
+                         "if the IPC setup succeeds")
     return ap.parse_args()
 
 
@@ -206,6 +210,18 @@ def run_ours(a, wl_full, world, rank, local):
     ws = torch.zeros(max(ws_n, 16), dtype=torch.uint8, device=dev)
     gathered = torch.empty((world * wl.S, wl.H, wl.D), dtype=q.dtype, device=dev) if world > 1 else None
     full_out = torch.empty((wl.S, wl.H * world, wl.D), dtype=q.dtype, device=dev) if world > 1 else None
+    tp_gather, ftp = "none", None
+    if world > 1:
+        tp_gather = "nccl"
+        if a.tp_gather in ("auto", "fused") and not a.unfused:
+            from paper_2309_06180_b200.tp import FusedTP
+            try:
+                ftp = FusedTP(None, wl.S, wl.H * world, wl.D, q.dtype, dev)
+                tp_gather = "fused"
+            except Exception as exc:  # e.g. CUDA IPC not permitted in this container
+                if a.tp_gather == "fused":
+                    raise
+                tp_gather = f"nccl (fused setup failed: {type(exc).__name__}: {exc})"
     has_pairs = len(wl.block_mapping) > 0
     stream = torch.cuda.current_stream(dev)
     ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
@@ -218,14 +234,16 @@ def run_ours(a, wl_full, world, rank, local):
             pa.reshape_and_cache(kn, vn, kc, vc, sm)
         if i is not None:
             ev_a0[i].record(stream)
-        if a.unfused:
+        if ftp is not None:  # attention + fused all-gather: rows stored into every rank's buffer
+            ftp.decode(q, kn, vn, kc, vc, bt, cl, wl.scale, max_context_len=mcl, workspace=ws)
+        elif a.unfused:
             pa.paged_attention(out, q, kc, vc, bt, cl, wl.scale, max_context_len=mcl,
                                partition_tokens=a.partition_tokens, workspace=ws)
         else:  # the decode step's cache write fused into the attention kernel
             pa.paged_attention_decode(out, q, kn, vn, kc, vc, bt, cl, wl.scale, max_context_len=mcl, workspace=ws)
         if i is not None:
             ev_a1[i].record(stream)
-        if world > 1:  # the one exchange: all-gather of the output head slices (NCCL / NVLink)
+        if world > 1 and ftp is None:  # the one exchange: all-gather of the output head slices (NCCL)
             full_out.copy_(gather_heads(out, buffer=gathered))
 
     for _ in range(max(3, a.warmup)):
@@ -253,6 +271,11 @@ def run_ours(a, wl_full, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total, attn_ms = float(t[0]), float(t[1])
     ms_step = ms_total / a.steps
+    if ftp is not None:
+        status = int(ftp.status.item())
+        if status != 0:
+            raise RuntimeError("fused TP all-gather: a flag wait timed out")
+        ftp.close()
 
     # ---- e2e: the same step through pa_decode_step with pinned host buffers ----------
     e2e = None
@@ -279,6 +302,7 @@ def run_ours(a, wl_full, world, rank, local):
                    "head_dim": wl_full.D, "block_size": wl_full.B, "kv_dtype": wl_full.dtype,
                    "mean_ctx": float(wl_full.context_lens.mean()), "max_ctx": int(wl_full.max_context_len),
                    "cow_pairs": int(len(wl_full.block_mapping)), "parallelism": f"tp{world}",
+                   "tp_gather": tp_gather,
                    "partition_tokens": a.partition_tokens or pa.DEFAULT_PARTITION_TOKENS,
                    "l2": "inputs larger than L2 (KV %.2f GB vs 126 MB L2); no flush" % (kv_all / 1e9)},
         "tokens_per_s": wl_full.S / (ms_step * 1e-3),

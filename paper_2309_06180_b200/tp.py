@@ -93,32 +93,50 @@ class FusedTP:
         self.out_bytes = S * H_total * D * esz
         self._opened = []
         if _peer_ptrs is None:
-            self.bufs = [_DevBuf(self.out_bytes), _DevBuf(self.out_bytes), _DevBuf(4 * self.world + 4)]
-            flags = _as_tensor(self.bufs[2].ptr.value, (self.world + 1,), torch.int32, self.device)
-            flags.zero_()
-            torch.cuda.synchronize(self.device)
-            nb = _lib.raw().pa_ipc_handle_bytes()
-            mine = []
-            for b in self.bufs:
-                hb = ctypes.create_string_buffer(nb)
-                _lib.check(_lib.raw().pa_ipc_get_handle(b.ptr, hb), "pa_ipc_get_handle")
-                mine.append(hb.raw)
+            # every rank takes part in every collective below even if its own step fails,
+            # and all ranks agree on the outcome (raise everywhere or nowhere)
+            self.bufs, mine, err = None, None, None
+            try:
+                self.bufs = [_DevBuf(self.out_bytes), _DevBuf(self.out_bytes), _DevBuf(4 * self.world + 4)]
+                flags = _as_tensor(self.bufs[2].ptr.value, (self.world + 1,), torch.int32, self.device)
+                flags.zero_()
+                torch.cuda.synchronize(self.device)
+                nb = _lib.raw().pa_ipc_handle_bytes()
+                mine = []
+                for b in self.bufs:
+                    hb = ctypes.create_string_buffer(nb)
+                    _lib.check(_lib.raw().pa_ipc_get_handle(b.ptr, hb), "pa_ipc_get_handle")
+                    mine.append(hb.raw)
+            except Exception as exc:  # noqa: BLE001 -- reported to every rank below
+                err, mine = f"{type(exc).__name__}: {exc}", None
             allh = [None] * self.world
             dist.all_gather_object(allh, mine, group=group)
             peers = []
-            for k in range(self.world):
-                if k == self.rank:
-                    peers.append([b.ptr.value for b in self.bufs])
-                    continue
-                ptrs = []
-                for hbytes in allh[k]:
-                    p = ctypes.c_void_p()
-                    _lib.check(_lib.raw().pa_ipc_open_handle(ctypes.create_string_buffer(hbytes, nb), ctypes.byref(p)),
-                               "pa_ipc_open_handle")
-                    self._opened.append(p)
-                    ptrs.append(p.value)
-                peers.append(ptrs)
-            dist.barrier(group=group)
+            if err is None and all(h is not None for h in allh):
+                try:
+                    nb = _lib.raw().pa_ipc_handle_bytes()
+                    for k in range(self.world):
+                        if k == self.rank:
+                            peers.append([b.ptr.value for b in self.bufs])
+                            continue
+                        ptrs = []
+                        for hbytes in allh[k]:
+                            p = ctypes.c_void_p()
+                            _lib.check(_lib.raw().pa_ipc_open_handle(ctypes.create_string_buffer(hbytes, nb),
+                                                                      ctypes.byref(p)), "pa_ipc_open_handle")
+                            self._opened.append(p)
+                            ptrs.append(p.value)
+                        peers.append(ptrs)
+                except Exception as exc:  # noqa: BLE001
+                    err = f"{type(exc).__name__}: {exc}"
+            elif err is None:
+                err = "a peer failed to create its buffers"
+            errs = [None] * self.world
+            dist.all_gather_object(errs, err, group=group)
+            if any(e is not None for e in errs):
+                self.close()
+                raise RuntimeError("fused TP setup failed: " + "; ".join(f"rank {k}: {e}" for k, e in
+                                                                         enumerate(errs) if e is not None))
         else:  # simulated ranks in one process: peers = [[gather_a, gather_b, flags_with_status], ...]
             self.bufs = None
             peers = _peer_ptrs
