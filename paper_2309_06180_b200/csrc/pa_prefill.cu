@@ -750,11 +750,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
                 emit(sb, 32);
                 emit(sc, 64);
                 emit(sd, 96);
-                // P_t is out; now O_t *= alpha (PV_t of the previous tile has completed: this
-                // S_t was issued after it)
-                if (j > 0 && bump) {
+                // P_t is out; now O_t *= alpha.  PV_t of the previous tile has completed (this
+                // S_t was issued after it), so this wait returns at once; it is not skipped
+                // so that every o_done phase is waited on
+                if (j > 0) {
                     mbar_wait(&o_done[t], (ns - 1) & 1);
                     tc_fence_after();
+                }
+                if (j > 0 && bump) {
 #pragma unroll
                     for (int c0 = 0; c0 < 128; c0 += 32) {
                         float v[32];
@@ -1092,9 +1095,11 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_split_kernel(cons
                 };
                 emit(sa, 0);
                 emit(sb, 32);
-                if (j > 0 && bump) {  // O columns of this half *= alpha
+                if (j > 0) {  // P V of the previous tile done (never skipped: every phase is waited on)
                     mbar_wait(o_done, (ns - 1) & 1);
                     tc_fence_after();
+                }
+                if (j > 0 && bump) {  // O columns of this half *= alpha
 #pragma unroll
                     for (int c0 = 0; c0 < 64; c0 += 32) {
                         float v[32];
