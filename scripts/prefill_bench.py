@@ -5,7 +5,9 @@ Per config, one JSON line: kernel time (CUDA events on the launching stream, mea
 (query row, head, attended token), causal) against the measured dense bf16 peak of
 MEASURED_PEAKS.json (f16 has the same nominal tensor rate), query tokens/s, and as
 context torch's scaled_dot_product_attention on the same prompts with CONTIGUOUS K/V
-(no paging; library kernels, padded batch) where the prompts are uniform (p_2k).
+(no paging; library kernels, padded batch) where the prompts are uniform (p_2k), and the
+fp64 oracle (oracle.prefill_attention, as it stands) timed on the host cores on a bounded
+sample of the same workload (`cpu_baseline`, TFLOP/s of the sample's algorithmic flops).
 Caches hold U(-1,1) values; unused slots are NaN.
 """
 import argparse
@@ -14,7 +16,7 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
+sys.path.insert(0, ROOT)  # the oracle (cpu_baseline only) and tests.pathutil live at the repo root
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -62,11 +64,36 @@ def build(c, dev="cuda"):
         torch.as_tensor(c["ctx"].astype(np.int32), device=dev), qs
 
 
+def oracle_baseline(c, q, kc, vc, bt, cl, budget_rows=512, heads=4):
+    """The fp64 oracle on a bounded sample: the last `budget_rows` query rows of the
+    longest sequence (the most expensive rows) x `heads` query heads (and their kv heads)."""
+    import time
+
+    import oracle
+    from tests.pathutil import bits
+    s = int(np.argmax(c["ctx"]))
+    ql, ctx = int(c["qlen"][s]), int(c["ctx"][s])
+    n = min(budget_rows, ql)
+    qs_all = np.concatenate([[0], np.cumsum(c["qlen"])])
+    rows = bits(q[qs_all[s] + ql - n: qs_all[s] + ql, :heads])
+    G = c["H"] // c["H_kv"]
+    kvh = max(1, heads // G)
+    kcs, vcs = bits(kc[:, :kvh].contiguous()), bits(vc[:, :kvh].contiguous())
+    t0 = time.perf_counter()
+    oracle.prefill_attention(rows, kcs, vcs, bt[s:s + 1].cpu().numpy(), np.array([ctx], np.int32),
+                             np.array([0, n], np.int32), 1.0 / np.sqrt(D), c["B"], kvh, c["dtype"])
+    dt = time.perf_counter() - t0
+    flops = algorithmic_flops(np.array([ctx]), np.array([n]), heads, D)
+    return {"value": round(flops / dt / 1e12, 6), "unit": "TFLOP/s", "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"last {n} query rows of the longest sequence (ctx {ctx}) x {heads} heads, {dt:.2f} s"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default=",".join(PREFILL_CONFIGS))
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--block-size", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     peak, peak_src = peaks()
     for name in args.configs.split(","):
@@ -94,6 +121,8 @@ def main():
                          args.iters)
             res["sdpa_contiguous_ms"] = round(ts * 1e3, 4)
             res["sdpa_contiguous_tflops"] = round(flops / ts / 1e12, 1)
+        if not args.no_cpu_baseline:
+            res["cpu_baseline"] = oracle_baseline(c, q, kc, vc, bt, cl)
         print(json.dumps(res), flush=True)
         del q, kc, vc, out
 
