@@ -117,6 +117,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="separate reshape_and_cache launch (ablation)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the N4 prompt-phase context line")
     ap.add_argument("--extra", action="store_true", help="also print per-config lines for the other configs")
     ap.add_argument("--tp-gather", default="auto", choices=["auto", "fused", "nccl"],
                     help="N>1 output exchange: fused (attention stores into every rank's buffer over "
@@ -283,6 +284,9 @@ def run_ours(a, wl_full, world, rank, local):
         e2e = run_e2e(a, wl, world, dev, {"query": q, "key": kn, "value": vn}, kc, vc, mcl, ws, stream)
 
     probe = read_probe(dev)
+    n4 = None
+    if world == 1 and not a.no_prefill:
+        n4 = prefill_summary(dev)
     if rank != 0:
         return
     peak, peak_src = load_peaks()
@@ -320,9 +324,54 @@ def run_ours(a, wl_full, world, rank, local):
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if n4 is not None:
+        line["n4_prefill"] = n4
     if not a.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(wl_full)
     print(json.dumps(line), flush=True)
+
+
+def prefill_summary(dev, name: str = "p_2k", iters: int = 20):
+    """Context only (not the headline): the N4 prompt-phase kernel on one synth.prefill
+    workload, timed the same way as scripts/prefill_bench.py (CUDA events, mean of
+    `iters` launches after 3 warm-up), algorithmic TFLOP/s vs the measured bf16 peak."""
+    import torch
+
+    import paper_2309_06180_b200 as pa
+    from synth.prefill import algorithmic_flops, make_prefill
+    c = make_prefill(name)
+    dt = torch.float16 if c["dtype"] == "f16" else torch.bfloat16
+    g = torch.Generator(device=dev)
+    g.manual_seed(c["seed"])
+    D = 128
+    kc = (torch.rand((c["num_blocks"], c["H_kv"], c["B"], D), generator=g, device=dev) * 2 - 1).to(dt)
+    vc = (torch.rand(tuple(kc.shape), generator=g, device=dev) * 2 - 1).to(dt)
+    T = int(c["qlen"].sum())
+    q = (torch.rand((T, c["H"], D), generator=g, device=dev) * 2 - 1).to(dt)
+    qs = torch.as_tensor(np.concatenate([[0], np.cumsum(c["qlen"])]).astype(np.int32), device=dev)
+    bt = torch.as_tensor(c["block_tables"], device=dev)
+    cl = torch.as_tensor(c["ctx"].astype(np.int32), device=dev)
+    out = torch.empty_like(q)
+    mql = int(c["qlen"].max())
+    for _ in range(3):
+        pa.paged_prefill_attention(out, q, kc, vc, bt, cl, qs, D ** -0.5, max_query_len=mql)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        pa.paged_prefill_attention(out, q, kc, vc, bt, cl, qs, D ** -0.5, max_query_len=mql)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    tflops = algorithmic_flops(c["ctx"], c["qlen"], c["H"], D) / (ms * 1e-3) / 1e12
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak = float(json.load(f)["bf16_tflops"])
+    except Exception:
+        peak = 2250.0
+    return {"workload": name, "ms": round(ms, 4), "tflops": round(tflops, 1), "peak_tflops": peak,
+            "frac": round(tflops / peak, 3), "bound": "tensor", "query_tokens": T,
+            "note": "tcgen05 prompt-phase kernel (SURVEY §8(f) N4), context only; see DESIGN.md §8c"}
 
 
 def read_probe(dev, gib: float = 4.0):
