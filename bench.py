@@ -353,13 +353,14 @@ def prefill_summary(dev, name: str = "p_2k", iters: int = 20):
     cl = torch.as_tensor(c["ctx"].astype(np.int32), device=dev)
     out = torch.empty_like(q)
     mql = int(c["qlen"].max())
+    ws = torch.empty(16, dtype=torch.uint8, device=dev)
     for _ in range(3):
-        pa.paged_prefill_attention(out, q, kc, vc, bt, cl, qs, D ** -0.5, max_query_len=mql)
+        pa.paged_prefill_attention(out, q, kc, vc, bt, cl, qs, D ** -0.5, max_query_len=mql, workspace=ws)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(iters):
-        pa.paged_prefill_attention(out, q, kc, vc, bt, cl, qs, D ** -0.5, max_query_len=mql)
+        pa.paged_prefill_attention(out, q, kc, vc, bt, cl, qs, D ** -0.5, max_query_len=mql, workspace=ws)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / iters

@@ -152,15 +152,19 @@ pa_status_t pa_paged_attention_decode_shared(void* out, const void* query, const
  * (sizes the grid).  All device pointers; the caller owns every buffer.  f16/bf16,
  * head_dim 128 only (PA_ERR_UNSUPPORTED otherwise).  Softmax weights are rounded to the
  * storage dtype before the P.V product.  T == 0 or S == 0 is a no-op.
- * Asynchronous on `stream`; no workspace.
+ * workspace: device, >= PA_PREFILL_WORKSPACE_BYTES, 16-byte aligned, any content: the
+ * call zeroes its work-item counter on `stream` (calls sharing a workspace must be
+ * ordered on one stream).  Asynchronous on `stream`.
  * ---------------------------------------------------------------------------------- */
+#define PA_PREFILL_WORKSPACE_BYTES 16
 pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void* key_cache,
                                        const void* value_cache, const int32_t* block_tables,
                                        const int32_t* context_lens, const int32_t* query_start,
                                        float scale, int block_size, int num_kv_heads,
                                        int num_blocks, int num_seqs, int num_heads, int head_dim,
                                        int max_blocks_per_seq, int num_query_tokens,
-                                       int max_query_len, pa_dtype_t dtype, pa_stream_t stream);
+                                       int max_query_len, pa_dtype_t dtype, void* workspace,
+                                       size_t workspace_bytes, pa_stream_t stream);
 
 /* ------------------------------------------------------------------------------------
  * Fused tensor-parallel all-gather.  Rank r of `world`

@@ -348,7 +348,8 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
                                        const int32_t* query_start, float scale, int block_size, int num_kv_heads,
                                        int num_blocks, int num_seqs, int num_heads, int head_dim,
                                        int max_blocks_per_seq, int num_query_tokens, int max_query_len,
-                                       pa_dtype_t dtype, pa_stream_t stream) {
+                                       pa_dtype_t dtype, void* workspace, size_t workspace_bytes,
+                                       pa_stream_t stream) {
     REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
     if (dtype == PA_F32) return fail(PA_ERR_UNSUPPORTED, "prefill attention supports f16 and bf16 only");
     if (head_dim != 128) return fail(PA_ERR_UNSUPPORTED, "prefill attention supports head_dim 128 only (got %d)", head_dim);
@@ -371,7 +372,12 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
     REQUIRE_PTR(block_tables, 4);
     REQUIRE_PTR(context_lens, 4);
     REQUIRE_PTR(query_start, 4);
+    if (workspace == nullptr || workspace_bytes < PA_PREFILL_WORKSPACE_BYTES)
+        return fail(PA_ERR_WORKSPACE, "prefill workspace must be >= %d bytes (got %zu)", PA_PREFILL_WORKSPACE_BYTES,
+                    workspace ? workspace_bytes : (size_t)0);
+    REQUIRE_PTR(workspace, 16);
     pa::PrefillParams p{};
+    p.work_counter = static_cast<int*>(workspace);
     const CUtensorMapDataType dt =
         dtype == PA_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     {

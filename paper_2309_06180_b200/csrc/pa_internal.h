@@ -26,6 +26,7 @@ struct PrefillParams {
     int log2B, H, H_kv, G, W;
     int box_rows;                 // min(block_size, 128) tokens per TMA box
     int X, S;                     // query-tile pairs per sequence (grid of work items), sequences
+    int* work_counter;            // v2: dynamic work-item counter (zeroed on the stream by the launcher)
 };
 
 constexpr int kMaxTpPeers = 8;

@@ -112,22 +112,30 @@ def paged_attention_decode_shared(out, query, key, value, key_cache, value_cache
     return out
 
 
+PREFILL_WORKSPACE_BYTES = 16
+
+
 def paged_prefill_attention(out, query, key_cache, value_cache, block_tables, context_lens, query_start,
-                            scale: float, max_query_len: int = 0, stream=None):
+                            scale: float, max_query_len: int = 0, workspace: torch.Tensor | None = None,
+                            stream=None):
     """Causal multi-token attention over the paged cache (pa.h):
     query/out [T][H][D] with sequence s's rows in [query_start[s], query_start[s+1]), the
     last q_len of its context_lens[s] cached tokens.  tcgen05 tensor cores, f16/bf16, D=128.
-    max_query_len sizes the grid; 0 reads it from query_start (a device->host sync)."""
+    max_query_len sizes the grid; 0 reads it from query_start (a device->host sync).
+    `workspace` (uint8 device tensor, >= 16 bytes, any content) holds the work-item
+    counter; allocated per call when omitted."""
     T, H, D = query.shape
     NB, hk, B, _ = key_cache.shape
     S, W = block_tables.shape
     if max_query_len <= 0:
         max_query_len = int((query_start[1:] - query_start[:-1]).max().item()) if S > 0 else 0
+    if workspace is None:
+        workspace = torch.empty(PREFILL_WORKSPACE_BYTES, dtype=torch.uint8, device=query.device)
     check(_lib.raw().pa_paged_prefill_attention(
         _dev(out, "out"), _dev(query, "query"), _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"),
         _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"), _dev(query_start, "query_start"),
-        float(scale), B, hk, NB, S, H, D, W, T, int(max_query_len), _code(query), _stream(stream)),
-        "pa_paged_prefill_attention")
+        float(scale), B, hk, NB, S, H, D, W, T, int(max_query_len), _code(query), _dev(workspace, "workspace"),
+        workspace.numel() * workspace.element_size(), _stream(stream)), "pa_paged_prefill_attention")
     return out
 
 

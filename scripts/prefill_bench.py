@@ -102,7 +102,9 @@ def main():
         out = torch.empty_like(q)
         mql = int(c["qlen"].max())
         scale = 1.0 / np.sqrt(D)
-        fn = lambda: pa.paged_prefill_attention(out, q, kc, vc, bt, cl, qs, scale, max_query_len=mql)  # noqa: E731
+        ws = torch.empty(16, dtype=torch.uint8, device="cuda")
+        fn = lambda: pa.paged_prefill_attention(out, q, kc, vc, bt, cl, qs, scale, max_query_len=mql,  # noqa: E731
+                                                workspace=ws)
         pa.take_launch_count()
         t = time_it(fn, args.iters)
         launches = pa.take_launch_count() / (args.iters + 5)

@@ -80,11 +80,11 @@ def test_attention_argument_validation(kw, status):
 
 def prefill(**kw):
     a = dict(out=FAKE, q=FAKE, kc=FAKE, vc=FAKE, bt=FAKE, cl=FAKE, qs=FAKE, scale=0.125, B=16, hkv=2, NB=64, S=4, H=2,
-             D=128, W=8, T=100, mql=40, dt=2)
+             D=128, W=8, T=100, mql=40, dt=2, ws=FAKE, wsb=16)
     a.update(kw)
     return L.pa_paged_prefill_attention(a["out"], a["q"], a["kc"], a["vc"], a["bt"], a["cl"], a["qs"], a["scale"],
                                         a["B"], a["hkv"], a["NB"], a["S"], a["H"], a["D"], a["W"], a["T"], a["mql"],
-                                        a["dt"], None)
+                                        a["dt"], a["ws"], a["wsb"], None)
 
 
 @pytest.mark.parametrize("kw,status", [
@@ -99,6 +99,9 @@ def prefill(**kw):
     (dict(dt=7), INVALID),
     (dict(scale=float("inf")), INVALID),
     (dict(NB=1 << 28, hkv=8, H=8), INVALID),
+    (dict(ws=None), WORKSPACE),
+    (dict(wsb=8), WORKSPACE),
+    (dict(ws=FAKE + 4), INVALID),
 ])
 def test_prefill_argument_validation(kw, status):
     assert prefill(**kw) == status
