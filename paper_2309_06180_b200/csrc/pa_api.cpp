@@ -387,7 +387,7 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
         if (!encode_map(&p.tmap_q, dt, 3, query, dims, str, box))
             return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the query map");
     }
-    p.box_rows = std::min(block_size, 128);
+    p.box_rows = std::min(block_size, 64);  // a box never spans a 64-token tile (v4)
     {
         const cuuint64_t dims[2] = {(cuuint64_t)head_dim, (cuuint64_t)num_blocks * num_kv_heads * block_size};
         const cuuint64_t str[1] = {(cuuint64_t)head_dim * 2};

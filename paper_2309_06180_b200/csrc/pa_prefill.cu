@@ -168,14 +168,14 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t
 }
 
 // Instruction descriptor, kind::f16: fp32 accumulate, M=128, N=128.
-__host__ __device__ constexpr uint32_t umma_idesc(bool bf16, bool b_mn_major) {
+__host__ __device__ constexpr uint32_t umma_idesc(bool bf16, bool b_mn_major, uint32_t n = 128) {
     return (1u << 4)                        // c_format = F32
            | ((bf16 ? 1u : 0u) << 7)        // a_format
            | ((bf16 ? 1u : 0u) << 10)       // b_format
            | (0u << 15)                     // a K-major
            | ((b_mn_major ? 1u : 0u) << 16) // b major
-           | ((128u >> 3) << 17)            // N
-           | ((128u >> 4) << 24);           // M
+           | ((n >> 3) << 17)               // N
+           | ((128u >> 4) << 24);           // M = 128
 }
 
 constexpr int kQ = 128;        // query rows per CTA
@@ -850,6 +850,376 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     }
 }
 
+// ---- v4: as v2 with 64-token K/V tiles and two S buffers per query tile ------------------
+// Tensor memory: S_t[b] (64 columns each, t = query tile, b = tile parity) in columns
+// [0,256), O_0 / O_1 in [256,512).  P_t(j) aliases S_t[j&1], so S_t(j+1) goes to the other
+// buffer and is computed while the softmax of tile j runs: the tensor-core work of a tile
+// no longer sits between one softmax and the next (v2's critical chain).  MMA order per
+// tile j: PV_0(j), PV_1(j), then S_0(j+2), S_1(j+2).  K and V in four 16 KB stages each.
+constexpr int kN4 = 64;                 // K/V tokens per tile
+constexpr int kHalf4 = kN4 * 128;       // bytes of one [64 rows][64 elements] swizzled half
+constexpr int kStages4 = 4;
+
+__device__ __forceinline__ bool prefill_item4(const PrefillParams& p, int i, PrefillItem& it) {
+    const int g = i / p.X;
+    const int qp = p.X - 1 - i % p.X;
+    it.h = g % p.H;
+    it.s = g / p.H;
+    it.qs = __ldg(p.query_start + it.s);
+    it.qlen = __ldg(p.query_start + it.s + 1) - it.qs;
+    it.q0 = qp * 2 * kQ;
+    if (it.q0 >= it.qlen) return false;
+    it.base_pos = __ldg(p.context_lens + it.s) - it.qlen;
+    it.kv0 = it.base_pos + min(it.q0 + kQ, it.qlen);
+    it.kv1 = it.q0 + kQ < it.qlen ? it.base_pos + min(it.q0 + 2 * kQ, it.qlen) : 0;
+    it.n0 = it.kv0 > 0 ? (it.kv0 + kN4 - 1) / kN4 : 0;
+    it.n1 = it.kv1 > 0 ? (it.kv1 + kN4 - 1) / kN4 : 0;
+    it.kv_len = max(it.kv0, it.kv1);
+    it.n = max(it.n0, it.n1);
+    return true;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_db_kernel(const __grid_constant__ PrefillParams p) {
+    constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* sQ = smem;                                 // [2 tiles][2 halves][128][64]
+    unsigned char* sK = smem + 4 * kHalf;                     // [4 stages][2 halves][64][64]
+    unsigned char* sV = sK + kStages4 * 2 * kHalf4;           // [4 stages][2 halves][64][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kStages4 * 2 * kHalf4);
+    uint64_t* q_full = bars;                     // 1
+    uint64_t* q_empty = bars + 1;                // 1
+    uint64_t* k_full = bars + 2;                 // 4
+    uint64_t* k_empty = bars + 6;                // 4
+    uint64_t* v_full = bars + 10;                // 4
+    uint64_t* v_empty = bars + 14;               // 4
+    uint64_t* s_full = bars + 18;                // [2 tiles][2 buffers]
+    uint64_t* p_full = bars + 22;                // 2
+    uint64_t* o_done = bars + 24;                // 2
+    uint64_t* o_free = bars + 26;                // 2
+    uint64_t* sched_full = bars + 28;            // 4
+    uint64_t* sched_empty = bars + 32;           // 4
+    int* sched_item = reinterpret_cast<int*>(bars + 36);  // 4
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_item + 4);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n_items = p.X * p.H * p.S;
+    pdl_wait();
+
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&sched_full[i], 1);
+            mbar_init(&sched_empty[i], 1 + 2 * kQ);
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+        }
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&p_full[i], kQ);
+            mbar_init(&o_done[i], 1);
+            mbar_init(&o_free[i], kQ);
+        }
+        fence_mbar_init();
+    }
+    for (int i = tid; i < kStages4 * 2 * kHalf4 / 16; i += kThreadsV2)
+        reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);  // see v2
+    fence_proxy_async_smem();
+    if (warp == 0) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int B = 1 << p.log2B;
+
+    if (warp == 8) {
+        // ---------------- TMA producer ----------------
+        const int br = p.box_rows;  // <= 64
+        uint32_t g = 0, nq = 0;
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t slot = k & 3;
+            if (k >= 4) mbar_wait(&sched_empty[slot], ((k - 4) >> 2) & 1);
+            int i = 0;
+            if (lane == 0) {
+                i = atomicAdd(p.work_counter, 1);
+                sched_item[slot] = i;
+                mbar_arrive(&sched_full[slot]);
+            }
+            i = __shfl_sync(0xffffffffu, i, 0);
+            if (i >= n_items) break;
+            PrefillItem it;
+            if (!prefill_item4(p, i, it)) continue;
+            const int kvh = it.h / p.G;
+            const int32_t* btrow = p.block_tables + (int64_t)it.s * p.W;
+            auto box_token = [&](int b, int nf) { return b < nf ? b * br : nf * br + (b - nf); };
+            auto lookup = [&](int j, int (&rowv)[2]) {
+                const int t0 = j * kN4, len = min(it.kv_len, t0 + kN4) - t0;
+                const int nf = len / br, nb = nf + len % br;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int b = lane + 32 * u;
+                    if (b < nb) {
+                        const int t = t0 + box_token(b, nf);
+                        const int blk = __ldg(btrow + (t >> p.log2B));
+                        rowv[u] = (blk * p.H_kv + kvh) * B + (t & (B - 1));
+                    }
+                }
+            };
+            auto issue = [&](unsigned char* dst0, const CUtensorMap* map, const CUtensorMap* map1, int j,
+                             uint64_t* bar, const int (&rowv)[2]) {
+                const int t0 = j * kN4, len = min(it.kv_len, t0 + kN4) - t0;
+                const int nf = len / br, nb = nf + len % br;
+                if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int b = lane + 32 * u;
+                    if (b < nb) {
+                        const int off = box_token(b, nf) * 128;
+                        const CUtensorMap* m = b < nf ? map : map1;
+                        tma_load_2d(dst0 + off, m, 0, rowv[u], bar);
+                        tma_load_2d(dst0 + kHalf4 + off, m, 64, rowv[u], bar);
+                    }
+                }
+                __syncwarp();
+            };
+            int rowv[2] = {0, 0};
+            if (it.n > 0) lookup(0, rowv);
+            if (nq > 0) mbar_wait(q_empty, (nq - 1) & 1);
+            if (lane == 0) {
+                mbar_arrive_expect_tx(q_full, 4u * kHalf);
+                tma_load_3d(sQ, &p.tmap_q, 0, it.h, it.qs + it.q0, q_full);
+                tma_load_3d(sQ + kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0, q_full);
+                tma_load_3d(sQ + 2 * kHalf, &p.tmap_q, 0, it.h, it.qs + it.q0 + kQ, q_full);
+                tma_load_3d(sQ + 3 * kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0 + kQ, q_full);
+            }
+            __syncwarp();
+            ++nq;
+            for (int j = 0; j < it.n; ++j, ++g) {
+                const uint32_t st = g % kStages4, ph = (g / kStages4 - 1) & 1;
+                if (g >= kStages4) mbar_wait(&k_empty[st], ph);
+                issue(sK + st * 2 * kHalf4, &p.tmap_k, &p.tmap_k1, j, &k_full[st], rowv);
+                if (g >= kStages4) mbar_wait(&v_empty[st], ph);
+                issue(sV + st * 2 * kHalf4, &p.tmap_v, &p.tmap_v1, j, &v_full[st], rowv);
+                if (j + 1 < it.n) lookup(j + 1, rowv);
+            }
+        }
+    } else if (warp == 9) {
+        // ---------------- MMA issuer ----------------
+        const uint32_t idesc_s = umma_idesc(kBF16, false, kN4), idesc_o = umma_idesc(kBF16, true, 128);
+        uint32_t gs = 0, gv = 0, nq = 0;       // K/V tiles (stage counters)
+        uint32_t np[2] = {0, 0}, nf[2] = {0, 0};
+        uint32_t ms[2] = {0, 0}, mp[2] = {0, 0};  // S_t / P_t V tiles issued per query tile (buffer = count & 1)
+        // S_t = Q_t K(gs)^T into S_t[ms[t] & 1]
+        auto issue_S = [&](int t) {
+            const uint32_t b = ms[t]++ & 1;
+            if (lane == 0) {
+                const uint32_t q = smem_u32(sQ) + t * 2 * kHalf, k = smem_u32(sK) + (gs % kStages4) * 2 * kHalf4;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t qo = (kk >> 2) * kHalf + (kk & 3) * 32, ko = (kk >> 2) * kHalf4 + (kk & 3) * 32;
+                    umma_f16(tmem + (2 * t + b) * kN4, umma_desc_sw128(q + qo, 16, 1024),
+                             umma_desc_sw128(k + ko, 16, 1024), idesc_s, kk > 0);
+                }
+                umma_commit(&s_full[2 * t + b]);
+            }
+            __syncwarp();
+        };
+        // S for the next tile of the item (both query tiles), then release its K stage
+        auto next_S = [&](const PrefillItem& it, int jn, bool last_s) {
+            mbar_wait(&k_full[gs % kStages4], (gs / kStages4) & 1);
+            tc_fence_after();
+            if (jn < it.n0) issue_S(0);
+            if (jn < it.n1) issue_S(1);
+            if (lane == 0) {
+                umma_commit(&k_empty[gs % kStages4]);
+                if (last_s) umma_commit(q_empty);  // every S of this pair issued
+            }
+            __syncwarp();
+            ++gs;
+        };
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t slot = k & 3;
+            mbar_wait(&sched_full[slot], (k >> 2) & 1);
+            const int i = *reinterpret_cast<volatile int*>(&sched_item[slot]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sched_empty[slot]);
+            if (i >= n_items) break;
+            PrefillItem it;
+            if (!prefill_item4(p, i, it)) continue;
+            mbar_wait(q_full, nq & 1);
+            ++nq;
+            if (it.n == 0 && lane == 0) umma_commit(q_empty);
+            for (int jn = 0; jn < min(it.n, 2); ++jn) next_S(it, jn, jn + 1 == it.n);
+            if (it.n0 > 0 && nf[0]++ > 0) mbar_wait(&o_free[0], (nf[0] - 2) & 1);
+            if (it.n1 > 0 && nf[1]++ > 0) mbar_wait(&o_free[1], (nf[1] - 2) & 1);
+            for (int j = 0; j < it.n; ++j) {
+                const uint32_t st = gv % kStages4;
+                mbar_wait(&v_full[st], (gv / kStages4) & 1);
+                for (int t = 0; t < 2; ++t) {
+                    if (j >= (t == 0 ? it.n0 : it.n1)) continue;
+                    mbar_wait(&p_full[t], np[t]++ & 1);
+                    tc_fence_after();
+                    const uint32_t b = mp[t]++ & 1;  // P_t of this tile sits in S_t[b]
+                    if (lane == 0) {
+                        const uint32_t v = smem_u32(sV) + st * 2 * kHalf4;
+#pragma unroll
+                        for (int kk = 0; kk < kN4 / 16; ++kk)
+                            umma_f16_ts(tmem + 256 + t * 128, tmem + (2 * t + b) * kN4 + kk * 8,
+                                        umma_desc_sw128(v + kk * 2048, kHalf4, 1024), idesc_o, (j > 0) | (kk > 0));
+                        umma_commit(&o_done[t]);
+                    }
+                    __syncwarp();
+                }
+                if (lane == 0) umma_commit(&v_empty[st]);
+                __syncwarp();
+                ++gv;
+                if (j + 2 < it.n) next_S(it, j + 2, j + 3 == it.n);  // into the buffer P(j) just left
+            }
+        }
+    } else {
+        // ---------------- softmax warp groups ----------------
+        const int t = warp >> 2;
+        const int r = tid & (kQ - 1);
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t tO = tmem + 256 + t * 128 + lane_off;
+        uint32_t ns = 0;
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t slot = k & 3;
+            mbar_wait(&sched_full[slot], (k >> 2) & 1);
+            const int i = *reinterpret_cast<volatile int*>(&sched_item[slot]);
+            mbar_arrive(&sched_empty[slot]);
+            if (i >= n_items) break;
+            PrefillItem it;
+            if (!prefill_item4(p, i, it)) continue;
+            const int nt = t == 0 ? it.n0 : it.n1;
+            const int kvt = t == 0 ? it.kv0 : it.kv1;
+            const int row = it.q0 + t * kQ + r;
+            const bool row_valid = row < it.qlen;
+            const int pos = row_valid ? it.base_pos + row : -1;
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < nt; ++j, ++ns) {
+                const uint32_t b = ns & 1;
+                const uint32_t tS = tmem + (2 * t + b) * kN4 + lane_off;
+                mbar_wait(&s_full[2 * t + b], (ns >> 1) & 1);
+                tc_fence_after();
+                float sa[32], sb[32];
+                tmem_ld32_nw(tS + 0, sa);
+                tmem_ld32_nw(tS + 32, sb);
+                tmem_ld_wait();
+                const int lim = row_valid ? min(pos + 1, kvt) - j * kN4 : 0;
+                const bool full = __all_sync(0xffffffffu, lim >= kN4);
+                float mt = -INFINITY;
+                if (full) {
+#pragma unroll
+                    for (int u = 0; u < 32; u += 2)
+                        mt = fmaxf(fmaxf(mt, fmaxf(sa[u], sa[u + 1])), fmaxf(sb[u], sb[u + 1]));
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) {
+                        if (u < lim) mt = fmaxf(mt, sa[u]);
+                        if (u + 32 < lim) mt = fmaxf(mt, sb[u]);
+                    }
+                }
+                mt *= p.scale_log2;
+                const bool bump = __any_sync(0xffffffffu, mt > m + kLazy);
+                const float mn = bump ? fmaxf(m, mt) : m;
+                const float ms = (mn == -INFINITY) ? 0.f : mn;
+                const float alpha = bump ? ex2(m - ms) : 1.f;
+                float2 rs2 = make_float2(0.f, 0.f);
+                const float2 c2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-ms, -ms);
+                auto emit = [&](const float (&x)[32], int c0) {
+                    uint32_t pk[16];
+                    if (full) {
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) {
+                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
+                            const float2 a = make_float2(ex2(e.x), ex2(e.y));
+                            rs2 = __fadd2_rn(rs2, a);
+                            pk[u / 2] = pack2<T>(a.x, a.y);
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) {
+                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
+                            float2 a = make_float2(ex2(e.x), ex2(e.y));
+                            a.x = (c0 + u < lim) ? a.x : 0.f;
+                            a.y = (c0 + u + 1 < lim) ? a.y : 0.f;
+                            rs2 = __fadd2_rn(rs2, a);
+                            pk[u / 2] = pack2<T>(a.x, a.y);
+                        }
+                    }
+                    tmem_st16(tS + c0 / 2, pk);
+                };
+                emit(sa, 0);
+                emit(sb, 32);
+                if (j > 0) {  // P V of the previous tile complete (every o_done phase waited)
+                    mbar_wait(&o_done[t], (ns - 1) & 1);
+                    tc_fence_after();
+                }
+                if (j > 0 && bump) {
+#pragma unroll
+                    for (int c0 = 0; c0 < 128; c0 += 32) {
+                        float v[32];
+                        tmem_ld32_nw(tO + c0, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) v[u] *= alpha;
+                        tmem_st32(tO + c0, v);
+                    }
+                }
+                l = l * alpha + (rs2.x + rs2.y);
+                m = mn;
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&p_full[t]);
+            }
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            T* orow = static_cast<T*>(p.out) + ((int64_t)(it.qs + row) * p.H + it.h) * 128;
+            if (nt > 0) {
+                mbar_wait(&o_done[t], (ns - 1) & 1);
+                tc_fence_after();
+            }
+#pragma unroll
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+                float v[32];
+                if (nt > 0) {
+                    tmem_ld32_nw(tO + c0, v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) v[u] = 0.f;
+                }
+                if (row_valid) {
+#pragma unroll
+                    for (int c1 = 0; c1 < 32; c1 += 8) {
+                        alignas(16) T w[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) w[u] = Elem<T>::from_f32(v[c1 + u] * inv);
+                        *reinterpret_cast<uint4*>(orow + c0 + c1) = *reinterpret_cast<const uint4*>(w);
+                    }
+                }
+            }
+            if (nt > 0) {
+                tc_fence_before();
+                mbar_arrive(&o_free[t]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+size_t prefill_db_smem_bytes() { return 1024 + 4 * (size_t)kHalf + 2 * kStages4 * 2 * (size_t)kHalf4 + 36 * 8 + 32; }
+
 // ---- v3 (default): persistent, one query tile per item, softmax split by columns ----------
 // The two softmax warp groups share the 128 rows of ONE query tile: group 0 takes key
 // columns [0,64), group 1 [64,128) of every 128-key tile (warps w and w+4 address the same
@@ -1213,7 +1583,7 @@ cudaError_t set_smem(Kern k, size_t smem) {
 // else v2, whose two query tiles share each K/V tile (measured).
 int prefill_variant(int max_query_len) {
     const char* e = getenv("PA_PREFILL");
-    if (e && e[0] >= '1' && e[0] <= '3') return e[0] - '0';
+    if (e && e[0] >= '1' && e[0] <= '4') return e[0] - '0';
     return max_query_len <= kQ + kQ / 2 ? 3 : 2;
 }
 }  // namespace
@@ -1250,6 +1620,19 @@ cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int 
         if (e != cudaSuccess) return e;
         return dtype == 1 ? launch_k(paged_prefill_ws_kernel<__half>, grid, dim3(kThreadsV2), smem, stream, q)
                           : launch_k(paged_prefill_ws_kernel<__nv_bfloat16>, grid, dim3(kThreadsV2), smem, stream, q);
+    }
+    if (variant == 4) {
+        const size_t smem = prefill_db_smem_bytes();
+        q.X = (max_query_len + 2 * kQ - 1) / (2 * kQ);
+        cudaError_t me = cudaMemsetAsync(q.work_counter, 0, sizeof(int), stream);
+        if (me != cudaSuccess) return me;
+        const long long items = (long long)q.X * q.H * q.S;
+        const dim3 grid((unsigned)std::min<long long>(items, num_sms));
+        cudaError_t e = dtype == 1 ? set_smem(paged_prefill_db_kernel<__half>, smem)
+                                   : set_smem(paged_prefill_db_kernel<__nv_bfloat16>, smem);
+        if (e != cudaSuccess) return e;
+        return dtype == 1 ? launch_k(paged_prefill_db_kernel<__half>, grid, dim3(kThreadsV2), smem, stream, q)
+                          : launch_k(paged_prefill_db_kernel<__nv_bfloat16>, grid, dim3(kThreadsV2), smem, stream, q);
     }
     const size_t smem = prefill_split_smem_bytes();
     q.X = (max_query_len + kQ - 1) / kQ;
