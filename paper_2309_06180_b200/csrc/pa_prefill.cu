@@ -29,9 +29,6 @@
 #include "pa_common.cuh"
 #include "pa_internal.h"
 
-#ifndef PA_POLY_EVERY
-#define PA_POLY_EVERY 1000  // polynomial exp2 measured slower here: off
-#endif
 
 namespace pa {
 
@@ -393,26 +390,6 @@ __global__ void __launch_bounds__(128, 1) paged_prefill_kernel(const __grid_cons
     }
 }
 
-// 2^x for a pair on the FMA pipe (FA4-style offload of MUFU.EX2): x = j + f with
-// j = round(x), f in [-1/2, 1/2]; 2^f by a degree-3 minimax polynomial (relative error
-// 7.5e-5, below the storage rounding of P: 2^-9 bf16, 2^-11 f16); 2^j added to the
-// exponent field.  x is clamped to >= -127 (2^-127 rounds to 0 in P's storage type).
-__device__ __forceinline__ float2 exp2_poly2(float2 x) {
-    constexpr float kMagic = 12582912.f;  // 1.5 * 2^23: x + kMagic rounds x to an integer
-    x.x = fmaxf(x.x, -127.f);
-    x.y = fmaxf(x.y, -127.f);
-    const float2 t = __fadd2_rn(x, make_float2(kMagic, kMagic));
-    const float2 j = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
-    const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
-    float2 q = ffma2(make_float2(0.05517334f, 0.05517334f), f, make_float2(0.24261126f, 0.24261126f));
-    q = ffma2(q, f, make_float2(0.69326067f, 0.69326067f));
-    q = ffma2(q, f, make_float2(0.99992806f, 0.99992806f));
-    // (bits(t) - bits(kMagic)) << 23 == bits(t) << 23 (mod 2^32): the low 22 bits of
-    // bits(kMagic) are zero
-    return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
-                       __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
-}
-
 // two fp32 -> packed storage pair (lo = a, hi = b), one cvt (F2FP) per pair
 template <typename T>
 __device__ __forceinline__ uint32_t pack2(float a, float b);
@@ -439,7 +416,6 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
 // differences from v1: lazy rescaling (kLazy) and l summed from the fp32 weights.
 constexpr int kWarpsV2 = 10;
 constexpr float kLazy = 8.f;  // P <= 2^8: no overflow in f16/bf16, same relative rounding
-constexpr int kPolyEvery = PA_POLY_EVERY;  // 1 in kPolyEvery exp2 pairs on the FMA pipe
 constexpr int kThreadsV2 = kWarpsV2 * 32;
 
 // Work item = (query-tile pair qp, head h, sequence s); items are dealt to persistent CTAs
@@ -762,9 +738,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
 #pragma unroll
                         for (int u = 0; u < 32; u += 2) {
                             const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);  // s*c - m
-                            const float2 a = ((u / 2) % kPolyEvery == kPolyEvery - 1)
-                                                 ? exp2_poly2(e)
-                                                 : make_float2(ex2(e.x), ex2(e.y));
+                            const float2 a = make_float2(ex2(e.x), ex2(e.y));
                             rs2 = __fadd2_rn(rs2, a);
                             pk[u / 2] = pack2<T>(a.x, a.y);
                         }
@@ -1479,9 +1453,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_split_kernel(cons
 #pragma unroll
                         for (int u = 0; u < 32; u += 2) {
                             const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
-                            const float2 a = ((u / 2) % kPolyEvery == kPolyEvery - 1)
-                                                 ? exp2_poly2(e)
-                                                 : make_float2(ex2(e.x), ex2(e.y));
+                            const float2 a = make_float2(ex2(e.x), ex2(e.y));
                             rs2 = __fadd2_rn(rs2, a);
                             pk[u / 2] = pack2<T>(a.x, a.y);
                         }
