@@ -824,6 +824,412 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     }
 }
 
+// ---- v5: v2 with FOUR softmax warp groups -- (query tile, key-column half) --------------
+// The per-tile softmax -> P V -> next S chain bounds v2; here each query
+// tile's softmax is split by key columns across two warp groups (row maxima exchanged
+// through shared memory, partial row sums added in the epilogue, as v3), halving the
+// softmax on that chain while keeping v2's two query tiles per K/V tile.  Warps 0-15
+// softmax, 16 TMA producer, 17 MMA issuer.
+constexpr int kThreadsV5 = 18 * 32;
+
+#ifdef PA_PREFILL_TRACE  // timing experiments (variant build): clock64 events of CTA 0..63
+__device__ long long g_pf_trace[64 * 256];
+#define PF_T(slot)                                                                   \
+    do {                                                                             \
+        if (blockIdx.x < 64 && (slot) < 256) g_pf_trace[blockIdx.x * 256 + (slot)] = clock64(); \
+    } while (0)
+#else
+#define PF_T(slot) \
+    do {           \
+    } while (0)
+#endif
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreadsV5, 1) paged_prefill_wide_kernel(const __grid_constant__ PrefillParams p) {
+    constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* sQ = smem;                // [2 tiles][2 halves][128][64]
+    unsigned char* sK = smem + 4 * kHalf;    // [2 stages][2 halves][128][64]
+    unsigned char* sV = sK + 4 * kHalf;      // [2 stages][2 halves][128][64]
+    float* red = reinterpret_cast<float*>(sV + 4 * kHalf);  // [2 tiles][2 parity][2 halves][128] row maxima
+    float* lsum = red + 1024;                                 // [2 tiles][2 halves][128] row sums
+    uint64_t* bars = reinterpret_cast<uint64_t*>(lsum + 512);
+    uint64_t* q_full = bars;         // 1
+    uint64_t* q_empty = bars + 1;    // 1
+    uint64_t* k_full = bars + 2;     // 2
+    uint64_t* k_empty = bars + 4;    // 2
+    uint64_t* v_full = bars + 6;     // 2
+    uint64_t* v_empty = bars + 8;    // 2
+    uint64_t* s_full = bars + 10;    // 2 (per query tile)
+    uint64_t* p_full = bars + 12;    // 2
+    uint64_t* o_done = bars + 14;    // 2
+    uint64_t* o_free = bars + 16;    // 2
+    uint64_t* sched_full = bars + 18;   // 4: work-item ring (producer -> MMA + softmax warps)
+    uint64_t* sched_empty = bars + 22;  // 4
+    int* sched_item = reinterpret_cast<int*>(bars + 26);  // 4
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_item + 4);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n_items = p.X * p.H * p.S;
+    pdl_wait();
+
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&sched_full[i], 1);
+            mbar_init(&sched_empty[i], 1 + 4 * kQ);  // MMA warp (one arrive) + 512 softmax threads
+        }
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 2 * kQ);
+            mbar_init(&o_done[i], 1);
+            mbar_init(&o_free[i], 2 * kQ);
+        }
+        fence_mbar_init();
+    }
+    // V stages start zeroed: rows past kv_len of a last tile are never loaded and must not
+    // hold NaN bit patterns (P = 0 there, but 0 * NaN = NaN in the MMA); later they hold
+    // rows of earlier tiles (finite cache data)
+    for (int i = tid; i < 4 * kHalf / 16; i += kThreadsV5)
+        reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+    if (warp == 0) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int B = 1 << p.log2B;
+
+    if (warp == 16) {
+        // ---------------- TMA producer ----------------
+        const int br = p.box_rows;
+        uint32_t g = 0;    // KV tiles loaded by this CTA (stage = g & 1)
+        uint32_t nq = 0;   // query tile pairs loaded
+        for (uint32_t k = 0;; ++k) {
+            // the producer draws the next work item and publishes it to the other warps
+            const uint32_t slot = k & 3;
+            if (k >= 4) mbar_wait(&sched_empty[slot], ((k - 4) >> 2) & 1);
+            int i = 0;
+            if (lane == 0) {
+                i = atomicAdd(p.work_counter, 1);
+                sched_item[slot] = i;
+                mbar_arrive(&sched_full[slot]);
+            }
+            i = __shfl_sync(0xffffffffu, i, 0);
+            if (i >= n_items) break;
+            PrefillItem it;
+            if (!prefill_item(p, i, it)) continue;
+            const int kvh = it.h / p.G;
+            const int32_t* btrow = p.block_tables + (int64_t)it.s * p.W;
+            // tile j = tokens [128j, min(kv_len, 128j+128)): nf boxes of br rows, then
+            // single rows (never reading past kv_len).  Box b belongs to lane b % 32: the
+            // lanes look up the block table in parallel and issue their own TMA copies.
+            auto box_token = [&](int b, int nf) { return b < nf ? b * br : nf * br + (b - nf); };
+            auto lookup = [&](int j, int (&rowv)[4]) {
+                const int t0 = j * kN, len = min(it.kv_len, t0 + kN) - t0;
+                const int nf = len / br, nb = nf + len % br;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int b = lane + 32 * u;
+                    if (b < nb) {
+                        const int t = t0 + box_token(b, nf);
+                        const int blk = __ldg(btrow + (t >> p.log2B));
+                        rowv[u] = (blk * p.H_kv + kvh) * B + (t & (B - 1));
+                    }
+                }
+            };
+            auto issue = [&](unsigned char* dst0, const CUtensorMap* map, const CUtensorMap* map1, int j,
+                             uint64_t* bar, const int (&rowv)[4]) {
+                const int t0 = j * kN, len = min(it.kv_len, t0 + kN) - t0;
+                const int nf = len / br, nb = nf + len % br;
+                if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int b = lane + 32 * u;
+                    if (b < nb) {
+                        const int off = box_token(b, nf) * 128;
+                        const CUtensorMap* m = b < nf ? map : map1;
+                        tma_load_2d(dst0 + off, m, 0, rowv[u], bar);
+                        tma_load_2d(dst0 + kHalf + off, m, 64, rowv[u], bar);
+                    }
+                }
+                __syncwarp();
+            };
+            int rowv[4] = {0, 0, 0, 0};
+            if (it.n > 0) lookup(0, rowv);
+            if (nq > 0) mbar_wait(q_empty, (nq - 1) & 1);  // last S of the previous pair done
+            if (lane == 0) {
+                mbar_arrive_expect_tx(q_full, 4u * kHalf);
+                tma_load_3d(sQ, &p.tmap_q, 0, it.h, it.qs + it.q0, q_full);
+                tma_load_3d(sQ + kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0, q_full);
+                tma_load_3d(sQ + 2 * kHalf, &p.tmap_q, 0, it.h, it.qs + it.q0 + kQ, q_full);
+                tma_load_3d(sQ + 3 * kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0 + kQ, q_full);
+            }
+            __syncwarp();
+            ++nq;
+            for (int j = 0; j < it.n; ++j, ++g) {
+                const int st = g & 1;
+                if (g >= 2) mbar_wait(&k_empty[st], ((g - 2) >> 1) & 1);
+                issue(sK + st * 2 * kHalf, &p.tmap_k, &p.tmap_k1, j, &k_full[st], rowv);
+                if (g >= 2) mbar_wait(&v_empty[st], ((g - 2) >> 1) & 1);
+                issue(sV + st * 2 * kHalf, &p.tmap_v, &p.tmap_v1, j, &v_full[st], rowv);
+                if (j + 1 < it.n) lookup(j + 1, rowv);  // in flight while the next empty-wait spins
+            }
+        }
+    } else if (warp == 17) {
+        // ---------------- MMA issuer ----------------
+        const uint32_t idesc_s = umma_idesc(kBF16, false), idesc_o = umma_idesc(kBF16, true);
+        uint32_t g = 0, nq = 0;
+        uint32_t np[2] = {0, 0};  // P tiles consumed per query tile (p_full phases)
+        uint32_t nf[2] = {0, 0};  // pairs with tiles per query tile (o_free phases)
+        auto issue_S = [&](int t, uint32_t gs) {  // S_t = Q_t K^T, K in stage gs & 1
+            if (lane == 0) {
+                const uint32_t q = smem_u32(sQ) + t * 2 * kHalf, k = smem_u32(sK) + (gs & 1) * 2 * kHalf;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+                    umma_f16(tmem + t * 128, umma_desc_sw128(q + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024),
+                             idesc_s, kk > 0);
+                }
+                umma_commit(&s_full[t]);
+            }
+            __syncwarp();
+        };
+        auto issue_PV = [&](int t, uint32_t gs, bool first) {  // O_t (+)= P_t V, P_t in tensor memory
+            if (lane == 0) {
+                const uint32_t v = smem_u32(sV) + (gs & 1) * 2 * kHalf;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                                umma_desc_sw128(v + kk * 2048, kHalf, 1024), idesc_o, (!first) | (kk > 0));
+                umma_commit(&o_done[t]);
+            }
+            __syncwarp();
+        };
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t slot = k & 3;
+            mbar_wait(&sched_full[slot], (k >> 2) & 1);
+            const int i = *reinterpret_cast<volatile int*>(&sched_item[slot]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sched_empty[slot]);
+            if (i >= n_items) break;
+            PrefillItem it;
+            if (!prefill_item(p, i, it)) continue;
+            mbar_wait(q_full, nq & 1);
+            if (it.n > 0) {
+                mbar_wait(&k_full[g & 1], (g >> 1) & 1);
+                tc_fence_after();
+                if (it.n0 > 0) issue_S(0, g);
+                if (it.n1 > 0) issue_S(1, g);
+                if (lane == 0) umma_commit(&k_empty[g & 1]);
+                if (it.n == 1 && lane == 0) umma_commit(q_empty);
+            } else if (lane == 0) {
+                umma_commit(q_empty);
+            }
+            // O_t is overwritten by this pair's first P V: the softmax warp group must have
+            // read O_t of its previous pair with tiles (o_free; a group with no tiles in a
+            // pair neither arrives nor is waited for, so it can never run two phases ahead)
+            if (it.n0 > 0 && nf[0]++ > 0) mbar_wait(&o_free[0], (nf[0] - 2) & 1);
+            if (it.n1 > 0 && nf[1]++ > 0) mbar_wait(&o_free[1], (nf[1] - 2) & 1);
+            ++nq;
+            for (int j = 0; j < it.n; ++j, ++g) {
+                const int st = g & 1;
+                mbar_wait(&v_full[st], (g >> 1) & 1);
+                if (j < it.n0) {
+                    mbar_wait(&p_full[0], np[0]++ & 1);
+                    tc_fence_after();
+                    issue_PV(0, g, j == 0);
+                }
+                const bool more = j + 1 < it.n;
+                if (more) {
+                    mbar_wait(&k_full[st ^ 1], ((g + 1) >> 1) & 1);
+                    tc_fence_after();
+                    if (j + 1 < it.n0) issue_S(0, g + 1);
+                }
+                if (j < it.n1) {
+                    mbar_wait(&p_full[1], np[1]++ & 1);
+                    tc_fence_after();
+                    issue_PV(1, g, j == 0);
+                }
+                if (lane == 0) umma_commit(&v_empty[st]);
+                if (more) {
+                    if (j + 1 < it.n1) issue_S(1, g + 1);
+                    if (lane == 0) {
+                        umma_commit(&k_empty[st ^ 1]);
+                        if (j + 2 == it.n) umma_commit(q_empty);  // every S of this pair issued
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ---------------- softmax warp groups: (query tile t, key-column half hf) ----------------
+        const int t = warp >> 3, hf = (warp >> 2) & 1;
+        const int r = tid & (kQ - 1);
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + 256 + t * 128 + hf * 64 + lane_off;
+        const int bar_id = 1 + t;  // named barrier of the 256 threads of query tile t
+        uint32_t ns = 0;
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t slot = k & 3;
+            mbar_wait(&sched_full[slot], (k >> 2) & 1);
+            const int i = *reinterpret_cast<volatile int*>(&sched_item[slot]);
+            mbar_arrive(&sched_empty[slot]);
+            if (i >= n_items) break;
+            PrefillItem it;
+            if (!prefill_item(p, i, it)) continue;
+            const int nt = t == 0 ? it.n0 : it.n1;
+            const int kvt = t == 0 ? it.kv0 : it.kv1;
+            const int row = it.q0 + t * kQ + r;
+            const bool row_valid = row < it.qlen;
+            const int pos = row_valid ? it.base_pos + row : -1;
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < nt; ++j, ++ns) {
+                mbar_wait(&s_full[t], ns & 1);
+                if (tid == 0 && k == 0 && j < 64) PF_T(2 * j);
+                if (tid == 256 && k == 0 && j < 64) PF_T(129 + 2 * j);
+                tc_fence_after();
+                float sa[32], sb[32];
+                tmem_ld32_nw(tS + hf * 64, sa);
+                tmem_ld32_nw(tS + hf * 64 + 32, sb);
+                tmem_ld_wait();
+                if (tid == 0 && k == 0 && j == 3) PF_T(200);
+                const int lim = row_valid ? min(pos + 1, kvt) - j * kN - hf * 64 : 0;
+                const bool full = __all_sync(0xffffffffu, lim >= 64);
+                float mo = -INFINITY;
+                if (full) {
+#pragma unroll
+                    for (int u = 0; u < 32; u += 2)
+                        mo = fmaxf(fmaxf(mo, fmaxf(sa[u], sa[u + 1])), fmaxf(sb[u], sb[u + 1]));
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) {
+                        if (u < lim) mo = fmaxf(mo, sa[u]);
+                        if (u + 32 < lim) mo = fmaxf(mo, sb[u]);
+                    }
+                }
+                // row maximum over both halves; after this barrier both halves have read
+                // their S columns, so P may overwrite them
+                float* rd = red + (t * 2 + (ns & 1)) * 256;
+                rd[hf * 128 + r] = mo;
+                named_bar_sync(bar_id, 2 * kQ);
+                const float mt = fmaxf(mo, rd[(hf ^ 1) * 128 + r]) * p.scale_log2;
+                if (tid == 0 && k == 0 && j == 3) PF_T(201);
+                const bool bump = __any_sync(0xffffffffu, mt > m + kLazy);  // same decision in both halves
+                const float mn = bump ? fmaxf(m, mt) : m;
+                const float ms = (mn == -INFINITY) ? 0.f : mn;
+                const float alpha = bump ? ex2(m - ms) : 1.f;
+                float2 rs2 = make_float2(0.f, 0.f);
+                const float2 c2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-ms, -ms);
+                auto emit = [&](const float (&x)[32], int c0) {
+                    uint32_t pk[16];
+                    if (full) {
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) {
+                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
+                            const float2 a = make_float2(ex2(e.x), ex2(e.y));
+                            rs2 = __fadd2_rn(rs2, a);
+                            pk[u / 2] = pack2<T>(a.x, a.y);
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) {
+                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
+                            float2 a = make_float2(ex2(e.x), ex2(e.y));
+                            a.x = (c0 + u < lim) ? a.x : 0.f;
+                            a.y = (c0 + u + 1 < lim) ? a.y : 0.f;
+                            rs2 = __fadd2_rn(rs2, a);
+                            pk[u / 2] = pack2<T>(a.x, a.y);
+                        }
+                    }
+                    tmem_st16(tS + hf * 32 + c0 / 2, pk);  // P columns of this half
+                };
+                emit(sa, 0);
+                emit(sb, 32);
+                if (tid == 0 && k == 0 && j == 3) PF_T(202);
+                if (j > 0) {  // P V of the previous tile complete (returns at once; never skipped)
+                    mbar_wait(&o_done[t], (ns - 1) & 1);
+                    tc_fence_after();
+                }
+                if (j > 0 && bump) {  // this half's 64 O columns *= alpha
+#pragma unroll
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
+                        float v[32];
+                        tmem_ld32_nw(tO + c0, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) v[u] *= alpha;
+                        tmem_st32(tO + c0, v);
+                    }
+                }
+                if (tid == 0 && k == 0 && j == 3) PF_T(203);
+                l = l * alpha + (rs2.x + rs2.y);
+                m = mn;
+                tmem_st_wait();
+                tc_fence_before();
+                if (tid == 0 && k == 0 && j < 64) PF_T(2 * j + 1);
+                if (tid == 256 && k == 0 && j < 64) PF_T(128 + 2 * j);
+                mbar_arrive(&p_full[t]);
+            }
+            // epilogue: total row sum of both halves, then this half's 64 output columns
+            float* ls = lsum + t * 256;
+            ls[hf * 128 + r] = l;
+            named_bar_sync(bar_id, 2 * kQ);
+            const float lt = l + ls[(hf ^ 1) * 128 + r];
+            named_bar_sync(bar_id, 2 * kQ);  // ls may be rewritten by the next item
+            const float inv = lt > 0.f ? 1.f / lt : 0.f;
+            T* orow = static_cast<T*>(p.out) + ((int64_t)(it.qs + row) * p.H + it.h) * 128 + hf * 64;
+            if (nt > 0) {
+                mbar_wait(&o_done[t], (ns - 1) & 1);
+                tc_fence_after();
+            }
+#pragma unroll
+            for (int c0 = 0; c0 < 64; c0 += 32) {
+                float v[32];
+                if (nt > 0) {
+                    tmem_ld32_nw(tO + c0, v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) v[u] = 0.f;
+                }
+                if (row_valid) {
+#pragma unroll
+                    for (int c1 = 0; c1 < 32; c1 += 8) {
+                        alignas(16) T w[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) w[u] = Elem<T>::from_f32(v[c1 + u] * inv);
+                        *reinterpret_cast<uint4*>(orow + c0 + c1) = *reinterpret_cast<const uint4*>(w);
+                    }
+                }
+            }
+            if (nt > 0) {
+                tc_fence_before();
+                mbar_arrive(&o_free[t]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+size_t prefill_wide_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 1536 * 4 + 26 * 8 + 4 * 4 + 16; }
+
 // ---- v4: as v2 with 64-token K/V tiles and two S buffers per query tile ------------------
 // Tensor memory: S_t[b] (64 columns each, t = query tile, b = tile parity) in columns
 // [0,256), O_0 / O_1 in [256,512).  P_t(j) aliases S_t[j&1], so S_t(j+1) goes to the other
@@ -1555,7 +1961,7 @@ cudaError_t set_smem(Kern k, size_t smem) {
 // else v2, whose two query tiles share each K/V tile (measured).
 int prefill_variant(int max_query_len) {
     const char* e = getenv("PA_PREFILL");
-    if (e && e[0] >= '1' && e[0] <= '4') return e[0] - '0';
+    if (e && e[0] >= '1' && e[0] <= '5') return e[0] - '0';
     return max_query_len <= kQ + kQ / 2 ? 3 : 2;
 }
 }  // namespace
@@ -1593,6 +1999,19 @@ cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int 
         return dtype == 1 ? launch_k(paged_prefill_ws_kernel<__half>, grid, dim3(kThreadsV2), smem, stream, q)
                           : launch_k(paged_prefill_ws_kernel<__nv_bfloat16>, grid, dim3(kThreadsV2), smem, stream, q);
     }
+    if (variant == 5) {
+        const size_t smem = prefill_wide_smem_bytes();
+        q.X = (max_query_len + 2 * kQ - 1) / (2 * kQ);
+        cudaError_t me = cudaMemsetAsync(q.work_counter, 0, sizeof(int), stream);
+        if (me != cudaSuccess) return me;
+        const long long items = (long long)q.X * q.H * q.S;
+        const dim3 grid((unsigned)std::min<long long>(items, num_sms));
+        cudaError_t e = dtype == 1 ? set_smem(paged_prefill_wide_kernel<__half>, smem)
+                                   : set_smem(paged_prefill_wide_kernel<__nv_bfloat16>, smem);
+        if (e != cudaSuccess) return e;
+        return dtype == 1 ? launch_k(paged_prefill_wide_kernel<__half>, grid, dim3(kThreadsV5), smem, stream, q)
+                          : launch_k(paged_prefill_wide_kernel<__nv_bfloat16>, grid, dim3(kThreadsV5), smem, stream, q);
+    }
     if (variant == 4) {
         const size_t smem = prefill_db_smem_bytes();
         q.X = (max_query_len + 2 * kQ - 1) / (2 * kQ);
@@ -1618,3 +2037,9 @@ cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int 
 }
 
 }  // namespace pa
+
+#ifdef PA_PREFILL_TRACE
+extern "C" int pa_debug_prefill_trace_read(long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, pa::g_pf_trace, sizeof(long long) * (size_t)n);
+}
+#endif

@@ -106,7 +106,7 @@ def test_block_size_and_placement_invariance_bitwise():
         assert torch.equal(o, outs[0])
 
 
-@pytest.mark.parametrize("variant", ["2", "3", "4"])
+@pytest.mark.parametrize("variant", ["2", "3", "4", "5"])
 def test_chunked_prompt_equals_whole_prompt_bitwise(variant, monkeypatch):
     """Prefilling a prompt in chunks (each chunk attends to the cached earlier chunks)
     gives the rows of the whole-prompt prefill bit for bit: with a given kernel, a row's
@@ -179,7 +179,7 @@ def test_kernel_variants_agree(dtype, monkeypatch):
     q, kc, vc, bt, cl, qs = prefill_problem(ctx, qlen, 16, 8, 2, dtype, seed=91)
     r = ref(q, kc, vc, bt, cl, qs, 0.09, 16, 2, dtype)
     outs = []
-    for v in ("1", "2", "3", "4"):
+    for v in ("1", "2", "3", "4", "5"):
         monkeypatch.setenv("PA_PREFILL", v)
         outs.append(run(q, kc, vc, bt, cl, qs, 0.09))
         assert max_abs(outs[-1], r) <= TOL[dtype], f"variant {v}"
