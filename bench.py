@@ -405,7 +405,10 @@ def run_e2e(a, wl, world, dev, x, kc, vc, mcl, ws, stream):
     out = torch.empty(pin["query"].shape, dtype=pin["query"].dtype).pin_memory()
     st = torch.empty(pa.decode_step_staging_size(wl.S, wl.H, wl.H_kv, wl.D, wl.W, len(wl.block_mapping),
                                                  pin["query"].dtype), dtype=torch.uint8, device=dev)
-    h2d = sum(t.numel() * t.element_size() for t in list(pin.values()) + list(host.values()))
+    # bytes pa_decode_step copies: q, k, v, block tables, context lengths, CoW pairs (the
+    # slot mapping is implied by the tables and not sent)
+    h2d = sum(t.numel() * t.element_size() for t in list(pin.values()) + [host["bt"], host["cl"]]) + \
+        (host["bm"].numel() * host["bm"].element_size() if len(wl.block_mapping) else 0)
     d2h = out.numel() * out.element_size()
     steps = max(10, min(a.steps, 200))
 

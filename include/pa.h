@@ -282,6 +282,12 @@ pa_status_t pa_swap_blocks_memcpy(void* const* dst_key_caches, void* const* dst_
  * key_cache/value_cache/workspace/staging: DEVICE.  staging must hold
  * pa_decode_step_staging_size() bytes.  The call returns after enqueueing; the
  * caller synchronises the stream before reading host_out.
+ * Pipelining: the batch is processed in C chunks of sequences (default 4,
+ * PA_E2E_CHUNKS): chunk c's kernel overlaps the H2D of chunk c+1 and the D2H of chunk
+ * c-1 on two internal copy streams of the library (one set per device); every step
+ * still orders after the previous work of `stream` and joins back into `stream`, so
+ * the synchronisation rule above is unchanged.  Results equal the unchunked step bit
+ * for bit (sequences are independent).  Enqueueing is serialised per device.
  * ---------------------------------------------------------------------------------- */
 size_t pa_decode_step_staging_size(int num_seqs, int num_heads, int num_kv_heads, int head_dim,
                                    int max_blocks_per_seq, int num_pairs, pa_dtype_t dtype);
