@@ -421,8 +421,10 @@ def run_e2e(a, wl, world, dev, x, kc, vc, mcl, ws, stream):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    h0 = time.perf_counter()
     for _ in range(steps):
         one()
+    host_us = (time.perf_counter() - h0) / steps * 1e6  # CPU time to enqueue one step
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
@@ -433,7 +435,11 @@ def run_e2e(a, wl, world, dev, x, kc, vc, mcl, ws, stream):
         ms = float(t[0])
     kv_all = wl.logical_kv_bytes() * world
     return {"value": kv_all / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms, "steps": steps,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "pa_decode_step (C ABI, pinned host buffers)"}
+            "host_enqueue_us_per_step": round(host_us, 1),
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "pa_decode_step (C ABI, pinned host buffers)",
+            "transfer": ("zero-copy: kernel reads q/k/v and writes out over the host link; tables copied"
+                         if os.environ.get("PA_E2E_MODE") == "zerocopy" else
+                         "copy-engine chunks (PA_E2E_CHUNKS, default 4) overlapped with the chunk kernels")}
 
 
 def cpu_baseline(wl, target_s: float = 10.0):

@@ -282,10 +282,17 @@ pa_status_t pa_swap_blocks_memcpy(void* const* dst_key_caches, void* const* dst_
  * key_cache/value_cache/workspace/staging: DEVICE.  staging must hold
  * pa_decode_step_staging_size() bytes.  The call returns after enqueueing; the
  * caller synchronises the stream before reading host_out.
- * Pipelining: the batch is processed in C chunks of sequences (default 4,
- * PA_E2E_CHUNKS): chunk c's kernel overlaps the H2D of chunk c+1 and the D2H of chunk
- * c-1 on two internal copy streams of the library (one set per device); every step
- * still orders after the previous work of `stream` and joins back into `stream`, so
+ * Transfer modes.  Default: the batch is processed in C chunks of sequences (default 4,
+ * PA_E2E_CHUNKS; at most 16): chunk c's kernel overlaps the H2D of chunk c+1 and the
+ * D2H of chunk c-1 on two internal copy streams, and consecutive chunk kernels run on
+ * two internal compute streams (each with half of `workspace`, which must then hold
+ * 2 x the workspace of ceil(S/C) sequences, else one stream is used; PA_E2E_STREAMS=1
+ * forces one) so one chunk's CTAs fill the SMs while the previous chunk's tail drains.
+ * PA_E2E_MODE=zerocopy (ablation, measured slower): only block_tables, context_lens and
+ * block_mapping are copied; the kernel reads q / new k / new v straight from pinned,
+ * device-mapped host memory and stores out straight into host_out (PA_ERR_INVALID_ARG
+ * if a buffer is not mapped).  In every mode (internal streams: one set per device)
+ * every step still orders after the previous work of `stream` and joins back into `stream`, so
  * the synchronisation rule above is unchanged.  Results equal the unchunked step bit
  * for bit (sequences are independent).  Enqueueing is serialised per device.
  * ---------------------------------------------------------------------------------- */

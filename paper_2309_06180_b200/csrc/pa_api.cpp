@@ -681,10 +681,10 @@ namespace {
 // device, shared by the calls of all host threads on that device -- calls on different
 // user streams are serialised through the copy streams, never interleaved unsafely).
 struct E2EStreams {
-    static constexpr int kMaxChunks = 8;
+    static constexpr int kMaxChunks = 16;
     std::mutex mu;  // one enqueueing call at a time per device (the events are shared)
-    cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t start = nullptr, bm = nullptr, d2h_done = nullptr;
+    cudaStream_t h2d = nullptr, d2h = nullptr, comp[2] = {};
+    cudaEvent_t start = nullptr, bm = nullptr, ready = nullptr, d2h_done = nullptr;
     cudaEvent_t h2d_done[kMaxChunks] = {}, kern_done[kMaxChunks] = {};
 };
 E2EStreams* e2e_streams() {
@@ -699,7 +699,10 @@ E2EStreams* e2e_streams() {
         const unsigned f = cudaEventDisableTiming;
         if (cudaStreamCreateWithFlags(&e.h2d, cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamCreateWithFlags(&e.d2h, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&e.comp[0], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&e.comp[1], cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&e.start, f) != cudaSuccess || cudaEventCreateWithFlags(&e.bm, f) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e.ready, f) != cudaSuccess ||
             cudaEventCreateWithFlags(&e.d2h_done, f) != cudaSuccess)
             return nullptr;
         for (int i = 0; i < E2EStreams::kMaxChunks; ++i)
@@ -748,18 +751,74 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     // runs, so a step costs about one chunk's copies plus the kernels instead of all copies
     // plus the kernels.  Everything joins back into `stream` before the call returns, so
     // synchronising `stream` still covers the whole step.  PA_E2E_CHUNKS overrides C.
-    E2EStreams* es = e2e_streams();
-    if (es == nullptr) return fail(PA_ERR_CUDA, "pa_decode_step: could not create its copy streams");
-    std::lock_guard<std::mutex> lock(es->mu);
-    int C = 4;  // measured on c2_sharegpt: 1 -> 3181, 2 -> 3583, 3 -> 4161, 4 -> 4174-4706, 6 -> 4521, 8 -> 4423 GB/s
-    if (const char* ev = getenv("PA_E2E_CHUNKS")) C = atoi(ev) > 0 ? atoi(ev) : C;
-    C = std::max(1, std::min({C, num_seqs > 0 ? num_seqs : 1, E2EStreams::kMaxChunks}));
     cudaError_t err;
 #define E2E_CHECK(call)                                                   \
     do {                                                                  \
         err = (call);                                                     \
         if (err != cudaSuccess) return cuda_fail(err, "pa_decode_step"); \
     } while (0)
+    // Zero-copy mode (PA_E2E_MODE=zerocopy; ablation): only the small tables
+    // (block_tables, context_lens, CoW pairs) are copied into `staging`; the attention
+    // kernel reads each sequence's q / new k / new v rows straight from pinned host memory
+    // over the host link and stores its output rows into host_out.  Measured slower than
+    // the copy-engine chunks on c2_sharegpt (669 vs 473 us per step: the CTAs stall on
+    // host-link read latency), so the default is the chunked path below.
+    const char* mode = getenv("PA_E2E_MODE");
+    const bool zero_copy = mode != nullptr && std::strcmp(mode, "zerocopy") == 0;
+    void* dq = nullptr;
+    void* dk = nullptr;
+    void* dv = nullptr;
+    void* dout = nullptr;
+    auto mapped = [](const void* h, void** d) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+            cudaGetLastError();  // clear: pageable memory is not an error here
+            return false;
+        }
+        *d = a.devicePointer;
+        return a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
+    };
+    if (zero_copy && num_seqs > 0 && mapped(host_query, &dq) && mapped(host_key, &dk) &&
+        mapped(host_value, &dv) && mapped(host_out, &dout)) {
+        const size_t btb = (size_t)num_seqs * max_blocks_per_seq * 4;
+        E2E_CHECK(cudaMemcpyAsync(st + L.bt, host_block_tables, btb, cudaMemcpyHostToDevice, s));
+        E2E_CHECK(cudaMemcpyAsync(st + L.ctx, host_context_lens, (size_t)num_seqs * 4, cudaMemcpyHostToDevice, s));
+        if (num_pairs > 0) {
+            E2E_CHECK(cudaMemcpyAsync(st + L.bm, host_block_mapping, (size_t)num_pairs * 16, cudaMemcpyHostToDevice,
+                                      s));
+            void* kcs[1] = {key_cache};
+            void* vcs[1] = {value_cache};
+            pa_status_t r = pa_copy_blocks(kcs, vcs, 1, reinterpret_cast<const int64_t*>(st + L.bm), num_pairs,
+                                           num_kv_heads, block_size, head_dim, dtype, stream);
+            if (r != PA_OK) return r;
+        }
+        return pa_paged_attention_decode(dout, dq, dk, dv, key_cache, value_cache,
+                                         reinterpret_cast<const int32_t*>(st + L.bt),
+                                         reinterpret_cast<const int32_t*>(st + L.ctx), scale, block_size,
+                                         num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq,
+                                         max_context_len, dtype, workspace, workspace_bytes, stream);
+    }
+    if (zero_copy && num_seqs > 0)
+        return fail(PA_ERR_INVALID_ARG, "PA_E2E_MODE=zerocopy needs pinned, device-mapped host buffers");
+    E2EStreams* es = e2e_streams();
+    if (es == nullptr) return fail(PA_ERR_CUDA, "pa_decode_step: could not create its copy streams");
+    std::lock_guard<std::mutex> lock(es->mu);
+    int C = 4;
+    if (const char* ev = getenv("PA_E2E_CHUNKS")) C = atoi(ev) > 0 ? atoi(ev) : C;
+    C = std::max(1, std::min({C, num_seqs > 0 ? num_seqs : 1, E2EStreams::kMaxChunks}));
+    // Chunk kernels alternate between two internal compute streams so that chunk c+1's
+    // CTAs fill the SMs while chunk c's longest CTAs drain (a kernel's tail is its longest
+    // partition, ~26 us on c2_sharegpt); each stream then needs its own workspace, carved
+    // from the caller's (sized for the whole batch).  One stream if it does not fit or
+    // PA_E2E_STREAMS=1.
+    const int n_max = (num_seqs + C - 1) / C;
+    const int PT = PA_DEFAULT_PARTITION_TOKENS;
+    const int cap = max_blocks_per_seq * block_size;
+    const int mctx = max_context_len > 0 ? std::min(max_context_len, cap) : cap;
+    const size_t ws_chunk = (workspace_bytes_for(n_max, num_heads, head_dim, mctx, PT) + 255) & ~(size_t)255;
+    int NS = 2;
+    if (const char* ev = getenv("PA_E2E_STREAMS")) NS = atoi(ev) == 1 ? 1 : 2;
+    if (C == 1 || workspace == nullptr || 2 * ws_chunk > workspace_bytes) NS = 1;
     // the staging buffer may still be read by this stream's previous step
     E2E_CHECK(cudaEventRecord(es->start, s));
     E2E_CHECK(cudaStreamWaitEvent(es->h2d, es->start, 0));
@@ -773,6 +832,11 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
         pa_status_t r = pa_copy_blocks(kcs, vcs, 1, reinterpret_cast<const int64_t*>(st + L.bm), num_pairs,
                                        num_kv_heads, block_size, head_dim, dtype, stream);
         if (r != PA_OK) return r;
+    }
+    if (NS == 2) {  // the compute streams start after everything before (copy_blocks included)
+        E2E_CHECK(cudaEventRecord(es->ready, s));
+        E2E_CHECK(cudaStreamWaitEvent(es->comp[0], es->ready, 0));
+        E2E_CHECK(cudaStreamWaitEvent(es->comp[1], es->ready, 0));
     }
     const size_t qrow = (size_t)num_heads * head_dim * e, kvrow = (size_t)num_kv_heads * head_dim * e;
     const size_t btrow = (size_t)max_blocks_per_seq * 4;
@@ -793,18 +857,22 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     }
     for (int c = 0; c < C; ++c) {
         const size_t s0 = lo(c), n = lo(c + 1) - lo(c);
-        E2E_CHECK(cudaStreamWaitEvent(s, es->h2d_done[c], 0));
+        cudaStream_t cs = NS == 2 ? es->comp[c & 1] : s;
+        void* ws = NS == 2 ? static_cast<char*>(workspace) + (c & 1) * ws_chunk : workspace;
+        const size_t wsb = NS == 2 ? ws_chunk : workspace_bytes;
+        E2E_CHECK(cudaStreamWaitEvent(cs, es->h2d_done[c], 0));
         pa_status_t r = pa_paged_attention_decode(
             st + L.out + s0 * qrow, st + L.q + s0 * qrow, st + L.k + s0 * kvrow, st + L.v + s0 * kvrow, key_cache,
             value_cache, reinterpret_cast<const int32_t*>(st + L.bt + s0 * btrow),
             reinterpret_cast<const int32_t*>(st + L.ctx) + s0, scale, block_size, num_kv_heads, (int)n, num_heads,
-            head_dim, max_blocks_per_seq, max_context_len, dtype, workspace, workspace_bytes, stream);
+            head_dim, max_blocks_per_seq, max_context_len, dtype, ws, wsb, (pa_stream_t)cs);
         if (r != PA_OK) return r;
-        E2E_CHECK(cudaEventRecord(es->kern_done[c], s));
+        E2E_CHECK(cudaEventRecord(es->kern_done[c], cs));
         E2E_CHECK(cudaStreamWaitEvent(es->d2h, es->kern_done[c], 0));
         E2E_CHECK(cudaMemcpyAsync(static_cast<char*>(host_out) + s0 * qrow, st + L.out + s0 * qrow, n * qrow,
                                   cudaMemcpyDeviceToHost, es->d2h));
     }
+    // every chunk's D2H waited on its kernel, so this joins all internal streams into s
     E2E_CHECK(cudaEventRecord(es->d2h_done, es->d2h));
     E2E_CHECK(cudaStreamWaitEvent(s, es->d2h_done, 0));
 #undef E2E_CHECK

@@ -257,8 +257,18 @@ def test_validate_tables():
     assert pa.validate_tables(tb["block_tables"], cl, wl.B, wl.num_blocks) == -6
 
 
-def test_decode_step_host_api_matches_device_api():
-    wl = make_config("c3_fork", S=24, H=2, H_kv=2)
+@pytest.mark.parametrize("name", ["c3_fork", "c4_long"])
+@pytest.mark.parametrize("mode", ["chunks4", "chunks4_1stream", "chunks1", "chunks7", "zerocopy"])
+def test_decode_step_host_api_matches_device_api(mode, name, monkeypatch):
+    """pa_decode_step from pinned host buffers, in every transfer mode (copy-engine
+    chunks on one or two compute streams, or zero-copy reads of q/k/v and writes of out
+    by the kernel), equals the device API bit for bit (outputs and caches)."""
+    if mode == "zerocopy":
+        monkeypatch.setenv("PA_E2E_MODE", "zerocopy")
+    else:
+        monkeypatch.setenv("PA_E2E_CHUNKS", mode[6])
+        monkeypatch.setenv("PA_E2E_STREAMS", "1" if mode.endswith("1stream") else "2")
+    wl = make_config(name, **SMALL[name])
     x = materialize_torch(wl, "cuda")
     ref, rk, rv, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()})
     kc, vc = x["key_cache"].clone(), x["value_cache"].clone()
