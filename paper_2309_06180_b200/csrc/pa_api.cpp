@@ -181,6 +181,8 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     if (sched_env && std::strcmp(sched_env, "persistent") == 0) sched = 1;
     if (sched_env && std::strcmp(sched_env, "pcoop") == 0) sched = 3;
     if (sched_env && std::strcmp(sched_env, "lcoop") == 0) sched = 5;
+    bool natural = false;  // pcoop over items in grid order (no work-list launch)
+    if (sched_env && std::strcmp(sched_env, "ncoop") == 0) sched = 3, natural = true;
     REQUIRE(group_size >= 1, "group_size must be >= 1");
     const int gm = std::min(group_size, 8);
     if (gm > 1) sched = 4;  // sharing-aware: groups of gm consecutive sequences
@@ -254,6 +256,7 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     p.GM = gm;
     p.S = num_seqs;
     p.listed = sched == 5;
+    p.natural = natural ? 1 : 0;
     if (const char* ev = getenv("PA_HPW")) p.HPW = atoi(ev) > 0 ? atoi(ev) : 1;
     if (tp != nullptr) {
         p.n_out_peers = tp->n;

@@ -779,6 +779,24 @@ __global__ void __launch_bounds__(256) paged_attention_kernel(const AttnParams p
 // their head, and release the stage with one arrive per warp on empty[k]; the producer
 // waits on empty[k] before refilling it.  The CTA's warps therefore stay in lockstep on
 // the same blocks (contiguous DRAM reads), and no consumer ever issues a copy.
+#ifdef PA_DECODE_TRACE  // timing experiments (variant build): per-CTA globaltimer events
+__device__ unsigned long long g_dec_trace[(1 << 17) * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define DEC_T(slot, v)                                                                              \
+    do {                                                                                          \
+        const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);      \
+        if (cta < (1u << 17)) g_dec_trace[cta * 4 + (slot)] = (v);                                  \
+    } while (0)
+#else
+#define DEC_T(slot, v) \
+    do {               \
+    } while (0)
+#endif
+
 template <typename T, int D>
 __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnParams p) {
     using C = AttnCfg<T, D>;
@@ -790,8 +808,15 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
     const int NKVmax = HPC % G == 0 ? HPC / G : (HPC + G - 1) / G + 1;  // stage layout stride (host-sized)
     const int slab = kTile * RB;                   // one kv head x 16 rows
     const int stage_bytes = 2 * NKVmax * slab;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STG * stage_bytes);
+    uint64_t* empty = full + STG;
+    int* sbt = reinterpret_cast<int*>(empty + STG);
     pdl_wait();
+#ifdef PA_DECODE_TRACE
+    if (threadIdx.x == 0) DEC_T(0, gtimer());
+#endif
     int hg, s, ctx, c0;
+    int bt_pref = 0;  // producer lane i: block id jb0 + i, loaded while ctx is in flight
     if (p.listed) {  // CTA = one entry of the longest-first work list x head group
         const int NG = (p.H + HPC - 1) / HPC;
         const int idx = blockIdx.x;
@@ -804,11 +829,31 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
     } else {
         hg = blockIdx.y;
         s = blockIdx.z;
-        ctx = p.context_lens[s];
         // this CTA walks the arithmetic partitions [c0, c0 + PPC) of the context back to
         // back; each is finished exactly as if it had its own CTA (bitwise identical)
         c0 = blockIdx.x * p.PPC;
+        // the partition's first 32 block ids depend only on (s, c0): the producer loads
+        // them (in-row entries past the context are read, never used) in parallel with
+        // context_lens[s] instead of after it -- one dependent global round trip less
+        const int jb = (c0 * PT) >> p.log2B;
+        if (warp == HPC && jb + lane < p.W) bt_pref = __ldg(p.block_tables + (int64_t)s * p.W + jb + lane);
+        ctx = p.context_lens[s];
     }
+    // consumer warps' query rows, also in flight across the barrier below
+    uint4 q0 = make_uint4(0u, 0u, 0u, 0u), q1 = q0;
+    if (warp < HPC && hg * HPC + warp < p.H) {
+        const uint4* qrow = reinterpret_cast<const uint4*>(static_cast<const char*>(p.query) +
+                                                           ((int64_t)s * p.H + hg * HPC + warp) * RB);
+        q0 = __ldg(qrow + lane % LT);
+        q1 = __ldg(qrow + lane % LT + LT);
+    }
+    if (threadIdx.x < STG) {
+        mbar_init(&full[threadIdx.x], 1);
+        mbar_init(&empty[threadIdx.x], min(HPC, p.H - hg * HPC));
+    }
+    fence_mbar_init();
+    __syncthreads();
+    pdl_launch_dependents();  // the next kernel may become resident during our last wave
     const int h0 = hg * HPC;
     const int nh = min(HPC, p.H - h0);          // consumer warps with a head
     const int kvh0 = h0 / G;
@@ -821,22 +866,14 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
     const int t_new = (p.new_key != nullptr && ctx > 0 && p1 == ctx) ? ctx - 1 : -1;
     const int pc = t_new >= 0 ? t_new : p1;
 
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STG * stage_bytes);
-    uint64_t* empty = full + STG;
-    int* sbt = reinterpret_cast<int*>(empty + STG);
-    const int jb0 = p0 >> p.log2B;
-    const int nb = p1 > p0 ? ((p1 - 1) >> p.log2B) - jb0 + 1 : 0;
-    const int32_t* btrow = p.block_tables + (int64_t)s * p.W;
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) sbt[i] = __ldg(btrow + jb0 + i);
-    if (threadIdx.x < STG) {
-        mbar_init(&full[threadIdx.x], 1);
-        mbar_init(&empty[threadIdx.x], nh);
-    }
-    fence_mbar_init();
-    __syncthreads();
-    pdl_launch_dependents();  // the next kernel may become resident during our last wave
-
     if (warp == HPC) {  // ------------------------------------------------ producer warp
+        // the partition's block ids into shared memory (producer-only: no CTA barrier)
+        const int jb0 = p0 >> p.log2B;
+        const int nb = p1 > p0 ? ((p1 - 1) >> p.log2B) - jb0 + 1 : 0;
+        const int32_t* btrow = p.block_tables + (int64_t)s * p.W;
+        if (lane < nb) sbt[lane] = p.listed ? __ldg(btrow + jb0 + lane) : bt_pref;
+        for (int i = 32 + lane; i < nb; i += 32) sbt[i] = __ldg(btrow + jb0 + i);
+        __syncwarp();
         const int B = 1 << p.log2B;
         const char* kc = static_cast<const char*>(p.key_cache);
         const char* vc = static_cast<const char*>(p.value_cache);
@@ -911,8 +948,6 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
                         smem + (((size_t)STG * stage_bytes + 16 * STG + 4 * (size_t)(p.PPC * PT / (1 << p.log2B) + 2) +
                                  15) & ~(size_t)15) + (size_t)HPC * p.PPC * D * 4) +
                     (size_t)warp * p.PPC;
-    const uint4* qrow = reinterpret_cast<const uint4*>(static_cast<const char*>(p.query) + sh * RB);
-    const uint4 q0 = __ldg(qrow + c), q1 = __ldg(qrow + c + LT);
     float m = -INFINITY, l = 0.f;
     float2 acc[EPC];
 #pragma unroll
@@ -925,6 +960,9 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
     const int j_new = (t_new >= 0 && h % G == 0) ? (t_new - p0) / kTile : -1;
     for (int j = 0, tok0 = p0; j < ntiles; ++j, tok0 += kTile) {
         mbar_wait(&full[k], fphase);
+#ifdef PA_DECODE_TRACE
+        if (j == 0 && threadIdx.x == 0) DEC_T(1, gtimer());
+#endif
         const char* sK = sKb;
         const char* sV = sK + NKVmax * slab;
         if (j == j_new && g == 0)
@@ -963,6 +1001,14 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
         __syncwarp();
         merge_partitions_from<T, D, false>(p, sh, my_ml, my_po, nparts, lane);
     }
+#ifdef PA_DECODE_TRACE
+    if (threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        DEC_T(2, gtimer());
+        DEC_T(3, (unsigned long long)smid | ((unsigned long long)ntiles << 16) | ((unsigned long long)s << 32));
+    }
+#endif
 }
 
 // ======================================================= persistent coop scheduler ===
@@ -1008,7 +1054,9 @@ __global__ void __launch_bounds__(288) paged_attention_pcoop_kernel(const AttnPa
     const int NG = (H + HPC - 1) / HPC;
 
     if (warp == HPC) {  // ================================================ producer warp
-        const int total = __ldcg(p.n_items) * NG;
+        // natural order (p.natural): item g = (sequence, partition, head group) in grid
+        // order, descriptor from context_lens -- no work list, no list-building launch
+        const int total = p.natural ? p.S * p.NP * NG : __ldcg(p.n_items) * NG;
         const int B = 1 << p.log2B;
         const char* kc = static_cast<const char*>(p.key_cache);
         const char* vc = static_cast<const char*>(p.value_cache);
@@ -1028,14 +1076,36 @@ __global__ void __launch_bounds__(288) paged_attention_pcoop_kernel(const AttnPa
         // of the next item are fetched (right after cur's first tile is queued) and
         // the claim of the one after is in flight.  sbt is double-buffered.
         const int tbl = PT / B + 2;
-        auto fetch = [&](int g, int buf, int4& d) {  // descriptor + block ids of item g
-            d = __ldcg(&p.items[g / NG]);
+        auto fetch1 = [&](int g, int buf, int4& d) {  // descriptor + block ids of item g
+            int pre = 0;
+            if (p.natural) {  // the first 32 block ids load in parallel with context_lens[s]
+                const int ii = g / NG, sq = ii / p.NP, part = ii - sq * p.NP;
+                const int jb = (part * PT) >> p.log2B;
+                if (jb + lane < p.W) pre = __ldg(p.block_tables + (int64_t)sq * p.W + jb + lane);
+                d = make_int4(sq, part, __ldg(p.context_lens + sq), 0);
+            } else {
+                d = __ldcg(&p.items[g / NG]);
+                const int jb = (d.y * PT) >> p.log2B;
+                if (jb + lane < p.W) pre = __ldg(p.block_tables + (int64_t)d.x * p.W + jb + lane);
+            }
             const int p0 = d.y * PT, p1 = min(d.z, p0 + PT);
             const int jb0 = p0 >> p.log2B;
             const int nb = p1 > p0 ? ((p1 - 1) >> p.log2B) - jb0 + 1 : 0;
             const int32_t* btrow = p.block_tables + (int64_t)d.x * p.W;
-            for (int i = lane; i < nb; i += 32) sbt[buf * tbl + i] = __ldg(btrow + jb0 + i);
+            if (lane < nb) sbt[buf * tbl + lane] = pre;
+            for (int i = 32 + lane; i < nb; i += 32) sbt[buf * tbl + i] = __ldg(btrow + jb0 + i);
             __syncwarp();
+        };
+        // natural order: partitions past a context are not items; claim on until one is
+        auto fetch = [&](int& g, int buf, int4& d) {
+            fetch1(g, buf, d);
+            while (p.natural && d.y > 0 && d.y * PT >= d.z) {
+                int gg = 0;
+                if (lane == 0) gg = atom_add_global(p.work_counter, 1);
+                g = __shfl_sync(0xffffffffu, gg, 0);
+                if (g >= total) return;
+                fetch1(g, buf, d);
+            }
         };
         int gi = 0, gn = 0, buf = 0;
         if (lane == 0) gi = atom_add_global(p.work_counter, 1);
@@ -1105,7 +1175,7 @@ __global__ void __launch_bounds__(288) paged_attention_pcoop_kernel(const AttnPa
                 advance();
                 if (j == 0) {  // the first tile is queued: fetch the next item meanwhile
                     gnext = __shfl_sync(0xffffffffu, gn, 0);
-                    if (gnext < total) fetch(gnext, buf ^ 1, itn);
+                    if (gnext < total) fetch(gnext, buf ^ 1, itn);  // may claim on (natural order)
                     if (lane == 0) gn = atom_add_global(p.work_counter, 1);
                 }
             }
@@ -1480,7 +1550,14 @@ static cudaError_t launch_attention_t(const AttnParams& p, int num_seqs, int sch
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t items = (int64_t)num_seqs * p.NP * ((p.H + p.HPC - 1) / p.HPC);
         const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)cached_blocks * sms, items));
-        cudaError_t e = launch_k(build_worklist_kernel, dim3(1), dim3(1024), 0, stream, p, num_seqs);
+        cudaError_t e;
+        if (p.natural) {  // no work list: zero the claim counter (and the split counters)
+            e = cudaMemsetAsync(p.work_counter, 0, sizeof(int), stream);
+            if (e == cudaSuccess && p.NP > 1)
+                e = cudaMemsetAsync(p.counters, 0, sizeof(int) * (size_t)num_seqs * p.H, stream);
+        } else {
+            e = launch_k(build_worklist_kernel, dim3(1), dim3(1024), 0, stream, p, num_seqs);
+        }
         if (e != cudaSuccess) return e;
         return launch_k(kern, dim3((unsigned)grid), dim3(threads), smem, stream, p);
     }
@@ -1588,3 +1665,9 @@ cudaError_t launch_debug_gather(const GatherParams& p, int dtype, int head_dim, 
 }
 
 }  // namespace pa
+
+#ifdef PA_DECODE_TRACE
+extern "C" int pa_debug_decode_trace_read(unsigned long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, pa::g_dec_trace, sizeof(unsigned long long) * (size_t)n);
+}
+#endif

@@ -60,6 +60,7 @@ struct AttnParams {
     int GM;                     // sharing-aware scheduler: sequences per group
     int S;                      // number of sequences
     int listed;                 // coop: CTAs take (sequence, partition) from the work list
+    int natural;                // pcoop: items in grid order from context_lens (no work list)
     int STG;                    // tiles in flight per warp (shared-memory stages)
     // fused tensor-parallel all-gather (N2): when n_out_peers > 0 every output row of local
     // head h is stored to out_peers[k] + ((s * out_H) + out_h0 + h) * D for every rank k

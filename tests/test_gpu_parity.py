@@ -395,15 +395,15 @@ def test_fused_decode_gqa():
     assert max_abs(out, ref) <= TOL[wl.dtype]
 
 
-@pytest.mark.parametrize("name", ["c2_sharegpt", "c3_fork", "c4_long"])
+@pytest.mark.parametrize("name", ["c1_tiny", "c2_alpaca", "c2_sharegpt", "c3_fork", "c4_long"])
 def test_schedulers_bitwise_identical(name, monkeypatch):
-    """coop (default), grid, persistent, pcoop and lcoop run the same per-(sequence, head) tile
+    """coop (default), grid, persistent, pcoop, ncoop and lcoop run the same per-(sequence, head) tile
     arithmetic in the same order, so their outputs and cache writes are bit-identical;
     a stage-reuse race in any pipeline would break this (full-size c2/c4, repeated)."""
     wl = make_config(name)
     x = materialize_torch(wl, "cuda")
     ref = None
-    for sched in ("coop", "grid", "persistent", "pcoop", "lcoop", "coop"):
+    for sched in ("coop", "grid", "persistent", "pcoop", "ncoop", "lcoop", "coop"):
         monkeypatch.setenv("PA_SCHED", sched)
         out, kc, vc, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()}, fused=True)
         if ref is None:
