@@ -439,7 +439,9 @@ def run_e2e(a, wl, world, dev, x, kc, vc, mcl, ws, stream):
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "pa_decode_step (C ABI, pinned host buffers)",
             "transfer": ("zero-copy: kernel reads q/k/v and writes out over the host link; tables copied"
                          if os.environ.get("PA_E2E_MODE") == "zerocopy" else
-                         "copy-engine chunks (PA_E2E_CHUNKS, default 4) overlapped with the chunk kernels")}
+                         "copy-engine chunks (PA_E2E_CHUNKS, default 4) overlapped with the chunk kernels" +
+                         ("; the step is captured once into a CUDA graph and replayed"
+                          if os.environ.get("PA_E2E_GRAPH") == "1" else ""))}
 
 
 def cpu_baseline(wl, target_s: float = 10.0):

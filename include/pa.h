@@ -288,6 +288,11 @@ pa_status_t pa_swap_blocks_memcpy(void* const* dst_key_caches, void* const* dst_
  * two internal compute streams (each with half of `workspace`, which must then hold
  * 2 x the workspace of ceil(S/C) sequences, else one stream is used; PA_E2E_STREAMS=1
  * forces one) so one chunk's CTAs fill the SMs while the previous chunk's tail drains.
+ * PA_E2E_SPLIT="w0,w1,..." sets relative chunk sizes (first to last) instead of equal
+ * ones.  PA_E2E_GRAPH=1 captures the enqueued step once into a CUDA graph (internal
+ * capture stream; cache of 8 per device, keyed on every pointer, size and tuning
+ * variable of the call) and replays it with one launch on `stream`; host buffer
+ * CONTENTS are read when the graph runs, so they may change between calls.
  * PA_E2E_MODE=zerocopy (ablation, measured slower): only block_tables, context_lens and
  * block_mapping are copied; the kernel reads q / new k / new v straight from pinned,
  * device-mapped host memory and stores out straight into host_out (PA_ERR_INVALID_ARG

@@ -685,8 +685,18 @@ namespace {
 // user streams are serialised through the copy streams, never interleaved unsafely).
 struct E2EStreams {
     static constexpr int kMaxChunks = 16;
+    static constexpr int kMaxGraphs = 8;
     std::mutex mu;  // one enqueueing call at a time per device (the events are shared)
-    cudaStream_t h2d = nullptr, d2h = nullptr, comp[2] = {};
+    cudaStream_t h2d = nullptr, d2h = nullptr, comp[2] = {}, cap = nullptr;
+    // captured steps (CUDA graphs), keyed on every pointer, size and setting of the call;
+    // replayed with one cudaGraphLaunch (the host-side cost of ~50 enqueues otherwise)
+    struct Graph {
+        std::string key;
+        cudaGraphExec_t exec = nullptr;
+        uint64_t used = 0;
+    };
+    Graph graphs[kMaxGraphs];
+    uint64_t tick = 0;
     cudaEvent_t start = nullptr, bm = nullptr, ready = nullptr, d2h_done = nullptr;
     cudaEvent_t h2d_done[kMaxChunks] = {}, kern_done[kMaxChunks] = {};
 };
@@ -704,6 +714,7 @@ E2EStreams* e2e_streams() {
             cudaStreamCreateWithFlags(&e.d2h, cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamCreateWithFlags(&e.comp[0], cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamCreateWithFlags(&e.comp[1], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&e.cap, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&e.start, f) != cudaSuccess || cudaEventCreateWithFlags(&e.bm, f) != cudaSuccess ||
             cudaEventCreateWithFlags(&e.ready, f) != cudaSuccess ||
             cudaEventCreateWithFlags(&e.d2h_done, f) != cudaSuccess)
@@ -808,13 +819,34 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     std::lock_guard<std::mutex> lock(es->mu);
     int C = 4;
     if (const char* ev = getenv("PA_E2E_CHUNKS")) C = atoi(ev) > 0 ? atoi(ev) : C;
+    // chunk weights (PA_E2E_SPLIT="1,2,4,1": relative sizes, first to last); equal if unset
+    int wts[E2EStreams::kMaxChunks];
+    int nw_ = 0;
+    if (const char* ev = getenv("PA_E2E_SPLIT")) {
+        for (const char* q = ev; *q && nw_ < E2EStreams::kMaxChunks;) {
+            const int w = atoi(q);
+            if (w <= 0) break;
+            wts[nw_++] = w;
+            while (*q && *q != ',') ++q;
+            if (*q == ',') ++q;
+        }
+        if (nw_ > 0) C = nw_;
+    }
     C = std::max(1, std::min({C, num_seqs > 0 ? num_seqs : 1, E2EStreams::kMaxChunks}));
+    if (nw_ != C) {
+        nw_ = C;
+        for (int i = 0; i < C; ++i) wts[i] = 1;
+    }
+    int64_t wsum = 0, wcum[E2EStreams::kMaxChunks + 1] = {0};
+    for (int i = 0; i < C; ++i) wcum[i + 1] = (wsum += wts[i]);
     // Chunk kernels alternate between two internal compute streams so that chunk c+1's
     // CTAs fill the SMs while chunk c's longest CTAs drain (a kernel's tail is its longest
     // partition, ~26 us on c2_sharegpt); each stream then needs its own workspace, carved
     // from the caller's (sized for the whole batch).  One stream if it does not fit or
     // PA_E2E_STREAMS=1.
-    const int n_max = (num_seqs + C - 1) / C;
+    auto lo = [&](int c) { return (int)((int64_t)num_seqs * wcum[c] / wsum); };
+    int n_max = 1;
+    for (int c = 0; c < C; ++c) n_max = std::max(n_max, lo(c + 1) - lo(c));
     const int PT = PA_DEFAULT_PARTITION_TOKENS;
     const int cap = max_blocks_per_seq * block_size;
     const int mctx = max_context_len > 0 ? std::min(max_context_len, cap) : cap;
@@ -822,6 +854,12 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     int NS = 2;
     if (const char* ev = getenv("PA_E2E_STREAMS")) NS = atoi(ev) == 1 ? 1 : 2;
     if (C == 1 || workspace == nullptr || 2 * ws_chunk > workspace_bytes) NS = 1;
+    // Everything below is enqueued by `enqueue(origin)`: on the caller's stream (default),
+    // or (PA_E2E_GRAPH=1) once on an internal capture stream into a CUDA graph that later
+    // calls with the same pointers and sizes replay on the caller's stream.  Measured: no
+    // gain on c2_sharegpt (the step is bound by the host link, not by ~50 enqueues;
+    // DESIGN §8), so eager is the default and the graph path an option.
+    auto enqueue = [&](cudaStream_t s) -> pa_status_t {
     // the staging buffer may still be read by this stream's previous step
     E2E_CHECK(cudaEventRecord(es->start, s));
     E2E_CHECK(cudaStreamWaitEvent(es->h2d, es->start, 0));
@@ -833,7 +871,7 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
         void* kcs[1] = {key_cache};
         void* vcs[1] = {value_cache};
         pa_status_t r = pa_copy_blocks(kcs, vcs, 1, reinterpret_cast<const int64_t*>(st + L.bm), num_pairs,
-                                       num_kv_heads, block_size, head_dim, dtype, stream);
+                                       num_kv_heads, block_size, head_dim, dtype, (pa_stream_t)s);
         if (r != PA_OK) return r;
     }
     if (NS == 2) {  // the compute streams start after everything before (copy_blocks included)
@@ -843,7 +881,6 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     }
     const size_t qrow = (size_t)num_heads * head_dim * e, kvrow = (size_t)num_kv_heads * head_dim * e;
     const size_t btrow = (size_t)max_blocks_per_seq * 4;
-    auto lo = [&](int c) { return (int)((int64_t)num_seqs * c / C); };
     for (int c = 0; c < C; ++c) {
         const size_t s0 = lo(c), n = lo(c + 1) - lo(c);
         E2E_CHECK(cudaMemcpyAsync(st + L.q + s0 * qrow, static_cast<const char*>(host_query) + s0 * qrow, n * qrow,
@@ -860,6 +897,7 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     }
     for (int c = 0; c < C; ++c) {
         const size_t s0 = lo(c), n = lo(c + 1) - lo(c);
+        if (n == 0) continue;  // a weight too small for this batch
         cudaStream_t cs = NS == 2 ? es->comp[c & 1] : s;
         void* ws = NS == 2 ? static_cast<char*>(workspace) + (c & 1) * ws_chunk : workspace;
         const size_t wsb = NS == 2 ? ws_chunk : workspace_bytes;
@@ -878,6 +916,69 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     // every chunk's D2H waited on its kernel, so this joins all internal streams into s
     E2E_CHECK(cudaEventRecord(es->d2h_done, es->d2h));
     E2E_CHECK(cudaStreamWaitEvent(s, es->d2h_done, 0));
+    return PA_OK;
+    };
+
+    const char* gev = getenv("PA_E2E_GRAPH");
+    if (gev == nullptr || std::strcmp(gev, "1") != 0) return enqueue(s);
+    // key: every argument that shapes the enqueued work (host buffer CONTENTS are read
+    // when the graph runs, so they may change between calls) + the tuning environment
+    std::string key;
+    {
+        char buf[640];
+        uint32_t sc;
+        std::memcpy(&sc, &scale, 4);
+        std::snprintf(buf, sizeof(buf),
+                      "%p %p %p %p %p %p %p %d %p %p %08x %d %d %d %d %d %d %d %d %p %zu %p %zu %d %d",
+                      host_out, host_query, host_key, host_value, (const void*)host_block_tables,
+                      (const void*)host_context_lens, (const void*)host_block_mapping, num_pairs, key_cache,
+                      value_cache, sc, block_size, num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq,
+                      max_context_len, (int)dtype, staging, staging_bytes, workspace, workspace_bytes, C, NS);
+        key = buf;
+        for (const char* name : {"PA_E2E_SPLIT", "PA_SCHED", "PA_HPC", "PA_STG", "PA_PPC", "PA_HPW", "PA_PDL"}) {
+            const char* v = getenv(name);
+            key += ' ';
+            key += v ? v : "-";
+        }
+    }
+    E2EStreams::Graph* hit = nullptr;
+    for (auto& g : es->graphs)
+        if (g.exec != nullptr && g.key == key) hit = &g;
+    if (hit == nullptr) {
+        E2EStreams::Graph* slot = &es->graphs[0];
+        for (auto& g : es->graphs)
+            if (g.exec == nullptr || g.used < slot->used) slot = &g;
+        if (slot->exec != nullptr) {
+            cudaGraphExecDestroy(slot->exec);
+            slot->exec = nullptr;
+        }
+        cudaGraph_t graph = nullptr;
+        err = cudaStreamBeginCapture(es->cap, cudaStreamCaptureModeThreadLocal);
+        if (err != cudaSuccess) {
+            cudaGetLastError();
+            return enqueue(s);  // capture unavailable: eager
+        }
+        const pa_status_t r = enqueue(es->cap);
+        const cudaError_t ec = cudaStreamEndCapture(es->cap, &graph);
+        if (r != PA_OK || ec != cudaSuccess || graph == nullptr) {
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            if (r != PA_OK && r != PA_ERR_CUDA) return r;  // an argument error, as the eager call would
+            return enqueue(s);  // not capturable (e.g. pageable host memory): eager
+        }
+        cudaGraphExec_t exec = nullptr;
+        err = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (err != cudaSuccess) {
+            cudaGetLastError();
+            return enqueue(s);
+        }
+        slot->key = key;
+        slot->exec = exec;
+        hit = slot;
+    }
+    hit->used = ++es->tick;
+    E2E_CHECK(cudaGraphLaunch(hit->exec, s));
 #undef E2E_CHECK
     return PA_OK;
 }

@@ -258,13 +258,19 @@ def test_validate_tables():
 
 
 @pytest.mark.parametrize("name", ["c3_fork", "c4_long"])
-@pytest.mark.parametrize("mode", ["chunks4", "chunks4_1stream", "chunks1", "chunks7", "zerocopy"])
+@pytest.mark.parametrize("mode", ["chunks4", "chunks4_1stream", "chunks1", "chunks7", "zerocopy", "split1241",
+                                  "chunks4_graph"])
 def test_decode_step_host_api_matches_device_api(mode, name, monkeypatch):
     """pa_decode_step from pinned host buffers, in every transfer mode (copy-engine
-    chunks on one or two compute streams, or zero-copy reads of q/k/v and writes of out
-    by the kernel), equals the device API bit for bit (outputs and caches)."""
+    chunks on one or two compute streams, weighted chunks, captured-graph replay or eager
+    enqueue, or zero-copy reads of q/k/v and writes of out by the kernel), equals the
+    device API bit for bit (outputs and caches)."""
     if mode == "zerocopy":
         monkeypatch.setenv("PA_E2E_MODE", "zerocopy")
+    elif mode == "split1241":
+        monkeypatch.setenv("PA_E2E_SPLIT", "1,2,4,1")
+    elif mode == "chunks4_graph":
+        monkeypatch.setenv("PA_E2E_GRAPH", "1")
     else:
         monkeypatch.setenv("PA_E2E_CHUNKS", mode[6])
         monkeypatch.setenv("PA_E2E_STREAMS", "1" if mode.endswith("1stream") else "2")
@@ -285,6 +291,58 @@ def test_decode_step_host_api_matches_device_api(mode, name, monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(out, ref.cpu())
     assert np.array_equal(bits(kc), bits(rk)) and np.array_equal(bits(vc), bits(rv))
+
+
+@pytest.mark.parametrize("name", ["c3_fork", "c2_sharegpt"])
+def test_decode_step_graph_replay_reads_current_host_data(name, monkeypatch):
+    """pa_decode_step (PA_E2E_GRAPH=1) captures a step into a CUDA graph keyed on its
+    pointers and sizes and replays it: a replay must read the host buffers' CURRENT
+    contents (new queries under the same pointers) and equal the device API on them, bit
+    for bit; and a call with a different batch size (another key) must not replay the
+    old graph."""
+    monkeypatch.setenv("PA_E2E_GRAPH", "1")
+    wl = make_config(name, **SMALL[name])
+    x = materialize_torch(wl, "cuda")
+    kc, vc = x["key_cache"].clone(), x["value_cache"].clone()
+    pin = {k: x[k].cpu().pin_memory() for k in ("query", "key", "value")}
+    host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in
+            dict(slot=wl.slot_mapping, bt=wl.block_tables, cl=wl.context_lens, bm=wl.block_mapping).items()}
+    out = torch.empty(pin["query"].shape, dtype=pin["query"].dtype).pin_memory()
+    st = torch.empty(pa.decode_step_staging_size(wl.S, wl.H, wl.H_kv, wl.D, wl.W, len(wl.block_mapping),
+                                                 pin["query"].dtype), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(pa.paged_attention_workspace_size(wl.S, wl.H, wl.D, wl.max_context_len), 16),
+                     dtype=torch.uint8, device="cuda")
+
+    def call():
+        pa.decode_step(out, pin["query"], pin["key"], pin["value"], host["slot"], host["bt"], host["cl"],
+                       host["bm"], kc, vc, wl.scale, st, ws, max_context_len=wl.max_context_len)
+        torch.cuda.synchronize()
+        return out.clone()
+
+    first = call()
+    ref1, _, _, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()})
+    assert torch.equal(first, ref1.cpu())
+    # same pointers, new contents: the queries reversed across sequences
+    pin["query"].copy_(pin["query"].flip(0))
+    x2 = {k: v.clone() for k, v in x.items()}
+    x2["query"] = x["query"].flip(0).contiguous()
+    ref2, rk, rv, _ = gpu_step(wl, inputs=x2)
+    second = call()
+    assert torch.equal(second, ref2.cpu())
+    assert not torch.equal(second, first)
+    assert np.array_equal(bits(kc), bits(rk)) and np.array_equal(bits(vc), bits(rv))
+    monkeypatch.setenv("PA_E2E_GRAPH", "0")
+    assert torch.equal(call(), second)
+    monkeypatch.setenv("PA_E2E_GRAPH", "1")
+    # a smaller batch under the same buffers is a different key: outputs of its rows only
+    S2 = wl.S // 2
+    out.zero_()
+    pa.decode_step(out[:S2], pin["query"][:S2], pin["key"][:S2], pin["value"][:S2], host["slot"][:S2],
+                   host["bt"][:S2], host["cl"][:S2], host["bm"][:0], kc, vc, wl.scale, st, ws,
+                   max_context_len=wl.max_context_len)
+    torch.cuda.synchronize()
+    assert torch.equal(out[:S2], second[:S2])
+    assert not out[S2:].any()
 
 
 def test_cow_parent_unchanged():
