@@ -183,6 +183,9 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     if (sched_env && std::strcmp(sched_env, "lcoop") == 0) sched = 5;
     bool natural = false;  // pcoop over items in grid order (no work-list launch)
     if (sched_env && std::strcmp(sched_env, "ncoop") == 0) sched = 3, natural = true;
+    // (pcoop as the default for unsplit batches measured c2_alpaca 70.7 -> 69.2 us but
+    // c3_fork 98.5 -> 104.2 and c1_tiny 19.5 -> 21.7 us: the list-building launch sits on
+    // the critical path; DESIGN §7.  coop stays the default everywhere.)
     REQUIRE(group_size >= 1, "group_size must be >= 1");
     const int gm = std::min(group_size, 8);
     if (gm > 1) sched = 4;  // sharing-aware: groups of gm consecutive sequences
