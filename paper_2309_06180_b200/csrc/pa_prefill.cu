@@ -414,6 +414,18 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
 // double-buffered separately; the MMA order PV_0(j), S_0(j+1), PV_1(j), S_1(j+1) keeps the
 // tensor cores on one query tile while the other tile's softmax runs on the SM.  Softmax
 // differences from v1: lazy rescaling (kLazy) and l summed from the fp32 weights.
+#ifdef PA_PREFILL_TRACE  // timing experiments (variant build): clock64 events of CTA 0..63
+__device__ long long g_pf_trace[64 * 256];
+#define PF_T(slot)                                                                   \
+    do {                                                                             \
+        if (blockIdx.x < 64 && (slot) < 256) g_pf_trace[blockIdx.x * 256 + (slot)] = clock64(); \
+    } while (0)
+#else
+#define PF_T(slot) \
+    do {           \
+    } while (0)
+#endif
+
 constexpr int kWarpsV2 = 10;
 constexpr float kLazy = 8.f;  // P <= 2^8: no overflow in f16/bf16, same relative rounding
 constexpr int kThreadsV2 = kWarpsV2 * 32;
@@ -474,6 +486,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     uint64_t* sched_empty = bars + 22;  // 4
     int* sched_item = reinterpret_cast<int*>(bars + 26);  // 4
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_item + 4);
+#ifdef PA_PREFILL_MUTEX
+    int* mufu_owner = reinterpret_cast<int*>(tmem_slot + 1);  // softmax group in its exp phase, -1: none
+    if (threadIdx.x == 0) *mufu_owner = -1;
+#endif
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int n_items = p.X * p.H * p.S;
@@ -583,8 +599,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
                 const int st = g & 1;
                 if (g >= 2) mbar_wait(&k_empty[st], ((g - 2) >> 1) & 1);
                 issue(sK + st * 2 * kHalf, &p.tmap_k, &p.tmap_k1, j, &k_full[st], rowv);
+                if (lane == 0 && k == 0 && j < 16) PF_T(192 + 4 * j);
                 if (g >= 2) mbar_wait(&v_empty[st], ((g - 2) >> 1) & 1);
                 issue(sV + st * 2 * kHalf, &p.tmap_v, &p.tmap_v1, j, &v_full[st], rowv);
+                if (lane == 0 && k == 0 && j < 16) PF_T(192 + 4 * j + 1);
                 if (j + 1 < it.n) lookup(j + 1, rowv);  // in flight while the next empty-wait spins
             }
         }
@@ -647,6 +665,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
             for (int j = 0; j < it.n; ++j, ++g) {
                 const int st = g & 1;
                 mbar_wait(&v_full[st], (g >> 1) & 1);
+                if (lane == 0 && k == 0 && j < 16) PF_T(128 + 4 * j);
                 if (j < it.n0) {
                     mbar_wait(&p_full[0], np[0]++ & 1);
                     tc_fence_after();
@@ -654,12 +673,15 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
                 }
                 const bool more = j + 1 < it.n;
                 if (more) {
+                    if (lane == 0 && k == 0 && j < 16) PF_T(128 + 4 * j + 1);
                     mbar_wait(&k_full[st ^ 1], ((g + 1) >> 1) & 1);
+                    if (lane == 0 && k == 0 && j < 16) PF_T(128 + 4 * j + 2);
                     tc_fence_after();
                     if (j + 1 < it.n0) issue_S(0, g + 1);
                 }
                 if (j < it.n1) {
                     mbar_wait(&p_full[1], np[1]++ & 1);
+                    if (lane == 0 && k == 0 && j < 16) PF_T(128 + 4 * j + 3);
                     tc_fence_after();
                     issue_PV(1, g, j == 0);
                 }
@@ -698,12 +720,14 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
             for (int j = 0; j < nt; ++j, ++ns) {
                 mbar_wait(&s_full[t], ns & 1);
                 tc_fence_after();
+                if ((tid & 127) == 0 && k == 0 && j < 16) PF_T(t * 64 + 4 * j);
                 float sa[32], sb[32], sc[32], sd[32];
                 tmem_ld32_nw(tS + 0, sa);
                 tmem_ld32_nw(tS + 32, sb);
                 tmem_ld32_nw(tS + 64, sc);
                 tmem_ld32_nw(tS + 96, sd);
                 tmem_ld_wait();
+                if ((tid & 127) == 0 && k == 0 && j < 16) PF_T(t * 64 + 4 * j + 1);
                 const int lim = row_valid ? min(pos + 1, kvt) - j * kN : 0;
                 // scale > 0: max(s) * c == max(s * c) exactly (rounding is monotonic)
                 const bool full = __all_sync(0xffffffffu, lim >= kN);  // no masking in this tile
@@ -755,10 +779,23 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
                     }
                     tmem_st16(tS + c0 / 2, pk);
                 };
+#ifdef PA_PREFILL_MUTEX
+                // one softmax group at a time in the MUFU-bound exp phase: the two groups
+                // share every SM sub-partition's MUFU; alternating keeps each phase short
+                if ((tid & 127) == 0)
+                    while (atomicCAS(mufu_owner, -1, t) != -1) {
+                    }
+                asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");
+#endif
                 emit(sa, 0);
                 emit(sb, 32);
                 emit(sc, 64);
                 emit(sd, 96);
+#ifdef PA_PREFILL_MUTEX
+                asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");
+                if ((tid & 127) == 0) atomicExch(mufu_owner, -1);
+#endif
+                if ((tid & 127) == 0 && k == 0 && j < 16) PF_T(t * 64 + 4 * j + 2);
                 // P_t is out; now O_t *= alpha.  PV_t of the previous tile has completed (this
                 // S_t was issued after it), so this wait returns at once; it is not skipped
                 // so that every o_done phase is waited on
@@ -782,6 +819,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(&p_full[t]);
+                if ((tid & 127) == 0 && k == 0 && j < 16) PF_T(t * 64 + 4 * j + 3);
             }
             // epilogue: out row = O_t / l
             const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -832,17 +870,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
 // softmax, 16 TMA producer, 17 MMA issuer.
 constexpr int kThreadsV5 = 18 * 32;
 
-#ifdef PA_PREFILL_TRACE  // timing experiments (variant build): clock64 events of CTA 0..63
-__device__ long long g_pf_trace[64 * 256];
-#define PF_T(slot)                                                                   \
-    do {                                                                             \
-        if (blockIdx.x < 64 && (slot) < 256) g_pf_trace[blockIdx.x * 256 + (slot)] = clock64(); \
-    } while (0)
-#else
-#define PF_T(slot) \
-    do {           \
-    } while (0)
-#endif
+
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
