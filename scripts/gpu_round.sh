@@ -7,4 +7,5 @@ timeout 600 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_$
 STEPS=500 bash scripts/bench_all.sh > gpurun_out/bench_all_${TAG}.jsonl
 bash scripts/gpu_profile.sh c2_sharegpt $TAG
 bash scripts/gpu_profile.sh c2_alpaca $TAG
+bash scripts/gpu_profile.sh c5_beam $TAG
 NCU_CFG="p_2k p_prefix5" TAG=$TAG bash scripts/gpu_prefill_bench.sh
