@@ -307,7 +307,7 @@ def run_ours(a, wl_full, world, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms_step, "us_per_step": ms_step * 1e3, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "strong",
+        "scaling": "strong",  # heads of a fixed batch sharded over the ranks
         "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic (seeded; shapes of BASELINE.json configs)",
         "config": {"workload": wl_full.name, "seqs": wl_full.S, "heads": wl_full.H, "kv_heads": wl_full.H_kv,
                    "head_dim": wl_full.D, "block_size": wl_full.B, "kv_dtype": wl_full.dtype,
