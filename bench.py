@@ -116,6 +116,9 @@ def parse():
     ap.add_argument("--block-size", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="separate reshape_and_cache launch (ablation)")
+    ap.add_argument("--grouped", type=int, default=0,
+                    help="sharing-aware decode on the tensor cores over groups of this many sequences "
+                         "(SURVEY 8(f) N1; 0 = off, 'auto' sizes: C3 6, C5 4 via --grouped -1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-prefill", action="store_true", help="skip the N4 prompt-phase context line")
     ap.add_argument("--extra", action="store_true", help="also print per-config lines for the other configs")
@@ -224,6 +227,9 @@ def run_ours(a, wl_full, world, rank, local):
                     raise
                 tp_gather = f"nccl (fused setup failed: {type(exc).__name__}: {exc})"
     has_pairs = len(wl.block_mapping) > 0
+    grouped = a.grouped if a.grouped >= 0 else {"c3_parallel": 6, "c3_fork": 6, "c5_beam": 4}.get(wl_full.name, 0)
+    if grouped and (ftp is not None or a.unfused):
+        raise SystemExit("--grouped runs the single-GPU fused decode step only")
     stream = torch.cuda.current_stream(dev)
     ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
@@ -240,6 +246,9 @@ def run_ours(a, wl_full, world, rank, local):
         elif a.unfused:
             pa.paged_attention(out, q, kc, vc, bt, cl, wl.scale, max_context_len=mcl,
                                partition_tokens=a.partition_tokens, workspace=ws)
+        elif grouped:  # N1: groups of sequences sharing blocks, QK^T / PV on the tensor cores
+            pa.paged_attention_decode_grouped(out, q, kn, vn, kc, vc, bt, cl, wl.scale, grouped, max_context_len=mcl,
+                                              workspace=ws)
         else:  # the decode step's cache write fused into the attention kernel
             pa.paged_attention_decode(out, q, kn, vn, kc, vc, bt, cl, wl.scale, max_context_len=mcl, workspace=ws)
         if i is not None:
@@ -303,7 +312,7 @@ def run_ours(a, wl_full, world, rank, local):
     attn_bytes_u = attn_bytes - sb["kv_logical"] + kv_unique
     achieved_u = attn_bytes_u / (attn_ms * 1e-3) / 1e9
     value = kv_all / (ms_step * 1e-3) / 1e9
-    traffic = load_traffic(wl_full.name, world)
+    traffic = load_traffic(wl_full.name + ("_grouped" if grouped else ""), world)
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms_step, "us_per_step": ms_step * 1e3, "higher_is_better": True,
@@ -314,14 +323,17 @@ def run_ours(a, wl_full, world, rank, local):
                    "mean_ctx": float(wl_full.context_lens.mean()), "max_ctx": int(wl_full.max_context_len),
                    "cow_pairs": int(len(wl_full.block_mapping)), "parallelism": f"tp{world}",
                    "tp_gather": tp_gather,
+                   "decode_kernel": f"grouped{grouped} (N1, tensor cores)" if grouped else "coop",
                    "partition_tokens": a.partition_tokens or pa.DEFAULT_PARTITION_TOKENS,
                    "l2": "inputs larger than L2 (KV %.2f GB vs 126 MB L2); no flush" % (kv_all / 1e9)},
         "tokens_per_s": wl_full.S / (ms_step * 1e-3),
         "kv_tokens_per_s": float(wl_full.context_lens.sum()) / (ms_step * 1e-3),
         "frac_of_peak": value / peak,
-        "roofline": {"bound": "hbm", "kernel": "paged_attention_kernel (pa_paged_attention_decode: cache write + "
-                                                "attention + split-context merge in one launch)"
-                     if not a.unfused else "paged_attention_kernel (pa_paged_attention)",
+        "roofline": {"bound": "hbm", "kernel": (f"paged_attention_group_mma_kernel (pa_paged_attention_decode_grouped, "
+                                                 f"groups of {grouped}: shared blocks loaded once, QK^T and PV as "
+                                                 f"tensor-core MMAs; cache write fused)") if grouped else
+                     "paged_attention_kernel (pa_paged_attention_decode: cache write + attention + split-context "
+                     "merge in one launch)" if not a.unfused else "paged_attention_kernel (pa_paged_attention)",
                      "achieved": achieved_u if shared else achieved, "peak": peak, "peak_source": peak_src,
                      "unit": "GB/s", "frac": (achieved_u if shared else achieved) / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": attn_bytes_u if shared else attn_bytes,

@@ -132,6 +132,30 @@ pa_status_t pa_paged_attention_decode_shared(void* out, const void* query, const
                                              pa_stream_t stream);
 
 /* ------------------------------------------------------------------------------------
+ * pa_paged_attention_decode_grouped -- the sharing-aware decode step
+ * on the tensor cores.  Same grouping and arguments as pa_paged_attention_decode_shared
+ * plus num_blocks (NB, rows of the caches, for the TMA tensor maps).  One CTA per
+ * (partition, query head, group): every distinct physical block the group reads at a
+ * logical 16-token tile is TMA-loaded once, and Q K^T and P V are computed for all the
+ * group's members at once with m16n8k16 tensor-core MMAs (rows = members), each row
+ * masked to its own block and context (Eq.4; sharing P:295-332).  The new
+ * token's K/V is read from key/value and written to its cache slot as in
+ * pa_paged_attention_decode.  Results match the oracle within the stated tolerance
+ * (accumulation order differs from the CUDA-core kernels: not bit-identical to them).
+ * Supports f16/bf16, head_dim 128, power-of-two block_size >= 16, group_size in [1, 8]
+ * (PA_ERR_UNSUPPORTED otherwise); NB*H_kv*B < 2^31.  Workspace as pa_paged_attention.
+ * ---------------------------------------------------------------------------------- */
+pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, const void* key,
+                                              const void* value, void* key_cache, void* value_cache,
+                                              const int32_t* block_tables,
+                                              const int32_t* context_lens, float scale,
+                                              int block_size, int num_kv_heads, int num_blocks,
+                                              int num_seqs, int num_heads, int head_dim,
+                                              int max_blocks_per_seq, int max_context_len,
+                                              int group_size, pa_dtype_t dtype, void* workspace,
+                                              size_t workspace_bytes, pa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
  * pa_paged_prefill_attention -- multi-token causal attention over the paged cache: the
  * prompt phase, a chunk of a long prompt, or the user-specific suffix after
  * a cached shared prefix ("the prompt phase computation only needs to execute

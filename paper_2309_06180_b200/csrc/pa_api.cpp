@@ -350,6 +350,97 @@ bool encode_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* ba
 }
 }  // namespace
 
+pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, const void* key, const void* value,
+                                              void* key_cache, void* value_cache, const int32_t* block_tables,
+                                              const int32_t* context_lens, float scale, int block_size,
+                                              int num_kv_heads, int num_blocks, int num_seqs, int num_heads,
+                                              int head_dim, int max_blocks_per_seq, int max_context_len,
+                                              int group_size, pa_dtype_t dtype, void* workspace,
+                                              size_t workspace_bytes, pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
+    if (dtype == PA_F32) return fail(PA_ERR_UNSUPPORTED, "grouped decode supports f16 and bf16 only");
+    if (head_dim != 128) return fail(PA_ERR_UNSUPPORTED, "grouped decode supports head_dim 128 only (got %d)", head_dim);
+    const int log2B = log2_pow2(block_size);
+    if (log2B < 4) return fail(PA_ERR_UNSUPPORTED, "grouped decode needs a power-of-two block_size >= 16 (got %d)",
+                               block_size);
+    REQUIRE(group_size >= 1 && group_size <= 8, "group_size must be in [1, 8] (got %d)", group_size);
+    REQUIRE(num_seqs >= 0 && num_seqs <= 65535 * 8, "num_seqs out of range (got %d)", num_seqs);
+    REQUIRE(num_heads > 0 && num_kv_heads > 0 && num_heads <= 65535, "num_heads/num_kv_heads out of range");
+    REQUIRE(num_heads % num_kv_heads == 0, "num_heads (%d) must be a multiple of num_kv_heads (%d)", num_heads,
+            num_kv_heads);
+    REQUIRE(max_blocks_per_seq > 0 && num_blocks > 0, "max_blocks_per_seq and num_blocks must be positive");
+    REQUIRE((int64_t)num_blocks * num_kv_heads * block_size < (1LL << 31), "cache rows must fit in int32");
+    REQUIRE(std::isfinite(scale), "scale must be finite");
+    REQUIRE(key != nullptr && value != nullptr, "key/value (the step's new token) are NULL");
+    if (num_seqs == 0) return PA_OK;
+    REQUIRE_PTR(out, 16);
+    REQUIRE_PTR(query, 16);
+    REQUIRE_PTR(key, 16);
+    REQUIRE_PTR(value, 16);
+    REQUIRE_PTR(key_cache, 16);
+    REQUIRE_PTR(value_cache, 16);
+    REQUIRE_PTR(block_tables, 4);
+    REQUIRE_PTR(context_lens, 4);
+    const int PT = PA_DEFAULT_PARTITION_TOKENS;
+    const int64_t cap = (int64_t)max_blocks_per_seq * block_size;
+    int64_t mcl = max_context_len > 0 ? max_context_len : cap;
+    if (mcl > cap) mcl = cap;
+    const int NP = std::max<int>(1, (int)((mcl + PT - 1) / PT));
+    const size_t need = workspace_bytes_for(num_seqs, num_heads, head_dim, (int)mcl, PT);
+    if (workspace == nullptr || workspace_bytes < need)
+        return fail(PA_ERR_WORKSPACE, "workspace of %zu bytes required (got %zu)", need,
+                    workspace ? workspace_bytes : (size_t)0);
+    REQUIRE_PTR(workspace, 16);
+    pa::GroupParams gp{};
+    const CUtensorMapDataType dt = dtype == PA_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    {
+        const cuuint64_t dims[2] = {(cuuint64_t)head_dim, (cuuint64_t)num_blocks * num_kv_heads * block_size};
+        const cuuint64_t str[1] = {(cuuint64_t)head_dim * 2};
+        const cuuint32_t box[2] = {64, 16};
+        if (!encode_map(&gp.tmap_k, dt, 2, key_cache, dims, str, box) ||
+            !encode_map(&gp.tmap_v, dt, 2, value_cache, dims, str, box))
+            return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the cache maps");
+    }
+    pa::AttnParams& p = gp.a;
+    p.out = out;
+    p.query = query;
+    p.key_cache = key_cache;
+    p.value_cache = value_cache;
+    p.key_cache_w = key_cache;
+    p.value_cache_w = value_cache;
+    p.new_key = key;
+    p.new_value = value;
+    p.block_tables = block_tables;
+    p.context_lens = context_lens;
+    {
+        const WsLayout L = ws_layout(num_seqs, num_heads, head_dim, NP);
+        char* w = static_cast<char*>(workspace);
+        p.counters = reinterpret_cast<int*>(w + L.counters);
+        p.part_o = reinterpret_cast<float*>(w + L.part_o);
+        p.part_ml = reinterpret_cast<float2*>(w + L.part_ml);
+    }
+    p.scale_log2 = (float)((double)scale * 1.4426950408889634);
+    p.log2B = log2B;
+    p.H = num_heads;
+    p.H_kv = num_kv_heads;
+    p.G = num_heads / num_kv_heads;
+    p.W = max_blocks_per_seq;
+    p.PT = PT;
+    p.NP = NP;
+    p.GM = group_size;
+    p.S = num_seqs;
+    // stages: ~64 KB of slots per CTA (3 CTAs per SM), at least 2
+    int stg = std::max(2, std::min(8, (64 * 1024) / (group_size * 8192)));
+    if (const char* ev = getenv("PA_GROUP_STG")) stg = atoi(ev) > 0 ? atoi(ev) : stg;
+    p.STG = stg;
+    const size_t smem = pa::group_mma_smem_bytes(group_size, stg);
+    if (smem > 227 * 1024) return fail(PA_ERR_UNSUPPORTED, "group_size %d needs %zu B of shared memory", group_size, smem);
+    cudaError_t e = pa::launch_group_mma(gp, (int)dtype, num_seqs, smem, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "paged_attention_group_mma_kernel launch");
+    return PA_OK;
+}
+
 pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void* key_cache, const void* value_cache,
                                        const int32_t* block_tables, const int32_t* context_lens,
                                        const int32_t* query_start, float scale, int block_size, int num_kv_heads,

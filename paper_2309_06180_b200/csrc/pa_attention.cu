@@ -42,6 +42,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdio>
 
 namespace pa {
 
@@ -1424,6 +1425,348 @@ __global__ void __launch_bounds__(288) paged_attention_shared_kernel(const AttnP
     } else {
         finish_split<T, D>(p, sh, part, nparts, m, l, acc, g, c, lane);
     }
+}
+
+// ============================ sharing-aware decode on the tensor cores (N1, mma.sync) ===
+//
+// The sequences of one group (a request's parallel samples or beams) share
+// most physical blocks.  One CTA = (partition, query head, group of M <= 8 sequences);
+// warp 1 = producer, warp 0 = consumer.  The producer maps each 16-token logical tile of
+// the M members to their physical blocks and TMA-loads every DISTINCT block once (K and
+// V, two 64-column boxes each, 128-byte swizzle) into a slot of the stage.  The consumer
+// computes S = Q K^T for all members at once as an m16n8k16 tensor-core product (rows =
+// members, the group's queries held as A fragments), masks each row to the tokens of its
+// own slot and context, runs the online softmax per row on the accumulator fragments and
+// adds P V with a second product (V fragments through ldmatrix.trans).  A shared block
+// thus costs one K/V read from HBM/L2 and ~35 MMA instructions for the whole group,
+// instead of M separate FMA passes.  Accumulation order differs from the CUDA-core
+// kernels (results agree within the tolerance, not bitwise).
+template <bool BF>
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+    if (BF)
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+    else
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void tma_box(void* smem_dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+template <typename T>
+__device__ __forceinline__ uint32_t pack_pair(float a, float b) {
+    if constexpr (std::is_same<T, __half>::value) {
+        const __half2 v = __floats2half2_rn(a, b);
+        return *reinterpret_cast<const uint32_t*>(&v);
+    } else {
+        const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<const uint32_t*>(&v);
+    }
+}
+// byte offset of 16-byte chunk `ch` (0..15 over D = 128) of row `r` in a slot half
+// (K or V): two swizzled boxes of 16 rows x 128 bytes
+__device__ __forceinline__ uint32_t swz(int r, int ch) {
+    return (uint32_t)((ch >> 3) * 2048 + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
+}
+
+constexpr int kGroupSlot = 8192;  // K | V of one block x one kv head x 16 tokens (D = 128, 2-byte)
+
+size_t group_mma_smem_bytes(int gm, int stg) {
+    return 1024 + (size_t)stg * gm * kGroupSlot + 16 * (size_t)stg + 4 * (size_t)stg * gm + 16;
+}
+
+#ifdef PA_GROUP_DEBUG  // bounded waits that report where they stuck (debug variant)
+__device__ __forceinline__ void gwait(uint64_t* bar, uint32_t parity, int tag, int j) {
+    for (long long it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it == (tag == 2 ? (1LL << 18) : (1LL << 24))) {
+            printf("group_mma stuck: block (%d,%d,%d) thread %d tag %d tile %d parity %u\n", blockIdx.x, blockIdx.y,
+                   blockIdx.z, threadIdx.x, tag, j, parity);
+            __trap();
+        }
+    }
+}
+#define GWAIT(bar, par, tag, j) gwait(bar, par, tag, j)
+#else
+#define GWAIT(bar, par, tag, j) mbar_wait(bar, par)
+#endif
+
+template <typename T>
+__global__ void __launch_bounds__(64) paged_attention_group_mma_kernel(const __grid_constant__ GroupParams gp) {
+    constexpr int D = 128, RB = 256;
+    constexpr bool BF = std::is_same<T, __nv_bfloat16>::value;
+    constexpr unsigned FULL = 0xffffffffu;
+    const AttnParams& p = gp.a;
+    extern __shared__ __align__(1024) unsigned char gsmem_raw[];
+    unsigned char* smem =
+        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsmem_raw) + 1023) & ~(uintptr_t)1023);
+    const int part = blockIdx.x, h = blockIdx.y, grp = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int M = p.GM, STG = p.STG, PT = p.PT;
+    const int stage_bytes = M * kGroupSlot;
+    const int s0 = grp * M, nm = min(M, p.S - s0);
+    const int kvh = h / p.G;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STG * stage_bytes);
+    uint64_t* empty = full + STG;
+    int* smap = reinterpret_cast<int*>(empty + STG);  // [STG][M] member -> slot (-1: none)
+    if (threadIdx.x < STG) {
+        mbar_init(&full[threadIdx.x], 1);
+        mbar_init(&empty[threadIdx.x], 1);
+    }
+    fence_mbar_init();
+    __syncthreads();
+    pdl_wait();
+    // lane m < nm: member m's context, partition end and new-token position
+    const int my_ctx = lane < nm ? __ldg(p.context_lens + s0 + lane) : 0;
+    int gmax = my_ctx;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) gmax = max(gmax, __shfl_xor_sync(FULL, gmax, off));
+    const int p0 = part * PT;
+    if (part > 0 && p0 >= gmax) return;  // no member reaches this partition (CTA-uniform)
+    const int ntiles = (min(gmax, p0 + PT) - p0 + kTile - 1) / kTile;
+    const int my_p1 = min(my_ctx, p0 + PT);
+    const int my_tnew = (p.new_key != nullptr && lane < nm && my_ctx > 0 && my_p1 == my_ctx) ? my_ctx - 1 : -1;
+    const int B = 1 << p.log2B;
+
+    if (warp == 1) {  // ================================================ producer warp
+        const int32_t* btrow = p.block_tables + (int64_t)(s0 + min(lane, nm - 1)) * p.W;
+        for (int j = 0; j < ntiles; ++j) {
+            const int k = j % STG;
+            if (j >= STG) GWAIT(&empty[k], ((j / STG) - 1) & 1, 1, j);
+            const int tok0 = p0 + j * kTile;
+            const bool act = lane < nm && tok0 < my_p1;
+            const bool has_new = act && my_tnew >= tok0 && my_tnew < tok0 + kTile;
+            const int blk = act ? __ldg(btrow + (tok0 >> p.log2B)) : -1;
+            const bool shareable = act && !has_new;  // a new-token tile is private (CoW)
+            int leader = lane;
+            for (int m = 0; m < nm; ++m) {
+                const int bm = __shfl_sync(FULL, blk, m);
+                const bool sm = __shfl_sync(FULL, shareable, m);
+                if (shareable && sm && bm == blk && m < leader) leader = m;
+            }
+            const bool is_leader = act && leader == lane;
+            const unsigned leaders = __ballot_sync(FULL, is_leader);
+            const int my_slot = __popc(leaders & ((1u << lane) - 1u));
+            const int slot = __shfl_sync(FULL, my_slot, leader);
+            if (lane < M) smap[k * M + lane] = act ? slot : -1;
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(&full[k], (uint32_t)__popc(leaders) * kGroupSlot);  // + slot map
+            __syncwarp();
+            if (is_leader) {
+                unsigned char* sl = smem + (size_t)k * stage_bytes + (size_t)my_slot * kGroupSlot;
+                const int row = ((blk * p.H_kv + kvh) << p.log2B) + (tok0 & (B - 1));
+                tma_box(sl, &gp.tmap_k, 0, row, &full[k]);
+                tma_box(sl + 2048, &gp.tmap_k, 64, row, &full[k]);
+                tma_box(sl + 4096, &gp.tmap_v, 0, row, &full[k]);
+                tma_box(sl + 6144, &gp.tmap_v, 64, row, &full[k]);
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    // ================================================================== consumer warp
+    // fragment coordinates: row g (= member g; rows g + 8 are unused), column pair 2t, 2t+1
+    const int g = lane >> 2, t = lane & 3;
+    const bool row_ok = g < nm;
+    const int s_g = s0 + min(g, nm - 1);
+    const int ctx_g = __shfl_sync(FULL, my_ctx, g);
+    const int p1_g = min(ctx_g, p0 + PT);
+    uint32_t qa[8][2];  // A fragments of the members' queries: dims kk*16 + 2t (+8)
+    {
+        const uint32_t* qrow =
+            reinterpret_cast<const uint32_t*>(static_cast<const char*>(p.query) + ((int64_t)s_g * p.H + h) * RB);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            qa[kk][0] = row_ok ? __ldg(qrow + kk * 8 + t) : 0u;
+            qa[kk][1] = row_ok ? __ldg(qrow + kk * 8 + 4 + t) : 0u;
+        }
+    }
+    float o[16][4];
+#pragma unroll
+    for (int nd = 0; nd < 16; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
+    float m_g = -INFINITY, l_g = 0.f;  // l_g: this lane's partial row sum (quad-reduced at the end)
+    const int my_rows_lane = lane < nm ? my_p1 : 0;  // lane m: member m's partition end
+    for (int j = 0; j < ntiles; ++j) {
+        const int k = j % STG;
+        GWAIT(&full[k], (j / STG) & 1, 2, j);
+#ifdef PA_GROUP_DEBUG2
+        if (lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) printf("consumer got tile %d\n", j);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[k]);
+        continue;
+#endif
+        const int tok0 = p0 + j * kTile;
+        const int* sm = smap + k * M;
+        unsigned char* st = smem + (size_t)k * stage_bytes;
+        // lane m: its slot and the rows [0, rows) it reads in this tile
+        const int slot_l = lane < nm ? sm[lane] : -1;
+        const int rows_l = max(0, min(kTile, my_rows_lane - tok0));
+        int nslots = slot_l + 1;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) nslots = max(nslots, __shfl_xor_sync(FULL, nslots, off));
+        // new-token rows come from the step's inputs (the cache slot is written here too,
+        // by the first query head of each kv head)
+        for (int m = 0; m < nm; ++m) {
+            const int tn = __shfl_sync(FULL, my_tnew, m);
+            if (tn < tok0 || tn >= tok0 + kTile) continue;
+            const int sl = __shfl_sync(FULL, slot_l, m);
+            const int r = tn - tok0, ch = lane & 15;
+            const bool isv = lane >= 16;
+            const uint4 val = __ldg(reinterpret_cast<const uint4*>(static_cast<const char*>(isv ? p.new_value : p.new_key) +
+                                                                   ((int64_t)(s0 + m) * p.H_kv + kvh) * RB) +
+                                    ch);
+            *reinterpret_cast<uint4*>(st + (size_t)sl * kGroupSlot + (isv ? 4096 : 0) + swz(r, ch)) = val;
+            if (h % p.G == 0) {
+                const int blk = __ldg(p.block_tables + (int64_t)(s0 + m) * p.W + (tn >> p.log2B));
+                const int64_t off = ((((int64_t)blk * p.H_kv + kvh) << p.log2B) + (tn & (B - 1))) * RB;
+                reinterpret_cast<uint4*>(static_cast<char*>(isv ? p.value_cache_w : p.key_cache_w) + off)[ch] = val;
+            }
+        }
+        // V rows no member of a slot reads must be finite for P V (P = 0 there): zero them
+        for (int sl = 0; sl < nslots; ++sl) {
+            int need = slot_l == sl ? rows_l : 0;
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) need = max(need, __shfl_xor_sync(FULL, need, off));
+            for (int r = need + (lane >> 4); r < kTile; r += 2)
+                *reinterpret_cast<uint4*>(st + (size_t)sl * kGroupSlot + 4096 + swz(r, lane & 15)) =
+                    make_uint4(0u, 0u, 0u, 0u);
+        }
+        __syncwarp();
+        const int slot_g = __shfl_sync(FULL, slot_l, g);  // (every lane joins the shuffle)
+        const int my_slot = row_ok ? slot_g : -1;
+        for (int sl = 0; sl < nslots; ++sl) {
+            const uint32_t kbase = smem_u32(st + (size_t)sl * kGroupSlot), vbase = kbase + 4096;
+            float sacc[2][4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+#pragma unroll
+                for (int kp = 0; kp < 4; ++kp) {
+                    const int q = lane >> 3, tr = nt * 8 + (lane & 7), ch = (2 * kp + (q >> 1)) * 2 + (q & 1);
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4(kbase + swz(tr, ch), b0, b1, b2, b3);
+                    mma16816<BF>(sacc[nt], qa[2 * kp][0], qa[2 * kp][1], b0, b1);
+                    mma16816<BF>(sacc[nt], qa[2 * kp + 1][0], qa[2 * kp + 1][1], b2, b3);
+                }
+            }
+            // row g's scores of tokens tok0 + {2t, 2t+1, 8+2t, 8+2t+1}, masked to its slot and context
+            const bool mine = my_slot == sl;
+            float x[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int tk = tok0 + (i >> 1) * 8 + 2 * t + (i & 1);
+                x[i] = (mine && tk < p1_g) ? sacc[i >> 1][i & 1] * p.scale_log2 : -INFINITY;
+            }
+            float tmax = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+            tmax = fmaxf(tmax, __shfl_xor_sync(FULL, tmax, 1));
+            tmax = fmaxf(tmax, __shfl_xor_sync(FULL, tmax, 2));
+            const float mn = fmaxf(m_g, tmax);
+            const float ms = (mn == -INFINITY) ? 0.f : mn;
+            const float alpha = ex2(m_g - ms);
+            float pr[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pr[i] = ex2(x[i] - ms);
+            l_g = l_g * alpha + ((pr[0] + pr[1]) + (pr[2] + pr[3]));
+            if (__any_sync(FULL, alpha != 1.f)) {
+#pragma unroll
+                for (int nd = 0; nd < 16; ++nd) {
+                    o[nd][0] *= alpha;
+                    o[nd][1] *= alpha;
+                }
+            }
+            m_g = mn;
+            const uint32_t pa0 = pack_pair<T>(pr[0], pr[1]), pa2 = pack_pair<T>(pr[2], pr[3]);
+#pragma unroll
+            for (int np = 0; np < 8; ++np) {
+                const int q = lane >> 3, tr = (q & 1) * 8 + (lane & 7), ch = 2 * np + (q >> 1);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(vbase + swz(tr, ch), b0, b1, b2, b3);
+                mma16816<BF>(o[2 * np], pa0, pa2, b0, b1);
+                mma16816<BF>(o[2 * np + 1], pa0, pa2, b2, b3);
+            }
+        }
+        // generic-proxy writes of this stage (new rows, zeroed rows) before the TMA reuses it
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[k]);
+    }
+    l_g += __shfl_xor_sync(FULL, l_g, 1);
+    l_g += __shfl_xor_sync(FULL, l_g, 2);
+    // row g's result: members with tokens in this partition (every member at partition 0)
+    const bool has = row_ok && (part == 0 || p0 < ctx_g);
+    const int nparts_g = ctx_g > 0 ? (ctx_g + PT - 1) / PT : 1;
+    const int64_t sh = (int64_t)s_g * p.H + h;
+    const float inv = l_g > 0.f ? 1.f / l_g : 0.f;
+    if (has && nparts_g == 1) {
+        T* orow = static_cast<T*>(p.out) + sh * D;
+#pragma unroll
+        for (int nd = 0; nd < 16; ++nd)
+            *reinterpret_cast<uint32_t*>(orow + nd * 8 + 2 * t) = pack_pair<T>(o[nd][0] * inv, o[nd][1] * inv);
+    } else if (has) {
+        float* po = p.part_o + (sh * p.NP + part) * D;
+#pragma unroll
+        for (int nd = 0; nd < 16; ++nd)
+            *reinterpret_cast<float2*>(po + nd * 8 + 2 * t) = make_float2(o[nd][0] * inv, o[nd][1] * inv);
+        if (t == 0) p.part_ml[sh * p.NP + part] = make_float2(m_g, l_g);
+    }
+    __threadfence();
+    __syncwarp();
+    for (int r = 0; r < nm; ++r) {  // split members: the last partition to finish merges (finish_split)
+        const int ctx_r = __shfl_sync(FULL, my_ctx, r);
+        const int np_r = ctx_r > 0 ? (ctx_r + PT - 1) / PT : 1;
+        if (np_r == 1 || p0 >= ctx_r) continue;
+        const int64_t shr = (int64_t)(s0 + r) * p.H + h;
+        int last = 0;
+        if (lane == 0) last = atomicAdd(p.counters + shr, 1) == min(np_r, p.NP) - 1;
+        last = __shfl_sync(FULL, last, 0);
+        if (last) {
+            __threadfence();
+            merge_partitions<T, D>(p, shr, min(np_r, p.NP), lane);
+        }
+    }
+}
+
+cudaError_t launch_group_mma(const GroupParams& p, int dtype, int num_seqs, size_t smem, cudaStream_t stream) {
+    auto kern = dtype == 1 ? paged_attention_group_mma_kernel<__half> : paged_attention_group_mma_kernel<__nv_bfloat16>;
+    static size_t configured[2] = {0, 0};
+    if (smem > configured[dtype == 1 ? 0 : 1]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured[dtype == 1 ? 0 : 1] = smem;
+    }
+    if (p.a.NP > 1) {
+        cudaError_t e = cudaMemsetAsync(p.a.counters, 0, sizeof(int) * (size_t)num_seqs * p.a.H, stream);
+        if (e != cudaSuccess) return e;
+    }
+    const dim3 grid(p.a.NP, p.a.H, (num_seqs + p.a.GM - 1) / p.a.GM);
+    return launch_k(kern, grid, dim3(64), smem, stream, p);
 }
 
 // ==================================================================== debug gather ===

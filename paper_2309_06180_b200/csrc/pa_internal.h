@@ -70,6 +70,15 @@ struct AttnParams {
     void* out_peers[kMaxTpPeers];
 };
 
+// Sharing-aware decode on the tensor cores (N1, pa_paged_attention_decode_grouped): the
+// caches as 2-D tensor maps [NB*H_kv*B rows][D], box {64 cols, 16 rows}, 128-byte swizzle;
+// everything else in `a` (GM = sequences per group, STG = stages).
+struct GroupParams {
+    CUtensorMap tmap_k;
+    CUtensorMap tmap_v;
+    AttnParams a;
+};
+
 struct GatherParams {
     void* k_out;
     void* v_out;
@@ -136,6 +145,8 @@ size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int g
 // sched: 0 = grid, 1 = persistent, 2 = coop, 3 = persistent coop, 4 = sharing-aware groups, 5 = listed coop
 cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int sched, size_t smem,
                              cudaStream_t stream);
+size_t group_mma_smem_bytes(int gm, int stg);
+cudaError_t launch_group_mma(const GroupParams& p, int dtype, int num_seqs, size_t smem, cudaStream_t stream);
 size_t prefill_smem_bytes();
 cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, cudaStream_t stream);
 // N2: rank `rank` publishes `epoch` to every peer's flag array, then waits (bounded) until

@@ -112,6 +112,30 @@ def paged_attention_decode_shared(out, query, key, value, key_cache, value_cache
     return out
 
 
+def paged_attention_decode_grouped(out, query, key, value, key_cache, value_cache, block_tables, context_lens,
+                                   scale: float, group_size: int, max_context_len: int = 0,
+                                   workspace: torch.Tensor | None = None, stream=None):
+    """The sharing-aware decode step on the tensor cores (pa.h): groups of
+    group_size consecutive sequences; each distinct block of a group is loaded once per
+    logical tile and Q K^T / P V run as MMAs over the group's rows.  f16/bf16, D = 128,
+    block_size >= 16."""
+    S, H, D = query.shape
+    NB, hk, B, _ = key_cache.shape
+    W = block_tables.shape[1]
+    mcl = max_context_len if max_context_len > 0 else W * B
+    need = paged_attention_workspace_size(S, H, D, mcl, 0)
+    if workspace is None and need > 0:
+        workspace = torch.empty(need, dtype=torch.uint8, device=query.device)
+    ws_ptr = _dev(workspace, "workspace") if workspace is not None else None
+    ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    check(_lib.raw().pa_paged_attention_decode_grouped(
+        _dev(out, "out"), _dev(query, "query"), _dev(key, "key"), _dev(value, "value"), _dev(key_cache, "key_cache"),
+        _dev(value_cache, "value_cache"), _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"),
+        float(scale), B, hk, NB, S, H, D, W, int(mcl), int(group_size), _code(query), ws_ptr, ws_bytes,
+        _stream(stream)), "pa_paged_attention_decode_grouped")
+    return out
+
+
 PREFILL_WORKSPACE_BYTES = 16
 
 

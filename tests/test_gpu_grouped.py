@@ -1,0 +1,91 @@
+"""GPU parity of the sharing-aware decode step on the tensor cores (SURVEY 8(f) N1,
+pa_paged_attention_decode_grouped): the group's shared blocks are loaded once and
+Q K^T / P V run as MMAs over the group's rows.  Against the fp64 oracle on
+identical generated inputs (max-abs <= 2e-3 fp16, 1e-2 bf16; caches bit-exact), at
+small sizes spanning several tiles, split contexts, GQA, block sizes and unrelated
+(non-sharing) groups, and at the full C3/C5 sizes on sampled sequences."""
+import numpy as np
+import pytest
+import torch
+
+from synth import make_config, materialize_torch, shard, subset, tables_torch
+from tests.pathutil import TOL, bits, max_abs, oracle_step
+
+pytestmark = pytest.mark.gpu
+pa = pytest.importorskip("paper_2309_06180_b200")
+
+
+def grouped_step(wl, gs, x=None):
+    x = x or materialize_torch(wl, "cuda")
+    tb = tables_torch(wl, "cuda")
+    if len(wl.block_mapping):
+        pa.copy_blocks([x["key_cache"]], [x["value_cache"]], tb["block_mapping"])
+    out = torch.full_like(x["query"], float("nan"))
+    pa.paged_attention_decode_grouped(out, x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"],
+                                      tb["block_tables"], tb["context_lens"], wl.scale, gs,
+                                      max_context_len=wl.max_context_len)
+    torch.cuda.synchronize()
+    return out, x
+
+
+@pytest.mark.parametrize("name,over,gs", [
+    ("c5_beam", dict(S=14, H=4, H_kv=4), 4),            # beams: most blocks shared, last group ragged
+    ("c5_beam", dict(S=16, H=4, H_kv=2), 4),            # GQA (c13)
+    ("c5_beam", dict(S=16, H=2, H_kv=2, B=32), 4),      # 2 tiles per block
+    ("c3_parallel", dict(S=24, H=2, H_kv=2), 6),        # parallel samples, bf16
+    ("c3_fork", dict(S=24, H=2, H_kv=2), 6),            # fork step: CoW'd last blocks
+    ("c3_parallel", dict(S=24, H=2, H_kv=2), 8),        # groups not aligned with requests
+    ("c2_sharegpt", dict(S=24, H=4, H_kv=4), 4),        # unrelated sequences: no sharing
+    ("c4_long", dict(S=8, H=2, H_kv=2), 2),             # split contexts (up to 4 partitions)
+    ("c2_alpaca", dict(S=40, H=2, H_kv=2), 1),          # group of one
+])
+def test_grouped_decode_vs_oracle(name, over, gs):
+    wl = make_config(name, **over)
+    out, x = grouped_step(wl, gs)
+    ref, rkc, rvc = oracle_step(wl)
+    assert np.array_equal(bits(x["key_cache"]), rkc) and np.array_equal(bits(x["value_cache"]), rvc)
+    assert not torch.isnan(out).any()
+    assert max_abs(out, ref) <= TOL[wl.dtype]
+
+
+def test_grouped_decode_context_edges():
+    """ctx = 0 (zeros), ctx = 1 (the new token's V row), tile and partition boundaries,
+    inside groups of unrelated sequences."""
+    ctx = [0, 1, 2, 15, 16, 17, 31, 32, 33, 511, 512, 513, 1023, 1024, 1025, 2047, 2048]
+    wl = make_config("explicit", ctx=ctx, H=4, H_kv=4, D=128, B=16, dtype="f16", seed=5)
+    out, x = grouped_step(wl, 4)
+    ref, rkc, rvc = oracle_step(wl)
+    assert np.array_equal(bits(x["key_cache"]), rkc) and np.array_equal(bits(x["value_cache"]), rvc)
+    assert max_abs(out, ref) <= TOL["f16"]
+    assert not out[0].any()
+
+
+@pytest.mark.parametrize("name,gs", [("c5_beam", 4), ("c3_parallel", 6)])
+def test_grouped_decode_full_size_sampled(name, gs):
+    """BASELINE.json sizes: whole output finite, sampled sequences x a head slice against
+    the oracle, and every new token's K/V landed bit for bit."""
+    wl = make_config(name)
+    out, x = grouped_step(wl, gs)
+    assert not torch.isnan(out).any()
+    rs = np.random.default_rng(len(name))
+    seqs = sorted(set([int(np.argmax(wl.context_lens))] + rs.choice(wl.S, 5, replace=False).tolist()))
+    world = wl.H // 4
+    rank = int(rs.integers(world))
+    sub = shard(subset(wl, seqs), rank, world)
+    ref, *_ = oracle_step(sub)
+    got = out[seqs][:, sub.q_head0:sub.q_head0 + sub.H]
+    assert max_abs(got, ref) <= TOL[wl.dtype]
+    slots = torch.as_tensor(wl.slot_mapping, device="cuda")
+    kc, vc, B = x["key_cache"], x["value_cache"], wl.B
+    assert torch.equal(kc[slots // B, :, slots % B, :], x["key"])
+    assert torch.equal(vc[slots // B, :, slots % B, :], x["value"])
+
+
+def test_grouped_decode_rejects_unsupported():
+    wl = make_config("c1_tiny")  # fp32, D = 64
+    x = materialize_torch(wl, "cuda")
+    tb = tables_torch(wl, "cuda")
+    with pytest.raises(pa.PagedAttnError):
+        pa.paged_attention_decode_grouped(torch.empty_like(x["query"]), x["query"], x["key"], x["value"],
+                                          x["key_cache"], x["value_cache"], tb["block_tables"], tb["context_lens"],
+                                          wl.scale, 4)
