@@ -430,11 +430,15 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
     p.NP = NP;
     p.GM = group_size;
     p.S = num_seqs;
-    // stages: ~64 KB of slots per CTA (3 CTAs per SM), at least 2
-    int stg = std::max(2, std::min(8, (64 * 1024) / (group_size * 8192)));
+    // block slots per stage (a tile whose group reads more distinct blocks takes several
+    // stages) and stages: PA_GROUP_SLOTS / PA_GROUP_STG override
+    int gsl = std::min(group_size, 2);
+    if (const char* ev = getenv("PA_GROUP_SLOTS")) gsl = std::max(1, std::min(group_size, atoi(ev)));
+    int stg = 2;
     if (const char* ev = getenv("PA_GROUP_STG")) stg = atoi(ev) > 0 ? atoi(ev) : stg;
     p.STG = stg;
-    const size_t smem = pa::group_mma_smem_bytes(group_size, stg);
+    p.GSL = gsl;
+    const size_t smem = pa::group_mma_smem_bytes(group_size, gsl, stg, PT);
     if (smem > 227 * 1024) return fail(PA_ERR_UNSUPPORTED, "group_size %d needs %zu B of shared memory", group_size, smem);
     cudaError_t e = pa::launch_group_mma(gp, (int)dtype, num_seqs, smem, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "paged_attention_group_mma_kernel launch");

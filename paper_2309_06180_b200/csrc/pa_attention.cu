@@ -1443,6 +1443,10 @@ __global__ void __launch_bounds__(288) paged_attention_shared_kernel(const AttnP
 // kernels (results agree within the tolerance, not bitwise).
 template <bool BF>
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+#ifdef PA_GROUP_NOMMA  // timing experiment: the MMAs replaced by one dependent FADD
+    d[0] += __uint_as_float(a0 ^ b0) * 1e-30f;
+    return;
+#endif
     if (BF)
         asm volatile(
             "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -1491,8 +1495,11 @@ __device__ __forceinline__ uint32_t swz(int r, int ch) {
 
 constexpr int kGroupSlot = 8192;  // K | V of one block x one kv head x 16 tokens (D = 128, 2-byte)
 
-size_t group_mma_smem_bytes(int gm, int stg) {
-    return 1024 + (size_t)stg * gm * kGroupSlot + 16 * (size_t)stg + 4 * (size_t)stg * gm + 16;
+// per stage: gm slots | barriers | tile metadata (slot per member, slot count, new-token
+// member mask, rows needed per slot)
+size_t group_mma_smem_bytes(int gm, int gsl, int stg, int pt) {
+    return 1024 + (size_t)stg * gsl * kGroupSlot + 16 * (size_t)stg + 4 * (size_t)stg * (gm + 3 + gsl) +
+           4 * (size_t)gm * (pt / kTile) + 16;
 }
 
 #ifdef PA_GROUP_DEBUG  // bounded waits that report where they stuck (debug variant)
@@ -1518,7 +1525,7 @@ __device__ __forceinline__ void gwait(uint64_t* bar, uint32_t parity, int tag, i
 #endif
 
 template <typename T>
-__global__ void __launch_bounds__(64) paged_attention_group_mma_kernel(const __grid_constant__ GroupParams gp) {
+__global__ void __launch_bounds__(96) paged_attention_group_mma_kernel(const __grid_constant__ GroupParams gp) {
     constexpr int D = 128, RB = 256;
     constexpr bool BF = std::is_same<T, __nv_bfloat16>::value;
     constexpr unsigned FULL = 0xffffffffu;
@@ -1528,16 +1535,21 @@ __global__ void __launch_bounds__(64) paged_attention_group_mma_kernel(const __g
         reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsmem_raw) + 1023) & ~(uintptr_t)1023);
     const int part = blockIdx.x, h = blockIdx.y, grp = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int M = p.GM, STG = p.STG, PT = p.PT;
-    const int stage_bytes = M * kGroupSlot;
+    const int M = p.GM, STG = p.STG, PT = p.PT, GSL = p.GSL;
+    const int stage_bytes = GSL * kGroupSlot;
     const int s0 = grp * M, nm = min(M, p.S - s0);
     const int kvh = h / p.G;
+    // metadata per stage: [0, M) slot of member m in this stage (-1: none), [M] slots,
+    // [M+1] new-token members, [M+2] tile start (-1: end of the partition), [M+3, +GSL) rows
+    // each slot's members read
+    const int MW = M + 3 + GSL;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STG * stage_bytes);
     uint64_t* empty = full + STG;
-    int* smap = reinterpret_cast<int*>(empty + STG);  // [STG][M] member -> slot (-1: none)
+    int* meta = reinterpret_cast<int*>(empty + STG);  // [STG][MW]
+    int* sbt = meta + STG * MW;                        // [M][PT / 16] block id of member m's tile j
     if (threadIdx.x < STG) {
         mbar_init(&full[threadIdx.x], 1);
-        mbar_init(&empty[threadIdx.x], 1);
+        mbar_init(&empty[threadIdx.x], 2);  // both consumer warps release a stage
     }
     fence_mbar_init();
     __syncthreads();
@@ -1554,45 +1566,79 @@ __global__ void __launch_bounds__(64) paged_attention_group_mma_kernel(const __g
     const int my_tnew = (p.new_key != nullptr && lane < nm && my_ctx > 0 && my_p1 == my_ctx) ? my_ctx - 1 : -1;
     const int B = 1 << p.log2B;
 
-    if (warp == 1) {  // ================================================ producer warp
-        const int32_t* btrow = p.block_tables + (int64_t)(s0 + min(lane, nm - 1)) * p.W;
+    if (warp == 2) {  // ================================================ producer warp
+        // every member's block ids of the partition, loaded in parallel up front
+        const int TPP = PT / kTile;
+        for (int i = lane; i < nm * TPP; i += 32) {
+            const int m = i / TPP, jj = i - m * TPP;
+            const int tok = p0 + jj * kTile;
+            sbt[i] = jj < ntiles ? __ldg(p.block_tables + (int64_t)(s0 + m) * p.W + (tok >> p.log2B)) : -1;
+        }
+        __syncwarp();
+        int u = 0;  // stages posted
         for (int j = 0; j < ntiles; ++j) {
-            const int k = j % STG;
-            if (j >= STG) GWAIT(&empty[k], ((j / STG) - 1) & 1, 1, j);
             const int tok0 = p0 + j * kTile;
             const bool act = lane < nm && tok0 < my_p1;
             const bool has_new = act && my_tnew >= tok0 && my_tnew < tok0 + kTile;
-            const int blk = act ? __ldg(btrow + (tok0 >> p.log2B)) : -1;
+            const int blk = act ? sbt[lane * TPP + j] : -1;
+            const int rows = act ? min(kTile, my_p1 - tok0) : 0;
             const bool shareable = act && !has_new;  // a new-token tile is private (CoW)
-            int leader = lane;
-            for (int m = 0; m < nm; ++m) {
-                const int bm = __shfl_sync(FULL, blk, m);
-                const bool sm = __shfl_sync(FULL, shareable, m);
-                if (shareable && sm && bm == blk && m < leader) leader = m;
-            }
+            // leader = lowest member reading the same block (unshareable members lead themselves)
+            const unsigned same = __match_any_sync(FULL, shareable ? blk : -2 - lane);
+            const int leader = __ffs(same) - 1;
             const bool is_leader = act && leader == lane;
             const unsigned leaders = __ballot_sync(FULL, is_leader);
             const int my_slot = __popc(leaders & ((1u << lane) - 1u));
             const int slot = __shfl_sync(FULL, my_slot, leader);
-            if (lane < M) smap[k * M + lane] = act ? slot : -1;
-            __syncwarp();
-            if (lane == 0) mbar_arrive_expect_tx(&full[k], (uint32_t)__popc(leaders) * kGroupSlot);  // + slot map
-            __syncwarp();
-            if (is_leader) {
-                unsigned char* sl = smem + (size_t)k * stage_bytes + (size_t)my_slot * kGroupSlot;
-                const int row = ((blk * p.H_kv + kvh) << p.log2B) + (tok0 & (B - 1));
-                tma_box(sl, &gp.tmap_k, 0, row, &full[k]);
-                tma_box(sl + 2048, &gp.tmap_k, 64, row, &full[k]);
-                tma_box(sl + 4096, &gp.tmap_v, 0, row, &full[k]);
-                tma_box(sl + 6144, &gp.tmap_v, 64, row, &full[k]);
+            // rows a slot must hold: the largest need among its members
+            int need = 0;
+            for (int m = 0; m < nm; ++m) {
+                const int sl_m = __shfl_sync(FULL, act ? slot : -1, m);
+                const int r_m = __shfl_sync(FULL, rows, m);
+                if (is_leader && sl_m == my_slot) need = max(need, r_m);
             }
-            __syncwarp();
+            const int d = __popc(leaders);
+            for (int pass0 = 0; pass0 < d; pass0 += GSL, ++u) {  // GSL distinct blocks per stage
+                const int k = u % STG;
+                if (u >= STG) GWAIT(&empty[k], ((u / STG) - 1) & 1, 1, u);
+                const bool in = act && slot >= pass0 && slot < pass0 + GSL;
+                const unsigned newmask = __ballot_sync(FULL, has_new && in);
+                int* mt = meta + k * MW;
+                if (lane < M) mt[lane] = in ? slot - pass0 : -1;
+                if (is_leader && in) mt[M + 3 + my_slot - pass0] = need;
+                if (lane == 0) {
+                    mt[M] = min(GSL, d - pass0);
+                    mt[M + 1] = (int)newmask;
+                    mt[M + 2] = tok0;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive_expect_tx(&full[k], (uint32_t)min(GSL, d - pass0) * kGroupSlot);
+                __syncwarp();
+                if (is_leader && in) {
+                    unsigned char* sl = smem + (size_t)k * stage_bytes + (size_t)(my_slot - pass0) * kGroupSlot;
+                    const int row = ((blk * p.H_kv + kvh) << p.log2B) + (tok0 & (B - 1));
+                    tma_box(sl, &gp.tmap_k, 0, row, &full[k]);
+                    tma_box(sl + 2048, &gp.tmap_k, 64, row, &full[k]);
+                    tma_box(sl + 4096, &gp.tmap_v, 0, row, &full[k]);
+                    tma_box(sl + 6144, &gp.tmap_v, 64, row, &full[k]);
+                }
+                __syncwarp();
+            }
+        }
+        // end marker for the consumers
+        const int k = u % STG;
+        if (u >= STG) GWAIT(&empty[k], ((u / STG) - 1) & 1, 1, u);
+        if (lane == 0) {
+            meta[k * MW + M + 2] = -1;
+            mbar_arrive_expect_tx(&full[k], 0u);
         }
         return;
     }
 
-    // ================================================================== consumer warp
-    // fragment coordinates: row g (= member g; rows g + 8 are unused), column pair 2t, 2t+1
+    // ============================================================= consumer warps 0, 1
+    // Both compute S for all members; warp w accumulates P V for dims [64w, 64w + 64) only.
+    // Fragment coordinates: row g (= member g; rows g + 8 are unused), column pair 2t, 2t+1.
+    const int w = warp;
     const int g = lane >> 2, t = lane & 3;
     const bool row_ok = g < nm;
     const int s_g = s0 + min(g, nm - 1);
@@ -1608,72 +1654,69 @@ __global__ void __launch_bounds__(64) paged_attention_group_mma_kernel(const __g
             qa[kk][1] = row_ok ? __ldg(qrow + kk * 8 + 4 + t) : 0u;
         }
     }
-    float o[16][4];
+    float o[8][4];  // dims 64w + nd*8 + 2t (+1)
 #pragma unroll
-    for (int nd = 0; nd < 16; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
+    for (int nd = 0; nd < 8; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
     float m_g = -INFINITY, l_g = 0.f;  // l_g: this lane's partial row sum (quad-reduced at the end)
-    const int my_rows_lane = lane < nm ? my_p1 : 0;  // lane m: member m's partition end
-    for (int j = 0; j < ntiles; ++j) {
-        const int k = j % STG;
-        GWAIT(&full[k], (j / STG) & 1, 2, j);
-#ifdef PA_GROUP_DEBUG2
-        if (lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) printf("consumer got tile %d\n", j);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[k]);
-        continue;
-#endif
-        const int tok0 = p0 + j * kTile;
-        const int* sm = smap + k * M;
+    for (int u = 0;; ++u) {
+        const int k = u % STG;
+        GWAIT(&full[k], (u / STG) & 1, 2, u);
+        const int* mt = meta + k * MW;
+        const int tok0 = mt[M + 2];
+        if (tok0 < 0) break;  // end of the partition
         unsigned char* st = smem + (size_t)k * stage_bytes;
-        // lane m: its slot and the rows [0, rows) it reads in this tile
-        const int slot_l = lane < nm ? sm[lane] : -1;
-        const int rows_l = max(0, min(kTile, my_rows_lane - tok0));
-        int nslots = slot_l + 1;
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) nslots = max(nslots, __shfl_xor_sync(FULL, nslots, off));
-        // new-token rows come from the step's inputs (the cache slot is written here too,
-        // by the first query head of each kv head)
-        for (int m = 0; m < nm; ++m) {
-            const int tn = __shfl_sync(FULL, my_tnew, m);
-            if (tn < tok0 || tn >= tok0 + kTile) continue;
-            const int sl = __shfl_sync(FULL, slot_l, m);
-            const int r = tn - tok0, ch = lane & 15;
-            const bool isv = lane >= 16;
-            const uint4 val = __ldg(reinterpret_cast<const uint4*>(static_cast<const char*>(isv ? p.new_value : p.new_key) +
-                                                                   ((int64_t)(s0 + m) * p.H_kv + kvh) * RB) +
-                                    ch);
-            *reinterpret_cast<uint4*>(st + (size_t)sl * kGroupSlot + (isv ? 4096 : 0) + swz(r, ch)) = val;
-            if (h % p.G == 0) {
-                const int blk = __ldg(p.block_tables + (int64_t)(s0 + m) * p.W + (tn >> p.log2B));
-                const int64_t off = ((((int64_t)blk * p.H_kv + kvh) << p.log2B) + (tn & (B - 1))) * RB;
-                reinterpret_cast<uint4*>(static_cast<char*>(isv ? p.value_cache_w : p.key_cache_w) + off)[ch] = val;
+        const int nslots = mt[M];
+        const unsigned newmask = (unsigned)mt[M + 1];
+        if (newmask) {  // new-token rows from the step's inputs: warp w writes dims half w of K and V
+            for (unsigned mm = newmask; mm; mm &= mm - 1) {
+                const int m = __ffs(mm) - 1;
+                const int tn = __shfl_sync(FULL, my_tnew, m);
+                const int sl = mt[m], r = tn - tok0;
+                const int ch = w * 8 + (lane & 7);  // 16-byte chunk of the row (dims 8ch..8ch+7)
+                const bool isv = lane >= 8;
+                if (lane < 16) {
+                    const uint4 val = __ldg(reinterpret_cast<const uint4*>(
+                                                static_cast<const char*>(isv ? p.new_value : p.new_key) +
+                                                ((int64_t)(s0 + m) * p.H_kv + kvh) * RB) +
+                                            ch);
+                    *reinterpret_cast<uint4*>(st + (size_t)sl * kGroupSlot + (isv ? 4096 : 0) + swz(r, ch)) = val;
+                    if (h % p.G == 0) {  // the cache slot, once per kv head
+                        const int blk = __ldg(p.block_tables + (int64_t)(s0 + m) * p.W + (tn >> p.log2B));
+                        const int64_t off = ((((int64_t)blk * p.H_kv + kvh) << p.log2B) + (tn & (B - 1))) * RB;
+                        reinterpret_cast<uint4*>(static_cast<char*>(isv ? p.value_cache_w : p.key_cache_w) + off)[ch] =
+                            val;
+                    }
+                }
             }
+            asm volatile("bar.sync 1, 64;" ::: "memory");  // both K halves in place before S
         }
-        // V rows no member of a slot reads must be finite for P V (P = 0 there): zero them
+        // V rows of this warp's half that no member of a slot reads: finite (zero) for P V
         for (int sl = 0; sl < nslots; ++sl) {
-            int need = slot_l == sl ? rows_l : 0;
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) need = max(need, __shfl_xor_sync(FULL, need, off));
-            for (int r = need + (lane >> 4); r < kTile; r += 2)
-                *reinterpret_cast<uint4*>(st + (size_t)sl * kGroupSlot + 4096 + swz(r, lane & 15)) =
+            const int need = mt[M + 3 + sl];
+            for (int r = need + (lane >> 3); r < kTile; r += 4)
+                *reinterpret_cast<uint4*>(st + (size_t)sl * kGroupSlot + 4096 + swz(r, w * 8 + (lane & 7))) =
                     make_uint4(0u, 0u, 0u, 0u);
         }
         __syncwarp();
-        const int slot_g = __shfl_sync(FULL, slot_l, g);  // (every lane joins the shuffle)
+        const int slot_g = mt[min(g, M - 1)];
         const int my_slot = row_ok ? slot_g : -1;
         for (int sl = 0; sl < nslots; ++sl) {
             const uint32_t kbase = smem_u32(st + (size_t)sl * kGroupSlot), vbase = kbase + 4096;
-            float sacc[2][4];
+            float sa[2][4], sb[2][4];  // two accumulation chains per n-tile (even / odd k pairs)
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
-                sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+                sa[nt][0] = sa[nt][1] = sa[nt][2] = sa[nt][3] = 0.f;
+                sb[nt][0] = sb[nt][1] = sb[nt][2] = sb[nt][3] = 0.f;
+            }
 #pragma unroll
-                for (int kp = 0; kp < 4; ++kp) {
+            for (int kp = 0; kp < 4; ++kp) {
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
                     const int q = lane >> 3, tr = nt * 8 + (lane & 7), ch = (2 * kp + (q >> 1)) * 2 + (q & 1);
                     uint32_t b0, b1, b2, b3;
                     ldsm_x4(kbase + swz(tr, ch), b0, b1, b2, b3);
-                    mma16816<BF>(sacc[nt], qa[2 * kp][0], qa[2 * kp][1], b0, b1);
-                    mma16816<BF>(sacc[nt], qa[2 * kp + 1][0], qa[2 * kp + 1][1], b2, b3);
+                    mma16816<BF>(sa[nt], qa[2 * kp][0], qa[2 * kp][1], b0, b1);
+                    mma16816<BF>(sb[nt], qa[2 * kp + 1][0], qa[2 * kp + 1][1], b2, b3);
                 }
             }
             // row g's scores of tokens tok0 + {2t, 2t+1, 8+2t, 8+2t+1}, masked to its slot and context
@@ -1682,7 +1725,7 @@ __global__ void __launch_bounds__(64) paged_attention_group_mma_kernel(const __g
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int tk = tok0 + (i >> 1) * 8 + 2 * t + (i & 1);
-                x[i] = (mine && tk < p1_g) ? sacc[i >> 1][i & 1] * p.scale_log2 : -INFINITY;
+                x[i] = (mine && tk < p1_g) ? (sa[i >> 1][i & 1] + sb[i >> 1][i & 1]) * p.scale_log2 : -INFINITY;
             }
             float tmax = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
             tmax = fmaxf(tmax, __shfl_xor_sync(FULL, tmax, 1));
@@ -1696,7 +1739,7 @@ __global__ void __launch_bounds__(64) paged_attention_group_mma_kernel(const __g
             l_g = l_g * alpha + ((pr[0] + pr[1]) + (pr[2] + pr[3]));
             if (__any_sync(FULL, alpha != 1.f)) {
 #pragma unroll
-                for (int nd = 0; nd < 16; ++nd) {
+                for (int nd = 0; nd < 8; ++nd) {
                     o[nd][0] *= alpha;
                     o[nd][1] *= alpha;
                 }
@@ -1704,8 +1747,8 @@ __global__ void __launch_bounds__(64) paged_attention_group_mma_kernel(const __g
             m_g = mn;
             const uint32_t pa0 = pack_pair<T>(pr[0], pr[1]), pa2 = pack_pair<T>(pr[2], pr[3]);
 #pragma unroll
-            for (int np = 0; np < 8; ++np) {
-                const int q = lane >> 3, tr = (q & 1) * 8 + (lane & 7), ch = 2 * np + (q >> 1);
+            for (int np = 0; np < 4; ++np) {
+                const int q = lane >> 3, tr = (q & 1) * 8 + (lane & 7), ch = w * 8 + 2 * np + (q >> 1);
                 uint32_t b0, b1, b2, b3;
                 ldsm_x4_t(vbase + swz(tr, ch), b0, b1, b2, b3);
                 mma16816<BF>(o[2 * np], pa0, pa2, b0, b1);
@@ -1725,19 +1768,20 @@ __global__ void __launch_bounds__(64) paged_attention_group_mma_kernel(const __g
     const int64_t sh = (int64_t)s_g * p.H + h;
     const float inv = l_g > 0.f ? 1.f / l_g : 0.f;
     if (has && nparts_g == 1) {
-        T* orow = static_cast<T*>(p.out) + sh * D;
+        T* orow = static_cast<T*>(p.out) + sh * D + w * 64;
 #pragma unroll
-        for (int nd = 0; nd < 16; ++nd)
+        for (int nd = 0; nd < 8; ++nd)
             *reinterpret_cast<uint32_t*>(orow + nd * 8 + 2 * t) = pack_pair<T>(o[nd][0] * inv, o[nd][1] * inv);
     } else if (has) {
-        float* po = p.part_o + (sh * p.NP + part) * D;
+        float* po = p.part_o + (sh * p.NP + part) * D + w * 64;
 #pragma unroll
-        for (int nd = 0; nd < 16; ++nd)
+        for (int nd = 0; nd < 8; ++nd)
             *reinterpret_cast<float2*>(po + nd * 8 + 2 * t) = make_float2(o[nd][0] * inv, o[nd][1] * inv);
-        if (t == 0) p.part_ml[sh * p.NP + part] = make_float2(m_g, l_g);
+        if (t == 0 && w == 0) p.part_ml[sh * p.NP + part] = make_float2(m_g, l_g);
     }
     __threadfence();
-    __syncwarp();
+    asm volatile("bar.sync 1, 64;" ::: "memory");  // both halves of every partial are out
+    if (w == 1) return;
     for (int r = 0; r < nm; ++r) {  // split members: the last partition to finish merges (finish_split)
         const int ctx_r = __shfl_sync(FULL, my_ctx, r);
         const int np_r = ctx_r > 0 ? (ctx_r + PT - 1) / PT : 1;
@@ -1766,7 +1810,7 @@ cudaError_t launch_group_mma(const GroupParams& p, int dtype, int num_seqs, size
         if (e != cudaSuccess) return e;
     }
     const dim3 grid(p.a.NP, p.a.H, (num_seqs + p.a.GM - 1) / p.a.GM);
-    return launch_k(kern, grid, dim3(64), smem, stream, p);
+    return launch_k(kern, grid, dim3(96), smem, stream, p);
 }
 
 // ==================================================================== debug gather ===

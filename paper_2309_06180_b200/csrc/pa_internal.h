@@ -62,6 +62,8 @@ struct AttnParams {
     int listed;                 // coop: CTAs take (sequence, partition) from the work list
     int natural;                // pcoop: items in grid order from context_lens (no work list)
     int STG;                    // tiles in flight per warp (shared-memory stages)
+    int GSL;                    // grouped decode: block slots per stage (a tile with more distinct
+                                // blocks than GSL takes several stages)
     // fused tensor-parallel all-gather (N2): when n_out_peers > 0 every output row of local
     // head h is stored to out_peers[k] + ((s * out_H) + out_h0 + h) * D for every rank k
     // (peer memory over NVLink) instead of `out`
@@ -145,7 +147,7 @@ size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int g
 // sched: 0 = grid, 1 = persistent, 2 = coop, 3 = persistent coop, 4 = sharing-aware groups, 5 = listed coop
 cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int sched, size_t smem,
                              cudaStream_t stream);
-size_t group_mma_smem_bytes(int gm, int stg);
+size_t group_mma_smem_bytes(int gm, int gsl, int stg, int pt);
 cudaError_t launch_group_mma(const GroupParams& p, int dtype, int num_seqs, size_t smem, cudaStream_t stream);
 size_t prefill_smem_bytes();
 cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, cudaStream_t stream);
