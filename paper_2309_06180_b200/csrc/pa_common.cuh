@@ -176,9 +176,46 @@ __device__ __forceinline__ float dot16<float>(const uint4& q, const uint4& k, fl
     return acc + (a.x + a.y);
 }
 
-// acc[0..EPC/2) += p * v  for one 16-byte chunk of V (EPC elements), fp32 pairs.
+// acc += p * (lo(v), hi(v)) for one packed 16-bit pair, p already in the storage dtype:
+// two mixed-precision FMAs (FHFMA: 16-bit operands, fp32 accumulator), no unpacking.
+__device__ __forceinline__ void fhfma_pv_f16(float2& acc, uint32_t v, unsigned short p) {
+    asm("{\n\t.reg .f16 vl, vh, pp;\n\tmov.b32 {vl, vh}, %2;\n\tmov.b16 pp, %3;\n\t"
+        "fma.rn.f32.f16 %0, vl, pp, %0;\n\tfma.rn.f32.f16 %1, vh, pp, %1;\n\t}"
+        : "+f"(acc.x), "+f"(acc.y)
+        : "r"(v), "h"(p));
+}
+__device__ __forceinline__ void fhfma_pv_bf16(float2& acc, uint32_t v, unsigned short p) {
+    asm("{\n\t.reg .b16 vl, vh;\n\tmov.b32 {vl, vh}, %2;\n\t"
+        "fma.rn.f32.bf16 %0, vl, %3, %0;\n\tfma.rn.f32.bf16 %1, vh, %3, %1;\n\t}"
+        : "+f"(acc.x), "+f"(acc.y)
+        : "r"(v), "h"(p));
+}
+
+// acc[0..EPC/2) += p * v  for one 16-byte chunk of V (EPC elements), fp32 accumulators.
+// 16-bit caches: the softmax weight p is rounded once to the storage dtype (RN) and
+// multiplied in FHFMA (as FlashAttention rounds P for its P.V product, DESIGN c25):
+// 8 instructions per chunk instead of 4 unpacks (8 HADD2.F32) + 4 FFMA2.  -DPA_PV_F32
+// restores the fp32-weight path (unpack + FFMA2) for A/B.
 template <typename T>
 __device__ __forceinline__ void axpy16(float2* acc, float p, const uint4& v);
+#ifndef PA_PV_F32
+template <>
+__device__ __forceinline__ void axpy16<__half>(float2* acc, float p, const uint4& v) {
+    const unsigned short ph = __half_as_ushort(__float2half_rn(p));
+    fhfma_pv_f16(acc[0], v.x, ph);
+    fhfma_pv_f16(acc[1], v.y, ph);
+    fhfma_pv_f16(acc[2], v.z, ph);
+    fhfma_pv_f16(acc[3], v.w, ph);
+}
+template <>
+__device__ __forceinline__ void axpy16<__nv_bfloat16>(float2* acc, float p, const uint4& v) {
+    const unsigned short pb = __bfloat16_as_ushort(__float2bfloat16_rn(p));
+    fhfma_pv_bf16(acc[0], v.x, pb);
+    fhfma_pv_bf16(acc[1], v.y, pb);
+    fhfma_pv_bf16(acc[2], v.z, pb);
+    fhfma_pv_bf16(acc[3], v.w, pb);
+}
+#else
 template <>
 __device__ __forceinline__ void axpy16<__half>(float2* acc, float p, const uint4& v) {
     const float2 pp = make_float2(p, p);
@@ -195,6 +232,7 @@ __device__ __forceinline__ void axpy16<__nv_bfloat16>(float2* acc, float p, cons
     acc[2] = ffma2(pp, unpack_bf16(v.z), acc[2]);
     acc[3] = ffma2(pp, unpack_bf16(v.w), acc[3]);
 }
+#endif
 template <>
 __device__ __forceinline__ void axpy16<float>(float2* acc, float p, const uint4& v) {
     const float2 pp = make_float2(p, p);
