@@ -179,6 +179,19 @@ def test_peaked_softmax_and_large_scores():
     assert np.max(np.abs(g - ref)) <= 5e-2
 
 
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("qmul", [1.0, 8.0])
+def test_peaked_softmax_16bit(dtype, qmul):
+    """16-bit caches, D=128: the P.V product multiplies the softmax weight rounded to the
+    storage dtype (DESIGN reading c25).  Flat and peaked (q x 8) softmax stay inside the
+    north-star tolerance against the fp64 oracle, across tiles and split partitions."""
+    wl = make_config("c1_tiny", dtype=dtype, D=128, H=4, H_kv=4, S=8, scale=qmul / 128 ** 0.5,
+                     kind="explicit", ctx=[1, 15, 16, 17, 100, 513, 1100, 2048], seed=1077)
+    out, *_ = gpu_step(wl)
+    ref, *_ = oracle_step(wl)
+    assert max_abs(out, ref) <= TOL[dtype]
+
+
 # ------------------------------------------------------------ cache kernels ---------
 
 def test_reshape_and_cache_prefill_shaped():
