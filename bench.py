@@ -119,6 +119,10 @@ def parse():
     ap.add_argument("--grouped", type=int, default=0,
                     help="sharing-aware decode on the tensor cores over groups of this many sequences "
                          "(SURVEY 8(f) N1; 0 = off, 'auto' sizes: C3 6, C5 4 via --grouped -1)")
+    ap.add_argument("--shared", type=int, default=-1,
+                    help="sharing-aware decode on the CUDA cores over groups of this many sequences "
+                         "(pa_paged_attention_decode_shared, SURVEY 8(f) N1; 0 = off (coop), -1 = auto: C5's "
+                         "beam groups of 4, where it measured faster than coop; coop elsewhere)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-prefill", action="store_true", help="skip the N4 prompt-phase context line")
     ap.add_argument("--extra", action="store_true", help="also print per-config lines for the other configs")
@@ -230,6 +234,12 @@ def run_ours(a, wl_full, world, rank, local):
     grouped = a.grouped if a.grouped >= 0 else {"c3_parallel": 6, "c3_fork": 6, "c5_beam": 4}.get(wl_full.name, 0)
     if grouped and (ftp is not None or a.unfused):
         raise SystemExit("--grouped runs the single-GPU fused decode step only")
+    auto_shared = {"c5_beam": 4}.get(wl_full.name, 0)
+    shared_g = a.shared if a.shared >= 0 else auto_shared
+    if ftp is not None or a.unfused or grouped:
+        if a.shared > 0:
+            raise SystemExit("--shared runs the single-GPU fused decode step only")
+        shared_g = 0
     stream = torch.cuda.current_stream(dev)
     ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
@@ -249,6 +259,9 @@ def run_ours(a, wl_full, world, rank, local):
         elif grouped:  # N1: groups of sequences sharing blocks, QK^T / PV on the tensor cores
             pa.paged_attention_decode_grouped(out, q, kn, vn, kc, vc, bt, cl, wl.scale, grouped, max_context_len=mcl,
                                               workspace=ws)
+        elif shared_g:  # N1: groups of sequences sharing blocks, each distinct block staged once
+            pa.paged_attention_decode_shared(out, q, kn, vn, kc, vc, bt, cl, wl.scale, shared_g, max_context_len=mcl,
+                                             workspace=ws)
         else:  # the decode step's cache write fused into the attention kernel
             pa.paged_attention_decode(out, q, kn, vn, kc, vc, bt, cl, wl.scale, max_context_len=mcl, workspace=ws)
         if i is not None:
@@ -312,7 +325,9 @@ def run_ours(a, wl_full, world, rank, local):
     attn_bytes_u = attn_bytes - sb["kv_logical"] + kv_unique
     achieved_u = attn_bytes_u / (attn_ms * 1e-3) / 1e9
     value = kv_all / (ms_step * 1e-3) / 1e9
-    traffic = load_traffic(wl_full.name + ("_grouped" if grouped else ""), world)
+    # ncu_traffic.json keys: the workload for its default kernel, _grouped / _coop otherwise
+    traffic = load_traffic(wl_full.name + ("_grouped" if grouped else "_coop" if auto_shared and not shared_g
+                                           else "_shared" if shared_g and not auto_shared else ""), world)
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms_step, "us_per_step": ms_step * 1e3, "higher_is_better": True,
@@ -323,7 +338,8 @@ def run_ours(a, wl_full, world, rank, local):
                    "mean_ctx": float(wl_full.context_lens.mean()), "max_ctx": int(wl_full.max_context_len),
                    "cow_pairs": int(len(wl_full.block_mapping)), "parallelism": f"tp{world}",
                    "tp_gather": tp_gather,
-                   "decode_kernel": f"grouped{grouped} (N1, tensor cores)" if grouped else "coop",
+                   "decode_kernel": (f"grouped{grouped} (N1, tensor cores)" if grouped else
+                                     f"shared{shared_g} (N1, CUDA cores)" if shared_g else "coop"),
                    "partition_tokens": a.partition_tokens or pa.DEFAULT_PARTITION_TOKENS,
                    "l2": "inputs larger than L2 (KV %.2f GB vs 126 MB L2); no flush" % (kv_all / 1e9)},
         "tokens_per_s": wl_full.S / (ms_step * 1e-3),
@@ -332,6 +348,8 @@ def run_ours(a, wl_full, world, rank, local):
         "roofline": {"bound": "hbm", "kernel": (f"paged_attention_group_mma_kernel (pa_paged_attention_decode_grouped, "
                                                  f"groups of {grouped}: shared blocks loaded once, QK^T and PV as "
                                                  f"tensor-core MMAs; cache write fused)") if grouped else
+                     (f"paged_attention_shared_kernel (pa_paged_attention_decode_shared, groups of {shared_g}: each "
+                      f"distinct block staged once for the group's members; cache write fused)") if shared_g else
                      "paged_attention_kernel (pa_paged_attention_decode: cache write + attention + split-context "
                      "merge in one launch)" if not a.unfused else "paged_attention_kernel (pa_paged_attention)",
                      "achieved": achieved_u if shared else achieved, "peak": peak, "peak_source": peak_src,

@@ -200,9 +200,20 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     if (const char* ev = getenv("PA_HPC")) nw = atoi(ev) > 0 ? atoi(ev) : nw;
     if (nw > 8) nw = 8;
     const int nkv_max = nw % G == 0 ? nw / G : (nw + G - 1) / G + 1;
-    if (sched == 4) nw = std::max(1, 4 / gm);  // gm * nw consumer warps per CTA
+    // sharing-aware (sched 4): gm * nw consumer warps per CTA (<= 8), stages of nsl
+    // distinct-block slots (a tile with more distinct blocks takes several stages);
+    // PA_SHARED_HPC / PA_SHARED_SLOTS override
+    // Defaults (measured): 8 consumer warps (gm members x 8/gm heads) and ONE
+    // slot per stage -- a tile whose members read d distinct blocks takes d stages, so a
+    // stage is never sized for the worst case and 4 x 16 KB stages fit 3 CTAs per SM.
+    int nsl = 1;
+    if (sched == 4) {
+        nw = std::max(1, 8 / gm);
+        if (const char* ev = getenv("PA_SHARED_HPC")) nw = std::max(1, std::min(8 / gm, atoi(ev)));
+        if (const char* ev = getenv("PA_SHARED_SLOTS")) nsl = std::max(1, std::min(gm, atoi(ev)));
+    }
     const int nkv_max4 = nw % G == 0 ? nw / G : (nw + G - 1) / G + 1;
-    const int stage = sched == 4 ? gm * 2 * nkv_max4 * 16 * rb : sched >= 2 ? 2 * nkv_max * 16 * rb : 2 * 16 * rb;
+    const int stage = sched == 4 ? nsl * 2 * nkv_max4 * 16 * rb : sched >= 2 ? 2 * nkv_max * 16 * rb : 2 * 16 * rb;
     // (sched 5 = listed coop shares the coop kernel and its shared-memory layout)
     int stg = sched >= 2 ? (64 * 1024) / stage : (64 * 1024) / (nw * stage);
     stg = stg < 2 ? 2 : (stg > 8 ? 8 : stg);
@@ -214,7 +225,7 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     if (const char* ev = getenv("PA_PPC")) ppc = atoi(ev) > 0 ? atoi(ev) : ppc;
     ppc = std::max(1, std::min(ppc, NP));
     if (sched == 5) ppc = 1;  // listed CTAs take single partitions
-    const size_t smem = sched == 4   ? pa::attention_smem_bytes_shared(rb, nw, G, stg, gm)
+    const size_t smem = sched == 4   ? pa::attention_smem_bytes_shared(rb, nw, G, stg, gm, nsl)
                         : (sched == 2 || sched == 5)
                             ? pa::attention_smem_bytes_coop(rb, nw, G, stg, PT * ppc, block_size, ppc, head_dim)
                         : sched == 3 ? pa::attention_smem_bytes_pcoop(rb, nw, G, stg, PT, block_size)
@@ -257,6 +268,7 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     p.HPW = 1;
     p.PPC = ppc;
     p.GM = gm;
+    p.GSL = nsl;
     p.S = num_seqs;
     p.listed = sched == 5;
     p.natural = natural ? 1 : 0;

@@ -1273,7 +1273,10 @@ __global__ void __launch_bounds__(288) paged_attention_shared_kernel(const AttnP
     const int NKVmax = HPC % G == 0 ? HPC / G : (HPC + G - 1) / G + 1;
     const int slab = kTile * RB;                          // one kv head x 16 rows
     const int slot_bytes = 2 * NKVmax * slab;             // K | V of the head group
-    const int stage_bytes = M * slot_bytes + 16 * ((M + 15) / 16) * 4;  // slots | member->slot map
+    const int NSL = p.GSL;                                // distinct-block slots per stage
+    // stage = NSL slots | header: member -> slot map [M], then the logical tile index
+    // (-1 = end of the partition's stream)
+    const int stage_bytes = NSL * slot_bytes + 16 * ((M + 16) / 16) * 4;
     const int s0 = grp * M, nm = min(M, p.S - s0);        // members of this group
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STG * stage_bytes);
     uint64_t* empty = full + STG;
@@ -1290,7 +1293,7 @@ __global__ void __launch_bounds__(288) paged_attention_shared_kernel(const AttnP
     const int p0 = part * PT;
     if (part > 0 && p0 >= gmax) return;  // no member reaches this partition (CTA-uniform)
     const int ntiles = (min(gmax, p0 + PT) - p0 + kTile - 1) / kTile;
-    auto slot_map = [&](int k) { return reinterpret_cast<int*>(smem + (size_t)k * stage_bytes + M * slot_bytes); };
+    auto slot_map = [&](int k) { return reinterpret_cast<int*>(smem + (size_t)k * stage_bytes + NSL * slot_bytes); };
 
     if (warp == NC) {  // ================================================ producer warp
         const int B = 1 << p.log2B;
@@ -1304,17 +1307,20 @@ __global__ void __launch_bounds__(288) paged_attention_shared_kernel(const AttnP
         const int my_tnew = (p.new_key != nullptr && lane < nm && my_ctx > 0 && my_p1 == my_ctx) ? my_ctx - 1 : -1;
         const int my_pc = my_tnew >= 0 ? my_tnew : my_p1;
         const int32_t* btrow = p.block_tables + (int64_t)my_s * p.W;
+        int n = 0;  // stages emitted so far
+        // block id of the member's next tile, loaded one tile ahead (its L2 round trip
+        // overlaps this tile's stage wait and copy issue)
+        int blk_next = (lane < nm && B >= kTile && p0 < my_p1) ? __ldg(btrow + (p0 >> p.log2B)) : -1;
         for (int j = 0; j < ntiles; ++j) {
-            const int k = j % STG;
-            if (j >= STG) mbar_wait(&empty[k], ((j / STG) - 1) & 1);
-            char* st = reinterpret_cast<char*>(smem) + (size_t)k * stage_bytes;
             const int tok0 = p0 + j * kTile;
+            const int blk_cur = blk_next;
+            if (lane < nm && B >= kTile && tok0 + kTile < my_p1) blk_next = __ldg(btrow + ((tok0 + kTile) >> p.log2B));
             // per member: block id, rows needed, whether the tile holds its new token
             const bool act = lane < nm && tok0 < my_p1;
             const int rows = act ? max(0, min(kTile, my_pc - tok0)) : 0;
             const bool has_new = act && my_tnew >= tok0 && my_tnew < tok0 + kTile;
             // B >= 16: one block per tile; B < 16: a tile spans several blocks -> no sharing
-            const int blk = (act && rows > 0 && B >= kTile) ? __ldg(btrow + (tok0 >> p.log2B)) : -1;
+            const int blk = (act && rows > 0 && B >= kTile) ? blk_cur : -1;
             const bool shareable = act && !has_new && B >= kTile && rows > 0;
             // leader = first member with the same block (shareable tiles only)
             int leader = lane;
@@ -1328,57 +1334,79 @@ __global__ void __launch_bounds__(288) paged_attention_shared_kernel(const AttnP
             const int my_slot_if_leader = __popc(leaders & ((1u << lane) - 1u));
             const int slot = __shfl_sync(0xffffffffu, my_slot_if_leader, leader);
             // rows a shared slot must hold: the largest need among its members
+            // (a match.any / redux.sync version of this leader search measured 60% slower)
             int need = rows;
             for (int m = 0; m < nm; ++m) {
                 const int lm = __shfl_sync(0xffffffffu, leader, m);
                 const int rm = __shfl_sync(0xffffffffu, rows, m);
                 if (is_leader && lm == lane) need = max(need, rm);
             }
-            const uint32_t my_tx = is_leader ? (uint32_t)(2 * NKV * (need + (has_new ? 1 : 0)) * RB) : 0u;
-            uint32_t tx = my_tx;
+            const int nd = __popc(leaders);  // distinct slots the tile needs
+            for (int r0 = 0; r0 < nd; r0 += NSL) {  // one stage per NSL distinct blocks
+                const int k = n % STG;
+                if (n >= STG) mbar_wait(&empty[k], ((n / STG) - 1) & 1);
+                char* st = reinterpret_cast<char*>(smem) + (size_t)k * stage_bytes;
+                const bool mine = is_leader && my_slot_if_leader >= r0 && my_slot_if_leader < r0 + NSL;
+                const uint32_t my_tx = mine ? (uint32_t)(2 * NKV * (need + (has_new ? 1 : 0)) * RB) : 0u;
+                uint32_t tx = my_tx;
 #pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, off);
-            if (lane < M) slot_map(k)[lane] = act ? slot : -1;
-            __syncwarp();
-            if (lane == 0) mbar_arrive_expect_tx(&full[k], tx);  // also publishes the slot map
-            __syncwarp();
-            if (is_leader) {
-                char* sK = st + (size_t)my_slot_if_leader * slot_bytes;
-                char* sV = sK + NKVmax * slab;
-                if (need > 0) {
-                    if (B >= kTile) {
-                        if (B == kTile && need == kTile) {  // NKV contiguous head slabs of one block
-                            const int64_t off = (int64_t)blk * blk_bytes + (int64_t)kvh0 * slab;
-                            bulk_g2s(sK, kc + off, (uint32_t)(NKV * slab), &full[k]);
-                            bulk_g2s(sV, vc + off, (uint32_t)(NKV * slab), &full[k]);
+                for (int off = 16; off >= 1; off >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, off);
+                if (lane < M) slot_map(k)[lane] = (act && slot >= r0 && slot < r0 + NSL) ? slot - r0 : -1;
+                if (lane == 0) slot_map(k)[M] = j;
+                __syncwarp();
+                if (lane == 0) mbar_arrive_expect_tx(&full[k], tx);  // also publishes the header
+                __syncwarp();
+                if (mine) {
+                    char* sK = st + (size_t)(my_slot_if_leader - r0) * slot_bytes;
+                    char* sV = sK + NKVmax * slab;
+                    if (need > 0) {
+                        if (B >= kTile) {
+                            if (B == kTile && need == kTile) {  // NKV contiguous head slabs of one block
+                                const int64_t off = (int64_t)blk * blk_bytes + (int64_t)kvh0 * slab;
+                                bulk_g2s(sK, kc + off, (uint32_t)(NKV * slab), &full[k]);
+                                bulk_g2s(sV, vc + off, (uint32_t)(NKV * slab), &full[k]);
+                            } else {
+                                for (int kh = 0; kh < NKV; ++kh) {
+                                    const int64_t off = (int64_t)blk * blk_bytes +
+                                                        ((int64_t)(kvh0 + kh) << p.log2B) * RB +
+                                                        (int64_t)(tok0 & (B - 1)) * RB;
+                                    bulk_g2s(sK + kh * slab, kc + off, (uint32_t)(need * RB), &full[k]);
+                                    bulk_g2s(sV + kh * slab, vc + off, (uint32_t)(need * RB), &full[k]);
+                                }
+                            }
                         } else {
-                            for (int kh = 0; kh < NKV; ++kh) {
-                                const int64_t off = (int64_t)blk * blk_bytes + ((int64_t)(kvh0 + kh) << p.log2B) * RB +
-                                                    (int64_t)(tok0 & (B - 1)) * RB;
-                                bulk_g2s(sK + kh * slab, kc + off, (uint32_t)(need * RB), &full[k]);
-                                bulk_g2s(sV + kh * slab, vc + off, (uint32_t)(need * RB), &full[k]);
-                            }
+                            for (int kh = 0; kh < NKV; ++kh)
+                                for (int tk = tok0; tk < tok0 + need; tk += B) {
+                                    const int b2 = __ldg(btrow + (tk >> p.log2B));
+                                    const int r2 = min(B, tok0 + need - tk);
+                                    const int64_t off =
+                                        (int64_t)b2 * blk_bytes + ((int64_t)(kvh0 + kh) << p.log2B) * RB;
+                                    bulk_g2s(sK + kh * slab + (tk - tok0) * RB, kc + off, (uint32_t)(r2 * RB),
+                                             &full[k]);
+                                    bulk_g2s(sV + kh * slab + (tk - tok0) * RB, vc + off, (uint32_t)(r2 * RB),
+                                             &full[k]);
+                                }
                         }
-                    } else {
-                        for (int kh = 0; kh < NKV; ++kh)
-                            for (int tk = tok0; tk < tok0 + need; tk += B) {
-                                const int b2 = __ldg(btrow + (tk >> p.log2B));
-                                const int r2 = min(B, tok0 + need - tk);
-                                const int64_t off = (int64_t)b2 * blk_bytes + ((int64_t)(kvh0 + kh) << p.log2B) * RB;
-                                bulk_g2s(sK + kh * slab + (tk - tok0) * RB, kc + off, (uint32_t)(r2 * RB), &full[k]);
-                                bulk_g2s(sV + kh * slab + (tk - tok0) * RB, vc + off, (uint32_t)(r2 * RB), &full[k]);
-                            }
                     }
+                    if (has_new)
+                        for (int kh = 0; kh < NKV; ++kh) {
+                            const int64_t src = ((int64_t)my_s * p.H_kv + kvh0 + kh) * RB;
+                            const int dst = kh * slab + (my_tnew - tok0) * RB;
+                            bulk_g2s(sK + dst, static_cast<const char*>(p.new_key) + src, RB, &full[k]);
+                            bulk_g2s(sV + dst, static_cast<const char*>(p.new_value) + src, RB, &full[k]);
+                        }
                 }
-                if (has_new)
-                    for (int kh = 0; kh < NKV; ++kh) {
-                        const int64_t src = ((int64_t)my_s * p.H_kv + kvh0 + kh) * RB;
-                        const int dst = kh * slab + (my_tnew - tok0) * RB;
-                        bulk_g2s(sK + dst, static_cast<const char*>(p.new_key) + src, RB, &full[k]);
-                        bulk_g2s(sV + dst, static_cast<const char*>(p.new_value) + src, RB, &full[k]);
-                    }
+                __syncwarp();
+                ++n;
             }
-            __syncwarp();
+        }
+        {  // end-of-stream stage: header only
+            const int k = n % STG;
+            if (n >= STG) mbar_wait(&empty[k], ((n / STG) - 1) & 1);
+            if (lane == 0) {
+                slot_map(k)[M] = -1;
+                mbar_arrive_expect_tx(&full[k], 0u);
+            }
         }
         return;
     }
@@ -1401,11 +1429,13 @@ __global__ void __launch_bounds__(288) paged_attention_shared_kernel(const AttnP
     float2 acc[EPC];
 #pragma unroll
     for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
-    for (int j = 0; j < ntiles; ++j) {
-        const int k = j % STG;
-        mbar_wait(&full[k], (j / STG) & 1);
-        if (active && j < my_ntiles) {
-            const int slot = slot_map(k)[mem];
+    for (int n = 0;; ++n) {  // the producer's stage stream, ended by tile index -1
+        const int k = n % STG;
+        mbar_wait(&full[k], (n / STG) & 1);
+        const int j = slot_map(k)[M];
+        if (j < 0) break;
+        const int slot = slot_map(k)[mem];
+        if (active && j < my_ntiles && slot >= 0) {
             const char* sK = reinterpret_cast<const char*>(smem) + (size_t)k * stage_bytes + (size_t)slot * slot_bytes +
                              kh * slab;
             const char* sV = sK + NKVmax * slab;
@@ -1879,9 +1909,9 @@ size_t attention_smem_bytes_pcoop(int row_bytes, int hpc, int G, int stg, int pa
     return (size_t)stg * stage + 16 * (size_t)stg + tbl;
 }
 
-size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int gm) {
+size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int gm, int nsl) {
     const int nkv_max = hpc % G == 0 ? hpc / G : (hpc + G - 1) / G + 1;
-    const size_t stage = (size_t)gm * 2 * nkv_max * kTile * row_bytes + 16 * (size_t)((gm + 15) / 16) * 4;
+    const size_t stage = (size_t)nsl * 2 * nkv_max * kTile * row_bytes + 16 * (size_t)((gm + 16) / 16) * 4;
     return (size_t)stg * stage + 16 * (size_t)stg;
 }
 

@@ -62,7 +62,7 @@ struct AttnParams {
     int listed;                 // coop: CTAs take (sequence, partition) from the work list
     int natural;                // pcoop: items in grid order from context_lens (no work list)
     int STG;                    // tiles in flight per warp (shared-memory stages)
-    int GSL;                    // grouped decode: block slots per stage (a tile with more distinct
+    int GSL;                    // grouped / shared decode: block slots per stage (a tile with more distinct
                                 // blocks than GSL takes several stages)
     // fused tensor-parallel all-gather (N2): when n_out_peers > 0 every output row of local
     // head h is stored to out_peers[k] + ((s * out_H) + out_h0 + h) * D for every rank k
@@ -143,7 +143,7 @@ size_t attention_smem_bytes(bool persistent, int row_bytes, int nw, int stg, int
 size_t attention_smem_bytes_coop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size,
                                  int ppc, int head_dim);
 size_t attention_smem_bytes_pcoop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size);
-size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int gm);
+size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int gm, int nsl);
 // sched: 0 = grid, 1 = persistent, 2 = coop, 3 = persistent coop, 4 = sharing-aware groups, 5 = listed coop
 cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int sched, size_t smem,
                              cudaStream_t stream);

@@ -29,9 +29,10 @@ def main():
     tag, cfgs = sys.argv[1], sys.argv[2:]
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     d = json.load(open(path)) if os.path.exists(path) else {}
-    d["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel "
-                  "(paged_attention_coop_kernel), one ncu --set full capture per round "
-                  f"(profiles/{tag}_<workload>_attention_ncu_details.txt); keyed by workload then n_gpus")
+    d["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel of bench.py's "
+                  "default path for the workload (paged_attention_coop_kernel; paged_attention_shared_kernel for "
+                  "c5_beam, whose coop figure is c5_beam_coop), one ncu --set full capture per round "
+                  f"(profiles/{tag}_<workload>[_coop]_attention_ncu_details.txt); keyed by workload then n_gpus")
     for c in cfgs:
         rep = os.path.join(ROOT, "gpurun_out", f"prof_attn_{c}_{tag}.ncu-rep")
         if os.path.exists(rep):

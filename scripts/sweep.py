@@ -42,6 +42,8 @@ def main():
             os.environ["PA_HPC"], os.environ["PA_STG"] = str(hpc), str(stg)
             os.environ["PA_HPW"] = str(hpw)
             os.environ["PA_PPC"] = str(hpw)  # 4th field doubles as coop partitions-per-CTA
+            if sched.startswith("shared"):  # sharedG: heads per CTA and block slots per stage
+                os.environ["PA_SHARED_HPC"], os.environ["PA_SHARED_SLOTS"] = str(hpc), str(hpw)
             ws = torch.zeros(max(16, pa.paged_attention_workspace_size(wl.S, wl.H, wl.D, wl.max_context_len, pt)),
                              dtype=torch.uint8, device="cuda")
 
@@ -78,7 +80,7 @@ def main():
             print(json.dumps({"config": name, "sched": sched, "hpc": hpc, "stg": stg, "hpw": hpw, "pt": pt,
                               "us": round(us, 2),
                               "kv_GBps": round(kv / us / 1e3, 1)}), flush=True)
-        for k in ("PA_HPC", "PA_STG", "PA_HPW", "PA_SCHED", "PA_PPC"):
+        for k in ("PA_HPC", "PA_STG", "PA_HPW", "PA_SCHED", "PA_PPC", "PA_SHARED_HPC", "PA_SHARED_SLOTS"):
             os.environ.pop(k, None)
         del x
 

@@ -542,13 +542,21 @@ def test_partitions_per_cta_bitwise_identical(name, monkeypatch):
             assert torch.equal(kc.view(torch.int16), ref[1].view(torch.int16)), ppc
 
 
-@pytest.mark.parametrize("name,gs", [("c5_beam", 4), ("c3_parallel", 6), ("c3_fork", 6), ("c2_sharegpt", 4),
-                                     ("c5_beam", 3), ("c3_parallel", 8)])
-def test_shared_decode_bitwise_equals_decode(name, gs):
+@pytest.mark.parametrize("name,gs,hpc,slots", [("c5_beam", 4, 0, 0), ("c3_parallel", 6, 0, 0), ("c3_fork", 6, 0, 0),
+                                               ("c2_sharegpt", 4, 0, 0), ("c5_beam", 3, 0, 0), ("c3_parallel", 8, 0, 0),
+                                               ("c5_beam", 4, 2, 1), ("c5_beam", 4, 1, 2), ("c3_fork", 6, 1, 1),
+                                               ("c3_parallel", 4, 2, 3), ("c2_sharegpt", 2, 4, 1)])
+def test_shared_decode_bitwise_equals_decode(name, gs, hpc, slots, monkeypatch):
     """N1 sharing-aware entry: every distinct block of a sequence group is loaded once;
     outputs and cache bytes bit-identical to pa_paged_attention_decode at full size,
-    including groups that do not align with the requests (gs 3 / 8)."""
+    including groups that do not align with the requests (gs 3 / 8), several heads per
+    CTA, and stages with fewer block slots than members (a tile's distinct blocks then
+    stream through several stages)."""
     import paper_2309_06180_b200 as pa
+    if hpc:
+        monkeypatch.setenv("PA_SHARED_HPC", str(hpc))
+    if slots:
+        monkeypatch.setenv("PA_SHARED_SLOTS", str(slots))
     wl = make_config(name)
     x = materialize_torch(wl, "cuda")
     tb = tables_torch(wl, "cuda")
@@ -565,9 +573,11 @@ def test_shared_decode_bitwise_equals_decode(name, gs):
     assert torch.equal(bits_t(ka), bits_t(y["key_cache"])) and torch.equal(bits_t(va), bits_t(y["value_cache"]))
 
 
-@pytest.mark.parametrize("B", [1, 16, 32])
-def test_shared_decode_small_vs_oracle(B):
+@pytest.mark.parametrize("B,slots", [(1, 0), (16, 0), (32, 0), (16, 1), (8, 2)])
+def test_shared_decode_small_vs_oracle(B, slots, monkeypatch):
     import paper_2309_06180_b200 as pa
+    if slots:
+        monkeypatch.setenv("PA_SHARED_SLOTS", str(slots))
     wl = make_config("c5_beam", S=14, H=4, H_kv=4, B=B)
     x = materialize_torch(wl, "cuda")
     tb = tables_torch(wl, "cuda")
