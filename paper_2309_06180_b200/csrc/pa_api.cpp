@@ -215,7 +215,8 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     const int nkv_max4 = nw % G == 0 ? nw / G : (nw + G - 1) / G + 1;
     const int stage = sched == 4 ? nsl * 2 * nkv_max4 * 16 * rb : sched >= 2 ? 2 * nkv_max * 16 * rb : 2 * 16 * rb;
     // (sched 5 = listed coop shares the coop kernel and its shared-memory layout)
-    int stg = sched >= 2 ? (64 * 1024) / stage : (64 * 1024) / (nw * stage);
+    // (sharing-aware: 48 KB of stages, so 4 CTAs fit in shared memory as in registers)
+    int stg = sched == 4 ? (48 * 1024) / stage : sched >= 2 ? (64 * 1024) / stage : (64 * 1024) / (nw * stage);
     stg = stg < 2 ? 2 : (stg > 8 ? 8 : stg);
     if (const char* ev = getenv("PA_STG")) stg = atoi(ev) > 0 ? atoi(ev) : stg;
     // coop: partitions per CTA (scheduling only: the arithmetic partition stays PT and a

@@ -1258,8 +1258,12 @@ __global__ void __launch_bounds__(288) paged_attention_pcoop_kernel(const AttnPa
 // publishes the member -> slot map with the stage: a block shared by the whole group
 // crosses L2 -> SM once instead of M times.  Tiles holding a member's new token are
 // never shared (copy-on-write made that block private).
+#ifndef PA_SHARED_MINB
+#define PA_SHARED_MINB 4  // register cap for 4 CTAs/SM (56 regs): c5 470-476 vs 475-486 us at 72 regs
+                          // (no cap: 102 regs, 2 CTAs/SM, 930 us)
+#endif
 template <typename T, int D>
-__global__ void __launch_bounds__(288) paged_attention_shared_kernel(const AttnParams p) {
+__global__ void __launch_bounds__(288, PA_SHARED_MINB) paged_attention_shared_kernel(const AttnParams p) {
     using C = AttnCfg<T, D>;
     constexpr int RB = C::RB, LT = C::LT, EPC = C::EPC;
     extern __shared__ __align__(128) unsigned char smem[];
