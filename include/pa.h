@@ -123,7 +123,7 @@ pa_status_t pa_paged_attention_decode(void* out, const void* query, const void* 
  * A CTA (partition, 8/group_size query heads, one group) streams ONE distinct block per
  * shared-memory stage, so a logical tile costs one stage when the members share its
  * block and d stages when they read d different blocks: faster than the plain entry when
- * the members share most blocks (beam search, C5: 504 vs 561 us), slower when they
+ * the members share most blocks (beam search, C5: 498 vs 561 us), slower when they
  * diverge (parallel samples after the fork, C3) -- the caller chooses per batch.
  * ---------------------------------------------------------------------------------- */
 pa_status_t pa_paged_attention_decode_shared(void* out, const void* query, const void* key,
