@@ -64,7 +64,10 @@ int log2_pow2(int b) {  // -1 if not a power of two in [1, 256]
     } while (0)
 
 int effective_partition(int partition_tokens) {
-    return partition_tokens == 0 ? PA_DEFAULT_PARTITION_TOKENS : partition_tokens;
+    if (partition_tokens != 0) return partition_tokens;
+    // PA_PT (A/B knob only, not a tuning default): the default partition for callers that pass 0
+    if (const char* ev = getenv("PA_PT")) return atoi(ev) > 0 ? atoi(ev) : PA_DEFAULT_PARTITION_TOKENS;
+    return PA_DEFAULT_PARTITION_TOKENS;
 }
 
 int64_t pad16(int64_t x) { return (x + 15) / 16 * 16; }
