@@ -275,6 +275,8 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     p.GSL = nsl;
     p.S = num_seqs;
     p.listed = sched == 5;
+    p.pz = 0;
+    if (const char* ev = getenv("PA_PZ")) p.pz = atoi(ev) > 0 ? 1 : 0;
     p.natural = natural ? 1 : 0;
     if (const char* ev = getenv("PA_HPW")) p.HPW = atoi(ev) > 0 ? atoi(ev) : 1;
     if (tp != nullptr) {

@@ -828,11 +828,11 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
         c0 = it.y;
         ctx = it.z;
     } else {
-        hg = blockIdx.y;
-        s = blockIdx.z;
+        hg = p.pz ? blockIdx.x : blockIdx.y;
+        s = p.pz ? blockIdx.y : blockIdx.z;
         // this CTA walks the arithmetic partitions [c0, c0 + PPC) of the context back to
         // back; each is finished exactly as if it had its own CTA (bitwise identical)
-        c0 = blockIdx.x * p.PPC;
+        c0 = (p.pz ? blockIdx.z : blockIdx.x) * p.PPC;
         // the partition's first 32 block ids depend only on (s, c0): the producer loads
         // them (in-row entries past the context are read, never used) in parallel with
         // context_lens[s] instead of after it -- one dependent global round trip less
@@ -2009,6 +2009,9 @@ static cudaError_t launch_attention_t(const AttnParams& p, int num_seqs, int sch
             if (e != cudaSuccess) return e;
         }
         const int groups = (p.H + p.HPC - 1) / p.HPC;
+        if (p.pz)  // partition index slowest: partitions >= 1 (and the empty ones) launch last
+            return launch_k(kern, dim3(groups, num_seqs, (p.NP + p.PPC - 1) / p.PPC), dim3((p.HPC + 1) * 32), smem,
+                            stream, p);
         return launch_k(kern, dim3((p.NP + p.PPC - 1) / p.PPC, groups, num_seqs), dim3((p.HPC + 1) * 32), smem,
                         stream, p);
     }

@@ -60,6 +60,7 @@ struct AttnParams {
     int GM;                     // sharing-aware scheduler: sequences per group
     int S;                      // number of sequences
     int listed;                 // coop: CTAs take (sequence, partition) from the work list
+    int pz;                     // coop: grid (head group, sequence, partition), partitions slowest
     int natural;                // pcoop: items in grid order from context_lens (no work list)
     int STG;                    // tiles in flight per warp (shared-memory stages)
     int GSL;                    // grouped / shared decode: block slots per stage (a tile with more distinct
