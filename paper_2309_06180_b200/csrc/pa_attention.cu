@@ -1618,8 +1618,17 @@ __global__ void __launch_bounds__(96) paged_attention_group_mma_kernel(const __g
             const int rows = act ? min(kTile, my_p1 - tok0) : 0;
             const bool shareable = act && !has_new;  // a new-token tile is private (CoW)
             // leader = lowest member reading the same block (unshareable members lead themselves)
+#ifdef PA_GROUP_MATCH
             const unsigned same = __match_any_sync(FULL, shareable ? blk : -2 - lane);
             const int leader = __ffs(same) - 1;
+#else  // shuffle loop: measured faster than match.any in the CUDA-core shared kernel (§7)
+            int leader = lane;
+            for (int m = 0; m < nm; ++m) {
+                const int bm = __shfl_sync(FULL, blk, m);
+                const bool sm = __shfl_sync(FULL, shareable, m);
+                if (shareable && sm && bm == blk && m < leader) leader = m;
+            }
+#endif
             const bool is_leader = act && leader == lane;
             const unsigned leaders = __ballot_sync(FULL, is_leader);
             const int my_slot = __popc(leaders & ((1u << lane) - 1u));
