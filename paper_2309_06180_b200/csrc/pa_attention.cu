@@ -1558,8 +1558,11 @@ __device__ __forceinline__ void gwait(uint64_t* bar, uint32_t parity, int tag, i
 #define GWAIT(bar, par, tag, j) mbar_wait(bar, par)
 #endif
 
+#ifndef PA_GROUP_MINB
+#define PA_GROUP_MINB 6  // register cap (113) for 6 CTAs/SM: c5 644 -> 514 us (uncapped 138 regs, 4 CTAs/SM)
+#endif
 template <typename T>
-__global__ void __launch_bounds__(96) paged_attention_group_mma_kernel(const __grid_constant__ GroupParams gp) {
+__global__ void __launch_bounds__(96, PA_GROUP_MINB) paged_attention_group_mma_kernel(const __grid_constant__ GroupParams gp) {
     constexpr int D = 128, RB = 256;
     constexpr bool BF = std::is_same<T, __nv_bfloat16>::value;
     constexpr unsigned FULL = 0xffffffffu;
