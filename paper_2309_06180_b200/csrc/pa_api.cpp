@@ -456,7 +456,12 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
     if (const char* ev = getenv("PA_GROUP_STG")) stg = atoi(ev) > 0 ? atoi(ev) : stg;
     p.STG = stg;
     p.GSL = gsl;
-    const size_t smem = pa::group_mma_smem_bytes(group_size, gsl, stg, PT);
+    // heads per CTA (one consumer-warp pair each; 2 when the head count allows): PA_GROUP_HG
+    int hg = 2;  // c5 515 vs 523 us with one head per CTA
+    if (const char* ev = getenv("PA_GROUP_HG")) hg = atoi(ev) == 2 ? 2 : 1;
+    if (num_heads % hg != 0) hg = 1;
+    p.HPC = hg;
+    const size_t smem = pa::group_mma_smem_bytes(group_size, gsl, stg, PT, hg);
     if (smem > 227 * 1024) return fail(PA_ERR_UNSUPPORTED, "group_size %d needs %zu B of shared memory", group_size, smem);
     cudaError_t e = pa::launch_group_mma(gp, (int)dtype, num_seqs, smem, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "paged_attention_group_mma_kernel launch");

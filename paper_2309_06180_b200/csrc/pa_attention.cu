@@ -1464,8 +1464,9 @@ __global__ void __launch_bounds__(288, PA_SHARED_MINB) paged_attention_shared_ke
 // ============================ sharing-aware decode on the tensor cores (N1, mma.sync) ===
 //
 // The sequences of one group (a request's parallel samples or beams) share
-// most physical blocks.  One CTA = (partition, query head, group of M <= 8 sequences);
-// warp 1 = producer, warp 0 = consumer.  The producer maps each 16-token logical tile of
+// most physical blocks.  One CTA = (partition, HG = 1 or 2 query heads, group of M <= 8
+// sequences); per head a pair of consumer warps (each owning half of the head dimension
+// for P V), then one producer warp.  The producer maps each 16-token logical tile of
 // the M members to their physical blocks and TMA-loads every DISTINCT block once (K and
 // V, two 64-column boxes each, 128-byte swizzle) into a slot of the stage.  The consumer
 // computes S = Q K^T for all members at once as an m16n8k16 tensor-core product (rows =
@@ -1531,8 +1532,8 @@ constexpr int kGroupSlot = 8192;  // K | V of one block x one kv head x 16 token
 
 // per stage: gm slots | barriers | tile metadata (slot per member, slot count, new-token
 // member mask, rows needed per slot)
-size_t group_mma_smem_bytes(int gm, int gsl, int stg, int pt) {
-    return 1024 + (size_t)stg * gsl * kGroupSlot + 16 * (size_t)stg + 4 * (size_t)stg * (gm + 3 + gsl) +
+size_t group_mma_smem_bytes(int gm, int gsl, int stg, int pt, int hg) {
+    return 1024 + (size_t)stg * gsl * hg * kGroupSlot + 16 * (size_t)stg + 4 * (size_t)stg * (gm + 3 + gsl) +
            4 * (size_t)gm * (pt / kTile) + 16;
 }
 
@@ -1558,11 +1559,14 @@ __device__ __forceinline__ void gwait(uint64_t* bar, uint32_t parity, int tag, i
 #define GWAIT(bar, par, tag, j) mbar_wait(bar, par)
 #endif
 
+#ifndef PA_GROUP_MINB_HG
+#define PA_GROUP_MINB_HG 4  // two heads per CTA (160 threads)
+#endif
 #ifndef PA_GROUP_MINB
 #define PA_GROUP_MINB 6  // register cap (113) for 6 CTAs/SM: c5 644 -> 514 us (uncapped 138 regs, 4 CTAs/SM)
 #endif
-template <typename T>
-__global__ void __launch_bounds__(96, PA_GROUP_MINB) paged_attention_group_mma_kernel(const __grid_constant__ GroupParams gp) {
+template <typename T, int HG>
+__global__ void __launch_bounds__(32 * (2 * HG + 1), HG == 1 ? PA_GROUP_MINB : PA_GROUP_MINB_HG) paged_attention_group_mma_kernel(const __grid_constant__ GroupParams gp) {
     constexpr int D = 128, RB = 256;
     constexpr bool BF = std::is_same<T, __nv_bfloat16>::value;
     constexpr unsigned FULL = 0xffffffffu;
@@ -1570,12 +1574,13 @@ __global__ void __launch_bounds__(96, PA_GROUP_MINB) paged_attention_group_mma_k
     extern __shared__ __align__(1024) unsigned char gsmem_raw[];
     unsigned char* smem =
         reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsmem_raw) + 1023) & ~(uintptr_t)1023);
-    const int part = blockIdx.x, h = blockIdx.y, grp = blockIdx.z;
+    const int part = blockIdx.x, grp = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int M = p.GM, STG = p.STG, PT = p.PT, GSL = p.GSL;
-    const int stage_bytes = GSL * kGroupSlot;
+    const int stage_bytes = GSL * HG * kGroupSlot;
     const int s0 = grp * M, nm = min(M, p.S - s0);
-    const int kvh = h / p.G;
+    const int hid = warp < 2 * HG ? warp >> 1 : 0;  // consumer pair -> head of the CTA
+    const int h = blockIdx.y * HG + hid, kvh = h / p.G;
     // metadata per stage: [0, M) slot of member m in this stage (-1: none), [M] slots,
     // [M+1] new-token members, [M+2] tile start (-1: end of the partition), [M+3, +GSL) rows
     // each slot's members read
@@ -1586,7 +1591,7 @@ __global__ void __launch_bounds__(96, PA_GROUP_MINB) paged_attention_group_mma_k
     int* sbt = meta + STG * MW;                        // [M][PT / 16] block id of member m's tile j
     if (threadIdx.x < STG) {
         mbar_init(&full[threadIdx.x], 1);
-        mbar_init(&empty[threadIdx.x], 2);  // both consumer warps release a stage
+        mbar_init(&empty[threadIdx.x], 2 * HG);  // both consumer warps of every head release a stage
     }
     fence_mbar_init();
     __syncthreads();
@@ -1603,7 +1608,7 @@ __global__ void __launch_bounds__(96, PA_GROUP_MINB) paged_attention_group_mma_k
     const int my_tnew = (p.new_key != nullptr && lane < nm && my_ctx > 0 && my_p1 == my_ctx) ? my_ctx - 1 : -1;
     const int B = 1 << p.log2B;
 
-    if (warp == 2) {  // ================================================ producer warp
+    if (warp == 2 * HG) {  // ================================================ producer warp
         // every member's block ids of the partition, loaded in parallel up front
         const int TPP = PT / kTile;
         for (int i = lane; i < nm * TPP; i += 32) {
@@ -1658,15 +1663,19 @@ __global__ void __launch_bounds__(96, PA_GROUP_MINB) paged_attention_group_mma_k
                     mt[M + 2] = tok0;
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive_expect_tx(&full[k], (uint32_t)min(GSL, d - pass0) * kGroupSlot);
+                if (lane == 0) mbar_arrive_expect_tx(&full[k], (uint32_t)(min(GSL, d - pass0) * HG * kGroupSlot));
                 __syncwarp();
                 if (is_leader && in) {
-                    unsigned char* sl = smem + (size_t)k * stage_bytes + (size_t)(my_slot - pass0) * kGroupSlot;
-                    const int row = ((blk * p.H_kv + kvh) << p.log2B) + (tok0 & (B - 1));
-                    tma_box(sl, &gp.tmap_k, 0, row, &full[k]);
-                    tma_box(sl + 2048, &gp.tmap_k, 64, row, &full[k]);
-                    tma_box(sl + 4096, &gp.tmap_v, 0, row, &full[k]);
-                    tma_box(sl + 6144, &gp.tmap_v, 64, row, &full[k]);
+                    unsigned char* sl = smem + (size_t)k * stage_bytes + (size_t)(my_slot - pass0) * HG * kGroupSlot;
+#pragma unroll
+                    for (int hi = 0; hi < HG; ++hi) {  // the CTA's heads: one K|V box set each
+                        const int row = ((blk * p.H_kv + (blockIdx.y * HG + hi) / p.G) << p.log2B) + (tok0 & (B - 1));
+                        unsigned char* slh = sl + hi * kGroupSlot;
+                        tma_box(slh, &gp.tmap_k, 0, row, &full[k]);
+                        tma_box(slh + 2048, &gp.tmap_k, 64, row, &full[k]);
+                        tma_box(slh + 4096, &gp.tmap_v, 0, row, &full[k]);
+                        tma_box(slh + 6144, &gp.tmap_v, 64, row, &full[k]);
+                    }
                 }
                 __syncwarp();
             }
@@ -1681,10 +1690,10 @@ __global__ void __launch_bounds__(96, PA_GROUP_MINB) paged_attention_group_mma_k
         return;
     }
 
-    // ============================================================= consumer warps 0, 1
+    // ====================================== consumer warps 2*hid, 2*hid + 1 (head h0 + hid)
     // Both compute S for all members; warp w accumulates P V for dims [64w, 64w + 64) only.
     // Fragment coordinates: row g (= member g; rows g + 8 are unused), column pair 2t, 2t+1.
-    const int w = warp;
+    const int w = warp & 1;
     const int g = lane >> 2, t = lane & 3;
     const bool row_ok = g < nm;
     const int s_g = s0 + min(g, nm - 1);
@@ -1725,7 +1734,7 @@ __global__ void __launch_bounds__(96, PA_GROUP_MINB) paged_attention_group_mma_k
                                                 static_cast<const char*>(isv ? p.new_value : p.new_key) +
                                                 ((int64_t)(s0 + m) * p.H_kv + kvh) * RB) +
                                             ch);
-                    *reinterpret_cast<uint4*>(st + (size_t)sl * kGroupSlot + (isv ? 4096 : 0) + swz(r, ch)) = val;
+                    *reinterpret_cast<uint4*>(st + ((size_t)sl * HG + hid) * kGroupSlot + (isv ? 4096 : 0) + swz(r, ch)) = val;
                     if (h % p.G == 0) {  // the cache slot, once per kv head
                         const int blk = __ldg(p.block_tables + (int64_t)(s0 + m) * p.W + (tn >> p.log2B));
                         const int64_t off = ((((int64_t)blk * p.H_kv + kvh) << p.log2B) + (tn & (B - 1))) * RB;
@@ -1734,20 +1743,20 @@ __global__ void __launch_bounds__(96, PA_GROUP_MINB) paged_attention_group_mma_k
                     }
                 }
             }
-            asm volatile("bar.sync 1, 64;" ::: "memory");  // both K halves in place before S
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + hid) : "memory");  // both K halves in place before S
         }
         // V rows of this warp's half that no member of a slot reads: finite (zero) for P V
         for (int sl = 0; sl < nslots; ++sl) {
             const int need = mt[M + 3 + sl];
             for (int r = need + (lane >> 3); r < kTile; r += 4)
-                *reinterpret_cast<uint4*>(st + (size_t)sl * kGroupSlot + 4096 + swz(r, w * 8 + (lane & 7))) =
+                *reinterpret_cast<uint4*>(st + ((size_t)sl * HG + hid) * kGroupSlot + 4096 + swz(r, w * 8 + (lane & 7))) =
                     make_uint4(0u, 0u, 0u, 0u);
         }
         __syncwarp();
         const int slot_g = mt[min(g, M - 1)];
         const int my_slot = row_ok ? slot_g : -1;
         for (int sl = 0; sl < nslots; ++sl) {
-            const uint32_t kbase = smem_u32(st + (size_t)sl * kGroupSlot), vbase = kbase + 4096;
+            const uint32_t kbase = smem_u32(st + ((size_t)sl * HG + hid) * kGroupSlot), vbase = kbase + 4096;
             float sa[2][4], sb[2][4];  // two accumulation chains per n-tile (even / odd k pairs)
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
@@ -1826,7 +1835,7 @@ __global__ void __launch_bounds__(96, PA_GROUP_MINB) paged_attention_group_mma_k
         if (t == 0 && w == 0) p.part_ml[sh * p.NP + part] = make_float2(m_g, l_g);
     }
     __threadfence();
-    asm volatile("bar.sync 1, 64;" ::: "memory");  // both halves of every partial are out
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + hid) : "memory");  // both halves of every partial are out
     if (w == 1) return;
     for (int r = 0; r < nm; ++r) {  // split members: the last partition to finish merges (finish_split)
         const int ctx_r = __shfl_sync(FULL, my_ctx, r);
@@ -1844,19 +1853,23 @@ __global__ void __launch_bounds__(96, PA_GROUP_MINB) paged_attention_group_mma_k
 }
 
 cudaError_t launch_group_mma(const GroupParams& p, int dtype, int num_seqs, size_t smem, cudaStream_t stream) {
-    auto kern = dtype == 1 ? paged_attention_group_mma_kernel<__half> : paged_attention_group_mma_kernel<__nv_bfloat16>;
-    static size_t configured[2] = {0, 0};
-    if (smem > configured[dtype == 1 ? 0 : 1]) {
+    const int HG = p.a.HPC == 2 ? 2 : 1;  // heads per CTA
+    auto kern = dtype == 1 ? (HG == 2 ? paged_attention_group_mma_kernel<__half, 2> : paged_attention_group_mma_kernel<__half, 1>)
+                           : (HG == 2 ? paged_attention_group_mma_kernel<__nv_bfloat16, 2>
+                                      : paged_attention_group_mma_kernel<__nv_bfloat16, 1>);
+    static size_t configured[4] = {0, 0, 0, 0};
+    const int ci = (dtype == 1 ? 0 : 1) + 2 * (HG - 1);
+    if (smem > configured[ci]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        configured[dtype == 1 ? 0 : 1] = smem;
+        configured[ci] = smem;
     }
     if (p.a.NP > 1) {
         cudaError_t e = cudaMemsetAsync(p.a.counters, 0, sizeof(int) * (size_t)num_seqs * p.a.H, stream);
         if (e != cudaSuccess) return e;
     }
-    const dim3 grid(p.a.NP, p.a.H, (num_seqs + p.a.GM - 1) / p.a.GM);
-    return launch_k(kern, grid, dim3(96), smem, stream, p);
+    const dim3 grid(p.a.NP, p.a.H / HG, (num_seqs + p.a.GM - 1) / p.a.GM);
+    return launch_k(kern, grid, dim3(32 * (2 * HG + 1)), smem, stream, p);
 }
 
 // ==================================================================== debug gather ===

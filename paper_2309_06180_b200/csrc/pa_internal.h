@@ -148,7 +148,7 @@ size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int g
 // sched: 0 = grid, 1 = persistent, 2 = coop, 3 = persistent coop, 4 = sharing-aware groups, 5 = listed coop
 cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int sched, size_t smem,
                              cudaStream_t stream);
-size_t group_mma_smem_bytes(int gm, int gsl, int stg, int pt);
+size_t group_mma_smem_bytes(int gm, int gsl, int stg, int pt, int hg);
 cudaError_t launch_group_mma(const GroupParams& p, int dtype, int num_seqs, size_t smem, cudaStream_t stream);
 size_t prefill_smem_bytes();
 cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, cudaStream_t stream);
