@@ -69,11 +69,15 @@ typedef enum {
  * partition size depends on nothing but the context length, so results are bitwise
  * identical for any batch composition, block size, physical placement or head
  * sharding.  max_context_len: host upper bound of context_lens (<= 0 -> W *
- * block_size); it only sizes the grid.  workspace: device, >=
- * pa_paged_attention_workspace_size(), 16-byte aligned, any content (its completion
- * counters are zeroed on the stream by the call; do not share one workspace between
- * calls running concurrently on different streams);
- * may be NULL when that size is 0.
+ * block_size); it only sizes the grid.  PRECONDITION: every context_lens[s] <=
+ * max_context_len (a longer context is undefined behaviour: only its first
+ * ceil(max_context_len / PT) partitions are attended; pass <= 0 when unsure).
+ * workspace: device, >= pa_paged_attention_workspace_size(), 16-byte aligned, any
+ * content, never zeroed by the call: the split-completion words carry a per-launch
+ * 32-bit tag and the completing partition resets its word, so no memset node sits
+ * between decode steps (that keeps the programmatic-dependent-launch chain of
+ * consecutive steps intact).  Do not share one workspace between calls running
+ * concurrently on different streams.  May be NULL when that size is 0.
  * ---------------------------------------------------------------------------------- */
 pa_status_t pa_paged_attention(void* out, const void* query, const void* key_cache,
                                const void* value_cache, const int32_t* block_tables,
@@ -204,8 +208,9 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
  * completion flags: no NCCL call, no permute.
  *
  * pa_tp_comm_create: gather_a/gather_b/flags are HOST arrays of `world` DEVICE pointers
- * as seen from this process (index k = rank k's buffer: gather buffers S*H_total*D*e
- * bytes, 16-byte aligned; flag arrays int32[world], zero-initialised before first use);
+ * as seen from this process (index k = rank k's buffer: gather buffers of
+ * gather_bytes >= S*H_total*D*e bytes each, 16-byte aligned; flag arrays int32[world],
+ * zero-initialised before first use);
  * status: this rank's device int32, set to 1 if a flag wait times out (PA_TP_TIMEOUT_MS,
  * default 10000) instead of hanging.  Returns NULL on invalid arguments (pa_last_error).
  * The comm does not own any buffer.
@@ -214,12 +219,18 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
  * head counts (num_heads * world == num_heads_total).  Calls alternate between the two
  * gather buffers; *buffer_out (0 = gather_a, 1 = gather_b) names the one holding this
  * call's full [S][H_total][D] output once the stream reaches the end of the call.  A
- * result stays valid until this rank issues the call after next.  Every rank must make
- * the same sequence of calls.  Output bits equal the single-GPU decode's.
+ * result is valid until this rank issues its NEXT call: reads of it must be enqueued on
+ * `stream` before that call (a peer's call after next may overwrite the buffer as soon
+ * as this rank's next call has published its flags).  Every rank must make the same
+ * sequence of calls.  Output bits equal the single-GPU decode's.  Returns
+ * PA_ERR_INVALID_ARG if num_seqs*H_total*head_dim*e exceeds gather_bytes or the local
+ * head count does not match.  The attention kernel issues a system-scope fence after
+ * its peer stores, before the flag kernel's st.release.sys.
  * ---------------------------------------------------------------------------------- */
 typedef struct pa_tp_comm pa_tp_comm_t;
-pa_tp_comm_t* pa_tp_comm_create(int world, int rank, int num_heads_total, void* const* gather_a,
-                                void* const* gather_b, int32_t* const* flags, int32_t* status);
+pa_tp_comm_t* pa_tp_comm_create(int world, int rank, int num_heads_total, size_t gather_bytes,
+                                void* const* gather_a, void* const* gather_b,
+                                int32_t* const* flags, int32_t* status);
 void pa_tp_comm_destroy(pa_tp_comm_t* comm);
 pa_status_t pa_paged_attention_decode_tp(pa_tp_comm_t* comm, int* buffer_out, const void* query,
                                          const void* key, const void* value, void* key_cache,
@@ -240,7 +251,8 @@ pa_status_t pa_ipc_close_handle(void* dev_ptr);
 pa_status_t pa_device_alloc(size_t bytes, void** dev_ptr_out);
 pa_status_t pa_device_free(void* dev_ptr);
 
-/* Bytes of workspace pa_paged_attention(_ex) needs (0 if no context is split).
+/* Bytes of workspace pa_paged_attention(_ex) needs: 8 bytes of split-completion word
+ * per (sequence, head) plus, when a context is split, the partials.
  * partition_tokens as in pa_paged_attention_ex. */
 size_t pa_paged_attention_workspace_size(int num_seqs, int num_heads, int head_dim,
                                          int max_context_len, int partition_tokens);
@@ -399,6 +411,11 @@ pa_status_t pa_alloc_export(const pa_alloc_t* a, const int* seqs, int n, int W,
 int pa_alloc_refcount(const pa_alloc_t* a, int block);
 int pa_alloc_num_free(const pa_alloc_t* a);
 int pa_alloc_num_blocks_of(const pa_alloc_t* a, int seq); /* -1 if unknown */
+
+/* Tests / A-B scripts only: re-read the PA_* tuning environment variables (read once,
+ * at the first call, otherwise; never on the launch path).  Not thread-safe with
+ * concurrent launches. */
+void pa_reload_tuning(void);
 
 #ifdef __cplusplus
 }

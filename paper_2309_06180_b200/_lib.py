@@ -11,9 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# PA_LIB_VARIANT (experiments only): load a variant build (scripts/build_variant.sh), e.g. "pe3" ->
-# libpagedattn_pe3.so next to the default library
-LIB_PATH = os.path.join(_HERE, "libpagedattn%s.so" % ("_" + os.environ["PA_LIB_VARIANT"] if os.environ.get("PA_LIB_VARIANT") else ""))
+LIB_PATH = os.path.join(_HERE, "libpagedattn.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -57,11 +55,12 @@ _sig("pa_decode_step_staging_size", _sz, [_i32, _i32, _i32, _i32, _i32, _i32, _i
 _sig("pa_decode_step", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _f32, _i32, _i32, _i32, _i32,
                               _i32, _i32, _i32, _i32, _vp, _sz, _vp, _sz, _vp])
 _sig("pa_last_error", ctypes.c_char_p, [])
+_sig("pa_reload_tuning", None, [])
 _sig("pa_take_launch_count", ctypes.c_longlong, [])
 _sig("pa_debug_gather_kv", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp])
 _sig("pa_validate_tables", _i32, [_vp, _vp, _i32, _i32, _i32, _i32, ctypes.POINTER(_i64), _vp])
-_sig("pa_tp_comm_create", _vp, [_i32, _i32, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
-                                _vp])
+_sig("pa_tp_comm_create", _vp, [_i32, _i32, _i32, _sz, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                ctypes.POINTER(_vp), _vp])
 _sig("pa_tp_comm_destroy", None, [_vp])
 _sig("pa_paged_attention_decode_tp", _i32, [_vp, ctypes.POINTER(ctypes.c_int), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                             _f32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _sz, _vp])
@@ -108,3 +107,8 @@ def last_error() -> str:
 
 def take_launch_count() -> int:
     return int(_lib.pa_take_launch_count())
+
+
+def reload_tuning() -> None:
+    """Re-read the PA_* tuning environment (tests / A-B scripts; read once otherwise)."""
+    _lib.pa_reload_tuning()

@@ -13,8 +13,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
+#include <tuple>
+#include <vector>
 
 #include "pa_internal.h"
 
@@ -63,26 +66,97 @@ int log2_pow2(int b) {  // -1 if not a power of two in [1, 256]
             return fail(PA_ERR_INVALID_ARG, "%s is not %d-byte aligned", #p, (int)(align));   \
     } while (0)
 
-int effective_partition(int partition_tokens) {
-    if (partition_tokens != 0) return partition_tokens;
-    // PA_PT (A/B knob only, not a tuning default): the default partition for callers that pass 0
-    if (const char* ev = getenv("PA_PT")) return atoi(ev) > 0 ? atoi(ev) : PA_DEFAULT_PARTITION_TOKENS;
-    return PA_DEFAULT_PARTITION_TOKENS;
+// Tuning knobs, read ONCE (first use, thread-safe static init) -- never on the launch
+// path.  Every knob is an A/B switch for the measurements in DESIGN §7; the defaults are
+// the measured best.  Values that change after the first call are ignored.
+struct Tuning {
+    int pt = PA_DEFAULT_PARTITION_TOKENS;  // PA_PT: default partition for callers passing 0
+    int hpc = 0;                           // PA_HPC: coop consumer warps per CTA (0 = auto)
+    int stg = 0;                           // PA_STG: stages (0 = auto)
+    int ppc = 1;                           // PA_PPC: coop partitions per CTA (scheduling only)
+    int pz = 0;                            // PA_PZ: coop grid with the partition index slowest
+    int shared_hpc = 0, shared_slots = 1;  // PA_SHARED_HPC / PA_SHARED_SLOTS (N1 CUDA-core kernel)
+    int group_slots = 1, group_stg = 2, group_hg = 2;  // PA_GROUP_SLOTS / _STG / _HG (N1 mma kernel)
+    bool pdl = true;                       // PA_PDL=0 disables programmatic dependent launch
+    int prefill = 0;                       // PA_PREFILL=2|3 forces a prompt kernel (0 = auto)
+    bool e2e_zero_copy = false;            // PA_E2E_MODE=zerocopy
+    int e2e_chunks = 4;                    // PA_E2E_CHUNKS
+    int e2e_split[16] = {};                // PA_E2E_SPLIT="1,2,4,1"
+    int e2e_nsplit = 0;
+    int e2e_streams = 2;                   // PA_E2E_STREAMS
+    bool e2e_graph = false;                // PA_E2E_GRAPH=1
+    long long tp_timeout_ms = 10000;       // PA_TP_TIMEOUT_MS
+    std::string key;                       // all of the above, for the e2e graph cache key
+};
+
+int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return (v && atoi(v) > 0) ? atoi(v) : dflt;
 }
+
+Tuning load_tuning() {
+    Tuning t;
+    t.pt = env_int("PA_PT", t.pt);
+    t.hpc = std::min(8, env_int("PA_HPC", 0));
+    t.stg = env_int("PA_STG", 0);
+    t.ppc = env_int("PA_PPC", 1);
+    t.pz = env_int("PA_PZ", 0) > 0 ? 1 : 0;
+    t.shared_hpc = env_int("PA_SHARED_HPC", 0);
+    t.shared_slots = env_int("PA_SHARED_SLOTS", 1);
+    t.group_slots = env_int("PA_GROUP_SLOTS", 1);
+    t.group_stg = env_int("PA_GROUP_STG", 2);
+    if (const char* v = getenv("PA_GROUP_HG")) t.group_hg = atoi(v) == 1 ? 1 : 2;
+    if (const char* v = getenv("PA_PDL")) t.pdl = v[0] != '0';
+    t.prefill = env_int("PA_PREFILL", 0);
+    if (const char* v = getenv("PA_E2E_MODE")) t.e2e_zero_copy = std::strcmp(v, "zerocopy") == 0;
+    t.e2e_chunks = env_int("PA_E2E_CHUNKS", 4);
+    if (const char* ev = getenv("PA_E2E_SPLIT")) {
+        for (const char* q = ev; *q && t.e2e_nsplit < 16;) {
+            const int w = atoi(q);
+            if (w <= 0) break;
+            t.e2e_split[t.e2e_nsplit++] = w;
+            while (*q && *q != ',') ++q;
+            if (*q == ',') ++q;
+        }
+    }
+    if (const char* v = getenv("PA_E2E_STREAMS")) t.e2e_streams = atoi(v) == 1 ? 1 : 2;
+    if (const char* v = getenv("PA_E2E_GRAPH")) t.e2e_graph = std::strcmp(v, "1") == 0;
+    t.tp_timeout_ms = env_int("PA_TP_TIMEOUT_MS", 10000);
+    char buf[256];
+    std::snprintf(buf, sizeof(buf), "%d %d %d %d %d %d %d %d %d %d %d %d %d %d %d %d", t.pt, t.hpc, t.stg, t.ppc,
+                  t.pz, t.shared_hpc, t.shared_slots, t.group_slots, t.group_stg, t.group_hg, (int)t.pdl, t.prefill,
+                  (int)t.e2e_zero_copy, t.e2e_chunks, t.e2e_streams, t.e2e_nsplit);
+    t.key = buf;
+    for (int i = 0; i < t.e2e_nsplit; ++i) t.key += "," + std::to_string(t.e2e_split[i]);
+    return t;
+}
+
+// The active knobs: loaded once; pa_reload_tuning (tests / A-B scripts only) swaps in a
+// freshly read copy.  Old copies are leaked on purpose so references stay valid.
+std::atomic<const Tuning*> g_tuning{nullptr};
+const Tuning& tuning() {
+    const Tuning* t = g_tuning.load(std::memory_order_acquire);
+    if (t == nullptr) {
+        static std::once_flag once;
+        std::call_once(once, [] { g_tuning.store(new Tuning(load_tuning()), std::memory_order_release); });
+        t = g_tuning.load(std::memory_order_acquire);
+    }
+    return *t;
+}
+
+int effective_partition(int partition_tokens) { return partition_tokens != 0 ? partition_tokens : tuning().pt; }
 
 int64_t pad16(int64_t x) { return (x + 15) / 16 * 16; }
 
-// Workspace layout: counters [S][H] int32 | control (work counter, unit count) 16 B |
-// work list [S][NP] int4 | (split only) part_o [S][H][NP][D] fp32 | part_ml [S][H][NP] float2
+// Workspace layout: split completion words [S][H] uint64 | (split only) part_o
+// [S][H][NP][D] fp32 | part_ml [S][H][NP] float2.  No region needs zeroing (split_arrive).
 struct WsLayout {
-    int64_t counters, ctrl, items, part_o, part_ml, total;
+    int64_t counters, part_o, part_ml, total;
 };
 WsLayout ws_layout(int64_t S, int64_t H, int64_t D, int64_t NP) {
     WsLayout L{};
     int64_t o = 0;
-    L.counters = o; o += pad16(S * H * 4);
-    L.ctrl = o;     o += 16;
-    L.items = o;    o += pad16(S * NP * 16);
+    L.counters = o; o += pad16(S * H * 8);
     L.part_o = o;   if (NP > 1) o += S * H * NP * D * 4;
     L.part_ml = o;  if (NP > 1) o += S * H * NP * 8;
     L.total = o;
@@ -99,15 +173,54 @@ size_t workspace_bytes_for(int64_t S, int64_t H, int64_t D, int max_ctx, int PT)
 
 namespace pa {
 void count_launch() { ++g_launches; }
-bool pdl_enabled() {
-    const char* e = getenv("PA_PDL");
-    return !(e && e[0] == '0');
+bool pdl_enabled() { return tuning().pdl; }
+
+uint32_t next_epoch() {
+    // SplitMix32-style scramble of a process-wide counter: consecutive launches get
+    // unrelated tags, so stale words (old epochs, or partial-output floats left by an
+    // earlier call with another workspace layout) match this launch's tag with
+    // probability ~2^-32; 0 is reserved for "reset"
+    static std::atomic<uint32_t> ctr{0x9e3779b9u};
+    for (;;) {
+        uint32_t z = ctr.fetch_add(0x9e3779b9u, std::memory_order_relaxed);
+        z = (z ^ (z >> 16)) * 0x85ebca6bu;
+        z = (z ^ (z >> 13)) * 0xc2b2ae35u;
+        z ^= z >> 16;
+        if (z != 0) return z;
+    }
+}
+
+cudaError_t ensure_smem_attr(const void* kern, size_t smem) {
+    if (smem <= 48 * 1024) return cudaSuccess;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    // (kernel, device) -> largest size configured; the attribute is per device context
+    static std::mutex mu;
+    static std::vector<std::tuple<const void*, int, size_t>> done;
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& d : done)
+        if (std::get<0>(d) == kern && std::get<1>(d) == dev && std::get<2>(d) >= smem) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    for (auto& d : done)
+        if (std::get<0>(d) == kern && std::get<1>(d) == dev) {
+            std::get<2>(d) = smem;
+            return cudaSuccess;
+        }
+    done.emplace_back(kern, dev, smem);
+    return cudaSuccess;
 }
 }  // namespace pa
 
 extern "C" {
 
 const char* pa_last_error(void) { return g_err.c_str(); }
+
+void pa_reload_tuning(void) {
+    tuning();
+    g_tuning.store(new Tuning(load_tuning()), std::memory_order_release);
+}
 
 long long pa_take_launch_count(void) {
     long long n = g_launches;
@@ -173,67 +286,45 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
         return fail(PA_ERR_WORKSPACE, "workspace of %zu bytes required (got %zu)", need,
                     workspace ? workspace_bytes : (size_t)0);
     REQUIRE_PTR(workspace, 16);
-    // Scheduler (PA_SCHED): "coop" (default) -- one CTA per (partition, group of 4 query
-    // heads, sequence), one producer warp filling shared K/V stages for 4 consumer warps;
-    // "grid" -- same CTAs, every warp loading its own head's tiles; "persistent" --
-    // warps streaming a longest-first work list.  ~64 KB of stages per CTA (3 CTAs per
-    // SM), measured best (scripts/sweep.py).  PA_HPC / PA_STG / PA_HPW override.
-    const char* sched_env = getenv("PA_SCHED");
-    int sched = 2;  // coop
-    if (sched_env && std::strcmp(sched_env, "grid") == 0) sched = 0;
-    if (sched_env && std::strcmp(sched_env, "persistent") == 0) sched = 1;
-    if (sched_env && std::strcmp(sched_env, "pcoop") == 0) sched = 3;
-    if (sched_env && std::strcmp(sched_env, "lcoop") == 0) sched = 5;
-    bool natural = false;  // pcoop over items in grid order (no work-list launch)
-    if (sched_env && std::strcmp(sched_env, "ncoop") == 0) sched = 3, natural = true;
-    // (pcoop as the default for unsplit batches measured c2_alpaca 70.7 -> 69.2 us but
-    // c3_fork 98.5 -> 104.2 and c1_tiny 19.5 -> 21.7 us: the list-building launch sits on
-    // the critical path; DESIGN §7.  coop stays the default everywhere.)
+    // Scheduler: "coop" -- one CTA per (partition, group of 4 query heads, sequence), one
+    // producer warp filling shared K/V stages for 4 consumer warps, ~64 KB of stages per
+    // CTA (3 CTAs per SM), measured best; group_size > 1: the sharing-aware
+    // kernel over groups of consecutive sequences (N1).
+    const Tuning& tu = tuning();
     REQUIRE(group_size >= 1, "group_size must be >= 1");
     const int gm = std::min(group_size, 8);
-    if (gm > 1) sched = 4;  // sharing-aware: groups of gm consecutive sequences
-    const bool persistent = sched == 1;
+    const int sched = gm > 1 ? 4 : 2;
     const int rb = pa::attention_row_bytes((int)dtype, head_dim);
     const int G = num_heads / num_kv_heads;
     int nw = 4;
-    if (sched != 1 && num_heads % 4 != 0) {
+    if (num_heads % 4 != 0) {
         for (int d = 8; d >= 1; --d)
             if (num_heads % d == 0) { nw = d; break; }
     }
-    if (const char* ev = getenv("PA_HPC")) nw = atoi(ev) > 0 ? atoi(ev) : nw;
-    if (nw > 8) nw = 8;
-    const int nkv_max = nw % G == 0 ? nw / G : (nw + G - 1) / G + 1;
+    if (tu.hpc > 0) nw = tu.hpc;
     // sharing-aware (sched 4): gm * nw consumer warps per CTA (<= 8), stages of nsl
-    // distinct-block slots (a tile with more distinct blocks takes several stages);
-    // PA_SHARED_HPC / PA_SHARED_SLOTS override
+    // distinct-block slots (a tile with more distinct blocks takes several stages).
     // Defaults (measured): 8 consumer warps (gm members x 8/gm heads) and ONE
     // slot per stage -- a tile whose members read d distinct blocks takes d stages, so a
     // stage is never sized for the worst case and 4 x 16 KB stages fit 3 CTAs per SM.
     int nsl = 1;
     if (sched == 4) {
         nw = std::max(1, 8 / gm);
-        if (const char* ev = getenv("PA_SHARED_HPC")) nw = std::max(1, std::min(8 / gm, atoi(ev)));
-        if (const char* ev = getenv("PA_SHARED_SLOTS")) nsl = std::max(1, std::min(gm, atoi(ev)));
+        if (tu.shared_hpc > 0) nw = std::max(1, std::min(8 / gm, tu.shared_hpc));
+        nsl = std::max(1, std::min(gm, tu.shared_slots));
     }
-    const int nkv_max4 = nw % G == 0 ? nw / G : (nw + G - 1) / G + 1;
-    const int stage = sched == 4 ? nsl * 2 * nkv_max4 * 16 * rb : sched >= 2 ? 2 * nkv_max * 16 * rb : 2 * 16 * rb;
-    // (sched 5 = listed coop shares the coop kernel and its shared-memory layout)
+    const int nkv_max = nw % G == 0 ? nw / G : (nw + G - 1) / G + 1;
+    const int stage = sched == 4 ? nsl * 2 * nkv_max * 16 * rb : 2 * nkv_max * 16 * rb;
     // (sharing-aware: 48 KB of stages, so 4 CTAs fit in shared memory as in registers)
-    int stg = sched == 4 ? (48 * 1024) / stage : sched >= 2 ? (64 * 1024) / stage : (64 * 1024) / (nw * stage);
+    int stg = (sched == 4 ? 48 * 1024 : 64 * 1024) / stage;
     stg = stg < 2 ? 2 : (stg > 8 ? 8 : stg);
-    if (const char* ev = getenv("PA_STG")) stg = atoi(ev) > 0 ? atoi(ev) : stg;
+    if (tu.stg > 0) stg = tu.stg;
     // coop: partitions per CTA (scheduling only: the arithmetic partition stays PT and a
     // CTA owning all partitions merges them in shared memory, bit-identically).  Measured
     // neutral on c4 and worse on c2 (longer tail), so 1 unless PA_PPC says otherwise.
-    int ppc = 1;
-    if (const char* ev = getenv("PA_PPC")) ppc = atoi(ev) > 0 ? atoi(ev) : ppc;
-    ppc = std::max(1, std::min(ppc, NP));
-    if (sched == 5) ppc = 1;  // listed CTAs take single partitions
-    const size_t smem = sched == 4   ? pa::attention_smem_bytes_shared(rb, nw, G, stg, gm, nsl)
-                        : (sched == 2 || sched == 5)
-                            ? pa::attention_smem_bytes_coop(rb, nw, G, stg, PT * ppc, block_size, ppc, head_dim)
-                        : sched == 3 ? pa::attention_smem_bytes_pcoop(rb, nw, G, stg, PT, block_size)
-                                     : pa::attention_smem_bytes(persistent, rb, nw, stg, PT, block_size);
+    const int ppc = std::max(1, std::min(tu.ppc, NP));
+    const size_t smem = sched == 4 ? pa::attention_smem_bytes_shared(rb, nw, G, stg, gm, nsl)
+                                   : pa::attention_smem_bytes_coop(rb, nw, G, stg, PT * ppc, block_size, ppc, head_dim);
     if (smem > 227 * 1024)
         return fail(PA_ERR_UNSUPPORTED, "partition_tokens %d with block_size %d needs %zu B of shared memory", PT,
                     block_size, smem);
@@ -252,10 +343,7 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     {
         const WsLayout L = ws_layout(num_seqs, num_heads, head_dim, NP);
         char* w = static_cast<char*>(workspace);
-        p.counters = reinterpret_cast<int*>(w + L.counters);
-        p.work_counter = reinterpret_cast<int*>(w + L.ctrl);
-        p.n_items = reinterpret_cast<int*>(w + L.ctrl + 4);
-        p.items = reinterpret_cast<int4*>(w + L.items);
+        p.counters = reinterpret_cast<unsigned long long*>(w + L.counters);
         p.part_o = reinterpret_cast<float*>(w + L.part_o);
         p.part_ml = reinterpret_cast<float2*>(w + L.part_ml);
     }
@@ -269,16 +357,12 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     p.NP = NP;
     p.HPC = nw;
     p.STG = stg;
-    p.HPW = 1;
     p.PPC = ppc;
     p.GM = gm;
     p.GSL = nsl;
     p.S = num_seqs;
-    p.listed = sched == 5;
-    p.pz = 0;
-    if (const char* ev = getenv("PA_PZ")) p.pz = atoi(ev) > 0 ? 1 : 0;
-    p.natural = natural ? 1 : 0;
-    if (const char* ev = getenv("PA_HPW")) p.HPW = atoi(ev) > 0 ? atoi(ev) : 1;
+    p.pz = tu.pz;
+    p.epoch = pa::next_epoch();
     if (tp != nullptr) {
         p.n_out_peers = tp->n;
         p.out_H = tp->H_total;
@@ -434,7 +518,7 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
     {
         const WsLayout L = ws_layout(num_seqs, num_heads, head_dim, NP);
         char* w = static_cast<char*>(workspace);
-        p.counters = reinterpret_cast<int*>(w + L.counters);
+        p.counters = reinterpret_cast<unsigned long long*>(w + L.counters);
         p.part_o = reinterpret_cast<float*>(w + L.part_o);
         p.part_ml = reinterpret_cast<float2*>(w + L.part_ml);
     }
@@ -448,17 +532,16 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
     p.NP = NP;
     p.GM = group_size;
     p.S = num_seqs;
+    p.epoch = pa::next_epoch();
     // block slots per stage (a tile whose group reads more distinct blocks takes several
     // stages) and stages: PA_GROUP_SLOTS / PA_GROUP_STG override
-    int gsl = 1;  // one block slot per stage: c5 514 vs 541 us with 2
-    if (const char* ev = getenv("PA_GROUP_SLOTS")) gsl = std::max(1, std::min(group_size, atoi(ev)));
-    int stg = 2;
-    if (const char* ev = getenv("PA_GROUP_STG")) stg = atoi(ev) > 0 ? atoi(ev) : stg;
+    // (one block slot per stage: c5 514 vs 541 us with 2)
+    const int gsl = std::max(1, std::min(group_size, tuning().group_slots));
+    const int stg = tuning().group_stg;
     p.STG = stg;
     p.GSL = gsl;
     // heads per CTA (one consumer-warp pair each; 2 when the head count allows): PA_GROUP_HG
-    int hg = 2;  // c5 515 vs 523 us with one head per CTA
-    if (const char* ev = getenv("PA_GROUP_HG")) hg = atoi(ev) == 2 ? 2 : 1;
+    int hg = tuning().group_hg;  // 2: c5 515 vs 523 us with one head per CTA
     if (num_heads % hg != 0) hg = 1;
     p.HPC = hg;
     const size_t smem = pa::group_mma_smem_bytes(group_size, gsl, stg, PT, hg);
@@ -534,7 +617,7 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
     p.H_kv = num_kv_heads;
     p.G = num_heads / num_kv_heads;
     p.W = max_blocks_per_seq;
-    cudaError_t e = pa::launch_prefill(p, (int)dtype, num_seqs, max_query_len, (cudaStream_t)stream);
+    cudaError_t e = pa::launch_prefill(p, (int)dtype, num_seqs, max_query_len, tuning().prefill, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "paged_prefill_kernel launch");
     return PA_OK;
 }
@@ -542,6 +625,7 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
 // ---- N2: fused tensor-parallel all-gather ------------------------------------------------
 struct pa_tp_comm {
     int world, rank, H_total;
+    size_t gather_bytes;
     void* gather[2][pa::kMaxTpPeers];
     int32_t* flags[pa::kMaxTpPeers];
     int32_t* status;
@@ -549,8 +633,9 @@ struct pa_tp_comm {
     long long timeout_ns;
 };
 
-pa_tp_comm_t* pa_tp_comm_create(int world, int rank, int num_heads_total, void* const* gather_a,
-                                void* const* gather_b, int32_t* const* flags, int32_t* status) {
+pa_tp_comm_t* pa_tp_comm_create(int world, int rank, int num_heads_total, size_t gather_bytes,
+                                void* const* gather_a, void* const* gather_b, int32_t* const* flags,
+                                int32_t* status) {
     g_err.clear();
     if (world < 1 || world > pa::kMaxTpPeers || rank < 0 || rank >= world || num_heads_total <= 0 ||
         num_heads_total % world != 0 || !gather_a || !gather_b || !flags || !status) {
@@ -569,6 +654,7 @@ pa_tp_comm_t* pa_tp_comm_create(int world, int rank, int num_heads_total, void* 
     c->world = world;
     c->rank = rank;
     c->H_total = num_heads_total;
+    c->gather_bytes = gather_bytes;
     for (int k = 0; k < world; ++k) {
         c->gather[0][k] = gather_a[k];
         c->gather[1][k] = gather_b[k];
@@ -576,8 +662,7 @@ pa_tp_comm_t* pa_tp_comm_create(int world, int rank, int num_heads_total, void* 
     }
     c->status = status;
     c->epoch = 0;
-    const char* ev = getenv("PA_TP_TIMEOUT_MS");
-    c->timeout_ns = (ev && atoll(ev) > 0 ? atoll(ev) : 10000) * 1000000LL;
+    c->timeout_ns = tuning().tp_timeout_ms * 1000000LL;
     return c;
 }
 
@@ -594,8 +679,13 @@ pa_status_t pa_paged_attention_decode_tp(pa_tp_comm_t* comm, int* buffer_out, co
     REQUIRE(num_heads * comm->world == comm->H_total, "local heads (%d) x world (%d) != total heads (%d)", num_heads,
             comm->world, comm->H_total);
     REQUIRE(key != nullptr && value != nullptr, "key/value (the step's new token) are NULL");
+    REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
+    REQUIRE(num_seqs >= 0 && head_dim > 0 &&
+                (uint64_t)num_seqs * comm->H_total * head_dim * elem_bytes(dtype) <= comm->gather_bytes,
+            "%d sequences x %d heads x %d dims do not fit the %zu-byte gather buffers", num_seqs, comm->H_total,
+            head_dim, comm->gather_bytes);
     const int32_t epoch = comm->epoch + 1;
-    const int buf = (epoch - 1) & 1;  // the two gather buffers alternate (result valid until call +2)
+    const int buf = (epoch - 1) & 1;  // the two gather buffers alternate (result valid until the next call)
     TpOut tp{};
     tp.n = comm->world;
     tp.H_total = comm->H_total;
@@ -898,8 +988,8 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     // over the host link and stores its output rows into host_out.  Measured slower than
     // the copy-engine chunks on c2_sharegpt (669 vs 473 us per step: the CTAs stall on
     // host-link read latency), so the default is the chunked path below.
-    const char* mode = getenv("PA_E2E_MODE");
-    const bool zero_copy = mode != nullptr && std::strcmp(mode, "zerocopy") == 0;
+    const Tuning& tu = tuning();
+    const bool zero_copy = tu.e2e_zero_copy;
     void* dq = nullptr;
     void* dk = nullptr;
     void* dv = nullptr;
@@ -938,21 +1028,12 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     E2EStreams* es = e2e_streams();
     if (es == nullptr) return fail(PA_ERR_CUDA, "pa_decode_step: could not create its copy streams");
     std::lock_guard<std::mutex> lock(es->mu);
-    int C = 4;
-    if (const char* ev = getenv("PA_E2E_CHUNKS")) C = atoi(ev) > 0 ? atoi(ev) : C;
+    int C = tu.e2e_chunks;
     // chunk weights (PA_E2E_SPLIT="1,2,4,1": relative sizes, first to last); equal if unset
     int wts[E2EStreams::kMaxChunks];
     int nw_ = 0;
-    if (const char* ev = getenv("PA_E2E_SPLIT")) {
-        for (const char* q = ev; *q && nw_ < E2EStreams::kMaxChunks;) {
-            const int w = atoi(q);
-            if (w <= 0) break;
-            wts[nw_++] = w;
-            while (*q && *q != ',') ++q;
-            if (*q == ',') ++q;
-        }
-        if (nw_ > 0) C = nw_;
-    }
+    for (int i = 0; i < tu.e2e_nsplit && nw_ < E2EStreams::kMaxChunks; ++i) wts[nw_++] = tu.e2e_split[i];
+    if (nw_ > 0) C = nw_;
     C = std::max(1, std::min({C, num_seqs > 0 ? num_seqs : 1, E2EStreams::kMaxChunks}));
     if (nw_ != C) {
         nw_ = C;
@@ -972,8 +1053,7 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     const int cap = max_blocks_per_seq * block_size;
     const int mctx = max_context_len > 0 ? std::min(max_context_len, cap) : cap;
     const size_t ws_chunk = (workspace_bytes_for(n_max, num_heads, head_dim, mctx, PT) + 255) & ~(size_t)255;
-    int NS = 2;
-    if (const char* ev = getenv("PA_E2E_STREAMS")) NS = atoi(ev) == 1 ? 1 : 2;
+    int NS = tu.e2e_streams;
     if (C == 1 || workspace == nullptr || 2 * ws_chunk > workspace_bytes) NS = 1;
     // Everything below is enqueued by `enqueue(origin)`: on the caller's stream (default),
     // or (PA_E2E_GRAPH=1) once on an internal capture stream into a CUDA graph that later
@@ -1040,8 +1120,7 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     return PA_OK;
     };
 
-    const char* gev = getenv("PA_E2E_GRAPH");
-    if (gev == nullptr || std::strcmp(gev, "1") != 0) return enqueue(s);
+    if (!tu.e2e_graph) return enqueue(s);
     // key: every argument that shapes the enqueued work (host buffer CONTENTS are read
     // when the graph runs, so they may change between calls) + the tuning environment
     std::string key;
@@ -1056,11 +1135,8 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
                       value_cache, sc, block_size, num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq,
                       max_context_len, (int)dtype, staging, staging_bytes, workspace, workspace_bytes, C, NS);
         key = buf;
-        for (const char* name : {"PA_E2E_SPLIT", "PA_SCHED", "PA_HPC", "PA_STG", "PA_PPC", "PA_HPW", "PA_PDL"}) {
-            const char* v = getenv(name);
-            key += ' ';
-            key += v ? v : "-";
-        }
+        key += ' ';
+        key += tu.key;
     }
     E2EStreams::Graph* hit = nullptr;
     for (auto& g : es->graphs)

@@ -4,35 +4,30 @@
 // the sequence's logical tokens through its block table, computes
 // l_t = scale * q.K_t, a numerically stable softmax and sum_t softmax_t * V_t.
 //
-// B200 design (DESIGN.md §Kernels):
+// B200 design (DESIGN.md §6):
 //  * Work unit = (sequence, query head, partition of <= PT logical tokens); one WARP
 //    walks the unit's 16-token LOGICAL tiles in order, so the arithmetic never depends
 //    on block_size, physical placement, head grouping, scheduling or grid shape ->
 //    bitwise invariance (BJ:north_star's permutation / block-size properties).
-//  * Tiles are staged into shared memory by 1-D bulk async copies (cp.async.bulk,
-//    SASS UBLKCP) completing on per-stage mbarriers; each warp keeps STG tiles in
-//    flight.  For block_size < 16 a tile is several pieces issued by several lanes.
-//  * Default scheduler ("persistent"): a tiny build kernel counting-sorts the
-//    (sequence, partition) units by length, longest first, into a work list; a
-//    persistent grid (occupancy x SMs) of independent warps takes units from it in a
-//    static zig-zag deal and streams their tiles back to back -- the bulk copies of
-//    the next unit (its q row included) are issued while the current one is being
-//    computed, so no warp idles in a prologue and the tail is made of the shortest
-//    units.
-//    Alternative ("grid", PA_SCHED=grid): one CTA per (partition, head group, seq).
+//  * Scheduler ("coop", the only one shipped): one CTA per (partition, group of 4 query
+//    heads, sequence); a producer warp stages the group's K/V tiles into shared memory
+//    with 1-D bulk async copies (cp.async.bulk, SASS UBLKCP) completing on per-stage
+//    mbarriers, 4 consumer warps compute.  For block_size < 16 a tile is several pieces.
+//    (Grid, persistent-warp, persistent-CTA and work-list schedulers were measured and
+//    removed; DESIGN §7 keeps their numbers.)
 //  * Lane mapping: a K/V row of RB = D*e bytes is covered by LT = RB/32 lanes, each
 //    owning two 16-byte chunks (c and c+LT: conflict-free 128-byte phases); a warp
 //    handles TG = 32/LT tokens at once.  q.k uses the sm_100 mixed-precision FMA
 //    (FHFMA, f16/bf16 x f16/bf16 + f32) straight from the packed storage dtype; the
 //    dot product is reduced with warp shuffles across the LT lanes.  Each token group
 //    keeps its own online-softmax state (m, l, acc[]) in the exp2 domain, and p*V is
-//    accumulated with packed fp32x2 FMAs (FFMA2).  No tensor cores: a one-query decode
-//    step is a memory-bound GEMV (BJ:north_star).
+//    accumulated with packed FMAs.  No tensor cores: a one-query decode step is a
+//    memory-bound GEMV (BJ:north_star).
 //  * End of a unit: token groups merge by shuffles (log-sum-exp, fixed order).  A
 //    context that fits one partition writes `out` directly (16-byte stores); otherwise
 //    each partition publishes (m, L, o~) and the LAST partition of the (sequence,
-//    head) to finish -- an atomic counter -- merges them in partition order
-//    (split-context variant, BJ:north_star).
+//    head) to finish -- an epoch-tagged atomic counter, see split_arrive -- merges them
+//    in partition order (split-context variant, BJ:north_star).
 //  * Fused decode entry (pa_paged_attention_decode): the step's new token (logical
 //    position ctx-1) is bulk-copied from the key/value inputs straight into its tile
 //    row, and one warp per (sequence, kv head) stores it to its cache slot
@@ -56,7 +51,6 @@ struct AttnCfg {
     static constexpr int TPL = kTile / TG;   // tokens per lane per tile
     static constexpr int EPC = 16 / E;       // elements per chunk
     static constexpr int STAGE_BYTES = 2 * kTile * RB;
-    static constexpr int PSTAGE_BYTES = STAGE_BYTES + RB;  // persistent stage: K | V | q row
     static_assert(LT >= 1 && LT <= 16 && TG * LT == 32, "row must span 2..32 lanes");
     static_assert(TPL >= 1 && TPL * TG == kTile, "tile must split evenly over token groups");
 };
@@ -176,6 +170,10 @@ __device__ __forceinline__ void store_out_p(const AttnParams& p, int64_t sh, flo
     const int64_t s = sh / p.H, h = sh - s * p.H;
     const int64_t off = (s * p.out_H + p.out_h0 + h) * D;
     for (int k = 0; k < p.n_out_peers; ++k) store_out<T, D>(static_cast<T*>(p.out_peers[k]) + off, l, acc, c);
+    // order this thread's peer stores before the completion flag at system scope: the flag
+    // kernel's st.release.sys then covers them without relying on kernel-boundary
+    // semantics for memory written to ANOTHER GPU (pa_tp.cu)
+    __threadfence_system();
 }
 
 // Lanes of token group 0: normalised partial o~ = acc / l (fp32).
@@ -227,12 +225,38 @@ __device__ __forceinline__ void merge_partitions_from(const AttnParams& p, int64
         const int64_t s = sh / p.H, h = sh - s * p.H;
         const int64_t off = (s * p.out_H + p.out_h0 + h) * D;
         for (int k = 0; k < p.n_out_peers; ++k) store_row(static_cast<T*>(p.out_peers[k]) + off);
+        __threadfence_system();  // see store_out_p
     }
 }
 
 template <typename T, int D>
 __device__ __forceinline__ void merge_partitions(const AttnParams& p, int64_t sh, int np, int lane) {
     merge_partitions_from<T, D, true>(p, sh, p.part_ml + sh * p.NP, p.part_o + sh * p.NP * D, np, lane);
+}
+
+// Split-context completion count of (sequence, head) sh, called once per partition by
+// lane 0 after its (m, L, o~) is published; true for the partition that completes the
+// set of n.  The counter word is (epoch << 32 | partitions done): a word carrying another
+// launch's epoch counts as 0, and the completing partition stores 0 back (nobody else
+// touches the word again in this launch).  So the host never zeroes the counters -- no
+// memset node between decode steps, which keeps the programmatic-dependent-launch chain
+// intact -- and a workspace region that held partials of an earlier call with another
+// layout is still a valid counter array (epochs are scrambled 32-bit tags, pa_api.cpp).
+// The first CAS guesses the common state 0 (no extra load).
+__device__ __forceinline__ bool split_arrive(const AttnParams& p, int64_t sh, int n) {
+    unsigned long long* ctr = p.counters + sh;
+    const unsigned long long E = (unsigned long long)p.epoch << 32;
+    unsigned long long cur = 0ull;
+    for (;;) {
+        const unsigned long long want = ((cur & 0xffffffff00000000ull) == E ? cur : E) + 1ull;
+        const unsigned long long prev = atomicCAS(ctr, cur, want);
+        if (prev == cur) {
+            if ((int)(want & 0xffffffffull) < n) return false;
+            atomicExch(ctr, 0ull);
+            return true;
+        }
+        cur = prev;
+    }
 }
 
 // Publish this partition's (m, L, o~); the last partition to finish merges.  Whole warp.
@@ -245,8 +269,7 @@ __device__ __forceinline__ void finish_split(const AttnParams& p, int64_t sh, in
     int last = 0;
     if (lane == 0) {
         __threadfence();
-        const int old = atomicAdd(p.counters + sh, 1);
-        last = (old == min(nparts, p.NP) - 1);
+        last = split_arrive(p, sh, min(nparts, p.NP));
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
@@ -293,49 +316,6 @@ __device__ __forceinline__ void issue_tile(char* sK, char* sV, uint64_t* bar, co
     __syncwarp();
 }
 
-// Persistent scheduler: block id prefetched (blk_pre >= 0) or read straight from the
-// block-table row (L1/L2 resident); optional extra rows (the unit's q row, the new token's K/V) ride on the
-// same mbarrier.  Copies cache rows [tok0, pc) of the tile.
-__device__ __forceinline__ void issue_tile_p(char* sK, char* sV, uint64_t* bar, const char* kc, const char* vc,
-                                             const int32_t* btrow, int tok0, int pc, int log2B, int64_t blk_stride,
-                                             int64_t head_off, int RB, int lane, const char* q_src, char* q_dst,
-                                             const char* nk_src, const char* nv_src, int new_row, int blk_pre) {
-    const int B = 1 << log2B;
-    const int nv = max(0, min(kTile, pc - tok0));
-    if (lane == 0) {
-        uint32_t tx = (uint32_t)(2 * nv * RB);
-        if (q_src) tx += RB;
-        if (nk_src) tx += 2 * RB;
-        mbar_arrive_expect_tx(bar, tx);
-        if (q_src) bulk_g2s(q_dst, q_src, RB, bar);
-        if (nk_src) {
-            bulk_g2s(sK + new_row * RB, nk_src, RB, bar);
-            bulk_g2s(sV + new_row * RB, nv_src, RB, bar);
-        }
-        if (B >= kTile && nv > 0) {
-            const int blk = blk_pre >= 0 ? blk_pre : __ldg(btrow + (tok0 >> log2B));
-            const int64_t off = (int64_t)blk * blk_stride + head_off + (int64_t)(tok0 & (B - 1)) * RB;
-            bulk_g2s(sK, kc + off, (uint32_t)(nv * RB), bar);
-            bulk_g2s(sV, vc + off, (uint32_t)(nv * RB), bar);
-        }
-    }
-    if (B < kTile) {
-        __syncwarp();
-        const int pieces = kTile >> log2B;
-        if (lane < pieces) {
-            const int tk = tok0 + (lane << log2B);
-            if (tk < pc) {
-                const int blk = __ldg(btrow + (tk >> log2B));
-                const int nvp = min(B, pc - tk);
-                const int64_t off = (int64_t)blk * blk_stride + head_off;
-                bulk_g2s(sK + (lane << log2B) * RB, kc + off, (uint32_t)(nvp * RB), bar);
-                bulk_g2s(sV + (lane << log2B) * RB, vc + off, (uint32_t)(nvp * RB), bar);
-            }
-        }
-    }
-    __syncwarp();
-}
-
 // Store the new token's row (already in shared memory) to its cache slot: lanes of
 // token group 0, two 16-byte chunks of K and of V each.
 template <typename T, int D>
@@ -352,422 +332,6 @@ __device__ __forceinline__ void write_new_token(const AttnParams& p, const char*
     dk[c + LT] = lds128(sKrow + (c + LT) * 16);
     dv[c] = lds128(sVrow + c * 16);
     dv[c + LT] = lds128(sVrow + (c + LT) * 16);
-}
-
-// ============================================================ persistent scheduler ===
-
-// Stable counting sort of the (sequence, partition) units by tile count, longest first
-// (ties keep sequence order, so sibling sequences that share blocks -- parallel
-// sampling, beam search -- stay adjacent and hit in L2), and zero the split counters
-// and the work counter.  One CTA of 1024 threads.  items[i] = (s, part, ctx, 0).
-constexpr int kBuckets = 256;
-
-__device__ __forceinline__ int unit_key(int ctx, int part, int PT) {
-    const int len = max(0, min(ctx, (part + 1) * PT) - part * PT);
-    return kBuckets - 1 - min((len + kTile - 1) / kTile, kBuckets - 1);  // 0 = longest
-}
-
-__global__ void __launch_bounds__(1024) build_worklist_kernel(const AttnParams p, int S) {
-    pdl_launch_dependents();
-    pdl_wait();
-    __shared__ int base[kBuckets];
-    __shared__ int wcnt[32][kBuckets];
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int64_t ncnt = (int64_t)S * p.H;
-    for (int64_t i = tid; i < ncnt; i += 1024) p.counters[i] = 0;
-    if (tid == 0) *p.work_counter = 0;
-    if (tid < kBuckets) base[tid] = 0;
-    __syncthreads();
-    for (int s = tid; s < S; s += 1024) {  // histogram
-        const int ctx = p.context_lens[s];
-        const int np = min(ctx > 0 ? (ctx + p.PT - 1) / p.PT : 1, p.NP);
-        for (int part = 0; part < np; ++part) atomicAdd(&base[unit_key(ctx, part, p.PT)], 1);
-    }
-    __syncthreads();
-    if (w == 0) {  // exclusive scan over the buckets (8 per lane)
-        int v[kBuckets / 32], sum = 0;
-#pragma unroll
-        for (int i = 0; i < kBuckets / 32; ++i) {
-            v[i] = base[lane * (kBuckets / 32) + i];
-            sum += v[i];
-        }
-        int x = sum;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, off);
-            if (lane >= off) x += y;
-        }
-        int run = x - sum;
-#pragma unroll
-        for (int i = 0; i < kBuckets / 32; ++i) {
-            base[lane * (kBuckets / 32) + i] = run;
-            run += v[i];
-        }
-        if (lane == 31) *p.n_items = run;
-    }
-    __syncthreads();
-    // stable scatter, in rounds of (1024 sequences, partition index)
-    for (int s0 = 0; s0 < S; s0 += 1024) {
-        const int s = s0 + tid;
-        const int ctx = s < S ? p.context_lens[s] : 0;
-        const int np = s < S ? min(ctx > 0 ? (ctx + p.PT - 1) / p.PT : 1, p.NP) : 0;
-        for (int part = 0; part < p.NP; ++part) {
-            const bool has = part < np;
-            const int b = has ? unit_key(ctx, part, p.PT) : -1;
-            for (int i = tid; i < 32 * kBuckets; i += 1024) (&wcnt[0][0])[i] = 0;
-            __syncthreads();
-            const unsigned peers = __match_any_sync(0xffffffffu, b);
-            const int rank = __popc(peers & ((1u << lane) - 1u));
-            if (has && rank == 0) wcnt[w][b] = __popc(peers);
-            __syncthreads();
-            if (tid < kBuckets) {
-                int run = base[tid];
-                for (int ww = 0; ww < 32; ++ww) {
-                    const int t = wcnt[ww][tid];
-                    wcnt[ww][tid] = run;
-                    run += t;
-                }
-                base[tid] = run;
-            }
-            __syncthreads();
-            if (has) p.items[wcnt[w][b] + rank] = make_int4(s, part, ctx, 0);
-            __syncthreads();
-        }
-    }
-}
-
-// Persistent warps.  Each warp runs a producer (issue the bulk copies of its units'
-// tiles -- up to STG in flight, across unit boundaries) and a consumer (wait, compute,
-// finish the unit) in one loop.  Unit fetching is software-pipelined so no latency is
-// exposed at unit boundaries (see below).  Unit descriptors travel from producer to
-// consumer through a small per-warp ring in shared memory.
-template <typename T, int D>
-__global__ void __launch_bounds__(256) paged_attention_persistent_kernel(const AttnParams p) {
-    using C = AttnCfg<T, D>;
-    constexpr int RB = C::RB, LT = C::LT, EPC = C::EPC;
-    constexpr int SB = C::PSTAGE_BYTES;
-    constexpr int DESC = 8;
-    extern __shared__ __align__(128) unsigned char smem[];
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int NW = blockDim.x >> 5, STG = p.STG, RING = STG + 2;
-    char* wst = reinterpret_cast<char*>(smem) + (size_t)warp * STG * SB;
-    uint64_t* bars_all = reinterpret_cast<uint64_t*>(smem + (size_t)NW * STG * SB);
-    uint64_t* bars = bars_all + warp * STG;
-    int* ring = reinterpret_cast<int*>(bars_all + NW * STG) + warp * RING * DESC;
-    if (lane < STG) mbar_init(&bars[lane], 1);
-    fence_mbar_init();
-    __syncwarp();
-    pdl_wait();  // work list, counters, copy_blocks of this step: all complete
-
-    const int H = p.H, PT = p.PT, log2B = p.log2B;
-    const int total = __ldcg(p.n_items) * H;
-    const char* kc = static_cast<const char*>(p.key_cache);
-    const char* vc = static_cast<const char*>(p.value_cache);
-    const int64_t blk_stride = ((int64_t)p.H_kv << log2B) * RB;
-    const int g = lane / LT, c = lane % LT;
-
-    // ---- unit-fetch pipeline -------------------------------------------------------------
-    // Static zig-zag assignment of the longest-first list: round r gives warp wg the unit
-    // r*NWT + wg (r even) or r*NWT + NWT-1-wg (r odd) -- an LPT-like deal that balances
-    // the warps' totals and, being known in advance, lets every fetch be prefetched: the
-    // block ids of the next unit C sit in lane registers and the descriptor of the unit
-    // after it is in flight while unit P is being issued.  (An atomic work queue would
-    // either expose its round trip at every unit boundary or, with lookahead, commit the
-    // longest units to the warps that start first.)
-    const int NWT = gridDim.x * NW;
-    const int wg = blockIdx.x * NW + warp;
-    auto unit_of = [&](int r) -> int { return r * NWT + ((r & 1) ? NWT - 1 - wg : wg); };
-    auto load_desc = [&](int gi) -> int4 {
-        return gi < total ? __ldcg(&p.items[gi / H]) : make_int4(-1, 0, 0, 0);
-    };
-    // block id of logical block jb0 + lane of the unit (s, p0, p1); -1 past the range
-    auto load_bids = [&](int s, int p0, int p1) -> int {
-        const int jb0 = p0 >> log2B;
-        const int nb = p1 > p0 ? ((p1 - 1) >> log2B) - jb0 + 1 : 0;
-        return lane < nb ? __ldg(p.block_tables + (int64_t)s * p.W + jb0 + lane) : -1;
-    };
-    int round = 0;
-    // unit C (the next one for P) and unit N (the one after C; descriptor in flight)
-    int cg = unit_of(0);
-    int4 cd = load_desc(cg);
-    int ng = unit_of(1);
-    int4 nd = load_desc(ng);
-    int cs = cd.x, cpart = cd.y, cctx = cd.z;
-    int cbid = cs >= 0 ? load_bids(cs, cpart * PT, min(cctx, cpart * PT + PT)) : -1;
-
-    // producer state: current unit P
-    bool pr_done = false, pr_have = false;
-    int pr_slot = 0, queued = 0, pr_tile = 0, pr_ntiles = 0, st_issue = 0, in_flight = 0;
-    int pr_s = 0, pr_h = 0, pr_p0 = 0, pr_pc = 0, pr_tnew = -1, pr_bid = -1;
-    // consumer state
-    bool c_have = false;
-    int cs_slot = 0, c_tile = 0, st_cons = 0;
-    uint32_t phase = 0;
-    int c_s = 0, c_h = 0, c_part = 0, c_p0 = 0, c_p1 = 0, c_tnew = -1, c_nparts = 1, c_ntiles = 0;
-    float m = -INFINITY, l = 0.f;
-    float2 acc[EPC];
-#pragma unroll
-    for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
-    uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-
-    while (true) {
-        // ---------------- producer: keep up to STG tiles in flight -------------------
-        while (!pr_done && in_flight < STG) {
-            if (!pr_have || pr_tile == pr_ntiles) {
-                pr_have = false;
-                if (queued == RING) break;
-                if (cs < 0) {  // no unit left
-                    pr_done = true;
-                    break;
-                }
-                // P <- C
-                const int s = cs, part = cpart, ctx = cctx, h = cg - (cg / H) * H;
-                const int p0 = part * PT, p1 = min(ctx, p0 + PT);
-                const int ntiles = p1 > p0 ? (p1 - p0 + kTile - 1) / kTile : 0;
-                const int nparts = ctx > 0 ? (ctx + PT - 1) / PT : 1;
-                const int t_new = (p.new_key != nullptr && ctx > 0 && p1 == ctx) ? ctx - 1 : -1;
-                pr_bid = cbid;
-                // C <- N (descriptor loaded one switch ago); its block ids start loading now
-                cg = ng;
-                cs = nd.x; cpart = nd.y; cctx = nd.z;
-                cbid = cs >= 0 ? load_bids(cs, cpart * PT, min(cctx, cpart * PT + PT)) : -1;
-                // N <- the unit after; its descriptor starts loading now
-                ++round;
-                ng = unit_of(round + 1);
-                nd = load_desc(ng);
-                if (lane == 0) {
-                    int* d = ring + pr_slot * DESC;
-                    d[0] = s; d[1] = h; d[2] = part; d[3] = p0; d[4] = p1; d[5] = t_new; d[6] = nparts; d[7] = ntiles;
-                }
-                __syncwarp();
-                pr_slot = (pr_slot + 1 == RING) ? 0 : pr_slot + 1;
-                ++queued;
-                pr_have = true;
-                pr_tile = 0;
-                pr_ntiles = ntiles;
-                pr_s = s; pr_h = h; pr_p0 = p0; pr_tnew = t_new; pr_pc = t_new >= 0 ? t_new : p1;
-                continue;
-            }
-            const int tok0 = pr_p0 + pr_tile * kTile;
-            const int kvh = pr_h / p.G;
-            char* sK = wst + st_issue * SB;
-            char* sV = sK + kTile * RB;
-            const bool has_new = pr_tnew >= tok0 && pr_tnew < tok0 + kTile;
-            const char* q_src = pr_tile == 0 ? static_cast<const char*>(p.query) + ((int64_t)pr_s * H + pr_h) * RB
-                                             : nullptr;
-            const char* nk = has_new ? static_cast<const char*>(p.new_key) + ((int64_t)pr_s * p.H_kv + kvh) * RB : nullptr;
-            const char* nvp = has_new ? static_cast<const char*>(p.new_value) + ((int64_t)pr_s * p.H_kv + kvh) * RB
-                                      : nullptr;
-            // block id of this tile from the prefetched lane registers (B >= 16: one block per tile)
-            const int bidx = (tok0 >> log2B) - (pr_p0 >> log2B);
-            const int blk = __shfl_sync(0xffffffffu, pr_bid, bidx & 31);
-            issue_tile_p(sK, sV, &bars[st_issue], kc, vc, p.block_tables + (int64_t)pr_s * p.W, tok0, pr_pc, log2B,
-                         blk_stride, ((int64_t)kvh << log2B) * RB, RB, lane, q_src, sV + kTile * RB, nk, nvp,
-                         pr_tnew - tok0, (bidx < 32 && blk >= 0) ? blk : -1);
-            ++pr_tile;
-            st_issue = (st_issue + 1 == STG) ? 0 : st_issue + 1;
-            ++in_flight;
-        }
-
-        // ---------------- consumer ----------------------------------------------------
-        if (!c_have) {
-            if (queued == 0) {
-                if (pr_done) break;
-                continue;
-            }
-            const int* d = ring + cs_slot * DESC;
-            c_s = d[0]; c_h = d[1]; c_part = d[2]; c_p0 = d[3]; c_p1 = d[4]; c_tnew = d[5]; c_nparts = d[6];
-            c_ntiles = d[7];
-            c_have = true;
-            c_tile = 0;
-            m = -INFINITY;
-            l = 0.f;
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
-        }
-        if (c_tile < c_ntiles) {
-            const int tok0 = c_p0 + c_tile * kTile;
-            const int nv = min(kTile, c_p1 - tok0);
-            const char* sK = wst + st_cons * SB;
-            const char* sV = sK + kTile * RB;
-            mbar_wait(&bars[st_cons], phase);
-            if (c_tile == 0) {
-                const char* sQ = sV + kTile * RB;
-                q0 = lds128(sQ + c * 16);
-                q1 = lds128(sQ + (c + LT) * 16);
-            }
-            tile_update<T, D>(sK, sV, nv, q0, q1, p.scale_log2, g, c, m, l, acc);
-            if (c_tnew >= tok0 && c_tnew < tok0 + kTile && c_h % p.G == 0 && g == 0)
-                write_new_token<T, D>(p, sK + (c_tnew - tok0) * RB, sV + (c_tnew - tok0) * RB, c_s, c_h / p.G, c_tnew,
-                                      c);
-            __syncwarp();
-            ++c_tile;
-            --in_flight;
-            if (++st_cons == STG) {
-                st_cons = 0;
-                phase ^= 1u;
-            }
-        }
-        if (c_tile == c_ntiles) {
-            merge_token_groups<T, D>(m, l, acc);
-            const int64_t sh = (int64_t)c_s * H + c_h;
-            if (c_nparts == 1) {
-                if (g == 0) store_out_p<T, D>(p, sh, l, acc, c);
-            } else {
-                finish_split<T, D>(p, sh, c_part, c_nparts, m, l, acc, g, c, lane);
-            }
-            c_have = false;
-            cs_slot = (cs_slot + 1 == RING) ? 0 : cs_slot + 1;
-            --queued;
-        }
-    }
-}
-
-// ================================================================== grid scheduler ===
-
-// One warp streams the partition [p0, p1) of nu query heads h_first + u*h_step of
-// sequence s, tile after tile with no break between heads: the copies of the next
-// head's first tiles are in flight while the current head finishes (its q row is
-// prefetched into registers one head ahead).  Block ids come from shared memory.
-template <typename T, int D>
-__device__ __forceinline__ void stream_heads(const AttnParams& p, int s, int part, int nparts, int p0, int p1,
-                                             int t_new, const int* sbt, int jb0, char* stage0, uint64_t* wbars,
-                                             int lane, int h_first, int h_step, int nu) {
-    using C = AttnCfg<T, D>;
-    constexpr int RB = C::RB, LT = C::LT, EPC = C::EPC;
-    const int STG = p.STG;
-    const int ntiles = p1 > p0 ? (p1 - p0 + kTile - 1) / kTile : 0;
-    const int g = lane / LT, c = lane % LT;
-    const char* kc = static_cast<const char*>(p.key_cache);
-    const char* vc = static_cast<const char*>(p.value_cache);
-    const int64_t blk_bytes = ((int64_t)p.H_kv << p.log2B) * RB;
-    const int pc = t_new >= 0 ? t_new : p1;  // cache rows copied end before the new token
-    float m, l;
-    float2 acc[EPC];
-
-    if (ntiles == 0) {  // empty context: zeros
-        if (g == 0)
-            for (int u = 0; u < nu; ++u)
-                store_out_p<T, D>(p, (int64_t)s * p.H + h_first + u * h_step, 0.f, acc, c);
-        return;
-    }
-    const int total = nu * ntiles;
-    // issue cursor (unit iu, tile ju)
-    int iu = 0, ju = 0;
-    auto issue_next = [&](int k) {
-        const int h = h_first + iu * h_step;
-        const int tok0 = p0 + ju * kTile;
-        issue_tile(stage0 + k * C::STAGE_BYTES, stage0 + k * C::STAGE_BYTES + kTile * RB, &wbars[k], kc, vc, sbt,
-                   jb0, tok0, max(0, min(kTile, pc - tok0)), pc, p.log2B, blk_bytes,
-                   ((int64_t)(h / p.G) << p.log2B) * RB, RB, lane);
-        if (++ju == ntiles) {
-            ju = 0;
-            ++iu;
-        }
-    };
-    for (int i = 0; i < STG && i < total; ++i) issue_next(i);
-
-    auto qrow = [&](int h) {
-        return reinterpret_cast<const uint4*>(static_cast<const char*>(p.query) + ((int64_t)s * p.H + h) * RB);
-    };
-    uint4 qn0 = __ldg(qrow(h_first) + c), qn1 = __ldg(qrow(h_first) + c + LT);
-    uint4 q0 = qn0, q1 = qn1;
-    int k = 0, u = 0, j = 0, h = h_first;
-    uint32_t phase = 0;
-    for (int i = 0; i < total; ++i) {
-        if (j == 0) {  // a new head
-            h = h_first + u * h_step;
-            q0 = qn0;
-            q1 = qn1;
-            if (u + 1 < nu) {
-                const uint4* qr = qrow(h + h_step);
-                qn0 = __ldg(qr + c);
-                qn1 = __ldg(qr + c + LT);
-            }
-            m = -INFINITY;
-            l = 0.f;
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
-        }
-        const int tok0 = p0 + j * kTile;
-        const int nv = min(kTile, p1 - tok0);
-        char* sK = stage0 + k * C::STAGE_BYTES;
-        char* sV = sK + kTile * RB;
-        mbar_wait(&wbars[k], phase);
-        if (t_new >= tok0 && t_new < tok0 + kTile) {  // the new token's row (last tile)
-            const int kvh = h / p.G;
-            if (g == 0) {
-                const uint4* kr = reinterpret_cast<const uint4*>(static_cast<const char*>(p.new_key) +
-                                                                  ((int64_t)s * p.H_kv + kvh) * RB);
-                const uint4* vr = reinterpret_cast<const uint4*>(static_cast<const char*>(p.new_value) +
-                                                                  ((int64_t)s * p.H_kv + kvh) * RB);
-                uint4* rk = reinterpret_cast<uint4*>(sK + (t_new - tok0) * RB);
-                uint4* rv = reinterpret_cast<uint4*>(sV + (t_new - tok0) * RB);
-                rk[c] = __ldg(kr + c);
-                rk[c + LT] = __ldg(kr + c + LT);
-                rv[c] = __ldg(vr + c);
-                rv[c + LT] = __ldg(vr + c + LT);
-            }
-            __syncwarp();
-            if (h % p.G == 0 && g == 0)
-                write_new_token<T, D>(p, sK + (t_new - tok0) * RB, sV + (t_new - tok0) * RB, s, kvh, t_new, c);
-        }
-        tile_update<T, D>(sK, sV, nv, q0, q1, p.scale_log2, g, c, m, l, acc);
-        __syncwarp();
-        if (i + STG < total) issue_next(k);
-        if (++k == STG) {
-            k = 0;
-            phase ^= 1u;
-        }
-        if (++j == ntiles) {  // head finished
-            j = 0;
-            ++u;
-            merge_token_groups<T, D>(m, l, acc);
-            const int64_t sh = (int64_t)s * p.H + h;
-            if (nparts == 1) {
-                if (g == 0) store_out_p<T, D>(p, sh, l, acc, c);
-            } else {
-                finish_split<T, D>(p, sh, part, nparts, m, l, acc, g, c, lane);
-            }
-        }
-    }
-}
-
-// One CTA = (partition, group of HPC*HPW query heads, sequence).  Warp w streams heads
-// base + w, base + w + HPC, ... (HPW of them), so at any moment the CTA's warps read
-// neighbouring heads of the same blocks.
-template <typename T, int D>
-__global__ void __launch_bounds__(256) paged_attention_kernel(const AttnParams p) {
-    using C = AttnCfg<T, D>;
-    extern __shared__ __align__(128) unsigned char smem[];
-
-    const int part = blockIdx.x, hg = blockIdx.y, s = blockIdx.z;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int HPC = p.HPC, STG = p.STG;
-    const int h_first = hg * HPC * p.HPW + warp;
-    const int nu = h_first < p.H ? min(p.HPW, (p.H - h_first + HPC - 1) / HPC) : 0;
-    pdl_wait();
-    const int ctx = p.context_lens[s];
-    const int p0 = part * p.PT;
-    if (part > 0 && p0 >= ctx) return;  // this sequence has fewer partitions (CTA-uniform)
-    const int p1 = min(ctx, p0 + p.PT);
-    const int nparts = ctx > 0 ? (ctx + p.PT - 1) / p.PT : 1;
-
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)HPC * STG * C::STAGE_BYTES);
-    int* sbt = reinterpret_cast<int*>(bars + HPC * STG);
-    const int jb0 = p0 >> p.log2B;
-    const int nb = p1 > p0 ? ((p1 - 1) >> p.log2B) - jb0 + 1 : 0;
-    const int32_t* btrow = p.block_tables + (int64_t)s * p.W;
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) sbt[i] = __ldg(btrow + jb0 + i);
-    if (threadIdx.x < HPC * STG) mbar_init(&bars[threadIdx.x], 1);
-    fence_mbar_init();
-    __syncthreads();
-    if (nu == 0) return;
-    const int t_new = (p.new_key != nullptr && ctx > 0 && p1 == ctx) ? ctx - 1 : -1;
-    stream_heads<T, D>(p, s, part, nparts, p0, p1, t_new, sbt, jb0,
-                       reinterpret_cast<char*>(smem) + (size_t)warp * STG * C::STAGE_BYTES, bars + warp * STG, lane,
-                       h_first, HPC, nu);
 }
 
 // ================================================================== coop scheduler ===
@@ -816,23 +380,14 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
 #ifdef PA_DECODE_TRACE
     if (threadIdx.x == 0) DEC_T(0, gtimer());
 #endif
-    int hg, s, ctx, c0;
     int bt_pref = 0;  // producer lane i: block id jb0 + i, loaded while ctx is in flight
-    if (p.listed) {  // CTA = one entry of the longest-first work list x head group
-        const int NG = (p.H + HPC - 1) / HPC;
-        const int idx = blockIdx.x;
-        if (idx >= __ldcg(p.n_items) * NG) return;  // past the list (CTA-uniform)
-        const int4 it = __ldcg(&p.items[idx / NG]);
-        hg = idx - (idx / NG) * NG;
-        s = it.x;
-        c0 = it.y;
-        ctx = it.z;
-    } else {
-        hg = p.pz ? blockIdx.x : blockIdx.y;
-        s = p.pz ? blockIdx.y : blockIdx.z;
-        // this CTA walks the arithmetic partitions [c0, c0 + PPC) of the context back to
-        // back; each is finished exactly as if it had its own CTA (bitwise identical)
-        c0 = (p.pz ? blockIdx.z : blockIdx.x) * p.PPC;
+    const int hg = p.pz ? blockIdx.x : blockIdx.y;
+    const int s = p.pz ? blockIdx.y : blockIdx.z;
+    // this CTA walks the arithmetic partitions [c0, c0 + PPC) of the context back to
+    // back; each is finished exactly as if it had its own CTA (bitwise identical)
+    const int c0 = (p.pz ? blockIdx.z : blockIdx.x) * p.PPC;
+    int ctx;
+    {
         // the partition's first 32 block ids depend only on (s, c0): the producer loads
         // them (in-row entries past the context are read, never used) in parallel with
         // context_lens[s] instead of after it -- one dependent global round trip less
@@ -872,7 +427,7 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
         const int jb0 = p0 >> p.log2B;
         const int nb = p1 > p0 ? ((p1 - 1) >> p.log2B) - jb0 + 1 : 0;
         const int32_t* btrow = p.block_tables + (int64_t)s * p.W;
-        if (lane < nb) sbt[lane] = p.listed ? __ldg(btrow + jb0 + lane) : bt_pref;
+        if (lane < nb) sbt[lane] = bt_pref;
         for (int i = 32 + lane; i < nb; i += 32) sbt[i] = __ldg(btrow + jb0 + i);
         __syncwarp();
         const int B = 1 << p.log2B;
@@ -1010,241 +565,6 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
         DEC_T(3, (unsigned long long)smid | ((unsigned long long)ntiles << 16) | ((unsigned long long)s << 32));
     }
 #endif
-}
-
-// ======================================================= persistent coop scheduler ===
-//
-// The coop CTA made persistent: a grid of occupancy x SMs CTAs, each with one producer
-// warp and HPC consumer warps, walks the longest-first work list of (sequence,
-// partition, head group) items (build_worklist_kernel).  The producer claims items with
-// one atomic each (the next claim is in flight while the current item's tiles are
-// issued), prefetches the item's block ids, and streams its tiles into the shared
-// stages; each stage carries the item descriptor and, for an item's first tile, the
-// group's q rows, so consumers never touch global memory before computing.  Consumers
-// see one continuous stream of tiles across items -- no CTA prologue or epilogue
-// bubbles -- and the list order makes the tail the shortest items.
-struct StageMeta {
-    int s, h0, nh, part, p0, p1, t_new, nparts, j, ntiles, kvh0, pad[5];
-};
-
-template <typename T, int D>
-__global__ void __launch_bounds__(288) paged_attention_pcoop_kernel(const AttnParams p) {
-    using C = AttnCfg<T, D>;
-    constexpr int RB = C::RB, LT = C::LT, EPC = C::EPC;
-    extern __shared__ __align__(128) unsigned char smem[];
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int HPC = p.HPC, STG = p.STG, G = p.G, H = p.H, PT = p.PT;
-    const int NKVmax = HPC % G == 0 ? HPC / G : (HPC + G - 1) / G + 1;
-    const int slab = kTile * RB;
-    const int kv_bytes = 2 * NKVmax * slab;
-    const int stage_bytes = (kv_bytes + HPC * RB + (int)sizeof(StageMeta) + 127) / 128 * 128;  // K | V | q | meta
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STG * stage_bytes);
-    uint64_t* empty = full + STG;
-    int* sbt = reinterpret_cast<int*>(empty + STG);
-    if (threadIdx.x < STG) {
-        mbar_init(&full[threadIdx.x], 1);
-        mbar_init(&empty[threadIdx.x], HPC);
-    }
-    fence_mbar_init();
-    __syncthreads();
-    pdl_wait();  // work list and counters built, this step's copy_blocks done
-
-    auto stage_ptr = [&](int k) { return reinterpret_cast<char*>(smem) + (size_t)k * stage_bytes; };
-    auto meta_ptr = [&](int k) { return reinterpret_cast<StageMeta*>(stage_ptr(k) + kv_bytes + HPC * RB); };
-    const int NG = (H + HPC - 1) / HPC;
-
-    if (warp == HPC) {  // ================================================ producer warp
-        // natural order (p.natural): item g = (sequence, partition, head group) in grid
-        // order, descriptor from context_lens -- no work list, no list-building launch
-        const int total = p.natural ? p.S * p.NP * NG : __ldcg(p.n_items) * NG;
-        const int B = 1 << p.log2B;
-        const char* kc = static_cast<const char*>(p.key_cache);
-        const char* vc = static_cast<const char*>(p.value_cache);
-        const int64_t blk_bytes = ((int64_t)p.H_kv << p.log2B) * RB;
-        const int pieces = B >= kTile ? 1 : kTile / B;
-        int k = 0, uses = 0;  // stage cursor, stages issued so far
-        auto next_stage = [&](uint64_t*& fb) -> char* {
-            if (uses >= STG) mbar_wait(&empty[k], ((uses / STG) - 1) & 1);
-            fb = &full[k];
-            return stage_ptr(k);
-        };
-        auto advance = [&]() {
-            ++uses;
-            if (++k == STG) k = 0;
-        };
-        // Item pipeline: while item `cur` is being issued, the descriptor and block ids
-        // of the next item are fetched (right after cur's first tile is queued) and
-        // the claim of the one after is in flight.  sbt is double-buffered.
-        const int tbl = PT / B + 2;
-        auto fetch1 = [&](int g, int buf, int4& d) {  // descriptor + block ids of item g
-            int pre = 0;
-            if (p.natural) {  // the first 32 block ids load in parallel with context_lens[s]
-                const int ii = g / NG, sq = ii / p.NP, part = ii - sq * p.NP;
-                const int jb = (part * PT) >> p.log2B;
-                if (jb + lane < p.W) pre = __ldg(p.block_tables + (int64_t)sq * p.W + jb + lane);
-                d = make_int4(sq, part, __ldg(p.context_lens + sq), 0);
-            } else {
-                d = __ldcg(&p.items[g / NG]);
-                const int jb = (d.y * PT) >> p.log2B;
-                if (jb + lane < p.W) pre = __ldg(p.block_tables + (int64_t)d.x * p.W + jb + lane);
-            }
-            const int p0 = d.y * PT, p1 = min(d.z, p0 + PT);
-            const int jb0 = p0 >> p.log2B;
-            const int nb = p1 > p0 ? ((p1 - 1) >> p.log2B) - jb0 + 1 : 0;
-            const int32_t* btrow = p.block_tables + (int64_t)d.x * p.W;
-            if (lane < nb) sbt[buf * tbl + lane] = pre;
-            for (int i = 32 + lane; i < nb; i += 32) sbt[buf * tbl + i] = __ldg(btrow + jb0 + i);
-            __syncwarp();
-        };
-        // natural order: partitions past a context are not items; claim on until one is
-        auto fetch = [&](int& g, int buf, int4& d) {
-            fetch1(g, buf, d);
-            while (p.natural && d.y > 0 && d.y * PT >= d.z) {
-                int gg = 0;
-                if (lane == 0) gg = atom_add_global(p.work_counter, 1);
-                g = __shfl_sync(0xffffffffu, gg, 0);
-                if (g >= total) return;
-                fetch1(g, buf, d);
-            }
-        };
-        int gi = 0, gn = 0, buf = 0;
-        if (lane == 0) gi = atom_add_global(p.work_counter, 1);
-        gi = __shfl_sync(0xffffffffu, gi, 0);
-        int4 it = make_int4(-1, 0, 0, 0);
-        if (gi < total) fetch(gi, 0, it);
-        if (lane == 0) gn = atom_add_global(p.work_counter, 1);  // in flight
-        while (gi < total) {
-            const int hg = gi - (gi / NG) * NG;
-            const int s = it.x, part = it.y, ctx = it.z;
-            const int p0 = part * PT, p1 = min(ctx, p0 + PT);
-            const int ntiles = p1 > p0 ? (p1 - p0 + kTile - 1) / kTile : 0;
-            const int nparts = ctx > 0 ? (ctx + PT - 1) / PT : 1;
-            const int t_new = (p.new_key != nullptr && ctx > 0 && p1 == ctx) ? ctx - 1 : -1;
-            const int pc = t_new >= 0 ? t_new : p1;
-            const int h0 = hg * HPC, nh = min(HPC, H - h0);
-            const int kvh0 = h0 / G, NKV = (h0 + nh - 1) / G - kvh0 + 1;
-            const int jb0 = p0 >> p.log2B;
-            const int* cbt = sbt + buf * tbl;
-            StageMeta meta{s, h0, nh, part, p0, p1, t_new, nparts, 0, ntiles, kvh0, {0, 0, 0, 0, 0}};
-            int gnext = total;
-            int4 itn = make_int4(-1, 0, 0, 0);
-            for (int j = 0; j < max(ntiles, 1); ++j) {  // an empty context still posts one stage
-                uint64_t* fb;
-                char* sK = next_stage(fb);
-                char* sV = sK + NKVmax * slab;
-                char* sQ = sK + kv_bytes;
-                const int tok0 = p0 + j * kTile;
-                const int nvc = ntiles ? max(0, min(kTile, pc - tok0)) : 0;
-                const bool has_new = ntiles && t_new >= tok0 && t_new < tok0 + kTile;
-                if (lane == 0) {
-                    meta.j = j;
-                    *meta_ptr(k) = meta;
-                    mbar_arrive_expect_tx(fb, (uint32_t)(2 * NKV * (nvc + (has_new ? 1 : 0)) * RB +
-                                                         (j == 0 && ntiles ? nh * RB : 0)));
-                }
-                __syncwarp();
-                if (j == 0 && ntiles && lane < nh)
-                    bulk_g2s(sQ + lane * RB, static_cast<const char*>(p.query) + ((int64_t)s * H + h0 + lane) * RB, RB,
-                             fb);
-                if (B == kTile && nvc == kTile) {
-                    if (lane == 0) {
-                        const int64_t off = (int64_t)cbt[(tok0 >> p.log2B) - jb0] * blk_bytes + (int64_t)kvh0 * slab;
-                        bulk_g2s(sK, kc + off, (uint32_t)(NKV * slab), fb);
-                        bulk_g2s(sV, vc + off, (uint32_t)(NKV * slab), fb);
-                    }
-                } else if (nvc > 0) {
-                    for (int w = lane; w < NKV * pieces; w += 32) {
-                        const int kh = w / pieces, pi = w - kh * pieces;
-                        const int tk = tok0 + pi * min(B, kTile);
-                        if (tk >= pc) continue;
-                        const int rows = min(min(B, kTile), pc - tk);
-                        const int64_t off = (int64_t)cbt[(tk >> p.log2B) - jb0] * blk_bytes +
-                                            ((int64_t)(kvh0 + kh) << p.log2B) * RB + (int64_t)(tk & (B - 1)) * RB;
-                        const int dst = kh * slab + (tk - tok0) * RB;
-                        bulk_g2s(sK + dst, kc + off, (uint32_t)(rows * RB), fb);
-                        bulk_g2s(sV + dst, vc + off, (uint32_t)(rows * RB), fb);
-                    }
-                }
-                if (has_new && lane < NKV) {
-                    const int64_t src = ((int64_t)s * p.H_kv + kvh0 + lane) * RB;
-                    const int dst = lane * slab + (t_new - tok0) * RB;
-                    bulk_g2s(sK + dst, static_cast<const char*>(p.new_key) + src, RB, fb);
-                    bulk_g2s(sV + dst, static_cast<const char*>(p.new_value) + src, RB, fb);
-                }
-                __syncwarp();
-                advance();
-                if (j == 0) {  // the first tile is queued: fetch the next item meanwhile
-                    gnext = __shfl_sync(0xffffffffu, gn, 0);
-                    if (gnext < total) fetch(gnext, buf ^ 1, itn);  // may claim on (natural order)
-                    if (lane == 0) gn = atom_add_global(p.work_counter, 1);
-                }
-            }
-            gi = gnext;
-            it = itn;
-            buf ^= 1;
-        }
-        // termination marker for the consumers
-        uint64_t* fb;
-        next_stage(fb);
-        if (lane == 0) {
-            meta_ptr(k)->s = -1;
-            mbar_arrive_expect_tx(fb, 0);
-        }
-        return;
-    }
-
-    // ============================================================== consumer warps
-    const int g = lane / LT, c = lane % LT;
-    int k = 0;
-    uint32_t phase = 0;
-    float m = -INFINITY, l = 0.f;
-    float2 acc[EPC];
-    uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-    while (true) {
-        mbar_wait(&full[k], phase);
-        const StageMeta* mp = meta_ptr(k);
-        const int s = mp->s;
-        if (s < 0) break;
-        const int nh = mp->nh, j = mp->j, ntiles = mp->ntiles;
-        const bool active = warp < nh;
-        const int h = mp->h0 + warp;
-        const char* sK = stage_ptr(k) + (h / G - mp->kvh0) * slab;
-        const char* sV = sK + NKVmax * slab;
-        if (j == 0) {
-            m = -INFINITY;
-            l = 0.f;
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) acc[e] = make_float2(0.f, 0.f);
-            if (active && ntiles) {
-                const char* sQ = stage_ptr(k) + kv_bytes + warp * RB;
-                q0 = lds128(sQ + c * 16);
-                q1 = lds128(sQ + (c + LT) * 16);
-            }
-        }
-        const int p0 = mp->p0, p1 = mp->p1, t_new = mp->t_new, part = mp->part, nparts = mp->nparts;
-        if (active && ntiles) {
-            const int tok0 = p0 + j * kTile;
-            if (t_new >= tok0 && t_new < tok0 + kTile && h % G == 0 && g == 0)
-                write_new_token<T, D>(p, sK + (t_new - tok0) * RB, sV + (t_new - tok0) * RB, s, h / G, t_new, c);
-            tile_update<T, D>(sK, sV, min(kTile, p1 - tok0), q0, q1, p.scale_log2, g, c, m, l, acc);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[k]);
-        if (++k == STG) {
-            k = 0;
-            phase ^= 1u;
-        }
-        if (active && j >= ntiles - 1) {  // last tile of the item (or an empty context)
-            merge_token_groups<T, D>(m, l, acc);
-            const int64_t sh = (int64_t)s * H + h;
-            if (nparts == 1) {
-                if (g == 0) store_out_p<T, D>(p, sh, l, acc, c);
-            } else {
-                finish_split<T, D>(p, sh, part, nparts, m, l, acc, g, c, lane);
-            }
-        }
-    }
 }
 
 // ========================================= sharing-aware scheduler ===
@@ -1843,7 +1163,10 @@ __global__ void __launch_bounds__(32 * (2 * HG + 1), HG == 1 ? PA_GROUP_MINB : P
         if (np_r == 1 || p0 >= ctx_r) continue;
         const int64_t shr = (int64_t)(s0 + r) * p.H + h;
         int last = 0;
-        if (lane == 0) last = atomicAdd(p.counters + shr, 1) == min(np_r, p.NP) - 1;
+        if (lane == 0) {
+            __threadfence();
+            last = split_arrive(p, shr, min(np_r, p.NP));
+        }
         last = __shfl_sync(FULL, last, 0);
         if (last) {
             __threadfence();
@@ -1857,17 +1180,8 @@ cudaError_t launch_group_mma(const GroupParams& p, int dtype, int num_seqs, size
     auto kern = dtype == 1 ? (HG == 2 ? paged_attention_group_mma_kernel<__half, 2> : paged_attention_group_mma_kernel<__half, 1>)
                            : (HG == 2 ? paged_attention_group_mma_kernel<__nv_bfloat16, 2>
                                       : paged_attention_group_mma_kernel<__nv_bfloat16, 1>);
-    static size_t configured[4] = {0, 0, 0, 0};
-    const int ci = (dtype == 1 ? 0 : 1) + 2 * (HG - 1);
-    if (smem > configured[ci]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured[ci] = smem;
-    }
-    if (p.a.NP > 1) {
-        cudaError_t e = cudaMemsetAsync(p.a.counters, 0, sizeof(int) * (size_t)num_seqs * p.a.H, stream);
-        if (e != cudaSuccess) return e;
-    }
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
+    if (e != cudaSuccess) return e;
     const dim3 grid(p.a.NP, p.a.H / HG, (num_seqs + p.a.GM - 1) / p.a.GM);
     return launch_k(kern, grid, dim3(32 * (2 * HG + 1)), smem, stream, p);
 }
@@ -1930,158 +1244,33 @@ size_t attention_smem_bytes_coop(int row_bytes, int hpc, int G, int stg, int par
     return head + (size_t)hpc * ppc * ((size_t)head_dim * 4 + 8);  // in-CTA partials
 }
 
-size_t attention_smem_bytes_pcoop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size) {
-    const int nkv_max = hpc % G == 0 ? hpc / G : (hpc + G - 1) / G + 1;
-    const size_t stage = (2 * nkv_max * kTile * (size_t)row_bytes + (size_t)hpc * row_bytes + sizeof(StageMeta) + 127) /
-                         128 * 128;
-    const size_t tbl = 2 * 4 * (size_t)(partition_tokens / block_size + 2);  // double-buffered block ids
-    return (size_t)stg * stage + 16 * (size_t)stg + tbl;
-}
-
 size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int gm, int nsl) {
     const int nkv_max = hpc % G == 0 ? hpc / G : (hpc + G - 1) / G + 1;
     const size_t stage = (size_t)nsl * 2 * nkv_max * kTile * row_bytes + 16 * (size_t)((gm + 16) / 16) * 4;
     return (size_t)stg * stage + 16 * (size_t)stg;
 }
 
-size_t attention_smem_bytes(bool persistent, int row_bytes, int nw, int stg, int partition_tokens, int block_size) {
-    if (persistent) {
-        const size_t sb = 2 * kTile * (size_t)row_bytes + row_bytes;
-        return (size_t)nw * stg * sb + 8 * (size_t)nw * stg + 4 * 8 * (size_t)nw * (stg + 2);
-    }
-    const size_t tbl = 4 * (size_t)(partition_tokens / block_size + 2);
-    return (size_t)nw * stg * (2 * kTile * (size_t)row_bytes) + 8 * (size_t)nw * stg + tbl;
-}
-
 template <typename T, int D>
 static cudaError_t launch_attention_t(const AttnParams& p, int num_seqs, int sched, size_t smem,
                                       cudaStream_t stream) {
-    const bool persistent = sched == 1;
     if (sched == 4) {  // sharing-aware: groups of GM consecutive sequences
         auto kern = paged_attention_shared_kernel<T, D>;
-        static size_t configured = 0;
-        if (smem > configured) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            configured = smem;
-        }
-        if (p.NP > 1) {
-            cudaError_t e = cudaMemsetAsync(p.counters, 0, sizeof(int) * (size_t)num_seqs * p.H, stream);
-            if (e != cudaSuccess) return e;
-        }
+        cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
+        if (e != cudaSuccess) return e;
         const int groups = (p.H + p.HPC - 1) / p.HPC;
         const int sgroups = (num_seqs + p.GM - 1) / p.GM;
         return launch_k(kern, dim3(p.NP, groups, sgroups), dim3((p.GM * p.HPC + 1) * 32), smem, stream, p);
     }
-    if (sched == 3) {  // persistent coop
-        auto kern = paged_attention_pcoop_kernel<T, D>;
-        static size_t configured = 0;
-        static int cached_blocks = 0, cached_smem = -1, cached_threads = -1;
-        if (smem > configured) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            configured = smem;
-        }
-        const int threads = (p.HPC + 1) * 32;
-        if ((int)smem != cached_smem || threads != cached_threads) {
-            int nb = 0;
-            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
-            if (e != cudaSuccess) return e;
-            cached_blocks = nb > 0 ? nb : 1;
-            cached_smem = (int)smem;
-            cached_threads = threads;
-        }
-        int dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t items = (int64_t)num_seqs * p.NP * ((p.H + p.HPC - 1) / p.HPC);
-        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)cached_blocks * sms, items));
-        cudaError_t e;
-        if (p.natural) {  // no work list: zero the claim counter (and the split counters)
-            e = cudaMemsetAsync(p.work_counter, 0, sizeof(int), stream);
-            if (e == cudaSuccess && p.NP > 1)
-                e = cudaMemsetAsync(p.counters, 0, sizeof(int) * (size_t)num_seqs * p.H, stream);
-        } else {
-            e = launch_k(build_worklist_kernel, dim3(1), dim3(1024), 0, stream, p, num_seqs);
-        }
-        if (e != cudaSuccess) return e;
-        return launch_k(kern, dim3((unsigned)grid), dim3(threads), smem, stream, p);
-    }
-    if (sched == 5) {  // listed coop: one CTA per (work-list entry, head group), longest first
-        auto kern = paged_attention_coop_kernel<T, D>;
-        static size_t configured = 0;
-        if (smem > configured) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            configured = smem;
-        }
-        const int groups = (p.H + p.HPC - 1) / p.HPC;
-        cudaError_t e = launch_k(build_worklist_kernel, dim3(1), dim3(1024), 0, stream, p, num_seqs);
-        if (e != cudaSuccess) return e;
-        return launch_k(kern, dim3((unsigned)((int64_t)num_seqs * p.NP * groups)), dim3((p.HPC + 1) * 32), smem,
-                        stream, p);
-    }
-    if (sched == 2) {  // coop: HPC consumer warps + 1 producer warp per CTA
-        auto kern = paged_attention_coop_kernel<T, D>;
-        static size_t configured = 0;
-        if (smem > configured) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            configured = smem;
-        }
-        if (p.NP > 1) {
-            cudaError_t e = cudaMemsetAsync(p.counters, 0, sizeof(int) * (size_t)num_seqs * p.H, stream);
-            if (e != cudaSuccess) return e;
-        }
-        const int groups = (p.H + p.HPC - 1) / p.HPC;
-        if (p.pz)  // partition index slowest: partitions >= 1 (and the empty ones) launch last
-            return launch_k(kern, dim3(groups, num_seqs, (p.NP + p.PPC - 1) / p.PPC), dim3((p.HPC + 1) * 32), smem,
-                            stream, p);
-        return launch_k(kern, dim3((p.NP + p.PPC - 1) / p.PPC, groups, num_seqs), dim3((p.HPC + 1) * 32), smem,
-                        stream, p);
-    }
-    if (!persistent) {
-        auto kern = paged_attention_kernel<T, D>;
-        static size_t configured = 0;
-        if (smem > configured) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            configured = smem;
-        }
-        if (p.NP > 1) {
-            cudaError_t e = cudaMemsetAsync(p.counters, 0, sizeof(int) * (size_t)num_seqs * p.H, stream);
-            if (e != cudaSuccess) return e;
-        }
-        const int groups = (p.H + p.HPC * p.HPW - 1) / (p.HPC * p.HPW);
-        return launch_k(kern, dim3(p.NP, groups, num_seqs), dim3(p.HPC * 32), smem, stream, p);
-    }
-    auto kern = paged_attention_persistent_kernel<T, D>;
-    static size_t configured = 0;
-    static int cached_blocks = 0, cached_smem = -1, cached_threads = -1;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
-    const int threads = p.HPC * 32;
-    if ((int)smem != cached_smem || threads != cached_threads) {
-        int nb = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
-        if (e != cudaSuccess) return e;
-        cached_blocks = nb > 0 ? nb : 1;
-        cached_smem = (int)smem;
-        cached_threads = threads;
-    }
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t units = (int64_t)num_seqs * p.NP * p.H;
-    const int64_t warps_wanted = (units + 1) / 2;  // >= 2 units per warp on average
-    int64_t grid = (int64_t)cached_blocks * sms;
-    grid = std::min<int64_t>(grid, std::max<int64_t>(1, (warps_wanted + p.HPC - 1) / p.HPC));
-    cudaError_t e = launch_k(build_worklist_kernel, dim3(1), dim3(1024), 0, stream, p, num_seqs);
+    // coop: HPC consumer warps + 1 producer warp per CTA
+    auto kern = paged_attention_coop_kernel<T, D>;
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
-    return launch_k(kern, dim3((unsigned)grid), dim3(threads), smem, stream, p);
+    const int groups = (p.H + p.HPC - 1) / p.HPC;
+    if (p.pz)  // partition index slowest: partitions >= 1 (and the empty ones) launch last
+        return launch_k(kern, dim3(groups, num_seqs, (p.NP + p.PPC - 1) / p.PPC), dim3((p.HPC + 1) * 32), smem,
+                        stream, p);
+    return launch_k(kern, dim3((p.NP + p.PPC - 1) / p.PPC, groups, num_seqs), dim3((p.HPC + 1) * 32), smem, stream,
+                    p);
 }
 
 cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int sched, size_t smem,

@@ -44,10 +44,9 @@ struct AttnParams {
     void* value_cache_w;
     float2* part_ml;            // [S][H][NP] (m, L) in the exp2 domain (split only)
     float* part_o;              // [S][H][NP][D] normalised partial outputs (split only)
-    int* counters;              // [S][H] partitions finished (split only; zeroed by each call)
-    int* work_counter;          // persistent scheduler: next work unit
-    int* n_items;               // persistent scheduler: (sequence, partition) units in the list
-    int4* items;                // persistent scheduler: units (s, part, ctx, 0), longest first
+    unsigned long long* counters;  // [S][H] split completion words (epoch << 32 | partitions done);
+                                   // never zeroed by the host: see split_arrive (pa_attention.cu)
+    uint32_t epoch;             // this launch's nonzero 32-bit tag for the completion words
     float scale_log2;           // scale * log2(e)
     int log2B;                  // block_size = 1 << log2B
     int H, H_kv, G;             // query heads, kv heads, H / H_kv
@@ -55,13 +54,10 @@ struct AttnParams {
     int PT;                     // partition size in tokens (multiple of 16)
     int NP;                     // partitions in the grid = ceil(max_ctx / PT)
     int HPC;                    // warps per CTA
-    int HPW;                    // grid scheduler: query heads streamed by each warp
     int PPC;                    // coop scheduler: partitions walked by one CTA (scheduling only)
     int GM;                     // sharing-aware scheduler: sequences per group
     int S;                      // number of sequences
-    int listed;                 // coop: CTAs take (sequence, partition) from the work list
     int pz;                     // coop: grid (head group, sequence, partition), partitions slowest
-    int natural;                // pcoop: items in grid order from context_lens (no work list)
     int STG;                    // tiles in flight per warp (shared-memory stages)
     int GSL;                    // grouped / shared decode: block slots per stage (a tile with more distinct
                                 // blocks than GSL takes several stages)
@@ -119,7 +115,10 @@ struct SwapBlocksParams {
 };
 
 void count_launch();
-bool pdl_enabled();  // PA_PDL=0 disables programmatic dependent launch
+bool pdl_enabled();  // PA_PDL=0 (read once at load) disables programmatic dependent launch
+uint32_t next_epoch();  // nonzero, scrambled per-launch tag for split completion words
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device), thread-safe
+cudaError_t ensure_smem_attr(const void* kern, size_t smem);
 
 // Launch `kern` on `stream`, with programmatic stream serialisation when enabled.
 template <typename... KArgs, typename... Args>
@@ -140,18 +139,17 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 }
 
 int attention_row_bytes(int dtype, int head_dim);
-size_t attention_smem_bytes(bool persistent, int row_bytes, int nw, int stg, int partition_tokens, int block_size);
 size_t attention_smem_bytes_coop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size,
                                  int ppc, int head_dim);
-size_t attention_smem_bytes_pcoop(int row_bytes, int hpc, int G, int stg, int partition_tokens, int block_size);
 size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int gm, int nsl);
-// sched: 0 = grid, 1 = persistent, 2 = coop, 3 = persistent coop, 4 = sharing-aware groups, 5 = listed coop
+// sched: 2 = coop (default), 4 = sharing-aware groups of GM sequences
 cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int sched, size_t smem,
                              cudaStream_t stream);
 size_t group_mma_smem_bytes(int gm, int gsl, int stg, int pt, int hg);
 cudaError_t launch_group_mma(const GroupParams& p, int dtype, int num_seqs, size_t smem, cudaStream_t stream);
-size_t prefill_smem_bytes();
-cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, cudaStream_t stream);
+// variant: 0 = by max_query_len (default), 2 / 3 = force (PA_PREFILL ablation)
+cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, int variant,
+                           cudaStream_t stream);
 // N2: rank `rank` publishes `epoch` to every peer's flag array, then waits (bounded) until
 // every peer has published it to this rank; status = 1 on timeout
 cudaError_t launch_tp_signal_wait(int32_t* const* flag_peers, int world, int rank, int32_t epoch, int32_t* status,

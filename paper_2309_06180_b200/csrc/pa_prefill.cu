@@ -8,18 +8,17 @@
 // user's task input").  The new tokens' K/V are already in the cache
 // (pa_reshape_and_cache with a multi-token slot mapping, reading c5).
 //
-// One CTA = (tile of 128 query tokens, query head, sequence), 128 threads.  Thread 0
-// drives the Tensor Memory Accelerator and the tensor cores; every thread owns one
-// query row for the softmax:
-//   * Q tile [128 x 128] and, per 128-token KV tile, K and V ([128 x 128] each) are
-//     brought into shared memory by TMA tensor copies with the 128-byte swizzle (K and V
-//     gathered block by block through the block table), double-buffered;
+// Two persistent, warp-specialised kernels (one CTA per SM, TMA producer warp, tcgen05
+// MMA-issuer warp, softmax warp groups; thread = query row = tensor-memory lane):
+//   * Q tiles [128 x 128] and, per 128-token KV tile, K and V are brought into shared
+//     memory by TMA tensor copies with the 128-byte swizzle (K and V gathered block by
+//     block through the block table);
 //   * S = Q K^T by 8 tcgen05.mma (M=128, N=128, K=16) into tensor memory (fp32);
-//   * threads read S rows back with tcgen05.ld, apply scale + causal mask, online
-//     softmax in the exp2 domain, and write P (storage dtype) to shared memory in the
-//     swizzled K-major layout;
-//   * O_t = P V by 8 tcgen05.mma (B operand V read MN-major) into tensor memory; threads
-//     fold it into their fp32 O row: O = O*alpha + O_t.
+//   * softmax threads read S rows back with tcgen05.ld, apply scale + causal mask, online
+//     softmax in the exp2 domain, and write P (storage dtype) back into tensor memory;
+//   * O += P V by 8 tcgen05.mma (P from tensor memory, V read MN-major).
+// v2: two query tiles per work item share each K/V tile; v3: one query tile, its softmax
+// split by key columns over two warp groups.
 // P is rounded to the storage dtype before the second product (the FlashAttention
 // convention); the parity tolerance covers it.
 #include <cuda.h>
@@ -66,21 +65,6 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 }
 
 // 32 consecutive fp32 columns of this thread's TMEM lane (32x32b shape, x32)
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-    uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
     asm volatile(
@@ -180,215 +164,6 @@ constexpr int kN = 128;        // KV tokens per tile
 constexpr int kHalf = 128 * 128;  // bytes of one [128 rows][64 elements] swizzled half (2-byte elements)
 
 }  // namespace
-
-template <typename T>
-__global__ void __launch_bounds__(128, 1) paged_prefill_kernel(const __grid_constant__ PrefillParams p) {
-    constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-byte alignment for the swizzle atoms
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    unsigned char* sQ = smem;                   // [2 halves][128][64]
-    unsigned char* sK = smem + 2 * kHalf;       // [2 stages][2 halves][128][64]
-    unsigned char* sV = sK + 4 * kHalf;         // [2 stages][2 halves][128][64]
-    unsigned char* sP = sV + 4 * kHalf;         // [2 halves][128][64]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kHalf);  // q, kv[2], mma
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
-
-    const int qt = blockIdx.x, h = blockIdx.y, s = blockIdx.z;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    pdl_wait();
-    const int qs = p.query_start[s], qlen = p.query_start[s + 1] - qs;
-    const int q0 = qt * kQ;
-    if (q0 >= qlen) return;  // CTA-uniform
-    const int ctx = p.context_lens[s];
-    const int base_pos = ctx - qlen;  // logical position of query token 0
-    const int kv_len = base_pos + min(q0 + kQ, qlen);  // tokens this tile may attend to
-    const int ntiles = (kv_len + kN - 1) / kN;
-    const int kvh = h / p.G;
-    const int B = 1 << p.log2B;
-    const int32_t* btrow = p.block_tables + (int64_t)s * p.W;
-
-    if (tid == 0) {
-        for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
-        fence_mbar_init();
-    }
-    if (warp == 0) tmem_alloc(tmem_slot, 256);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t tmem_S = tmem, tmem_O = tmem + 128;  // columns [0,128) S, [128,256) O_t
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-
-    auto load_kv = [&](int j, int st) {  // thread 0 only
-        unsigned char* k0 = sK + st * 2 * kHalf;
-        unsigned char* v0 = sV + st * 2 * kHalf;
-        const int br = p.box_rows;
-        uint32_t bytes = 0;
-        for (int t = j * kN; t < min(kv_len, (j + 1) * kN); t += br) bytes += 2u * 2u * br * 128u;
-        mbar_arrive_expect_tx(&bars[1 + st], bytes);
-        for (int t = j * kN; t < min(kv_len, (j + 1) * kN); t += br) {
-            const int blk = __ldg(btrow + (t >> p.log2B));
-            const int row = (blk * p.H_kv + kvh) * B + (t & (B - 1));
-            const int r = (t - j * kN) * 128;  // byte offset of the row inside a half
-            tma_load_2d(k0 + r, &p.tmap_k, 0, row, &bars[1 + st]);
-            tma_load_2d(k0 + kHalf + r, &p.tmap_k, 64, row, &bars[1 + st]);
-            tma_load_2d(v0 + r, &p.tmap_v, 0, row, &bars[1 + st]);
-            tma_load_2d(v0 + kHalf + r, &p.tmap_v, 64, row, &bars[1 + st]);
-        }
-    };
-
-    if (tid == 0) {
-        mbar_arrive_expect_tx(&bars[0], 2u * kHalf);
-        tma_load_3d(sQ, &p.tmap_q, 0, h, qs + q0, &bars[0]);
-        tma_load_3d(sQ + kHalf, &p.tmap_q, 64, h, qs + q0, &bars[0]);
-        if (ntiles > 0) load_kv(0, 0);
-    }
-
-    // this thread's query row
-    const int r = tid;
-    const bool row_valid = q0 + r < qlen;
-    const int pos = row_valid ? base_pos + q0 + r : -1;
-    float m = -INFINITY, l = 0.f;
-    const uint32_t idesc_s = umma_idesc(kBF16, false), idesc_o = umma_idesc(kBF16, true);
-    uint32_t mma_phase = 0;
-
-    mbar_wait(&bars[0], 0);
-    for (int j = 0; j < ntiles; ++j) {
-        const int st = j & 1;
-        if (tid == 0 && j + 1 < ntiles) load_kv(j + 1, st ^ 1);
-        mbar_wait(&bars[1 + st], (j >> 1) & 1);
-        unsigned char* kst = sK + st * 2 * kHalf;
-        unsigned char* vst = sV + st * 2 * kHalf;
-        const int tile0 = j * kN;
-        if (tile0 + kN > kv_len) {  // last tile: zero V rows past the attended range
-            const int first = kv_len - tile0;
-            for (int i = tid; i < (kN - first) * 16; i += 128) {
-                const int rr = first + i / 16, ch = i % 16;
-                uint4* dst = reinterpret_cast<uint4*>(vst + (ch >> 3) * kHalf + rr * 128 + (ch & 7) * 16);
-                *dst = make_uint4(0, 0, 0, 0);
-            }
-            fence_proxy_async_smem();
-        }
-        __syncthreads();
-        // ---- S = Q K^T ------------------------------------------------------------------
-        if (tid == 0) {
-            tc_fence_after();
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint32_t half = (k >> 2) * kHalf, koff = (k & 3) * 32;
-                const uint64_t a = umma_desc_sw128(smem_u32(sQ) + half + koff, 16, 1024);
-                const uint64_t b = umma_desc_sw128(smem_u32(kst) + half + koff, 16, 1024);
-                umma_f16(tmem_S, a, b, idesc_s, k > 0);
-            }
-            umma_commit(&bars[3]);
-        }
-        mbar_wait(&bars[3], mma_phase);
-        mma_phase ^= 1u;
-        tc_fence_after();
-        // ---- softmax on this row: pass 1 row max, pass 2 exp / sum / P -------------------
-        const int lim = row_valid ? min(pos + 1, kv_len) - tile0 : 0;  // valid columns [0, lim)
-        float mt = -INFINITY;
-#pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-            float v[32];
-            tmem_ld32(tmem_S + lane_off + c0, v);
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (c0 + i < lim) mt = fmaxf(mt, v[i] * p.scale_log2);
-        }
-        const float mn = fmaxf(m, mt);
-        const float ms = (mn == -INFINITY) ? 0.f : mn;
-        const float alpha = ex2(m - ms);
-        float rs = 0.f;
-#pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-            float v[32];
-            tmem_ld32(tmem_S + lane_off + c0, v);
-            uint32_t pk[16];
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-                const float a0 = (c0 + i < lim) ? ex2(v[i] * p.scale_log2 - ms) : 0.f;
-                const float a1 = (c0 + i + 1 < lim) ? ex2(v[i + 1] * p.scale_log2 - ms) : 0.f;
-                T t0 = Elem<T>::from_f32(a0), t1 = Elem<T>::from_f32(a1);
-                rs += Elem<T>::to_f32(t0) + Elem<T>::to_f32(t1);  // l sums what P V actually uses
-                pk[i / 2] = (uint32_t)(*reinterpret_cast<uint16_t*>(&t0)) |
-                            ((uint32_t)(*reinterpret_cast<uint16_t*>(&t1)) << 16);
-            }
-            // columns c0..c0+31 of row r -> half (c0/64), chunks (c0%64)/8 .. +3, swizzled
-            unsigned char* prow = sP + (c0 >> 6) * kHalf + r * 128;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int ch = ((c0 & 63) >> 3) + q;
-                *reinterpret_cast<uint4*>(prow + ((ch ^ (r & 7)) << 4)) =
-                    make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-            }
-        }
-        l = l * alpha + rs;
-        m = mn;
-        // O (tensor memory, fp32) *= alpha before this tile's P V accumulates into it;
-        // skipped when no row of the warp changed its max
-        if (j > 0 && !__all_sync(0xffffffffu, alpha == 1.f)) {
-#pragma unroll
-            for (int c0 = 0; c0 < 128; c0 += 32) {
-                float v[32];
-                tmem_ld32(tmem_O + lane_off + c0, v);
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] *= alpha;
-                tmem_st32(tmem_O + lane_off + c0, v);
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        }
-        fence_proxy_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        // ---- O_t = P V -------------------------------------------------------------------
-        if (tid == 0) {
-            tc_fence_after();
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {  // K = tokens, 16 per step
-                const uint64_t a = umma_desc_sw128(smem_u32(sP) + (k >> 2) * kHalf + (k & 3) * 32, 16, 1024);
-                const uint64_t b = umma_desc_sw128(smem_u32(vst) + k * 2048, kHalf, 1024);
-                umma_f16(tmem_O, a, b, idesc_o, (j > 0) | (k > 0));
-            }
-            umma_commit(&bars[3]);
-        }
-        mbar_wait(&bars[3], mma_phase);
-        mma_phase ^= 1u;
-        tc_fence_after();
-    }
-
-    // ---- epilogue: out row = O / l -----------------------------------------------------
-    {
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        T* orow = static_cast<T*>(p.out) + ((int64_t)(qs + q0 + r) * p.H + h) * 128;
-#pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-            float v[32];
-            if (ntiles > 0) {
-                tmem_ld32(tmem_O + lane_off + c0, v);  // warp-collective: every lane loads
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = 0.f;
-            }
-            if (row_valid) {
-#pragma unroll
-                for (int c1 = 0; c1 < 32; c1 += 8) {
-                    alignas(16) T w[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) w[i] = Elem<T>::from_f32(v[c1 + i] * inv);
-                    *reinterpret_cast<uint4*>(orow + c0 + c1) = *reinterpret_cast<const uint4*>(w);
-                }
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        tmem_dealloc(tmem, 256);
-    }
-}
 
 // two fp32 -> packed storage pair (lo = a, hi = b), one cvt (F2FP) per pair
 template <typename T>
@@ -862,771 +637,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     }
 }
 
-// ---- v5: v2 with FOUR softmax warp groups -- (query tile, key-column half) --------------
-// The per-tile softmax -> P V -> next S chain bounds v2; here each query
-// tile's softmax is split by key columns across two warp groups (row maxima exchanged
-// through shared memory, partial row sums added in the epilogue, as v3), halving the
-// softmax on that chain while keeping v2's two query tiles per K/V tile.  Warps 0-15
-// softmax, 16 TMA producer, 17 MMA issuer.
-constexpr int kThreadsV5 = 18 * 32;
 
-
-
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kThreadsV5, 1) paged_prefill_wide_kernel(const __grid_constant__ PrefillParams p) {
-    constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    unsigned char* sQ = smem;                // [2 tiles][2 halves][128][64]
-    unsigned char* sK = smem + 4 * kHalf;    // [2 stages][2 halves][128][64]
-    unsigned char* sV = sK + 4 * kHalf;      // [2 stages][2 halves][128][64]
-    float* red = reinterpret_cast<float*>(sV + 4 * kHalf);  // [2 tiles][2 parity][2 halves][128] row maxima
-    float* lsum = red + 1024;                                 // [2 tiles][2 halves][128] row sums
-    uint64_t* bars = reinterpret_cast<uint64_t*>(lsum + 512);
-    uint64_t* q_full = bars;         // 1
-    uint64_t* q_empty = bars + 1;    // 1
-    uint64_t* k_full = bars + 2;     // 2
-    uint64_t* k_empty = bars + 4;    // 2
-    uint64_t* v_full = bars + 6;     // 2
-    uint64_t* v_empty = bars + 8;    // 2
-    uint64_t* s_full = bars + 10;    // 2 (per query tile)
-    uint64_t* p_full = bars + 12;    // 2
-    uint64_t* o_done = bars + 14;    // 2
-    uint64_t* o_free = bars + 16;    // 2
-    uint64_t* sched_full = bars + 18;   // 4: work-item ring (producer -> MMA + softmax warps)
-    uint64_t* sched_empty = bars + 22;  // 4
-    int* sched_item = reinterpret_cast<int*>(bars + 26);  // 4
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_item + 4);
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int n_items = p.X * p.H * p.S;
-    pdl_wait();
-
-    if (tid == 0) {
-        for (int i = 0; i < 4; ++i) {
-            mbar_init(&sched_full[i], 1);
-            mbar_init(&sched_empty[i], 1 + 4 * kQ);  // MMA warp (one arrive) + 512 softmax threads
-        }
-        mbar_init(q_full, 1);
-        mbar_init(q_empty, 1);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&k_full[i], 1);
-            mbar_init(&k_empty[i], 1);
-            mbar_init(&v_full[i], 1);
-            mbar_init(&v_empty[i], 1);
-            mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 2 * kQ);
-            mbar_init(&o_done[i], 1);
-            mbar_init(&o_free[i], 2 * kQ);
-        }
-        fence_mbar_init();
-    }
-    // V stages start zeroed: rows past kv_len of a last tile are never loaded and must not
-    // hold NaN bit patterns (P = 0 there, but 0 * NaN = NaN in the MMA); later they hold
-    // rows of earlier tiles (finite cache data)
-    for (int i = tid; i < 4 * kHalf / 16; i += kThreadsV5)
-        reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
-    fence_proxy_async_smem();
-    if (warp == 0) tmem_alloc(tmem_slot, 512);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const int B = 1 << p.log2B;
-
-    if (warp == 16) {
-        // ---------------- TMA producer ----------------
-        const int br = p.box_rows;
-        uint32_t g = 0;    // KV tiles loaded by this CTA (stage = g & 1)
-        uint32_t nq = 0;   // query tile pairs loaded
-        for (uint32_t k = 0;; ++k) {
-            // the producer draws the next work item and publishes it to the other warps
-            const uint32_t slot = k & 3;
-            if (k >= 4) mbar_wait(&sched_empty[slot], ((k - 4) >> 2) & 1);
-            int i = 0;
-            if (lane == 0) {
-                i = atomicAdd(p.work_counter, 1);
-                sched_item[slot] = i;
-                mbar_arrive(&sched_full[slot]);
-            }
-            i = __shfl_sync(0xffffffffu, i, 0);
-            if (i >= n_items) break;
-            PrefillItem it;
-            if (!prefill_item(p, i, it)) continue;
-            const int kvh = it.h / p.G;
-            const int32_t* btrow = p.block_tables + (int64_t)it.s * p.W;
-            // tile j = tokens [128j, min(kv_len, 128j+128)): nf boxes of br rows, then
-            // single rows (never reading past kv_len).  Box b belongs to lane b % 32: the
-            // lanes look up the block table in parallel and issue their own TMA copies.
-            auto box_token = [&](int b, int nf) { return b < nf ? b * br : nf * br + (b - nf); };
-            auto lookup = [&](int j, int (&rowv)[4]) {
-                const int t0 = j * kN, len = min(it.kv_len, t0 + kN) - t0;
-                const int nf = len / br, nb = nf + len % br;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int b = lane + 32 * u;
-                    if (b < nb) {
-                        const int t = t0 + box_token(b, nf);
-                        const int blk = __ldg(btrow + (t >> p.log2B));
-                        rowv[u] = (blk * p.H_kv + kvh) * B + (t & (B - 1));
-                    }
-                }
-            };
-            auto issue = [&](unsigned char* dst0, const CUtensorMap* map, const CUtensorMap* map1, int j,
-                             uint64_t* bar, const int (&rowv)[4]) {
-                const int t0 = j * kN, len = min(it.kv_len, t0 + kN) - t0;
-                const int nf = len / br, nb = nf + len % br;
-                if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
-                __syncwarp();
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int b = lane + 32 * u;
-                    if (b < nb) {
-                        const int off = box_token(b, nf) * 128;
-                        const CUtensorMap* m = b < nf ? map : map1;
-                        tma_load_2d(dst0 + off, m, 0, rowv[u], bar);
-                        tma_load_2d(dst0 + kHalf + off, m, 64, rowv[u], bar);
-                    }
-                }
-                __syncwarp();
-            };
-            int rowv[4] = {0, 0, 0, 0};
-            if (it.n > 0) lookup(0, rowv);
-            if (nq > 0) mbar_wait(q_empty, (nq - 1) & 1);  // last S of the previous pair done
-            if (lane == 0) {
-                mbar_arrive_expect_tx(q_full, 4u * kHalf);
-                tma_load_3d(sQ, &p.tmap_q, 0, it.h, it.qs + it.q0, q_full);
-                tma_load_3d(sQ + kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0, q_full);
-                tma_load_3d(sQ + 2 * kHalf, &p.tmap_q, 0, it.h, it.qs + it.q0 + kQ, q_full);
-                tma_load_3d(sQ + 3 * kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0 + kQ, q_full);
-            }
-            __syncwarp();
-            ++nq;
-            for (int j = 0; j < it.n; ++j, ++g) {
-                const int st = g & 1;
-                if (g >= 2) mbar_wait(&k_empty[st], ((g - 2) >> 1) & 1);
-                issue(sK + st * 2 * kHalf, &p.tmap_k, &p.tmap_k1, j, &k_full[st], rowv);
-                if (g >= 2) mbar_wait(&v_empty[st], ((g - 2) >> 1) & 1);
-                issue(sV + st * 2 * kHalf, &p.tmap_v, &p.tmap_v1, j, &v_full[st], rowv);
-                if (j + 1 < it.n) lookup(j + 1, rowv);  // in flight while the next empty-wait spins
-            }
-        }
-    } else if (warp == 17) {
-        // ---------------- MMA issuer ----------------
-        const uint32_t idesc_s = umma_idesc(kBF16, false), idesc_o = umma_idesc(kBF16, true);
-        uint32_t g = 0, nq = 0;
-        uint32_t np[2] = {0, 0};  // P tiles consumed per query tile (p_full phases)
-        uint32_t nf[2] = {0, 0};  // pairs with tiles per query tile (o_free phases)
-        auto issue_S = [&](int t, uint32_t gs) {  // S_t = Q_t K^T, K in stage gs & 1
-            if (lane == 0) {
-                const uint32_t q = smem_u32(sQ) + t * 2 * kHalf, k = smem_u32(sK) + (gs & 1) * 2 * kHalf;
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-                    umma_f16(tmem + t * 128, umma_desc_sw128(q + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024),
-                             idesc_s, kk > 0);
-                }
-                umma_commit(&s_full[t]);
-            }
-            __syncwarp();
-        };
-        auto issue_PV = [&](int t, uint32_t gs, bool first) {  // O_t (+)= P_t V, P_t in tensor memory
-            if (lane == 0) {
-                const uint32_t v = smem_u32(sV) + (gs & 1) * 2 * kHalf;
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
-                                umma_desc_sw128(v + kk * 2048, kHalf, 1024), idesc_o, (!first) | (kk > 0));
-                umma_commit(&o_done[t]);
-            }
-            __syncwarp();
-        };
-        for (uint32_t k = 0;; ++k) {
-            const uint32_t slot = k & 3;
-            mbar_wait(&sched_full[slot], (k >> 2) & 1);
-            const int i = *reinterpret_cast<volatile int*>(&sched_item[slot]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sched_empty[slot]);
-            if (i >= n_items) break;
-            PrefillItem it;
-            if (!prefill_item(p, i, it)) continue;
-            mbar_wait(q_full, nq & 1);
-            if (it.n > 0) {
-                mbar_wait(&k_full[g & 1], (g >> 1) & 1);
-                tc_fence_after();
-                if (it.n0 > 0) issue_S(0, g);
-                if (it.n1 > 0) issue_S(1, g);
-                if (lane == 0) umma_commit(&k_empty[g & 1]);
-                if (it.n == 1 && lane == 0) umma_commit(q_empty);
-            } else if (lane == 0) {
-                umma_commit(q_empty);
-            }
-            // O_t is overwritten by this pair's first P V: the softmax warp group must have
-            // read O_t of its previous pair with tiles (o_free; a group with no tiles in a
-            // pair neither arrives nor is waited for, so it can never run two phases ahead)
-            if (it.n0 > 0 && nf[0]++ > 0) mbar_wait(&o_free[0], (nf[0] - 2) & 1);
-            if (it.n1 > 0 && nf[1]++ > 0) mbar_wait(&o_free[1], (nf[1] - 2) & 1);
-            ++nq;
-            for (int j = 0; j < it.n; ++j, ++g) {
-                const int st = g & 1;
-                mbar_wait(&v_full[st], (g >> 1) & 1);
-                if (j < it.n0) {
-                    mbar_wait(&p_full[0], np[0]++ & 1);
-                    tc_fence_after();
-                    issue_PV(0, g, j == 0);
-                }
-                const bool more = j + 1 < it.n;
-                if (more) {
-                    mbar_wait(&k_full[st ^ 1], ((g + 1) >> 1) & 1);
-                    tc_fence_after();
-                    if (j + 1 < it.n0) issue_S(0, g + 1);
-                }
-                if (j < it.n1) {
-                    mbar_wait(&p_full[1], np[1]++ & 1);
-                    tc_fence_after();
-                    issue_PV(1, g, j == 0);
-                }
-                if (lane == 0) umma_commit(&v_empty[st]);
-                if (more) {
-                    if (j + 1 < it.n1) issue_S(1, g + 1);
-                    if (lane == 0) {
-                        umma_commit(&k_empty[st ^ 1]);
-                        if (j + 2 == it.n) umma_commit(q_empty);  // every S of this pair issued
-                    }
-                }
-                __syncwarp();
-            }
-        }
-    } else {
-        // ---------------- softmax warp groups: (query tile t, key-column half hf) ----------------
-        const int t = warp >> 3, hf = (warp >> 2) & 1;
-        const int r = tid & (kQ - 1);
-        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-        const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + 256 + t * 128 + hf * 64 + lane_off;
-        const int bar_id = 1 + t;  // named barrier of the 256 threads of query tile t
-        uint32_t ns = 0;
-        for (uint32_t k = 0;; ++k) {
-            const uint32_t slot = k & 3;
-            mbar_wait(&sched_full[slot], (k >> 2) & 1);
-            const int i = *reinterpret_cast<volatile int*>(&sched_item[slot]);
-            mbar_arrive(&sched_empty[slot]);
-            if (i >= n_items) break;
-            PrefillItem it;
-            if (!prefill_item(p, i, it)) continue;
-            const int nt = t == 0 ? it.n0 : it.n1;
-            const int kvt = t == 0 ? it.kv0 : it.kv1;
-            const int row = it.q0 + t * kQ + r;
-            const bool row_valid = row < it.qlen;
-            const int pos = row_valid ? it.base_pos + row : -1;
-            float m = -INFINITY, l = 0.f;
-            for (int j = 0; j < nt; ++j, ++ns) {
-                mbar_wait(&s_full[t], ns & 1);
-                if (tid == 0 && k == 0 && j < 64) PF_T(2 * j);
-                if (tid == 256 && k == 0 && j < 64) PF_T(129 + 2 * j);
-                tc_fence_after();
-                float sa[32], sb[32];
-                tmem_ld32_nw(tS + hf * 64, sa);
-                tmem_ld32_nw(tS + hf * 64 + 32, sb);
-                tmem_ld_wait();
-                if (tid == 0 && k == 0 && j == 3) PF_T(200);
-                const int lim = row_valid ? min(pos + 1, kvt) - j * kN - hf * 64 : 0;
-                const bool full = __all_sync(0xffffffffu, lim >= 64);
-                float mo = -INFINITY;
-                if (full) {
-#pragma unroll
-                    for (int u = 0; u < 32; u += 2)
-                        mo = fmaxf(fmaxf(mo, fmaxf(sa[u], sa[u + 1])), fmaxf(sb[u], sb[u + 1]));
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) {
-                        if (u < lim) mo = fmaxf(mo, sa[u]);
-                        if (u + 32 < lim) mo = fmaxf(mo, sb[u]);
-                    }
-                }
-                // row maximum over both halves; after this barrier both halves have read
-                // their S columns, so P may overwrite them
-                float* rd = red + (t * 2 + (ns & 1)) * 256;
-                rd[hf * 128 + r] = mo;
-                named_bar_sync(bar_id, 2 * kQ);
-                const float mt = fmaxf(mo, rd[(hf ^ 1) * 128 + r]) * p.scale_log2;
-                if (tid == 0 && k == 0 && j == 3) PF_T(201);
-                const bool bump = __any_sync(0xffffffffu, mt > m + kLazy);  // same decision in both halves
-                const float mn = bump ? fmaxf(m, mt) : m;
-                const float ms = (mn == -INFINITY) ? 0.f : mn;
-                const float alpha = bump ? ex2(m - ms) : 1.f;
-                float2 rs2 = make_float2(0.f, 0.f);
-                const float2 c2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-ms, -ms);
-                auto emit = [&](const float (&x)[32], int c0) {
-                    uint32_t pk[16];
-                    if (full) {
-#pragma unroll
-                        for (int u = 0; u < 32; u += 2) {
-                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
-                            const float2 a = make_float2(ex2(e.x), ex2(e.y));
-                            rs2 = __fadd2_rn(rs2, a);
-                            pk[u / 2] = pack2<T>(a.x, a.y);
-                        }
-                    } else {
-#pragma unroll
-                        for (int u = 0; u < 32; u += 2) {
-                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
-                            float2 a = make_float2(ex2(e.x), ex2(e.y));
-                            a.x = (c0 + u < lim) ? a.x : 0.f;
-                            a.y = (c0 + u + 1 < lim) ? a.y : 0.f;
-                            rs2 = __fadd2_rn(rs2, a);
-                            pk[u / 2] = pack2<T>(a.x, a.y);
-                        }
-                    }
-                    tmem_st16(tS + hf * 32 + c0 / 2, pk);  // P columns of this half
-                };
-                emit(sa, 0);
-                emit(sb, 32);
-                if (tid == 0 && k == 0 && j == 3) PF_T(202);
-                if (j > 0) {  // P V of the previous tile complete (returns at once; never skipped)
-                    mbar_wait(&o_done[t], (ns - 1) & 1);
-                    tc_fence_after();
-                }
-                if (j > 0 && bump) {  // this half's 64 O columns *= alpha
-#pragma unroll
-                    for (int c0 = 0; c0 < 64; c0 += 32) {
-                        float v[32];
-                        tmem_ld32_nw(tO + c0, v);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int u = 0; u < 32; ++u) v[u] *= alpha;
-                        tmem_st32(tO + c0, v);
-                    }
-                }
-                if (tid == 0 && k == 0 && j == 3) PF_T(203);
-                l = l * alpha + (rs2.x + rs2.y);
-                m = mn;
-                tmem_st_wait();
-                tc_fence_before();
-                if (tid == 0 && k == 0 && j < 64) PF_T(2 * j + 1);
-                if (tid == 256 && k == 0 && j < 64) PF_T(128 + 2 * j);
-                mbar_arrive(&p_full[t]);
-            }
-            // epilogue: total row sum of both halves, then this half's 64 output columns
-            float* ls = lsum + t * 256;
-            ls[hf * 128 + r] = l;
-            named_bar_sync(bar_id, 2 * kQ);
-            const float lt = l + ls[(hf ^ 1) * 128 + r];
-            named_bar_sync(bar_id, 2 * kQ);  // ls may be rewritten by the next item
-            const float inv = lt > 0.f ? 1.f / lt : 0.f;
-            T* orow = static_cast<T*>(p.out) + ((int64_t)(it.qs + row) * p.H + it.h) * 128 + hf * 64;
-            if (nt > 0) {
-                mbar_wait(&o_done[t], (ns - 1) & 1);
-                tc_fence_after();
-            }
-#pragma unroll
-            for (int c0 = 0; c0 < 64; c0 += 32) {
-                float v[32];
-                if (nt > 0) {
-                    tmem_ld32_nw(tO + c0, v);
-                    tmem_ld_wait();
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) v[u] = 0.f;
-                }
-                if (row_valid) {
-#pragma unroll
-                    for (int c1 = 0; c1 < 32; c1 += 8) {
-                        alignas(16) T w[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) w[u] = Elem<T>::from_f32(v[c1 + u] * inv);
-                        *reinterpret_cast<uint4*>(orow + c0 + c1) = *reinterpret_cast<const uint4*>(w);
-                    }
-                }
-            }
-            if (nt > 0) {
-                tc_fence_before();
-                mbar_arrive(&o_free[t]);
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        tmem_dealloc(tmem, 512);
-    }
-}
-
-size_t prefill_wide_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 1536 * 4 + 26 * 8 + 4 * 4 + 16; }
-
-// ---- v4: as v2 with 64-token K/V tiles and two S buffers per query tile ------------------
-// Tensor memory: S_t[b] (64 columns each, t = query tile, b = tile parity) in columns
-// [0,256), O_0 / O_1 in [256,512).  P_t(j) aliases S_t[j&1], so S_t(j+1) goes to the other
-// buffer and is computed while the softmax of tile j runs: the tensor-core work of a tile
-// no longer sits between one softmax and the next (v2's critical chain).  MMA order per
-// tile j: PV_0(j), PV_1(j), then S_0(j+2), S_1(j+2).  K and V in four 16 KB stages each.
-constexpr int kN4 = 64;                 // K/V tokens per tile
-constexpr int kHalf4 = kN4 * 128;       // bytes of one [64 rows][64 elements] swizzled half
-constexpr int kStages4 = 4;
-
-__device__ __forceinline__ bool prefill_item4(const PrefillParams& p, int i, PrefillItem& it) {
-    const int g = i / p.X;
-    const int qp = p.X - 1 - i % p.X;
-    it.h = g % p.H;
-    it.s = g / p.H;
-    it.qs = __ldg(p.query_start + it.s);
-    it.qlen = __ldg(p.query_start + it.s + 1) - it.qs;
-    it.q0 = qp * 2 * kQ;
-    if (it.q0 >= it.qlen) return false;
-    it.base_pos = __ldg(p.context_lens + it.s) - it.qlen;
-    it.kv0 = it.base_pos + min(it.q0 + kQ, it.qlen);
-    it.kv1 = it.q0 + kQ < it.qlen ? it.base_pos + min(it.q0 + 2 * kQ, it.qlen) : 0;
-    it.n0 = it.kv0 > 0 ? (it.kv0 + kN4 - 1) / kN4 : 0;
-    it.n1 = it.kv1 > 0 ? (it.kv1 + kN4 - 1) / kN4 : 0;
-    it.kv_len = max(it.kv0, it.kv1);
-    it.n = max(it.n0, it.n1);
-    return true;
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_db_kernel(const __grid_constant__ PrefillParams p) {
-    constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    unsigned char* sQ = smem;                                 // [2 tiles][2 halves][128][64]
-    unsigned char* sK = smem + 4 * kHalf;                     // [4 stages][2 halves][64][64]
-    unsigned char* sV = sK + kStages4 * 2 * kHalf4;           // [4 stages][2 halves][64][64]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kStages4 * 2 * kHalf4);
-    uint64_t* q_full = bars;                     // 1
-    uint64_t* q_empty = bars + 1;                // 1
-    uint64_t* k_full = bars + 2;                 // 4
-    uint64_t* k_empty = bars + 6;                // 4
-    uint64_t* v_full = bars + 10;                // 4
-    uint64_t* v_empty = bars + 14;               // 4
-    uint64_t* s_full = bars + 18;                // [2 tiles][2 buffers]
-    uint64_t* p_full = bars + 22;                // 2
-    uint64_t* o_done = bars + 24;                // 2
-    uint64_t* o_free = bars + 26;                // 2
-    uint64_t* sched_full = bars + 28;            // 4
-    uint64_t* sched_empty = bars + 32;           // 4
-    int* sched_item = reinterpret_cast<int*>(bars + 36);  // 4
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_item + 4);
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int n_items = p.X * p.H * p.S;
-    pdl_wait();
-
-    if (tid == 0) {
-        for (int i = 0; i < 4; ++i) {
-            mbar_init(&sched_full[i], 1);
-            mbar_init(&sched_empty[i], 1 + 2 * kQ);
-            mbar_init(&k_full[i], 1);
-            mbar_init(&k_empty[i], 1);
-            mbar_init(&v_full[i], 1);
-            mbar_init(&v_empty[i], 1);
-            mbar_init(&s_full[i], 1);
-        }
-        mbar_init(q_full, 1);
-        mbar_init(q_empty, 1);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&p_full[i], kQ);
-            mbar_init(&o_done[i], 1);
-            mbar_init(&o_free[i], kQ);
-        }
-        fence_mbar_init();
-    }
-    for (int i = tid; i < kStages4 * 2 * kHalf4 / 16; i += kThreadsV2)
-        reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);  // see v2
-    fence_proxy_async_smem();
-    if (warp == 0) tmem_alloc(tmem_slot, 512);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const int B = 1 << p.log2B;
-
-    if (warp == 8) {
-        // ---------------- TMA producer ----------------
-        const int br = p.box_rows;  // <= 64
-        uint32_t g = 0, nq = 0;
-        for (uint32_t k = 0;; ++k) {
-            const uint32_t slot = k & 3;
-            if (k >= 4) mbar_wait(&sched_empty[slot], ((k - 4) >> 2) & 1);
-            int i = 0;
-            if (lane == 0) {
-                i = atomicAdd(p.work_counter, 1);
-                sched_item[slot] = i;
-                mbar_arrive(&sched_full[slot]);
-            }
-            i = __shfl_sync(0xffffffffu, i, 0);
-            if (i >= n_items) break;
-            PrefillItem it;
-            if (!prefill_item4(p, i, it)) continue;
-            const int kvh = it.h / p.G;
-            const int32_t* btrow = p.block_tables + (int64_t)it.s * p.W;
-            auto box_token = [&](int b, int nf) { return b < nf ? b * br : nf * br + (b - nf); };
-            auto lookup = [&](int j, int (&rowv)[2]) {
-                const int t0 = j * kN4, len = min(it.kv_len, t0 + kN4) - t0;
-                const int nf = len / br, nb = nf + len % br;
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int b = lane + 32 * u;
-                    if (b < nb) {
-                        const int t = t0 + box_token(b, nf);
-                        const int blk = __ldg(btrow + (t >> p.log2B));
-                        rowv[u] = (blk * p.H_kv + kvh) * B + (t & (B - 1));
-                    }
-                }
-            };
-            auto issue = [&](unsigned char* dst0, const CUtensorMap* map, const CUtensorMap* map1, int j,
-                             uint64_t* bar, const int (&rowv)[2]) {
-                const int t0 = j * kN4, len = min(it.kv_len, t0 + kN4) - t0;
-                const int nf = len / br, nb = nf + len % br;
-                if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
-                __syncwarp();
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int b = lane + 32 * u;
-                    if (b < nb) {
-                        const int off = box_token(b, nf) * 128;
-                        const CUtensorMap* m = b < nf ? map : map1;
-                        tma_load_2d(dst0 + off, m, 0, rowv[u], bar);
-                        tma_load_2d(dst0 + kHalf4 + off, m, 64, rowv[u], bar);
-                    }
-                }
-                __syncwarp();
-            };
-            int rowv[2] = {0, 0};
-            if (it.n > 0) lookup(0, rowv);
-            if (nq > 0) mbar_wait(q_empty, (nq - 1) & 1);
-            if (lane == 0) {
-                mbar_arrive_expect_tx(q_full, 4u * kHalf);
-                tma_load_3d(sQ, &p.tmap_q, 0, it.h, it.qs + it.q0, q_full);
-                tma_load_3d(sQ + kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0, q_full);
-                tma_load_3d(sQ + 2 * kHalf, &p.tmap_q, 0, it.h, it.qs + it.q0 + kQ, q_full);
-                tma_load_3d(sQ + 3 * kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0 + kQ, q_full);
-            }
-            __syncwarp();
-            ++nq;
-            for (int j = 0; j < it.n; ++j, ++g) {
-                const uint32_t st = g % kStages4, ph = (g / kStages4 - 1) & 1;
-                if (g >= kStages4) mbar_wait(&k_empty[st], ph);
-                issue(sK + st * 2 * kHalf4, &p.tmap_k, &p.tmap_k1, j, &k_full[st], rowv);
-                if (g >= kStages4) mbar_wait(&v_empty[st], ph);
-                issue(sV + st * 2 * kHalf4, &p.tmap_v, &p.tmap_v1, j, &v_full[st], rowv);
-                if (j + 1 < it.n) lookup(j + 1, rowv);
-            }
-        }
-    } else if (warp == 9) {
-        // ---------------- MMA issuer ----------------
-        const uint32_t idesc_s = umma_idesc(kBF16, false, kN4), idesc_o = umma_idesc(kBF16, true, 128);
-        uint32_t gs = 0, gv = 0, nq = 0;       // K/V tiles (stage counters)
-        uint32_t np[2] = {0, 0}, nf[2] = {0, 0};
-        uint32_t ms[2] = {0, 0}, mp[2] = {0, 0};  // S_t / P_t V tiles issued per query tile (buffer = count & 1)
-        // S_t = Q_t K(gs)^T into S_t[ms[t] & 1]
-        auto issue_S = [&](int t) {
-            const uint32_t b = ms[t]++ & 1;
-            if (lane == 0) {
-                const uint32_t q = smem_u32(sQ) + t * 2 * kHalf, k = smem_u32(sK) + (gs % kStages4) * 2 * kHalf4;
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t qo = (kk >> 2) * kHalf + (kk & 3) * 32, ko = (kk >> 2) * kHalf4 + (kk & 3) * 32;
-                    umma_f16(tmem + (2 * t + b) * kN4, umma_desc_sw128(q + qo, 16, 1024),
-                             umma_desc_sw128(k + ko, 16, 1024), idesc_s, kk > 0);
-                }
-                umma_commit(&s_full[2 * t + b]);
-            }
-            __syncwarp();
-        };
-        // S for the next tile of the item (both query tiles), then release its K stage
-        auto next_S = [&](const PrefillItem& it, int jn, bool last_s) {
-            mbar_wait(&k_full[gs % kStages4], (gs / kStages4) & 1);
-            tc_fence_after();
-            if (jn < it.n0) issue_S(0);
-            if (jn < it.n1) issue_S(1);
-            if (lane == 0) {
-                umma_commit(&k_empty[gs % kStages4]);
-                if (last_s) umma_commit(q_empty);  // every S of this pair issued
-            }
-            __syncwarp();
-            ++gs;
-        };
-        for (uint32_t k = 0;; ++k) {
-            const uint32_t slot = k & 3;
-            mbar_wait(&sched_full[slot], (k >> 2) & 1);
-            const int i = *reinterpret_cast<volatile int*>(&sched_item[slot]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sched_empty[slot]);
-            if (i >= n_items) break;
-            PrefillItem it;
-            if (!prefill_item4(p, i, it)) continue;
-            mbar_wait(q_full, nq & 1);
-            ++nq;
-            if (it.n == 0 && lane == 0) umma_commit(q_empty);
-            for (int jn = 0; jn < min(it.n, 2); ++jn) next_S(it, jn, jn + 1 == it.n);
-            if (it.n0 > 0 && nf[0]++ > 0) mbar_wait(&o_free[0], (nf[0] - 2) & 1);
-            if (it.n1 > 0 && nf[1]++ > 0) mbar_wait(&o_free[1], (nf[1] - 2) & 1);
-            for (int j = 0; j < it.n; ++j) {
-                const uint32_t st = gv % kStages4;
-                mbar_wait(&v_full[st], (gv / kStages4) & 1);
-                for (int t = 0; t < 2; ++t) {
-                    if (j >= (t == 0 ? it.n0 : it.n1)) continue;
-                    mbar_wait(&p_full[t], np[t]++ & 1);
-                    tc_fence_after();
-                    const uint32_t b = mp[t]++ & 1;  // P_t of this tile sits in S_t[b]
-                    if (lane == 0) {
-                        const uint32_t v = smem_u32(sV) + st * 2 * kHalf4;
-#pragma unroll
-                        for (int kk = 0; kk < kN4 / 16; ++kk)
-                            umma_f16_ts(tmem + 256 + t * 128, tmem + (2 * t + b) * kN4 + kk * 8,
-                                        umma_desc_sw128(v + kk * 2048, kHalf4, 1024), idesc_o, (j > 0) | (kk > 0));
-                        umma_commit(&o_done[t]);
-                    }
-                    __syncwarp();
-                }
-                if (lane == 0) umma_commit(&v_empty[st]);
-                __syncwarp();
-                ++gv;
-                if (j + 2 < it.n) next_S(it, j + 2, j + 3 == it.n);  // into the buffer P(j) just left
-            }
-        }
-    } else {
-        // ---------------- softmax warp groups ----------------
-        const int t = warp >> 2;
-        const int r = tid & (kQ - 1);
-        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-        const uint32_t tO = tmem + 256 + t * 128 + lane_off;
-        uint32_t ns = 0;
-        for (uint32_t k = 0;; ++k) {
-            const uint32_t slot = k & 3;
-            mbar_wait(&sched_full[slot], (k >> 2) & 1);
-            const int i = *reinterpret_cast<volatile int*>(&sched_item[slot]);
-            mbar_arrive(&sched_empty[slot]);
-            if (i >= n_items) break;
-            PrefillItem it;
-            if (!prefill_item4(p, i, it)) continue;
-            const int nt = t == 0 ? it.n0 : it.n1;
-            const int kvt = t == 0 ? it.kv0 : it.kv1;
-            const int row = it.q0 + t * kQ + r;
-            const bool row_valid = row < it.qlen;
-            const int pos = row_valid ? it.base_pos + row : -1;
-            float m = -INFINITY, l = 0.f;
-            for (int j = 0; j < nt; ++j, ++ns) {
-                const uint32_t b = ns & 1;
-                const uint32_t tS = tmem + (2 * t + b) * kN4 + lane_off;
-                mbar_wait(&s_full[2 * t + b], (ns >> 1) & 1);
-                tc_fence_after();
-                float sa[32], sb[32];
-                tmem_ld32_nw(tS + 0, sa);
-                tmem_ld32_nw(tS + 32, sb);
-                tmem_ld_wait();
-                const int lim = row_valid ? min(pos + 1, kvt) - j * kN4 : 0;
-                const bool full = __all_sync(0xffffffffu, lim >= kN4);
-                float mt = -INFINITY;
-                if (full) {
-#pragma unroll
-                    for (int u = 0; u < 32; u += 2)
-                        mt = fmaxf(fmaxf(mt, fmaxf(sa[u], sa[u + 1])), fmaxf(sb[u], sb[u + 1]));
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) {
-                        if (u < lim) mt = fmaxf(mt, sa[u]);
-                        if (u + 32 < lim) mt = fmaxf(mt, sb[u]);
-                    }
-                }
-                mt *= p.scale_log2;
-                const bool bump = __any_sync(0xffffffffu, mt > m + kLazy);
-                const float mn = bump ? fmaxf(m, mt) : m;
-                const float ms = (mn == -INFINITY) ? 0.f : mn;
-                const float alpha = bump ? ex2(m - ms) : 1.f;
-                float2 rs2 = make_float2(0.f, 0.f);
-                const float2 c2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-ms, -ms);
-                auto emit = [&](const float (&x)[32], int c0) {
-                    uint32_t pk[16];
-                    if (full) {
-#pragma unroll
-                        for (int u = 0; u < 32; u += 2) {
-                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
-                            const float2 a = make_float2(ex2(e.x), ex2(e.y));
-                            rs2 = __fadd2_rn(rs2, a);
-                            pk[u / 2] = pack2<T>(a.x, a.y);
-                        }
-                    } else {
-#pragma unroll
-                        for (int u = 0; u < 32; u += 2) {
-                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
-                            float2 a = make_float2(ex2(e.x), ex2(e.y));
-                            a.x = (c0 + u < lim) ? a.x : 0.f;
-                            a.y = (c0 + u + 1 < lim) ? a.y : 0.f;
-                            rs2 = __fadd2_rn(rs2, a);
-                            pk[u / 2] = pack2<T>(a.x, a.y);
-                        }
-                    }
-                    tmem_st16(tS + c0 / 2, pk);
-                };
-                emit(sa, 0);
-                emit(sb, 32);
-                if (j > 0) {  // P V of the previous tile complete (every o_done phase waited)
-                    mbar_wait(&o_done[t], (ns - 1) & 1);
-                    tc_fence_after();
-                }
-                if (j > 0 && bump) {
-#pragma unroll
-                    for (int c0 = 0; c0 < 128; c0 += 32) {
-                        float v[32];
-                        tmem_ld32_nw(tO + c0, v);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int u = 0; u < 32; ++u) v[u] *= alpha;
-                        tmem_st32(tO + c0, v);
-                    }
-                }
-                l = l * alpha + (rs2.x + rs2.y);
-                m = mn;
-                tmem_st_wait();
-                tc_fence_before();
-                mbar_arrive(&p_full[t]);
-            }
-            const float inv = l > 0.f ? 1.f / l : 0.f;
-            T* orow = static_cast<T*>(p.out) + ((int64_t)(it.qs + row) * p.H + it.h) * 128;
-            if (nt > 0) {
-                mbar_wait(&o_done[t], (ns - 1) & 1);
-                tc_fence_after();
-            }
-#pragma unroll
-            for (int c0 = 0; c0 < 128; c0 += 32) {
-                float v[32];
-                if (nt > 0) {
-                    tmem_ld32_nw(tO + c0, v);
-                    tmem_ld_wait();
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) v[u] = 0.f;
-                }
-                if (row_valid) {
-#pragma unroll
-                    for (int c1 = 0; c1 < 32; c1 += 8) {
-                        alignas(16) T w[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) w[u] = Elem<T>::from_f32(v[c1 + u] * inv);
-                        *reinterpret_cast<uint4*>(orow + c0 + c1) = *reinterpret_cast<const uint4*>(w);
-                    }
-                }
-            }
-            if (nt > 0) {
-                tc_fence_before();
-                mbar_arrive(&o_free[t]);
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        tmem_dealloc(tmem, 512);
-    }
-}
-
-size_t prefill_db_smem_bytes() { return 1024 + 4 * (size_t)kHalf + 2 * kStages4 * 2 * (size_t)kHalf4 + 36 * 8 + 32; }
 
 // ---- v3 (default): persistent, one query tile per item, softmax split by columns ----------
 // The two softmax warp groups share the 128 rows of ONE query tile: group 0 takes key
@@ -1976,42 +987,20 @@ size_t prefill_split_smem_bytes() {
     return 1024 + (4 + 2 * kKStages + 2 * kVStages) * (size_t)kHalf + (512 + 256) * 4 + 20 * 8;
 }
 
-size_t prefill_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 64; }
 size_t prefill_ws_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 26 * 8 + 4 * 4 + 16; }
 
-namespace {
-template <typename Kern>
-cudaError_t set_smem(Kern k, size_t smem) {
-    return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
-// PA_PREFILL=1/2/3 forces a kernel (ablations).  Default: v3 when no query needs more than
-// 1.5 tiles of 128 rows (v2's pairs would mostly leave the second softmax group idle),
-// else v2, whose two query tiles share each K/V tile (measured).
-int prefill_variant(int max_query_len) {
-    const char* e = getenv("PA_PREFILL");
-    if (e && e[0] >= '1' && e[0] <= '5') return e[0] - '0';
-    return max_query_len <= kQ + kQ / 2 ? 3 : 2;
-}
-}  // namespace
-
-cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, cudaStream_t stream) {
-    const int variant = prefill_variant(max_query_len);
-    if (variant == 1) {
-        const size_t smem = prefill_smem_bytes();
-        const dim3 grid((max_query_len + kQ - 1) / kQ, p.H, num_seqs);
-        cudaError_t e = dtype == 1 ? set_smem(paged_prefill_kernel<__half>, smem)
-                                   : set_smem(paged_prefill_kernel<__nv_bfloat16>, smem);
-        if (e != cudaSuccess) return e;
-        return dtype == 1 ? launch_k(paged_prefill_kernel<__half>, grid, dim3(128), smem, stream, p)
-                          : launch_k(paged_prefill_kernel<__nv_bfloat16>, grid, dim3(128), smem, stream, p);
-    }
-    static int num_sms = 0;
-    if (num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (num_sms <= 0) num_sms = 148;
-    }
+// variant: 2 / 3 forces a kernel (PA_PREFILL, read once by pa_api.cpp); 0 = default: v3 when
+// no query needs more than 1.5 tiles of 128 rows (v2's pairs would mostly leave the second
+// softmax group idle), else v2, whose two query tiles share each K/V tile (measured,
+// DESIGN.md §8c).  (v1: one tile per CTA, v4: 64-token K/V tiles, v5: four softmax warp
+// groups -- measured slower and removed; their numbers stay in DESIGN §8c.)
+cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, int variant,
+                           cudaStream_t stream) {
+    if (variant != 2 && variant != 3) variant = max_query_len <= kQ + kQ / 2 ? 3 : 2;
+    int dev = 0, num_sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (num_sms <= 0) num_sms = 148;
     PrefillParams q = p;
     q.S = num_seqs;
     if (variant == 2) {
@@ -2021,47 +1010,19 @@ cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int 
         if (me != cudaSuccess) return me;
         const long long items = (long long)q.X * q.H * q.S;
         const dim3 grid((unsigned)std::min<long long>(items, num_sms));
-        cudaError_t e = dtype == 1 ? set_smem(paged_prefill_ws_kernel<__half>, smem)
-                                   : set_smem(paged_prefill_ws_kernel<__nv_bfloat16>, smem);
+        auto kern = dtype == 1 ? paged_prefill_ws_kernel<__half> : paged_prefill_ws_kernel<__nv_bfloat16>;
+        cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
         if (e != cudaSuccess) return e;
-        return dtype == 1 ? launch_k(paged_prefill_ws_kernel<__half>, grid, dim3(kThreadsV2), smem, stream, q)
-                          : launch_k(paged_prefill_ws_kernel<__nv_bfloat16>, grid, dim3(kThreadsV2), smem, stream, q);
-    }
-    if (variant == 5) {
-        const size_t smem = prefill_wide_smem_bytes();
-        q.X = (max_query_len + 2 * kQ - 1) / (2 * kQ);
-        cudaError_t me = cudaMemsetAsync(q.work_counter, 0, sizeof(int), stream);
-        if (me != cudaSuccess) return me;
-        const long long items = (long long)q.X * q.H * q.S;
-        const dim3 grid((unsigned)std::min<long long>(items, num_sms));
-        cudaError_t e = dtype == 1 ? set_smem(paged_prefill_wide_kernel<__half>, smem)
-                                   : set_smem(paged_prefill_wide_kernel<__nv_bfloat16>, smem);
-        if (e != cudaSuccess) return e;
-        return dtype == 1 ? launch_k(paged_prefill_wide_kernel<__half>, grid, dim3(kThreadsV5), smem, stream, q)
-                          : launch_k(paged_prefill_wide_kernel<__nv_bfloat16>, grid, dim3(kThreadsV5), smem, stream, q);
-    }
-    if (variant == 4) {
-        const size_t smem = prefill_db_smem_bytes();
-        q.X = (max_query_len + 2 * kQ - 1) / (2 * kQ);
-        cudaError_t me = cudaMemsetAsync(q.work_counter, 0, sizeof(int), stream);
-        if (me != cudaSuccess) return me;
-        const long long items = (long long)q.X * q.H * q.S;
-        const dim3 grid((unsigned)std::min<long long>(items, num_sms));
-        cudaError_t e = dtype == 1 ? set_smem(paged_prefill_db_kernel<__half>, smem)
-                                   : set_smem(paged_prefill_db_kernel<__nv_bfloat16>, smem);
-        if (e != cudaSuccess) return e;
-        return dtype == 1 ? launch_k(paged_prefill_db_kernel<__half>, grid, dim3(kThreadsV2), smem, stream, q)
-                          : launch_k(paged_prefill_db_kernel<__nv_bfloat16>, grid, dim3(kThreadsV2), smem, stream, q);
+        return launch_k(kern, grid, dim3(kThreadsV2), smem, stream, q);
     }
     const size_t smem = prefill_split_smem_bytes();
     q.X = (max_query_len + kQ - 1) / kQ;
     const long long items = (long long)q.X * q.H * q.S;
     const dim3 grid((unsigned)std::min<long long>(items, num_sms));
-    cudaError_t e = dtype == 1 ? set_smem(paged_prefill_split_kernel<__half>, smem)
-                               : set_smem(paged_prefill_split_kernel<__nv_bfloat16>, smem);
+    auto kern = dtype == 1 ? paged_prefill_split_kernel<__half> : paged_prefill_split_kernel<__nv_bfloat16>;
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
-    return dtype == 1 ? launch_k(paged_prefill_split_kernel<__half>, grid, dim3(kThreadsV2), smem, stream, q)
-                      : launch_k(paged_prefill_split_kernel<__nv_bfloat16>, grid, dim3(kThreadsV2), smem, stream, q);
+    return launch_k(kern, grid, dim3(kThreadsV2), smem, stream, q);
 }
 
 }  // namespace pa

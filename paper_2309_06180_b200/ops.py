@@ -31,6 +31,29 @@ def _dev(t: torch.Tensor, name: str) -> int:
     return t.data_ptr()
 
 
+def _check(dtype=None, idx32=(), idx64=(), **tensors):
+    """Host-side type checks the C ABI cannot make (it sees raw pointers): every named
+    value tensor in `tensors` has `dtype` (the query's) and the same head_dim (last dim);
+    index tensors are int32 (block tables, context lengths) / int64 (slot and block
+    mappings).  An int32 mapping read as int64 pairs would address garbage blocks."""
+    D = None
+    for name, t in tensors.items():
+        if t is None:
+            continue
+        if dtype is not None and t.dtype != dtype:
+            raise TypeError(f"{name} is {t.dtype}, expected {dtype} (query / caches share one dtype)")
+        if D is None:
+            D = t.shape[-1]
+        elif t.shape[-1] != D:
+            raise ValueError(f"{name} has head_dim {t.shape[-1]}, expected {D}")
+    for name, t in idx32:
+        if t.dtype != torch.int32:
+            raise TypeError(f"{name} must be int32 (got {t.dtype})")
+    for name, t in idx64:
+        if t.dtype != torch.int64:
+            raise TypeError(f"{name} must be int64 (got {t.dtype})")
+
+
 def _stream(stream) -> int:
     if stream is None:
         return torch.cuda.current_stream().cuda_stream
@@ -50,6 +73,8 @@ def paged_attention(out, query, key_cache, value_cache, block_tables, context_le
     block-table-addressed cache.  out/query [S][H][D]; caches [NB][H_kv][B][D];
     block_tables int32 [S][W]; context_lens int32 [S].  `workspace` (uint8, device, any
     content; see pa.h) is allocated when omitted and the context needs splitting."""
+    _check(query.dtype, [("block_tables", block_tables), ("context_lens", context_lens)], out=out, query=query,
+           key_cache=key_cache, value_cache=value_cache)
     S, H, D = query.shape
     _, hk, B, _ = key_cache.shape
     block_size = B if block_size is None else block_size
@@ -73,6 +98,8 @@ def paged_attention_decode(out, query, key, value, key_cache, value_cache, block
                            max_context_len: int = 0, workspace: torch.Tensor | None = None, stream=None):
     """The decode step's reshape_and_cache fused into paged_attention (pa.h): token s
     (key/value [S][H_kv][D]) is written at logical position ctx[s]-1 and attended."""
+    _check(query.dtype, [("block_tables", block_tables), ("context_lens", context_lens)], out=out, query=query,
+           key=key, value=value, key_cache=key_cache, value_cache=value_cache)
     S, H, D = query.shape
     _, hk, B, _ = key_cache.shape
     W = block_tables.shape[1]
@@ -95,6 +122,8 @@ def paged_attention_decode_shared(out, query, key, value, key_cache, value_cache
                                   workspace: torch.Tensor | None = None, stream=None):
     """paged_attention_decode for sequence groups sharing blocks (parallel samples, beams):
     each distinct block of a group is read once per logical tile (pa.h)."""
+    _check(query.dtype, [("block_tables", block_tables), ("context_lens", context_lens)], out=out, query=query,
+           key=key, value=value, key_cache=key_cache, value_cache=value_cache)
     S, H, D = query.shape
     _, hk, B, _ = key_cache.shape
     W = block_tables.shape[1]
@@ -119,6 +148,8 @@ def paged_attention_decode_grouped(out, query, key, value, key_cache, value_cach
     group_size consecutive sequences; each distinct block of a group is loaded once per
     logical tile and Q K^T / P V run as MMAs over the group's rows.  f16/bf16, D = 128,
     block_size >= 16."""
+    _check(query.dtype, [("block_tables", block_tables), ("context_lens", context_lens)], out=out, query=query,
+           key=key, value=value, key_cache=key_cache, value_cache=value_cache)
     S, H, D = query.shape
     NB, hk, B, _ = key_cache.shape
     W = block_tables.shape[1]
@@ -148,6 +179,9 @@ def paged_prefill_attention(out, query, key_cache, value_cache, block_tables, co
     max_query_len sizes the grid; 0 reads it from query_start (a device->host sync).
     `workspace` (uint8 device tensor, >= 16 bytes, any content) holds the work-item
     counter; allocated per call when omitted."""
+    _check(query.dtype, [("block_tables", block_tables), ("context_lens", context_lens),
+                         ("query_start", query_start)], out=out, query=query, key_cache=key_cache,
+           value_cache=value_cache)
     T, H, D = query.shape
     NB, hk, B, _ = key_cache.shape
     S, W = block_tables.shape
@@ -166,6 +200,8 @@ def paged_prefill_attention(out, query, key_cache, value_cache, block_tables, co
 def reshape_and_cache(key, value, key_cache, value_cache, slot_mapping, stream=None):
     """Fused reshape + block write: key/value [T][H_kv][D] into the caches at
     slot_mapping (int64 [T], -1 = skip)."""
+    _check(key.dtype, idx64=[("slot_mapping", slot_mapping)], key=key, value=value, key_cache=key_cache,
+           value_cache=value_cache)
     T, hk, D = key.shape
     B = key_cache.shape[2]
     check(_lib.raw().pa_reshape_and_cache(
@@ -176,6 +212,9 @@ def reshape_and_cache(key, value, key_cache, value_cache, slot_mapping, stream=N
 def copy_blocks(key_caches, value_caches, block_mapping, stream=None):
     """Fused copy-on-write block copy over every layer in one launch.
     block_mapping: int64 [P][2] (src, dst) on the device."""
+    _check(key_caches[0].dtype, idx64=[("block_mapping", block_mapping)],
+           **{f"key_caches[{i}]": k for i, k in enumerate(key_caches)},
+           **{f"value_caches[{i}]": v for i, v in enumerate(value_caches)})
     L = len(key_caches)
     kp = (ctypes.c_void_p * L)(*[_dev(k, "key_caches[i]") for k in key_caches])
     vp = (ctypes.c_void_p * L)(*[_dev(v, "value_caches[i]") for v in value_caches])
@@ -198,6 +237,9 @@ def swap_blocks(dst_key_caches, dst_value_caches, src_key_caches, src_value_cach
     """Swap blocks between pools: dst[l][d] <- src[l][s] for every (s, d) pair in
     block_mapping (int64 [P][2], device or pinned host) and layer, one launch.  Pools may be
     device tensors or pinned host tensors (the CPU swap pool)."""
+    pools = list(dst_key_caches) + list(dst_value_caches) + list(src_key_caches) + list(src_value_caches)
+    _check(dst_key_caches[0].dtype, idx64=[("block_mapping", block_mapping)],
+           **{f"pool[{i}]": t for i, t in enumerate(pools)})
     L = len(dst_key_caches)
     arr = lambda xs, n: (ctypes.c_void_p * L)(*[_dev_or_pinned(x, n) for x in xs])  # noqa: E731
     _, hk, B, D = dst_key_caches[0].shape

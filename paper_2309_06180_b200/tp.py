@@ -144,9 +144,9 @@ class FusedTP:
         arr = lambda xs: (ctypes.c_void_p * self.world)(*xs)  # noqa: E731
         own_flags = peers[self.rank][2]
         self.status_ptr = own_flags + 4 * self.world  # int32 right after the flag array
-        self.comm = _lib.raw().pa_tp_comm_create(self.world, self.rank, H_total, arr([p[0] for p in peers]),
-                                                 arr([p[1] for p in peers]), arr([p[2] for p in peers]),
-                                                 ctypes.c_void_p(self.status_ptr))
+        self.comm = _lib.raw().pa_tp_comm_create(self.world, self.rank, H_total, self.out_bytes,
+                                                 arr([p[0] for p in peers]), arr([p[1] for p in peers]),
+                                                 arr([p[2] for p in peers]), ctypes.c_void_p(self.status_ptr))
         if not self.comm:
             raise _lib.PagedAttnError(_lib.last_error())
         self.views = [_as_tensor(peers[self.rank][i], (S, H_total, D), dtype, self.device) for i in (0, 1)]
@@ -170,9 +170,14 @@ class FusedTP:
     def decode(self, query, key, value, key_cache, value_cache, block_tables, context_lens, scale: float,
                max_context_len: int = 0, workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """The decode step (cache write fused) on this rank's heads; returns the gathered
-        [S][H_total][D] output (valid until the call after next)."""
+        [S][H_total][D] output, a view of one of the two alternating gather buffers.  It is
+        valid until this rank's NEXT decode call: read it (on the same stream) before
+        issuing that call (include/pa.h)."""
         from .ops import _code, _dev, _stream, paged_attention_workspace_size
         S, H, D = query.shape
+        if S > self.S or H * self.world != self.H or D != self.D or query.dtype != self.dtype:
+            raise ValueError(f"FusedTP built for <= {self.S} sequences x {self.H} heads ({self.H // self.world} per "
+                             f"rank) x {self.D} dims, {self.dtype}; got query {tuple(query.shape)} {query.dtype}")
         _, hk, B, _ = key_cache.shape
         W = block_tables.shape[1]
         mcl = max_context_len if max_context_len > 0 else W * B
@@ -187,7 +192,7 @@ class FusedTP:
             _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"), _dev(block_tables, "block_tables"),
             _dev(context_lens, "context_lens"), float(scale), B, hk, S, H, D, W, int(mcl), _code(query), ws_ptr,
             ws_bytes, _stream(stream)), "pa_paged_attention_decode_tp")
-        return self.views[buf.value]
+        return self.views[buf.value][:S]
 
     def close(self):
         if getattr(self, "comm", None):

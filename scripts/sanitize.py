@@ -1,5 +1,6 @@
-"""Tiny decode steps for compute-sanitizer (memcheck / racecheck / synccheck): every
-scheduler, fused and unfused paths, copy_blocks, block sizes 1 and 16, a split context."""
+"""Tiny decode steps for compute-sanitizer (memcheck / racecheck / synccheck): the coop
+kernel with 1 and 2 partitions per CTA, fused and unfused paths, copy_blocks, block sizes
+1 and 16, a split context."""
 import os
 import sys
 
@@ -11,9 +12,11 @@ import torch  # noqa: E402
 from synth import make_config  # noqa: E402
 from tests.pathutil import gpu_step  # noqa: E402
 
-scheds = sys.argv[1:] or ["coop", "grid", "pcoop", "persistent"]
-for sched in scheds:
-    os.environ["PA_SCHED"] = sched
+import paper_2309_06180_b200 as pa  # noqa: E402
+
+for ppc in sys.argv[1:] or ["1", "2"]:
+    os.environ["PA_PPC"] = ppc
+    pa.reload_tuning()
     for name, over in (("c1_tiny", {}), ("c3_fork", dict(S=12, H=4, H_kv=4)),
                        ("explicit", dict(ctx=[0, 1, 17, 600], H=4, H_kv=4, D=128, B=1, dtype="f16", seed=3))):
         wl = make_config(name, **over)

@@ -14,6 +14,7 @@ from synth import make_config, materialize_torch, tables_torch  # noqa: E402
 
 for slots in ("1", "2"):
     os.environ["PA_SHARED_SLOTS"] = slots
+    pa.reload_tuning()
     for name, over, gs in (("c5_beam", dict(S=8, H=4, H_kv=4), 4), ("c5_beam", dict(S=6, H=2, H_kv=2, B=32), 3),
                            ("c3_fork", dict(S=12, H=2, H_kv=2, B=8), 6), ("c4_long", dict(S=4, H=2, H_kv=2), 2)):
         wl = make_config(name, **over)

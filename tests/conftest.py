@@ -25,3 +25,29 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture
+def tuning_env():
+    """Set PA_* tuning variables for one test: the library reads them once, so each change
+    is followed by pa_reload_tuning; the environment and the library's knobs are restored
+    afterwards."""
+    import paper_2309_06180_b200 as pa
+    saved = {}
+
+    def set_(name, value):
+        if name not in saved:
+            saved[name] = os.environ.get(name)
+        if value is None:
+            os.environ.pop(name, None)
+        else:
+            os.environ[name] = str(value)
+        pa.reload_tuning()
+
+    yield set_
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+    pa.reload_tuning()

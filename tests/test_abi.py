@@ -241,21 +241,25 @@ def test_tp_comm_validation():
     the fused decode entry rejects a NULL comm and a head-count mismatch."""
     import ctypes as C
     arr = (C.c_void_p * 2)(FAKE, FAKE)
-    ok = L.pa_tp_comm_create(2, 0, 8, arr, arr, arr, FAKE)
+    GB = 4 * 8 * 128 * 2  # gather buffers for 4 sequences x 8 heads x 128 f16
+    ok = L.pa_tp_comm_create(2, 0, 8, GB, arr, arr, arr, FAKE)
     assert ok
     L.pa_tp_comm_destroy(ok)
-    assert not L.pa_tp_comm_create(0, 0, 8, arr, arr, arr, FAKE)
-    assert not L.pa_tp_comm_create(2, 2, 8, arr, arr, arr, FAKE)
-    assert not L.pa_tp_comm_create(2, 0, 7, arr, arr, arr, FAKE)
-    assert not L.pa_tp_comm_create(9, 0, 9, arr, arr, arr, FAKE)
+    assert not L.pa_tp_comm_create(0, 0, 8, GB, arr, arr, arr, FAKE)
+    assert not L.pa_tp_comm_create(2, 2, 8, GB, arr, arr, arr, FAKE)
+    assert not L.pa_tp_comm_create(2, 0, 7, GB, arr, arr, arr, FAKE)
+    assert not L.pa_tp_comm_create(9, 0, 9, GB, arr, arr, arr, FAKE)
     bad = (C.c_void_p * 2)(FAKE, FAKE + 8)
-    assert not L.pa_tp_comm_create(2, 0, 8, bad, arr, arr, FAKE)
+    assert not L.pa_tp_comm_create(2, 0, 8, GB, bad, arr, arr, FAKE)
     assert _lib.last_error() != ""
     r = L.pa_paged_attention_decode_tp
     assert r(None, None, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 0.1, 16, 4, 4, 4, 128, 8, 100, 1, FAKE, 4096,
              None) == INVALID
-    comm = L.pa_tp_comm_create(2, 1, 8, arr, arr, arr, FAKE)
+    comm = L.pa_tp_comm_create(2, 1, 8, GB, arr, arr, arr, FAKE)
     assert r(comm, None, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 0.1, 16, 4, 4, 8, 128, 8, 100, 1, FAKE, 4096,
              None) == INVALID  # 8 local heads x 2 ranks != 8
+    assert r(comm, None, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 0.1, 16, 4, 5, 4, 128, 8, 100, 1, FAKE, 4096,
+             None) == INVALID  # 5 sequences do not fit gather buffers sized for 4
+    assert "gather buffers" in _lib.last_error()
     L.pa_tp_comm_destroy(comm)
     assert L.pa_ipc_handle_bytes() == 64

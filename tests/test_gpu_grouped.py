@@ -91,7 +91,7 @@ def test_grouped_decode_rejects_unsupported():
                                           wl.scale, 4)
 
 
-def test_grouped_decode_deterministic_and_stage_packing_invariant(monkeypatch):
+def test_grouped_decode_deterministic_and_stage_packing_invariant(tuning_env):
     """Full-size C5 run three times and with 1, 2 and 4 block slots per stage: outputs
     bit-identical (a row's arithmetic does not depend on which stage holds its block;
     a stage-reuse race between the producer and the two consumer warps would show here)."""
@@ -99,7 +99,7 @@ def test_grouped_decode_deterministic_and_stage_packing_invariant(monkeypatch):
     x0 = materialize_torch(wl, "cuda")
     ref = None
     for slots in ("2", "2", "1", "4", "2"):
-        monkeypatch.setenv("PA_GROUP_SLOTS", slots)
+        tuning_env("PA_GROUP_SLOTS", slots)
         out, _ = grouped_step(wl, 4, x={k: v.clone() for k, v in x0.items()})
         if ref is None:
             ref = out

@@ -273,20 +273,20 @@ def test_validate_tables():
 @pytest.mark.parametrize("name", ["c3_fork", "c4_long"])
 @pytest.mark.parametrize("mode", ["chunks4", "chunks4_1stream", "chunks1", "chunks7", "zerocopy", "split1241",
                                   "chunks4_graph"])
-def test_decode_step_host_api_matches_device_api(mode, name, monkeypatch):
+def test_decode_step_host_api_matches_device_api(mode, name, tuning_env):
     """pa_decode_step from pinned host buffers, in every transfer mode (copy-engine
     chunks on one or two compute streams, weighted chunks, captured-graph replay or eager
     enqueue, or zero-copy reads of q/k/v and writes of out by the kernel), equals the
     device API bit for bit (outputs and caches)."""
     if mode == "zerocopy":
-        monkeypatch.setenv("PA_E2E_MODE", "zerocopy")
+        tuning_env("PA_E2E_MODE", "zerocopy")
     elif mode == "split1241":
-        monkeypatch.setenv("PA_E2E_SPLIT", "1,2,4,1")
+        tuning_env("PA_E2E_SPLIT", "1,2,4,1")
     elif mode == "chunks4_graph":
-        monkeypatch.setenv("PA_E2E_GRAPH", "1")
+        tuning_env("PA_E2E_GRAPH", "1")
     else:
-        monkeypatch.setenv("PA_E2E_CHUNKS", mode[6])
-        monkeypatch.setenv("PA_E2E_STREAMS", "1" if mode.endswith("1stream") else "2")
+        tuning_env("PA_E2E_CHUNKS", mode[6])
+        tuning_env("PA_E2E_STREAMS", "1" if mode.endswith("1stream") else "2")
     wl = make_config(name, **SMALL[name])
     x = materialize_torch(wl, "cuda")
     ref, rk, rv, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()})
@@ -307,13 +307,13 @@ def test_decode_step_host_api_matches_device_api(mode, name, monkeypatch):
 
 
 @pytest.mark.parametrize("name", ["c3_fork", "c2_sharegpt"])
-def test_decode_step_graph_replay_reads_current_host_data(name, monkeypatch):
+def test_decode_step_graph_replay_reads_current_host_data(name, tuning_env):
     """pa_decode_step (PA_E2E_GRAPH=1) captures a step into a CUDA graph keyed on its
     pointers and sizes and replays it: a replay must read the host buffers' CURRENT
     contents (new queries under the same pointers) and equal the device API on them, bit
     for bit; and a call with a different batch size (another key) must not replay the
     old graph."""
-    monkeypatch.setenv("PA_E2E_GRAPH", "1")
+    tuning_env("PA_E2E_GRAPH", "1")
     wl = make_config(name, **SMALL[name])
     x = materialize_torch(wl, "cuda")
     kc, vc = x["key_cache"].clone(), x["value_cache"].clone()
@@ -344,9 +344,9 @@ def test_decode_step_graph_replay_reads_current_host_data(name, monkeypatch):
     assert torch.equal(second, ref2.cpu())
     assert not torch.equal(second, first)
     assert np.array_equal(bits(kc), bits(rk)) and np.array_equal(bits(vc), bits(rv))
-    monkeypatch.setenv("PA_E2E_GRAPH", "0")
+    tuning_env("PA_E2E_GRAPH", "0")
     assert torch.equal(call(), second)
-    monkeypatch.setenv("PA_E2E_GRAPH", "1")
+    tuning_env("PA_E2E_GRAPH", "1")
     # a smaller batch under the same buffers is a different key: outputs of its rows only
     S2 = wl.S // 2
     out.zero_()
@@ -467,22 +467,24 @@ def test_fused_decode_gqa():
 
 
 @pytest.mark.parametrize("name", ["c1_tiny", "c2_alpaca", "c2_sharegpt", "c3_fork", "c4_long"])
-def test_schedulers_bitwise_identical(name, monkeypatch):
-    """coop (default), grid, persistent, pcoop, ncoop and lcoop run the same per-(sequence, head) tile
-    arithmetic in the same order, so their outputs and cache writes are bit-identical;
-    a stage-reuse race in any pipeline would break this (full-size c2/c4, repeated)."""
+def test_pdl_and_grid_order_bitwise_identical(name, tuning_env):
+    """The coop kernel with programmatic dependent launch on/off and with the partition
+    index slowest in the grid (PA_PZ) runs the same per-(sequence, head) tile arithmetic
+    in the same order: outputs and cache writes are bit-identical, on repeated full-size
+    runs (a stage-reuse or completion-word race would break this)."""
     wl = make_config(name)
     x = materialize_torch(wl, "cuda")
     ref = None
-    for sched in ("coop", "grid", "persistent", "pcoop", "ncoop", "lcoop", "coop"):
-        monkeypatch.setenv("PA_SCHED", sched)
+    for pdl, pz in (("1", "0"), ("0", "0"), ("1", "1"), ("1", "0")):
+        tuning_env("PA_PDL", pdl)
+        tuning_env("PA_PZ", pz)
         out, kc, vc, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()}, fused=True)
         if ref is None:
             ref = (out, kc, vc)
         else:
-            assert torch.equal(out, ref[0]), sched
-            assert torch.equal(kc.view(torch.int16), ref[1].view(torch.int16)), sched
-            assert torch.equal(vc.view(torch.int16), ref[2].view(torch.int16)), sched
+            assert torch.equal(out, ref[0]), (pdl, pz)
+            assert torch.equal(kc.view(torch.int16), ref[1].view(torch.int16)), (pdl, pz)
+            assert torch.equal(vc.view(torch.int16), ref[2].view(torch.int16)), (pdl, pz)
 
 
 @pytest.mark.parametrize("B", [1, 16])
@@ -524,7 +526,7 @@ def bits_t(t):
 
 
 @pytest.mark.parametrize("name", ["c2_sharegpt", "c4_long"])
-def test_partitions_per_cta_bitwise_identical(name, monkeypatch):
+def test_partitions_per_cta_bitwise_identical(name, tuning_env):
     """The coop scheduler may walk several 512-token partitions in one CTA (PA_PPC): each
     is finished and merged exactly as with one CTA per partition, so outputs and cache
     bytes are bit-identical for any PPC (TP / batch-composition invariance is kept)."""
@@ -532,8 +534,7 @@ def test_partitions_per_cta_bitwise_identical(name, monkeypatch):
     x = materialize_torch(wl, "cuda")
     ref = None
     for ppc in ("1", "2", "3", "4"):
-        monkeypatch.setenv("PA_SCHED", "coop")
-        monkeypatch.setenv("PA_PPC", ppc)
+        tuning_env("PA_PPC", ppc)
         out, kc, vc, _ = gpu_step(wl, inputs={k: v.clone() for k, v in x.items()}, fused=True)
         if ref is None:
             ref = (out, kc)
@@ -546,7 +547,7 @@ def test_partitions_per_cta_bitwise_identical(name, monkeypatch):
                                                ("c2_sharegpt", 4, 0, 0), ("c5_beam", 3, 0, 0), ("c3_parallel", 8, 0, 0),
                                                ("c5_beam", 4, 2, 1), ("c5_beam", 4, 1, 2), ("c3_fork", 6, 1, 1),
                                                ("c3_parallel", 4, 2, 3), ("c2_sharegpt", 2, 4, 1)])
-def test_shared_decode_bitwise_equals_decode(name, gs, hpc, slots, monkeypatch):
+def test_shared_decode_bitwise_equals_decode(name, gs, hpc, slots, tuning_env):
     """N1 sharing-aware entry: every distinct block of a sequence group is loaded once;
     outputs and cache bytes bit-identical to pa_paged_attention_decode at full size,
     including groups that do not align with the requests (gs 3 / 8), several heads per
@@ -554,9 +555,9 @@ def test_shared_decode_bitwise_equals_decode(name, gs, hpc, slots, monkeypatch):
     stream through several stages)."""
     import paper_2309_06180_b200 as pa
     if hpc:
-        monkeypatch.setenv("PA_SHARED_HPC", str(hpc))
+        tuning_env("PA_SHARED_HPC", str(hpc))
     if slots:
-        monkeypatch.setenv("PA_SHARED_SLOTS", str(slots))
+        tuning_env("PA_SHARED_SLOTS", str(slots))
     wl = make_config(name)
     x = materialize_torch(wl, "cuda")
     tb = tables_torch(wl, "cuda")
@@ -574,10 +575,10 @@ def test_shared_decode_bitwise_equals_decode(name, gs, hpc, slots, monkeypatch):
 
 
 @pytest.mark.parametrize("B,slots", [(1, 0), (16, 0), (32, 0), (16, 1), (8, 2)])
-def test_shared_decode_small_vs_oracle(B, slots, monkeypatch):
+def test_shared_decode_small_vs_oracle(B, slots, tuning_env):
     import paper_2309_06180_b200 as pa
     if slots:
-        monkeypatch.setenv("PA_SHARED_SLOTS", str(slots))
+        tuning_env("PA_SHARED_SLOTS", str(slots))
     wl = make_config("c5_beam", S=14, H=4, H_kv=4, B=B)
     x = materialize_torch(wl, "cuda")
     tb = tables_torch(wl, "cuda")
