@@ -12,8 +12,12 @@ with NCCL (+ permute to [S][H][D]).
 value = logical K/V bytes read per step by all ranks / device step time (GB/s); the
 roofline object reports the dominant call (pa_paged_attention) against
 MEASURED_PEAKS.json's HBM copy bandwidth.  Inputs are seeded synthetic data with the
-BASELINE.json shapes (synth/), resident in HBM; the 2+ GB KV working set is > 15x the
-126 MB L2, so consecutive steps stream from HBM (no flush needed; stated in config).
+BASELINE.json shapes (synth/), resident in HBM.  R layer caches (each with its own
+seeded values) are rotated step by step, R chosen so that R x the K/V one step reads on
+this rank >= 4 x the L2 size queried at run time (R >= 2), so every step streams its
+cache from HBM (no flush; stated in config.l2).  The JSON line carries p10/p50/p90 of
+the per-step and per-launch event times, the same-run read-only HBM ceiling
+(pa_hbm_read_probe) beside the copy peak, and, at N > 1, per-rank GB/s and gather us.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_sharegpt] [--impl ours|reference]
 Under torchrun (N > 1) every rank runs its head shard; rank 0 prints ONE JSON line.
@@ -33,7 +37,7 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-METRIC = "paged decode-attention achieved HBM GB/s (% of peak), us/step"
+METRIC = "paged decode-attention achieved HBM GB/s (% of peak), \u00b5s/step at 1/2/4/8 GPUs"  # BASELINE.json metric
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
 
@@ -123,6 +127,8 @@ def parse():
                     help="sharing-aware decode on the CUDA cores over groups of this many sequences "
                          "(pa_paged_attention_decode_shared, SURVEY 8(f) N1; 0 = off (coop), -1 = auto: C5's "
                          "beam groups of 4, where it measured faster than coop; coop elsewhere)")
+    ap.add_argument("--layers", type=int, default=0,
+                    help="rotated layer caches (0 = auto: R x K/V read per step >= 4 x L2, R >= 2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-prefill", action="store_true", help="skip the N4 prompt-phase context line")
     ap.add_argument("--extra", action="store_true", help="also print per-config lines for the other configs")
@@ -197,6 +203,21 @@ def run_reference(a, wl, world, rank):
 
 # --------------------------------------------------------------------- our arm ---------
 
+def layer_count(kv_layer_bytes: int, l2_bytes: int, cache_alloc_bytes: int, free_bytes: int, forced: int = 0):
+    """R rotated layer caches: R x (K/V bytes one layer-step reads) >= 4 x L2,
+    R >= 2, at most 96 (OPT-175B's layer count; only tiny configs such as C1, which make no
+    HBM claim, hit it), and the R caches fit in 60% of the free device memory."""
+    if forced > 0:
+        return forced
+    r = min(96, max(2, math.ceil(4 * l2_bytes / max(1, kv_layer_bytes))))
+    fit = max(1, int(0.6 * free_bytes // max(1, cache_alloc_bytes)))
+    return max(1, min(r, fit))
+
+
+def pct(xs, q):
+    return float(np.percentile(np.asarray(xs, dtype=np.float64), q))
+
+
 def run_ours(a, wl_full, world, rank, local):
     import torch
     import torch.distributed as dist
@@ -207,11 +228,20 @@ def run_ours(a, wl_full, world, rank, local):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    props = torch.cuda.get_device_properties(dev)
+    l2_bytes = int(getattr(props, "L2_cache_size", 0) or 126 * (1 << 20))
     wl = shard(wl_full, rank, world) if world > 1 else wl_full
-    x = materialize_torch(wl, dev)
     tb = tables_torch(wl, dev)
-    q, kn, vn, kc, vc = x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"]
     bt, cl, sm, bm = tb["block_tables"], tb["context_lens"], tb["slot_mapping"], tb["block_mapping"]
+    # R layer caches rotated step by step, so consecutive steps never re-read a cache that
+    # could still sit in L2 (the rank's shard can be smaller than L2 at TP=8)
+    kv_unique_rank = wl.unique_kv_bytes()
+    cache_alloc = 2 * wl.num_blocks * wl.H_kv * wl.B * wl.D * wl.elem_bytes
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    R = layer_count(min(kv_unique_rank, wl.logical_kv_bytes()), l2_bytes, cache_alloc, free_b, a.layers)
+    layers = [materialize_torch(wl, dev, layer=l) for l in range(R)]
+    x = layers[0]
+    q = x["query"]
     out = torch.empty_like(q)
     mcl = wl.max_context_len
     ws_n = pa.paged_attention_workspace_size(wl.S, wl.H, wl.D, mcl, a.partition_tokens)
@@ -241,36 +271,64 @@ def run_ours(a, wl_full, world, rank, local):
             raise SystemExit("--shared runs the single-GPU fused decode step only")
         shared_g = 0
     stream = torch.cuda.current_stream(dev)
-    ev_a0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
-    ev_a1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
 
-    def step(i=None):
+    # every launch of the step prepared once per layer cache (pa.prepare: Python checks and
+    # argument marshalling done up front), so the timed loop is not bound by host overhead
+    def layer_calls(L):
+        q, kn, vn, kc, vc = L["query"], L["key"], L["value"], L["key_cache"], L["value_cache"]
+        pre = []
         if has_pairs:
-            pa.copy_blocks([kc], [vc], bm)
+            pre.append(pa.prepare(pa.copy_blocks, [kc], [vc], bm))
         if a.unfused:
-            pa.reshape_and_cache(kn, vn, kc, vc, sm)
-        if i is not None:
-            ev_a0[i].record(stream)
+            pre.append(pa.prepare(pa.reshape_and_cache, kn, vn, kc, vc, sm))
         if ftp is not None:  # attention + fused all-gather: rows stored into every rank's buffer
-            ftp.decode(q, kn, vn, kc, vc, bt, cl, wl.scale, max_context_len=mcl, workspace=ws)
+            attn = lambda: ftp.decode(q, kn, vn, kc, vc, bt, cl, wl.scale, max_context_len=mcl,  # noqa: E731
+                                      workspace=ws)
         elif a.unfused:
-            pa.paged_attention(out, q, kc, vc, bt, cl, wl.scale, max_context_len=mcl,
-                               partition_tokens=a.partition_tokens, workspace=ws)
+            attn = pa.prepare(pa.paged_attention, out, q, kc, vc, bt, cl, wl.scale, max_context_len=mcl,
+                              partition_tokens=a.partition_tokens, workspace=ws)
         elif grouped:  # N1: groups of sequences sharing blocks, QK^T / PV on the tensor cores
-            pa.paged_attention_decode_grouped(out, q, kn, vn, kc, vc, bt, cl, wl.scale, grouped, max_context_len=mcl,
-                                              workspace=ws)
+            attn = pa.prepare(pa.paged_attention_decode_grouped, out, q, kn, vn, kc, vc, bt, cl, wl.scale, grouped,
+                              max_context_len=mcl, workspace=ws)
         elif shared_g:  # N1: groups of sequences sharing blocks, each distinct block staged once
-            pa.paged_attention_decode_shared(out, q, kn, vn, kc, vc, bt, cl, wl.scale, shared_g, max_context_len=mcl,
-                                             workspace=ws)
+            attn = pa.prepare(pa.paged_attention_decode_shared, out, q, kn, vn, kc, vc, bt, cl, wl.scale, shared_g,
+                              max_context_len=mcl, workspace=ws)
         else:  # the decode step's cache write fused into the attention kernel
-            pa.paged_attention_decode(out, q, kn, vn, kc, vc, bt, cl, wl.scale, max_context_len=mcl, workspace=ws)
+            attn = pa.prepare(pa.paged_attention_decode, out, q, kn, vn, kc, vc, bt, cl, wl.scale,
+                              max_context_len=mcl, workspace=ws)
+        return pre, attn
+
+    calls = [layer_calls(L) for L in layers]
+    post = world > 1 and ftp is None  # the one exchange: all-gather of the output head slices (NCCL)
+    mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]  # noqa: E731
+    ev_s0, ev_a1 = mk(), mk()
+    ev_a0 = mk() if calls[0][0] else ev_s0  # attention starts the step when nothing precedes it
+    ev_s1 = mk() if post else ev_a1
+
+    def step(j, i=None):
+        pre, attn = calls[j % R]
+        if i is not None:
+            ev_s0[i].record(stream)
+        for c in pre:
+            c()
+        if i is not None and ev_a0 is not ev_s0:
+            ev_a0[i].record(stream)
+        attn()
         if i is not None:
             ev_a1[i].record(stream)
-        if world > 1 and ftp is None:  # the one exchange: all-gather of the output head slices (NCCL)
+        if post:
             full_out.copy_(gather_heads(out, buffer=gathered))
+            if i is not None:
+                ev_s1[i].record(stream)
 
-    for _ in range(max(3, a.warmup)):
-        step()
+    # warm-up behind a GPU sleep: the host's unblocked cost to issue one step is measured
+    # here (in the timed loop the launch queue fills and the host waits on the GPU)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(50_000_000)
+    hw = time.perf_counter()
+    for j in range(max(3, a.warmup)):
+        step(j)
+    host_issue_us = (time.perf_counter() - hw) / max(3, a.warmup) * 1e6
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -278,9 +336,12 @@ def run_ours(a, wl_full, world, rank, local):
     pa.take_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        torch.cuda._sleep(50_000_000)  # ~25 ms head start (untimed): the host queues steps ahead of the GPU
         e0.record(stream)
+        h0 = time.perf_counter()
         for i in range(a.steps):
-            step(i)
+            step(i, i)
+        host_us = (time.perf_counter() - h0) / a.steps * 1e6
         e1.record(stream)
         torch.cuda.synchronize()
     launches = pa.take_launch_count()
@@ -288,11 +349,21 @@ def run_ours(a, wl_full, world, rank, local):
         dist.barrier()
     torch.cuda.synchronize()
     ms_total = e0.elapsed_time(e1)
-    attn_ms = float(np.mean([ev_a0[i].elapsed_time(ev_a1[i]) for i in range(a.steps)]))
-    t = torch.tensor([ms_total, attn_ms], dtype=torch.float64, device=dev)
+    step_ms = [ev_s0[i].elapsed_time(ev_s1[i]) for i in range(a.steps)]
+    attn_l = [ev_a0[i].elapsed_time(ev_a1[i]) for i in range(a.steps)]
+    gath_l = [ev_a1[i].elapsed_time(ev_s1[i]) for i in range(a.steps)] if post else [0.0]
+    attn_ms = float(np.mean(attn_l))
+    stats = [ms_total, attn_ms, pct(step_ms, 10), pct(step_ms, 50), pct(step_ms, 90), pct(attn_l, 10),
+             pct(attn_l, 50), pct(attn_l, 90), float(np.mean(gath_l))]
+    t = torch.tensor(stats, dtype=torch.float64, device=dev)
+    per_rank = None
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total, attn_ms = float(t[0]), float(t[1])
+        allr = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allr, t)
+        per_rank = torch.stack(allr).cpu().numpy()
+        t = torch.as_tensor(per_rank.max(axis=0))
+    stats = [float(v) for v in t.tolist()]
+    ms_total, attn_ms = stats[0], stats[1]
     ms_step = ms_total / a.steps
     if ftp is not None:
         status = int(ftp.status.item())
@@ -303,8 +374,10 @@ def run_ours(a, wl_full, world, rank, local):
     # ---- e2e: the same step through pa_decode_step with pinned host buffers ----------
     e2e = None
     if not a.no_e2e:
-        e2e = run_e2e(a, wl, world, dev, {"query": q, "key": kn, "value": vn}, kc, vc, mcl, ws, stream)
+        e2e = run_e2e(a, wl, world, dev, {"query": q, "key": x["key"], "value": x["value"]}, x["key_cache"],
+                      x["value_cache"], mcl, ws, stream)
 
+    del layers, x
     probe = read_probe(dev)
     n4 = None
     if world == 1 and not a.no_prefill:
@@ -320,14 +393,16 @@ def run_ours(a, wl_full, world, rank, local):
     # sequences that share physical blocks (parallel samples, beams: C3 / C5) read each
     # shared block once from HBM at best; SURVEY §8(d) quotes those configs' % of peak on
     # the UNIQUE K/V bytes, with the logical figure beside it
-    kv_unique = wl.unique_kv_bytes()
+    kv_unique = kv_unique_rank
     shared = kv_unique < 0.99 * sb["kv_logical"]
     attn_bytes_u = attn_bytes - sb["kv_logical"] + kv_unique
     achieved_u = attn_bytes_u / (attn_ms * 1e-3) / 1e9
     value = kv_all / (ms_step * 1e-3) / 1e9
+    ach = achieved_u if shared else achieved
     # ncu_traffic.json keys: the workload for its default kernel, _grouped / _coop otherwise
     traffic = load_traffic(wl_full.name + ("_grouped" if grouped else "_coop" if auto_shared and not shared_g
                                            else "_shared" if shared_g and not auto_shared else ""), world)
+    read_kv = min(kv_unique, sb["kv_logical"])
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms_step, "us_per_step": ms_step * 1e3, "higher_is_better": True,
@@ -341,10 +416,20 @@ def run_ours(a, wl_full, world, rank, local):
                    "decode_kernel": (f"grouped{grouped} (N1, tensor cores)" if grouped else
                                      f"shared{shared_g} (N1, CUDA cores)" if shared_g else "coop"),
                    "partition_tokens": a.partition_tokens or pa.DEFAULT_PARTITION_TOKENS,
-                   "l2": "inputs larger than L2 (KV %.2f GB vs 126 MB L2); no flush" % (kv_all / 1e9)},
+                   "layer_caches": R,
+                   "l2": (f"{'inputs larger than L2' if R * read_kv >= 4 * l2_bytes else 'WORKING SET NOT >= 4x L2'}: "
+                          f"{R} layer caches rotated step by step, each step reads "
+                          f"{read_kv / 1e6:.1f} MB of K/V per rank ({R} x = {R * read_kv / 1e6:.0f} MB vs "
+                          f"{l2_bytes / 1e6:.0f} MB L2 = {R * read_kv / l2_bytes:.1f}x); no flush")},
         "tokens_per_s": wl_full.S / (ms_step * 1e-3),
         "kv_tokens_per_s": float(wl_full.context_lens.sum()) / (ms_step * 1e-3),
         "frac_of_peak": value / peak,
+        "step_us": {"mean": ms_step * 1e3, "p10": stats[2] * 1e3, "p50": stats[3] * 1e3, "p90": stats[4] * 1e3,
+                    "host_issue_us": round(host_issue_us, 2), "host_loop_us": round(host_us, 2),
+                    "note": "mean = whole timed region / steps; p10/p50/p90 of per-step CUDA events; max over ranks; "
+                            "host_issue_us = rank 0's CPU time to issue one step (prepared calls) while the GPU is "
+                            "busy elsewhere (warm-up behind a sleep): the loop is device-bound when it is below the "
+                            "step time; host_loop_us = the timed loop's CPU time per step (blocks on a full queue)"},
         "roofline": {"bound": "hbm", "kernel": (f"paged_attention_group_mma_kernel (pa_paged_attention_decode_grouped, "
                                                  f"groups of {grouped}: shared blocks loaded once, QK^T and PV as "
                                                  f"tensor-core MMAs; cache write fused)") if grouped else
@@ -352,18 +437,30 @@ def run_ours(a, wl_full, world, rank, local):
                       f"distinct block staged once for the group's members; cache write fused)") if shared_g else
                      "paged_attention_kernel (pa_paged_attention_decode: cache write + attention + split-context "
                      "merge in one launch)" if not a.unfused else "paged_attention_kernel (pa_paged_attention)",
-                     "achieved": achieved_u if shared else achieved, "peak": peak, "peak_source": peak_src,
-                     "unit": "GB/s", "frac": (achieved_u if shared else achieved) / peak, "traffic": traffic,
+                     "achieved": ach, "peak": peak, "peak_source": peak_src,
+                     "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
+                     "read_peak": probe["gbs"], "frac_of_read_peak": ach / probe["gbs"],
                      "algorithmic_bytes_per_launch": attn_bytes_u if shared else attn_bytes,
                      "basis": ("unique K/V bytes (blocks shared by samples/beams counted once; SURVEY 8(d))"
                                if shared else "logical K/V bytes (no sharing)"),
                      "achieved_logical": achieved, "frac_logical": achieved / peak,
                      "kv_unique_over_logical": kv_unique / sb["kv_logical"],
-                     "avg_launch_ms": attn_ms},
-        "read_probe_gbs": probe,
+                     "avg_launch_ms": attn_ms,
+                     "launch_us": {"p10": stats[5] * 1e3, "p50": stats[6] * 1e3, "p90": stats[7] * 1e3}},
+        "read_probe": probe,
         "clocks": clk.summary(),
         "gpu_launches": launches,
     }
+    if per_rank is not None:
+        rb = attn_bytes_u if shared else attn_bytes
+        line["per_rank"] = {
+            "attention_gbs": [round(rb / (r[1] * 1e-3) / 1e9, 1) for r in per_rank],
+            "frac_of_peak": [round(rb / (r[1] * 1e-3) / 1e9 / peak, 4) for r in per_rank],
+            "step_us_p50": [round(r[3] * 1e3, 2) for r in per_rank],
+            "gather_us": ([round(r[8] * 1e3, 2) for r in per_rank] if ftp is None else None),
+            "gather_note": ("NCCL all_gather_into_tensor + permute, CUDA events after the attention launch"
+                            if ftp is None else "fused: the all-gather stores happen inside the attention kernel "
+                            "and its flag handshake; attention_gbs includes them")}
     if e2e is not None:
         line["e2e"] = e2e
     if n4 is not None:
@@ -417,21 +514,47 @@ def prefill_summary(dev, name: str = "p_2k", iters: int = 20):
             "note": "tcgen05 prompt-phase kernel (SURVEY §8(f) N4), context only; see DESIGN.md §8c"}
 
 
+PROBE_SHAPES = ((8192, 3, 4), (32768, 2, 2), (65536, 2, 1))  # (chunk B, stages, CTAs/SM): the best of
+# scripts/read_probe.py's sweep on a B200 (profiles/r02_read_probe.txt), 7.37-7.39 TB/s
+
+
 def read_probe(dev, gib: float = 4.0):
-    """Same-run read-only HBM probe: torch's sum over a 4 GiB fp16 buffer, best of 5
-    (context for the copy-based MEASURED_PEAKS number; never the roofline peak)."""
+    """Same-run read-only HBM ceiling: pa_hbm_read_probe streams a 4 GiB
+    buffer into shared memory with 1-D bulk copies (the attention kernel's load path) and
+    writes nothing but one word per CTA; best of 6.  Beside it, torch's copy (read+write,
+    the MEASURED_PEAKS method) in the same run."""
     import torch
-    x = torch.ones(int(gib * (1 << 30)) // 2, dtype=torch.float16, device=dev)
-    best = 0.0
-    for _ in range(6):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        x.sum(dtype=torch.float32)
-        e1.record()
-        torch.cuda.synchronize()
-        best = max(best, x.numel() * 2 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
-    del x
-    return round(best, 1)
+
+    import paper_2309_06180_b200 as pa
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    x = torch.empty(int(gib * (1 << 30)), dtype=torch.uint8, device=dev)
+    x.fill_(1)
+    sink = torch.zeros(8 * sms, dtype=torch.int32, device=dev)
+
+    def best_of(fn, nbytes, n=6):
+        b = 0.0
+        for _ in range(n):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            b = max(b, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        return round(b, 1)
+
+    shapes = {}
+    for chunk, stages, cps in PROBE_SHAPES:
+        shapes[f"{chunk}x{stages}x{cps}"] = best_of(
+            lambda: pa.hbm_read_probe(x, sink, chunk=chunk, stages=stages, ctas=cps * sms), x.numel())
+    gbs = max(shapes.values())
+    half = x.numel() // 2
+    a_, b_ = x[:half], x[half:]
+    copy = best_of(lambda: b_.copy_(a_), 2 * half)
+    del x, a_, b_
+    return {"gbs": gbs, "copy_gbs": copy, "shapes": shapes,
+            "how": f"pa_hbm_read_probe: {gib:g} GiB streamed into shared memory by bulk copies (chunk B x stages x "
+                   "CTAs/SM as keyed in shapes), no global writes, best of 6 each, gbs = the max; copy_gbs = torch "
+                   "copy_ of 2 GiB (read+write bytes)"}
 
 
 def run_e2e(a, wl, world, dev, x, kc, vc, mcl, ws, stream):

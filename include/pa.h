@@ -412,6 +412,20 @@ int pa_alloc_refcount(const pa_alloc_t* a, int block);
 int pa_alloc_num_free(const pa_alloc_t* a);
 int pa_alloc_num_blocks_of(const pa_alloc_t* a, int seq); /* -1 if unknown */
 
+/* ------------------------------------------------------------------------------------
+ * pa_hbm_read_probe -- measurement helper (not on the hot path): the same-run read-only
+ * HBM ceiling for the roofline (SURVEY §8(d) asks for a read-only probe beside the copy
+ * peak; the decode kernel is a read stream).  Persistent CTAs (grid = `ctas`,
+ * <= 0 -> 2 per SM) stream the buffer `buf` (DEVICE, `bytes` a multiple of `chunk`, 16-B
+ * aligned) into shared memory with 1-D bulk copies of `chunk` bytes (multiple of 16,
+ * <= 64 KiB), `stages` in flight per CTA (stages * chunk <= 200 KiB), the attention
+ * kernel's own load mechanism.  Nothing is written to global memory except one 32-bit
+ * word per CTA into `sink` (DEVICE, >= grid words).  Asynchronous on `stream`; time it
+ * with events.  Errors: PA_ERR_INVALID_ARG on bad sizes / pointers.
+ * ---------------------------------------------------------------------------------- */
+pa_status_t pa_hbm_read_probe(const void* buf, size_t bytes, int chunk, int stages, int ctas,
+                              uint32_t* sink, pa_stream_t stream);
+
 /* Tests / A-B scripts only: re-read the PA_* tuning environment variables (read once,
  * at the first call, otherwise; never on the launch path).  Not thread-safe with
  * concurrent launches. */

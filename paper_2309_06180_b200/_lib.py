@@ -64,6 +64,7 @@ _sig("pa_tp_comm_create", _vp, [_i32, _i32, _i32, _sz, ctypes.POINTER(_vp), ctyp
 _sig("pa_tp_comm_destroy", None, [_vp])
 _sig("pa_paged_attention_decode_tp", _i32, [_vp, ctypes.POINTER(ctypes.c_int), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                             _f32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _sz, _vp])
+_sig("pa_hbm_read_probe", _i32, [_vp, _sz, _i32, _i32, _i32, _vp, _vp])
 _sig("pa_ipc_handle_bytes", _sz, [])
 _sig("pa_ipc_get_handle", _i32, [_vp, _vp])
 _sig("pa_ipc_open_handle", _i32, [_vp, ctypes.POINTER(_vp)])

@@ -1180,6 +1180,24 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     return PA_OK;
 }
 
+pa_status_t pa_hbm_read_probe(const void* buf, size_t bytes, int chunk, int stages, int ctas, uint32_t* sink,
+                              pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(chunk >= 16 && chunk % 16 == 0 && chunk <= 65536, "chunk must be a multiple of 16 in [16, 65536]");
+    REQUIRE(stages >= 1 && (size_t)stages * chunk <= 200 * 1024, "stages * chunk must be <= 200 KiB");
+    REQUIRE(bytes > 0 && bytes % (size_t)chunk == 0, "bytes must be a positive multiple of chunk");
+    REQUIRE_PTR(buf, 16);
+    REQUIRE_PTR(sink, 4);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = ctas > 0 ? ctas : 2 * sms;
+    cudaError_t e = pa::launch_hbm_read_probe(buf, (int64_t)(bytes / chunk), chunk, stages, grid, sink,
+                                              (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pa_hbm_read_probe");
+    return PA_OK;
+}
+
 // ---- test-only helpers -------------------------------------------------------------
 
 pa_status_t pa_debug_gather_kv(void* k_out, void* v_out, const void* key_cache, const void* value_cache,

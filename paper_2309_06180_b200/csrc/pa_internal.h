@@ -158,6 +158,8 @@ cudaError_t launch_debug_gather(const GatherParams& p, int dtype, int head_dim, 
 cudaError_t launch_reshape_and_cache(const CacheWriteParams& p, cudaStream_t stream);
 cudaError_t launch_copy_blocks(const CopyBlocksParams& p, int num_layers, int num_pairs, cudaStream_t stream);
 cudaError_t launch_swap_blocks(const SwapBlocksParams& p, int num_layers, int num_pairs, cudaStream_t stream);
+cudaError_t launch_hbm_read_probe(const void* buf, int64_t nchunks, int chunk, int stages, int grid, uint32_t* sink,
+                                  cudaStream_t stream);
 cudaError_t launch_validate_tables(const int32_t* bt, const int32_t* ctx, int S, int W, int B, int NB,
                                    unsigned long long* d_first_bad, cudaStream_t stream);
 

@@ -7,6 +7,7 @@ computation happens in the library's sm_100a kernels.  P:N = PAPER.md line N.
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import torch
 
@@ -54,6 +55,44 @@ def _check(dtype=None, idx32=(), idx64=(), **tensors):
             raise TypeError(f"{name} must be int64 (got {t.dtype})")
 
 
+_CAPTURE = threading.local()
+
+
+def _call(name: str, args: tuple):
+    """Issue C entry point `name` -- or, inside prepare(), hand the marshalled call back."""
+    f = getattr(_lib.raw(), name)
+    if getattr(_CAPTURE, "on", False):
+        _CAPTURE.got = (f, args, name)
+        return
+    check(f(*args), name)
+
+
+def prepare(fn, *args, **kwargs):
+    """A zero-argument callable that re-issues ``fn(*args, **kwargs)`` -- one of this
+    module's launch entry points -- with the Python-side checks and marshalling done once:
+    same pointers, sizes and stream (captured now; the tensors are kept alive by the
+    callable).  For launch-bound loops such as bench.py's timed region, where the
+    per-call Python overhead would otherwise approach a short kernel's duration."""
+    _CAPTURE.on, _CAPTURE.got = True, None
+    try:
+        fn(*args, **kwargs)
+        got = _CAPTURE.got
+    finally:
+        _CAPTURE.on = False
+    if got is None:
+        raise ValueError(f"{getattr(fn, '__name__', fn)} issued no library call (nothing to prepare)")
+    f, cargs, name = got
+    keep = (args, kwargs)
+
+    def run():
+        st = f(*cargs)
+        if st:
+            raise _lib.PagedAttnError(st, name)
+        return keep
+
+    return run
+
+
 def _stream(stream) -> int:
     if stream is None:
         return torch.cuda.current_stream().cuda_stream
@@ -86,11 +125,11 @@ def paged_attention(out, query, key_cache, value_cache, block_tables, context_le
         workspace = torch.empty(need, dtype=torch.uint8, device=query.device)
     ws_ptr = _dev(workspace, "workspace") if workspace is not None else None
     ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
-    check(_lib.raw().pa_paged_attention_ex(
+    _call("pa_paged_attention_ex", (
         _dev(out, "out"), _dev(query, "query"), _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"),
         _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"), float(scale), int(block_size),
         int(num_kv_heads), S, H, D, W, int(mcl), _code(query), int(partition_tokens), ws_ptr, ws_bytes,
-        _stream(stream)), "pa_paged_attention")
+        _stream(stream)))
     return out
 
 
@@ -109,11 +148,10 @@ def paged_attention_decode(out, query, key, value, key_cache, value_cache, block
         workspace = torch.empty(need, dtype=torch.uint8, device=query.device)
     ws_ptr = _dev(workspace, "workspace") if workspace is not None else None
     ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
-    check(_lib.raw().pa_paged_attention_decode(
+    _call("pa_paged_attention_decode", (
         _dev(out, "out"), _dev(query, "query"), _dev(key, "key"), _dev(value, "value"), _dev(key_cache, "key_cache"),
         _dev(value_cache, "value_cache"), _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"),
-        float(scale), B, hk, S, H, D, W, int(mcl), _code(query), ws_ptr, ws_bytes, _stream(stream)),
-        "pa_paged_attention_decode")
+        float(scale), B, hk, S, H, D, W, int(mcl), _code(query), ws_ptr, ws_bytes, _stream(stream)))
     return out
 
 
@@ -133,11 +171,10 @@ def paged_attention_decode_shared(out, query, key, value, key_cache, value_cache
         workspace = torch.empty(need, dtype=torch.uint8, device=query.device)
     ws_ptr = _dev(workspace, "workspace") if workspace is not None else None
     ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
-    check(_lib.raw().pa_paged_attention_decode_shared(
+    _call("pa_paged_attention_decode_shared", (
         _dev(out, "out"), _dev(query, "query"), _dev(key, "key"), _dev(value, "value"), _dev(key_cache, "key_cache"),
         _dev(value_cache, "value_cache"), _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"),
-        float(scale), B, hk, S, H, D, W, int(mcl), int(group_size), _code(query), ws_ptr, ws_bytes, _stream(stream)),
-        "pa_paged_attention_decode_shared")
+        float(scale), B, hk, S, H, D, W, int(mcl), int(group_size), _code(query), ws_ptr, ws_bytes, _stream(stream)))
     return out
 
 
@@ -159,11 +196,11 @@ def paged_attention_decode_grouped(out, query, key, value, key_cache, value_cach
         workspace = torch.empty(need, dtype=torch.uint8, device=query.device)
     ws_ptr = _dev(workspace, "workspace") if workspace is not None else None
     ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
-    check(_lib.raw().pa_paged_attention_decode_grouped(
+    _call("pa_paged_attention_decode_grouped", (
         _dev(out, "out"), _dev(query, "query"), _dev(key, "key"), _dev(value, "value"), _dev(key_cache, "key_cache"),
         _dev(value_cache, "value_cache"), _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"),
         float(scale), B, hk, NB, S, H, D, W, int(mcl), int(group_size), _code(query), ws_ptr, ws_bytes,
-        _stream(stream)), "pa_paged_attention_decode_grouped")
+        _stream(stream)))
     return out
 
 
@@ -189,11 +226,11 @@ def paged_prefill_attention(out, query, key_cache, value_cache, block_tables, co
         max_query_len = int((query_start[1:] - query_start[:-1]).max().item()) if S > 0 else 0
     if workspace is None:
         workspace = torch.empty(PREFILL_WORKSPACE_BYTES, dtype=torch.uint8, device=query.device)
-    check(_lib.raw().pa_paged_prefill_attention(
+    _call("pa_paged_prefill_attention", (
         _dev(out, "out"), _dev(query, "query"), _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"),
         _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"), _dev(query_start, "query_start"),
         float(scale), B, hk, NB, S, H, D, W, T, int(max_query_len), _code(query), _dev(workspace, "workspace"),
-        workspace.numel() * workspace.element_size(), _stream(stream)), "pa_paged_prefill_attention")
+        workspace.numel() * workspace.element_size(), _stream(stream)))
     return out
 
 
@@ -204,9 +241,9 @@ def reshape_and_cache(key, value, key_cache, value_cache, slot_mapping, stream=N
            value_cache=value_cache)
     T, hk, D = key.shape
     B = key_cache.shape[2]
-    check(_lib.raw().pa_reshape_and_cache(
+    _call("pa_reshape_and_cache", (
         _dev(key, "key"), _dev(value, "value"), _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"),
-        _dev(slot_mapping, "slot_mapping"), T, hk, D, B, _code(key), _stream(stream)), "pa_reshape_and_cache")
+        _dev(slot_mapping, "slot_mapping"), T, hk, D, B, _code(key), _stream(stream)))
 
 
 def copy_blocks(key_caches, value_caches, block_mapping, stream=None):
@@ -221,8 +258,7 @@ def copy_blocks(key_caches, value_caches, block_mapping, stream=None):
     _, hk, B, D = key_caches[0].shape
     P = block_mapping.shape[0] if block_mapping.numel() else 0
     bm = _dev(block_mapping, "block_mapping") if P else None
-    check(_lib.raw().pa_copy_blocks(kp, vp, L, bm, P, hk, B, D, _code(key_caches[0]), _stream(stream)),
-          "pa_copy_blocks")
+    _call("pa_copy_blocks", (kp, vp, L, bm, P, hk, B, D, _code(key_caches[0]), _stream(stream)))
 
 
 def _dev_or_pinned(t: torch.Tensor, name: str) -> int:
@@ -293,6 +329,16 @@ def decode_step(host_out, host_query, host_key, host_value, host_slot_mapping, h
         _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"), float(scale), B, hk, S, H, D, W,
         int(max_context_len), _code(host_query), _dev(staging, "staging"), staging.numel(), ws_ptr, ws_bytes,
         _stream(stream)), "pa_decode_step")
+
+
+def hbm_read_probe(buf: torch.Tensor, sink: torch.Tensor, chunk: int = 32768, stages: int = 4, ctas: int = 0,
+                   stream=None):
+    """Measurement helper (pa.h pa_hbm_read_probe): stream `buf` (device, contiguous,
+    nbytes a multiple of `chunk`) into shared memory with bulk copies, writing only one
+    word per CTA into `sink` (int32/uint32 device tensor with >= grid elements)."""
+    nbytes = buf.numel() * buf.element_size()
+    check(_lib.raw().pa_hbm_read_probe(_dev(buf, "buf"), nbytes, chunk, stages, ctas, _dev(sink, "sink"),
+                                       _stream(stream)), "pa_hbm_read_probe")
 
 
 def debug_gather_kv(key_cache, value_cache, block_tables, context_lens, max_ctx: int, stream=None):

@@ -161,14 +161,19 @@ def _perm(seed: int, n: int) -> np.ndarray:
 
 # ------------------------------------------------------------------ placement ------
 
-def place_private(ctx: np.ndarray, B: int, seed: int, pool_factor: float = 1.1, min_extra: int = 0):
+def place_private(ctx: np.ndarray, B: int, seed: int, pool_factor: float = 1.1, min_extra: int = 0,
+                  placement: str = "shuffled"):
     """Every sequence owns its blocks (no sharing).  Returns tables, NB, slot_mapping,
-    live mask.  Blocks come from a shuffled pool of ceil(pool_factor * needed) ids."""
+    live mask.  Blocks come from a shuffled pool of ceil(pool_factor * needed) ids
+    (placement="sorted": ids handed out in order, each sequence's blocks consecutive --
+    the contiguous-cache ablation, SURVEY §8(d) "Block placement")."""
     S = len(ctx)
     nb = (ctx + B - 1) // B
     need = int(nb.sum())
     NB = max(1, int(math.ceil(pool_factor * need)) + min_extra)
-    perm = _perm(seed, NB)
+    if placement not in ("shuffled", "sorted"):
+        raise ValueError(f"placement must be 'shuffled' or 'sorted' (got {placement!r})")
+    perm = _perm(seed, NB) if placement == "shuffled" else np.arange(NB)
     W = max(1, int(nb.max()) if S else 1)
     bt = np.full((S, W), -1, dtype=np.int32)
     live = np.zeros((NB, B), dtype=bool)
@@ -363,7 +368,8 @@ CONFIGS = {
 
 def make_config(name: str, **over) -> Workload:
     """Build a named config; keyword overrides: seed, S, H, H_kv, D, B, dtype, mix,
-    n, stickiness, ctx (explicit context lengths for 'explicit' kind)."""
+    n, stickiness, ctx (explicit context lengths for 'explicit' kind), placement
+    ('shuffled' default / 'sorted', private-block kinds only)."""
     c = dict(CONFIGS[name]) if name in CONFIGS else dict(kind="explicit", seed=0)
     c.update({k: v for k, v in over.items() if v is not None})
     seed, B, D, H, H_kv, dtype = c["seed"], c["B"], c["D"], c["H"], c["H_kv"], c["dtype"]
@@ -386,7 +392,9 @@ def make_config(name: str, **over) -> Workload:
             ctx = np.asarray(c["ctx"], dtype=np.int64)
             S = len(ctx)
             pool_factor = c.get("pool_factor", 2.0)
-        bt, NB, slots, live = place_private(ctx, B, seed, pool_factor, c.get("min_extra", 1))
+        bt, NB, slots, live = place_private(ctx, B, seed, pool_factor, c.get("min_extra", 1),
+                                            c.get("placement", "shuffled"))
+        meta["placement"] = c.get("placement", "shuffled")
         ctx = ctx.astype(np.int32)
     elif kind in ("parallel", "parallel_fork"):
         n = c["n"]

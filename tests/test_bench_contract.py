@@ -45,6 +45,8 @@ def test_our_arm_contract():
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= d["steps"]
+    assert d["config"]["layer_caches"] >= 2 and d["step_us"]["p10"] <= d["step_us"]["p50"] <= d["step_us"]["p90"]
+    assert d["read_probe"]["gbs"] > 0 and abs(r["frac_of_read_peak"] - r["achieved"] / r["read_peak"]) < 1e-9
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
 
@@ -59,3 +61,37 @@ def test_c5_defaults_to_sharing_aware_decode():
     assert a["config"]["decode_kernel"].startswith("shared4") and b["config"]["decode_kernel"] == "coop"
     for d in (a, b):
         assert d["roofline"]["basis"].startswith("unique") and d["roofline"]["kv_unique_over_logical"] < 0.5
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gather", ["nccl", "fused"])
+def test_two_rank_bench_line(gather):
+    """bench.py under torchrun with 2 ranks sharing the one GPU (gloo for the plumbing and
+    the all-gather; the fused path over CUDA IPC): rank 0 prints one line with the N>1
+    fields (per-rank GB/s, gather us for the NCCL-style path, rotated layer caches)."""
+    env = dict(os.environ, PA_BENCH_SAME_DEVICE="1", PA_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--steps", "5", "--warmup", "3", "--config", "c2_alpaca", "--tp-gather", gather,
+                        "--no-cpu-baseline", "--no-prefill", "--no-e2e"], capture_output=True, text=True, timeout=600,
+                       cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "tp2" and d["config"]["layer_caches"] >= 2
+    assert d["config"]["tp_gather"] == gather
+    pr = d["per_rank"]
+    assert len(pr["attention_gbs"]) == 2 and all(v > 0 for v in pr["attention_gbs"])
+    if gather == "nccl":
+        assert len(pr["gather_us"]) == 2
+    assert d["step_us"]["p10"] <= d["step_us"]["p50"] <= d["step_us"]["p90"]

@@ -115,3 +115,20 @@ def test_sharing_fixtures():
 def test_determinism():
     a, b = make_config("c5_beam", S=16), make_config("c5_beam", S=16)
     assert np.array_equal(a.block_tables, b.block_tables) and np.array_equal(a.block_mapping, b.block_mapping)
+
+
+def test_sorted_placement_is_consecutive():
+    """placement='sorted' (the contiguous-cache ablation) hands out block ids in order:
+    each sequence's blocks are consecutive, with the same lengths, pool size and live-slot
+    count as the shuffled placement."""
+    a = make_config("c2_alpaca", S=16, H=2, H_kv=2)
+    b = make_config("c2_alpaca", S=16, H=2, H_kv=2, placement="sorted")
+    assert np.array_equal(a.context_lens, b.context_lens) and a.num_blocks == b.num_blocks
+    assert a.live.sum() == b.live.sum()
+    off = 0
+    for s in range(b.S):
+        nb = -(-int(b.context_lens[s]) // b.B)
+        assert np.array_equal(b.block_tables[s, :nb], np.arange(off, off + nb))
+        off += nb
+    with pytest.raises(ValueError):
+        make_config("c2_alpaca", S=4, H=2, H_kv=2, placement="random")
