@@ -87,15 +87,32 @@ pa_status_t pa_paged_attention(void* out, const void* query, const void* key_cac
                                void* workspace, size_t workspace_bytes, pa_stream_t stream);
 
 /* Same, with an explicit partition size in tokens (a positive multiple of 16;
- * 0 -> PA_DEFAULT_PARTITION_TOKENS).  A partition size >= max_context_len runs the
- * single-pass kernel only.  Used by tests (split vs single-pass) and ablations. */
+ * 0 -> PA_DEFAULT_PARTITION_TOKENS; a partition size >= max_context_len runs the
+ * single-pass kernel only) and an optional grid order host_seq_order (HOST int32
+ * [num_seqs], a permutation of 0..num_seqs-1, e.g. from pa_decode_plan; NULL = natural
+ * order; honoured when num_seqs <= PA_MAX_SEQ_ORDER, ignored above).  The order is
+ * scheduling only -- which sequence's CTAs the hardware dispatches first -- and never
+ * changes a result bit.  Not a permutation -> PA_ERR_INVALID_ARG. */
+#define PA_MAX_SEQ_ORDER 2048
 pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_cache,
                                   const void* value_cache, const int32_t* block_tables,
                                   const int32_t* context_lens, float scale, int block_size,
                                   int num_kv_heads, int num_seqs, int num_heads, int head_dim,
                                   int max_blocks_per_seq, int max_context_len, pa_dtype_t dtype,
-                                  int partition_tokens, void* workspace, size_t workspace_bytes,
-                                  pa_stream_t stream);
+                                  int partition_tokens, const int32_t* host_seq_order,
+                                  void* workspace, size_t workspace_bytes, pa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------
+ * pa_decode_plan -- the longest-first grid order of a decode batch (scheduling only).
+ * host_context_lens: HOST int32 [num_seqs]; order_out: HOST int32 [num_seqs] receives
+ * the sequence indices sorted by context length, longest first (ties in index order).
+ * With the natural order the CTAs of a long sequence that happens to sit at the end of
+ * the batch start in the last wave and run alone (the kernel's tail); longest first they
+ * start in the first wave and short sequences fill the end.  O(S log S) on the host,
+ * once per decode iteration: every layer of the iteration reuses it, as it reuses the
+ * block tables (the paper's scheduler already holds the lengths on the CPU).
+ * ---------------------------------------------------------------------------------- */
+pa_status_t pa_decode_plan(const int32_t* host_context_lens, int num_seqs, int32_t* order_out);
 
 /* ------------------------------------------------------------------------------------
  * pa_paged_attention_decode -- the decode step's cache write fused into the attention
@@ -105,14 +122,16 @@ pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_
  * block_tables[s][(ctx-1)/B]*B + (ctx-1)%B).  Equivalent to pa_reshape_and_cache with
  * that slot_mapping followed by pa_paged_attention, bit for bit: the cache receives the
  * same bytes and the output is identical.  Sequences with ctx == 0 write nothing and
- * output 0.  Default partitioning; workspace as for pa_paged_attention.
+ * output 0.  Default partitioning; workspace as for pa_paged_attention; host_seq_order
+ * as for pa_paged_attention_ex (NULL = natural order).
  * ---------------------------------------------------------------------------------- */
 pa_status_t pa_paged_attention_decode(void* out, const void* query, const void* key,
                                       const void* value, void* key_cache, void* value_cache,
                                       const int32_t* block_tables, const int32_t* context_lens,
                                       float scale, int block_size, int num_kv_heads, int num_seqs,
                                       int num_heads, int head_dim, int max_blocks_per_seq,
-                                      int max_context_len, pa_dtype_t dtype, void* workspace,
+                                      int max_context_len, pa_dtype_t dtype,
+                                      const int32_t* host_seq_order, void* workspace,
                                       size_t workspace_bytes, pa_stream_t stream);
 
 /* ------------------------------------------------------------------------------------
@@ -225,7 +244,8 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
  * sequence of calls.  Output bits equal the single-GPU decode's.  Returns
  * PA_ERR_INVALID_ARG if num_seqs*H_total*head_dim*e exceeds gather_bytes or the local
  * head count does not match.  The attention kernel issues a system-scope fence after
- * its peer stores, before the flag kernel's st.release.sys.
+ * its peer stores, before the flag kernel's st.release.sys.  host_seq_order as for
+ * pa_paged_attention_ex.
  * ---------------------------------------------------------------------------------- */
 typedef struct pa_tp_comm pa_tp_comm_t;
 pa_tp_comm_t* pa_tp_comm_create(int world, int rank, int num_heads_total, size_t gather_bytes,
@@ -238,7 +258,8 @@ pa_status_t pa_paged_attention_decode_tp(pa_tp_comm_t* comm, int* buffer_out, co
                                          const int32_t* context_lens, float scale, int block_size,
                                          int num_kv_heads, int num_seqs, int num_heads,
                                          int head_dim, int max_blocks_per_seq,
-                                         int max_context_len, pa_dtype_t dtype, void* workspace,
+                                         int max_context_len, pa_dtype_t dtype,
+                                         const int32_t* host_seq_order, void* workspace,
                                          size_t workspace_bytes, pa_stream_t stream);
 
 /* CUDA IPC of device allocations between the ranks' processes (for the gather buffers and

@@ -38,9 +38,10 @@ def _sig(name, res, args):
 _sig("pa_paged_attention", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
                                   _i32, _vp, _sz, _vp])
 _sig("pa_paged_attention_ex", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
-                                     _i32, _i32, _vp, _sz, _vp])
+                                     _i32, _i32, _vp, _vp, _sz, _vp])
 _sig("pa_paged_attention_decode", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _i32,
-                                         _i32, _i32, _i32, _vp, _sz, _vp])
+                                         _i32, _i32, _i32, _vp, _vp, _sz, _vp])
+_sig("pa_decode_plan", _i32, [_vp, _i32, _vp])
 _sig("pa_paged_attention_decode_shared", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32,
                                                 _i32, _i32, _i32, _i32, _i32, _vp, _sz, _vp])
 _sig("pa_paged_attention_decode_grouped", _i32, [_vp] * 8 + [_f32] + [_i32] * 10 + [_vp, _sz, _vp])
@@ -63,7 +64,7 @@ _sig("pa_tp_comm_create", _vp, [_i32, _i32, _i32, _sz, ctypes.POINTER(_vp), ctyp
                                 ctypes.POINTER(_vp), _vp])
 _sig("pa_tp_comm_destroy", None, [_vp])
 _sig("pa_paged_attention_decode_tp", _i32, [_vp, ctypes.POINTER(ctypes.c_int), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                                            _f32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _sz, _vp])
+                                            _f32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _sz, _vp])
 _sig("pa_hbm_read_probe", _i32, [_vp, _sz, _i32, _i32, _i32, _vp, _vp])
 _sig("pa_ipc_handle_bytes", _sz, [])
 _sig("pa_ipc_get_handle", _i32, [_vp, _vp])

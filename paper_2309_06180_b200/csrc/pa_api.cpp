@@ -250,7 +250,8 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
                            const int32_t* context_lens, float scale, int block_size, int num_kv_heads, int num_seqs,
                            int num_heads, int head_dim, int max_blocks_per_seq, int max_context_len,
                            pa_dtype_t dtype, int partition_tokens, void* workspace, size_t workspace_bytes,
-                           pa_stream_t stream, int group_size = 1, const TpOut* tp = nullptr) {
+                           pa_stream_t stream, int group_size = 1, const TpOut* tp = nullptr,
+                           const int32_t* host_seq_order = nullptr) {
     REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
     REQUIRE(num_seqs >= 0, "num_seqs must be >= 0 (got %d)", num_seqs);
     REQUIRE(num_heads > 0 && num_kv_heads > 0, "num_heads and num_kv_heads must be positive");
@@ -363,6 +364,20 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     p.S = num_seqs;
     p.pz = tu.pz;
     p.epoch = pa::next_epoch();
+    if (host_seq_order != nullptr && sched == 2 && num_seqs <= pa::kMaxSeqOrder) {
+        // a permutation of [0, num_seqs) (checked: a repeated or missing sequence would
+        // compute one output twice and leave another unwritten)
+        static thread_local std::vector<unsigned char> seen;
+        seen.assign((size_t)num_seqs, 0);
+        for (int i = 0; i < num_seqs; ++i) {
+            const int32_t v = host_seq_order[i];
+            REQUIRE(v >= 0 && v < num_seqs && !seen[(size_t)v], "host_seq_order is not a permutation of [0, %d) "
+                    "(entry %d = %d)", num_seqs, i, (int)v);
+            seen[(size_t)v] = 1;
+            p.seq_order[i] = (uint16_t)v;
+        }
+        p.n_order = num_seqs;
+    }
     if (tp != nullptr) {
         p.n_out_peers = tp->n;
         p.out_H = tp->H_total;
@@ -381,12 +396,13 @@ pa_status_t pa_paged_attention_ex(void* out, const void* query, const void* key_
                                   const int32_t* block_tables, const int32_t* context_lens, float scale,
                                   int block_size, int num_kv_heads, int num_seqs, int num_heads, int head_dim,
                                   int max_blocks_per_seq, int max_context_len, pa_dtype_t dtype,
-                                  int partition_tokens, void* workspace, size_t workspace_bytes,
-                                  pa_stream_t stream) {
+                                  int partition_tokens, const int32_t* host_seq_order, void* workspace,
+                                  size_t workspace_bytes, pa_stream_t stream) {
     g_err.clear();
     return attention_impl(out, query, nullptr, nullptr, key_cache, value_cache, block_tables, context_lens, scale,
                           block_size, num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq,
-                          max_context_len, dtype, partition_tokens, workspace, workspace_bytes, stream);
+                          max_context_len, dtype, partition_tokens, workspace, workspace_bytes, stream, 1, nullptr,
+                          host_seq_order);
 }
 
 pa_status_t pa_paged_attention_decode_shared(void* out, const void* query, const void* key, const void* value,
@@ -407,13 +423,13 @@ pa_status_t pa_paged_attention_decode(void* out, const void* query, const void* 
                                       void* key_cache, void* value_cache, const int32_t* block_tables,
                                       const int32_t* context_lens, float scale, int block_size, int num_kv_heads,
                                       int num_seqs, int num_heads, int head_dim, int max_blocks_per_seq,
-                                      int max_context_len, pa_dtype_t dtype, void* workspace,
-                                      size_t workspace_bytes, pa_stream_t stream) {
+                                      int max_context_len, pa_dtype_t dtype, const int32_t* host_seq_order,
+                                      void* workspace, size_t workspace_bytes, pa_stream_t stream) {
     g_err.clear();
     REQUIRE(key != nullptr && value != nullptr, "key/value (the step's new token) are NULL");
     return attention_impl(out, query, key, value, key_cache, value_cache, block_tables, context_lens, scale,
                           block_size, num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq,
-                          max_context_len, dtype, 0, workspace, workspace_bytes, stream);
+                          max_context_len, dtype, 0, workspace, workspace_bytes, stream, 1, nullptr, host_seq_order);
 }
 
 pa_status_t pa_paged_attention(void* out, const void* query, const void* key_cache, const void* value_cache,
@@ -423,7 +439,7 @@ pa_status_t pa_paged_attention(void* out, const void* query, const void* key_cac
                                pa_stream_t stream) {
     return pa_paged_attention_ex(out, query, key_cache, value_cache, block_tables, context_lens, scale, block_size,
                                  num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq, max_context_len,
-                                 dtype, 0, workspace, workspace_bytes, stream);
+                                 dtype, 0, nullptr, workspace, workspace_bytes, stream);
 }
 
 namespace {
@@ -673,7 +689,8 @@ pa_status_t pa_paged_attention_decode_tp(pa_tp_comm_t* comm, int* buffer_out, co
                                          const int32_t* block_tables, const int32_t* context_lens, float scale,
                                          int block_size, int num_kv_heads, int num_seqs, int num_heads, int head_dim,
                                          int max_blocks_per_seq, int max_context_len, pa_dtype_t dtype,
-                                         void* workspace, size_t workspace_bytes, pa_stream_t stream) {
+                                         const int32_t* host_seq_order, void* workspace, size_t workspace_bytes,
+                                         pa_stream_t stream) {
     g_err.clear();
     REQUIRE(comm != nullptr, "comm is NULL");
     REQUIRE(num_heads * comm->world == comm->H_total, "local heads (%d) x world (%d) != total heads (%d)", num_heads,
@@ -694,7 +711,7 @@ pa_status_t pa_paged_attention_decode_tp(pa_tp_comm_t* comm, int* buffer_out, co
     pa_status_t st = attention_impl(nullptr, query, key, value, key_cache, value_cache, block_tables, context_lens,
                                     scale, block_size, num_kv_heads, num_seqs, num_heads, head_dim,
                                     max_blocks_per_seq, max_context_len, dtype, 0, workspace, workspace_bytes,
-                                    stream, 1, &tp);
+                                    stream, 1, &tp, host_seq_order);
     if (st != PA_OK) return st;
     cudaError_t e = pa::launch_tp_signal_wait(comm->flags, comm->world, comm->rank, epoch, comm->status,
                                               comm->timeout_ns, (cudaStream_t)stream);
@@ -1021,7 +1038,7 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
                                          reinterpret_cast<const int32_t*>(st + L.bt),
                                          reinterpret_cast<const int32_t*>(st + L.ctx), scale, block_size,
                                          num_kv_heads, num_seqs, num_heads, head_dim, max_blocks_per_seq,
-                                         max_context_len, dtype, workspace, workspace_bytes, stream);
+                                         max_context_len, dtype, nullptr, workspace, workspace_bytes, stream);
     }
     if (zero_copy && num_seqs > 0)
         return fail(PA_ERR_INVALID_ARG, "PA_E2E_MODE=zerocopy needs pinned, device-mapped host buffers");
@@ -1047,6 +1064,11 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
     // from the caller's (sized for the whole batch).  One stream if it does not fit or
     // PA_E2E_STREAMS=1.
     auto lo = [&](int c) { return (int)((int64_t)num_seqs * wcum[c] / wsum); };
+    static thread_local std::vector<int32_t> order_store[E2EStreams::kMaxChunks];
+    auto order_buf = [&](int c, size_t n) {
+        order_store[c].resize(std::max<size_t>(n, 1));
+        return order_store[c].data();
+    };
     int n_max = 1;
     for (int c = 0; c < C; ++c) n_max = std::max(n_max, lo(c + 1) - lo(c));
     const int PT = PA_DEFAULT_PARTITION_TOKENS;
@@ -1103,11 +1125,14 @@ pa_status_t pa_decode_step(void* host_out, const void* host_query, const void* h
         void* ws = NS == 2 ? static_cast<char*>(workspace) + (c & 1) * ws_chunk : workspace;
         const size_t wsb = NS == 2 ? ws_chunk : workspace_bytes;
         E2E_CHECK(cudaStreamWaitEvent(cs, es->h2d_done[c], 0));
+        // the chunk's longest-first grid order from the host context lengths (pa_decode_plan)
+        int32_t* ord = order_buf(c, n);
+        pa_decode_plan(host_context_lens + s0, (int)n, ord);
         pa_status_t r = pa_paged_attention_decode(
             st + L.out + s0 * qrow, st + L.q + s0 * qrow, st + L.k + s0 * kvrow, st + L.v + s0 * kvrow, key_cache,
             value_cache, reinterpret_cast<const int32_t*>(st + L.bt + s0 * btrow),
             reinterpret_cast<const int32_t*>(st + L.ctx) + s0, scale, block_size, num_kv_heads, (int)n, num_heads,
-            head_dim, max_blocks_per_seq, max_context_len, dtype, ws, wsb, (pa_stream_t)cs);
+            head_dim, max_blocks_per_seq, max_context_len, dtype, ord, ws, wsb, (pa_stream_t)cs);
         if (r != PA_OK) return r;
         E2E_CHECK(cudaEventRecord(es->kern_done[c], cs));
         E2E_CHECK(cudaStreamWaitEvent(es->d2h, es->kern_done[c], 0));
@@ -1195,6 +1220,17 @@ pa_status_t pa_hbm_read_probe(const void* buf, size_t bytes, int chunk, int stag
     cudaError_t e = pa::launch_hbm_read_probe(buf, (int64_t)(bytes / chunk), chunk, stages, grid, sink,
                                               (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "pa_hbm_read_probe");
+    return PA_OK;
+}
+
+pa_status_t pa_decode_plan(const int32_t* host_context_lens, int num_seqs, int32_t* order_out) {
+    g_err.clear();
+    REQUIRE(num_seqs >= 0, "num_seqs must be >= 0");
+    if (num_seqs == 0) return PA_OK;
+    REQUIRE(host_context_lens != nullptr && order_out != nullptr, "host pointer is NULL");
+    for (int i = 0; i < num_seqs; ++i) order_out[i] = i;
+    std::stable_sort(order_out, order_out + num_seqs,
+                     [&](int32_t a, int32_t b) { return host_context_lens[a] > host_context_lens[b]; });
     return PA_OK;
 }
 

@@ -382,7 +382,8 @@ __global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnPar
 #endif
     int bt_pref = 0;  // producer lane i: block id jb0 + i, loaded while ctx is in flight
     const int hg = p.pz ? blockIdx.x : blockIdx.y;
-    const int s = p.pz ? blockIdx.y : blockIdx.z;
+    const int zs = p.pz ? blockIdx.y : blockIdx.z;
+    const int s = zs < p.n_order ? (int)p.seq_order[zs] : zs;  // longest-first plan (scheduling only)
     // this CTA walks the arithmetic partitions [c0, c0 + PPC) of the context back to
     // back; each is finished exactly as if it had its own CTA (bitwise identical)
     const int c0 = (p.pz ? blockIdx.z : blockIdx.x) * p.PPC;

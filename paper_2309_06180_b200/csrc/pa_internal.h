@@ -8,6 +8,8 @@
 
 #include <utility>
 
+#include "../../include/pa.h"
+
 namespace pa {
 
 // Multi-token causal attention over the paged cache (pa_prefill.cu, N4).  TMA tensor maps
@@ -30,6 +32,7 @@ struct PrefillParams {
 };
 
 constexpr int kMaxTpPeers = 8;
+constexpr int kMaxSeqOrder = PA_MAX_SEQ_ORDER;  // longest-first grid order carried in the kernel parameters
 
 struct AttnParams {
     void* out;                  // [S][H][D]
@@ -67,6 +70,11 @@ struct AttnParams {
     int n_out_peers;
     int out_H, out_h0;
     void* out_peers[kMaxTpPeers];
+    // grid order (scheduling only, pa_decode_plan): the CTAs of grid sequence slot z work on
+    // sequence seq_order[z] when z < n_order (longest contexts first, so the long CTAs do
+    // not start in the last wave); kernel parameters, so no extra memory round trip
+    int n_order;
+    uint16_t seq_order[kMaxSeqOrder];
 };
 
 // Sharing-aware decode on the tensor cores (N1, pa_paged_attention_decode_grouped): the

@@ -105,13 +105,36 @@ def paged_attention_workspace_size(num_seqs: int, num_heads: int, head_dim: int,
                                                            partition_tokens))
 
 
+def decode_plan(context_lens) -> "np.ndarray":
+    """pa_decode_plan: the longest-first grid order (int32 numpy [S]) of a batch, from its
+    HOST context lengths (numpy / CPU tensor / list).  Scheduling only: pass it as
+    `seq_order` to the decode entries, once per decode iteration for every layer."""
+    import numpy as np
+    cl = np.ascontiguousarray(np.asarray(context_lens.cpu() if hasattr(context_lens, "cpu") else context_lens,
+                                         dtype=np.int32))
+    order = np.empty(cl.shape[0], dtype=np.int32)
+    check(_lib.raw().pa_decode_plan(cl.ctypes.data, cl.shape[0], order.ctypes.data), "pa_decode_plan")
+    return order
+
+
+def _order(seq_order, S: int):
+    """Host int32 copy of a grid order (kept alive by the marshalled arguments) or None."""
+    if seq_order is None:
+        return None
+    vals = seq_order.cpu().tolist() if hasattr(seq_order, "cpu") else list(seq_order)
+    if len(vals) != S:
+        raise ValueError(f"seq_order has {len(vals)} entries for {S} sequences")
+    return (ctypes.c_int32 * S)(*[int(v) for v in vals])
+
+
 def paged_attention(out, query, key_cache, value_cache, block_tables, context_lens, scale: float,
                     block_size: int | None = None, num_kv_heads: int | None = None, max_context_len: int = 0,
-                    partition_tokens: int = 0, workspace: torch.Tensor | None = None, stream=None):
+                    partition_tokens: int = 0, workspace: torch.Tensor | None = None, stream=None, seq_order=None):
     """Eq.4 decode attention: out[s][h] = softmax(scale q.K^T) V over the
     block-table-addressed cache.  out/query [S][H][D]; caches [NB][H_kv][B][D];
     block_tables int32 [S][W]; context_lens int32 [S].  `workspace` (uint8, device, any
-    content; see pa.h) is allocated when omitted and the context needs splitting."""
+    content; see pa.h) is allocated when omitted and the context needs splitting.
+    `seq_order`: optional host grid order (decode_plan); scheduling only."""
     _check(query.dtype, [("block_tables", block_tables), ("context_lens", context_lens)], out=out, query=query,
            key_cache=key_cache, value_cache=value_cache)
     S, H, D = query.shape
@@ -128,15 +151,17 @@ def paged_attention(out, query, key_cache, value_cache, block_tables, context_le
     _call("pa_paged_attention_ex", (
         _dev(out, "out"), _dev(query, "query"), _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"),
         _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"), float(scale), int(block_size),
-        int(num_kv_heads), S, H, D, W, int(mcl), _code(query), int(partition_tokens), ws_ptr, ws_bytes,
-        _stream(stream)))
+        int(num_kv_heads), S, H, D, W, int(mcl), _code(query), int(partition_tokens), _order(seq_order, S), ws_ptr,
+        ws_bytes, _stream(stream)))
     return out
 
 
 def paged_attention_decode(out, query, key, value, key_cache, value_cache, block_tables, context_lens, scale: float,
-                           max_context_len: int = 0, workspace: torch.Tensor | None = None, stream=None):
+                           max_context_len: int = 0, workspace: torch.Tensor | None = None, stream=None,
+                           seq_order=None):
     """The decode step's reshape_and_cache fused into paged_attention (pa.h): token s
-    (key/value [S][H_kv][D]) is written at logical position ctx[s]-1 and attended."""
+    (key/value [S][H_kv][D]) is written at logical position ctx[s]-1 and attended.
+    `seq_order`: optional host grid order (decode_plan); scheduling only."""
     _check(query.dtype, [("block_tables", block_tables), ("context_lens", context_lens)], out=out, query=query,
            key=key, value=value, key_cache=key_cache, value_cache=value_cache)
     S, H, D = query.shape
@@ -151,7 +176,8 @@ def paged_attention_decode(out, query, key, value, key_cache, value_cache, block
     _call("pa_paged_attention_decode", (
         _dev(out, "out"), _dev(query, "query"), _dev(key, "key"), _dev(value, "value"), _dev(key_cache, "key_cache"),
         _dev(value_cache, "value_cache"), _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"),
-        float(scale), B, hk, S, H, D, W, int(mcl), _code(query), ws_ptr, ws_bytes, _stream(stream)))
+        float(scale), B, hk, S, H, D, W, int(mcl), _code(query), _order(seq_order, S), ws_ptr, ws_bytes,
+        _stream(stream)))
     return out
 
 

@@ -168,12 +168,13 @@ class FusedTP:
         return ranks
 
     def decode(self, query, key, value, key_cache, value_cache, block_tables, context_lens, scale: float,
-               max_context_len: int = 0, workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+               max_context_len: int = 0, workspace: torch.Tensor | None = None, stream=None,
+               seq_order=None) -> torch.Tensor:
         """The decode step (cache write fused) on this rank's heads; returns the gathered
         [S][H_total][D] output, a view of one of the two alternating gather buffers.  It is
         valid until this rank's NEXT decode call: read it (on the same stream) before
         issuing that call (include/pa.h)."""
-        from .ops import _code, _dev, _stream, paged_attention_workspace_size
+        from .ops import _code, _dev, _order, _stream, paged_attention_workspace_size
         S, H, D = query.shape
         if S > self.S or H * self.world != self.H or D != self.D or query.dtype != self.dtype:
             raise ValueError(f"FusedTP built for <= {self.S} sequences x {self.H} heads ({self.H // self.world} per "
@@ -190,8 +191,8 @@ class FusedTP:
         self._lib.check(self._lib.raw().pa_paged_attention_decode_tp(
             self.comm, ctypes.byref(buf), _dev(query, "query"), _dev(key, "key"), _dev(value, "value"),
             _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"), _dev(block_tables, "block_tables"),
-            _dev(context_lens, "context_lens"), float(scale), B, hk, S, H, D, W, int(mcl), _code(query), ws_ptr,
-            ws_bytes, _stream(stream)), "pa_paged_attention_decode_tp")
+            _dev(context_lens, "context_lens"), float(scale), B, hk, S, H, D, W, int(mcl), _code(query),
+            _order(seq_order, S), ws_ptr, ws_bytes, _stream(stream)), "pa_paged_attention_decode_tp")
         return self.views[buf.value][:S]
 
     def close(self):

@@ -55,7 +55,8 @@ def attn(**kw):
              mcl=100, dt=0, pt=0, ws=None, wsb=0)
     a.update(kw)
     return L.pa_paged_attention_ex(a["out"], a["q"], a["kc"], a["vc"], a["bt"], a["cl"], a["scale"], a["B"], a["hkv"],
-                                   a["S"], a["H"], a["D"], a["W"], a["mcl"], a["dt"], a["pt"], a["ws"], a["wsb"], None)
+                                   a["S"], a["H"], a["D"], a["W"], a["mcl"], a["dt"], a["pt"], a.get("order"), a["ws"],
+                                   a["wsb"], None)
 
 
 @pytest.mark.parametrize("kw,status", [
@@ -253,13 +254,32 @@ def test_tp_comm_validation():
     assert not L.pa_tp_comm_create(2, 0, 8, GB, bad, arr, arr, FAKE)
     assert _lib.last_error() != ""
     r = L.pa_paged_attention_decode_tp
-    assert r(None, None, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 0.1, 16, 4, 4, 4, 128, 8, 100, 1, FAKE, 4096,
+    assert r(None, None, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 0.1, 16, 4, 4, 4, 128, 8, 100, 1, None, FAKE, 4096,
              None) == INVALID
     comm = L.pa_tp_comm_create(2, 1, 8, GB, arr, arr, arr, FAKE)
-    assert r(comm, None, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 0.1, 16, 4, 4, 8, 128, 8, 100, 1, FAKE, 4096,
+    assert r(comm, None, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 0.1, 16, 4, 4, 8, 128, 8, 100, 1, None, FAKE, 4096,
              None) == INVALID  # 8 local heads x 2 ranks != 8
-    assert r(comm, None, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 0.1, 16, 4, 5, 4, 128, 8, 100, 1, FAKE, 4096,
+    assert r(comm, None, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 0.1, 16, 4, 5, 4, 128, 8, 100, 1, None, FAKE, 4096,
              None) == INVALID  # 5 sequences do not fit gather buffers sized for 4
     assert "gather buffers" in _lib.last_error()
     L.pa_tp_comm_destroy(comm)
     assert L.pa_ipc_handle_bytes() == 64
+
+
+def test_decode_plan_longest_first_stable():
+    """pa_decode_plan: indices sorted by context length, longest first, ties in index
+    order (host only)."""
+    import numpy as np
+    import paper_2309_06180_b200 as pa
+    ctx = np.array([5, 300, 17, 300, 0, 2048, 17], np.int32)
+    assert pa.decode_plan(ctx).tolist() == [5, 1, 3, 2, 6, 0, 4]
+    assert pa.decode_plan(np.zeros(0, np.int32)).tolist() == []
+
+
+@pytest.mark.parametrize("order", [[0, 1, 2, 2], [0, 1, 2, 4], [3, 2, 1, -1]])
+def test_seq_order_must_be_a_permutation(order):
+    """A grid order that repeats or misses a sequence is rejected on the host, before any
+    launch (it would compute one output twice and leave another unwritten)."""
+    arr = (ctypes.c_int32 * 4)(*order)
+    assert attn(order=arr, ws=FAKE, wsb=1 << 20) == INVALID
+    assert "permutation" in _lib.last_error()

@@ -592,3 +592,38 @@ def test_shared_decode_small_vs_oracle(B, slots, tuning_env):
     ref, rkc, rvc = oracle_step(wl)
     assert np.array_equal(bits(x["key_cache"]), rkc) and np.array_equal(bits(x["value_cache"]), rvc)
     assert max_abs(out, ref) <= TOL[wl.dtype]
+
+
+@pytest.mark.parametrize("name", ["c2_sharegpt_full", "c2_alpaca_full", "c4_long", "c3_fork"])
+def test_grid_order_is_scheduling_only_bitwise(name):
+    """A longest-first grid order (pa_decode_plan) or any other permutation changes which
+    CTAs run first, never a result bit: fused decode and unfused attention outputs and the
+    caches equal the natural-order run's."""
+    wl = make_config(name[:-5]) if name.endswith("_full") else make_config(name, S=40, H=8, H_kv=8)
+    x = materialize_torch(wl, "cuda")
+    tb = tables_torch(wl, "cuda")
+    plan = pa.decode_plan(wl.context_lens)
+    assert np.all(np.diff(wl.context_lens[plan]) <= 0)
+    rnd = np.random.default_rng(3).permutation(wl.S).astype(np.int32)
+    outs, caches = [], []
+    for order in (None, plan, rnd):
+        y = {k: v.clone() for k, v in x.items()}
+        if len(wl.block_mapping):
+            pa.copy_blocks([y["key_cache"]], [y["value_cache"]], tb["block_mapping"])
+        out = torch.empty_like(y["query"])
+        pa.paged_attention_decode(out, y["query"], y["key"], y["value"], y["key_cache"], y["value_cache"],
+                                  tb["block_tables"], tb["context_lens"], wl.scale, max_context_len=wl.max_context_len,
+                                  seq_order=order)
+        out2 = torch.empty_like(out)
+        pa.paged_attention(out2, y["query"], y["key_cache"], y["value_cache"], tb["block_tables"], tb["context_lens"],
+                           wl.scale, max_context_len=wl.max_context_len, seq_order=order)
+        torch.cuda.synchronize()
+        assert torch.equal(out, out2)
+        outs.append(out)
+        caches.append((y["key_cache"], y["value_cache"]))
+    for o, (k, v) in zip(outs[1:], caches[1:]):
+        assert torch.equal(o, outs[0])
+        assert np.array_equal(bits(k), bits(caches[0][0])) and np.array_equal(bits(v), bits(caches[0][1]))
+    if not name.endswith("_full"):
+        ref, *_ = oracle_step(wl)
+        assert max_abs(outs[1], ref) <= TOL[wl.dtype]
