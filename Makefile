@@ -1,11 +1,12 @@
 # Build libpagedattn.so (sm_100a kernels + C ABI + host allocator) and the oracle.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+NVXFLAGS ?=
+NVFLAGS := $(ARCH) $(NVXFLAGS) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 PKG := paper_2309_06180_b200
 SRC := $(PKG)/csrc
-OBJS := $(SRC)/pa_attention.o $(SRC)/pa_prefill.o $(SRC)/pa_tp.o $(SRC)/pa_cache.o $(SRC)/pa_probe.o $(SRC)/pa_api.o $(SRC)/pa_alloc.o
-HDRS := $(SRC)/pa_common.cuh $(SRC)/pa_internal.h include/pa.h
+OBJS := $(SRC)/pa_attention.o $(SRC)/pa_prefill.o $(SRC)/pa_decode_tc.o $(SRC)/pa_tp.o $(SRC)/pa_cache.o $(SRC)/pa_probe.o $(SRC)/pa_api.o $(SRC)/pa_alloc.o
+HDRS := $(SRC)/pa_common.cuh $(SRC)/pa_tc.cuh $(SRC)/pa_internal.h include/pa.h
 
 all: $(PKG)/libpagedattn.so oracle/liboracle.so
 

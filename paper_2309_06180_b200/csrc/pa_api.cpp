@@ -76,7 +76,6 @@ struct Tuning {
     int ppc = 1;                           // PA_PPC: coop partitions per CTA (scheduling only)
     int pz = 0;                            // PA_PZ: coop grid with the partition index slowest
     int shared_hpc = 0, shared_slots = 1;  // PA_SHARED_HPC / PA_SHARED_SLOTS (N1 CUDA-core kernel)
-    int group_slots = 1, group_stg = 2, group_hg = 2;  // PA_GROUP_SLOTS / _STG / _HG (N1 mma kernel)
     bool pdl = true;                       // PA_PDL=0 disables programmatic dependent launch
     int prefill = 0;                       // PA_PREFILL=2|3 forces a prompt kernel (0 = auto)
     bool e2e_zero_copy = false;            // PA_E2E_MODE=zerocopy
@@ -103,9 +102,6 @@ Tuning load_tuning() {
     t.pz = env_int("PA_PZ", 0) > 0 ? 1 : 0;
     t.shared_hpc = env_int("PA_SHARED_HPC", 0);
     t.shared_slots = env_int("PA_SHARED_SLOTS", 1);
-    t.group_slots = env_int("PA_GROUP_SLOTS", 1);
-    t.group_stg = env_int("PA_GROUP_STG", 2);
-    if (const char* v = getenv("PA_GROUP_HG")) t.group_hg = atoi(v) == 1 ? 1 : 2;
     if (const char* v = getenv("PA_PDL")) t.pdl = v[0] != '0';
     t.prefill = env_int("PA_PREFILL", 0);
     if (const char* v = getenv("PA_E2E_MODE")) t.e2e_zero_copy = std::strcmp(v, "zerocopy") == 0;
@@ -123,9 +119,9 @@ Tuning load_tuning() {
     if (const char* v = getenv("PA_E2E_GRAPH")) t.e2e_graph = std::strcmp(v, "1") == 0;
     t.tp_timeout_ms = env_int("PA_TP_TIMEOUT_MS", 10000);
     char buf[256];
-    std::snprintf(buf, sizeof(buf), "%d %d %d %d %d %d %d %d %d %d %d %d %d %d %d %d", t.pt, t.hpc, t.stg, t.ppc,
-                  t.pz, t.shared_hpc, t.shared_slots, t.group_slots, t.group_stg, t.group_hg, (int)t.pdl, t.prefill,
-                  (int)t.e2e_zero_copy, t.e2e_chunks, t.e2e_streams, t.e2e_nsplit);
+    std::snprintf(buf, sizeof(buf), "%d %d %d %d %d %d %d %d %d %d %d %d %d", t.pt, t.hpc, t.stg, t.ppc, t.pz,
+                  t.shared_hpc, t.shared_slots, (int)t.pdl, t.prefill, (int)t.e2e_zero_copy, t.e2e_chunks,
+                  t.e2e_streams, t.e2e_nsplit);
     t.key = buf;
     for (int i = 0; i < t.e2e_nsplit; ++i) t.key += "," + std::to_string(t.e2e_split[i]);
     return t;
@@ -461,7 +457,7 @@ bool encode_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* ba
                 const cuuint64_t* strides_bytes, const cuuint32_t* box) {
     auto enc = tensor_map_encoder();
     if (!enc) return false;
-    const cuuint32_t estr[3] = {1, 1, 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     return enc(m, dt, (cuuint32_t)rank, const_cast<void*>(base), dims, strides_bytes, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -500,70 +496,58 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
     REQUIRE_PTR(value_cache, 16);
     REQUIRE_PTR(block_tables, 4);
     REQUIRE_PTR(context_lens, 4);
-    const int PT = PA_DEFAULT_PARTITION_TOKENS;
-    const int64_t cap = (int64_t)max_blocks_per_seq * block_size;
-    int64_t mcl = max_context_len > 0 ? max_context_len : cap;
-    if (mcl > cap) mcl = cap;
-    const int NP = std::max<int>(1, (int)((mcl + PT - 1) / PT));
-    const size_t need = workspace_bytes_for(num_seqs, num_heads, head_dim, (int)mcl, PT);
-    if (workspace == nullptr || workspace_bytes < need)
-        return fail(PA_ERR_WORKSPACE, "workspace of %zu bytes required (got %zu)", need,
-                    workspace ? workspace_bytes : (size_t)0);
+    (void)max_context_len;  // the kernel walks each group's contexts whole (no grid sized by it)
+    if (workspace == nullptr || workspace_bytes < 16)
+        return fail(PA_ERR_WORKSPACE, "workspace of 16 bytes required (got %zu)", workspace ? workspace_bytes : (size_t)0);
     REQUIRE_PTR(workspace, 16);
-    pa::GroupParams gp{};
+    static thread_local pa::GroupTcParams gp;  // ~1.8 KB of tensor maps, kept off the stack
+    std::memset(&gp, 0, sizeof(gp));
     const CUtensorMapDataType dt = dtype == PA_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     {
-        const cuuint64_t dims[2] = {(cuuint64_t)head_dim, (cuuint64_t)num_blocks * num_kv_heads * block_size};
         const cuuint64_t str[1] = {(cuuint64_t)head_dim * 2};
-        const cuuint32_t box[2] = {64, 16};
-        if (!encode_map(&gp.tmap_k, dt, 2, key_cache, dims, str, box) ||
-            !encode_map(&gp.tmap_v, dt, 2, value_cache, dims, str, box))
-            return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the cache maps");
+        const cuuint64_t cdims[2] = {(cuuint64_t)head_dim, (cuuint64_t)num_blocks * num_kv_heads * block_size};
+        for (int i = 0; i < 5; ++i) {
+            const cuuint32_t box[2] = {64, (cuuint32_t)(16 >> i)};
+            if (!encode_map(&gp.tmap_k[i], dt, 2, key_cache, cdims, str, box) ||
+                !encode_map(&gp.tmap_v[i], dt, 2, value_cache, cdims, str, box))
+                return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the cache maps");
+        }
+        {
+            const cuuint32_t box[2] = {64, 32};  // a piece of two adjacent kv heads (B >= 16 rows each)
+            if (!encode_map(&gp.tmap_kp, dt, 2, key_cache, cdims, str, box) ||
+                !encode_map(&gp.tmap_vp, dt, 2, value_cache, cdims, str, box))
+                return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the piece-pair maps");
+        }
+        const cuuint32_t box1[2] = {64, 1};
+        const cuuint64_t ndims[2] = {(cuuint64_t)head_dim, (cuuint64_t)num_seqs * num_kv_heads};
+        if (!encode_map(&gp.tmap_nk, dt, 2, key, ndims, str, box1) ||
+            !encode_map(&gp.tmap_nv, dt, 2, value, ndims, str, box1))
+            return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the query / new-token maps");
     }
-    pa::AttnParams& p = gp.a;
-    p.out = out;
-    p.query = query;
-    p.key_cache = key_cache;
-    p.value_cache = value_cache;
-    p.key_cache_w = key_cache;
-    p.value_cache_w = value_cache;
-    p.new_key = key;
-    p.new_value = value;
-    p.block_tables = block_tables;
-    p.context_lens = context_lens;
-    {
-        const WsLayout L = ws_layout(num_seqs, num_heads, head_dim, NP);
-        char* w = static_cast<char*>(workspace);
-        p.counters = reinterpret_cast<unsigned long long*>(w + L.counters);
-        p.part_o = reinterpret_cast<float*>(w + L.part_o);
-        p.part_ml = reinterpret_cast<float2*>(w + L.part_ml);
-    }
-    p.scale_log2 = (float)((double)scale * 1.4426950408889634);
-    p.log2B = log2B;
-    p.H = num_heads;
-    p.H_kv = num_kv_heads;
-    p.G = num_heads / num_kv_heads;
-    p.W = max_blocks_per_seq;
-    p.PT = PT;
-    p.NP = NP;
-    p.GM = group_size;
-    p.S = num_seqs;
-    p.epoch = pa::next_epoch();
-    // block slots per stage (a tile whose group reads more distinct blocks takes several
-    // stages) and stages: PA_GROUP_SLOTS / PA_GROUP_STG override
-    // (one block slot per stage: c5 514 vs 541 us with 2)
-    const int gsl = std::max(1, std::min(group_size, tuning().group_slots));
-    const int stg = tuning().group_stg;
-    p.STG = stg;
-    p.GSL = gsl;
-    // heads per CTA (one consumer-warp pair each; 2 when the head count allows): PA_GROUP_HG
-    int hg = tuning().group_hg;  // 2: c5 515 vs 523 us with one head per CTA
-    if (num_heads % hg != 0) hg = 1;
-    p.HPC = hg;
-    const size_t smem = pa::group_mma_smem_bytes(group_size, gsl, stg, PT, hg);
-    if (smem > 227 * 1024) return fail(PA_ERR_UNSUPPORTED, "group_size %d needs %zu B of shared memory", group_size, smem);
-    cudaError_t e = pa::launch_group_mma(gp, (int)dtype, num_seqs, smem, (cudaStream_t)stream);
-    if (e != cudaSuccess) return cuda_fail(e, "paged_attention_group_mma_kernel launch");
+    gp.out = out;
+    gp.query = query;
+    gp.key_cache = key_cache;
+    gp.value_cache = value_cache;
+    gp.new_key = key;
+    gp.new_value = value;
+    gp.block_tables = block_tables;
+    gp.context_lens = context_lens;
+    gp.work_counter = static_cast<unsigned long long*>(workspace);
+    gp.epoch = pa::next_epoch();
+    gp.scale_log2 = (float)((double)scale * 1.4426950408889634);
+    gp.log2B = log2B;
+    gp.H = num_heads;
+    gp.H_kv = num_kv_heads;
+    gp.G = num_heads / num_kv_heads;
+    gp.W = max_blocks_per_seq;
+    gp.S = num_seqs;
+    gp.GM = group_size;
+    gp.n_hp = (num_heads + 1) / 2;
+    const int64_t items = (int64_t)((num_seqs + group_size - 1) / group_size) * gp.n_hp;
+    REQUIRE(items < (1LL << 31), "too many work items");
+    gp.n_items = (int)items;
+    cudaError_t e = pa::launch_group_tc(gp, (int)dtype, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "paged_attention_group_tc_kernel launch");
     return PA_OK;
 }
 

@@ -782,411 +782,6 @@ __global__ void __launch_bounds__(288, PA_SHARED_MINB) paged_attention_shared_ke
     }
 }
 
-// ============================ sharing-aware decode on the tensor cores (N1, mma.sync) ===
-//
-// The sequences of one group (a request's parallel samples or beams) share
-// most physical blocks.  One CTA = (partition, HG = 1 or 2 query heads, group of M <= 8
-// sequences); per head a pair of consumer warps (each owning half of the head dimension
-// for P V), then one producer warp.  The producer maps each 16-token logical tile of
-// the M members to their physical blocks and TMA-loads every DISTINCT block once (K and
-// V, two 64-column boxes each, 128-byte swizzle) into a slot of the stage.  The consumer
-// computes S = Q K^T for all members at once as an m16n8k16 tensor-core product (rows =
-// members, the group's queries held as A fragments), masks each row to the tokens of its
-// own slot and context, runs the online softmax per row on the accumulator fragments and
-// adds P V with a second product (V fragments through ldmatrix.trans).  A shared block
-// thus costs one K/V read from HBM/L2 and ~35 MMA instructions for the whole group,
-// instead of M separate FMA passes.  Accumulation order differs from the CUDA-core
-// kernels (results agree within the tolerance, not bitwise).
-template <bool BF>
-__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
-#ifdef PA_GROUP_NOMMA  // timing experiment: the MMAs replaced by one dependent FADD
-    d[0] += __uint_as_float(a0 ^ b0) * 1e-30f;
-    return;
-#endif
-    if (BF)
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-            "{%0,%1,%2,%3};"
-            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-            : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
-    else
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-            "{%0,%1,%2,%3};"
-            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-            : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-__device__ __forceinline__ void tma_box(void* smem_dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(smem_dst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-        : "memory");
-}
-template <typename T>
-__device__ __forceinline__ uint32_t pack_pair(float a, float b) {
-    if constexpr (std::is_same<T, __half>::value) {
-        const __half2 v = __floats2half2_rn(a, b);
-        return *reinterpret_cast<const uint32_t*>(&v);
-    } else {
-        const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-        return *reinterpret_cast<const uint32_t*>(&v);
-    }
-}
-// byte offset of 16-byte chunk `ch` (0..15 over D = 128) of row `r` in a slot half
-// (K or V): two swizzled boxes of 16 rows x 128 bytes
-__device__ __forceinline__ uint32_t swz(int r, int ch) {
-    return (uint32_t)((ch >> 3) * 2048 + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
-}
-
-constexpr int kGroupSlot = 8192;  // K | V of one block x one kv head x 16 tokens (D = 128, 2-byte)
-
-// per stage: gm slots | barriers | tile metadata (slot per member, slot count, new-token
-// member mask, rows needed per slot)
-size_t group_mma_smem_bytes(int gm, int gsl, int stg, int pt, int hg) {
-    return 1024 + (size_t)stg * gsl * hg * kGroupSlot + 16 * (size_t)stg + 4 * (size_t)stg * (gm + 3 + gsl) +
-           4 * (size_t)gm * (pt / kTile) + 16;
-}
-
-#ifdef PA_GROUP_DEBUG  // bounded waits that report where they stuck (debug variant)
-__device__ __forceinline__ void gwait(uint64_t* bar, uint32_t parity, int tag, int j) {
-    for (long long it = 0;; ++it) {
-        uint32_t ok;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (ok) return;
-        if (it == (tag == 2 ? (1LL << 18) : (1LL << 24))) {
-            printf("group_mma stuck: block (%d,%d,%d) thread %d tag %d tile %d parity %u\n", blockIdx.x, blockIdx.y,
-                   blockIdx.z, threadIdx.x, tag, j, parity);
-            __trap();
-        }
-    }
-}
-#define GWAIT(bar, par, tag, j) gwait(bar, par, tag, j)
-#else
-#define GWAIT(bar, par, tag, j) mbar_wait(bar, par)
-#endif
-
-#ifndef PA_GROUP_MINB_HG
-#define PA_GROUP_MINB_HG 4  // two heads per CTA (160 threads)
-#endif
-#ifndef PA_GROUP_MINB
-#define PA_GROUP_MINB 6  // register cap (113) for 6 CTAs/SM: c5 644 -> 514 us (uncapped 138 regs, 4 CTAs/SM)
-#endif
-template <typename T, int HG>
-__global__ void __launch_bounds__(32 * (2 * HG + 1), HG == 1 ? PA_GROUP_MINB : PA_GROUP_MINB_HG) paged_attention_group_mma_kernel(const __grid_constant__ GroupParams gp) {
-    constexpr int D = 128, RB = 256;
-    constexpr bool BF = std::is_same<T, __nv_bfloat16>::value;
-    constexpr unsigned FULL = 0xffffffffu;
-    const AttnParams& p = gp.a;
-    extern __shared__ __align__(1024) unsigned char gsmem_raw[];
-    unsigned char* smem =
-        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsmem_raw) + 1023) & ~(uintptr_t)1023);
-    const int part = blockIdx.x, grp = blockIdx.z;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int M = p.GM, STG = p.STG, PT = p.PT, GSL = p.GSL;
-    const int stage_bytes = GSL * HG * kGroupSlot;
-    const int s0 = grp * M, nm = min(M, p.S - s0);
-    const int hid = warp < 2 * HG ? warp >> 1 : 0;  // consumer pair -> head of the CTA
-    const int h = blockIdx.y * HG + hid, kvh = h / p.G;
-    // metadata per stage: [0, M) slot of member m in this stage (-1: none), [M] slots,
-    // [M+1] new-token members, [M+2] tile start (-1: end of the partition), [M+3, +GSL) rows
-    // each slot's members read
-    const int MW = M + 3 + GSL;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STG * stage_bytes);
-    uint64_t* empty = full + STG;
-    int* meta = reinterpret_cast<int*>(empty + STG);  // [STG][MW]
-    int* sbt = meta + STG * MW;                        // [M][PT / 16] block id of member m's tile j
-    if (threadIdx.x < STG) {
-        mbar_init(&full[threadIdx.x], 1);
-        mbar_init(&empty[threadIdx.x], 2 * HG);  // both consumer warps of every head release a stage
-    }
-    fence_mbar_init();
-    __syncthreads();
-    pdl_wait();
-    // lane m < nm: member m's context, partition end and new-token position
-    const int my_ctx = lane < nm ? __ldg(p.context_lens + s0 + lane) : 0;
-    int gmax = my_ctx;
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) gmax = max(gmax, __shfl_xor_sync(FULL, gmax, off));
-    const int p0 = part * PT;
-    if (part > 0 && p0 >= gmax) return;  // no member reaches this partition (CTA-uniform)
-    const int ntiles = (min(gmax, p0 + PT) - p0 + kTile - 1) / kTile;
-    const int my_p1 = min(my_ctx, p0 + PT);
-    const int my_tnew = (p.new_key != nullptr && lane < nm && my_ctx > 0 && my_p1 == my_ctx) ? my_ctx - 1 : -1;
-    const int B = 1 << p.log2B;
-
-    if (warp == 2 * HG) {  // ================================================ producer warp
-        // every member's block ids of the partition, loaded in parallel up front
-        const int TPP = PT / kTile;
-        for (int i = lane; i < nm * TPP; i += 32) {
-            const int m = i / TPP, jj = i - m * TPP;
-            const int tok = p0 + jj * kTile;
-            sbt[i] = jj < ntiles ? __ldg(p.block_tables + (int64_t)(s0 + m) * p.W + (tok >> p.log2B)) : -1;
-        }
-        __syncwarp();
-        int u = 0;  // stages posted
-        for (int j = 0; j < ntiles; ++j) {
-            const int tok0 = p0 + j * kTile;
-            const bool act = lane < nm && tok0 < my_p1;
-            const bool has_new = act && my_tnew >= tok0 && my_tnew < tok0 + kTile;
-            const int blk = act ? sbt[lane * TPP + j] : -1;
-            const int rows = act ? min(kTile, my_p1 - tok0) : 0;
-            const bool shareable = act && !has_new;  // a new-token tile is private (CoW)
-            // leader = lowest member reading the same block (unshareable members lead themselves)
-#ifdef PA_GROUP_MATCH
-            const unsigned same = __match_any_sync(FULL, shareable ? blk : -2 - lane);
-            const int leader = __ffs(same) - 1;
-#else  // shuffle loop: measured faster than match.any in the CUDA-core shared kernel (§7)
-            int leader = lane;
-            for (int m = 0; m < nm; ++m) {
-                const int bm = __shfl_sync(FULL, blk, m);
-                const bool sm = __shfl_sync(FULL, shareable, m);
-                if (shareable && sm && bm == blk && m < leader) leader = m;
-            }
-#endif
-            const bool is_leader = act && leader == lane;
-            const unsigned leaders = __ballot_sync(FULL, is_leader);
-            const int my_slot = __popc(leaders & ((1u << lane) - 1u));
-            const int slot = __shfl_sync(FULL, my_slot, leader);
-            // rows a slot must hold: the largest need among its members
-            int need = 0;
-            for (int m = 0; m < nm; ++m) {
-                const int sl_m = __shfl_sync(FULL, act ? slot : -1, m);
-                const int r_m = __shfl_sync(FULL, rows, m);
-                if (is_leader && sl_m == my_slot) need = max(need, r_m);
-            }
-            const int d = __popc(leaders);
-            for (int pass0 = 0; pass0 < d; pass0 += GSL, ++u) {  // GSL distinct blocks per stage
-                const int k = u % STG;
-                if (u >= STG) GWAIT(&empty[k], ((u / STG) - 1) & 1, 1, u);
-                const bool in = act && slot >= pass0 && slot < pass0 + GSL;
-                const unsigned newmask = __ballot_sync(FULL, has_new && in);
-                int* mt = meta + k * MW;
-                if (lane < M) mt[lane] = in ? slot - pass0 : -1;
-                if (is_leader && in) mt[M + 3 + my_slot - pass0] = need;
-                if (lane == 0) {
-                    mt[M] = min(GSL, d - pass0);
-                    mt[M + 1] = (int)newmask;
-                    mt[M + 2] = tok0;
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive_expect_tx(&full[k], (uint32_t)(min(GSL, d - pass0) * HG * kGroupSlot));
-                __syncwarp();
-                if (is_leader && in) {
-                    unsigned char* sl = smem + (size_t)k * stage_bytes + (size_t)(my_slot - pass0) * HG * kGroupSlot;
-#pragma unroll
-                    for (int hi = 0; hi < HG; ++hi) {  // the CTA's heads: one K|V box set each
-                        const int row = ((blk * p.H_kv + (blockIdx.y * HG + hi) / p.G) << p.log2B) + (tok0 & (B - 1));
-                        unsigned char* slh = sl + hi * kGroupSlot;
-                        tma_box(slh, &gp.tmap_k, 0, row, &full[k]);
-                        tma_box(slh + 2048, &gp.tmap_k, 64, row, &full[k]);
-                        tma_box(slh + 4096, &gp.tmap_v, 0, row, &full[k]);
-                        tma_box(slh + 6144, &gp.tmap_v, 64, row, &full[k]);
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        // end marker for the consumers
-        const int k = u % STG;
-        if (u >= STG) GWAIT(&empty[k], ((u / STG) - 1) & 1, 1, u);
-        if (lane == 0) {
-            meta[k * MW + M + 2] = -1;
-            mbar_arrive_expect_tx(&full[k], 0u);
-        }
-        return;
-    }
-
-    // ====================================== consumer warps 2*hid, 2*hid + 1 (head h0 + hid)
-    // Both compute S for all members; warp w accumulates P V for dims [64w, 64w + 64) only.
-    // Fragment coordinates: row g (= member g; rows g + 8 are unused), column pair 2t, 2t+1.
-    const int w = warp & 1;
-    const int g = lane >> 2, t = lane & 3;
-    const bool row_ok = g < nm;
-    const int s_g = s0 + min(g, nm - 1);
-    const int ctx_g = __shfl_sync(FULL, my_ctx, g);
-    const int p1_g = min(ctx_g, p0 + PT);
-    uint32_t qa[8][2];  // A fragments of the members' queries: dims kk*16 + 2t (+8)
-    {
-        const uint32_t* qrow =
-            reinterpret_cast<const uint32_t*>(static_cast<const char*>(p.query) + ((int64_t)s_g * p.H + h) * RB);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            qa[kk][0] = row_ok ? __ldg(qrow + kk * 8 + t) : 0u;
-            qa[kk][1] = row_ok ? __ldg(qrow + kk * 8 + 4 + t) : 0u;
-        }
-    }
-    float o[8][4];  // dims 64w + nd*8 + 2t (+1)
-#pragma unroll
-    for (int nd = 0; nd < 8; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
-    float m_g = -INFINITY, l_g = 0.f;  // l_g: this lane's partial row sum (quad-reduced at the end)
-    for (int u = 0;; ++u) {
-        const int k = u % STG;
-        GWAIT(&full[k], (u / STG) & 1, 2, u);
-        const int* mt = meta + k * MW;
-        const int tok0 = mt[M + 2];
-        if (tok0 < 0) break;  // end of the partition
-        unsigned char* st = smem + (size_t)k * stage_bytes;
-        const int nslots = mt[M];
-        const unsigned newmask = (unsigned)mt[M + 1];
-        if (newmask) {  // new-token rows from the step's inputs: warp w writes dims half w of K and V
-            for (unsigned mm = newmask; mm; mm &= mm - 1) {
-                const int m = __ffs(mm) - 1;
-                const int tn = __shfl_sync(FULL, my_tnew, m);
-                const int sl = mt[m], r = tn - tok0;
-                const int ch = w * 8 + (lane & 7);  // 16-byte chunk of the row (dims 8ch..8ch+7)
-                const bool isv = lane >= 8;
-                if (lane < 16) {
-                    const uint4 val = __ldg(reinterpret_cast<const uint4*>(
-                                                static_cast<const char*>(isv ? p.new_value : p.new_key) +
-                                                ((int64_t)(s0 + m) * p.H_kv + kvh) * RB) +
-                                            ch);
-                    *reinterpret_cast<uint4*>(st + ((size_t)sl * HG + hid) * kGroupSlot + (isv ? 4096 : 0) + swz(r, ch)) = val;
-                    if (h % p.G == 0) {  // the cache slot, once per kv head
-                        const int blk = __ldg(p.block_tables + (int64_t)(s0 + m) * p.W + (tn >> p.log2B));
-                        const int64_t off = ((((int64_t)blk * p.H_kv + kvh) << p.log2B) + (tn & (B - 1))) * RB;
-                        reinterpret_cast<uint4*>(static_cast<char*>(isv ? p.value_cache_w : p.key_cache_w) + off)[ch] =
-                            val;
-                    }
-                }
-            }
-            asm volatile("bar.sync %0, 64;" ::"r"(1 + hid) : "memory");  // both K halves in place before S
-        }
-        // V rows of this warp's half that no member of a slot reads: finite (zero) for P V
-        for (int sl = 0; sl < nslots; ++sl) {
-            const int need = mt[M + 3 + sl];
-            for (int r = need + (lane >> 3); r < kTile; r += 4)
-                *reinterpret_cast<uint4*>(st + ((size_t)sl * HG + hid) * kGroupSlot + 4096 + swz(r, w * 8 + (lane & 7))) =
-                    make_uint4(0u, 0u, 0u, 0u);
-        }
-        __syncwarp();
-        const int slot_g = mt[min(g, M - 1)];
-        const int my_slot = row_ok ? slot_g : -1;
-        for (int sl = 0; sl < nslots; ++sl) {
-            const uint32_t kbase = smem_u32(st + ((size_t)sl * HG + hid) * kGroupSlot), vbase = kbase + 4096;
-            float sa[2][4], sb[2][4];  // two accumulation chains per n-tile (even / odd k pairs)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                sa[nt][0] = sa[nt][1] = sa[nt][2] = sa[nt][3] = 0.f;
-                sb[nt][0] = sb[nt][1] = sb[nt][2] = sb[nt][3] = 0.f;
-            }
-#pragma unroll
-            for (int kp = 0; kp < 4; ++kp) {
-#pragma unroll
-                for (int nt = 0; nt < 2; ++nt) {
-                    const int q = lane >> 3, tr = nt * 8 + (lane & 7), ch = (2 * kp + (q >> 1)) * 2 + (q & 1);
-                    uint32_t b0, b1, b2, b3;
-                    ldsm_x4(kbase + swz(tr, ch), b0, b1, b2, b3);
-                    mma16816<BF>(sa[nt], qa[2 * kp][0], qa[2 * kp][1], b0, b1);
-                    mma16816<BF>(sb[nt], qa[2 * kp + 1][0], qa[2 * kp + 1][1], b2, b3);
-                }
-            }
-            // row g's scores of tokens tok0 + {2t, 2t+1, 8+2t, 8+2t+1}, masked to its slot and context
-            const bool mine = my_slot == sl;
-            float x[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int tk = tok0 + (i >> 1) * 8 + 2 * t + (i & 1);
-                x[i] = (mine && tk < p1_g) ? (sa[i >> 1][i & 1] + sb[i >> 1][i & 1]) * p.scale_log2 : -INFINITY;
-            }
-            float tmax = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-            tmax = fmaxf(tmax, __shfl_xor_sync(FULL, tmax, 1));
-            tmax = fmaxf(tmax, __shfl_xor_sync(FULL, tmax, 2));
-            const float mn = fmaxf(m_g, tmax);
-            const float ms = (mn == -INFINITY) ? 0.f : mn;
-            const float alpha = ex2(m_g - ms);
-            float pr[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) pr[i] = ex2(x[i] - ms);
-            l_g = l_g * alpha + ((pr[0] + pr[1]) + (pr[2] + pr[3]));
-            if (__any_sync(FULL, alpha != 1.f)) {
-#pragma unroll
-                for (int nd = 0; nd < 8; ++nd) {
-                    o[nd][0] *= alpha;
-                    o[nd][1] *= alpha;
-                }
-            }
-            m_g = mn;
-            const uint32_t pa0 = pack_pair<T>(pr[0], pr[1]), pa2 = pack_pair<T>(pr[2], pr[3]);
-#pragma unroll
-            for (int np = 0; np < 4; ++np) {
-                const int q = lane >> 3, tr = (q & 1) * 8 + (lane & 7), ch = w * 8 + 2 * np + (q >> 1);
-                uint32_t b0, b1, b2, b3;
-                ldsm_x4_t(vbase + swz(tr, ch), b0, b1, b2, b3);
-                mma16816<BF>(o[2 * np], pa0, pa2, b0, b1);
-                mma16816<BF>(o[2 * np + 1], pa0, pa2, b2, b3);
-            }
-        }
-        // generic-proxy writes of this stage (new rows, zeroed rows) before the TMA reuses it
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[k]);
-    }
-    l_g += __shfl_xor_sync(FULL, l_g, 1);
-    l_g += __shfl_xor_sync(FULL, l_g, 2);
-    // row g's result: members with tokens in this partition (every member at partition 0)
-    const bool has = row_ok && (part == 0 || p0 < ctx_g);
-    const int nparts_g = ctx_g > 0 ? (ctx_g + PT - 1) / PT : 1;
-    const int64_t sh = (int64_t)s_g * p.H + h;
-    const float inv = l_g > 0.f ? 1.f / l_g : 0.f;
-    if (has && nparts_g == 1) {
-        T* orow = static_cast<T*>(p.out) + sh * D + w * 64;
-#pragma unroll
-        for (int nd = 0; nd < 8; ++nd)
-            *reinterpret_cast<uint32_t*>(orow + nd * 8 + 2 * t) = pack_pair<T>(o[nd][0] * inv, o[nd][1] * inv);
-    } else if (has) {
-        float* po = p.part_o + (sh * p.NP + part) * D + w * 64;
-#pragma unroll
-        for (int nd = 0; nd < 8; ++nd)
-            *reinterpret_cast<float2*>(po + nd * 8 + 2 * t) = make_float2(o[nd][0] * inv, o[nd][1] * inv);
-        if (t == 0 && w == 0) p.part_ml[sh * p.NP + part] = make_float2(m_g, l_g);
-    }
-    __threadfence();
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + hid) : "memory");  // both halves of every partial are out
-    if (w == 1) return;
-    for (int r = 0; r < nm; ++r) {  // split members: the last partition to finish merges (finish_split)
-        const int ctx_r = __shfl_sync(FULL, my_ctx, r);
-        const int np_r = ctx_r > 0 ? (ctx_r + PT - 1) / PT : 1;
-        if (np_r == 1 || p0 >= ctx_r) continue;
-        const int64_t shr = (int64_t)(s0 + r) * p.H + h;
-        int last = 0;
-        if (lane == 0) {
-            __threadfence();
-            last = split_arrive(p, shr, min(np_r, p.NP));
-        }
-        last = __shfl_sync(FULL, last, 0);
-        if (last) {
-            __threadfence();
-            merge_partitions<T, D>(p, shr, min(np_r, p.NP), lane);
-        }
-    }
-}
-
-cudaError_t launch_group_mma(const GroupParams& p, int dtype, int num_seqs, size_t smem, cudaStream_t stream) {
-    const int HG = p.a.HPC == 2 ? 2 : 1;  // heads per CTA
-    auto kern = dtype == 1 ? (HG == 2 ? paged_attention_group_mma_kernel<__half, 2> : paged_attention_group_mma_kernel<__half, 1>)
-                           : (HG == 2 ? paged_attention_group_mma_kernel<__nv_bfloat16, 2>
-                                      : paged_attention_group_mma_kernel<__nv_bfloat16, 1>);
-    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
-    if (e != cudaSuccess) return e;
-    const dim3 grid(p.a.NP, p.a.H / HG, (num_seqs + p.a.GM - 1) / p.a.GM);
-    return launch_k(kern, grid, dim3(32 * (2 * HG + 1)), smem, stream, p);
-}
-
 // ==================================================================== debug gather ===
 
 // Test-only: copy the logical K/V rows of (s, kvh) through the grid scheduler's loader.

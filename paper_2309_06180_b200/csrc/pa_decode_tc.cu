@@ -1,0 +1,669 @@
+// pa_decode_tc.cu -- sharing-aware decode attention on the tcgen05 tensor cores (SURVEY
+// §8(f) N1, pa_paged_attention_decode_grouped).
+//
+// Sequences of one sequence group (the n samples of a request, the k beams of a beam search,
+// P:295-332) share physical blocks.  Eq.4 for every member of the group and every
+// query head, with each DISTINCT 16-row block piece read from HBM once for the whole group:
+//
+//   * work item = (group of GM consecutive sequences, pair of query heads); persistent CTAs
+//     (one per SM) draw items from an epoch-tagged counter;
+//   * producer warp: looks up the members' block ids 32 logical 16-token positions at a
+//     time, keeps one "slot" per distinct piece (owner mask = the members that read it at
+//     that position) and TMA-loads its K and V rows for both heads into a tile of 4 slots
+//     (128-byte swizzle; a partial piece in 16/8/4/2/1-row boxes so nothing past the context
+//     is read; a member's new token row comes from the step's key/value input);
+//   * MMA warp: S_h = Q_h K_h^T for the tile's 4 slots at once (M = 128 rows: the members'
+//     query rows, replicated by a zero row stride in the descriptor; N = 64 tokens; K = 128)
+//     into tensor memory, then O_h += P_h V_h (P from tensor memory, one K=16 step per slot);
+//   * softmax warps (one per head, TMEM lane quadrant = head): lane m = member m reads its S
+//     row, masks columns it does not own or that lie past its context, online softmax in the
+//     exp2 domain with lazy rescaling, writes P (storage dtype) back into tensor memory;
+//     epilogue O / l to `out` and the member's new K/V row to its cache slot (the fused
+//     reshape_and_cache of the decode step).
+// So the per-(member, token) CUDA-core work of the coop/shared kernels (a 128-wide dot
+// product and axpy each) becomes two tensor-core MMAs per shared piece; a shared piece costs
+// the same MMA work whether one or eight members own it.
+#include "pa_common.cuh"
+#include "pa_internal.h"
+#include "pa_tc.cuh"
+
+#include <type_traits>
+
+namespace pa {
+using namespace tc;
+
+namespace {
+constexpr int kSlots = 4;                   // 16-row block pieces per MMA tile
+constexpr int kBuf = 3;                     // tile buffers in shared memory
+constexpr int kPiece = 16 * 128;            // [16 rows][64 cols] swizzled, 2-byte elements
+constexpr int kPair = 2 * kPiece;           // one piece, both kv heads stacked: [32 rows][128 B] = 4 KB
+constexpr int kHalfReg = kSlots * kPair;    // one 64-column half of the tile: 16 KB
+constexpr int kTensor = 2 * kHalfReg;       // K (or V) of the tile: 32 KB
+constexpr int kTileBytes = 2 * kTensor;     // 64 KB: [K|V][half][piece][head][16 rows][128 B]
+constexpr int kMaxGM = 8;
+constexpr int kListCap = 32 * kMaxGM;       // pieces of one 32-position chunk
+constexpr float kLazyTc = 8.f;              // P <= 2^8 between rescales
+constexpr int kThreadsTc = 128;             // warps: 0 softmax head 0, 1 producer, 2 softmax head 1, 3 MMA
+// tensor memory columns: Q (16-bit pairs) | S0 | S1 | O; lanes 0-31 = head 0's members,
+// lanes 64-95 = head 1's members (the softmax warps 0 and 2 own those lane quadrants)
+constexpr int kTmQ = 0, kTmS = 64, kSCols = 32 * kSlots, kTmO = kTmS + 2 * kSCols;
+constexpr int kNumBars = 2 * kBuf + 2 + 2 + 2 + 1 + 1 + 4 + 4;
+
+struct TileMeta {
+    int ns, last;
+    int p[kSlots], own[kSlots];
+};
+
+struct TcItem {
+    int s0, gmv, h[2], kvh[2];
+    bool st1, kvpair;  // second head stored; the two heads read different kv heads (else one, GQA)
+};
+
+__device__ __forceinline__ TcItem tc_item(const GroupTcParams& p, int i) {
+    TcItem it;
+    const int g = i / p.n_hp, hp = i - g * p.n_hp;
+    it.s0 = g * p.GM;
+    it.gmv = min(p.GM, p.S - it.s0);
+    it.h[0] = 2 * hp;
+    it.h[1] = min(2 * hp + 1, p.H - 1);
+    it.st1 = 2 * hp + 1 < p.H;
+    it.kvh[0] = it.h[0] / p.G;
+    it.kvh[1] = it.h[1] / p.G;
+    it.kvpair = it.kvh[1] != it.kvh[0];
+    return it;
+}
+
+// Next dynamic work item of this launch: the counter word is (epoch << 32 | items handed
+// out).  One atomic add per fetch; a word still carrying another launch's epoch is claimed
+// with a compare-and-swap that starts this launch's count (so the host never resets it).
+__device__ __forceinline__ int fetch_item(unsigned long long* ctr, uint32_t epoch) {
+    const unsigned long long E = (unsigned long long)epoch << 32;
+    for (;;) {
+        const unsigned long long old = atomicAdd(ctr, 1ull);
+        if ((old & 0xffffffff00000000ull) == E) return (int)(old & 0xffffffffull);
+        // stale word: install (E, 1) -- this call's item 0 -- unless another caller converts
+        // it first; CAS against the latest stale value, so concurrent adds cannot livelock it
+        unsigned long long cur = old + 1ull;
+        for (;;) {
+            const unsigned long long prev = atomicCAS(ctr, cur, E | 1ull);
+            if (prev == cur) return 0;
+            if ((prev & 0xffffffff00000000ull) == E) break;  // converted by another caller: add again
+            cur = prev;
+        }
+    }
+}
+}  // namespace
+
+#ifdef PA_TC_TRACE  // timing experiments (variant build): clock64 per tile of CTAs 0..7
+constexpr int kTrTiles = 1024;
+__device__ long long g_tc_trace[8 * kTrTiles * 8];
+#define TC_T(tile, ev)                                                                               \
+    do {                                                                                             \
+        if (blockIdx.x < 8 && (tile) < kTrTiles) g_tc_trace[(blockIdx.x * kTrTiles + (tile)) * 8 + (ev)] = clock64(); \
+    } while (0)
+#else
+#define TC_T(tile, ev) \
+    do {               \
+    } while (0)
+#endif
+
+template <typename T>
+__global__ void __launch_bounds__(kThreadsTc, 1)
+    paged_attention_group_tc_kernel(const __grid_constant__ GroupTcParams p) {
+    constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem =
+        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* sT = smem;                         // kBuf x [K|V][half][piece][head][16][128 B]
+    TileMeta* meta = reinterpret_cast<TileMeta*>(sT + kBuf * kTileBytes);
+    int2* list = reinterpret_cast<int2*>(meta + kBuf);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(list + kListCap);
+    uint64_t* tile_full = bars;                 // kBuf: TMA bytes + producer arrive
+    uint64_t* tile_empty = bars + kBuf;         // kBuf: MMA commit + 2 softmax warps
+    uint64_t* q_full = bars + 2 * kBuf;         // 2 (by item parity): 64 softmax lanes wrote Q
+    uint64_t* s_full = q_full + 2;              // [S buffer]
+    uint64_t* p_full = s_full + 2;              // [S buffer]: 64 softmax lanes
+    uint64_t* o_done = p_full + 2;              // 1
+    uint64_t* o_free = o_done + 1;              // 1: 64 softmax lanes
+    uint64_t* item_full = o_free + 1;           // 4: producer -> MMA + softmax
+    uint64_t* item_empty = item_full + 4;       // 4: MMA + 2 softmax warps
+    int* item_ring = reinterpret_cast<int*>(bars + kNumBars);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_ring + 4);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int i = 0; i < kBuf; ++i) {
+            mbar_init(&tile_full[i], 1);
+            mbar_init(&tile_empty[i], 3);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&q_full[i], 64);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 64);
+        }
+        mbar_init(o_done, 1);
+        mbar_init(o_free, 64);
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&item_full[i], 1);
+            mbar_init(&item_empty[i], 3);
+        }
+        fence_mbar_init();
+    }
+    // V rows past a piece's last loaded row are multiplied by P = 0, so they must not hold
+    // NaN bit patterns: zero the V halves once; later they only hold loaded, finite rows
+    for (int b = 0; b < kBuf; ++b)
+        for (int i = tid; i < kTensor / 16; i += kThreadsTc)
+            reinterpret_cast<uint4*>(sT + b * kTileBytes + kTensor)[i] = make_uint4(0u, 0u, 0u, 0u);
+    fence_proxy_async_smem();
+    if (warp == 3) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // inputs of the preceding kernel on the stream are visible from here on
+    pdl_launch_dependents();
+    const int ppb_log = p.log2B - 4;  // 16-row pieces per block (log2)
+
+    if (warp == 1) {
+        // ================================================================ producer ===
+        uint32_t tcount = 0;
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t slot = k & 3;
+            if (k >= 4) mbar_wait(&item_empty[slot], ((k - 4) >> 2) & 1);
+            int i = 0;
+            if (lane == 0) {
+                // first item by CTA index, later ones from the shared counter
+                i = k == 0 ? (int)blockIdx.x : (int)gridDim.x + fetch_item(p.work_counter, p.epoch);
+                item_ring[slot] = i;
+                mbar_arrive(&item_full[slot]);
+            }
+            i = __shfl_sync(0xffffffffu, i, 0);
+            if (i >= p.n_items) break;
+            const TcItem it = tc_item(p, i);
+            const int myctx = lane < it.gmv ? max(0, __ldg(p.context_lens + it.s0 + lane)) : 0;
+            int ctxs[kMaxGM];
+            int maxp = 0;
+#pragma unroll
+            for (int m = 0; m < kMaxGM; ++m) {
+                ctxs[m] = __shfl_sync(0xffffffffu, myctx, m);
+                if (m < it.gmv) maxp = max(maxp, (ctxs[m] + 15) >> 4);
+            }
+            const int kvstep = it.kvpair ? (1 << p.log2B) : 0;  // rows from kv head 0 to kv head 1
+            int fill = 0, b = 0;
+            unsigned char* tb = sT;
+            for (int p0 = 0; p0 < maxp; p0 += 32) {
+                // distinct pieces of 32 logical positions: lane = position
+                const int pp = p0 + lane;
+                int id[kMaxGM];
+#pragma unroll
+                for (int m = 0; m < kMaxGM; ++m) {
+                    id[m] = -1;
+                    if (m < it.gmv && pp < ((ctxs[m] + 15) >> 4)) {
+                        const int blk =
+                            __ldg(p.block_tables + (int64_t)(it.s0 + m) * p.W + ((pp << 4) >> p.log2B));
+                        id[m] = (blk << ppb_log) | (pp & ((1 << ppb_log) - 1));
+                    }
+                }
+                unsigned lead = 0;
+#pragma unroll
+                for (int m = 0; m < kMaxGM; ++m) {
+                    bool first = id[m] >= 0;
+#pragma unroll
+                    for (int m2 = 0; m2 < m; ++m2) first = first && id[m2] != id[m];
+                    if (first) lead |= 1u << m;
+                }
+                const int n = __popc(lead);
+                int incl = n;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= off) incl += v;
+                }
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                int e = incl - n;
+#pragma unroll
+                for (int m = 0; m < kMaxGM; ++m) {
+                    if ((lead >> m) & 1u) {
+                        int own = 0, nrows = 0, newm = -1;
+#pragma unroll
+                        for (int m2 = 0; m2 < kMaxGM; ++m2) {
+                            if (id[m2] == id[m]) {
+                                own |= 1 << m2;
+                                nrows = max(nrows, min(16, ctxs[m2] - 16 * pp));
+                                if (((ctxs[m2] - 1) >> 4) == pp) newm = m2;
+                            }
+                        }
+                        const int blk = id[m] >> ppb_log, pc = id[m] & ((1 << ppb_log) - 1);
+                        list[e++] = make_int2(((blk * p.H_kv + it.kvh[0]) << p.log2B) | (pc << 4),
+                                              (pp << 18) | (own << 10) | (nrows << 4) | (newm + 1));
+                    }
+                }
+                __syncwarp();
+                for (int q = 0; q < total;) {
+                    if (fill == 0) {
+                        b = (int)(tcount % kBuf);
+                        if (tcount >= (uint32_t)kBuf) mbar_wait(&tile_empty[b], ((tcount / kBuf) - 1) & 1);
+                        tb = sT + b * kTileBytes;
+                        if (lane == 0) TC_T(tcount, 0);
+                    }
+                    // the next k2 pieces of the open tile are issued together
+                    const int k2 = min(kSlots - fill, total - q);
+                    uint64_t* bar = &tile_full[b];
+                    if (lane == 0) {
+                        uint32_t bytes = 0;
+                        for (int jj = 0; jj < k2; ++jj) {
+                            const int y = list[q + jj].y;
+                            meta[b].p[fill + jj] = y >> 18;
+                            meta[b].own[fill + jj] = (y >> 10) & 0xff;
+                            bytes += (uint32_t)((y >> 4) & 31) * 1024u;  // K, V x 2 heads x 256 B rows
+                        }
+                        mbar_expect_tx(bar, bytes);
+                    }
+                    __syncwarp();
+                    {   // whole pieces without the new token: lane = (piece, tensor, half); both
+                        // kv heads' 16 rows in ONE 32-row box (they are adjacent in the block)
+                        const int jj = lane >> 2, t = lane & 1, c = (lane >> 1) & 1;
+                        if (jj < k2) {
+                            const int2 ent = list[q + jj];
+                            if (((ent.y >> 4) & 31) == 16 && (ent.y & 15) == 0) {
+                                unsigned char* dst = tb + t * kTensor + c * kHalfReg + (fill + jj) * kPair;
+                                if (it.kvpair && p.log2B == 4) {
+                                    tma_load_2d(dst, t ? &p.tmap_vp : &p.tmap_kp, c * 64, ent.x, bar);
+                                } else {  // B > 16 (heads B rows apart) or a GQA pair (one kv head twice)
+                                    tma_load_2d(dst, t ? &p.tmap_v[0] : &p.tmap_k[0], c * 64, ent.x, bar);
+                                    tma_load_2d(dst + kPiece, t ? &p.tmap_v[0] : &p.tmap_k[0], c * 64, ent.x + kvstep,
+                                                bar);
+                                }
+                            }
+                        }
+                    }
+                    for (int jj = 0; jj < k2; ++jj) {
+                        // a piece the context ends in: 8/4/2/1-row boxes per (tensor, half, head),
+                        // nothing past the context is read, then the new token's row from the input
+                        const int2 ent = list[q + jj];
+                        const int nrows = (ent.y >> 4) & 31, newm = (ent.y & 15) - 1;
+                        if (nrows == 16 && newm < 0) continue;
+                        const int ncache = nrows - (newm >= 0 ? 1 : 0);
+                        const int nb8 = __popc(ncache) * 8;  // ncache < 16 here
+                        const int nops = nb8 + (newm >= 0 ? 8 : 0);
+                        unsigned char* sbase = tb + (fill + jj) * kPair;
+                        for (int o = lane; o < nops; o += 32) {
+                            const bool cached = o < nb8;
+                            const int oo = cached ? o : o - nb8;
+                            const int bx = oo >> 3, t = oo & 1, c = (oo >> 1) & 1, hr = (oo >> 2) & 1;
+                            unsigned char* dst = sbase + t * kTensor + c * kHalfReg + hr * kPiece;
+                            if (cached) {
+                                int r0 = 0, mi = 1, seen = 0;
+                                for (int rb = 8; rb >= 1; rb >>= 1, ++mi) {
+                                    if (ncache & rb) {
+                                        if (seen == bx) break;
+                                        ++seen;
+                                        r0 += rb;
+                                    }
+                                }
+                                tma_load_2d(dst + r0 * 128, t ? &p.tmap_v[mi] : &p.tmap_k[mi], c * 64,
+                                            ent.x + hr * kvstep + r0, bar);
+                            } else {
+                                tma_load_2d(dst + (nrows - 1) * 128, t ? &p.tmap_nv : &p.tmap_nk, c * 64,
+                                            (it.s0 + newm) * p.H_kv + (hr ? it.kvh[1] : it.kvh[0]), bar);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    fill += k2;
+                    q += k2;
+                    if (fill == kSlots) {
+                        if (lane == 0) {
+                            TC_T(tcount, 1);
+                            meta[b].ns = kSlots;
+                            meta[b].last = 0;
+                            mbar_arrive(&tile_full[b]);
+                        }
+                        ++tcount;
+                        fill = 0;
+                    }
+                }
+                __syncwarp();  // every lane has read the chunk's list before it is rewritten
+            }
+            // close the item: its partial tile, or an empty one, carries last = 1
+            if (fill == 0) {
+                b = (int)(tcount % kBuf);
+                if (tcount >= (uint32_t)kBuf) mbar_wait(&tile_empty[b], ((tcount / kBuf) - 1) & 1);
+            }
+            if (lane == 0) {
+                TC_T(tcount, 1);
+                meta[b].ns = fill;
+                meta[b].last = 1;
+                mbar_arrive(&tile_full[b]);
+            }
+            ++tcount;
+            __syncwarp();
+        }
+    } else if (warp == 3) {
+        // ================================================================ MMA issuer ===
+        // One set of products covers both heads: A rows (tensor-memory lanes) 0-31 hold head 0's
+        // members, 64-95 head 1's; B rows of each piece are head 0's 16 K rows, then head 1's.
+        // S (N = 32 per piece) is then block-diagonal -- the off-diagonal head-0 x head-1
+        // products are computed and ignored -- and P carries zeros off the diagonal, so
+        // O = P V accumulates each head's rows from its own V rows only.
+        const uint32_t idesc_o = umma_idesc(kBF16, true, 128);
+        uint32_t tcount = 0, nitem = 0, scount = 0, pvitems = 0;
+        auto issue_pv = [&](int pb, uint32_t pt, int pns, bool started) {
+            const uint32_t sb = pt & 1;
+            mbar_wait(&p_full[sb], (pt >> 1) & 1);
+            if (lane == 0) TC_T(pt, 3);
+            if (!started) {  // the item's first P V overwrites O: its previous item's epilogue must be done
+                if (pvitems > 0) mbar_wait(o_free, (pvitems - 1) & 1);
+                ++pvitems;
+            }
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t vbase = smem_u32(sT + pb * kTileBytes + kTensor);
+                for (int j = 0; j < pns; ++j)
+                    for (int h = 0; h < 2; ++h)  // k-step = one head's 16 rows of piece j
+                        umma_f16_ts(tmem + kTmO, tmem + kTmS + sb * kSCols + 16 * j + 8 * h,
+                                    umma_desc_sw128(vbase + j * kPair + h * kPiece, kHalfReg, 1024), idesc_o,
+                                    (started || j > 0 || h > 0) ? 1u : 0u);
+                umma_commit(o_done);
+                umma_commit(&tile_empty[pb]);
+            }
+            __syncwarp();
+        };
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t slot = k & 3;
+            mbar_wait(&item_full[slot], (k >> 2) & 1);
+            const int i = *reinterpret_cast<volatile int*>(&item_ring[slot]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&item_empty[slot]);
+            if (i >= p.n_items) break;
+            const uint32_t qb = nitem & 1;
+            bool q_seen = false;
+            bool started = false;
+            int pend_b = -1, pend_ns = 0;
+            uint32_t pend_t = 0;
+            for (;;) {
+                const int b = (int)(tcount % kBuf);
+                mbar_wait(&tile_full[b], (tcount / kBuf) & 1);
+                if (lane == 0) TC_T(tcount, 2);
+                ++tcount;
+                const int ns = *reinterpret_cast<volatile int*>(&meta[b].ns);
+                const int last = *reinterpret_cast<volatile int*>(&meta[b].last);
+                uint32_t t = 0;
+                if (ns > 0) {
+                    if (!q_seen) {  // the softmax warps have put this item's queries in tensor memory
+                        mbar_wait(&q_full[qb], (nitem >> 1) & 1);
+                        q_seen = true;
+                    }
+                    t = scount++;
+                    const uint32_t sb = t & 1;
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t idesc_s = umma_idesc(kBF16, false, 32 * ns);
+                        const uint32_t kbase = smem_u32(sT + b * kTileBytes);
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk)  // S = Q (tensor memory) x K^T (all pieces, both heads)
+                            umma_f16_ts(tmem + kTmS + sb * kSCols, tmem + kTmQ + 8 * kk,
+                                        umma_desc_sw128(kbase + (kk >> 2) * kHalfReg + (kk & 3) * 32, 16, 1024),
+                                        idesc_s, kk > 0 ? 1u : 0u);
+                        umma_commit(&s_full[sb]);
+                    }
+                    __syncwarp();
+                }
+                if (pend_b >= 0) {
+                    issue_pv(pend_b, pend_t, pend_ns, started);
+                    started = true;
+                    pend_b = -1;
+                }
+                if (ns > 0) {
+                    pend_b = b;
+                    pend_t = t;
+                    pend_ns = ns;
+                } else {
+                    if (lane == 0) umma_commit(&tile_empty[b]);
+                    __syncwarp();
+                }
+                if (last) break;
+            }
+            if (pend_b >= 0) issue_pv(pend_b, pend_t, pend_ns, started);
+            if (!q_seen) mbar_wait(&q_full[qb], (nitem >> 1) & 1);  // keep the q_full phases in step
+            ++nitem;
+        }
+    } else {
+        // ================================================================ softmax ===
+        const int hh = warp >> 1;  // warp 0: head 0 (lanes 0-31), warp 2: head 1 (lanes 64-95)
+        const uint32_t lane_base = (uint32_t)(64 * hh) << 16;
+        const uint32_t tO = tmem + lane_base + kTmO;
+        const float c2 = p.scale_log2;
+        uint32_t tcount = 0, scount = 0, ocount = 0, nq = 0;
+        // the members' query rows of this head into tensor memory (the A operand of S = Q K^T):
+        // lane m = member m's row (16-bit pairs), signalled on q_full[nq & 1]
+        auto put_q = [&](const TcItem& q_it) {
+            const bool mem = lane < q_it.gmv;  // tcgen05.st is warp-collective: other lanes store zeros
+            const uint4* src = reinterpret_cast<const uint4*>(static_cast<const T*>(p.query) +
+                                                              ((int64_t)(q_it.s0 + (mem ? lane : 0)) * p.H +
+                                                               (hh ? q_it.h[1] : q_it.h[0])) * 128);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t w0[16], w1[16];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const uint4 v0 = mem ? __ldg(src + 8 * half + c) : make_uint4(0u, 0u, 0u, 0u);
+                    const uint4 v1 = mem ? __ldg(src + 8 * half + 4 + c) : make_uint4(0u, 0u, 0u, 0u);
+                    w0[4 * c] = v0.x;
+                    w0[4 * c + 1] = v0.y;
+                    w0[4 * c + 2] = v0.z;
+                    w0[4 * c + 3] = v0.w;
+                    w1[4 * c] = v1.x;
+                    w1[4 * c + 1] = v1.y;
+                    w1[4 * c + 2] = v1.z;
+                    w1[4 * c + 3] = v1.w;
+                }
+                tmem_st16(tmem + lane_base + kTmQ + 32 * half, w0);
+                tmem_st16(tmem + lane_base + kTmQ + 32 * half + 16, w1);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&q_full[nq & 1]);
+            ++nq;
+        };
+        int i = 0;
+        {
+            mbar_wait(&item_full[0], 0);
+            i = *reinterpret_cast<volatile int*>(&item_ring[0]);
+            if (i < p.n_items) put_q(tc_item(p, i));
+        }
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t slot = k & 3;
+            if (k > 0) {
+                mbar_wait(&item_full[slot], (k >> 2) & 1);
+                i = *reinterpret_cast<volatile int*>(&item_ring[slot]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&item_empty[slot]);
+            if (i >= p.n_items) break;
+            const TcItem it = tc_item(p, i);
+            const bool member = lane < it.gmv;
+            const int ctx = member ? max(0, __ldg(p.context_lens + it.s0 + lane)) : 0;
+            float mref = -INFINITY, l = 0.f;
+            int npv = 0;
+            for (;;) {
+                const int b = (int)(tcount % kBuf);
+                mbar_wait(&tile_full[b], (tcount / kBuf) & 1);
+                ++tcount;
+                const int ns = *reinterpret_cast<volatile int*>(&meta[b].ns);
+                const int last = *reinterpret_cast<volatile int*>(&meta[b].last);
+                int vm[kSlots];
+#pragma unroll
+                for (int j = 0; j < kSlots; ++j) {
+                    const int own = *reinterpret_cast<volatile int*>(&meta[b].own[j]);
+                    const int pj = *reinterpret_cast<volatile int*>(&meta[b].p[j]);
+                    vm[j] = (j < ns && member && ((own >> lane) & 1)) ? min(16, ctx - 16 * pj) : 0;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tile_empty[b]);
+                if (ns > 0) {
+                    const uint32_t t = scount++, sb = t & 1;
+                    mbar_wait(&s_full[sb], (t >> 1) & 1);
+                    if (lane == 0 && hh == 0) TC_T(t, 4);
+                    tc_fence_after();
+                    const uint32_t tS = tmem + lane_base + kTmS + sb * kSCols;
+                    // this head's 16 columns of every piece (the diagonal block)
+                    float sv[kSlots][16];
+#pragma unroll
+                    for (int j = 0; j < kSlots; ++j) tmem_ld16_nw(tS + 32 * j + 16 * hh, sv[j]);
+                    tmem_ld_wait();
+                    float mt = -INFINITY;
+#pragma unroll
+                    for (int j = 0; j < kSlots; ++j)
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            sv[j][u] *= c2;
+                            if (u < vm[j]) mt = fmaxf(mt, sv[j][u]);
+                        }
+                    const bool bump = __any_sync(0xffffffffu, mt > mref + kLazyTc);
+                    const float mn = bump ? fmaxf(mref, mt) : mref;
+                    const float ms = (mn == -INFINITY) ? 0.f : mn;
+                    const float alpha = bump ? ex2(mref - ms) : 1.f;
+                    float rs = 0.f;
+#pragma unroll
+                    for (int j = 0; j < kSlots; ++j) {
+                        // packed P of piece j: this head's 8 columns, zeros in the other head's 8
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int u = 0; u < 16; u += 2) {
+                            const float a0 = u < vm[j] ? ex2(sv[j][u] - ms) : 0.f;
+                            const float a1 = u + 1 < vm[j] ? ex2(sv[j][u + 1] - ms) : 0.f;
+                            rs += a0 + a1;
+                            const uint32_t pv = pack2<T>(a0, a1);
+                            pk[u / 2] = hh ? 0u : pv;
+                            pk[8 + u / 2] = hh ? pv : 0u;
+                        }
+                        tmem_st16(tS + 16 * j, pk);
+                    }
+                    if (lane == 0 && hh == 0) TC_T(t, 5);
+                    if (npv > 0) {  // P V of the previous tile has completed before O is rescaled
+                        mbar_wait(o_done, ocount & 1);
+                        ++ocount;
+                        tc_fence_after();
+                        if (bump) {
+#pragma unroll
+                            for (int c0 = 0; c0 < 128; c0 += 32) {
+                                float v[32];
+                                tmem_ld32_nw(tO + c0, v);
+                                tmem_ld_wait();
+#pragma unroll
+                                for (int u = 0; u < 32; ++u) v[u] *= alpha;
+                                tmem_st32(tO + c0, v);
+                            }
+                        }
+                    }
+                    l = l * alpha + rs;
+                    mref = mn;
+                    tmem_st_wait();
+                    tc_fence_before();
+                    mbar_arrive(&p_full[sb]);
+                    if (lane == 0 && hh == 0) TC_T(t, 6);
+                    ++npv;
+                }
+                if (last) break;
+            }
+            // every S of this item has been read: the next item's queries may replace Q now,
+            // so the MMA warp can start it while this epilogue runs
+            {
+                const uint32_t ns2 = (k + 1) & 3;
+                mbar_wait(&item_full[ns2], ((k + 1) >> 2) & 1);
+                const int i2 = *reinterpret_cast<volatile int*>(&item_ring[ns2]);
+                if (i2 < p.n_items) put_q(tc_item(p, i2));
+                i = i2;
+            }
+            // ---- epilogue: out row = O / l; then the new token's K/V row to its cache slot
+            if (npv > 0) {
+                mbar_wait(o_done, ocount & 1);
+                ++ocount;
+                tc_fence_after();
+            }
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            const bool store = member && (hh == 0 || it.st1);
+            T* orow = static_cast<T*>(p.out) + ((int64_t)(it.s0 + lane) * p.H + (hh ? it.h[1] : it.h[0])) * 128;
+#pragma unroll
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+                float v[32];
+                if (npv > 0) {
+                    tmem_ld32_nw(tO + c0, v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) v[u] = 0.f;
+                }
+                if (store) {
+#pragma unroll
+                    for (int c1 = 0; c1 < 32; c1 += 8) {
+                        uint4 w;
+                        w.x = pack2<T>(v[c1] * inv, v[c1 + 1] * inv);
+                        w.y = pack2<T>(v[c1 + 2] * inv, v[c1 + 3] * inv);
+                        w.z = pack2<T>(v[c1 + 4] * inv, v[c1 + 5] * inv);
+                        w.w = pack2<T>(v[c1 + 6] * inv, v[c1 + 7] * inv);
+                        *reinterpret_cast<uint4*>(orow + c0 + c1) = w;
+                    }
+                }
+            }
+            if (npv > 0) {
+                tc_fence_before();
+                mbar_arrive(o_free);
+            }
+            if (hh == 0 || it.st1) {
+                // reshape_and_cache of the step: member m's new K/V rows of this
+                // head's kv head to slot ctx_m - 1; lane = (K|V, 16-byte chunk)
+                const int t = lane >> 4, ch = lane & 15;
+                const int kvh = hh ? it.kvh[1] : it.kvh[0];
+                for (int m = 0; m < it.gmv; ++m) {
+                    const int cm = __shfl_sync(0xffffffffu, ctx, m);
+                    if (cm <= 0) continue;
+                    const int tp = cm - 1;
+                    const int blk = __ldg(p.block_tables + (int64_t)(it.s0 + m) * p.W + (tp >> p.log2B));
+                    const int64_t dst = ((((int64_t)blk * p.H_kv + kvh) << p.log2B) + (tp & ((1 << p.log2B) - 1))) * 128;
+                    const int64_t src = ((int64_t)(it.s0 + m) * p.H_kv + kvh) * 128;
+                    const uint4 val = __ldg(reinterpret_cast<const uint4*>(
+                                                static_cast<const T*>(t ? p.new_value : p.new_key) + src) +
+                                            ch);
+                    reinterpret_cast<uint4*>(static_cast<T*>(t ? p.value_cache : p.key_cache) + dst)[ch] = val;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 3) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+#ifdef PA_TC_TRACE
+extern "C" int pa_debug_tc_trace(void* host_out, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host_out, g_tc_trace, bytes < sizeof(g_tc_trace) ? bytes : sizeof(g_tc_trace));
+}
+#endif
+
+size_t group_tc_smem_bytes() {
+    return 1024 + (size_t)kBuf * kTileBytes + kBuf * sizeof(TileMeta) + kListCap * sizeof(int2) + kNumBars * 8 +
+           4 * 4 + 16;
+}
+
+cudaError_t launch_group_tc(const GroupTcParams& p, int dtype, cudaStream_t stream) {
+    const size_t smem = group_tc_smem_bytes();
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::max(1, std::min(sms, p.n_items));
+    if (dtype == 2) {
+        cudaError_t e = ensure_smem_attr((const void*)paged_attention_group_tc_kernel<__nv_bfloat16>, smem);
+        if (e != cudaSuccess) return e;
+        return launch_k(paged_attention_group_tc_kernel<__nv_bfloat16>, dim3(grid), dim3(kThreadsTc), smem, stream, p);
+    }
+    cudaError_t e = ensure_smem_attr((const void*)paged_attention_group_tc_kernel<__half>, smem);
+    if (e != cudaSuccess) return e;
+    return launch_k(paged_attention_group_tc_kernel<__half>, dim3(grid), dim3(kThreadsTc), smem, stream, p);
+}
+
+}  // namespace pa

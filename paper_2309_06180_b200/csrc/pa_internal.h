@@ -77,13 +77,30 @@ struct AttnParams {
     uint16_t seq_order[kMaxSeqOrder];
 };
 
-// Sharing-aware decode on the tensor cores (N1, pa_paged_attention_decode_grouped): the
-// caches as 2-D tensor maps [NB*H_kv*B rows][D], box {64 cols, 16 rows}, 128-byte swizzle;
-// everything else in `a` (GM = sequences per group, STG = stages).
-struct GroupParams {
-    CUtensorMap tmap_k;
-    CUtensorMap tmap_v;
-    AttnParams a;
+// Sharing-aware decode on the tcgen05 tensor cores (N1, pa_paged_attention_decode_grouped,
+// pa_decode_tc.cu).  TMA tensor maps are built by the host for every call.
+struct GroupTcParams {
+    CUtensorMap tmap_kp;     // key cache as [NB*H_kv*B rows][D], box {64 cols, 32 rows}: a 16-row
+                             // piece of two adjacent kv heads (consecutive in a block), one half
+    CUtensorMap tmap_vp;     // value cache, same
+    CUtensorMap tmap_k[5];   // key cache as [NB*H_kv*B rows][D], boxes {64 cols, 16 >> i rows}, 128-B swizzle
+    CUtensorMap tmap_v[5];   // value cache, same
+    CUtensorMap tmap_nk;     // the step's new key as [S*H_kv rows][D], box {64, 1}
+    CUtensorMap tmap_nv;     // new value, same
+    void* out;               // [S][H][D]
+    const void* query;       // [S][H][D] (rows copied into tensor memory by the softmax warps)
+    void* key_cache;         // writable cache bases (the new token's row is stored by the kernel)
+    void* value_cache;
+    const void* new_key;     // [S][H_kv][D]
+    const void* new_value;
+    const int32_t* block_tables;  // [S][W]
+    const int32_t* context_lens;  // [S]
+    unsigned long long* work_counter;  // 8 bytes of workspace: (epoch << 32 | items handed out)
+    uint32_t epoch;
+    float scale_log2;
+    int log2B, H, H_kv, G, W, S;
+    int GM;                  // sequences per group (<= 8)
+    int n_hp, n_items;       // head pairs, work items = groups x head pairs
 };
 
 struct GatherParams {
@@ -153,8 +170,8 @@ size_t attention_smem_bytes_shared(int row_bytes, int hpc, int G, int stg, int g
 // sched: 2 = coop (default), 4 = sharing-aware groups of GM sequences
 cudaError_t launch_attention(const AttnParams& p, int dtype, int head_dim, int num_seqs, int sched, size_t smem,
                              cudaStream_t stream);
-size_t group_mma_smem_bytes(int gm, int gsl, int stg, int pt, int hg);
-cudaError_t launch_group_mma(const GroupParams& p, int dtype, int num_seqs, size_t smem, cudaStream_t stream);
+size_t group_tc_smem_bytes();
+cudaError_t launch_group_tc(const GroupTcParams& p, int dtype, cudaStream_t stream);
 // variant: 0 = by max_query_len (default), 2 / 3 = force (PA_PREFILL ablation)
 cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, int variant,
                            cudaStream_t stream);

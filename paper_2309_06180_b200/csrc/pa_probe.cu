@@ -57,3 +57,66 @@ cudaError_t launch_hbm_read_probe(const void* buf, int64_t nchunks, int chunk, i
 }
 
 }  // namespace pa
+
+// ---- TMA tensor-copy throughput probe (test-only) ---------------------------
+// `warps` issuing warps per CTA (one elected lane each) stream 128-byte-swizzled 2-D boxes
+// {64 cols, rows} of a [nrows][128] 2-byte tensor into `stages` shared-memory slots per warp,
+// at pseudo-random row offsets (box-aligned), `iters` boxes per warp.  Bytes / time = the
+// tensor-copy ceiling of one SM for that box shape.
+#include "pa_tc.cuh"
+namespace pa {
+__global__ void __launch_bounds__(256) tma_probe_kernel(const __grid_constant__ CUtensorMap map, int nrows, int rows,
+                                                        int stages, int iters, uint32_t* sink) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem =
+        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int box = rows * 128;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)nw * stages * box);
+    if (threadIdx.x < nw * stages) mbar_init(&bars[threadIdx.x], 1);
+    fence_mbar_init();
+    __syncthreads();
+    if (lane != 0) return;
+    uint64_t* wb = bars + warp * stages;
+    unsigned char* ws = smem + (size_t)warp * stages * box;
+    uint32_t x = 2654435761u * (blockIdx.x * nw + warp + 1);
+    const int nbox = nrows / rows;
+    for (int it = 0; it < iters; ++it) {
+        const int s = it % stages;
+        if (it >= stages) mbar_wait(&wb[s], ((it / stages) - 1) & 1);
+        x = x * 1664525u + 1013904223u;
+        const int r = (int)((x >> 8) % (uint32_t)nbox) * rows;
+        mbar_arrive_expect_tx(&wb[s], (uint32_t)box);
+        tc::tma_load_2d(ws + (size_t)s * box, &map, (it & 1) * 64, r, &wb[s]);
+    }
+    for (int it = iters - stages; it < iters; ++it)
+        if (it >= 0) mbar_wait(&wb[it % stages], (it / stages) & 1);
+    sink[blockIdx.x * nw + warp] = x;
+}
+}  // namespace pa
+
+extern "C" int pa_debug_tma_probe(const void* buf, long long nrows, int rows, int warps, int stages, int iters,
+                                  int grid, uint32_t* sink, void* stream) {
+    CUtensorMap map;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return -1;
+    auto enc = reinterpret_cast<CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                             CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                             CUtensorMapFloatOOBfill)>(fn);
+    const cuuint64_t dims[2] = {128, (cuuint64_t)nrows};
+    const cuuint64_t str[1] = {256};
+    const cuuint32_t box[2] = {64, (cuuint32_t)rows};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(buf), dims, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return -2;
+    const size_t smem = 1024 + (size_t)warps * stages * rows * 128 + 8 * warps * stages;
+    if (cudaFuncSetAttribute(pa::tma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return -3;
+    pa::tma_probe_kernel<<<grid, 32 * warps, smem, (cudaStream_t)stream>>>(map, (int)nrows, rows, stages, iters, sink);
+    return (int)cudaGetLastError();
+}

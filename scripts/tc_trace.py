@@ -1,0 +1,55 @@
+"""Per-tile timeline of the tcgen05 grouped decode (variant build with -DPA_TC_TRACE):
+clock64 stamps of CTAs 0..7 for every tile -- producer acquired/published (0/1), MMA saw
+the tile (2) and issued its P V (3), softmax warp 0 saw S (4), wrote P (5), released P (6).
+  make clean && make NVXFLAGS=-DPA_TC_TRACE && python scripts/tc_trace.py c5_beam 4"""
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2309_06180_b200 as pa  # noqa: E402
+from paper_2309_06180_b200 import _lib  # noqa: E402
+from synth import make_config, materialize_torch, tables_torch  # noqa: E402
+
+name, gs = (sys.argv[1] if len(sys.argv) > 1 else "c5_beam"), int(sys.argv[2]) if len(sys.argv) > 2 else 4
+wl = make_config(name)
+x = materialize_torch(wl, "cuda")
+tb = tables_torch(wl, "cuda")
+out = torch.empty_like(x["query"])
+for _ in range(3):
+    pa.paged_attention_decode_grouped(out, x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"],
+                                      tb["block_tables"], tb["context_lens"], wl.scale, gs,
+                                      max_context_len=wl.max_context_len)
+torch.cuda.synchronize()
+NT = 1024
+buf = np.zeros(8 * NT * 8, np.int64)
+L = _lib.raw()
+L.pa_debug_tc_trace.restype = ctypes.c_int
+assert L.pa_debug_tc_trace(buf.ctypes.data, buf.nbytes) == 0
+tr = buf.reshape(8, NT, 8)
+res = {}
+for c in range(8):
+    t = tr[c]
+    n = int((t[:, 2] > 0).sum())
+    ns = int((t[:, 4] > 0).sum())
+    d = lambda a, b, m: np.median(t[:m, b] - t[:m, a]) if m > 1 else None  # noqa: E731
+    per = np.diff(t[:n, 2])
+    res[c] = {"tiles": n, "s_tiles": ns,
+              "span_us": float((t[n - 1, 2] - t[0, 2]) / 1.9e3) if n > 1 else None,
+              "tile_period_cyc_med": float(np.median(per)) if n > 2 else None,
+              "prod_issue_cyc_med(0->1)": float(d(0, 1, n)),
+              "publish_to_mma_cyc_med(1->2)": float(d(1, 2, n)),
+              "s_seen_to_P_cyc_med(4->5)": float(d(4, 5, ns)),
+              "P_to_release_cyc_med(5->6)": float(d(5, 6, ns)),
+              "release_to_pv_cyc_med(6->3)": float(d(6, 3, ns)),
+              "s_seen_period_cyc_med": float(np.median(np.diff(t[:ns, 4]))) if ns > 2 else None}
+    print(json.dumps({"cta": c, **res[c]}))
+# first 40 tiles of CTA 0, cycles relative to the first stamp
+t0 = tr[0][tr[0] > 0].min()
+for i in range(40):
+    print(i, [int(v - t0) if v > 0 else -1 for v in tr[0, i, :7]])
