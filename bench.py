@@ -120,13 +120,13 @@ def parse():
     ap.add_argument("--block-size", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="separate reshape_and_cache launch (ablation)")
-    ap.add_argument("--grouped", type=int, default=0,
+    ap.add_argument("--grouped", type=int, default=-1,
                     help="sharing-aware decode on the tensor cores over groups of this many sequences "
-                         "(SURVEY 8(f) N1; 0 = off, 'auto' sizes: C3 6, C5 4 via --grouped -1)")
-    ap.add_argument("--shared", type=int, default=-1,
+                         "(tcgen05 kernel, SURVEY 8(f) N1; 0 = off; -1 = auto: C5's beam groups of 4, where it "
+                         "measured fastest; coop elsewhere)")
+    ap.add_argument("--shared", type=int, default=0,
                     help="sharing-aware decode on the CUDA cores over groups of this many sequences "
-                         "(pa_paged_attention_decode_shared, SURVEY 8(f) N1; 0 = off (coop), -1 = auto: C5's "
-                         "beam groups of 4, where it measured faster than coop; coop elsewhere)")
+                         "(pa_paged_attention_decode_shared, SURVEY 8(f) N1; ablation, 0 = off)")
     ap.add_argument("--layers", type=int, default=0,
                     help="rotated layer caches (0 = auto: R x K/V read per step >= 4 x L2, R >= 2)")
     ap.add_argument("--no-plan", action="store_true",
@@ -263,11 +263,13 @@ def run_ours(a, wl_full, world, rank, local):
                     raise
                 tp_gather = f"nccl (fused setup failed: {type(exc).__name__}: {exc})"
     has_pairs = len(wl.block_mapping) > 0
-    grouped = a.grouped if a.grouped >= 0 else {"c3_parallel": 6, "c3_fork": 6, "c5_beam": 4}.get(wl_full.name, 0)
+    auto_grouped = {"c5_beam": 4}.get(wl_full.name, 0)
+    grouped = a.grouped if a.grouped >= 0 else auto_grouped
+    if a.shared > 0 or ftp is not None or a.unfused:
+        grouped = 0 if a.grouped < 0 else grouped
     if grouped and (ftp is not None or a.unfused):
         raise SystemExit("--grouped runs the single-GPU fused decode step only")
-    auto_shared = {"c5_beam": 4}.get(wl_full.name, 0)
-    shared_g = a.shared if a.shared >= 0 else auto_shared
+    shared_g = a.shared
     if ftp is not None or a.unfused or grouped:
         if a.shared > 0:
             raise SystemExit("--shared runs the single-GPU fused decode step only")
@@ -276,7 +278,7 @@ def run_ours(a, wl_full, world, rank, local):
 
     # longest-first grid order from the host context lengths, once per decode iteration
     # (every layer reuses it, like the block tables): scheduling only, bit-identical output
-    use_plan = not a.no_plan and not grouped and not shared_g
+    use_plan = not a.no_plan and not shared_g
     plan = pa.decode_plan(wl.context_lens) if use_plan else None
     # every launch of the step prepared once per layer cache (pa.prepare: Python checks and
     # argument marshalling done up front), so the timed loop is not bound by host overhead
@@ -295,7 +297,7 @@ def run_ours(a, wl_full, world, rank, local):
                               partition_tokens=a.partition_tokens, workspace=ws, seq_order=plan)
         elif grouped:  # N1: groups of sequences sharing blocks, QK^T / PV on the tensor cores
             attn = pa.prepare(pa.paged_attention_decode_grouped, out, q, kn, vn, kc, vc, bt, cl, wl.scale, grouped,
-                              max_context_len=mcl, workspace=ws)
+                              max_context_len=mcl, workspace=ws, seq_order=plan)
         elif shared_g:  # N1: groups of sequences sharing blocks, each distinct block staged once
             attn = pa.prepare(pa.paged_attention_decode_shared, out, q, kn, vn, kc, vc, bt, cl, wl.scale, shared_g,
                               max_context_len=mcl, workspace=ws)
@@ -408,8 +410,8 @@ def run_ours(a, wl_full, world, rank, local):
     value = kv_all / (ms_step * 1e-3) / 1e9
     ach = achieved_u if shared else achieved
     # ncu_traffic.json keys: the workload for its default kernel, _grouped / _coop otherwise
-    traffic = load_traffic(wl_full.name + ("_grouped" if grouped else "_coop" if auto_shared and not shared_g
-                                           else "_shared" if shared_g and not auto_shared else ""), world)
+    traffic = load_traffic(wl_full.name + ("" if grouped == auto_grouped and not shared_g else "_grouped" if grouped
+                                           else "_shared" if shared_g else "_coop"), world)
     read_kv = min(kv_unique, sb["kv_logical"])
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
@@ -440,9 +442,9 @@ def run_ours(a, wl_full, world, rank, local):
                             "host_issue_us = rank 0's CPU time to issue one step (prepared calls) while the GPU is "
                             "busy elsewhere (warm-up behind a sleep): the loop is device-bound when it is below the "
                             "step time; host_loop_us = the timed loop's CPU time per step (blocks on a full queue)"},
-        "roofline": {"bound": "hbm", "kernel": (f"paged_attention_group_mma_kernel (pa_paged_attention_decode_grouped, "
-                                                 f"groups of {grouped}: shared blocks loaded once, QK^T and PV as "
-                                                 f"tensor-core MMAs; cache write fused)") if grouped else
+        "roofline": {"bound": "hbm", "kernel": (f"paged_attention_group_tc_kernel (pa_paged_attention_decode_grouped, "
+                                                 f"groups of {grouped}: each distinct block piece loaded once, QK^T "
+                                                 f"and PV as tcgen05 MMAs; cache write fused)") if grouped else
                      (f"paged_attention_shared_kernel (pa_paged_attention_decode_shared, groups of {shared_g}: each "
                       f"distinct block staged once for the group's members; cache write fused)") if shared_g else
                      "paged_attention_kernel (pa_paged_attention_decode: cache write + attention + split-context "

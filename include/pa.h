@@ -161,17 +161,23 @@ pa_status_t pa_paged_attention_decode_shared(void* out, const void* query, const
 
 /* ------------------------------------------------------------------------------------
  * pa_paged_attention_decode_grouped -- the sharing-aware decode step
- * on the tensor cores.  Same grouping and arguments as pa_paged_attention_decode_shared
- * plus num_blocks (NB, rows of the caches, for the TMA tensor maps).  One CTA per
- * (partition, query head, group): every distinct physical block the group reads at a
- * logical 16-token tile is TMA-loaded once, and Q K^T and P V are computed for all the
- * group's members at once with m16n8k16 tensor-core MMAs (rows = members), each row
- * masked to its own block and context (Eq.4; sharing P:295-332).  The new
- * token's K/V is read from key/value and written to its cache slot as in
- * pa_paged_attention_decode.  Results match the oracle within the stated tolerance
- * (accumulation order differs from the CUDA-core kernels: not bit-identical to them).
- * Supports f16/bf16, head_dim 128, power-of-two block_size >= 16, group_size in [1, 8]
- * (PA_ERR_UNSUPPORTED otherwise); NB*H_kv*B < 2^31.  Workspace as pa_paged_attention.
+ * on the tcgen05 tensor cores.  Same grouping and arguments as
+ * pa_paged_attention_decode_shared plus num_blocks (NB, rows of the caches, for the TMA
+ * tensor maps) and host_seq_order (as pa_paged_attention_ex: the groups are walked in the
+ * order of their first sequence in it, e.g. pa_decode_plan's longest first; NULL =
+ * natural order; scheduling only).  Persistent CTAs (one per SM) take work items =
+ * (group, 4 query heads): a producer warp looks up the members' physical blocks, keeps
+ * every DISTINCT 16-row block piece once (its owner set) and TMA-loads it for the 4 heads
+ * in one 64-row box per tensor half; S = Q K^T and O += P V run as tcgen05.mma with Q, S,
+ * P and O in tensor memory -- one set of products for the 4 heads, block-diagonal by
+ * lane quadrant -- each member's scores masked to the pieces it owns and its context
+ * (Eq.4; sharing P:295-332).  The new token's K/V is written to its
+ * cache slot before the pieces are read, as pa_paged_attention_decode leaves the cache.
+ * P is rounded to the storage dtype before P V (results match the oracle within the
+ * stated tolerance; not bit-identical to the CUDA-core kernels).  Supports f16/bf16,
+ * head_dim 128, power-of-two block_size >= 16, group_size in [1, 8]
+ * (PA_ERR_UNSUPPORTED otherwise); NB*H_kv*B < 2^31.  workspace: >= 16 bytes, any
+ * content (an epoch-tagged work counter; never reset by the host).
  * ---------------------------------------------------------------------------------- */
 pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, const void* key,
                                               const void* value, void* key_cache, void* value_cache,
@@ -180,7 +186,8 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
                                               int block_size, int num_kv_heads, int num_blocks,
                                               int num_seqs, int num_heads, int head_dim,
                                               int max_blocks_per_seq, int max_context_len,
-                                              int group_size, pa_dtype_t dtype, void* workspace,
+                                              int group_size, pa_dtype_t dtype,
+                                              const int32_t* host_seq_order, void* workspace,
                                               size_t workspace_bytes, pa_stream_t stream);
 
 /* ------------------------------------------------------------------------------------

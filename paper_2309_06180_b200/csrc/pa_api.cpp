@@ -469,8 +469,8 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
                                               const int32_t* context_lens, float scale, int block_size,
                                               int num_kv_heads, int num_blocks, int num_seqs, int num_heads,
                                               int head_dim, int max_blocks_per_seq, int max_context_len,
-                                              int group_size, pa_dtype_t dtype, void* workspace,
-                                              size_t workspace_bytes, pa_stream_t stream) {
+                                              int group_size, pa_dtype_t dtype, const int32_t* host_seq_order,
+                                              void* workspace, size_t workspace_bytes, pa_stream_t stream) {
     g_err.clear();
     REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
     if (dtype == PA_F32) return fail(PA_ERR_UNSUPPORTED, "grouped decode supports f16 and bf16 only");
@@ -513,9 +513,9 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
                 return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the cache maps");
         }
         {
-            const cuuint32_t box[2] = {64, 32};  // a piece of two adjacent kv heads (B >= 16 rows each)
-            if (!encode_map(&gp.tmap_kp, dt, 2, key_cache, cdims, str, box) ||
-                !encode_map(&gp.tmap_vp, dt, 2, value_cache, cdims, str, box))
+            const cuuint32_t box[2] = {64, 64};  // a piece of four adjacent kv heads (B = 16)
+            if (!encode_map(&gp.tmap_kq, dt, 2, key_cache, cdims, str, box) ||
+                !encode_map(&gp.tmap_vq, dt, 2, value_cache, cdims, str, box))
                 return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the piece-pair maps");
         }
         const cuuint32_t box1[2] = {64, 1};
@@ -542,10 +542,29 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
     gp.W = max_blocks_per_seq;
     gp.S = num_seqs;
     gp.GM = group_size;
-    gp.n_hp = (num_heads + 1) / 2;
+    gp.n_hp = (num_heads + 3) / 4;
     const int64_t items = (int64_t)((num_seqs + group_size - 1) / group_size) * gp.n_hp;
     REQUIRE(items < (1LL << 31), "too many work items");
     gp.n_items = (int)items;
+    gp.n_gorder = 0;
+    const int ngroups = (num_seqs + group_size - 1) / group_size;
+    if (host_seq_order != nullptr && ngroups <= pa::kMaxSeqOrder) {
+        // groups in the order of their first sequence in the plan (longest first)
+        static thread_local std::vector<unsigned char> seen;
+        seen.assign((size_t)ngroups, 0);
+        int n = 0;
+        for (int i = 0; i < num_seqs; ++i) {
+            const int32_t v = host_seq_order[i];
+            REQUIRE(v >= 0 && v < num_seqs, "host_seq_order entry %d = %d is out of range", i, (int)v);
+            const int g = v / group_size;
+            if (!seen[(size_t)g]) {
+                seen[(size_t)g] = 1;
+                gp.gorder[n++] = (uint16_t)g;
+            }
+        }
+        REQUIRE(n == ngroups, "host_seq_order is not a permutation of [0, %d)", num_seqs);
+        gp.n_gorder = ngroups;
+    }
     cudaError_t e = pa::launch_group_tc(gp, (int)dtype, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "paged_attention_group_tc_kernel launch");
     return PA_OK;

@@ -33,43 +33,49 @@ namespace pa {
 using namespace tc;
 
 namespace {
-constexpr int kSlots = 4;                   // 16-row block pieces per MMA tile
+constexpr int kNH = 4;                      // query heads per work item (one TMEM lane quadrant each)
+constexpr int kSlots = 2;                   // 16-row block pieces per MMA tile
 constexpr int kBuf = 3;                     // tile buffers in shared memory
 constexpr int kPiece = 16 * 128;            // [16 rows][64 cols] swizzled, 2-byte elements
-constexpr int kPair = 2 * kPiece;           // one piece, both kv heads stacked: [32 rows][128 B] = 4 KB
-constexpr int kHalfReg = kSlots * kPair;    // one 64-column half of the tile: 16 KB
+constexpr int kQuad = kNH * kPiece;         // one piece, the item's kv heads stacked: [64 rows][128 B] = 8 KB
+constexpr int kHalfReg = kSlots * kQuad;    // one 64-column half of the tile: 16 KB
 constexpr int kTensor = 2 * kHalfReg;       // K (or V) of the tile: 32 KB
 constexpr int kTileBytes = 2 * kTensor;     // 64 KB: [K|V][half][piece][head][16 rows][128 B]
 constexpr int kMaxGM = 8;
 constexpr int kListCap = 32 * kMaxGM;       // pieces of one 32-position chunk
 constexpr float kLazyTc = 8.f;              // P <= 2^8 between rescales
-constexpr int kThreadsTc = 128;             // warps: 0 softmax head 0, 1 producer, 2 softmax head 1, 3 MMA
-// tensor memory columns: Q (16-bit pairs) | S0 | S1 | O; lanes 0-31 = head 0's members,
-// lanes 64-95 = head 1's members (the softmax warps 0 and 2 own those lane quadrants)
-constexpr int kTmQ = 0, kTmS = 64, kSCols = 32 * kSlots, kTmO = kTmS + 2 * kSCols;
-constexpr int kNumBars = 2 * kBuf + 2 + 2 + 2 + 1 + 1 + 4 + 4;
+constexpr int kThreadsTc = 192;             // warps: 0-3 softmax (head w = lane quadrant w), 4 producer, 5 MMA
+// tensor memory columns: Q0 | Q1 (16-bit pairs, by item parity) | S0 | S1 | O; lanes
+// 32w..32w+31 = head w's members
+constexpr int kTmQ = 0, kTmS = 128, kSCols = 16 * kNH * kSlots, kTmO = kTmS + 2 * kSCols;
+constexpr int kNumBars = 2 * kBuf + 2 + 2 + 2 + 1 + 1 + 4 + 4 + 2;
 
 struct TileMeta {
     int ns, last;
-    int p[kSlots], own[kSlots];
+    int p[kSlots], own[kSlots], nrows[kSlots];
 };
 
 struct TcItem {
-    int s0, gmv, h[2], kvh[2];
-    bool st1, kvpair;  // second head stored; the two heads read different kv heads (else one, GQA)
+    int s0, gmv, h[kNH], kvh[kNH];
+    unsigned st;  // bit w: head w of the quad exists (H % 4 tail: duplicates are not stored)
+    bool quad;    // the 4 kv heads are consecutive (one 64-row box per piece half when B == 16)
 };
 
 __device__ __forceinline__ TcItem tc_item(const GroupTcParams& p, int i) {
     TcItem it;
-    const int g = i / p.n_hp, hp = i - g * p.n_hp;
+    const int gi = i / p.n_hp, hq = i - gi * p.n_hp;
+    const int g = gi < p.n_gorder ? (int)p.gorder[gi] : gi;  // longest-first plan (scheduling only)
     it.s0 = g * p.GM;
     it.gmv = min(p.GM, p.S - it.s0);
-    it.h[0] = 2 * hp;
-    it.h[1] = min(2 * hp + 1, p.H - 1);
-    it.st1 = 2 * hp + 1 < p.H;
-    it.kvh[0] = it.h[0] / p.G;
-    it.kvh[1] = it.h[1] / p.G;
-    it.kvpair = it.kvh[1] != it.kvh[0];
+    it.st = 0;
+    it.quad = true;
+#pragma unroll
+    for (int w = 0; w < kNH; ++w) {
+        it.h[w] = min(kNH * hq + w, p.H - 1);
+        if (kNH * hq + w < p.H) it.st |= 1u << w;
+        it.kvh[w] = it.h[w] / p.G;
+        if (it.kvh[w] != it.kvh[0] + w) it.quad = false;
+    }
     return it;
 }
 
@@ -107,10 +113,15 @@ __device__ long long g_tc_trace[8 * kTrTiles * 8];
     } while (0)
 #endif
 
+__device__ __forceinline__ int sel4(const int (&a)[kNH], int w) {
+    return w == 0 ? a[0] : w == 1 ? a[1] : w == 2 ? a[2] : a[3];
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     paged_attention_group_tc_kernel(const __grid_constant__ GroupTcParams p) {
     constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+    constexpr int kProd = kNH, kMma = kNH + 1;  // warp roles; warps 0..kNH-1 run the softmax
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem =
         reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -119,43 +130,42 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     int2* list = reinterpret_cast<int2*>(meta + kBuf);
     uint64_t* bars = reinterpret_cast<uint64_t*>(list + kListCap);
     uint64_t* tile_full = bars;                 // kBuf: TMA bytes + producer arrive
-    uint64_t* tile_empty = bars + kBuf;         // kBuf: MMA commit + 2 softmax warps
-    uint64_t* q_full = bars + 2 * kBuf;         // 2 (by item parity): 64 softmax lanes wrote Q
+    uint64_t* tile_empty = bars + kBuf;         // kBuf: MMA commit + kNH softmax warps
+    uint64_t* q_full = bars + 2 * kBuf;         // 2 (by item parity): the softmax lanes wrote Q
     uint64_t* s_full = q_full + 2;              // [S buffer]
-    uint64_t* p_full = s_full + 2;              // [S buffer]: 64 softmax lanes
-    uint64_t* o_done = p_full + 2;              // 1
-    uint64_t* o_free = o_done + 1;              // 1: 64 softmax lanes
+    uint64_t* p_full = s_full + 2;              // [S buffer]: the softmax lanes
+    uint64_t* o_last = p_full + 2;              // 1: an item's last P V has completed
+    uint64_t* o_free = o_last + 1;              // 1: the softmax lanes read O
     uint64_t* item_full = o_free + 1;           // 4: producer -> MMA + softmax
-    uint64_t* item_empty = item_full + 4;       // 4: MMA + 2 softmax warps
+    uint64_t* item_empty = item_full + 4;       // 4: MMA + kNH softmax warps
+    uint64_t* o_step = item_empty + 4;          // 2: P V number k on o_step[k & 1] (MMA warp only)
     int* item_ring = reinterpret_cast<int*>(bars + kNumBars);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_ring + 4);
+    volatile int* pv_done = reinterpret_cast<volatile int*>(tmem_slot + 1);  // last completed P V (tile index)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int i = 0; i < kBuf; ++i) {
             mbar_init(&tile_full[i], 1);
-            mbar_init(&tile_empty[i], 3);
+            mbar_init(&tile_empty[i], 1 + kNH);
         }
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&q_full[i], 64);
+            mbar_init(&q_full[i], 32 * kNH);
             mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 64);
+            mbar_init(&p_full[i], 32 * kNH);
         }
-        mbar_init(o_done, 1);
-        mbar_init(o_free, 64);
+        mbar_init(o_last, 1);
+        mbar_init(&o_step[0], 1);
+        mbar_init(&o_step[1], 1);
+        mbar_init(o_free, 32 * kNH);
+        *pv_done = -1;
         for (int i = 0; i < 4; ++i) {
             mbar_init(&item_full[i], 1);
-            mbar_init(&item_empty[i], 3);
+            mbar_init(&item_empty[i], 1 + kNH);
         }
         fence_mbar_init();
     }
-    // V rows past a piece's last loaded row are multiplied by P = 0, so they must not hold
-    // NaN bit patterns: zero the V halves once; later they only hold loaded, finite rows
-    for (int b = 0; b < kBuf; ++b)
-        for (int i = tid; i < kTensor / 16; i += kThreadsTc)
-            reinterpret_cast<uint4*>(sT + b * kTileBytes + kTensor)[i] = make_uint4(0u, 0u, 0u, 0u);
-    fence_proxy_async_smem();
-    if (warp == 3) tmem_alloc(tmem_slot, 512);
+    if (warp == kMma) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -164,7 +174,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     pdl_launch_dependents();
     const int ppb_log = p.log2B - 4;  // 16-row pieces per block (log2)
 
-    if (warp == 1) {
+    if (warp == kProd) {
         // ================================================================ producer ===
         uint32_t tcount = 0;
         for (uint32_t k = 0;; ++k) {
@@ -188,7 +198,28 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 ctxs[m] = __shfl_sync(0xffffffffu, myctx, m);
                 if (m < it.gmv) maxp = max(maxp, (ctxs[m] + 15) >> 4);
             }
-            const int kvstep = it.kvpair ? (1 << p.log2B) : 0;  // rows from kv head 0 to kv head 1
+            // reshape_and_cache of the step, first: member m's new K/V rows of the
+            // quad's kv heads to slot ctx_m - 1, so that every piece below is read whole from
+            // the cache (one box per tensor and half); lane = (head w, K|V, 16-byte chunk group)
+            for (int m = 0; m < it.gmv; ++m) {
+                const int cm = ctxs[m];
+                if (cm <= 0) continue;
+                const int tp = cm - 1;
+                const int blk = __ldg(p.block_tables + (int64_t)(it.s0 + m) * p.W + (tp >> p.log2B));
+                const int w = lane >> 3, t = (lane >> 2) & 1, c4 = lane & 3;
+                if ((it.st >> w) & 1u) {
+                    const int kvw = sel4(it.kvh, w);
+                    const int64_t dst = ((((int64_t)blk * p.H_kv + kvw) << p.log2B) + (tp & ((1 << p.log2B) - 1))) * 128;
+                    const int64_t src = ((int64_t)(it.s0 + m) * p.H_kv + kvw) * 128;
+                    const uint4* sp = reinterpret_cast<const uint4*>(static_cast<const T*>(t ? p.new_value : p.new_key) + src);
+                    uint4* dp = reinterpret_cast<uint4*>(static_cast<T*>(t ? p.value_cache : p.key_cache) + dst);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) dp[c4 * 4 + u] = __ldg(sp + c4 * 4 + u);
+                }
+            }
+            fence_proxy_async_global();  // the rows above are read by this warp's TMA copies below
+            __syncwarp();
+            const bool quad_box = it.quad && p.log2B == 4;  // the 4 kv heads' pieces are 64 adjacent rows
             int fill = 0, b = 0;
             unsigned char* tb = sT;
             for (int p0 = 0; p0 < maxp; p0 += 32) {
@@ -224,18 +255,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
                 for (int m = 0; m < kMaxGM; ++m) {
                     if ((lead >> m) & 1u) {
-                        int own = 0, nrows = 0, newm = -1;
+                        int own = 0, nrows = 0;
 #pragma unroll
                         for (int m2 = 0; m2 < kMaxGM; ++m2) {
                             if (id[m2] == id[m]) {
                                 own |= 1 << m2;
                                 nrows = max(nrows, min(16, ctxs[m2] - 16 * pp));
-                                if (((ctxs[m2] - 1) >> 4) == pp) newm = m2;
                             }
                         }
-                        const int blk = id[m] >> ppb_log, pc = id[m] & ((1 << ppb_log) - 1);
-                        list[e++] = make_int2(((blk * p.H_kv + it.kvh[0]) << p.log2B) | (pc << 4),
-                                              (pp << 18) | (own << 10) | (nrows << 4) | (newm + 1));
+                        list[e++] = make_int2(id[m], (pp << 18) | (own << 10) | (nrows << 4));
                     }
                 }
                 __syncwarp();
@@ -250,62 +278,31 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                     const int k2 = min(kSlots - fill, total - q);
                     uint64_t* bar = &tile_full[b];
                     if (lane == 0) {
-                        uint32_t bytes = 0;
                         for (int jj = 0; jj < k2; ++jj) {
                             const int y = list[q + jj].y;
                             meta[b].p[fill + jj] = y >> 18;
                             meta[b].own[fill + jj] = (y >> 10) & 0xff;
-                            bytes += (uint32_t)((y >> 4) & 31) * 1024u;  // K, V x 2 heads x 256 B rows
+                            meta[b].nrows[fill + jj] = (y >> 4) & 31;
                         }
-                        mbar_expect_tx(bar, bytes);
+                        mbar_expect_tx(bar, (uint32_t)k2 * (uint32_t)kQuad * 4u);  // whole pieces: K, V x 2 halves
                     }
                     __syncwarp();
-                    {   // whole pieces without the new token: lane = (piece, tensor, half); both
-                        // kv heads' 16 rows in ONE 32-row box (they are adjacent in the block)
-                        const int jj = lane >> 2, t = lane & 1, c = (lane >> 1) & 1;
-                        if (jj < k2) {
+                    {   // whole pieces (rows past a context are read but never used; V's are zeroed
+                        // in shared memory by the softmax warps).  quad: lane = (piece, tensor,
+                        // half), the 4 kv heads' rows in ONE 64-row box; otherwise lane = (piece,
+                        // tensor, half, head), 16-row boxes
+                        const int jj = quad_box ? (lane >> 2) : (lane >> 4);
+                        const int t = lane & 1, c = (lane >> 1) & 1, w = (lane >> 2) & 3;
+                        if (jj < k2 && (quad_box ? lane < 4 * k2 : true)) {
                             const int2 ent = list[q + jj];
-                            if (((ent.y >> 4) & 31) == 16 && (ent.y & 15) == 0) {
-                                unsigned char* dst = tb + t * kTensor + c * kHalfReg + (fill + jj) * kPair;
-                                if (it.kvpair && p.log2B == 4) {
-                                    tma_load_2d(dst, t ? &p.tmap_vp : &p.tmap_kp, c * 64, ent.x, bar);
-                                } else {  // B > 16 (heads B rows apart) or a GQA pair (one kv head twice)
-                                    tma_load_2d(dst, t ? &p.tmap_v[0] : &p.tmap_k[0], c * 64, ent.x, bar);
-                                    tma_load_2d(dst + kPiece, t ? &p.tmap_v[0] : &p.tmap_k[0], c * 64, ent.x + kvstep,
-                                                bar);
-                                }
-                            }
-                        }
-                    }
-                    for (int jj = 0; jj < k2; ++jj) {
-                        // a piece the context ends in: 8/4/2/1-row boxes per (tensor, half, head),
-                        // nothing past the context is read, then the new token's row from the input
-                        const int2 ent = list[q + jj];
-                        const int nrows = (ent.y >> 4) & 31, newm = (ent.y & 15) - 1;
-                        if (nrows == 16 && newm < 0) continue;
-                        const int ncache = nrows - (newm >= 0 ? 1 : 0);
-                        const int nb8 = __popc(ncache) * 8;  // ncache < 16 here
-                        const int nops = nb8 + (newm >= 0 ? 8 : 0);
-                        unsigned char* sbase = tb + (fill + jj) * kPair;
-                        for (int o = lane; o < nops; o += 32) {
-                            const bool cached = o < nb8;
-                            const int oo = cached ? o : o - nb8;
-                            const int bx = oo >> 3, t = oo & 1, c = (oo >> 1) & 1, hr = (oo >> 2) & 1;
-                            unsigned char* dst = sbase + t * kTensor + c * kHalfReg + hr * kPiece;
-                            if (cached) {
-                                int r0 = 0, mi = 1, seen = 0;
-                                for (int rb = 8; rb >= 1; rb >>= 1, ++mi) {
-                                    if (ncache & rb) {
-                                        if (seen == bx) break;
-                                        ++seen;
-                                        r0 += rb;
-                                    }
-                                }
-                                tma_load_2d(dst + r0 * 128, t ? &p.tmap_v[mi] : &p.tmap_k[mi], c * 64,
-                                            ent.x + hr * kvstep + r0, bar);
+                            const int blk = ent.x >> ppb_log, pc = ent.x & ((1 << ppb_log) - 1);
+                            unsigned char* dst = tb + t * kTensor + c * kHalfReg + (fill + jj) * kQuad;
+                            if (quad_box) {
+                                tma_load_2d(dst, t ? &p.tmap_vq : &p.tmap_kq, c * 64, (blk * p.H_kv + it.kvh[0]) << 4,
+                                            bar);
                             } else {
-                                tma_load_2d(dst + (nrows - 1) * 128, t ? &p.tmap_nv : &p.tmap_nk, c * 64,
-                                            (it.s0 + newm) * p.H_kv + (hr ? it.kvh[1] : it.kvh[0]), bar);
+                                tma_load_2d(dst + w * kPiece, t ? &p.tmap_v[0] : &p.tmap_k[0], c * 64,
+                                            ((blk * p.H_kv + sel4(it.kvh, w)) << p.log2B) | (pc << 4), bar);
                             }
                         }
                     }
@@ -339,99 +336,123 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             ++tcount;
             __syncwarp();
         }
-    } else if (warp == 3) {
+    } else if (warp == kMma) {
         // ================================================================ MMA issuer ===
-        // One set of products covers both heads: A rows (tensor-memory lanes) 0-31 hold head 0's
-        // members, 64-95 head 1's; B rows of each piece are head 0's 16 K rows, then head 1's.
-        // S (N = 32 per piece) is then block-diagonal -- the off-diagonal head-0 x head-1
-        // products are computed and ignored -- and P carries zeros off the diagonal, so
-        // O = P V accumulates each head's rows from its own V rows only.
-        const uint32_t idesc_o = umma_idesc(kBF16, true, 128);
-        uint32_t tcount = 0, nitem = 0, scount = 0, pvitems = 0;
-        auto issue_pv = [&](int pb, uint32_t pt, int pns, bool started) {
-            const uint32_t sb = pt & 1;
-            mbar_wait(&p_full[sb], (pt >> 1) & 1);
-            if (lane == 0) TC_T(pt, 3);
-            if (!started) {  // the item's first P V overwrites O: its previous item's epilogue must be done
-                if (pvitems > 0) mbar_wait(o_free, (pvitems - 1) & 1);
-                ++pvitems;
-            }
-            tc_fence_after();
-            if (lane == 0) {
-                const uint32_t vbase = smem_u32(sT + pb * kTileBytes + kTensor);
+        // One set of products covers the item's kNH heads: A rows (tensor-memory lanes)
+        // 32w..32w+31 hold head w's members, and the B rows of each piece are head 0's 16 K
+        // rows, then head 1's, ...  S (N = 16 kNH per piece) is then block-diagonal -- the
+        // off-diagonal products are computed and ignored -- and P carries zeros off the
+        // diagonal, so O = P V accumulates each head's rows from its own V rows only.
+        // One thread issues everything (tcgen05.mma is single-thread); descriptors are
+        // built once and stepped by constant offsets (address field = bytes >> 4).
+        if (lane == 0) {
+            const uint32_t idesc_o = umma_idesc(kBF16, true, 128);
+            const uint64_t kdesc0 = umma_desc_sw128(smem_u32(sT), 16, 1024);
+            const uint64_t vdesc0 = umma_desc_sw128(smem_u32(sT + kTensor), kHalfReg, 1024);
+            uint32_t tcount = 0, nitem = 0, scount = 0, pvitems = 0, pv_issued = 0, pv_pub = 0;
+            // the completion of every issued P V, in order, published to the softmax warps as
+            // a tile index in shared memory (they wait on it only to rescale O -- rarely).
+            // P V k commits to o_step[k & 1]; at most two are unpublished, so no barrier ever
+            // runs two phases ahead of this thread's waits
+            auto publish_one = [&](bool block) -> bool {
+                if (pv_pub >= pv_issued) return false;
+                uint64_t* bar = &o_step[pv_pub & 1];
+                const uint32_t par = (pv_pub >> 1) & 1;
+                if (block) {
+                    mbar_wait(bar, par);
+                } else if (!mbar_test(bar, par)) {
+                    return false;
+                }
+                tc_fence_after();
+                *pv_done = (int)pv_pub;
+                ++pv_pub;
+                return true;
+            };
+            auto issue_pv = [&](int pb, uint32_t pt, int pns, bool started, bool last_pv) {
+                const uint32_t sb = pt & 1;
+                while (pv_pub + 2 <= pv_issued) publish_one(true);
+                while (publish_one(false)) {
+                }
+                mbar_wait(&p_full[sb], (pt >> 1) & 1);
+                TC_T(pt, 3);
+                if (!started) {  // the item's first P V overwrites O: the previous epilogue must be done
+                    if (pvitems > 0) mbar_wait(o_free, (pvitems - 1) & 1);
+                    ++pvitems;
+                }
+                tc_fence_after();
+                const uint64_t vd = vdesc0 + (uint64_t)((pb * kTileBytes) >> 4);
+                const uint32_t pa = tmem + kTmS + sb * kSCols;
                 for (int j = 0; j < pns; ++j)
-                    for (int h = 0; h < 2; ++h)  // k-step = one head's 16 rows of piece j
-                        umma_f16_ts(tmem + kTmO, tmem + kTmS + sb * kSCols + 16 * j + 8 * h,
-                                    umma_desc_sw128(vbase + j * kPair + h * kPiece, kHalfReg, 1024), idesc_o,
-                                    (started || j > 0 || h > 0) ? 1u : 0u);
-                umma_commit(o_done);
-                umma_commit(&tile_empty[pb]);
-            }
-            __syncwarp();
-        };
-        for (uint32_t k = 0;; ++k) {
-            const uint32_t slot = k & 3;
-            mbar_wait(&item_full[slot], (k >> 2) & 1);
-            const int i = *reinterpret_cast<volatile int*>(&item_ring[slot]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&item_empty[slot]);
-            if (i >= p.n_items) break;
-            const uint32_t qb = nitem & 1;
-            bool q_seen = false;
-            bool started = false;
-            int pend_b = -1, pend_ns = 0;
-            uint32_t pend_t = 0;
-            for (;;) {
-                const int b = (int)(tcount % kBuf);
-                mbar_wait(&tile_full[b], (tcount / kBuf) & 1);
-                if (lane == 0) TC_T(tcount, 2);
-                ++tcount;
-                const int ns = *reinterpret_cast<volatile int*>(&meta[b].ns);
-                const int last = *reinterpret_cast<volatile int*>(&meta[b].last);
-                uint32_t t = 0;
-                if (ns > 0) {
-                    if (!q_seen) {  // the softmax warps have put this item's queries in tensor memory
-                        mbar_wait(&q_full[qb], (nitem >> 1) & 1);
-                        q_seen = true;
-                    }
-                    t = scount++;
-                    const uint32_t sb = t & 1;
-                    tc_fence_after();
-                    if (lane == 0) {
-                        const uint32_t idesc_s = umma_idesc(kBF16, false, 32 * ns);
-                        const uint32_t kbase = smem_u32(sT + b * kTileBytes);
 #pragma unroll
-                        for (int kk = 0; kk < 8; ++kk)  // S = Q (tensor memory) x K^T (all pieces, both heads)
-                            umma_f16_ts(tmem + kTmS + sb * kSCols, tmem + kTmQ + 8 * kk,
-                                        umma_desc_sw128(kbase + (kk >> 2) * kHalfReg + (kk & 3) * 32, 16, 1024),
+                    for (int w = 0; w < kNH; ++w)  // k-step = one head's 16 rows of piece j
+                        umma_f16_ts(tmem + kTmO, pa + 8 * kNH * j + 8 * w,
+                                    vd + (uint64_t)((j * kQuad + w * kPiece) >> 4), idesc_o,
+                                    (started || j > 0 || w > 0) ? 1u : 0u);
+                umma_commit(&o_step[pv_issued & 1]);
+                if (last_pv) umma_commit(o_last);
+                umma_commit(&tile_empty[pb]);
+                ++pv_issued;
+            };
+            for (uint32_t k = 0;; ++k) {
+                const uint32_t slot = k & 3;
+                mbar_wait(&item_full[slot], (k >> 2) & 1);
+                const int i = *reinterpret_cast<volatile int*>(&item_ring[slot]);
+                mbar_arrive(&item_empty[slot]);
+                if (i >= p.n_items) break;
+                const uint32_t qb = nitem & 1;
+                bool q_seen = false, started = false;
+                int pend_b = -1, pend_ns = 0;
+                uint32_t pend_t = 0;
+                for (;;) {
+                    const int b = (int)(tcount % kBuf);
+                    mbar_wait(&tile_full[b], (tcount / kBuf) & 1);
+                    TC_T(tcount, 2);
+                    ++tcount;
+                    const int ns = *reinterpret_cast<volatile int*>(&meta[b].ns);
+                    const int last = *reinterpret_cast<volatile int*>(&meta[b].last);
+                    uint32_t t = 0;
+                    if (ns > 0) {
+                        if (!q_seen) {  // the softmax warps have put this item's queries in tensor memory
+                            mbar_wait(&q_full[qb], (nitem >> 1) & 1);
+                            q_seen = true;
+                        }
+                        t = scount++;
+                        const uint32_t sb = t & 1;
+                        tc_fence_after();
+                        const uint32_t idesc_s = umma_idesc(kBF16, false, 16 * kNH * ns);
+                        const uint64_t kd = kdesc0 + (uint64_t)((b * kTileBytes) >> 4);
+                        const uint32_t d = tmem + kTmS + sb * kSCols, qa = tmem + kTmQ + 64 * qb;
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk)  // S = Q (tensor memory) x K^T (all pieces, all heads)
+                            umma_f16_ts(d, qa + 8 * kk, kd + (uint64_t)(((kk >> 2) * kHalfReg + (kk & 3) * 32) >> 4),
                                         idesc_s, kk > 0 ? 1u : 0u);
                         umma_commit(&s_full[sb]);
+                        TC_T(tcount - 1, 7);
                     }
-                    __syncwarp();
+                    if (pend_b >= 0) {
+                        issue_pv(pend_b, pend_t, pend_ns, started, last && ns == 0);
+                        started = true;
+                        pend_b = -1;
+                    }
+                    if (ns > 0) {
+                        pend_b = b;
+                        pend_t = t;
+                        pend_ns = ns;
+                    } else {
+                        umma_commit(&tile_empty[b]);
+                    }
+                    if (last) break;
                 }
-                if (pend_b >= 0) {
-                    issue_pv(pend_b, pend_t, pend_ns, started);
-                    started = true;
-                    pend_b = -1;
-                }
-                if (ns > 0) {
-                    pend_b = b;
-                    pend_t = t;
-                    pend_ns = ns;
-                } else {
-                    if (lane == 0) umma_commit(&tile_empty[b]);
-                    __syncwarp();
-                }
-                if (last) break;
+                if (pend_b >= 0) issue_pv(pend_b, pend_t, pend_ns, started, true);
+                if (!q_seen) mbar_wait(&q_full[qb], (nitem >> 1) & 1);  // keep the q_full phases in step
+                ++nitem;
             }
-            if (pend_b >= 0) issue_pv(pend_b, pend_t, pend_ns, started);
-            if (!q_seen) mbar_wait(&q_full[qb], (nitem >> 1) & 1);  // keep the q_full phases in step
-            ++nitem;
         }
+        __syncwarp();
     } else {
         // ================================================================ softmax ===
-        const int hh = warp >> 1;  // warp 0: head 0 (lanes 0-31), warp 2: head 1 (lanes 64-95)
-        const uint32_t lane_base = (uint32_t)(64 * hh) << 16;
+        const int hh = warp;  // head w of the quad = TMEM lane quadrant w
+        const uint32_t lane_base = (uint32_t)(32 * hh) << 16;
         const uint32_t tO = tmem + lane_base + kTmO;
         const float c2 = p.scale_log2;
         uint32_t tcount = 0, scount = 0, ocount = 0, nq = 0;
@@ -441,7 +462,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             const bool mem = lane < q_it.gmv;  // tcgen05.st is warp-collective: other lanes store zeros
             const uint4* src = reinterpret_cast<const uint4*>(static_cast<const T*>(p.query) +
                                                               ((int64_t)(q_it.s0 + (mem ? lane : 0)) * p.H +
-                                                               (hh ? q_it.h[1] : q_it.h[0])) * 128);
+                                                               sel4(q_it.h, hh)) * 128);
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 uint32_t w0[16], w1[16];
@@ -458,8 +479,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                     w1[4 * c + 2] = v1.z;
                     w1[4 * c + 3] = v1.w;
                 }
-                tmem_st16(tmem + lane_base + kTmQ + 32 * half, w0);
-                tmem_st16(tmem + lane_base + kTmQ + 32 * half + 16, w1);
+                tmem_st16(tmem + lane_base + kTmQ + 64 * (nq & 1) + 32 * half, w0);
+                tmem_st16(tmem + lane_base + kTmQ + 64 * (nq & 1) + 32 * half + 16, w1);
             }
             tmem_st_wait();
             tc_fence_before();
@@ -486,19 +507,45 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             const int ctx = member ? max(0, __ldg(p.context_lens + it.s0 + lane)) : 0;
             float mref = -INFINITY, l = 0.f;
             int npv = 0;
+            bool qnext = false;  // the next item's queries are in the other Q buffer already
+            const uint32_t nslot = (k + 1) & 3, npar = ((k + 1) >> 2) & 1;
             for (;;) {
+                if (!qnext) {  // as soon as the producer has published the next item
+                    int ready = lane == 0 ? (int)mbar_test(&item_full[nslot], npar) : 0;
+                    ready = __shfl_sync(0xffffffffu, ready, 0);
+                    if (ready) {
+                        const int i2 = *reinterpret_cast<volatile int*>(&item_ring[nslot]);
+                        if (i2 < p.n_items) put_q(tc_item(p, i2));
+                        qnext = true;
+                    }
+                }
                 const int b = (int)(tcount % kBuf);
                 mbar_wait(&tile_full[b], (tcount / kBuf) & 1);
                 ++tcount;
                 const int ns = *reinterpret_cast<volatile int*>(&meta[b].ns);
                 const int last = *reinterpret_cast<volatile int*>(&meta[b].last);
-                int vm[kSlots];
+                int vm[kSlots], nr[kSlots];
 #pragma unroll
                 for (int j = 0; j < kSlots; ++j) {
                     const int own = *reinterpret_cast<volatile int*>(&meta[b].own[j]);
                     const int pj = *reinterpret_cast<volatile int*>(&meta[b].p[j]);
+                    nr[j] = j < ns ? *reinterpret_cast<volatile int*>(&meta[b].nrows[j]) : 16;
                     vm[j] = (j < ns && member && ((own >> lane) & 1)) ? min(16, ctx - 16 * pj) : 0;
                 }
+                // V rows past the last context in a piece were loaded from unused cache slots:
+                // zero this head's (P = 0 there, but 0 x NaN = NaN in the product)
+#pragma unroll
+                for (int j = 0; j < kSlots; ++j) {
+                    if (nr[j] < 16) {
+                        unsigned char* vb = sT + b * kTileBytes + kTensor + j * kQuad + hh * kPiece;
+                        for (int u = lane; u < (16 - nr[j]) * 16; u += 32) {
+                            const int row = nr[j] + (u >> 4), half = (u >> 3) & 1, ch = u & 7;
+                            *reinterpret_cast<uint4*>(vb + half * kHalfReg + row * 128 + ch * 16) =
+                                make_uint4(0u, 0u, 0u, 0u);
+                        }
+                    }
+                }
+                fence_proxy_async_smem();  // before the P V product reads them (after p_full)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tile_empty[b]);
                 if (ns > 0) {
@@ -510,7 +557,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                     // this head's 16 columns of every piece (the diagonal block)
                     float sv[kSlots][16];
 #pragma unroll
-                    for (int j = 0; j < kSlots; ++j) tmem_ld16_nw(tS + 32 * j + 16 * hh, sv[j]);
+                    for (int j = 0; j < kSlots; ++j) tmem_ld16_nw(tS + 16 * kNH * j + 16 * hh, sv[j]);
                     tmem_ld_wait();
                     float mt = -INFINITY;
 #pragma unroll
@@ -527,34 +574,39 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                     float rs = 0.f;
 #pragma unroll
                     for (int j = 0; j < kSlots; ++j) {
-                        // packed P of piece j: this head's 8 columns, zeros in the other head's 8
-                        uint32_t pk[16];
+                        // packed P of piece j (8 kNH columns): this head's 8, zeros elsewhere
+                        uint32_t pk[8 * kNH];
 #pragma unroll
                         for (int u = 0; u < 16; u += 2) {
                             const float a0 = u < vm[j] ? ex2(sv[j][u] - ms) : 0.f;
                             const float a1 = u + 1 < vm[j] ? ex2(sv[j][u + 1] - ms) : 0.f;
                             rs += a0 + a1;
                             const uint32_t pv = pack2<T>(a0, a1);
-                            pk[u / 2] = hh ? 0u : pv;
-                            pk[8 + u / 2] = hh ? pv : 0u;
+#pragma unroll
+                            for (int w = 0; w < kNH; ++w) pk[8 * w + u / 2] = hh == w ? pv : 0u;
                         }
-                        tmem_st16(tS + 16 * j, pk);
+                        uint32_t pa[16], pb2[16];
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            pa[u] = pk[u];
+                            pb2[u] = pk[16 + u];
+                        }
+                        tmem_st16(tS + 8 * kNH * j, pa);
+                        tmem_st16(tS + 8 * kNH * j + 16, pb2);
                     }
                     if (lane == 0 && hh == 0) TC_T(t, 5);
-                    if (npv > 0) {  // P V of the previous tile has completed before O is rescaled
-                        mbar_wait(o_done, ocount & 1);
-                        ++ocount;
+                    if (npv > 0 && bump) {  // O is rescaled once P V of the previous tile has completed
+                        while (*pv_done < (int)t - 1) {
+                        }
                         tc_fence_after();
-                        if (bump) {
 #pragma unroll
-                            for (int c0 = 0; c0 < 128; c0 += 32) {
-                                float v[32];
-                                tmem_ld32_nw(tO + c0, v);
-                                tmem_ld_wait();
+                        for (int c0 = 0; c0 < 128; c0 += 32) {
+                            float v[32];
+                            tmem_ld32_nw(tO + c0, v);
+                            tmem_ld_wait();
 #pragma unroll
-                                for (int u = 0; u < 32; ++u) v[u] *= alpha;
-                                tmem_st32(tO + c0, v);
-                            }
+                            for (int u = 0; u < 32; ++u) v[u] *= alpha;
+                            tmem_st32(tO + c0, v);
                         }
                     }
                     l = l * alpha + rs;
@@ -570,21 +622,20 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             // every S of this item has been read: the next item's queries may replace Q now,
             // so the MMA warp can start it while this epilogue runs
             {
-                const uint32_t ns2 = (k + 1) & 3;
-                mbar_wait(&item_full[ns2], ((k + 1) >> 2) & 1);
-                const int i2 = *reinterpret_cast<volatile int*>(&item_ring[ns2]);
-                if (i2 < p.n_items) put_q(tc_item(p, i2));
+                mbar_wait(&item_full[nslot], npar);
+                const int i2 = *reinterpret_cast<volatile int*>(&item_ring[nslot]);
+                if (!qnext && i2 < p.n_items) put_q(tc_item(p, i2));
                 i = i2;
             }
-            // ---- epilogue: out row = O / l; then the new token's K/V row to its cache slot
+            // ---- epilogue: out row = O / l
             if (npv > 0) {
-                mbar_wait(o_done, ocount & 1);
+                mbar_wait(o_last, ocount & 1);  // one phase per item with tiles
                 ++ocount;
                 tc_fence_after();
             }
             const float inv = l > 0.f ? 1.f / l : 0.f;
-            const bool store = member && (hh == 0 || it.st1);
-            T* orow = static_cast<T*>(p.out) + ((int64_t)(it.s0 + lane) * p.H + (hh ? it.h[1] : it.h[0])) * 128;
+            const bool store = member && ((it.st >> hh) & 1u);
+            T* orow = static_cast<T*>(p.out) + ((int64_t)(it.s0 + lane) * p.H + sel4(it.h, hh)) * 128;
 #pragma unroll
             for (int c0 = 0; c0 < 128; c0 += 32) {
                 float v[32];
@@ -611,29 +662,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 tc_fence_before();
                 mbar_arrive(o_free);
             }
-            if (hh == 0 || it.st1) {
-                // reshape_and_cache of the step: member m's new K/V rows of this
-                // head's kv head to slot ctx_m - 1; lane = (K|V, 16-byte chunk)
-                const int t = lane >> 4, ch = lane & 15;
-                const int kvh = hh ? it.kvh[1] : it.kvh[0];
-                for (int m = 0; m < it.gmv; ++m) {
-                    const int cm = __shfl_sync(0xffffffffu, ctx, m);
-                    if (cm <= 0) continue;
-                    const int tp = cm - 1;
-                    const int blk = __ldg(p.block_tables + (int64_t)(it.s0 + m) * p.W + (tp >> p.log2B));
-                    const int64_t dst = ((((int64_t)blk * p.H_kv + kvh) << p.log2B) + (tp & ((1 << p.log2B) - 1))) * 128;
-                    const int64_t src = ((int64_t)(it.s0 + m) * p.H_kv + kvh) * 128;
-                    const uint4 val = __ldg(reinterpret_cast<const uint4*>(
-                                                static_cast<const T*>(t ? p.new_value : p.new_key) + src) +
-                                            ch);
-                    reinterpret_cast<uint4*>(static_cast<T*>(t ? p.value_cache : p.key_cache) + dst)[ch] = val;
-                }
-            }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 3) {
+    if (warp == kMma) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }

@@ -80,9 +80,9 @@ struct AttnParams {
 // Sharing-aware decode on the tcgen05 tensor cores (N1, pa_paged_attention_decode_grouped,
 // pa_decode_tc.cu).  TMA tensor maps are built by the host for every call.
 struct GroupTcParams {
-    CUtensorMap tmap_kp;     // key cache as [NB*H_kv*B rows][D], box {64 cols, 32 rows}: a 16-row
-                             // piece of two adjacent kv heads (consecutive in a block), one half
-    CUtensorMap tmap_vp;     // value cache, same
+    CUtensorMap tmap_kq;     // key cache as [NB*H_kv*B rows][D], box {64 cols, 64 rows}: a 16-row
+                             // piece of four adjacent kv heads (consecutive in a B = 16 block), one half
+    CUtensorMap tmap_vq;     // value cache, same
     CUtensorMap tmap_k[5];   // key cache as [NB*H_kv*B rows][D], boxes {64 cols, 16 >> i rows}, 128-B swizzle
     CUtensorMap tmap_v[5];   // value cache, same
     CUtensorMap tmap_nk;     // the step's new key as [S*H_kv rows][D], box {64, 1}
@@ -100,7 +100,9 @@ struct GroupTcParams {
     float scale_log2;
     int log2B, H, H_kv, G, W, S;
     int GM;                  // sequences per group (<= 8)
-    int n_hp, n_items;       // head pairs, work items = groups x head pairs
+    int n_hp, n_items;       // head quads per group, work items = groups x head quads
+    int n_gorder;            // > 0: work items walk the groups in gorder (pa_decode_plan's order,
+    uint16_t gorder[kMaxSeqOrder];  // by each group's first appearance; scheduling only)
 };
 
 struct GatherParams {

@@ -135,12 +135,25 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t
     return d;
 }
 
+// UMMA shared-memory descriptor, no swizzle (layout type 0): 8-row x 16-byte core matrices
+// stored as 128 contiguous bytes; K-major: LBO = bytes between core matrices adjacent in K,
+// SBO = bytes between core matrices adjacent in M/N.
+__device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+    return d;
+}
+
 // Instruction descriptor, kind::f16: fp32 accumulate, M=128, N=128.
-__host__ __device__ constexpr uint32_t umma_idesc(bool bf16, bool b_mn_major, uint32_t n = 128) {
+__host__ __device__ constexpr uint32_t umma_idesc(bool bf16, bool b_mn_major, uint32_t n = 128,
+                                                  bool a_mn_major = false) {
     return (1u << 4)                        // c_format = F32
            | ((bf16 ? 1u : 0u) << 7)        // a_format
            | ((bf16 ? 1u : 0u) << 10)       // b_format
-           | (0u << 15)                     // a K-major
+           | ((a_mn_major ? 1u : 0u) << 15) // a major
            | ((b_mn_major ? 1u : 0u) << 16) // b major
            | ((n >> 3) << 17)               // N
            | ((128u >> 4) << 24);           // M = 128
@@ -153,6 +166,21 @@ __device__ __forceinline__ void tma_load_4d(void* smem_dst, const CUtensorMap* m
         "[%6];" ::"r"(smem_u32(smem_dst)),
         "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
         : "memory");
+}
+
+// non-blocking: has the phase with the given parity completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// order this thread's generic-proxy global writes before later async-proxy (TMA) reads
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // arm the current phase for `bytes` more transaction bytes without arriving

@@ -206,11 +206,11 @@ def paged_attention_decode_shared(out, query, key, value, key_cache, value_cache
 
 def paged_attention_decode_grouped(out, query, key, value, key_cache, value_cache, block_tables, context_lens,
                                    scale: float, group_size: int, max_context_len: int = 0,
-                                   workspace: torch.Tensor | None = None, stream=None):
-    """The sharing-aware decode step on the tensor cores (pa.h): groups of
-    group_size consecutive sequences; each distinct block of a group is loaded once per
-    logical tile and Q K^T / P V run as MMAs over the group's rows.  f16/bf16, D = 128,
-    block_size >= 16."""
+                                   workspace: torch.Tensor | None = None, stream=None, seq_order=None):
+    """The sharing-aware decode step on the tcgen05 tensor cores (pa.h):
+    groups of group_size consecutive sequences; each distinct block piece of a group is
+    loaded once and Q K^T / P V run as tcgen05 MMAs over the group's rows.  f16/bf16,
+    D = 128, block_size >= 16.  `seq_order`: optional host grid order (decode_plan)."""
     _check(query.dtype, [("block_tables", block_tables), ("context_lens", context_lens)], out=out, query=query,
            key=key, value=value, key_cache=key_cache, value_cache=value_cache)
     S, H, D = query.shape
@@ -225,8 +225,8 @@ def paged_attention_decode_grouped(out, query, key, value, key_cache, value_cach
     _call("pa_paged_attention_decode_grouped", (
         _dev(out, "out"), _dev(query, "query"), _dev(key, "key"), _dev(value, "value"), _dev(key_cache, "key_cache"),
         _dev(value_cache, "value_cache"), _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"),
-        float(scale), B, hk, NB, S, H, D, W, int(mcl), int(group_size), _code(query), ws_ptr, ws_bytes,
-        _stream(stream)))
+        float(scale), B, hk, NB, S, H, D, W, int(mcl), int(group_size), _code(query), _order(seq_order, S), ws_ptr,
+        ws_bytes, _stream(stream)))
     return out
 
 

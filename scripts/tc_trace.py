@@ -47,9 +47,10 @@ for c in range(8):
               "s_seen_to_P_cyc_med(4->5)": float(d(4, 5, ns)),
               "P_to_release_cyc_med(5->6)": float(d(5, 6, ns)),
               "release_to_pv_cyc_med(6->3)": float(d(6, 3, ns)),
-              "s_seen_period_cyc_med": float(np.median(np.diff(t[:ns, 4]))) if ns > 2 else None}
+              "s_seen_period_cyc_med": float(np.median(np.diff(t[:ns, 4]))) if ns > 2 else None,
+              "s_issue_cyc_med(2->7)": float(d(2, 7, n))}
     print(json.dumps({"cta": c, **res[c]}))
 # first 40 tiles of CTA 0, cycles relative to the first stamp
 t0 = tr[0][tr[0] > 0].min()
 for i in range(40):
-    print(i, [int(v - t0) if v > 0 else -1 for v in tr[0, i, :7]])
+    print(i, [int(v - t0) if v > 0 else -1 for v in tr[0, i, :8]])

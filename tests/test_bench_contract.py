@@ -53,13 +53,16 @@ def test_our_arm_contract():
 
 @pytest.mark.gpu
 def test_c5_defaults_to_sharing_aware_decode():
-    """C5 (beam groups of 4) runs the N1 shared kernel by default, coop with --shared 0;
-    the roofline is quoted on unique K/V bytes either way."""
+    """C5 (beam groups of 4) runs the N1 tcgen05 kernel by default, coop with --grouped 0 and
+    the CUDA-core shared kernel with --shared 4; the roofline is quoted on unique K/V bytes
+    either way."""
     common = ("--steps", "5", "--warmup", "3", "--config", "c5_beam", "--no-cpu-baseline", "--no-e2e", "--no-prefill")
     a = run_bench(*common)
-    b = run_bench(*common, "--shared", "0")
-    assert a["config"]["decode_kernel"].startswith("shared4") and b["config"]["decode_kernel"] == "coop"
-    for d in (a, b):
+    b = run_bench(*common, "--grouped", "0")
+    c = run_bench(*common, "--shared", "4")
+    assert a["config"]["decode_kernel"].startswith("grouped4") and b["config"]["decode_kernel"] == "coop"
+    assert c["config"]["decode_kernel"].startswith("shared4")
+    for d in (a, b, c):
         assert d["roofline"]["basis"].startswith("unique") and d["roofline"]["kv_unique_over_logical"] < 0.5
 
 

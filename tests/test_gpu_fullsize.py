@@ -3,7 +3,7 @@ matrix, "attention | oracle fp64 | all").
 
 Every BASELINE.json config at its full size, in the launch configuration bench.py times
 (default partitioning, the cache write fused into the attention kernel; C5 on the
-sharing-aware shared kernel, groups of 4): the WHOLE [S][H][D] output is compared element
+sharing-aware tcgen05 kernel, groups of 4): the WHOLE [S][H][D] output is compared element
 by element with the fp64 oracle, and the caches after the step bit for bit.  The oracle
 runs head slice by head slice (shard(): the same seeded values, generated for that slice
 only) so host memory stays bounded; the oracle inputs come from the seeded generator
@@ -21,8 +21,9 @@ from tests.pathutil import TOL, as_f64, bits
 
 pytestmark = pytest.mark.gpu
 
-# bench.py's default decode entry per config (bench.py run_ours: shared4 on C5, coop elsewhere)
-DEFAULT_SHARED = {"c5_beam": 4}
+# bench.py's default decode entry per config (bench.py run_ours: the tcgen05 grouped kernel in
+# beam groups of 4 on C5, the fused coop decode elsewhere)
+DEFAULT_GROUPED = {"c5_beam": 4}
 CONFIGS = ["c2_sharegpt", "c2_alpaca", "c3_parallel", "c3_fork", "c4_sharegpt", "c4_long", "c5_beam"]
 
 
@@ -34,13 +35,15 @@ def _bench_step(wl):
     if len(wl.block_mapping):
         pa.copy_blocks([kc], [vc], tb["block_mapping"])
     out = torch.empty_like(x["query"])
-    g = DEFAULT_SHARED.get(wl.name, 0)
+    g = DEFAULT_GROUPED.get(wl.name, 0)
+    plan = pa.decode_plan(wl.context_lens)  # bench.py's longest-first grid order
     if g:
-        pa.paged_attention_decode_shared(out, x["query"], x["key"], x["value"], kc, vc, tb["block_tables"],
-                                         tb["context_lens"], wl.scale, g, max_context_len=wl.max_context_len)
+        pa.paged_attention_decode_grouped(out, x["query"], x["key"], x["value"], kc, vc, tb["block_tables"],
+                                          tb["context_lens"], wl.scale, g, max_context_len=wl.max_context_len,
+                                          seq_order=plan)
     else:
         pa.paged_attention_decode(out, x["query"], x["key"], x["value"], kc, vc, tb["block_tables"],
-                                  tb["context_lens"], wl.scale, max_context_len=wl.max_context_len)
+                                  tb["context_lens"], wl.scale, max_context_len=wl.max_context_len, seq_order=plan)
     torch.cuda.synchronize()
     return out, kc, vc
 

@@ -131,3 +131,23 @@ def test_grouped_decode_full_size_full_output(name, gs):
         assert err <= TOL[wl.dtype], (r, err)
         assert np.array_equal(bits(x["key_cache"][:, h0:h0 + sh.H]), kc)
         assert np.array_equal(bits(x["value_cache"][:, h0:h0 + sh.H]), vc)
+
+
+def test_grouped_decode_plan_order_is_scheduling_only():
+    """Walking the groups longest first (pa_decode_plan) changes which CTA computes an item,
+    never a bit of it."""
+    wl = make_config("c5_beam")
+    x0 = materialize_torch(wl, "cuda")
+    tb = tables_torch(wl, "cuda")
+    outs = []
+    for order in (None, pa.decode_plan(wl.context_lens)):
+        x = {k: v.clone() for k, v in x0.items()}
+        if len(wl.block_mapping):
+            pa.copy_blocks([x["key_cache"]], [x["value_cache"]], tb["block_mapping"])
+        out = torch.empty_like(x["query"])
+        pa.paged_attention_decode_grouped(out, x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"],
+                                          tb["block_tables"], tb["context_lens"], wl.scale, 4,
+                                          max_context_len=wl.max_context_len, seq_order=order)
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
