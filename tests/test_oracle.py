@@ -391,6 +391,28 @@ def test_prefill_shared_prefix_suffix_rows_equal_decode():
             assert np.array_equal(out[row], ref[0])
 
 
+def test_prefill_suffix_rows_equal_torch_causal_sdpa_of_the_whole_sequence():
+    """The suffix offset (reading c22: row i of a q_len-token suffix sits at position
+    ctx - q_len + i) pinned to a library routine, not to the oracle's own formula: the
+    suffix rows equal the LAST q_len rows of torch's causal scaled_dot_product_attention
+    over the whole ctx-token sequence (in fp64), whose earlier query rows are arbitrary."""
+    torch = pytest.importorskip("torch")
+    r = rng(33)
+    H, H_kv, D, B = 4, 2, 16, 8
+    ctxs, qlens = [50, 21, 9], [7, 21, 1]
+    Q, kc, vc, bt, cl, qs, Ks, Vs = _prefill_case(r, ctxs, qlens, H, H_kv, D, B)
+    scale = 0.27
+    out = oracle.prefill_attention(Q.view(np.uint32), kc.view(np.uint32), vc.view(np.uint32), bt, cl, qs,
+                                   scale, B, H_kv, "f32")
+    for s, (c, n) in enumerate(zip(ctxs, qlens)):
+        qfull = np.concatenate([r.uniform(-1, 1, (c - n, H, D)), Q[qs[s]:qs[s + 1]].astype(np.float64)])
+        q = torch.from_numpy(qfull).permute(1, 0, 2)  # [H][c][D]
+        k = torch.from_numpy(Ks[s].astype(np.float64)).permute(1, 0, 2).repeat_interleave(H // H_kv, 0)
+        v = torch.from_numpy(Vs[s].astype(np.float64)).permute(1, 0, 2).repeat_interleave(H // H_kv, 0)
+        ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, scale=scale)
+        np.testing.assert_allclose(out[qs[s]:qs[s + 1]], ref.permute(1, 0, 2).numpy()[c - n:], rtol=0, atol=1e-13)
+
+
 def test_prefill_first_prompt_row_is_v0_and_block_invariance():
     """Row 0 of a prompt attends to exactly one token: out = v_0 (closed form).  The
     result does not depend on block size or placement, bitwise."""
