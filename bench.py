@@ -131,6 +131,9 @@ def parse():
                     help="rotated layer caches (0 = auto: R x K/V read per step >= 4 x L2, R >= 2)")
     ap.add_argument("--no-plan", action="store_true",
                     help="natural grid order instead of pa_decode_plan's longest-first order (coop decode)")
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="run rank 0's head shard of a P-way tensor-parallel split on this one GPU (no exchange): "
+                         "the per-rank kernel time of TP=P, a scaling proxy on a single-GPU box")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-prefill", action="store_true", help="skip the N4 prompt-phase context line")
     ap.add_argument("--extra", action="store_true", help="also print per-config lines for the other configs")
@@ -232,7 +235,9 @@ def run_ours(a, wl_full, world, rank, local):
     torch.cuda.set_device(dev)
     props = torch.cuda.get_device_properties(dev)
     l2_bytes = int(getattr(props, "L2_cache_size", 0) or 126 * (1 << 20))
-    wl = shard(wl_full, rank, world) if world > 1 else wl_full
+    if a.shard_of > 1 and world > 1:
+        raise SystemExit("--shard-of simulates one rank on one GPU; run it without torchrun")
+    wl = shard(wl_full, rank, world) if world > 1 else (shard(wl_full, 0, a.shard_of) if a.shard_of > 1 else wl_full)
     tb = tables_torch(wl, dev)
     bt, cl, sm, bm = tb["block_tables"], tb["context_lens"], tb["slot_mapping"], tb["block_mapping"]
     # R layer caches rotated step by step, so consecutive steps never re-read a cache that
@@ -263,7 +268,12 @@ def run_ours(a, wl_full, world, rank, local):
                     raise
                 tp_gather = f"nccl (fused setup failed: {type(exc).__name__}: {exc})"
     has_pairs = len(wl.block_mapping) > 0
+    # the tcgen05 N1 kernel's persistent CTAs need work items (group, 4 heads) for at least two
+    # rounds over the SMs; a TP=8 shard of C5 (12 heads per rank) has too few and runs coop
+    # (measured: profiles/r02_tp_shard_tune.jsonl)
     auto_grouped = {"c5_beam": 4}.get(wl_full.name, 0)
+    if auto_grouped and (wl.S // auto_grouped) * ((wl.H + 3) // 4) < 2 * props.multi_processor_count:
+        auto_grouped = 0
     grouped = a.grouped if a.grouped >= 0 else auto_grouped
     if a.shared > 0 or ftp is not None or a.unfused:
         grouped = 0 if a.grouped < 0 else grouped
@@ -395,7 +405,7 @@ def run_ours(a, wl_full, world, rank, local):
     if rank != 0:
         return
     peak, peak_src = load_peaks()
-    kv_all = wl_full.logical_kv_bytes()
+    kv_all = wl_full.logical_kv_bytes() if a.shard_of <= 1 else wl.logical_kv_bytes()
     sb = wl.step_bytes()
     # per launch of the attention call on this rank: K/V read + q/out + tables (+ the fused new-token write)
     attn_bytes = sb["kv_logical"] + sb["q_out"] + sb["tables"] + (0 if a.unfused else sb["cache_write"] // 2)
@@ -410,8 +420,9 @@ def run_ours(a, wl_full, world, rank, local):
     value = kv_all / (ms_step * 1e-3) / 1e9
     ach = achieved_u if shared else achieved
     # ncu_traffic.json keys: the workload for its default kernel, _grouped / _coop otherwise
-    traffic = load_traffic(wl_full.name + ("" if grouped == auto_grouped and not shared_g else "_grouped" if grouped
-                                           else "_shared" if shared_g else "_coop"), world)
+    default_kernel = grouped == auto_grouped and not shared_g
+    traffic = None if a.shard_of > 1 else load_traffic(
+        wl_full.name + ("" if default_kernel else "_grouped" if grouped else "_shared" if shared_g else "_coop"), world)
     read_kv = min(kv_unique, sb["kv_logical"])
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
@@ -421,7 +432,8 @@ def run_ours(a, wl_full, world, rank, local):
         "config": {"workload": wl_full.name, "seqs": wl_full.S, "heads": wl_full.H, "kv_heads": wl_full.H_kv,
                    "head_dim": wl_full.D, "block_size": wl_full.B, "kv_dtype": wl_full.dtype,
                    "mean_ctx": float(wl_full.context_lens.mean()), "max_ctx": int(wl_full.max_context_len),
-                   "cow_pairs": int(len(wl_full.block_mapping)), "parallelism": f"tp{world}",
+                   "cow_pairs": int(len(wl_full.block_mapping)), "parallelism": (f"tp{world}" if a.shard_of <= 1 else
+                                   f"rank 0 of tp{a.shard_of}, simulated on one GPU (no exchange)"),
                    "tp_gather": tp_gather,
                    "decode_kernel": (f"grouped{grouped} (N1, tensor cores)" if grouped else
                                      f"shared{shared_g} (N1, CUDA cores)" if shared_g else "coop"),

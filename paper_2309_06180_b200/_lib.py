@@ -46,6 +46,7 @@ _sig("pa_paged_attention_decode_shared", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _v
                                                 _i32, _i32, _i32, _i32, _i32, _vp, _sz, _vp])
 _sig("pa_paged_attention_decode_grouped", _i32, [_vp] * 8 + [_f32] + [_i32] * 10 + [_vp, _vp, _sz, _vp])
 _sig("pa_paged_prefill_attention", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32] + [_i32] * 10 + [_vp, _sz, _vp])
+_sig("pa_paged_prefill_attention_packed", _i32, [_vp] * 10 + [_f32] + [_i32] * 10 + [_vp, _sz, _vp])
 _sig("pa_paged_attention_workspace_size", _sz, [_i32, _i32, _i32, _i32, _i32])
 _sig("pa_reshape_and_cache", _i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp])
 _sig("pa_copy_blocks", _i32, [ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i32, _vp, _i32, _i32, _i32, _i32, _i32,

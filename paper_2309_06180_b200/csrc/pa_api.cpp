@@ -570,13 +570,13 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
     return PA_OK;
 }
 
-pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void* key_cache, const void* value_cache,
+static pa_status_t prefill_impl(void* out, const void* query, const void* key_cache, const void* value_cache,
                                        const int32_t* block_tables, const int32_t* context_lens,
                                        const int32_t* query_start, float scale, int block_size, int num_kv_heads,
                                        int num_blocks, int num_seqs, int num_heads, int head_dim,
                                        int max_blocks_per_seq, int num_query_tokens, int max_query_len,
                                        pa_dtype_t dtype, void* workspace, size_t workspace_bytes,
-                                       pa_stream_t stream) {
+                                       pa_stream_t stream, const pa::PackTable* pack = nullptr) {
     REQUIRE(valid_dtype(dtype), "unknown dtype %d", (int)dtype);
     if (dtype == PA_F32) return fail(PA_ERR_UNSUPPORTED, "prefill attention supports f16 and bf16 only");
     if (head_dim != 128) return fail(PA_ERR_UNSUPPORTED, "prefill attention supports head_dim 128 only (got %d)", head_dim);
@@ -625,6 +625,13 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
             !encode_map(&p.tmap_k1, dt, 2, key_cache, dims, str, box1) ||
             !encode_map(&p.tmap_v1, dt, 2, value_cache, dims, str, box1))
             return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the cache maps");
+        if (pack != nullptr)
+            for (int i = 0; i < 3; ++i) {  // 8/4/2-row boxes for the packed kernel's partial pieces
+                const cuuint32_t boxr[2] = {64, (cuuint32_t)(8 >> i)};
+                if (!encode_map(&p.tmap_kr[i], dt, 2, key_cache, dims, str, boxr) ||
+                    !encode_map(&p.tmap_vr[i], dt, 2, value_cache, dims, str, boxr))
+                    return fail(PA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the cache maps");
+            }
     }
     p.out = out;
     p.block_tables = block_tables;
@@ -636,9 +643,93 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
     p.H_kv = num_kv_heads;
     p.G = num_heads / num_kv_heads;
     p.W = max_blocks_per_seq;
-    cudaError_t e = pa::launch_prefill(p, (int)dtype, num_seqs, max_query_len, tuning().prefill, (cudaStream_t)stream);
+    cudaError_t e = pack != nullptr
+                        ? pa::launch_prefill_packed(p, *pack, (int)dtype, (cudaStream_t)stream)
+                        : pa::launch_prefill(p, (int)dtype, num_seqs, max_query_len, tuning().prefill,
+                                             (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "paged_prefill_kernel launch");
     return PA_OK;
+}
+
+pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void* key_cache, const void* value_cache,
+                                       const int32_t* block_tables, const int32_t* context_lens,
+                                       const int32_t* query_start, float scale, int block_size, int num_kv_heads,
+                                       int num_blocks, int num_seqs, int num_heads, int head_dim,
+                                       int max_blocks_per_seq, int num_query_tokens, int max_query_len,
+                                       pa_dtype_t dtype, void* workspace, size_t workspace_bytes,
+                                       pa_stream_t stream) {
+    g_err.clear();
+    return prefill_impl(out, query, key_cache, value_cache, block_tables, context_lens, query_start, scale,
+                        block_size, num_kv_heads, num_blocks, num_seqs, num_heads, head_dim, max_blocks_per_seq,
+                        num_query_tokens, max_query_len, dtype, workspace, workspace_bytes, stream);
+}
+
+pa_status_t pa_paged_prefill_attention_packed(
+    void* out, const void* query, const void* key_cache, const void* value_cache, const int32_t* block_tables,
+    const int32_t* context_lens, const int32_t* query_start, const int32_t* host_query_start,
+    const int32_t* host_context_lens, const int32_t* host_shared_prefix, float scale, int block_size,
+    int num_kv_heads, int num_blocks, int num_seqs, int num_heads, int head_dim, int max_blocks_per_seq,
+    int num_query_tokens, int max_query_len, pa_dtype_t dtype, void* workspace, size_t workspace_bytes,
+    pa_stream_t stream) {
+    g_err.clear();
+    REQUIRE(num_seqs >= 0, "num_seqs must be >= 0");
+    REQUIRE(num_seqs == 0 || (host_query_start && host_context_lens && host_shared_prefix),
+            "host_query_start / host_context_lens / host_shared_prefix are NULL");
+    // Pack consecutive sequences into query tiles of <= 128 rows that share a cached prefix
+    // P (a multiple of the block size, <= every member's first query position): greedy, in
+    // order, a member joining while the tile stays <= 128 rows and its packed own-token
+    // columns (sum of ctx - P) stay <= 256 (two key tiles).  A query longer than 128 rows
+    // takes ceil(q_len / 128) tiles of its own.  Falls back to the per-sequence kernels
+    // when the block size is below 16 or the table would overflow.
+    static thread_local pa::PackTable t;
+    bool ok = block_size >= 16 && num_seqs > 0;
+    t.n_tiles = 0;
+    auto add_tile = [&](int s0, int nm, int P, int r0) {
+        if (t.n_tiles == pa::kMaxPackTiles) return false;
+        t.s0[t.n_tiles] = s0;
+        t.nm[t.n_tiles] = (uint16_t)nm;
+        t.P[t.n_tiles] = P;
+        t.r0[t.n_tiles] = (uint16_t)r0;
+        ++t.n_tiles;
+        return true;
+    };
+    for (int s = 0; ok && s < num_seqs;) {
+        const int q0 = host_query_start[s + 1] - host_query_start[s];
+        REQUIRE(q0 >= 0 && q0 <= host_context_lens[s], "sequence %d: q_len %d must be in [0, ctx %d]", s, q0,
+                host_context_lens[s]);
+        const int P0 = ((host_context_lens[s] - q0) / block_size) * block_size;
+        if (q0 > 128) {  // a long query: its own tiles of 128 rows
+            REQUIRE(q0 < 65536 + 128, "q_len %d too long for the packed table", q0);
+            for (int r0 = 0; ok && r0 < q0; r0 += 128) ok = add_tile(s, 1, P0, r0);
+            ++s;
+            continue;
+        }
+        int rows = q0, P = P0, e = s + 1;
+        int64_t cols = host_context_lens[s] - P0;
+        while (e < num_seqs) {
+            const int qe = host_query_start[e + 1] - host_query_start[e];
+            REQUIRE(qe >= 0 && qe <= host_context_lens[e], "sequence %d: q_len %d must be in [0, ctx %d]", e, qe,
+                    host_context_lens[e]);
+            if (qe > 128 || rows + qe > 128 || e - s >= 128) break;
+            const int Pe = std::min({P, (host_shared_prefix[e] / block_size) * block_size,
+                                     ((host_context_lens[e] - qe) / block_size) * block_size});
+            const int64_t cols_e = cols + (int64_t)(e - s) * (P - Pe) + (host_context_lens[e] - Pe);
+            if (cols_e > 256) break;
+            rows += qe;
+            cols = cols_e;
+            P = Pe;
+            ++e;
+        }
+        ok = add_tile(s, e - s, P, 0);
+        s = e;
+    }
+    if (!ok)
+        return prefill_impl(out, query, key_cache, value_cache, block_tables, context_lens, query_start, scale,
+                            block_size, num_kv_heads, num_blocks, num_seqs, num_heads, head_dim, max_blocks_per_seq,
+                            num_query_tokens, max_query_len, dtype, workspace, workspace_bytes, stream);
+    return prefill_impl(out, query, key_cache, value_cache, block_tables, context_lens, query_start, scale,
+                        block_size, num_kv_heads, num_blocks, num_seqs, num_heads, head_dim, max_blocks_per_seq,
+                        num_query_tokens, max_query_len, dtype, workspace, workspace_bytes, stream, &t);
 }
 
 // ---- N2: fused tensor-parallel all-gather ------------------------------------------------

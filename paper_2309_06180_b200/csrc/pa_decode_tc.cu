@@ -34,8 +34,14 @@ using namespace tc;
 
 namespace {
 constexpr int kNH = 4;                      // query heads per work item (one TMEM lane quadrant each)
-constexpr int kSlots = 2;                   // 16-row block pieces per MMA tile
-constexpr int kBuf = 3;                     // tile buffers in shared memory
+#ifndef PA_TC_SLOTS
+#define PA_TC_SLOTS 2
+#endif
+#ifndef PA_TC_BUF
+#define PA_TC_BUF 3
+#endif
+constexpr int kSlots = PA_TC_SLOTS;         // 16-row block pieces per MMA tile
+constexpr int kBuf = PA_TC_BUF;             // tile buffers in shared memory
 constexpr int kPiece = 16 * 128;            // [16 rows][64 cols] swizzled, 2-byte elements
 constexpr int kQuad = kNH * kPiece;         // one piece, the item's kv heads stacked: [64 rows][128 B] = 8 KB
 constexpr int kHalfReg = kSlots * kQuad;    // one 64-column half of the tile: 16 KB

@@ -20,6 +20,8 @@ struct PrefillParams {
     CUtensorMap tmap_v;           // value cache, same
     CUtensorMap tmap_k1;          // key cache, box {64, 1} (tails shorter than box_rows)
     CUtensorMap tmap_v1;          // value cache, box {64, 1}
+    CUtensorMap tmap_kr[3];       // key cache, boxes {64, 8 >> i} (packed kernel: partial pieces)
+    CUtensorMap tmap_vr[3];       // value cache, same
     void* out;                    // [T][H][D]
     const int32_t* block_tables;  // [S][W]
     const int32_t* context_lens;  // [S]
@@ -29,6 +31,20 @@ struct PrefillParams {
     int box_rows;                 // min(block_size, 128) tokens per TMA box
     int X, S;                     // query-tile pairs per sequence (grid of work items), sequences
     int* work_counter;            // v2: dynamic work-item counter (zeroed on the stream by the launcher)
+};
+
+// Packed prompt-phase work (N4, pa_paged_prefill_attention_packed): query tile t holds <= 128
+// query rows of sequences s0[t] .. s0[t] + nm[t] - 1 (consecutive), starting at row r0[t] of
+// the first (r0 > 0 only when one long query spans several tiles), which share their first
+// P[t] cached tokens (the same physical blocks; P a multiple of the block size, at most
+// every member's first query position).
+constexpr int kMaxPackTiles = 1024;
+struct PackTable {
+    int n_tiles;
+    int s0[kMaxPackTiles];
+    int P[kMaxPackTiles];
+    uint16_t nm[kMaxPackTiles];
+    uint16_t r0[kMaxPackTiles];
 };
 
 constexpr int kMaxTpPeers = 8;
@@ -177,6 +193,7 @@ cudaError_t launch_group_tc(const GroupTcParams& p, int dtype, cudaStream_t stre
 // variant: 0 = by max_query_len (default), 2 / 3 = force (PA_PREFILL ablation)
 cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, int variant,
                            cudaStream_t stream);
+cudaError_t launch_prefill_packed(const PrefillParams& p, const PackTable& t, int dtype, cudaStream_t stream);
 // N2: rank `rank` publishes `epoch` to every peer's flag array, then waits (bounded) until
 // every peer has published it to this rank; status = 1 on timeout
 cudaError_t launch_tp_signal_wait(int32_t* const* flag_peers, int world, int rank, int32_t epoch, int32_t* status,

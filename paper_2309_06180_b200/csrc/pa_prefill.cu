@@ -851,6 +851,467 @@ size_t prefill_split_smem_bytes() {
 
 size_t prefill_ws_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 26 * 8 + 4 * 4 + 16; }
 
+// ---- v6: packed shared-prefix suffixes (pa_paged_prefill_attention_packed) --------------
+// Work item = (packed query tile t, head h), heads outermost so the CTAs running together
+// read one head's shared prefix (it stays in L2).  The tile's 128 query rows are the rows
+// of nm consecutive sequences (each <= 128 rows) that share their first P cached tokens,
+// so the shared prefix is attended ONCE for all of them (cascade): K/V tiles 0..n_pre-1 are
+// the prefix tokens [0, P) (every row sees every column), then n_suf tiles pack the
+// members' own tokens [P, ctx_k) back to back (member k at packed columns [col_k, col_k +
+// ctx_k - P)); a row of member k at position pos sees the contiguous packed columns
+// [col_k, col_k + pos - P + 1) -- its causal range inside its own segment.
+// Otherwise the v3 pipeline: one query tile, softmax split by key columns over two warp
+// groups, S double-buffered in tensor memory, K / V in two stages each.  The producer
+// publishes each item's member table (row offset, context, packed column offset, piece
+// offset) in shared memory for the softmax warps.
+constexpr int kMaxMem = 128;
+struct PackMem {
+    int row_off, ctx, col_off, piece_off, qlen;
+};
+
+__device__ __forceinline__ void packed_item(const PackTable& t, const PrefillParams& p, int i, int& tile, int& h,
+                                            int& s0, int& nm, int& P, int& r0) {
+    tile = i % t.n_tiles;
+    h = i / t.n_tiles;
+    s0 = t.s0[tile];
+    nm = t.nm[tile];
+    P = t.P[tile];
+    r0 = t.r0[tile];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreadsV2, 1)
+    paged_prefill_packed_kernel(const __grid_constant__ PrefillParams p, const __grid_constant__ PackTable pt) {
+    constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* sQ = smem;                          // [2 buffers][2 halves][128][64]
+    unsigned char* sK = smem + 4 * kHalf;              // [2 stages][2 halves][128][64]
+    unsigned char* sV = sK + 2 * kKStages * kHalf;     // [2 stages][2 halves][128][64]
+    float* red = reinterpret_cast<float*>(sV + 2 * kVStages * kHalf);  // [2 parity][2 groups][128] row maxima
+    float* lsum = red + 512;                                            // [2 groups][128] row sums
+    PackMem* mem = reinterpret_cast<PackMem*>(lsum + 256);              // [2 parity][kMaxMem + 1]
+    int* mhdr = reinterpret_cast<int*>(mem + 2 * (kMaxMem + 1));       // [2 parity][4]: rows, C, n_pre, n
+    uint64_t* bars = reinterpret_cast<uint64_t*>(mhdr + 8);
+    uint64_t* q_full = bars;                 // 2
+    uint64_t* q_empty = bars + 2;            // 2
+    uint64_t* k_full = bars + 4;             // 2
+    uint64_t* k_empty = bars + 6;            // 2
+    uint64_t* v_full = bars + 8;             // 2
+    uint64_t* v_empty = bars + 10;           // 2
+    uint64_t* s_full = bars + 12;            // 2 (per S buffer)
+    uint64_t* p_full = bars + 14;            // 1
+    uint64_t* o_done = bars + 15;            // 1
+    uint64_t* o_free = bars + 16;            // 1
+    uint64_t* m_full = bars + 17;            // 2: member table published (producer)
+    uint64_t* m_empty = bars + 19;           // 2: member table read (8 softmax warps + MMA warp)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n_items = pt.n_tiles * p.H;
+    pdl_wait();
+
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&m_full[i], 1);
+            mbar_init(&m_empty[i], 9);
+        }
+        mbar_init(p_full, 2 * kQ);
+        mbar_init(o_done, 1);
+        mbar_init(o_free, 2 * kQ);
+        fence_mbar_init();
+    }
+    // V stages start zeroed: columns of a last tile past its tokens are never loaded
+    for (int i = tid; i < 2 * kVStages * kHalf / 16; i += kThreadsV2)
+        reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+    if (warp == 0) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int B = 1 << p.log2B;
+
+    if (warp == 8) {
+        // ---------------- TMA producer ----------------
+        const int br = p.box_rows;
+        uint32_t g = 0, nq = 0;
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++nq) {
+            int tile, h, s0, nm, P, r0;
+            packed_item(pt, p, i, tile, h, s0, nm, P, r0);
+            const int kvh = h / p.G;
+            const int qb = nq & 1;
+            // ---- member table of this item (double-buffered by item parity)
+            if (nq >= 2) mbar_wait(&m_empty[qb], ((nq - 2) >> 1) & 1);
+            PackMem* mt = mem + qb * (kMaxMem + 1);
+            const int qs0 = __ldg(p.query_start + s0) + r0;
+            int col = 0, pcs = 0;
+            for (int k0 = 0; k0 < nm; k0 += 32) {
+                const int k = k0 + lane;
+                int len = 0, np = 0, ro = 0, cx = 0, ql = 0;
+                if (k < nm) {
+                    const int a0 = __ldg(p.query_start + s0 + k);
+                    ro = a0 - qs0;
+                    ql = __ldg(p.query_start + s0 + k + 1) - a0;
+                    cx = __ldg(p.context_lens + s0 + k);
+                    len = cx - P;
+                    np = (len + 15) >> 4;
+                }
+                int il = len, ip = np;  // inclusive scans over the lanes
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int a = __shfl_up_sync(0xffffffffu, il, off), b2 = __shfl_up_sync(0xffffffffu, ip, off);
+                    if (lane >= off) {
+                        il += a;
+                        ip += b2;
+                    }
+                }
+                if (k < nm) mt[k] = PackMem{ro, cx, col + il - len, pcs + ip - np, ql};
+                col += __shfl_sync(0xffffffffu, il, 31);
+                pcs += __shfl_sync(0xffffffffu, ip, 31);
+            }
+            const int rows = min(kQ, __ldg(p.query_start + s0 + nm) - qs0);
+            __syncwarp();
+            {   // packed columns the tile's rows can see: the last member's causal range ends
+                // at its last row in this tile (a long query spans several tiles)
+                const PackMem ml = mt[nm - 1];
+                const int pos_max = ml.ctx - ml.qlen + (rows - 1 - ml.row_off);
+                col = ml.col_off + min(ml.ctx - P, pos_max - P + 1);
+            }
+            const int n_pre = (P + kN - 1) / kN, n_suf = (col + kN - 1) / kN, n = n_pre + n_suf;
+            if (lane == 0) {
+                mt[nm] = PackMem{rows, 0, col, pcs, 0};
+                mhdr[qb * 4 + 0] = rows;
+                mhdr[qb * 4 + 1] = col;
+                mhdr[qb * 4 + 2] = n_pre;
+                mhdr[qb * 4 + 3] = n;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&m_full[qb]);  // release: the table writes above
+            // ---- query tile
+            if (nq >= 2) mbar_wait(&q_empty[qb], ((nq - 2) >> 1) & 1);
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&q_full[qb], 2u * kHalf);
+                tma_load_3d(sQ + qb * 2 * kHalf, &p.tmap_q, 0, h, qs0, &q_full[qb]);
+                tma_load_3d(sQ + qb * 2 * kHalf + kHalf, &p.tmap_q, 64, h, qs0, &q_full[qb]);
+            }
+            __syncwarp();
+            const int32_t* bt0 = p.block_tables + (int64_t)s0 * p.W;
+            for (int j = 0; j < n; ++j, ++g) {
+                const uint32_t ks = g % kKStages, vs = g & 1;
+                for (int tsr = 0; tsr < 2; ++tsr) {  // K then V
+                    uint64_t* bar = tsr ? &v_full[vs] : &k_full[ks];
+                    if (tsr == 0 && g >= kKStages) mbar_wait(&k_empty[ks], ((g - kKStages) / kKStages) & 1);
+                    if (tsr == 1 && g >= 2) mbar_wait(&v_empty[vs], ((g - 2) >> 1) & 1);
+                    unsigned char* dst0 = tsr ? sV + vs * 2 * kHalf : sK + ks * 2 * kHalf;
+                    const CUtensorMap* map = tsr ? &p.tmap_v : &p.tmap_k;
+                    const CUtensorMap* map1 = tsr ? &p.tmap_v1 : &p.tmap_k1;
+                    if (j < n_pre) {
+                        // shared prefix tokens [128 j, min(P, 128 j + 128)) through s0's table
+                        const int t0 = j * kN, len = min(P, t0 + kN) - t0;
+                        const int nf = len / br, nb = nf + len % br;
+                        if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
+                        __syncwarp();
+                        for (int b2 = lane; b2 < nb; b2 += 32) {
+                            const int tt = t0 + (b2 < nf ? b2 * br : nf * br + (b2 - nf));
+                            const int blk = __ldg(bt0 + (tt >> p.log2B));
+                            const int row = (blk * p.H_kv + kvh) * B + (tt & (B - 1));
+                            const int off = (tt - t0) * 128;
+                            const CUtensorMap* m = b2 < nf ? map : map1;
+                            tma_load_2d(dst0 + off, m, 0, row, bar);
+                            tma_load_2d(dst0 + kHalf + off, m, 64, row, bar);
+                        }
+                    } else {
+                        // packed members' own tokens: packed columns [c_lo, c_hi) of this tile;
+                        // lane = one 16-token piece of one member (pieces are block-aligned
+                        // because P is), split into single rows where it crosses the tile
+                        const int c_lo = (j - n_pre) * kN, c_hi = min(col, c_lo + kN);
+                        if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(c_hi - c_lo) * 256u);
+                        __syncwarp();
+                        for (int gp = lane; gp < pcs; gp += 32) {
+                            int lo = 0, hi = nm - 1;  // member k of piece gp: last piece_off <= gp
+                            while (lo < hi) {
+                                const int mid = (lo + hi + 1) >> 1;
+                                if (mt[mid].piece_off <= gp) lo = mid; else hi = mid - 1;
+                            }
+                            const PackMem mk = mt[lo];
+                            const int q = gp - mk.piece_off;
+                            const int len_k = mk.ctx - P;
+                            const int pc0 = mk.col_off + 16 * q, pc1 = mk.col_off + min(16 * q + 16, len_k);
+                            const int a = max(pc0, c_lo), b3 = min(pc1, c_hi);
+                            if (a >= b3) continue;
+                            const int tt0 = P + 16 * q;  // first token of the piece
+                            const int blk = __ldg(p.block_tables + (int64_t)(s0 + lo) * p.W + (tt0 >> p.log2B));
+                            const int row0 = (blk * p.H_kv + kvh) * B + (tt0 & (B - 1));
+                            if (a == pc0 && b3 == pc1 && pc1 - pc0 == 16 && br == 16) {
+                                tma_load_2d(dst0 + (a - c_lo) * 128, map, 0, row0, bar);
+                                tma_load_2d(dst0 + kHalf + (a - c_lo) * 128, map, 64, row0, bar);
+                            } else {
+                                // rows [a, b3) of the piece as 8-row boxes, then 4/2/1
+                                int c = a;
+                                for (int rb = 8, mi = 0; rb >= 1; rb >>= 1, ++mi) {
+                                    const CUtensorMap* mr = rb == 1 ? map1 : (tsr ? &p.tmap_vr[mi] : &p.tmap_kr[mi]);
+                                    while (b3 - c >= rb && (rb == 8 || ((b3 - c) & rb))) {
+                                        tma_load_2d(dst0 + (c - c_lo) * 128, mr, 0, row0 + (c - pc0), bar);
+                                        tma_load_2d(dst0 + kHalf + (c - c_lo) * 128, mr, 64, row0 + (c - pc0), bar);
+                                        c += rb;
+                                    }
+                                }
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else if (warp == 9) {
+        // ---------------- MMA issuer (as v3) ----------------
+        const uint32_t idesc_s = umma_idesc(kBF16, false), idesc_o = umma_idesc(kBF16, true);
+        uint32_t gk = 0, gv = 0, nq = 0, np = 0, nf = 0;
+        auto issue_S = [&](uint32_t qb) {  // S(gk) = Q K(gk)^T into S buffer gk & 1
+            const uint32_t ks = gk % kKStages;
+            mbar_wait(&k_full[ks], (gk / kKStages) & 1);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t q = smem_u32(sQ) + qb * 2 * kHalf, k = smem_u32(sK) + ks * 2 * kHalf;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+                    umma_f16(tmem + (gk & 1) * 128, umma_desc_sw128(q + off, 16, 1024),
+                             umma_desc_sw128(k + off, 16, 1024), idesc_s, kk > 0);
+                }
+                umma_commit(&s_full[gk & 1]);
+                umma_commit(&k_empty[ks]);
+            }
+            __syncwarp();
+            ++gk;
+        };
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+            const uint32_t qb = nq & 1;
+            mbar_wait(&m_full[qb], (nq >> 1) & 1);
+            const int n = *reinterpret_cast<volatile int*>(&mhdr[qb * 4 + 3]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&m_empty[qb]);
+            mbar_wait(&q_full[qb], (nq >> 1) & 1);
+            ++nq;
+            for (int j = 0; j < min(n, 2); ++j) issue_S(qb);
+            if (n <= 2 && lane == 0) umma_commit(&q_empty[qb]);
+            if (n > 0 && nf++ > 0) mbar_wait(o_free, (nf - 2) & 1);
+            for (int j = 0; j < n; ++j) {
+                mbar_wait(&v_full[gv & 1], (gv >> 1) & 1);
+                mbar_wait(p_full, np++ & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t v = smem_u32(sV) + (gv & 1) * 2 * kHalf;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        umma_f16_ts(tmem + 256, tmem + (gv & 1) * 128 + kk * 8,
+                                    umma_desc_sw128(v + kk * 2048, kHalf, 1024), idesc_o, (j > 0) | (kk > 0));
+                    umma_commit(o_done);
+                    umma_commit(&v_empty[gv & 1]);
+                }
+                __syncwarp();
+                ++gv;
+                if (j + 2 < n) {
+                    issue_S(qb);
+                    if (j + 3 == n && lane == 0) umma_commit(&q_empty[qb]);
+                }
+            }
+        }
+    } else {
+        // ---------------- softmax warp groups (column halves) ----------------
+        const int hf = warp >> 2;
+        const int r = tid & (kQ - 1);
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t tO = tmem + 256 + hf * 64 + lane_off;
+        uint32_t ns = 0, nq = 0;
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++nq) {
+            int tile, h, s0, nm, P, r0;
+            packed_item(pt, p, i, tile, h, s0, nm, P, r0);
+            const uint32_t qb = nq & 1;
+            mbar_wait(&m_full[qb], (nq >> 1) & 1);
+            const PackMem* mt = mem + qb * (kMaxMem + 1);
+            const int rows = mhdr[qb * 4 + 0], n_pre = mhdr[qb * 4 + 2], n = mhdr[qb * 4 + 3];
+            // this row's member (last row_off <= r), its position and packed segment
+            const bool row_valid = r < rows;
+            int k = 0;
+            {
+                int lo = 0, hi = nm - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (mt[mid].row_off <= r) lo = mid; else hi = mid - 1;
+                }
+                k = lo;
+            }
+            const PackMem mk = mt[k];
+            const int pos = mk.ctx - mk.qlen + (r - mk.row_off);
+            const int seg_hi = mk.col_off + (pos - P) + 1;  // packed columns [col_off, seg_hi)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&m_empty[qb]);  // the table is read (the item's values are in registers)
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < n; ++j, ++ns) {
+                const uint32_t b = ns & 1;
+                const uint32_t tS = tmem + b * 128 + lane_off;
+                mbar_wait(&s_full[b], (ns >> 1) & 1);
+                tc_fence_after();
+                float sa[32], sb[32];
+                tmem_ld32_nw(tS + hf * 64, sa);
+                tmem_ld32_nw(tS + hf * 64 + 32, sb);
+                tmem_ld_wait();
+                // valid columns [lo, lim) of this half
+                int lo, lim;
+                if (!row_valid) {
+                    lo = 0;
+                    lim = 0;
+                } else if (j < n_pre) {
+                    lo = -hf * 64;
+                    lim = min(P - j * kN, kN) - hf * 64;
+                } else {
+                    const int c0 = (j - n_pre) * kN + hf * 64;
+                    lo = mk.col_off - c0;
+                    lim = seg_hi - c0;
+                }
+                const bool full = __all_sync(0xffffffffu, lo <= 0 && lim >= 64);
+                float mo = -INFINITY;
+                if (full) {
+#pragma unroll
+                    for (int u = 0; u < 32; u += 2)
+                        mo = fmaxf(fmaxf(mo, fmaxf(sa[u], sa[u + 1])), fmaxf(sb[u], sb[u + 1]));
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) {
+                        if (u >= lo && u < lim) mo = fmaxf(mo, sa[u]);
+                        if (u + 32 >= lo && u + 32 < lim) mo = fmaxf(mo, sb[u]);
+                    }
+                }
+                float* rd = red + (ns & 1) * 256;
+                rd[hf * 128 + r] = mo;
+                named_bar_sync_256();
+                float mt2 = fmaxf(mo, rd[(hf ^ 1) * 128 + r]);
+                mt2 *= p.scale_log2;
+                const bool bump = __any_sync(0xffffffffu, mt2 > m + kLazy);
+                const float mn = bump ? fmaxf(m, mt2) : m;
+                const float ms = (mn == -INFINITY) ? 0.f : mn;
+                const float alpha = bump ? ex2(m - ms) : 1.f;
+                float2 rs2 = make_float2(0.f, 0.f);
+                const float2 c2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-ms, -ms);
+                auto emit = [&](const float (&x)[32], int c0) {
+                    uint32_t pk[16];
+                    if (full) {
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) {
+                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
+                            const float2 a = make_float2(ex2(e.x), ex2(e.y));
+                            rs2 = __fadd2_rn(rs2, a);
+                            pk[u / 2] = pack2<T>(a.x, a.y);
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) {
+                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
+                            float2 a = make_float2(ex2(e.x), ex2(e.y));
+                            a.x = (c0 + u >= lo && c0 + u < lim) ? a.x : 0.f;
+                            a.y = (c0 + u + 1 >= lo && c0 + u + 1 < lim) ? a.y : 0.f;
+                            rs2 = __fadd2_rn(rs2, a);
+                            pk[u / 2] = pack2<T>(a.x, a.y);
+                        }
+                    }
+                    tmem_st16(tS + hf * 32 + c0 / 2, pk);
+                };
+                emit(sa, 0);
+                emit(sb, 32);
+                if (j > 0) {
+                    mbar_wait(o_done, (ns - 1) & 1);
+                    tc_fence_after();
+                }
+                if (j > 0 && bump) {
+#pragma unroll
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
+                        float v[32];
+                        tmem_ld32_nw(tO + c0, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) v[u] *= alpha;
+                        tmem_st32(tO + c0, v);
+                    }
+                }
+                l = l * alpha + (rs2.x + rs2.y);
+                m = mn;
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(p_full);
+            }
+            lsum[hf * 128 + r] = l;
+            named_bar_sync_256();
+            const float lt = l + lsum[(hf ^ 1) * 128 + r];
+            named_bar_sync_256();
+            const float inv = lt > 0.f ? 1.f / lt : 0.f;
+            const int qs0 = __ldg(p.query_start + s0) + r0;
+            T* orow = static_cast<T*>(p.out) + ((int64_t)(qs0 + r) * p.H + h) * 128 + hf * 64;
+            if (n > 0) {
+                mbar_wait(o_done, (ns - 1) & 1);
+                tc_fence_after();
+            }
+#pragma unroll
+            for (int c0 = 0; c0 < 64; c0 += 32) {
+                float v[32];
+                if (n > 0) {
+                    tmem_ld32_nw(tO + c0, v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) v[u] = 0.f;
+                }
+                if (row_valid) {
+#pragma unroll
+                    for (int c1 = 0; c1 < 32; c1 += 8) {
+                        alignas(16) T w[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) w[u] = Elem<T>::from_f32(v[c1 + u] * inv);
+                        *reinterpret_cast<uint4*>(orow + c0 + c1) = *reinterpret_cast<const uint4*>(w);
+                    }
+                }
+            }
+            if (n > 0) {
+                tc_fence_before();
+                mbar_arrive(o_free);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+size_t prefill_packed_smem_bytes() {
+    return 1024 + (4 + 2 * kKStages + 2 * kVStages) * (size_t)kHalf + (512 + 256) * 4 +
+           2 * (kMaxMem + 1) * sizeof(PackMem) + 8 * 4 + 21 * 8 + 16;
+}
+
+cudaError_t launch_prefill_packed(const PrefillParams& p, const PackTable& t, int dtype, cudaStream_t stream) {
+    int dev = 0, num_sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (num_sms <= 0) num_sms = 148;
+    const size_t smem = prefill_packed_smem_bytes();
+    const long long items = (long long)t.n_tiles * p.H;
+    const dim3 grid((unsigned)std::min<long long>(items, num_sms));
+    auto kern = dtype == 1 ? paged_prefill_packed_kernel<__half> : paged_prefill_packed_kernel<__nv_bfloat16>;
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
+    if (e != cudaSuccess) return e;
+    return launch_k(kern, grid, dim3(kThreadsV2), smem, stream, p, t);
+}
+
 // variant: 2 / 3 forces a kernel (PA_PREFILL, read once by pa_api.cpp); 0 = default: v3 when
 // no query needs more than 1.5 tiles of 128 rows (v2's pairs would mostly leave the second
 // softmax group idle), else v2, whose two query tiles share each K/V tile (measured,

@@ -233,6 +233,42 @@ def paged_attention_decode_grouped(out, query, key, value, key_cache, value_cach
 PREFILL_WORKSPACE_BYTES = 16
 
 
+def _host_i32(x, name):
+    import numpy as np
+    a = np.ascontiguousarray(np.asarray(x.cpu() if hasattr(x, "cpu") else x, dtype=np.int32))
+    return a
+
+
+def paged_prefill_attention_packed(out, query, key_cache, value_cache, block_tables, context_lens, query_start,
+                                   scale: float, host_query_start, host_context_lens, host_shared_prefix,
+                                   max_query_len: int = 0, workspace: torch.Tensor | None = None, stream=None):
+    """pa_paged_prefill_attention_packed (pa.h): requests sharing a cached prefix packed into
+    128-row query tiles, the prefix attended once per tile (cascade).  The host_* arrays
+    (numpy / CPU tensors / lists): query_start [S+1], context_lens [S], and per sequence the
+    number of leading tokens it shares with the previous one (same physical blocks)."""
+    _check(query.dtype, [("block_tables", block_tables), ("context_lens", context_lens),
+                         ("query_start", query_start)], out=out, query=query, key_cache=key_cache,
+           value_cache=value_cache)
+    T, H, D = query.shape
+    NB, hk, B, _ = key_cache.shape
+    S, W = block_tables.shape
+    hqs, hcl, hsp = (_host_i32(host_query_start, "host_query_start"), _host_i32(host_context_lens, "host_context_lens"),
+                     _host_i32(host_shared_prefix, "host_shared_prefix"))
+    if hqs.shape[0] != S + 1 or hcl.shape[0] != S or hsp.shape[0] != S:
+        raise ValueError("host arrays must have S+1, S and S entries")
+    if max_query_len <= 0:
+        max_query_len = int((hqs[1:] - hqs[:-1]).max()) if S > 0 else 0
+    if workspace is None:
+        workspace = torch.empty(PREFILL_WORKSPACE_BYTES, dtype=torch.uint8, device=query.device)
+    _call("pa_paged_prefill_attention_packed", (
+        _dev(out, "out"), _dev(query, "query"), _dev(key_cache, "key_cache"), _dev(value_cache, "value_cache"),
+        _dev(block_tables, "block_tables"), _dev(context_lens, "context_lens"), _dev(query_start, "query_start"),
+        hqs.ctypes.data, hcl.ctypes.data, hsp.ctypes.data, float(scale), B, hk, NB, S, H, D, W, T,
+        int(max_query_len), _code(query), _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(),
+        _stream(stream)))
+    return out
+
+
 def paged_prefill_attention(out, query, key_cache, value_cache, block_tables, context_lens, query_start,
                             scale: float, max_query_len: int = 0, workspace: torch.Tensor | None = None,
                             stream=None):

@@ -114,6 +114,15 @@ def main():
                "mean_ctx": round(float(c["ctx"].mean()), 1), "ms": round(t * 1e3, 4),
                "tflops": round(tf, 1), "peak_tflops": peak, "peak_src": peak_src, "frac": round(tf / peak, 3),
                "query_tokens_per_s": round(c["qlen"].sum() / t, 0), "launches_per_call": launches}
+        if c["kind"] == "prefix":  # the packed (cascade) entry on the same workload
+            hqs = np.concatenate([[0], np.cumsum(c["qlen"])]).astype(np.int32)
+            fnp = lambda: pa.paged_prefill_attention_packed(  # noqa: E731
+                out, q, kc, vc, bt, cl, qs, scale, hqs, c["ctx"].astype(np.int32), c["shared"].astype(np.int32),
+                max_query_len=mql, workspace=ws)
+            tp = time_it(fnp, args.iters)
+            res["packed_ms"] = round(tp * 1e3, 4)
+            res["packed_tflops"] = round(flops / tp / 1e12, 1)
+            res["packed_frac"] = round(flops / tp / 1e12 / peak, 3)
         if name == "p_2k":  # library context: contiguous causal SDPA, same flops
             S, n = len(c["ctx"]), int(c["ctx"][0])
             qq = q.view(S, n, c["H"], D).transpose(1, 2).contiguous()

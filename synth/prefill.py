@@ -75,7 +75,12 @@ def make_prefill(name: str, **over) -> dict:
         for s in range(S):
             bt[s, :nb[s]] = ids[off:off + nb[s]]
             off += nb[s]
-    c.update(name=name, ctx=ctx, qlen=qlen, block_tables=bt, num_blocks=NB)
+    # per sequence: leading cached tokens shared (same physical blocks) with the previous
+    # sequence -- the host-side hint of pa_paged_prefill_attention_packed
+    shared = np.zeros(S, np.int64)
+    if c["kind"] == "prefix" and S > 1:
+        shared[1:] = (c["prefix"] // B) * B
+    c.update(name=name, ctx=ctx, qlen=qlen, block_tables=bt, num_blocks=NB, shared=shared)
     return c
 
 

@@ -187,3 +187,96 @@ def test_kernel_variants_agree(dtype, tuning_env):
     for o in outs[1:]:
         diff = (o.float() - outs[0].float()).abs().max().item()
         assert diff <= 4 * ulp
+
+
+# ------------------------------------------------------------- packed (cascade) -------
+
+def shared_prefix_problem(groups, B, H, H_kv, dtype, seed=5):
+    """groups: list of (prefix_len, [(own_len, q_len), ...]).  Each group's first
+    prefix_len // B * B tokens sit in physical blocks SHARED by its members (the rest of a
+    member's context -- the prefix tail, then its own tokens -- in private blocks); member
+    ctx = prefix_len + own_len, its last q_len tokens are the query.  Returns the device
+    tensors plus the host hints of pa_paged_prefill_attention_packed."""
+    rs = np.random.default_rng(seed)
+    ctxs, qlens, shared, rows = [], [], [], []
+    blk = 0
+    for P, members in groups:
+        full = P // B
+        shared_ids = list(range(blk, blk + full))
+        blk += full
+        for mi, (own, ql) in enumerate(members):
+            c = P + own
+            nb = -(-c // B)
+            ids = shared_ids + list(range(blk, blk + nb - full))
+            blk += nb - full
+            ctxs.append(c)
+            qlens.append(ql)
+            shared.append(full * B if mi > 0 else 0)
+            rows.append(ids)
+    NB = blk + 3
+    W = max(len(r) for r in rows)
+    bt = np.full((len(rows), W), -1, np.int32)
+    for s, r in enumerate(rows):
+        bt[s, :len(r)] = r
+    tdt = torch.float16 if dtype == "f16" else torch.bfloat16
+    kc = torch.from_numpy(rs.uniform(-1, 1, (NB, H_kv, B, D)).astype(np.float32)).to(tdt).cuda()
+    vc = torch.from_numpy(rs.uniform(-1, 1, (NB, H_kv, B, D)).astype(np.float32)).to(tdt).cuda()
+    qs = np.concatenate([[0], np.cumsum(qlens)]).astype(np.int32)
+    q = torch.from_numpy(rs.uniform(-1, 1, (int(qs[-1]), H, D)).astype(np.float32)).to(tdt).cuda()
+    return (q, kc, vc, torch.as_tensor(bt).cuda(), torch.as_tensor(np.asarray(ctxs, np.int32)).cuda(),
+            torch.as_tensor(qs).cuda(), qs, np.asarray(ctxs, np.int32), np.asarray(shared, np.int32))
+
+
+def run_packed(q, kc, vc, bt, cl, qs, scale, hqs, hcl, hsp):
+    out = torch.full_like(q, float("nan"))
+    pa.paged_prefill_attention_packed(out, q, kc, vc, bt, cl, qs, scale, hqs, hcl, hsp)
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("dtype,B,H,H_kv", [("f16", 16, 4, 4), ("bf16", 16, 4, 2), ("f16", 32, 2, 2)])
+def test_packed_prefill_vs_oracle(dtype, B, H, H_kv):
+    """Shared-prefix suffixes packed into 128-row tiles (cascade): groups with prefixes that
+    are / are not block-aligned and longer / shorter than a key tile, members with 1..90
+    query rows, q_len 0, a lone sequence without sharing, and a 300-row query that takes
+    tiles of its own -- every row vs the fp64 oracle."""
+    groups = [(341, [(30, 30), (5, 5), (60, 60), (1, 1), (33, 20), (90, 90)]),
+              (80, [(40, 40), (20, 20), (31, 31), (0, 0), (16, 16)]),
+              (0, [(300, 300)]),
+              (200, [(10, 10)]),
+              (130, [(7, 3), (9, 9), (64, 64), (12, 12)])]
+    q, kc, vc, bt, cl, qs, hqs, hcl, hsp = shared_prefix_problem(groups, B, H, H_kv, dtype)
+    out = run_packed(q, kc, vc, bt, cl, qs, 0.09, hqs, hcl, hsp)
+    r = ref(q, kc, vc, bt, cl, qs, 0.09, B, H_kv, dtype)
+    assert not torch.isnan(out).any()
+    assert max_abs(out, r) <= TOL[dtype]
+
+
+def test_packed_prefill_full_size_sampled():
+    """The p_prefix5 / p_prefix1 workloads (256 requests after a 341 / 80-token shared
+    prefix, LLaMA-13B attention shape): whole output finite, sampled rows x heads vs the
+    oracle's Eq.4 row of length pos+1."""
+    from synth.prefill import make_prefill
+    for name in ("p_prefix5", "p_prefix1"):
+        c = make_prefill(name)
+        H, H_kv, B = c["H"], c["H_kv"], c["B"]
+        dt = torch.float16
+        g = torch.Generator(device="cuda")
+        g.manual_seed(c["seed"])
+        kc = (torch.rand((c["num_blocks"], H_kv, B, D), generator=g, device="cuda") * 2 - 1).to(dt)
+        vc = (torch.rand(tuple(kc.shape), generator=g, device="cuda") * 2 - 1).to(dt)
+        hqs = np.concatenate([[0], np.cumsum(c["qlen"])]).astype(np.int32)
+        q = (torch.rand((int(hqs[-1]), H, D), generator=g, device="cuda") * 2 - 1).to(dt)
+        bt = torch.as_tensor(c["block_tables"], device="cuda")
+        cl = torch.as_tensor(c["ctx"].astype(np.int32), device="cuda")
+        qs = torch.as_tensor(hqs, device="cuda")
+        out = run_packed(q, kc, vc, bt, cl, qs, D ** -0.5, hqs, c["ctx"].astype(np.int32), c["shared"].astype(np.int32))
+        assert torch.isfinite(out).all()
+        rs = np.random.default_rng(11)
+        qb, kb, vb, btn, cln = bits(q), bits(kc), bits(vc), bt.cpu().numpy(), cl.cpu().numpy()
+        for row in rs.integers(0, int(hqs[-1]), 40):
+            s = int(np.searchsorted(hqs, row, side="right") - 1)
+            pos = int(cln[s] - (hqs[s + 1] - hqs[s]) + (row - hqs[s]))
+            rr = oracle.paged_attention(qb[row:row + 1], kb, vb, btn[s:s + 1], np.array([pos + 1], np.int32),
+                                        D ** -0.5, B, H_kv, "f16")
+            assert max_abs(out[row:row + 1], rr) <= TOL["f16"], (name, row)
