@@ -685,7 +685,10 @@ pa_status_t pa_paged_prefill_attention_packed(
     bool ok = block_size >= 16 && num_seqs > 0;
     t.n_tiles = 0;
     auto add_tile = [&](int s0, int nm, int P, int r0) {
-        if (t.n_tiles == pa::kMaxPackTiles) return false;
+        if (t.n_tiles == pa::kMaxPackTiles || P > 4096) return false;  // kernel table limits
+        int64_t pieces = 0;
+        for (int k = 0; k < nm; ++k) pieces += (host_context_lens[s0 + k] - P + 15) / 16;
+        if (pieces > 512) return false;
         t.s0[t.n_tiles] = s0;
         t.nm[t.n_tiles] = (uint16_t)nm;
         t.P[t.n_tiles] = P;

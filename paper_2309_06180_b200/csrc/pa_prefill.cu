@@ -865,8 +865,20 @@ size_t prefill_ws_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 26 * 8 + 4 *
 // publishes each item's member table (row offset, context, packed column offset, piece
 // offset) in shared memory for the softmax warps.
 constexpr int kMaxMem = 128;
+constexpr int kMaxPre = 256;     // 16-token positions of the shared prefix (P <= 4096)
+constexpr int kMaxPieces = 512;  // 16-token pieces of the members' own tokens per tile
+constexpr int kThreadsV6 = kThreadsV2 + 32;  // + one scheduler warp
 struct PackMem {
     int row_off, ctx, col_off, piece_off, qlen;
+};
+// One item's table, built by the scheduler warp one item ahead: the members, and the
+// physical block of every 16-token position of the prefix and of every own-token piece,
+// so the TMA producer issues copies without a global round trip of its own.
+struct PackSlot {
+    PackMem mem[kMaxMem + 1];
+    int hdr[4];  // rows, packed columns seen, n_pre, n
+    int pre_blk[kMaxPre];
+    int piece_blk[kMaxPieces];
 };
 
 __device__ __forceinline__ void packed_item(const PackTable& t, const PrefillParams& p, int i, int& tile, int& h,
@@ -880,7 +892,7 @@ __device__ __forceinline__ void packed_item(const PackTable& t, const PrefillPar
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kThreadsV2, 1)
+__global__ void __launch_bounds__(kThreadsV6, 1)
     paged_prefill_packed_kernel(const __grid_constant__ PrefillParams p, const __grid_constant__ PackTable pt) {
     constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -890,9 +902,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     unsigned char* sV = sK + 2 * kKStages * kHalf;     // [2 stages][2 halves][128][64]
     float* red = reinterpret_cast<float*>(sV + 2 * kVStages * kHalf);  // [2 parity][2 groups][128] row maxima
     float* lsum = red + 512;                                            // [2 groups][128] row sums
-    PackMem* mem = reinterpret_cast<PackMem*>(lsum + 256);              // [2 parity][kMaxMem + 1]
-    int* mhdr = reinterpret_cast<int*>(mem + 2 * (kMaxMem + 1));       // [2 parity][4]: rows, C, n_pre, n
-    uint64_t* bars = reinterpret_cast<uint64_t*>(mhdr + 8);
+    PackSlot* slots = reinterpret_cast<PackSlot*>(lsum + 256);         // [2 parity]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + 2);
     uint64_t* q_full = bars;                 // 2
     uint64_t* q_empty = bars + 2;            // 2
     uint64_t* k_full = bars + 4;             // 2
@@ -903,8 +914,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     uint64_t* p_full = bars + 14;            // 1
     uint64_t* o_done = bars + 15;            // 1
     uint64_t* o_free = bars + 16;            // 1
-    uint64_t* m_full = bars + 17;            // 2: member table published (producer)
-    uint64_t* m_empty = bars + 19;           // 2: member table read (8 softmax warps + MMA warp)
+    uint64_t* m_full = bars + 17;            // 2: item table published (scheduler warp)
+    uint64_t* m_empty = bars + 19;           // 2: item table read (8 softmax warps, MMA, producer)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -921,7 +932,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             mbar_init(&k_full[i], 1);
             mbar_init(&k_empty[i], 1);
             mbar_init(&m_full[i], 1);
-            mbar_init(&m_empty[i], 9);
+            mbar_init(&m_empty[i], 10);
         }
         mbar_init(p_full, 2 * kQ);
         mbar_init(o_done, 1);
@@ -929,7 +940,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         fence_mbar_init();
     }
     // V stages start zeroed: columns of a last tile past its tokens are never loaded
-    for (int i = tid; i < 2 * kVStages * kHalf / 16; i += kThreadsV2)
+    for (int i = tid; i < 2 * kVStages * kHalf / 16; i += kThreadsV6)
         reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
     if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -939,18 +950,16 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
     const uint32_t tmem = *tmem_slot;
     const int B = 1 << p.log2B;
 
-    if (warp == 8) {
-        // ---------------- TMA producer ----------------
-        const int br = p.box_rows;
-        uint32_t g = 0, nq = 0;
+    if (warp == 10) {
+        // ---------------- scheduler: each item's table, one item ahead ----------------
+        uint32_t nq = 0;
         for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++nq) {
             int tile, h, s0, nm, P, r0;
             packed_item(pt, p, i, tile, h, s0, nm, P, r0);
-            const int kvh = h / p.G;
             const int qb = nq & 1;
-            // ---- member table of this item (double-buffered by item parity)
             if (nq >= 2) mbar_wait(&m_empty[qb], ((nq - 2) >> 1) & 1);
-            PackMem* mt = mem + qb * (kMaxMem + 1);
+            PackSlot& sl = slots[qb];
+            PackMem* mt = sl.mem;
             const int qs0 = __ldg(p.query_start + s0) + r0;
             int col = 0, pcs = 0;
             for (int k0 = 0; k0 < nm; k0 += 32) {
@@ -985,16 +994,45 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 const int pos_max = ml.ctx - ml.qlen + (rows - 1 - ml.row_off);
                 col = ml.col_off + min(ml.ctx - P, pos_max - P + 1);
             }
-            const int n_pre = (P + kN - 1) / kN, n_suf = (col + kN - 1) / kN, n = n_pre + n_suf;
+            // physical blocks: every 16-token position of the prefix (through s0's table) and
+            // every own-token piece of every member
+            const int32_t* bt0 = p.block_tables + (int64_t)s0 * p.W;
+            for (int q = lane; q < ((P + 15) >> 4); q += 32) sl.pre_blk[q] = __ldg(bt0 + ((q << 4) >> p.log2B));
+            for (int gp = lane; gp < pcs; gp += 32) {
+                int lo = 0, hi = nm - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (mt[mid].piece_off <= gp) lo = mid; else hi = mid - 1;
+                }
+                const int tt0 = P + 16 * (gp - mt[lo].piece_off);
+                sl.piece_blk[gp] = __ldg(p.block_tables + (int64_t)(s0 + lo) * p.W + (tt0 >> p.log2B));
+            }
+            const int n_pre = (P + kN - 1) / kN, n_suf = (col + kN - 1) / kN;
             if (lane == 0) {
                 mt[nm] = PackMem{rows, 0, col, pcs, 0};
-                mhdr[qb * 4 + 0] = rows;
-                mhdr[qb * 4 + 1] = col;
-                mhdr[qb * 4 + 2] = n_pre;
-                mhdr[qb * 4 + 3] = n;
+                sl.hdr[0] = rows;
+                sl.hdr[1] = col;
+                sl.hdr[2] = n_pre;
+                sl.hdr[3] = n_pre + n_suf;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&m_full[qb]);  // release: the table writes above
+        }
+    } else if (warp == 8) {
+        // ---------------- TMA producer ----------------
+        const int br = p.box_rows;
+        uint32_t g = 0, nq = 0;
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++nq) {
+            int tile, h, s0, nm, P, r0;
+            packed_item(pt, p, i, tile, h, s0, nm, P, r0);
+            const int kvh = h / p.G;
+            const int qb = nq & 1;
+            mbar_wait(&m_full[qb], (nq >> 1) & 1);
+            const PackSlot& sl = slots[qb];
+            const PackMem* mt = sl.mem;
+            const int qs0 = __ldg(p.query_start + s0) + r0;
+            const int col = sl.hdr[1], n_pre = sl.hdr[2], n = sl.hdr[3];
+            const int pcs = mt[nm].piece_off;
             // ---- query tile
             if (nq >= 2) mbar_wait(&q_empty[qb], ((nq - 2) >> 1) & 1);
             if (lane == 0) {
@@ -1003,7 +1041,6 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                 tma_load_3d(sQ + qb * 2 * kHalf + kHalf, &p.tmap_q, 64, h, qs0, &q_full[qb]);
             }
             __syncwarp();
-            const int32_t* bt0 = p.block_tables + (int64_t)s0 * p.W;
             for (int j = 0; j < n; ++j, ++g) {
                 const uint32_t ks = g % kKStages, vs = g & 1;
                 for (int tsr = 0; tsr < 2; ++tsr) {  // K then V
@@ -1021,7 +1058,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                         __syncwarp();
                         for (int b2 = lane; b2 < nb; b2 += 32) {
                             const int tt = t0 + (b2 < nf ? b2 * br : nf * br + (b2 - nf));
-                            const int blk = __ldg(bt0 + (tt >> p.log2B));
+                            const int blk = sl.pre_blk[tt >> 4];
                             const int row = (blk * p.H_kv + kvh) * B + (tt & (B - 1));
                             const int off = (tt - t0) * 128;
                             const CUtensorMap* m = b2 < nf ? map : map1;
@@ -1048,7 +1085,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                             const int a = max(pc0, c_lo), b3 = min(pc1, c_hi);
                             if (a >= b3) continue;
                             const int tt0 = P + 16 * q;  // first token of the piece
-                            const int blk = __ldg(p.block_tables + (int64_t)(s0 + lo) * p.W + (tt0 >> p.log2B));
+                            const int blk = sl.piece_blk[gp];
                             const int row0 = (blk * p.H_kv + kvh) * B + (tt0 & (B - 1));
                             if (a == pc0 && b3 == pc1 && pc1 - pc0 == 16 && br == 16) {
                                 tma_load_2d(dst0 + (a - c_lo) * 128, map, 0, row0, bar);
@@ -1070,6 +1107,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
                     __syncwarp();
                 }
             }
+            if (lane == 0) mbar_arrive(&m_empty[qb]);  // this item's table is no longer read here
         }
     } else if (warp == 9) {
         // ---------------- MMA issuer (as v3) ----------------
@@ -1096,7 +1134,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
         for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
             const uint32_t qb = nq & 1;
             mbar_wait(&m_full[qb], (nq >> 1) & 1);
-            const int n = *reinterpret_cast<volatile int*>(&mhdr[qb * 4 + 3]);
+            const int n = *reinterpret_cast<volatile int*>(&slots[qb].hdr[3]);
             __syncwarp();
             if (lane == 0) mbar_arrive(&m_empty[qb]);
             mbar_wait(&q_full[qb], (nq >> 1) & 1);
@@ -1137,8 +1175,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
             packed_item(pt, p, i, tile, h, s0, nm, P, r0);
             const uint32_t qb = nq & 1;
             mbar_wait(&m_full[qb], (nq >> 1) & 1);
-            const PackMem* mt = mem + qb * (kMaxMem + 1);
-            const int rows = mhdr[qb * 4 + 0], n_pre = mhdr[qb * 4 + 2], n = mhdr[qb * 4 + 3];
+            const PackMem* mt = slots[qb].mem;
+            const int rows = slots[qb].hdr[0], n_pre = slots[qb].hdr[2], n = slots[qb].hdr[3];
             // this row's member (last row_off <= r), its position and packed segment
             const bool row_valid = r < rows;
             int k = 0;
@@ -1294,8 +1332,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1)
 }
 
 size_t prefill_packed_smem_bytes() {
-    return 1024 + (4 + 2 * kKStages + 2 * kVStages) * (size_t)kHalf + (512 + 256) * 4 +
-           2 * (kMaxMem + 1) * sizeof(PackMem) + 8 * 4 + 21 * 8 + 16;
+    return 1024 + (4 + 2 * kKStages + 2 * kVStages) * (size_t)kHalf + (512 + 256) * 4 + 2 * sizeof(PackSlot) +
+           21 * 8 + 16;
 }
 
 cudaError_t launch_prefill_packed(const PrefillParams& p, const PackTable& t, int dtype, cudaStream_t stream) {
@@ -1309,7 +1347,7 @@ cudaError_t launch_prefill_packed(const PrefillParams& p, const PackTable& t, in
     auto kern = dtype == 1 ? paged_prefill_packed_kernel<__half> : paged_prefill_packed_kernel<__nv_bfloat16>;
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
-    return launch_k(kern, grid, dim3(kThreadsV2), smem, stream, p, t);
+    return launch_k(kern, grid, dim3(kThreadsV6), smem, stream, p, t);
 }
 
 // variant: 2 / 3 forces a kernel (PA_PREFILL, read once by pa_api.cpp); 0 = default: v3 when
