@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     constexpr int kProd = kNH, kMma = kNH + 1;  // warp roles; warps 0..kNH-1 run the softmax
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem =
-        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+        tc::smem_align1024(smem_raw);
     unsigned char* sT = smem;                         // kBuf x [K|V][half][piece][head][16][128 B]
     TileMeta* meta = reinterpret_cast<TileMeta*>(sT + kBuf * kTileBytes);
     int2* list = reinterpret_cast<int2*>(meta + kBuf);

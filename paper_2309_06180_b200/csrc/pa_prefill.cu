@@ -66,6 +66,21 @@ __device__ long long g_pf_trace[64 * 256];
 constexpr int kWarpsV2 = 10;
 constexpr float kLazy = 8.f;  // P <= 2^8: no overflow in f16/bf16, same relative rounding
 constexpr int kThreadsV2 = kWarpsV2 * 32;
+// TMA producer warps of v2 / v3 / v6.  A warp issues its tensor copies one at a time (SASS: an
+// ELECT loop around UTMALDG), and a 128-token tile of 16-token blocks is 32 copies of 2 KB
+// (K and V, two 64-column halves); with one producer warp that issue rate, not the tensor
+// cores, set the step time.  The extra producer warps split each tile's
+// copies with warp 8; warp 8 alone arms the barriers (expect_tx) and loads Q.
+#ifndef PA_PF_PROD
+#define PA_PF_PROD 4
+#endif
+constexpr int kProd = PA_PF_PROD;
+#ifndef PA_PF_PROD_V2
+#define PA_PF_PROD_V2 2  // v2 holds 157 registers per thread: 4 producers would cap it at 152
+#endif
+constexpr int kProdV2 = PA_PF_PROD_V2;
+constexpr int kThreadsV3 = kThreadsV2 + 32 * (kProd - 1);    // extra producers: warps 10..
+constexpr int kThreadsWs = kThreadsV2 + 32 * (kProdV2 - 1);  // v2's
 
 // Work item = (query-tile pair qp, head h, sequence s); items are dealt to persistent CTAs
 // (one per SM) round-robin, longest pairs first.  The barrier phases run on across items,
@@ -101,10 +116,10 @@ __device__ __forceinline__ bool prefill_item(const PrefillParams& p, int i, Pref
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const __grid_constant__ PrefillParams p) {
+__global__ void __launch_bounds__(kThreadsWs, 1) paged_prefill_ws_kernel(const __grid_constant__ PrefillParams p) {
     constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* smem = tc::smem_align1024(smem_raw);
     unsigned char* sQ = smem;                // [2 tiles][2 halves][128][64]
     unsigned char* sK = smem + 4 * kHalf;    // [2 stages][2 halves][128][64]
     unsigned char* sV = sK + 4 * kHalf;      // [2 stages][2 halves][128][64]
@@ -135,7 +150,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) {
             mbar_init(&sched_full[i], 1);
-            mbar_init(&sched_empty[i], 1 + 2 * kQ);  // MMA warp (one arrive) + 256 softmax threads
+            mbar_init(&sched_empty[i], kProdV2 + 2 * kQ);  // MMA warp + extra producers (one arrive each) + 256 softmax threads
         }
         mbar_init(q_full, 1);
         mbar_init(q_empty, 1);
@@ -154,7 +169,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     // V stages start zeroed: rows past kv_len of a last tile are never loaded and must not
     // hold NaN bit patterns (P = 0 there, but 0 * NaN = NaN in the MMA); later they hold
     // rows of earlier tiles (finite cache data)
-    for (int i = tid; i < 4 * kHalf / 16; i += kThreadsV2)
+    for (int i = tid; i < 4 * kHalf / 16; i += kThreadsWs)
         reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
     if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -164,22 +179,30 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
     const uint32_t tmem = *tmem_slot;
     const int B = 1 << p.log2B;
 
-    if (warp == 8) {
-        // ---------------- TMA producer ----------------
+    if (warp == 8 || warp >= kWarpsV2) {
+        // ---------------- TMA producers (pw 0 = warp 8) ----------------
+        const int pw = warp == 8 ? 0 : warp - kWarpsV2 + 1;
         const int br = p.box_rows;
         uint32_t g = 0;    // KV tiles loaded by this CTA (stage = g & 1)
         uint32_t nq = 0;   // query tile pairs loaded
         for (uint32_t k = 0;; ++k) {
-            // the producer draws the next work item and publishes it to the other warps
+            // producer 0 draws the next work item and publishes it to the other warps
             const uint32_t slot = k & 3;
-            if (k >= 4) mbar_wait(&sched_empty[slot], ((k - 4) >> 2) & 1);
             int i = 0;
-            if (lane == 0) {
-                i = atomicAdd(p.work_counter, 1);
-                sched_item[slot] = i;
-                mbar_arrive(&sched_full[slot]);
+            if (pw == 0) {
+                if (k >= 4) mbar_wait(&sched_empty[slot], ((k - 4) >> 2) & 1);
+                if (lane == 0) {
+                    i = atomicAdd(p.work_counter, 1);
+                    sched_item[slot] = i;
+                    mbar_arrive(&sched_full[slot]);
+                }
+                i = __shfl_sync(0xffffffffu, i, 0);
+            } else {
+                mbar_wait(&sched_full[slot], (k >> 2) & 1);
+                i = *reinterpret_cast<volatile int*>(&sched_item[slot]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sched_empty[slot]);
             }
-            i = __shfl_sync(0xffffffffu, i, 0);
             if (i >= n_items) break;
             PrefillItem it;
             if (!prefill_item(p, i, it)) continue;
@@ -193,8 +216,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
                 const int t0 = j * kN, len = min(it.kv_len, t0 + kN) - t0;
                 const int nf = len / br, nb = nf + len % br;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int b = lane + 32 * u;
+                for (int u = 0; u < (4 + kProdV2 - 1) / kProdV2; ++u) {
+                    const int b = pw + kProdV2 * (lane + 32 * u);  // boxes interleaved over the producers
                     if (b < nb) {
                         const int t = t0 + box_token(b, nf);
                         const int blk = __ldg(btrow + (t >> p.log2B));
@@ -206,11 +229,11 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
                              uint64_t* bar, const int (&rowv)[4]) {
                 const int t0 = j * kN, len = min(it.kv_len, t0 + kN) - t0;
                 const int nf = len / br, nb = nf + len % br;
-                if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
+                if (pw == 0 && lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
                 __syncwarp();
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int b = lane + 32 * u;
+                for (int u = 0; u < (4 + kProdV2 - 1) / kProdV2; ++u) {
+                    const int b = pw + kProdV2 * (lane + 32 * u);  // boxes interleaved over the producers
                     if (b < nb) {
                         const int off = box_token(b, nf) * 128;
                         const CUtensorMap* m = b < nf ? map : map1;
@@ -222,8 +245,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
             };
             int rowv[4] = {0, 0, 0, 0};
             if (it.n > 0) lookup(0, rowv);
-            if (nq > 0) mbar_wait(q_empty, (nq - 1) & 1);  // last S of the previous pair done
-            if (lane == 0) {
+            if (pw == 0 && nq > 0) mbar_wait(q_empty, (nq - 1) & 1);  // last S of the previous pair done
+            if (pw == 0 && lane == 0) {
                 mbar_arrive_expect_tx(q_full, 4u * kHalf);
                 tma_load_3d(sQ, &p.tmap_q, 0, it.h, it.qs + it.q0, q_full);
                 tma_load_3d(sQ + kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0, q_full);
@@ -236,10 +259,10 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
                 const int st = g & 1;
                 if (g >= 2) mbar_wait(&k_empty[st], ((g - 2) >> 1) & 1);
                 issue(sK + st * 2 * kHalf, &p.tmap_k, &p.tmap_k1, j, &k_full[st], rowv);
-                if (lane == 0 && k == 0 && j < 16) PF_T(192 + 4 * j);
+                if (pw == 0 && lane == 0 && k == 0 && j < 16) PF_T(192 + 4 * j);
                 if (g >= 2) mbar_wait(&v_empty[st], ((g - 2) >> 1) & 1);
                 issue(sV + st * 2 * kHalf, &p.tmap_v, &p.tmap_v1, j, &v_full[st], rowv);
-                if (lane == 0 && k == 0 && j < 16) PF_T(192 + 4 * j + 1);
+                if (pw == 0 && lane == 0 && k == 0 && j < 16) PF_T(192 + 4 * j + 1);
                 if (j + 1 < it.n) lookup(j + 1, rowv);  // in flight while the next empty-wait spins
             }
         }
@@ -399,7 +422,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_ws_kernel(const _
 #pragma unroll
                         for (int u = 0; u < 32; u += 2) {
                             const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);  // s*c - m
-                            const float2 a = make_float2(ex2(e.x), ex2(e.y));
+                            const float2 a = ex2_pair(e, u / 2);
                             rs2 = __fadd2_rn(rs2, a);
                             pk[u / 2] = pack2<T>(a.x, a.y);
                         }
@@ -535,10 +558,10 @@ __device__ __forceinline__ bool prefill_item1(const PrefillParams& p, int i, Pre
 __device__ __forceinline__ void named_bar_sync_256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 template <typename T>
-__global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_split_kernel(const __grid_constant__ PrefillParams p) {
+__global__ void __launch_bounds__(kThreadsV3, 1) paged_prefill_split_kernel(const __grid_constant__ PrefillParams p) {
     constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* smem = tc::smem_align1024(smem_raw);
     unsigned char* sQ = smem;                          // [2 buffers][2 halves][128][64]
     unsigned char* sK = smem + 4 * kHalf;              // [3 stages][2 halves][128][64]
     unsigned char* sV = sK + 2 * kKStages * kHalf;     // [2 stages][2 halves][128][64]
@@ -579,7 +602,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_split_kernel(cons
         fence_mbar_init();
     }
     // V stages start zeroed (see v2)
-    for (int i = tid; i < 2 * kVStages * kHalf / 16; i += kThreadsV2)
+    for (int i = tid; i < 2 * kVStages * kHalf / 16; i += kThreadsV3)
         reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
     if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -589,8 +612,9 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_split_kernel(cons
     const uint32_t tmem = *tmem_slot;
     const int B = 1 << p.log2B;
 
-    if (warp == 8) {
-        // ---------------- TMA producer ----------------
+    if (warp == 8 || warp >= kWarpsV2) {
+        // ---------------- TMA producers (pw 0 = warp 8) ----------------
+        const int pw = warp == 8 ? 0 : warp - kWarpsV2 + 1;
         const int br = p.box_rows;
         uint32_t g = 0, nq = 0;
         for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
@@ -603,8 +627,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_split_kernel(cons
                 const int t0 = j * kN, len = min(it.kv_len, t0 + kN) - t0;
                 const int nf = len / br, nb = nf + len % br;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int b = lane + 32 * u;
+                for (int u = 0; u < (4 + kProd - 1) / kProd; ++u) {
+                    const int b = pw + kProd * (lane + 32 * u);  // boxes interleaved over the producers
                     if (b < nb) {
                         const int t = t0 + box_token(b, nf);
                         const int blk = __ldg(btrow + (t >> p.log2B));
@@ -616,11 +640,11 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_split_kernel(cons
                              uint64_t* bar, const int (&rowv)[4]) {
                 const int t0 = j * kN, len = min(it.kv_len, t0 + kN) - t0;
                 const int nf = len / br, nb = nf + len % br;
-                if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
+                if (pw == 0 && lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
                 __syncwarp();
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int b = lane + 32 * u;
+                for (int u = 0; u < (4 + kProd - 1) / kProd; ++u) {
+                    const int b = pw + kProd * (lane + 32 * u);  // boxes interleaved over the producers
                     if (b < nb) {
                         const int off = box_token(b, nf) * 128;
                         const CUtensorMap* m = b < nf ? map : map1;
@@ -633,8 +657,8 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_split_kernel(cons
             int rowv[4] = {0, 0, 0, 0};
             if (it.n > 0) lookup(0, rowv);
             const int qb = nq & 1;
-            if (nq >= 2) mbar_wait(&q_empty[qb], ((nq - 2) >> 1) & 1);
-            if (lane == 0) {
+            if (pw == 0 && nq >= 2) mbar_wait(&q_empty[qb], ((nq - 2) >> 1) & 1);
+            if (pw == 0 && lane == 0) {
                 mbar_arrive_expect_tx(&q_full[qb], 2u * kHalf);
                 tma_load_3d(sQ + qb * 2 * kHalf, &p.tmap_q, 0, it.h, it.qs + it.q0, &q_full[qb]);
                 tma_load_3d(sQ + qb * 2 * kHalf + kHalf, &p.tmap_q, 64, it.h, it.qs + it.q0, &q_full[qb]);
@@ -760,7 +784,7 @@ __global__ void __launch_bounds__(kThreadsV2, 1) paged_prefill_split_kernel(cons
 #pragma unroll
                         for (int u = 0; u < 32; u += 2) {
                             const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
-                            const float2 a = make_float2(ex2(e.x), ex2(e.y));
+                            const float2 a = ex2_pair(e, u / 2);
                             rs2 = __fadd2_rn(rs2, a);
                             pk[u / 2] = pack2<T>(a.x, a.y);
                         }
@@ -867,7 +891,7 @@ size_t prefill_ws_smem_bytes() { return 1024 + 12 * (size_t)kHalf + 26 * 8 + 4 *
 constexpr int kMaxMem = 128;
 constexpr int kMaxPre = 256;     // 16-token positions of the shared prefix (P <= 4096)
 constexpr int kMaxPieces = 512;  // 16-token pieces of the members' own tokens per tile
-constexpr int kThreadsV6 = kThreadsV2 + 32;  // + one scheduler warp
+constexpr int kThreadsV6 = kThreadsV2 + 32 * kProd;  // + scheduler warp 10, producers 11..
 struct PackMem {
     int row_off, ctx, col_off, piece_off, qlen;
 };
@@ -876,7 +900,7 @@ struct PackMem {
 // so the TMA producer issues copies without a global round trip of its own.
 struct PackSlot {
     PackMem mem[kMaxMem + 1];
-    int hdr[4];  // rows, packed columns seen, n_pre, n
+    int hdr[9];  // rows, packed columns seen, n_pre, n, nm, P, first query row, head, s0
     int pre_blk[kMaxPre];
     int piece_blk[kMaxPieces];
 };
@@ -896,12 +920,13 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
     paged_prefill_packed_kernel(const __grid_constant__ PrefillParams p, const __grid_constant__ PackTable pt) {
     constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char* smem = tc::smem_align1024(smem_raw);
     unsigned char* sQ = smem;                          // [2 buffers][2 halves][128][64]
     unsigned char* sK = smem + 4 * kHalf;              // [2 stages][2 halves][128][64]
     unsigned char* sV = sK + 2 * kKStages * kHalf;     // [2 stages][2 halves][128][64]
-    float* red = reinterpret_cast<float*>(sV + 2 * kVStages * kHalf);  // [2 parity][2 groups][128] row maxima
-    float* lsum = red + 512;                                            // [2 groups][128] row sums
+    unsigned char* stage = sV + 2 * kVStages * kHalf;  // [8 softmax warps][32 rows][64 B] output staging
+    float* red = reinterpret_cast<float*>(stage + 8 * 2048);  // [2 parity][2 groups][128] row maxima
+    float* lsum = red + 512;                                   // [2 groups][128] row sums
     PackSlot* slots = reinterpret_cast<PackSlot*>(lsum + 256);         // [2 parity]
     uint64_t* bars = reinterpret_cast<uint64_t*>(slots + 2);
     uint64_t* q_full = bars;                 // 2
@@ -915,7 +940,7 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
     uint64_t* o_done = bars + 15;            // 1
     uint64_t* o_free = bars + 16;            // 1
     uint64_t* m_full = bars + 17;            // 2: item table published (scheduler warp)
-    uint64_t* m_empty = bars + 19;           // 2: item table read (8 softmax warps, MMA, producer)
+    uint64_t* m_empty = bars + 19;           // 2: item table read (8 softmax warps, MMA, producers)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -932,7 +957,7 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
             mbar_init(&k_full[i], 1);
             mbar_init(&k_empty[i], 1);
             mbar_init(&m_full[i], 1);
-            mbar_init(&m_empty[i], 10);
+            mbar_init(&m_empty[i], 9 + kProd);
         }
         mbar_init(p_full, 2 * kQ);
         mbar_init(o_done, 1);
@@ -1014,28 +1039,32 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
                 sl.hdr[1] = col;
                 sl.hdr[2] = n_pre;
                 sl.hdr[3] = n_pre + n_suf;
+                sl.hdr[4] = nm;  // the item's fields for the other warps (no dynamically indexed
+                sl.hdr[5] = P;   // parameter loads there)
+                sl.hdr[6] = qs0;
+                sl.hdr[7] = h;
+                sl.hdr[8] = s0;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&m_full[qb]);  // release: the table writes above
         }
-    } else if (warp == 8) {
-        // ---------------- TMA producer ----------------
+    } else if (warp == 8 || warp > 10) {
+        // ---------------- TMA producers (pw 0 = warp 8) ----------------
+        const int pw = warp == 8 ? 0 : warp - 10;
         const int br = p.box_rows;
         uint32_t g = 0, nq = 0;
         for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++nq) {
-            int tile, h, s0, nm, P, r0;
-            packed_item(pt, p, i, tile, h, s0, nm, P, r0);
-            const int kvh = h / p.G;
             const int qb = nq & 1;
             mbar_wait(&m_full[qb], (nq >> 1) & 1);
             const PackSlot& sl = slots[qb];
             const PackMem* mt = sl.mem;
-            const int qs0 = __ldg(p.query_start + s0) + r0;
             const int col = sl.hdr[1], n_pre = sl.hdr[2], n = sl.hdr[3];
+            const int nm = sl.hdr[4], P = sl.hdr[5], qs0 = sl.hdr[6], h = sl.hdr[7];
+            const int kvh = h / p.G;
             const int pcs = mt[nm].piece_off;
             // ---- query tile
-            if (nq >= 2) mbar_wait(&q_empty[qb], ((nq - 2) >> 1) & 1);
-            if (lane == 0) {
+            if (pw == 0 && nq >= 2) mbar_wait(&q_empty[qb], ((nq - 2) >> 1) & 1);
+            if (pw == 0 && lane == 0) {
                 mbar_arrive_expect_tx(&q_full[qb], 2u * kHalf);
                 tma_load_3d(sQ + qb * 2 * kHalf, &p.tmap_q, 0, h, qs0, &q_full[qb]);
                 tma_load_3d(sQ + qb * 2 * kHalf + kHalf, &p.tmap_q, 64, h, qs0, &q_full[qb]);
@@ -1054,9 +1083,9 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
                         // shared prefix tokens [128 j, min(P, 128 j + 128)) through s0's table
                         const int t0 = j * kN, len = min(P, t0 + kN) - t0;
                         const int nf = len / br, nb = nf + len % br;
-                        if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
+                        if (pw == 0 && lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
                         __syncwarp();
-                        for (int b2 = lane; b2 < nb; b2 += 32) {
+                        for (int b2 = pw + kProd * lane; b2 < nb; b2 += 32 * kProd) {
                             const int tt = t0 + (b2 < nf ? b2 * br : nf * br + (b2 - nf));
                             const int blk = sl.pre_blk[tt >> 4];
                             const int row = (blk * p.H_kv + kvh) * B + (tt & (B - 1));
@@ -1070,9 +1099,9 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
                         // lane = one 16-token piece of one member (pieces are block-aligned
                         // because P is), split into single rows where it crosses the tile
                         const int c_lo = (j - n_pre) * kN, c_hi = min(col, c_lo + kN);
-                        if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(c_hi - c_lo) * 256u);
+                        if (pw == 0 && lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(c_hi - c_lo) * 256u);
                         __syncwarp();
-                        for (int gp = lane; gp < pcs; gp += 32) {
+                        for (int gp = pw + kProd * lane; gp < pcs; gp += 32 * kProd) {
                             int lo = 0, hi = nm - 1;  // member k of piece gp: last piece_off <= gp
                             while (lo < hi) {
                                 const int mid = (lo + hi + 1) >> 1;
@@ -1138,13 +1167,17 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&m_empty[qb]);
             mbar_wait(&q_full[qb], (nq >> 1) & 1);
+            const int tb = min((int)nq, 17) * 14;  // trace slots of this item (PA_PREFILL_TRACE)
+            if (lane == 0) PF_T(tb + 8);
             ++nq;
             for (int j = 0; j < min(n, 2); ++j) issue_S(qb);
             if (n <= 2 && lane == 0) umma_commit(&q_empty[qb]);
             if (n > 0 && nf++ > 0) mbar_wait(o_free, (nf - 2) & 1);
+            if (lane == 0) PF_T(tb + 9);
             for (int j = 0; j < n; ++j) {
                 mbar_wait(&v_full[gv & 1], (gv >> 1) & 1);
                 mbar_wait(p_full, np++ & 1);
+                if (lane == 0 && j < 4) PF_T(tb + 10 + j);
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t v = smem_u32(sV) + (gv & 1) * 2 * kHalf;
@@ -1171,12 +1204,13 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
         const uint32_t tO = tmem + 256 + hf * 64 + lane_off;
         uint32_t ns = 0, nq = 0;
         for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++nq) {
-            int tile, h, s0, nm, P, r0;
-            packed_item(pt, p, i, tile, h, s0, nm, P, r0);
             const uint32_t qb = nq & 1;
             mbar_wait(&m_full[qb], (nq >> 1) & 1);
+            const int tb = min((int)nq, 17) * 14;  // trace slots of this item (PA_PREFILL_TRACE)
+            if (tid == 0) PF_T(tb);
             const PackMem* mt = slots[qb].mem;
             const int rows = slots[qb].hdr[0], n_pre = slots[qb].hdr[2], n = slots[qb].hdr[3];
+            const int nm = slots[qb].hdr[4], P = slots[qb].hdr[5], qs0 = slots[qb].hdr[6], h = slots[qb].hdr[7];
             // this row's member (last row_off <= r), its position and packed segment
             const bool row_valid = r < rows;
             int k = 0;
@@ -1198,6 +1232,7 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
                 const uint32_t b = ns & 1;
                 const uint32_t tS = tmem + b * 128 + lane_off;
                 mbar_wait(&s_full[b], (ns >> 1) & 1);
+                if (tid == 0 && j < 5) PF_T(tb + 1 + j);
                 tc_fence_after();
                 float sa[32], sb[32];
                 tmem_ld32_nw(tS + hf * 64, sa);
@@ -1216,19 +1251,25 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
                     lo = mk.col_off - c0;
                     lim = seg_hi - c0;
                 }
-                const bool full = __all_sync(0xffffffffu, lo <= 0 && lim >= 64);
-                float mo = -INFINITY;
-                if (full) {
-#pragma unroll
-                    for (int u = 0; u < 32; u += 2)
-                        mo = fmaxf(fmaxf(mo, fmaxf(sa[u], sa[u + 1])), fmaxf(sb[u], sb[u + 1]));
-                } else {
+                const bool partial = !__all_sync(0xffffffffu, lo <= 0 && lim >= 64);
+                // a 32-column chunk no row of the warp sees takes no exponentials (P = 0): most
+                // of a packed tile's own-token columns belong to the other members
+                const bool live0 = !partial || __any_sync(0xffffffffu, lo < 32 && lim > 0 && lim > lo);
+                const bool live1 = !partial || __any_sync(0xffffffffu, lo < 64 && lim > 32 && lim > lo);
+                if (partial) {
+                    // columns outside [lo, lim) become -inf: they drop out of the maximum and
+                    // their weights are ex2(-inf) = 0 (also for NaN bit patterns in unused slots)
+                    const uint32_t w = (uint32_t)max(lim - lo, 0);
 #pragma unroll
                     for (int u = 0; u < 32; ++u) {
-                        if (u >= lo && u < lim) mo = fmaxf(mo, sa[u]);
-                        if (u + 32 >= lo && u + 32 < lim) mo = fmaxf(mo, sb[u]);
+                        sa[u] = (uint32_t)(u - lo) < w ? sa[u] : -INFINITY;
+                        sb[u] = (uint32_t)(u + 32 - lo) < w ? sb[u] : -INFINITY;
                     }
                 }
+                float mo = -INFINITY;
+#pragma unroll
+                for (int u = 0; u < 32; u += 2)
+                    mo = fmaxf(fmaxf(mo, fmaxf(sa[u], sa[u + 1])), fmaxf(sb[u], sb[u + 1]));
                 float* rd = red + (ns & 1) * 256;
                 rd[hf * 128 + r] = mo;
                 named_bar_sync_256();
@@ -1242,29 +1283,18 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
                 const float2 c2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-ms, -ms);
                 auto emit = [&](const float (&x)[32], int c0) {
                     uint32_t pk[16];
-                    if (full) {
 #pragma unroll
-                        for (int u = 0; u < 32; u += 2) {
-                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
-                            const float2 a = make_float2(ex2(e.x), ex2(e.y));
-                            rs2 = __fadd2_rn(rs2, a);
-                            pk[u / 2] = pack2<T>(a.x, a.y);
-                        }
-                    } else {
-#pragma unroll
-                        for (int u = 0; u < 32; u += 2) {
-                            const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
-                            float2 a = make_float2(ex2(e.x), ex2(e.y));
-                            a.x = (c0 + u >= lo && c0 + u < lim) ? a.x : 0.f;
-                            a.y = (c0 + u + 1 >= lo && c0 + u + 1 < lim) ? a.y : 0.f;
-                            rs2 = __fadd2_rn(rs2, a);
-                            pk[u / 2] = pack2<T>(a.x, a.y);
-                        }
+                    for (int u = 0; u < 32; u += 2) {
+                        const float2 e = ffma2(make_float2(x[u], x[u + 1]), c2, nm2);
+                        const float2 a = ex2_pair(e, u / 2);
+                        rs2 = __fadd2_rn(rs2, a);
+                        pk[u / 2] = pack2<T>(a.x, a.y);
                     }
                     tmem_st16(tS + hf * 32 + c0 / 2, pk);
                 };
-                emit(sa, 0);
-                emit(sb, 32);
+                const uint32_t zero[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+                if (live0) emit(sa, 0); else tmem_st16(tS + hf * 32, zero);
+                if (live1) emit(sb, 32); else tmem_st16(tS + hf * 32 + 16, zero);
                 if (j > 0) {
                     mbar_wait(o_done, (ns - 1) & 1);
                     tc_fence_after();
@@ -1291,12 +1321,16 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
             const float lt = l + lsum[(hf ^ 1) * 128 + r];
             named_bar_sync_256();
             const float inv = lt > 0.f ? 1.f / lt : 0.f;
-            const int qs0 = __ldg(p.query_start + s0) + r0;
-            T* orow = static_cast<T*>(p.out) + ((int64_t)(qs0 + r) * p.H + h) * 128 + hf * 64;
             if (n > 0) {
                 mbar_wait(o_done, (ns - 1) & 1);
                 tc_fence_after();
             }
+            if (tid == 0) PF_T(tb + 6);
+            // each warp writes its 32 rows x 64 columns in two 32-column chunks through its own
+            // 2 KB of shared memory (16-B pieces XOR-swizzled by row), so that the global stores
+            // cover 8 rows x 64 contiguous bytes per instruction instead of 32 rows x 16 bytes
+            unsigned char* stg = stage + (warp & 7) * 2048;
+            const int rw0 = (warp & 3) * 32;  // the warp's first row in the tile
 #pragma unroll
             for (int c0 = 0; c0 < 64; c0 += 32) {
                 float v[32];
@@ -1307,16 +1341,28 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
 #pragma unroll
                     for (int u = 0; u < 32; ++u) v[u] = 0.f;
                 }
-                if (row_valid) {
 #pragma unroll
-                    for (int c1 = 0; c1 < 32; c1 += 8) {
-                        alignas(16) T w[8];
+                for (int c1 = 0; c1 < 4; ++c1) {
+                    alignas(16) T w[8];
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) w[u] = Elem<T>::from_f32(v[c1 + u] * inv);
-                        *reinterpret_cast<uint4*>(orow + c0 + c1) = *reinterpret_cast<const uint4*>(w);
+                    for (int u = 0; u < 8; ++u) w[u] = Elem<T>::from_f32(v[c1 * 8 + u] * inv);
+                    *reinterpret_cast<uint4*>(stg + lane * 64 + ((c1 ^ ((lane >> 1) & 3)) * 16)) =
+                        *reinterpret_cast<const uint4*>(w);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int rr = k * 8 + (lane >> 2), ch = lane & 3;
+                    if (rw0 + rr < rows) {
+                        const uint4 x = *reinterpret_cast<const uint4*>(stg + rr * 64 + ((ch ^ ((rr >> 1) & 3)) * 16));
+                        T* dst = static_cast<T*>(p.out) + ((int64_t)(qs0 + rw0 + rr) * p.H + h) * 128 + hf * 64 + c0 +
+                                 ch * 8;
+                        *reinterpret_cast<uint4*>(dst) = x;
                     }
                 }
+                __syncwarp();
             }
+            if (tid == 0) PF_T(tb + 7);
             if (n > 0) {
                 tc_fence_before();
                 mbar_arrive(o_free);
@@ -1332,7 +1378,7 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
 }
 
 size_t prefill_packed_smem_bytes() {
-    return 1024 + (4 + 2 * kKStages + 2 * kVStages) * (size_t)kHalf + (512 + 256) * 4 + 2 * sizeof(PackSlot) +
+    return 1024 + (4 + 2 * kKStages + 2 * kVStages) * (size_t)kHalf + 8 * 2048 + (512 + 256) * 4 + 2 * sizeof(PackSlot) +
            21 * 8 + 16;
 }
 
@@ -1374,7 +1420,7 @@ cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int 
         auto kern = dtype == 1 ? paged_prefill_ws_kernel<__half> : paged_prefill_ws_kernel<__nv_bfloat16>;
         cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
         if (e != cudaSuccess) return e;
-        return launch_k(kern, grid, dim3(kThreadsV2), smem, stream, q);
+        return launch_k(kern, grid, dim3(kThreadsWs), smem, stream, q);
     }
     const size_t smem = prefill_split_smem_bytes();
     q.X = (max_query_len + kQ - 1) / kQ;
@@ -1383,7 +1429,7 @@ cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int 
     auto kern = dtype == 1 ? paged_prefill_split_kernel<__half> : paged_prefill_split_kernel<__nv_bfloat16>;
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
-    return launch_k(kern, grid, dim3(kThreadsV2), smem, stream, q);
+    return launch_k(kern, grid, dim3(kThreadsV3), smem, stream, q);
 }
 
 }  // namespace pa

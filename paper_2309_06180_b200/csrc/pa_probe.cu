@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) tma_probe_kernel(const __grid_constant__ 
                                                         int stages, int iters, uint32_t* sink) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem =
-        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+        tc::smem_align1024(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int box = rows * 128;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)nw * stages * box);

@@ -10,6 +10,42 @@
 namespace pa {
 namespace tc {
 
+// The dynamic shared memory base rounded up to 1024 B (128-byte-swizzle atoms) as an offset
+// from the shared-space pointer, so the compiler keeps the shared address space for every
+// pointer derived from it (LDS/STS); rounding a generic address as an integer loses it and
+// turns every plain access of the derived pointers into a generic LD/ST.
+__device__ __forceinline__ unsigned char* smem_align1024(unsigned char* raw) {
+    return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
+
+// 2^x for a pair on the FMA pipe (the exponential emulation of FlashAttention-4, for the
+// MUFU-bound softmax of the prompt kernels): x = j + f with j = rint(x) (magic-number
+// rounding), f in [-0.5, 0.5]; 2^f = 1 + f (c1 + f (c2 + f c3)), a relative minimax fit
+// with p(0) = 1 (max relative error 1.0e-4, below the f16 / bf16 rounding of P); j is added
+// to the exponent field.  x <= -127 (-inf included) gives +0 exactly.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -127.f);
+    x.y = fmaxf(x.y, -127.f);
+    const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));  // 1.5 * 2^23 + rint(x)
+    const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));  // rint(x)
+    const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);
+    float2 q = __ffma2_rn(f, make_float2(0.055008581f, 0.055008581f), make_float2(0.24221037f, 0.24221037f));
+    q = __ffma2_rn(q, f, make_float2(0.69328290f, 0.69328290f));
+    q = __ffma2_rn(q, f, make_float2(1.f, 1.f));
+    return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+// Softmax exponentials of pair k (0..15 of a 32-column chunk): every PA_EXP_EMU-th pair on
+// the FMA pipe, the rest on MUFU (0: all MUFU).
+#ifndef PA_EXP_EMU
+#define PA_EXP_EMU 0
+#endif
+// k is a constant after the callers' loop unrolling, so the choice folds at compile time.
+__device__ __forceinline__ float2 ex2_pair(float2 e, int k) {
+    if (PA_EXP_EMU > 0 && k % PA_EXP_EMU == PA_EXP_EMU - 1) return ex2_poly2(e);
+    return make_float2(ex2(e.x), ex2(e.y));
+}
+
 // ---- tcgen05 / TMA wrappers ------------------------------------------------------------
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),

@@ -38,6 +38,23 @@ def timed(fn, nbytes, reps=3):
     return round(best, 1)
 
 
+if "--l2" in sys.argv:  # L2-resident source (32 MiB of the tensor), 16-row boxes, 1-8 issuing warps
+    for rows in (16, 64):
+        for warps in (1, 2, 4, 8):
+            stages = max(2, min(16, (64 * 1024) // (rows * 128 * warps)))
+            iters = max(64, (48 << 20) // (rows * 128 * warps * sms) * 4)
+            nbytes = sms * warps * iters * rows * 128
+            nr = (32 << 20) // 256
+
+            def run():
+                r = f(buf.data_ptr(), nr, rows, warps, stages, iters, sms, sink.data_ptr(), st)
+                assert r == 0, r
+            run()
+            torch.cuda.synchronize()
+            g = timed(run, nbytes)
+            print(json.dumps({"kind": "tma_tensor_sw128_l2", "box_bytes": rows * 128, "warps_per_sm": warps,
+                              "stages_per_warp": stages, "gbs": g, "per_sm_gbs": round(g / sms, 2)}), flush=True)
+    sys.exit(0)
 for rows in (16, 32, 64, 128):
     for warps in (1, 2, 4):
         stages = max(2, min(16, (64 * 1024) // (rows * 128 * warps)))
