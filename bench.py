@@ -271,7 +271,9 @@ def run_ours(a, wl_full, world, rank, local):
     # the tcgen05 N1 kernel's persistent CTAs need work items (group, 4 heads) for at least two
     # rounds over the SMs; a TP=8 shard of C5 (12 heads per rank) has too few and runs coop
     # (measured: profiles/r02_tp_shard_tune.jsonl)
-    auto_grouped = {"c5_beam": 4}.get(wl_full.name, 0)
+    # c3_fork (samples right after the fork share all but their last block) runs it too;
+    # c3_parallel (samples diverged: unique/logical 0.72) stays on coop (258 vs 328 us)
+    auto_grouped = {"c5_beam": 4, "c3_fork": 6}.get(wl_full.name, 0)
     if auto_grouped and (wl.S // auto_grouped) * ((wl.H + 3) // 4) < 2 * props.multi_processor_count:
         auto_grouped = 0
     grouped = a.grouped if a.grouped >= 0 else auto_grouped

@@ -77,6 +77,7 @@ struct Tuning {
     int pz = 0;                            // PA_PZ: coop grid with the partition index slowest
     int shared_hpc = 0, shared_slots = 1;  // PA_SHARED_HPC / PA_SHARED_SLOTS (N1 CUDA-core kernel)
     bool pdl = true;                       // PA_PDL=0 disables programmatic dependent launch
+    int tc_split = 1;                      // PA_TC_SPLIT: N1 tcgen05 split context 0 never, 1 auto, 2 always
     int prefill = 0;                       // PA_PREFILL=2|3 forces a prompt kernel (0 = auto)
     bool e2e_zero_copy = false;            // PA_E2E_MODE=zerocopy
     int e2e_chunks = 4;                    // PA_E2E_CHUNKS
@@ -103,6 +104,7 @@ Tuning load_tuning() {
     t.shared_hpc = env_int("PA_SHARED_HPC", 0);
     t.shared_slots = env_int("PA_SHARED_SLOTS", 1);
     if (const char* v = getenv("PA_PDL")) t.pdl = v[0] != '0';
+    if (const char* v = getenv("PA_TC_SPLIT")) t.tc_split = std::max(0, std::min(2, atoi(v)));
     t.prefill = env_int("PA_PREFILL", 0);
     if (const char* v = getenv("PA_E2E_MODE")) t.e2e_zero_copy = std::strcmp(v, "zerocopy") == 0;
     t.e2e_chunks = env_int("PA_E2E_CHUNKS", 4);
@@ -144,14 +146,16 @@ int effective_partition(int partition_tokens) { return partition_tokens != 0 ? p
 
 int64_t pad16(int64_t x) { return (x + 15) / 16 * 16; }
 
-// Workspace layout: split completion words [S][H] uint64 | (split only) part_o
-// [S][H][NP][D] fp32 | part_ml [S][H][NP] float2.  No region needs zeroing (split_arrive).
+// Workspace layout: work-item counter (16 B, the persistent N1 kernel's) | split completion
+// words [S][H] uint64 | (split only) part_o [S][H][NP][D] fp32 | part_ml [S][H][NP] float2.
+// No region needs zeroing (epoch-tagged words, split_arrive).
 struct WsLayout {
-    int64_t counters, part_o, part_ml, total;
+    int64_t work, counters, part_o, part_ml, total;
 };
 WsLayout ws_layout(int64_t S, int64_t H, int64_t D, int64_t NP) {
     WsLayout L{};
     int64_t o = 0;
+    L.work = o;     o += 16;
     L.counters = o; o += pad16(S * H * 8);
     L.part_o = o;   if (NP > 1) o += S * H * NP * D * 4;
     L.part_ml = o;  if (NP > 1) o += S * H * NP * 8;
@@ -496,9 +500,24 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
     REQUIRE_PTR(value_cache, 16);
     REQUIRE_PTR(block_tables, 4);
     REQUIRE_PTR(context_lens, 4);
-    (void)max_context_len;  // the kernel walks each group's contexts whole (no grid sized by it)
-    if (workspace == nullptr || workspace_bytes < 16)
-        return fail(PA_ERR_WORKSPACE, "workspace of 16 bytes required (got %zu)", workspace ? workspace_bytes : (size_t)0);
+    // split context (a6): parts of 512 tokens per group from max_context_len (<= 0: W * B);
+    // the last part takes every position past it, so a low bound costs balance, not tokens.
+    // Auto: only when (group, head quad) items alone give the persistent CTAs fewer than 4
+    // rounds (measured: c3_parallel 498 -> 328 us with, c5_beam 320 -> 337 us with; DESIGN 7c)
+    const int64_t mcl = max_context_len > 0 ? max_context_len : (int64_t)max_blocks_per_seq * block_size;
+    int NPt = (int)std::max<int64_t>(1, std::min<int64_t>((mcl + 511) / 512, 1024));
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t unsplit = (int64_t)((num_seqs + group_size - 1) / group_size) * ((num_heads + 3) / 4);
+        const int mode = tuning().tc_split;
+        if (mode == 0 || (mode == 1 && unsplit >= 4LL * sms)) NPt = 1;
+    }
+    const WsLayout WL = ws_layout(num_seqs, num_heads, head_dim, NPt);
+    if (workspace == nullptr || (int64_t)workspace_bytes < WL.total)
+        return fail(PA_ERR_WORKSPACE, "workspace of %lld bytes required (pa_paged_attention_workspace_size; got %zu)",
+                    (long long)WL.total, workspace ? workspace_bytes : (size_t)0);
     REQUIRE_PTR(workspace, 16);
     static thread_local pa::GroupTcParams gp;  // ~1.8 KB of tensor maps, kept off the stack
     std::memset(&gp, 0, sizeof(gp));
@@ -532,7 +551,14 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
     gp.new_value = value;
     gp.block_tables = block_tables;
     gp.context_lens = context_lens;
-    gp.work_counter = static_cast<unsigned long long*>(workspace);
+    {
+        char* w = static_cast<char*>(workspace);
+        gp.work_counter = reinterpret_cast<unsigned long long*>(w + WL.work);
+        gp.counters = reinterpret_cast<unsigned long long*>(w + WL.counters);
+        gp.part_o = reinterpret_cast<float*>(w + WL.part_o);
+        gp.part_ml = reinterpret_cast<float2*>(w + WL.part_ml);
+        gp.NPt = NPt;
+    }
     gp.epoch = pa::next_epoch();
     gp.scale_log2 = (float)((double)scale * 1.4426950408889634);
     gp.log2B = log2B;
@@ -543,7 +569,7 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
     gp.S = num_seqs;
     gp.GM = group_size;
     gp.n_hp = (num_heads + 3) / 4;
-    const int64_t items = (int64_t)((num_seqs + group_size - 1) / group_size) * gp.n_hp;
+    const int64_t items = (int64_t)((num_seqs + group_size - 1) / group_size) * gp.n_hp * NPt;
     REQUIRE(items < (1LL << 31), "too many work items");
     gp.n_items = (int)items;
     gp.n_gorder = 0;

@@ -50,11 +50,13 @@ constexpr int kTileBytes = 2 * kTensor;     // 64 KB: [K|V][half][piece][head][1
 constexpr int kMaxGM = 8;
 constexpr int kListCap = 32 * kMaxGM;       // pieces of one 32-position chunk
 constexpr float kLazyTc = 8.f;              // P <= 2^8 between rescales
-constexpr int kThreadsTc = 192;             // warps: 0-3 softmax (head w = lane quadrant w), 4 producer, 5 MMA
+constexpr int kNCh = 4;                     // piece-list chunks in flight (scheduler -> producer)
+constexpr int kThreadsTc = 384;             // warps: 0-3 softmax (head w = lane quadrant w), 4 producer, 5 MMA,
+                                            // 6 scheduler, 7 split-context merges, 8-11 epilogue (head w - 8)
 // tensor memory columns: Q0 | Q1 (16-bit pairs, by item parity) | S0 | S1 | O; lanes
 // 32w..32w+31 = head w's members
 constexpr int kTmQ = 0, kTmS = 128, kSCols = 16 * kNH * kSlots, kTmO = kTmS + 2 * kSCols;
-constexpr int kNumBars = 2 * kBuf + 2 + 2 + 2 + 1 + 1 + 4 + 4 + 2;
+constexpr int kNumBars = 2 * kBuf + 2 + 2 + 2 + 1 + 1 + 4 + 4 + 2 + 2 * kNCh + 8 + 4;
 
 struct TileMeta {
     int ns, last;
@@ -63,13 +65,18 @@ struct TileMeta {
 
 struct TcItem {
     int s0, gmv, h[kNH], kvh[kNH];
+    int part;     // split-context part: piece positions [32 part, 32 part + 32) (the last part: to the end)
     unsigned st;  // bit w: head w of the quad exists (H % 4 tail: duplicates are not stored)
     bool quad;    // the 4 kv heads are consecutive (one 64-row box per piece half when B == 16)
 };
 
 __device__ __forceinline__ TcItem tc_item(const GroupTcParams& p, int i) {
     TcItem it;
-    const int gi = i / p.n_hp, hq = i - gi * p.n_hp;
+    // item = (group, part, head quad), group-major: a group's parts and quads are consecutive
+    const int per_g = p.n_hp * p.NPt;
+    const int gi = i / per_g, r = i - gi * per_g;
+    it.part = r / p.n_hp;
+    const int hq = r - it.part * p.n_hp;
     const int g = gi < p.n_gorder ? (int)p.gorder[gi] : gi;  // longest-first plan (scheduling only)
     it.s0 = g * p.GM;
     it.gmv = min(p.GM, p.S - it.s0);
@@ -104,11 +111,46 @@ __device__ __forceinline__ int fetch_item(unsigned long long* ctr, uint32_t epoc
         }
     }
 }
+
+// Split-context completion count of row sh (one call per part holding its tokens, after the
+// part's (m, L, O / L) is published): true for the part that completes the set of n.  The
+// word is (epoch << 32 | parts done); another launch's epoch counts as 0 and the completing
+// part stores 0 back, so the host never resets the counters (as the coop kernel's).
+__device__ __forceinline__ bool split_done(const GroupTcParams& p, int64_t sh, int n) {
+    unsigned long long* ctr = p.counters + sh;
+    const unsigned long long E = (unsigned long long)p.epoch << 32;
+    unsigned long long cur = 0ull;
+    for (;;) {
+        const unsigned long long want = ((cur & 0xffffffff00000000ull) == E ? cur : E) + 1ull;
+        const unsigned long long prev = atomicCAS(ctr, cur, want);
+        if (prev == cur) {
+            if ((int)(want & 0xffffffffull) < n) return false;
+            atomicExch(ctr, 0ull);
+            return true;
+        }
+        cur = prev;
+    }
+}
 }  // namespace
 
 #ifdef PA_TC_TRACE  // timing experiments (variant build): clock64 per tile of CTAs 0..7
 constexpr int kTrTiles = 1024;
 __device__ long long g_tc_trace[8 * kTrTiles * 8];
+__device__ unsigned long long g_tc_span[1024 * 4];
+__device__ long long g_tc_ep[8 * 64 * 8];  // CTAs 0..7, items 0..63: epilogue start, o_last seen, O stored, done
+#define TC_EP(item, ev)                                                                                      \
+    do {                                                                                                     \
+        if (blockIdx.x < 8 && (item) < 64 && lane == 0 && hh == 0) g_tc_ep[(blockIdx.x * 64 + (item)) * 8 + (ev)] = clock64(); \
+    } while (0)  // per CTA: globaltimer at entry, after pdl_wait, at exit; items
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TC_SPAN(ev, v)                                                     \
+    do {                                                                   \
+        if (blockIdx.x < 1024) g_tc_span[blockIdx.x * 4 + (ev)] = (v);    \
+    } while (0)
 #define TC_T(tile, ev)                                                                               \
     do {                                                                                             \
         if (blockIdx.x < 8 && (tile) < kTrTiles) g_tc_trace[(blockIdx.x * kTrTiles + (tile)) * 8 + (ev)] = clock64(); \
@@ -116,6 +158,12 @@ __device__ long long g_tc_trace[8 * kTrTiles * 8];
 #else
 #define TC_T(tile, ev) \
     do {               \
+    } while (0)
+#define TC_SPAN(ev, v) \
+    do {               \
+    } while (0)
+#define TC_EP(item, ev) \
+    do {                \
     } while (0)
 #endif
 
@@ -127,14 +175,16 @@ template <typename T>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     paged_attention_group_tc_kernel(const __grid_constant__ GroupTcParams p) {
     constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
-    constexpr int kProd = kNH, kMma = kNH + 1;  // warp roles; warps 0..kNH-1 run the softmax
+    constexpr int kProd = kNH, kMma = kNH + 1, kSched = kNH + 2, kMerge = kNH + 3, kEpi0 = kNH + 4;  // 0..kNH-1: softmax
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem =
         tc::smem_align1024(smem_raw);
     unsigned char* sT = smem;                         // kBuf x [K|V][half][piece][head][16][128 B]
     TileMeta* meta = reinterpret_cast<TileMeta*>(sT + kBuf * kTileBytes);
-    int2* list = reinterpret_cast<int2*>(meta + kBuf);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(list + kListCap);
+    int2* clist = reinterpret_cast<int2*>(meta + kBuf);  // kNCh x kListCap distinct pieces
+    int4* chdr = reinterpret_cast<int4*>((reinterpret_cast<uintptr_t>(clist + kNCh * kListCap) + 15) &
+                                         ~uintptr_t(15));  // kNCh: (item, pieces, last list of the item)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(chdr + kNCh);
     uint64_t* tile_full = bars;                 // kBuf: TMA bytes + producer arrive
     uint64_t* tile_empty = bars + kBuf;         // kBuf: MMA commit + kNH softmax warps
     uint64_t* q_full = bars + 2 * kBuf;         // 2 (by item parity): the softmax lanes wrote Q
@@ -145,8 +195,17 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     uint64_t* item_full = o_free + 1;           // 4: producer -> MMA + softmax
     uint64_t* item_empty = item_full + 4;       // 4: MMA + kNH softmax warps
     uint64_t* o_step = item_empty + 4;          // 2: P V number k on o_step[k & 1] (MMA warp only)
+    uint64_t* chunk_full = o_step + 2;          // kNCh: scheduler -> producer (a piece list is written)
+    uint64_t* chunk_empty = chunk_full + kNCh;  // kNCh: producer -> scheduler (the list has been issued)
+    uint64_t* job_full = chunk_empty + kNCh;    // 4: the kNH softmax warps published an item's split partials
+    uint64_t* job_empty = job_full + 4;         // 4: the merge warp took the job
+    uint64_t* st_full = job_empty + 4;          // 2: the softmax warps handed an item's (m, L) rows over
+    uint64_t* st_empty = st_full + 2;           // 2: the epilogue warps read them
     int* item_ring = reinterpret_cast<int*>(bars + kNumBars);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_ring + 4);
+    int* job_ring = item_ring + 4;              // 4 item indices (-1: no more jobs)
+    int* st_item = job_ring + 4;                // 2 item indices handed to the epilogue warps (-1: done)
+    float4* stats = reinterpret_cast<float4*>(st_item + 4);  // [2][kNH][32] (m, L, P V count, ctx) per row
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stats + 2 * kNH * 32);
     volatile int* pv_done = reinterpret_cast<volatile int*>(tmem_slot + 1);  // last completed P V (tile index)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -169,6 +228,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             mbar_init(&item_full[i], 1);
             mbar_init(&item_empty[i], 1 + kNH);
         }
+        for (int i = 0; i < kNCh; ++i) {
+            mbar_init(&chunk_full[i], 1);
+            mbar_init(&chunk_empty[i], 1);
+        }
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&job_full[i], kNH);
+            mbar_init(&job_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&st_full[i], kNH);
+            mbar_init(&st_empty[i], kNH);
+        }
         fence_mbar_init();
     }
     if (warp == kMma) tmem_alloc(tmem_slot, 512);
@@ -176,60 +247,107 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+#ifdef PA_TC_TRACE
+    if (tid == 0) TC_SPAN(0, gtimer());
+#endif
     pdl_wait();  // inputs of the preceding kernel on the stream are visible from here on
+#ifdef PA_TC_TRACE
+    if (tid == 0) TC_SPAN(1, gtimer());
+#endif
     pdl_launch_dependents();
     const int ppb_log = p.log2B - 4;  // 16-row pieces per block (log2)
 
-    if (warp == kProd) {
-        // ================================================================ producer ===
-        uint32_t tcount = 0;
+    if (warp == kSched) {
+        // ================================================================ scheduler ===
+        // Runs one item ahead of the MMA / softmax warps (and up to kNCh piece lists ahead of
+        // the producer): claims work items, writes each member's new K/V row to its cache
+        // slot, and turns the members' block tables into lists of distinct pieces, so the
+        // producer only issues copies and no item boundary waits on a global round trip.
+        // An item is claimed only once the previous one has started, so no CTA hoards work
+        // that an idle one could take at the end of the launch.
+        uint32_t ccount = 0;
+        auto take_chunk = [&]() -> int {
+            const int c = (int)(ccount % kNCh);
+            if (ccount >= (uint32_t)kNCh) mbar_wait(&chunk_empty[c], ((ccount / kNCh) - 1) & 1);
+            return c;
+        };
         for (uint32_t k = 0;; ++k) {
             const uint32_t slot = k & 3;
-            if (k >= 4) mbar_wait(&item_empty[slot], ((k - 4) >> 2) & 1);
-            int i = 0;
-            if (lane == 0) {
+            if (k >= 1) mbar_wait(&item_empty[(k - 1) & 3], ((k - 1) >> 2) & 1);  // item k-1 has started
+            int i = 0, myctx = 0, maxp = 0;
+            TcItem it;
+            for (bool first = k == 0;; first = false) {
                 // first item by CTA index, later ones from the shared counter
-                i = k == 0 ? (int)blockIdx.x : (int)gridDim.x + fetch_item(p.work_counter, p.epoch);
+                i = (int)blockIdx.x;
+                if (!first) {
+                    if (lane == 0) i = (int)gridDim.x + fetch_item(p.work_counter, p.epoch);
+                    i = __shfl_sync(0xffffffffu, i, 0);
+                }
+                if (i >= p.n_items) break;
+                it = tc_item(p, i);
+                myctx = lane < it.gmv ? max(0, __ldg(p.context_lens + it.s0 + lane)) : 0;
+                maxp = 0;
+#pragma unroll
+                for (int m = 0; m < kMaxGM; ++m) maxp = max(maxp, (__shfl_sync(0xffffffffu, myctx, m) + 15) >> 4);
+                if (it.part == 0 || 32 * it.part < maxp) break;
+                // a part past the group's longest context: so are the group's remaining items
+                // (parts are consecutive), which a counter-claimed item may skip for everyone
+                if (!first && lane == 0) {
+                    const long long gend = (long long)(i / (p.n_hp * p.NPt) + 1) * (p.n_hp * p.NPt) - gridDim.x;
+                    atomicMax(p.work_counter, ((unsigned long long)p.epoch << 32) | (unsigned long long)gend);
+                }
+            }
+            if (lane == 0) {
                 item_ring[slot] = i;
                 mbar_arrive(&item_full[slot]);
             }
-            i = __shfl_sync(0xffffffffu, i, 0);
-            if (i >= p.n_items) break;
-            const TcItem it = tc_item(p, i);
-            const int myctx = lane < it.gmv ? max(0, __ldg(p.context_lens + it.s0 + lane)) : 0;
-            int ctxs[kMaxGM];
-            int maxp = 0;
-#pragma unroll
-            for (int m = 0; m < kMaxGM; ++m) {
-                ctxs[m] = __shfl_sync(0xffffffffu, myctx, m);
-                if (m < it.gmv) maxp = max(maxp, (ctxs[m] + 15) >> 4);
+            if (i >= p.n_items) {  // terminal list: the producer stops
+#ifdef PA_TC_TRACE
+                if (lane == 0) TC_SPAN(3, k);
+#endif
+                const int c = take_chunk();
+                if (lane == 0) {
+                    chdr[c] = make_int4(i, 0, 1, 0);
+                    mbar_arrive(&chunk_full[c]);
+                }
+                break;
             }
+            // member's new token: written by the item of the part holding its last piece
+            const int mypart = myctx > 0 ? min(((myctx - 1) >> 4) >> 5, p.NPt - 1) : -1;
+            const int myblk = mypart == it.part
+                                  ? __ldg(p.block_tables + (int64_t)(it.s0 + lane) * p.W + ((myctx - 1) >> p.log2B))
+                                  : 0;
+            int ctxs[kMaxGM];
+#pragma unroll
+            for (int m = 0; m < kMaxGM; ++m) ctxs[m] = __shfl_sync(0xffffffffu, myctx, m);
             // reshape_and_cache of the step, first: member m's new K/V rows of the
             // quad's kv heads to slot ctx_m - 1, so that every piece below is read whole from
-            // the cache (one box per tensor and half); lane = (head w, K|V, 16-byte chunk group)
-            for (int m = 0; m < it.gmv; ++m) {
-                const int cm = ctxs[m];
-                if (cm <= 0) continue;
-                const int tp = cm - 1;
-                const int blk = __ldg(p.block_tables + (int64_t)(it.s0 + m) * p.W + (tp >> p.log2B));
-                const int w = lane >> 3, t = (lane >> 2) & 1, c4 = lane & 3;
-                if ((it.st >> w) & 1u) {
-                    const int kvw = sel4(it.kvh, w);
+            // the cache (one box per tensor and half); lane = row (member, head w, K|V)
+            for (int r0 = 0; r0 < it.gmv * 2 * kNH; r0 += 32) {
+                const int r = r0 + lane, m = min(r >> 3, kMaxGM - 1), w = (r >> 1) & 3, t = r & 1;
+                const int cm = __shfl_sync(0xffffffffu, myctx, m);
+                const int blk = __shfl_sync(0xffffffffu, myblk, m);
+                const int mp = __shfl_sync(0xffffffffu, mypart, m);
+                if (r < it.gmv * 2 * kNH && cm > 0 && mp == it.part && ((it.st >> w) & 1u)) {
+                    const int tp = cm - 1, kvw = sel4(it.kvh, w);
                     const int64_t dst = ((((int64_t)blk * p.H_kv + kvw) << p.log2B) + (tp & ((1 << p.log2B) - 1))) * 128;
                     const int64_t src = ((int64_t)(it.s0 + m) * p.H_kv + kvw) * 128;
                     const uint4* sp = reinterpret_cast<const uint4*>(static_cast<const T*>(t ? p.new_value : p.new_key) + src);
                     uint4* dp = reinterpret_cast<uint4*>(static_cast<T*>(t ? p.value_cache : p.key_cache) + dst);
+                    uint4 v[16];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) dp[c4 * 4 + u] = __ldg(sp + c4 * 4 + u);
+                    for (int u = 0; u < 16; ++u) v[u] = __ldg(sp + u);
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) dp[u] = v[u];
                 }
             }
-            fence_proxy_async_global();  // the rows above are read by this warp's TMA copies below
+            fence_proxy_async_global();  // the rows above are read by the producer's TMA copies
             __syncwarp();
-            const bool quad_box = it.quad && p.log2B == 4;  // the 4 kv heads' pieces are 64 adjacent rows
-            int fill = 0, b = 0;
-            unsigned char* tb = sT;
-            for (int p0 = 0; p0 < maxp; p0 += 32) {
+            const int pbeg = 32 * it.part, pend = it.part == p.NPt - 1 ? maxp : min(maxp, pbeg + 32);
+            for (int p0 = pbeg; p0 < max(pend, pbeg + 1); p0 += 32) {
                 // distinct pieces of 32 logical positions: lane = position
+                const int c = take_chunk();
+                int2* list = clist + c * kListCap;
                 const int pp = p0 + lane;
                 int id[kMaxGM];
 #pragma unroll
@@ -273,74 +391,101 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                     }
                 }
                 __syncwarp();
-                for (int q = 0; q < total;) {
-                    if (fill == 0) {
-                        b = (int)(tcount % kBuf);
-                        if (tcount >= (uint32_t)kBuf) mbar_wait(&tile_empty[b], ((tcount / kBuf) - 1) & 1);
-                        tb = sT + b * kTileBytes;
-                        if (lane == 0) TC_T(tcount, 0);
+                if (lane == 0) {
+                    chdr[c] = make_int4(i, total, p0 + 32 >= pend ? 1 : 0, 0);
+                    mbar_arrive(&chunk_full[c]);
+                }
+                ++ccount;
+            }
+        }
+    } else if (warp == kProd) {
+        // ================================================================ producer ===
+        // Issues the TMA copies of the scheduler's piece lists, kSlots pieces per tile
+        uint32_t tcount = 0, ccount = 0;
+        int fill = 0, b = 0;
+        unsigned char* tb = sT;
+        for (;;) {
+            const int c = (int)(ccount % kNCh);
+            mbar_wait(&chunk_full[c], (ccount / kNCh) & 1);
+            const volatile int* hv = reinterpret_cast<const volatile int*>(&chdr[c]);
+            const int i = hv[0], total = hv[1], last_chunk = hv[2];
+            if (i >= p.n_items) break;
+            const TcItem it = tc_item(p, i);
+            const int2* list = clist + c * kListCap;
+            const bool quad_box = it.quad && p.log2B == 4;  // the 4 kv heads' pieces are 64 adjacent rows
+            for (int q = 0; q < total;) {
+                if (fill == 0) {
+                    b = (int)(tcount % kBuf);
+                    if (tcount >= (uint32_t)kBuf) mbar_wait(&tile_empty[b], ((tcount / kBuf) - 1) & 1);
+                    tb = sT + b * kTileBytes;
+                    if (lane == 0) TC_T(tcount, 0);
+                }
+                // the next k2 pieces of the open tile are issued together
+                const int k2 = min(kSlots - fill, total - q);
+                uint64_t* bar = &tile_full[b];
+                if (lane == 0) {
+                    for (int jj = 0; jj < k2; ++jj) {
+                        const int y = list[q + jj].y;
+                        meta[b].p[fill + jj] = y >> 18;
+                        meta[b].own[fill + jj] = (y >> 10) & 0xff;
+                        meta[b].nrows[fill + jj] = (y >> 4) & 31;
                     }
-                    // the next k2 pieces of the open tile are issued together
-                    const int k2 = min(kSlots - fill, total - q);
-                    uint64_t* bar = &tile_full[b];
-                    if (lane == 0) {
-                        for (int jj = 0; jj < k2; ++jj) {
-                            const int y = list[q + jj].y;
-                            meta[b].p[fill + jj] = y >> 18;
-                            meta[b].own[fill + jj] = (y >> 10) & 0xff;
-                            meta[b].nrows[fill + jj] = (y >> 4) & 31;
+                    mbar_expect_tx(bar, (uint32_t)k2 * (uint32_t)kQuad * 4u);  // whole pieces: K, V x 2 halves
+                }
+                __syncwarp();
+                {   // whole pieces (rows past a context are read but never used; V's are zeroed
+                    // in shared memory by the softmax warps).  quad: lane = (piece, tensor,
+                    // half), the 4 kv heads' rows in ONE 64-row box; otherwise lane = (piece,
+                    // tensor, half, head), 16-row boxes
+                    const int jj = quad_box ? (lane >> 2) : (lane >> 4);
+                    const int t = lane & 1, cc = (lane >> 1) & 1, w = (lane >> 2) & 3;
+                    if (jj < k2 && (quad_box ? lane < 4 * k2 : true)) {
+                        const int2 ent = list[q + jj];
+                        const int blk = ent.x >> ppb_log, pc = ent.x & ((1 << ppb_log) - 1);
+                        unsigned char* dst = tb + t * kTensor + cc * kHalfReg + (fill + jj) * kQuad;
+                        if (quad_box) {
+                            tma_load_2d(dst, t ? &p.tmap_vq : &p.tmap_kq, cc * 64, (blk * p.H_kv + it.kvh[0]) << 4,
+                                        bar);
+                        } else {
+                            tma_load_2d(dst + w * kPiece, t ? &p.tmap_v[0] : &p.tmap_k[0], cc * 64,
+                                        ((blk * p.H_kv + sel4(it.kvh, w)) << p.log2B) | (pc << 4), bar);
                         }
-                        mbar_expect_tx(bar, (uint32_t)k2 * (uint32_t)kQuad * 4u);  // whole pieces: K, V x 2 halves
-                    }
-                    __syncwarp();
-                    {   // whole pieces (rows past a context are read but never used; V's are zeroed
-                        // in shared memory by the softmax warps).  quad: lane = (piece, tensor,
-                        // half), the 4 kv heads' rows in ONE 64-row box; otherwise lane = (piece,
-                        // tensor, half, head), 16-row boxes
-                        const int jj = quad_box ? (lane >> 2) : (lane >> 4);
-                        const int t = lane & 1, c = (lane >> 1) & 1, w = (lane >> 2) & 3;
-                        if (jj < k2 && (quad_box ? lane < 4 * k2 : true)) {
-                            const int2 ent = list[q + jj];
-                            const int blk = ent.x >> ppb_log, pc = ent.x & ((1 << ppb_log) - 1);
-                            unsigned char* dst = tb + t * kTensor + c * kHalfReg + (fill + jj) * kQuad;
-                            if (quad_box) {
-                                tma_load_2d(dst, t ? &p.tmap_vq : &p.tmap_kq, c * 64, (blk * p.H_kv + it.kvh[0]) << 4,
-                                            bar);
-                            } else {
-                                tma_load_2d(dst + w * kPiece, t ? &p.tmap_v[0] : &p.tmap_k[0], c * 64,
-                                            ((blk * p.H_kv + sel4(it.kvh, w)) << p.log2B) | (pc << 4), bar);
-                            }
-                        }
-                    }
-                    __syncwarp();
-                    fill += k2;
-                    q += k2;
-                    if (fill == kSlots) {
-                        if (lane == 0) {
-                            TC_T(tcount, 1);
-                            meta[b].ns = kSlots;
-                            meta[b].last = 0;
-                            mbar_arrive(&tile_full[b]);
-                        }
-                        ++tcount;
-                        fill = 0;
                     }
                 }
-                __syncwarp();  // every lane has read the chunk's list before it is rewritten
+                __syncwarp();
+                fill += k2;
+                q += k2;
+                // the item's last piece closes its tile (last = 1: no empty tile takes a buffer)
+                const bool item_end = last_chunk && q == total;
+                if (fill == kSlots || item_end) {
+                    if (lane == 0) {
+                        TC_T(tcount, 1);
+                        meta[b].ns = fill;
+                        meta[b].last = item_end ? 1 : 0;
+                        mbar_arrive(&tile_full[b]);
+                    }
+                    ++tcount;
+                    fill = 0;
+                }
             }
-            // close the item: its partial tile, or an empty one, carries last = 1
-            if (fill == 0) {
-                b = (int)(tcount % kBuf);
-                if (tcount >= (uint32_t)kBuf) mbar_wait(&tile_empty[b], ((tcount / kBuf) - 1) & 1);
+            __syncwarp();  // every lane has read the list before the scheduler rewrites it
+            if (lane == 0) mbar_arrive(&chunk_empty[c]);
+            ++ccount;
+            if (last_chunk && total == 0) {  // an item without pieces (every context 0): an empty tile closes it
+                if (fill == 0) {
+                    b = (int)(tcount % kBuf);
+                    if (tcount >= (uint32_t)kBuf) mbar_wait(&tile_empty[b], ((tcount / kBuf) - 1) & 1);
+                }
+                if (lane == 0) {
+                    TC_T(tcount, 1);
+                    meta[b].ns = fill;
+                    meta[b].last = 1;
+                    mbar_arrive(&tile_full[b]);
+                }
+                ++tcount;
+                fill = 0;
+                __syncwarp();
             }
-            if (lane == 0) {
-                TC_T(tcount, 1);
-                meta[b].ns = fill;
-                meta[b].last = 1;
-                mbar_arrive(&tile_full[b]);
-            }
-            ++tcount;
-            __syncwarp();
         }
     } else if (warp == kMma) {
         // ================================================================ MMA issuer ===
@@ -411,6 +556,21 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 uint32_t pend_t = 0;
                 for (;;) {
                     const int b = (int)(tcount % kBuf);
+#ifdef PA_TC_EARLY_PV
+                    if (pend_b >= 0) {
+                        // the pending P V goes first if its P is ready before the next tile's data
+                        // (item starts, late copies); otherwise S of the next tile first, as below
+                        const uint32_t psb = pend_t & 1, ppar = (pend_t >> 1) & 1;
+                        while (!mbar_test(&tile_full[b], (tcount / kBuf) & 1)) {
+                            if (mbar_test(&p_full[psb], ppar)) {
+                                issue_pv(pend_b, pend_t, pend_ns, started, false);
+                                started = true;
+                                pend_b = -1;
+                                break;
+                            }
+                        }
+                    }
+#endif
                     mbar_wait(&tile_full[b], (tcount / kBuf) & 1);
                     TC_T(tcount, 2);
                     ++tcount;
@@ -455,6 +615,166 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             }
         }
         __syncwarp();
+    } else if (warp == kMerge) {
+        // ================================================================ merges ===
+        // Split context (a6) off the softmax warps' path: for each job (an item with split
+        // members, whose O / L and (m, L) rows the softmax warps have stored), lane = row
+        // (member m = lane / 4, head w = lane % 4) counts its part in; the part that completes
+        // a row's set merges it: o = sum_j L_j 2^(m_j - M) o~_j / sum_j L_j 2^(m_j - M), in
+        // part order (deterministic whichever CTA merges).
+        for (uint32_t jc = 0;; ++jc) {
+            const uint32_t js = jc & 3;
+            mbar_wait(&job_full[js], (jc >> 2) & 1);
+            const int i = *reinterpret_cast<volatile int*>(&job_ring[js]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&job_empty[js]);
+            if (i < 0) break;
+            const TcItem it = tc_item(p, i);
+            const int m = lane >> 2, w = lane & 3;
+            const int ctx = m < it.gmv ? max(0, __ldg(p.context_lens + it.s0 + m)) : 0;
+            const int nps = max(1, min((ctx + 511) >> 9, p.NPt));
+            const bool split = m < it.gmv && ((it.st >> w) & 1u) && nps > 1 && it.part < nps;
+            const int64_t sh = (int64_t)(it.s0 + m) * p.H + sel4(it.h, w);
+            __threadfence();  // the softmax warps' partial rows (seen through job_full) before the count
+            const bool done = split && split_done(p, sh, nps);
+            unsigned todo = __ballot_sync(0xffffffffu, done);
+            if (todo) __threadfence();
+            while (todo) {  // whole warp merges row r: lane = 4 dims
+                const int r = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const int np = __shfl_sync(0xffffffffu, nps, r);
+                const int64_t shr = __shfl_sync(0xffffffffu, sh, r);
+                const float2* ml = p.part_ml + shr * p.NPt;
+                const float4* po = reinterpret_cast<const float4*>(p.part_o + shr * p.NPt * 128) + lane;
+                float M = -INFINITY, L = 0.f;
+                float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int j0 = 0; j0 < np; j0 += 4) {
+                    float2 mv[4];
+                    float4 pv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (j0 + u < np) {
+                            mv[u] = __ldcg(&ml[j0 + u]);
+                            pv[u] = __ldcg(po + (j0 + u) * 32);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (j0 + u < np) {
+                            const float Mn = fmaxf(M, mv[u].x);
+                            const float sc = ex2(M - Mn), wj = mv[u].y * ex2(mv[u].x - Mn);
+                            o.x = o.x * sc + wj * pv[u].x;
+                            o.y = o.y * sc + wj * pv[u].y;
+                            o.z = o.z * sc + wj * pv[u].z;
+                            o.w = o.w * sc + wj * pv[u].w;
+                            L = L * sc + wj;
+                            M = Mn;
+                        }
+                    }
+                }
+                const float il = 1.f / L;
+                uint2 st;
+                st.x = pack2<T>(o.x * il, o.y * il);
+                st.y = pack2<T>(o.z * il, o.w * il);
+                *reinterpret_cast<uint2*>(static_cast<T*>(p.out) + shr * 128 + 4 * lane) = st;
+            }
+        }
+    } else if (warp >= kEpi0) {
+        // ================================================================ epilogue ===
+        // Per item, after its last P V: O (this warp's lane quadrant = head hh) / L to `out`
+        // -- or, for rows with a split context, O / L and (m, L) for the merge warp -- so the
+        // softmax warps go straight on to the next item's scores
+        const int hh = warp - kEpi0;
+        const uint32_t tO = tmem + ((uint32_t)(32 * hh) << 16) + kTmO;
+        uint32_t ocount = 0;
+        uint32_t jcount = 0;
+        auto publish_job = [&](int item) {  // whole warp; the merge warp reads job_ring[slot]
+            const uint32_t js = jcount & 3;
+            if (lane == 0) {
+                if (jcount >= 4) mbar_wait(&job_empty[js], ((jcount >> 2) - 1) & 1);
+                if (hh == 0) job_ring[js] = item;
+                mbar_arrive(&job_full[js]);
+            }
+            ++jcount;
+            __syncwarp();
+        };
+        for (uint32_t e = 0;; ++e) {
+            const uint32_t es = e & 1;
+            mbar_wait(&st_full[es], (e >> 1) & 1);
+            const int i_cur = *reinterpret_cast<volatile int*>(&st_item[es]);
+            const volatile float* sv4 = reinterpret_cast<const volatile float*>(&stats[(es * kNH + hh) * 32 + lane]);
+            const float4 stv = make_float4(sv4[0], sv4[1], sv4[2], sv4[3]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&st_empty[es]);
+            if (i_cur < 0) break;
+            const TcItem it = tc_item(p, i_cur);
+            const bool member = lane < it.gmv;
+            const float mref = stv.x, l = stv.y;
+            const int npv = __float_as_int(stv.z), ctx = __float_as_int(stv.w);
+            TC_EP(e, 0);
+            if (npv > 0) {
+                mbar_wait(o_last, ocount & 1);  // one phase per item with tiles
+                ++ocount;
+                tc_fence_after();
+            }
+            TC_EP(e, 1);
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            // split context (a6): parts holding this member's tokens; with more than one,
+            // each part publishes (m, L, O / L) and the last to finish merges
+            const int nps = max(1, min((ctx + 511) >> 9, p.NPt));
+            const bool mine = member && ((it.st >> hh) & 1u) && it.part < nps;
+            const bool split = mine && nps > 1;
+            const bool store = mine && !split;
+            const int64_t sh = (int64_t)(it.s0 + lane) * p.H + sel4(it.h, hh);
+            T* orow = static_cast<T*>(p.out) + sh * 128;
+            float* prow = p.part_o + (sh * p.NPt + it.part) * 128;
+            // all of O in registers with one wait, then tensor memory is released to the next
+            // item's P V before the stores
+            float ov[4][32];
+            if (npv > 0) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld32_nw(tO + 32 * c, ov[c]);
+                tmem_ld_wait();
+                TC_EP(e, 4);
+                tc_fence_before();
+                mbar_arrive(o_free);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) ov[c][u] = 0.f;
+            }
+#pragma unroll
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+                const float (&v)[32] = ov[c0 >> 5];
+                if (split) {
+#pragma unroll
+                    for (int c1 = 0; c1 < 32; c1 += 4)
+                        *reinterpret_cast<float4*>(prow + c0 + c1) =
+                            make_float4(v[c1] * inv, v[c1 + 1] * inv, v[c1 + 2] * inv, v[c1 + 3] * inv);
+                }
+                if (store) {
+#pragma unroll
+                    for (int c1 = 0; c1 < 32; c1 += 8) {
+                        uint4 w;
+                        w.x = pack2<T>(v[c1] * inv, v[c1 + 1] * inv);
+                        w.y = pack2<T>(v[c1 + 2] * inv, v[c1 + 3] * inv);
+                        w.z = pack2<T>(v[c1 + 4] * inv, v[c1 + 5] * inv);
+                        w.w = pack2<T>(v[c1 + 6] * inv, v[c1 + 7] * inv);
+                        *reinterpret_cast<uint4*>(orow + c0 + c1) = w;
+                    }
+                }
+            }
+            TC_EP(e, 2);
+            // items with split members: (m, L) next to O / L, then a job for the merge warp
+            if (__any_sync(0xffffffffu, member && nps > 1 && it.part < nps)) {  // same in every epilogue warp
+                if (split) p.part_ml[sh * p.NPt + it.part] = make_float2(mref, l);
+                __syncwarp();
+                publish_job(i_cur);
+            }
+            TC_EP(e, 3);
+        }
+        publish_job(-1);
     } else {
         // ================================================================ softmax ===
         const int hh = warp;  // head w of the quad = TMEM lane quadrant w
@@ -464,8 +784,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         uint32_t tcount = 0, scount = 0, ocount = 0, nq = 0;
         // the members' query rows of this head into tensor memory (the A operand of S = Q K^T):
         // lane m = member m's row (16-bit pairs), signalled on q_full[nq & 1]
+        int ctx_next = 0;  // the next item's context length of this lane's member, loaded with its queries
         auto put_q = [&](const TcItem& q_it) {
             const bool mem = lane < q_it.gmv;  // tcgen05.st is warp-collective: other lanes store zeros
+            ctx_next = mem ? max(0, __ldg(p.context_lens + q_it.s0 + lane)) : 0;
             const uint4* src = reinterpret_cast<const uint4*>(static_cast<const T*>(p.query) +
                                                               ((int64_t)(q_it.s0 + (mem ? lane : 0)) * p.H +
                                                                sel4(q_it.h, hh)) * 128);
@@ -493,6 +815,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             mbar_arrive(&q_full[nq & 1]);
             ++nq;
         };
+        uint32_t nep = 0;  // items handed to the epilogue warps
         int i = 0;
         {
             mbar_wait(&item_full[0], 0);
@@ -508,9 +831,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&item_empty[slot]);
             if (i >= p.n_items) break;
+            const int i_cur = i;
             const TcItem it = tc_item(p, i);
             const bool member = lane < it.gmv;
-            const int ctx = member ? max(0, __ldg(p.context_lens + it.s0 + lane)) : 0;
+            const int ctx = ctx_next;  // loaded when this item's queries were (off the item boundary)
             float mref = -INFINITY, l = 0.f;
             int npv = 0;
             bool qnext = false;  // the next item's queries are in the other Q buffer already
@@ -633,41 +957,23 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 if (!qnext && i2 < p.n_items) put_q(tc_item(p, i2));
                 i = i2;
             }
-            // ---- epilogue: out row = O / l
-            if (npv > 0) {
-                mbar_wait(o_last, ocount & 1);  // one phase per item with tiles
-                ++ocount;
-                tc_fence_after();
+            // ---- hand the item's epilogue (O / L to out) to the epilogue warps
+            {
+                const uint32_t es = nep & 1;
+                if (nep >= 2) mbar_wait(&st_empty[es], ((nep >> 1) - 1) & 1);
+                stats[(es * kNH + hh) * 32 + lane] = make_float4(mref, l, __int_as_float(npv), __int_as_float(ctx));
+                if (hh == 0 && lane == 0) st_item[es] = i_cur;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&st_full[es]);
+                ++nep;
             }
-            const float inv = l > 0.f ? 1.f / l : 0.f;
-            const bool store = member && ((it.st >> hh) & 1u);
-            T* orow = static_cast<T*>(p.out) + ((int64_t)(it.s0 + lane) * p.H + sel4(it.h, hh)) * 128;
-#pragma unroll
-            for (int c0 = 0; c0 < 128; c0 += 32) {
-                float v[32];
-                if (npv > 0) {
-                    tmem_ld32_nw(tO + c0, v);
-                    tmem_ld_wait();
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) v[u] = 0.f;
-                }
-                if (store) {
-#pragma unroll
-                    for (int c1 = 0; c1 < 32; c1 += 8) {
-                        uint4 w;
-                        w.x = pack2<T>(v[c1] * inv, v[c1 + 1] * inv);
-                        w.y = pack2<T>(v[c1 + 2] * inv, v[c1 + 3] * inv);
-                        w.z = pack2<T>(v[c1 + 4] * inv, v[c1 + 5] * inv);
-                        w.w = pack2<T>(v[c1 + 6] * inv, v[c1 + 7] * inv);
-                        *reinterpret_cast<uint4*>(orow + c0 + c1) = w;
-                    }
-                }
-            }
-            if (npv > 0) {
-                tc_fence_before();
-                mbar_arrive(o_free);
-            }
+        }
+        {   // no more items
+            const uint32_t es = nep & 1;
+            if (nep >= 2) mbar_wait(&st_empty[es], ((nep >> 1) - 1) & 1);
+            if (hh == 0 && lane == 0) st_item[es] = -1;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&st_full[es]);
         }
     }
     tc_fence_before();
@@ -676,17 +982,36 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
+#ifdef PA_TC_TRACE
+    if (tid == 0) TC_SPAN(2, gtimer());
+#endif
 }
 
 #ifdef PA_TC_TRACE
+extern "C" int pa_debug_tc_trace_reset(void) {
+    void* a = nullptr;
+    void* b = nullptr;
+    cudaGetSymbolAddress(&a, g_tc_trace);
+    cudaGetSymbolAddress(&b, g_tc_span);
+    cudaMemset(a, 0, sizeof(g_tc_trace));
+    cudaGetSymbolAddress(&a, g_tc_ep);
+    cudaMemset(a, 0, sizeof(g_tc_ep));
+    return (int)cudaMemset(b, 0, sizeof(g_tc_span));
+}
+extern "C" int pa_debug_tc_ep(void* host_out, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host_out, g_tc_ep, bytes < sizeof(g_tc_ep) ? bytes : sizeof(g_tc_ep));
+}
+extern "C" int pa_debug_tc_span(void* host_out, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host_out, g_tc_span, bytes < sizeof(g_tc_span) ? bytes : sizeof(g_tc_span));
+}
 extern "C" int pa_debug_tc_trace(void* host_out, size_t bytes) {
     return (int)cudaMemcpyFromSymbol(host_out, g_tc_trace, bytes < sizeof(g_tc_trace) ? bytes : sizeof(g_tc_trace));
 }
 #endif
 
 size_t group_tc_smem_bytes() {
-    return 1024 + (size_t)kBuf * kTileBytes + kBuf * sizeof(TileMeta) + kListCap * sizeof(int2) + kNumBars * 8 +
-           4 * 4 + 16;
+    return 1024 + (size_t)kBuf * kTileBytes + kBuf * sizeof(TileMeta) + kNCh * kListCap * sizeof(int2) + 16 +
+           kNCh * sizeof(int4) + kNumBars * 8 + 12 * 4 + 16 + 2 * kNH * 32 * sizeof(float4) + 16;
 }
 
 cudaError_t launch_group_tc(const GroupTcParams& p, int dtype, cudaStream_t stream) {

@@ -112,6 +112,10 @@ struct GroupTcParams {
     const int32_t* block_tables;  // [S][W]
     const int32_t* context_lens;  // [S]
     unsigned long long* work_counter;  // 8 bytes of workspace: (epoch << 32 | items handed out)
+    unsigned long long* counters;      // [S*H] split-context completion words (epoch-tagged)
+    float* part_o;                     // [S][H][NPt][128] O / L of each part
+    float2* part_ml;                   // [S][H][NPt] (m, L) of each part, exp2 domain
+    int NPt;                           // parts per group (split context: 512 tokens each; the last to the end)
     uint32_t epoch;
     float scale_log2;
     int log2B, H, H_kv, G, W, S;

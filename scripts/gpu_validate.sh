@@ -1,8 +1,9 @@
 #!/bin/bash
-# Round-2 validation on one B200: GPU suite, smoke, default bench line.
+# Validation on one B200: GPU suite, smoke, default bench line, prompt-kernel bench.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.txt
 timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/bench.jsonl 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+timeout 600 python scripts/prefill_bench.py --no-cpu-baseline > gpurun_out/prefill_bench.jsonl 2> gpurun_out/prefill_bench.err

@@ -21,14 +21,36 @@ wl = make_config(name)
 x = materialize_torch(wl, "cuda")
 tb = tables_torch(wl, "cuda")
 out = torch.empty_like(x["query"])
+plan = pa.decode_plan(wl.context_lens)  # bench.py's longest-first order
 for _ in range(3):
     pa.paged_attention_decode_grouped(out, x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"],
                                       tb["block_tables"], tb["context_lens"], wl.scale, gs,
-                                      max_context_len=wl.max_context_len)
+                                      max_context_len=wl.max_context_len, seq_order=plan)
 torch.cuda.synchronize()
+L = _lib.raw()
+L.pa_debug_tc_trace_reset.restype = ctypes.c_int
+assert L.pa_debug_tc_trace_reset() == 0
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+pa.paged_attention_decode_grouped(out, x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"],
+                                  tb["block_tables"], tb["context_lens"], wl.scale, gs,
+                                  max_context_len=wl.max_context_len, seq_order=plan)
+e1.record()
+torch.cuda.synchronize()
+span = np.zeros(1024 * 4, np.uint64)
+L.pa_debug_tc_span.restype = ctypes.c_int
+assert L.pa_debug_tc_span(span.ctypes.data, span.nbytes) == 0
+sp = span.reshape(1024, 4).astype(np.int64)
+sp = sp[sp[:, 0] > 0]
+t0 = sp[:, 0].min()
+print(json.dumps({"launch_event_us": e0.elapsed_time(e1) * 1e3, "ctas": len(sp),
+                  "entry_us_max": float((sp[:, 0].max() - t0) / 1e3),
+                  "pdl_wait_us_max": float((sp[:, 1] - sp[:, 0]).max() / 1e3),
+                  "exit_us": [float(np.percentile(sp[:, 2] - t0, q) / 1e3) for q in (0, 10, 50, 90, 100)],
+                  "items_per_cta": [int(np.percentile(sp[:, 3], q)) for q in (0, 50, 100)]}))
 NT = 1024
 buf = np.zeros(8 * NT * 8, np.int64)
-L = _lib.raw()
 L.pa_debug_tc_trace.restype = ctypes.c_int
 assert L.pa_debug_tc_trace(buf.ctypes.data, buf.nbytes) == 0
 tr = buf.reshape(8, NT, 8)
@@ -54,3 +76,35 @@ for c in range(8):
 t0 = tr[0][tr[0] > 0].min()
 for i in range(40):
     print(i, [int(v - t0) if v > 0 else -1 for v in tr[0, i, :8]])
+# epilogue stamps of the softmax warps (items 0..63 of CTAs 0..7): start, o_last seen, O
+# stored + o_free, job published; relative to the tile trace's first stamp
+ep = np.zeros(8 * 64 * 8, np.int64)
+L.pa_debug_tc_ep.restype = ctypes.c_int
+assert L.pa_debug_tc_ep(ep.ctypes.data, ep.nbytes) == 0
+ep = ep.reshape(8, 64, 8)
+d01, d12, d23, d14 = [], [], [], []
+for c in range(8):
+    for it in range(64):
+        e = ep[c, it]
+        if (e[:5] > 0).all():
+            d01.append(e[1] - e[0]); d12.append(e[2] - e[1]); d23.append(e[3] - e[2]); d14.append(e[4] - e[1])
+print(json.dumps({"epilogue_items": len(d01), "wait_o_last_cyc_med": float(np.median(d01)) if d01 else None,
+                  "o_store_cyc_med": float(np.median(d12)) if d12 else None,
+                  "split_publish_cyc_med": float(np.median(d23)) if d23 else None,
+                  "o_tmem_ld_cyc_med": float(np.median(d14)) if d14 else None}))
+for it in range(6):
+    print("ep", it, [int(v - t0) if v > 0 else -1 for v in ep[0, it, :5]])
+# where CTA 0..7's time goes: per-tile MMA-saw periods, excess over the median period
+gaps = []
+for c in range(8):
+    t = tr[c]
+    n = int((t[:, 2] > 0).sum())
+    per = np.diff(t[:n, 2])
+    med = np.median(per)
+    ex = per - med
+    top = np.argsort(-ex)[:8]
+    gaps.append({"cta": c, "tiles": n, "span_cyc": int(t[n - 1, 2] - t[0, 2]), "median": float(med),
+                 "excess_total": int(ex[ex > 0].sum()), "excess_over_2x": int(ex[per > 2 * med].sum()),
+                 "top": [(int(i), int(per[i])) for i in top]})
+for g in gaps:
+    print(json.dumps(g))

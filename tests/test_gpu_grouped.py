@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 pa = pytest.importorskip("paper_2309_06180_b200")
 
 
-def grouped_step(wl, gs, x=None):
+def grouped_step(wl, gs, x=None, mcl=None):
     x = x or materialize_torch(wl, "cuda")
     tb = tables_torch(wl, "cuda")
     if len(wl.block_mapping):
@@ -23,7 +23,7 @@ def grouped_step(wl, gs, x=None):
     out = torch.full_like(x["query"], float("nan"))
     pa.paged_attention_decode_grouped(out, x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"],
                                       tb["block_tables"], tb["context_lens"], wl.scale, gs,
-                                      max_context_len=wl.max_context_len)
+                                      max_context_len=wl.max_context_len if mcl is None else mcl)
     torch.cuda.synchronize()
     return out, x
 
@@ -58,6 +58,21 @@ def test_grouped_decode_context_edges():
     assert np.array_equal(bits(x["key_cache"]), rkc) and np.array_equal(bits(x["value_cache"]), rvc)
     assert max_abs(out, ref) <= TOL["f16"]
     assert not out[0].any()
+
+
+@pytest.mark.parametrize("mcl", [512, 1000, 0])
+def test_grouped_decode_split_parts_vs_oracle(mcl):
+    """Split context (a6) in the tcgen05 kernel: parts of 512 tokens per group, the last part
+    taking every position past the bound max_context_len gives (512: no split; 1000: two
+    parts, the second absorbing contexts up to 2048; 0: W * B, four parts), members of one
+    group with 1..4 parts of their own, merged by the last part to finish."""
+    ctx = [2048, 1500, 600, 513, 512, 511, 100, 1, 1025, 1024, 0, 2000]
+    wl = make_config("explicit", ctx=ctx, H=8, H_kv=8, D=128, B=16, dtype="f16", seed=11)
+    out, x = grouped_step(wl, 4, mcl=mcl)
+    ref, rkc, rvc = oracle_step(wl)
+    assert np.array_equal(bits(x["key_cache"]), rkc) and np.array_equal(bits(x["value_cache"]), rvc)
+    assert not torch.isnan(out).any()
+    assert max_abs(out, ref) <= TOL["f16"]
 
 
 @pytest.mark.parametrize("name,gs", [("c5_beam", 4), ("c3_parallel", 6)])
