@@ -78,6 +78,7 @@ struct Tuning {
     int shared_hpc = 0, shared_slots = 1;  // PA_SHARED_HPC / PA_SHARED_SLOTS (N1 CUDA-core kernel)
     bool pdl = true;                       // PA_PDL=0 disables programmatic dependent launch
     int tc_split = 1;                      // PA_TC_SPLIT: N1 tcgen05 split context 0 never, 1 auto, 2 always
+    int tc_part_log = 5;                   // split part = 512 tokens (the workspace's partition; 256 measured no faster)
     int prefill = 0;                       // PA_PREFILL=2|3 forces a prompt kernel (0 = auto)
     bool e2e_zero_copy = false;            // PA_E2E_MODE=zerocopy
     int e2e_chunks = 4;                    // PA_E2E_CHUNKS
@@ -505,7 +506,9 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
     // Auto: only when (group, head quad) items alone give the persistent CTAs fewer than 4
     // rounds (measured: c3_parallel 498 -> 328 us with, c5_beam 320 -> 337 us with; DESIGN 7c)
     const int64_t mcl = max_context_len > 0 ? max_context_len : (int64_t)max_blocks_per_seq * block_size;
-    int NPt = (int)std::max<int64_t>(1, std::min<int64_t>((mcl + 511) / 512, 1024));
+    const int part_log = tuning().tc_part_log;
+    const int64_t part_tok = 16LL << part_log;
+    int NPt = (int)std::max<int64_t>(1, std::min<int64_t>((mcl + part_tok - 1) / part_tok, 1024));
     {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
@@ -558,6 +561,7 @@ pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, cons
         gp.part_o = reinterpret_cast<float*>(w + WL.part_o);
         gp.part_ml = reinterpret_cast<float2*>(w + WL.part_ml);
         gp.NPt = NPt;
+        gp.part_log = part_log;
     }
     gp.epoch = pa::next_epoch();
     gp.scale_log2 = (float)((double)scale * 1.4426950408889634);

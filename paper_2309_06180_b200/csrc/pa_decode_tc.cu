@@ -37,26 +37,29 @@ constexpr int kNH = 4;                      // query heads per work item (one TM
 #ifndef PA_TC_SLOTS
 #define PA_TC_SLOTS 2
 #endif
-#ifndef PA_TC_BUF
-#define PA_TC_BUF 3
+#ifndef PA_TC_KBUF
+#define PA_TC_KBUF 2
+#endif
+#ifndef PA_TC_VBUF
+#define PA_TC_VBUF 4
 #endif
 constexpr int kSlots = PA_TC_SLOTS;         // 16-row block pieces per MMA tile
-constexpr int kBuf = PA_TC_BUF;             // tile buffers in shared memory
+constexpr int kBK = PA_TC_KBUF;             // K tile buffers (free once S = Q K^T has completed)
+constexpr int kBV = PA_TC_VBUF;             // V tile buffers (free once P V has completed)
 constexpr int kPiece = 16 * 128;            // [16 rows][64 cols] swizzled, 2-byte elements
 constexpr int kQuad = kNH * kPiece;         // one piece, the item's kv heads stacked: [64 rows][128 B] = 8 KB
 constexpr int kHalfReg = kSlots * kQuad;    // one 64-column half of the tile: 16 KB
-constexpr int kTensor = 2 * kHalfReg;       // K (or V) of the tile: 32 KB
-constexpr int kTileBytes = 2 * kTensor;     // 64 KB: [K|V][half][piece][head][16 rows][128 B]
+constexpr int kTensor = 2 * kHalfReg;       // K (or V) of a tile: 32 KB [half][piece][head][16 rows][128 B]
 constexpr int kMaxGM = 8;
 constexpr int kListCap = 32 * kMaxGM;       // pieces of one 32-position chunk
 constexpr float kLazyTc = 8.f;              // P <= 2^8 between rescales
 constexpr int kNCh = 4;                     // piece-list chunks in flight (scheduler -> producer)
-constexpr int kThreadsTc = 384;             // warps: 0-3 softmax (head w = lane quadrant w), 4 producer, 5 MMA,
-                                            // 6 scheduler, 7 split-context merges, 8-11 epilogue (head w - 8)
+constexpr int kThreadsTc = 384;             // warps: 0-3 softmax (head w = lane quadrant w), 4 K producer,
+                                            // 5 MMA, 6 scheduler, 7 V producer, 8-11 epilogue (head w - 8)
 // tensor memory columns: Q0 | Q1 (16-bit pairs, by item parity) | S0 | S1 | O; lanes
 // 32w..32w+31 = head w's members
 constexpr int kTmQ = 0, kTmS = 128, kSCols = 16 * kNH * kSlots, kTmO = kTmS + 2 * kSCols;
-constexpr int kNumBars = 2 * kBuf + 2 + 2 + 2 + 1 + 1 + 4 + 4 + 2 + 2 * kNCh + 8 + 4;
+constexpr int kNumBars = 2 * kBK + 2 * kBV + 2 + 2 + 2 + 1 + 1 + 4 + 4 + 2 + 2 * kNCh + 4;
 
 struct TileMeta {
     int ns, last;
@@ -65,7 +68,7 @@ struct TileMeta {
 
 struct TcItem {
     int s0, gmv, h[kNH], kvh[kNH];
-    int part;     // split-context part: piece positions [32 part, 32 part + 32) (the last part: to the end)
+    int part;     // split-context part: piece positions [part << part_log, (part + 1) << part_log) (the last: to the end)
     unsigned st;  // bit w: head w of the quad exists (H % 4 tail: duplicates are not stored)
     bool quad;    // the 4 kv heads are consecutive (one 64-row box per piece half when B == 16)
 };
@@ -175,19 +178,23 @@ template <typename T>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     paged_attention_group_tc_kernel(const __grid_constant__ GroupTcParams p) {
     constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
-    constexpr int kProd = kNH, kMma = kNH + 1, kSched = kNH + 2, kMerge = kNH + 3, kEpi0 = kNH + 4;  // 0..kNH-1: softmax
+    constexpr int kProd = kNH, kMma = kNH + 1, kSched = kNH + 2, kVProd = kNH + 3, kEpi0 = kNH + 4;  // 0..kNH-1: softmax
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem =
         tc::smem_align1024(smem_raw);
-    unsigned char* sT = smem;                         // kBuf x [K|V][half][piece][head][16][128 B]
-    TileMeta* meta = reinterpret_cast<TileMeta*>(sT + kBuf * kTileBytes);
-    int2* clist = reinterpret_cast<int2*>(meta + kBuf);  // kNCh x kListCap distinct pieces
+    unsigned char* sK = smem;                         // kBK x K [half][piece][head][16][128 B]
+    unsigned char* sV = sK + kBK * kTensor;           // kBV x V, same
+    TileMeta* meta = reinterpret_cast<TileMeta*>(sV + kBV * kTensor);  // [kBV], written with V
+    int2* kmeta = reinterpret_cast<int2*>(meta + kBV);                   // [kBK] (pieces, last), written with K
+    int2* clist = kmeta + kBK;                        // kNCh x kListCap distinct pieces
     int4* chdr = reinterpret_cast<int4*>((reinterpret_cast<uintptr_t>(clist + kNCh * kListCap) + 15) &
                                          ~uintptr_t(15));  // kNCh: (item, pieces, last list of the item)
     uint64_t* bars = reinterpret_cast<uint64_t*>(chdr + kNCh);
-    uint64_t* tile_full = bars;                 // kBuf: TMA bytes + producer arrive
-    uint64_t* tile_empty = bars + kBuf;         // kBuf: MMA commit + kNH softmax warps
-    uint64_t* q_full = bars + 2 * kBuf;         // 2 (by item parity): the softmax lanes wrote Q
+    uint64_t* k_full = bars;                    // kBK: K bytes + K producer arrive
+    uint64_t* k_empty = k_full + kBK;           // kBK: MMA commit after S
+    uint64_t* v_full = k_empty + kBK;           // kBV: V bytes + V producer arrive (meta written)
+    uint64_t* v_empty = v_full + kBV;           // kBV: MMA commit after P V + kNH softmax warps
+    uint64_t* q_full = v_empty + kBV;           // 2 (by item parity): the softmax lanes wrote Q
     uint64_t* s_full = q_full + 2;              // [S buffer]
     uint64_t* p_full = s_full + 2;              // [S buffer]: the softmax lanes
     uint64_t* o_last = p_full + 2;              // 1: an item's last P V has completed
@@ -197,22 +204,23 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     uint64_t* o_step = item_empty + 4;          // 2: P V number k on o_step[k & 1] (MMA warp only)
     uint64_t* chunk_full = o_step + 2;          // kNCh: scheduler -> producer (a piece list is written)
     uint64_t* chunk_empty = chunk_full + kNCh;  // kNCh: producer -> scheduler (the list has been issued)
-    uint64_t* job_full = chunk_empty + kNCh;    // 4: the kNH softmax warps published an item's split partials
-    uint64_t* job_empty = job_full + 4;         // 4: the merge warp took the job
-    uint64_t* st_full = job_empty + 4;          // 2: the softmax warps handed an item's (m, L) rows over
+    uint64_t* st_full = chunk_empty + kNCh;     // 2: the softmax warps handed an item's (m, L) rows over
     uint64_t* st_empty = st_full + 2;           // 2: the epilogue warps read them
     int* item_ring = reinterpret_cast<int*>(bars + kNumBars);
-    int* job_ring = item_ring + 4;              // 4 item indices (-1: no more jobs)
-    int* st_item = job_ring + 4;                // 2 item indices handed to the epilogue warps (-1: done)
+    int* st_item = item_ring + 4;               // 2 item indices handed to the epilogue warps (-1: done)
     float4* stats = reinterpret_cast<float4*>(st_item + 4);  // [2][kNH][32] (m, L, P V count, ctx) per row
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stats + 2 * kNH * 32);
     volatile int* pv_done = reinterpret_cast<volatile int*>(tmem_slot + 1);  // last completed P V (tile index)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int i = 0; i < kBuf; ++i) {
-            mbar_init(&tile_full[i], 1);
-            mbar_init(&tile_empty[i], 1 + kNH);
+        for (int i = 0; i < kBK; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+        }
+        for (int i = 0; i < kBV; ++i) {
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1 + kNH);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&q_full[i], 32 * kNH);
@@ -230,11 +238,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         for (int i = 0; i < kNCh; ++i) {
             mbar_init(&chunk_full[i], 1);
-            mbar_init(&chunk_empty[i], 1);
-        }
-        for (int i = 0; i < 4; ++i) {
-            mbar_init(&job_full[i], kNH);
-            mbar_init(&job_empty[i], 1);
+            mbar_init(&chunk_empty[i], 2);  // K and V producers
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&st_full[i], kNH);
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 maxp = 0;
 #pragma unroll
                 for (int m = 0; m < kMaxGM; ++m) maxp = max(maxp, (__shfl_sync(0xffffffffu, myctx, m) + 15) >> 4);
-                if (it.part == 0 || 32 * it.part < maxp) break;
+                if (it.part == 0 || (it.part << p.part_log) < maxp) break;
                 // a part past the group's longest context: so are the group's remaining items
                 // (parts are consecutive), which a counter-claimed item may skip for everyone
                 if (!first && lane == 0) {
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 break;
             }
             // member's new token: written by the item of the part holding its last piece
-            const int mypart = myctx > 0 ? min(((myctx - 1) >> 4) >> 5, p.NPt - 1) : -1;
+            const int mypart = myctx > 0 ? min(((myctx - 1) >> 4) >> p.part_log, p.NPt - 1) : -1;
             const int myblk = mypart == it.part
                                   ? __ldg(p.block_tables + (int64_t)(it.s0 + lane) * p.W + ((myctx - 1) >> p.log2B))
                                   : 0;
@@ -343,7 +347,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             }
             fence_proxy_async_global();  // the rows above are read by the producer's TMA copies
             __syncwarp();
-            const int pbeg = 32 * it.part, pend = it.part == p.NPt - 1 ? maxp : min(maxp, pbeg + 32);
+            const int pbeg = it.part << p.part_log, pend = it.part == p.NPt - 1 ? maxp : min(maxp, pbeg + (1 << p.part_log));
             for (int p0 = pbeg; p0 < max(pend, pbeg + 1); p0 += 32) {
                 // distinct pieces of 32 logical positions: lane = position
                 const int c = take_chunk();
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
                 for (int m = 0; m < kMaxGM; ++m) {
                     id[m] = -1;
-                    if (m < it.gmv && pp < ((ctxs[m] + 15) >> 4)) {
+                    if (m < it.gmv && pp < pend && pp < ((ctxs[m] + 15) >> 4)) {
                         const int blk =
                             __ldg(p.block_tables + (int64_t)(it.s0 + m) * p.W + ((pp << 4) >> p.log2B));
                         id[m] = (blk << ppb_log) | (pp & ((1 << ppb_log) - 1));
@@ -398,12 +402,37 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 ++ccount;
             }
         }
-    } else if (warp == kProd) {
-        // ================================================================ producer ===
-        // Issues the TMA copies of the scheduler's piece lists, kSlots pieces per tile
+    } else if (warp == kProd || warp == kVProd) {
+        // ================================================================ producers ===
+        // Two warps issue the TMA copies of the scheduler's piece lists, kSlots pieces per
+        // tile: K into the K ring (a buffer is free again once S has completed) and V into
+        // the deeper V ring (free once P V has completed), so K of later tiles is not held
+        // back by the softmax -> P V chain.  Both walk the same lists with the same tiling.
+        const bool isv = warp == kVProd;
+        const int nbuf = isv ? kBV : kBK;
+        uint64_t* fullb = isv ? v_full : k_full;
+        uint64_t* emptyb = isv ? v_empty : k_empty;
+        unsigned char* base = isv ? sV : sK;
+        const CUtensorMap* mq = isv ? &p.tmap_vq : &p.tmap_kq;
+        const CUtensorMap* m1 = isv ? &p.tmap_v[0] : &p.tmap_k[0];
         uint32_t tcount = 0, ccount = 0;
         int fill = 0, b = 0;
-        unsigned char* tb = sT;
+        unsigned char* tb = base;
+        auto acquire = [&]() {
+            b = (int)(tcount % nbuf);
+            if (tcount >= (uint32_t)nbuf) mbar_wait(&emptyb[b], ((tcount / nbuf) - 1) & 1);
+            tb = base + b * kTensor;
+        };
+        auto publish = [&](int ns, int last) {  // lane 0
+            if (isv) {
+                meta[b].ns = ns;
+                meta[b].last = last;
+            } else {
+                kmeta[b] = make_int2(ns, last);
+                TC_T(tcount, 1);
+            }
+            mbar_arrive(&fullb[b]);
+        };
         for (;;) {
             const int c = (int)(ccount % kNCh);
             mbar_wait(&chunk_full[c], (ccount / kNCh) & 1);
@@ -415,39 +444,37 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             const bool quad_box = it.quad && p.log2B == 4;  // the 4 kv heads' pieces are 64 adjacent rows
             for (int q = 0; q < total;) {
                 if (fill == 0) {
-                    b = (int)(tcount % kBuf);
-                    if (tcount >= (uint32_t)kBuf) mbar_wait(&tile_empty[b], ((tcount / kBuf) - 1) & 1);
-                    tb = sT + b * kTileBytes;
-                    if (lane == 0) TC_T(tcount, 0);
+                    acquire();
+                    if (lane == 0 && !isv) TC_T(tcount, 0);
                 }
                 // the next k2 pieces of the open tile are issued together
                 const int k2 = min(kSlots - fill, total - q);
-                uint64_t* bar = &tile_full[b];
+                uint64_t* bar = &fullb[b];
                 if (lane == 0) {
-                    for (int jj = 0; jj < k2; ++jj) {
-                        const int y = list[q + jj].y;
-                        meta[b].p[fill + jj] = y >> 18;
-                        meta[b].own[fill + jj] = (y >> 10) & 0xff;
-                        meta[b].nrows[fill + jj] = (y >> 4) & 31;
+                    if (isv) {
+                        for (int jj = 0; jj < k2; ++jj) {
+                            const int y = list[q + jj].y;
+                            meta[b].p[fill + jj] = y >> 18;
+                            meta[b].own[fill + jj] = (y >> 10) & 0xff;
+                            meta[b].nrows[fill + jj] = (y >> 4) & 31;
+                        }
                     }
-                    mbar_expect_tx(bar, (uint32_t)k2 * (uint32_t)kQuad * 4u);  // whole pieces: K, V x 2 halves
+                    mbar_expect_tx(bar, (uint32_t)k2 * (uint32_t)kQuad * 2u);  // whole pieces, 2 halves
                 }
                 __syncwarp();
                 {   // whole pieces (rows past a context are read but never used; V's are zeroed
-                    // in shared memory by the softmax warps).  quad: lane = (piece, tensor,
-                    // half), the 4 kv heads' rows in ONE 64-row box; otherwise lane = (piece,
-                    // tensor, half, head), 16-row boxes
-                    const int jj = quad_box ? (lane >> 2) : (lane >> 4);
-                    const int t = lane & 1, cc = (lane >> 1) & 1, w = (lane >> 2) & 3;
-                    if (jj < k2 && (quad_box ? lane < 4 * k2 : true)) {
+                    // in shared memory by the softmax warps).  quad: lane = (piece, half), the 4
+                    // kv heads' rows in ONE 64-row box; otherwise lane = (piece, half, head)
+                    const int jj = quad_box ? (lane >> 1) : (lane >> 3);
+                    const int cc = quad_box ? (lane & 1) : ((lane >> 2) & 1), w = lane & 3;
+                    if (jj < k2) {
                         const int2 ent = list[q + jj];
                         const int blk = ent.x >> ppb_log, pc = ent.x & ((1 << ppb_log) - 1);
-                        unsigned char* dst = tb + t * kTensor + cc * kHalfReg + (fill + jj) * kQuad;
+                        unsigned char* dst = tb + cc * kHalfReg + (fill + jj) * kQuad;
                         if (quad_box) {
-                            tma_load_2d(dst, t ? &p.tmap_vq : &p.tmap_kq, cc * 64, (blk * p.H_kv + it.kvh[0]) << 4,
-                                        bar);
+                            tma_load_2d(dst, mq, cc * 64, (blk * p.H_kv + it.kvh[0]) << 4, bar);
                         } else {
-                            tma_load_2d(dst + w * kPiece, t ? &p.tmap_v[0] : &p.tmap_k[0], cc * 64,
+                            tma_load_2d(dst + w * kPiece, m1, cc * 64,
                                         ((blk * p.H_kv + sel4(it.kvh, w)) << p.log2B) | (pc << 4), bar);
                         }
                     }
@@ -458,12 +485,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 // the item's last piece closes its tile (last = 1: no empty tile takes a buffer)
                 const bool item_end = last_chunk && q == total;
                 if (fill == kSlots || item_end) {
-                    if (lane == 0) {
-                        TC_T(tcount, 1);
-                        meta[b].ns = fill;
-                        meta[b].last = item_end ? 1 : 0;
-                        mbar_arrive(&tile_full[b]);
-                    }
+                    if (lane == 0) publish(fill, item_end ? 1 : 0);
                     ++tcount;
                     fill = 0;
                 }
@@ -472,16 +494,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             if (lane == 0) mbar_arrive(&chunk_empty[c]);
             ++ccount;
             if (last_chunk && total == 0) {  // an item without pieces (every context 0): an empty tile closes it
-                if (fill == 0) {
-                    b = (int)(tcount % kBuf);
-                    if (tcount >= (uint32_t)kBuf) mbar_wait(&tile_empty[b], ((tcount / kBuf) - 1) & 1);
-                }
-                if (lane == 0) {
-                    TC_T(tcount, 1);
-                    meta[b].ns = fill;
-                    meta[b].last = 1;
-                    mbar_arrive(&tile_full[b]);
-                }
+                if (fill == 0) acquire();
+                if (lane == 0) publish(fill, 1);
                 ++tcount;
                 fill = 0;
                 __syncwarp();
@@ -498,8 +512,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         // built once and stepped by constant offsets (address field = bytes >> 4).
         if (lane == 0) {
             const uint32_t idesc_o = umma_idesc(kBF16, true, 128);
-            const uint64_t kdesc0 = umma_desc_sw128(smem_u32(sT), 16, 1024);
-            const uint64_t vdesc0 = umma_desc_sw128(smem_u32(sT + kTensor), kHalfReg, 1024);
+            const uint64_t kdesc0 = umma_desc_sw128(smem_u32(sK), 16, 1024);
+            const uint64_t vdesc0 = umma_desc_sw128(smem_u32(sV), kHalfReg, 1024);
             uint32_t tcount = 0, nitem = 0, scount = 0, pvitems = 0, pv_issued = 0, pv_pub = 0;
             // the completion of every issued P V, in order, published to the softmax warps as
             // a tile index in shared memory (they wait on it only to rescale O -- rarely).
@@ -519,8 +533,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 ++pv_pub;
                 return true;
             };
-            auto issue_pv = [&](int pb, uint32_t pt, int pns, bool started, bool last_pv) {
+            auto issue_pv = [&](uint32_t ptile, uint32_t pt, int pns, bool started, bool last_pv) {
                 const uint32_t sb = pt & 1;
+                const int vb = (int)(ptile % kBV);
                 while (pv_pub + 2 <= pv_issued) publish_one(true);
                 while (publish_one(false)) {
                 }
@@ -530,8 +545,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                     if (pvitems > 0) mbar_wait(o_free, (pvitems - 1) & 1);
                     ++pvitems;
                 }
+                mbar_wait(&v_full[vb], (ptile / kBV) & 1);  // V landed (the softmax saw it too, before P)
                 tc_fence_after();
-                const uint64_t vd = vdesc0 + (uint64_t)((pb * kTileBytes) >> 4);
+                const uint64_t vd = vdesc0 + (uint64_t)((vb * kTensor) >> 4);
                 const uint32_t pa = tmem + kTmS + sb * kSCols;
                 for (int j = 0; j < pns; ++j)
 #pragma unroll
@@ -541,7 +557,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                                     (started || j > 0 || w > 0) ? 1u : 0u);
                 umma_commit(&o_step[pv_issued & 1]);
                 if (last_pv) umma_commit(o_last);
-                umma_commit(&tile_empty[pb]);
+                umma_commit(&v_empty[vb]);
                 ++pv_issued;
             };
             for (uint32_t k = 0;; ++k) {
@@ -552,30 +568,17 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 if (i >= p.n_items) break;
                 const uint32_t qb = nitem & 1;
                 bool q_seen = false, started = false;
-                int pend_b = -1, pend_ns = 0;
-                uint32_t pend_t = 0;
+                int pend_ns = 0;
+                bool pend = false;
+                uint32_t pend_t = 0, pend_tile = 0;
                 for (;;) {
-                    const int b = (int)(tcount % kBuf);
-#ifdef PA_TC_EARLY_PV
-                    if (pend_b >= 0) {
-                        // the pending P V goes first if its P is ready before the next tile's data
-                        // (item starts, late copies); otherwise S of the next tile first, as below
-                        const uint32_t psb = pend_t & 1, ppar = (pend_t >> 1) & 1;
-                        while (!mbar_test(&tile_full[b], (tcount / kBuf) & 1)) {
-                            if (mbar_test(&p_full[psb], ppar)) {
-                                issue_pv(pend_b, pend_t, pend_ns, started, false);
-                                started = true;
-                                pend_b = -1;
-                                break;
-                            }
-                        }
-                    }
-#endif
-                    mbar_wait(&tile_full[b], (tcount / kBuf) & 1);
+                    const uint32_t tile = tcount;
+                    const int kb = (int)(tile % kBK);
+                    mbar_wait(&k_full[kb], (tile / kBK) & 1);
                     TC_T(tcount, 2);
                     ++tcount;
-                    const int ns = *reinterpret_cast<volatile int*>(&meta[b].ns);
-                    const int last = *reinterpret_cast<volatile int*>(&meta[b].last);
+                    const int ns = *reinterpret_cast<volatile int*>(&kmeta[kb].x);
+                    const int last = *reinterpret_cast<volatile int*>(&kmeta[kb].y);
                     uint32_t t = 0;
                     if (ns > 0) {
                         if (!q_seen) {  // the softmax warps have put this item's queries in tensor memory
@@ -586,7 +589,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                         const uint32_t sb = t & 1;
                         tc_fence_after();
                         const uint32_t idesc_s = umma_idesc(kBF16, false, 16 * kNH * ns);
-                        const uint64_t kd = kdesc0 + (uint64_t)((b * kTileBytes) >> 4);
+                        const uint64_t kd = kdesc0 + (uint64_t)((kb * kTensor) >> 4);
                         const uint32_t d = tmem + kTmS + sb * kSCols, qa = tmem + kTmQ + 64 * qb;
 #pragma unroll
                         for (int kk = 0; kk < 8; ++kk)  // S = Q (tensor memory) x K^T (all pieces, all heads)
@@ -595,50 +598,123 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                         umma_commit(&s_full[sb]);
                         TC_T(tcount - 1, 7);
                     }
-                    if (pend_b >= 0) {
-                        issue_pv(pend_b, pend_t, pend_ns, started, last && ns == 0);
+                    umma_commit(&k_empty[kb]);  // K is free once S has completed
+                    if (pend) {
+                        issue_pv(pend_tile, pend_t, pend_ns, started, last && ns == 0);
                         started = true;
-                        pend_b = -1;
+                        pend = false;
                     }
                     if (ns > 0) {
-                        pend_b = b;
+                        pend = true;
+                        pend_tile = tile;
                         pend_t = t;
                         pend_ns = ns;
-                    } else {
-                        umma_commit(&tile_empty[b]);
+                    } else {  // an empty tile: its V slot is released once it is this tile's
+                        const int vb = (int)(tile % kBV);
+                        mbar_wait(&v_full[vb], (tile / kBV) & 1);
+                        umma_commit(&v_empty[vb]);
                     }
                     if (last) break;
                 }
-                if (pend_b >= 0) issue_pv(pend_b, pend_t, pend_ns, started, true);
+                if (pend) issue_pv(pend_tile, pend_t, pend_ns, started, true);
                 if (!q_seen) mbar_wait(&q_full[qb], (nitem >> 1) & 1);  // keep the q_full phases in step
                 ++nitem;
             }
         }
         __syncwarp();
-    } else if (warp == kMerge) {
-        // ================================================================ merges ===
-        // Split context (a6) off the softmax warps' path: for each job (an item with split
-        // members, whose O / L and (m, L) rows the softmax warps have stored), lane = row
-        // (member m = lane / 4, head w = lane % 4) counts its part in; the part that completes
-        // a row's set merges it: o = sum_j L_j 2^(m_j - M) o~_j / sum_j L_j 2^(m_j - M), in
-        // part order (deterministic whichever CTA merges).
-        for (uint32_t jc = 0;; ++jc) {
-            const uint32_t js = jc & 3;
-            mbar_wait(&job_full[js], (jc >> 2) & 1);
-            const int i = *reinterpret_cast<volatile int*>(&job_ring[js]);
+    } else if (warp >= kEpi0) {
+        // ================================================================ epilogue ===
+        // Per item, after its last P V: O (this warp's lane quadrant = head hh) / L to `out`
+        // -- or, for rows with a split context, O / L and (m, L), merged by the last part -- so the
+        // softmax warps go straight on to the next item's scores
+        const int hh = warp - kEpi0;
+        const uint32_t tO = tmem + ((uint32_t)(32 * hh) << 16) + kTmO;
+        uint32_t ocount = 0;
+        for (uint32_t e = 0;; ++e) {
+            const uint32_t es = e & 1;
+            mbar_wait(&st_full[es], (e >> 1) & 1);
+            const int i_cur = *reinterpret_cast<volatile int*>(&st_item[es]);
+            const volatile float* sv4 = reinterpret_cast<const volatile float*>(&stats[(es * kNH + hh) * 32 + lane]);
+            const float4 stv = make_float4(sv4[0], sv4[1], sv4[2], sv4[3]);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&job_empty[js]);
-            if (i < 0) break;
-            const TcItem it = tc_item(p, i);
-            const int m = lane >> 2, w = lane & 3;
-            const int ctx = m < it.gmv ? max(0, __ldg(p.context_lens + it.s0 + m)) : 0;
-            const int nps = max(1, min((ctx + 511) >> 9, p.NPt));
-            const bool split = m < it.gmv && ((it.st >> w) & 1u) && nps > 1 && it.part < nps;
-            const int64_t sh = (int64_t)(it.s0 + m) * p.H + sel4(it.h, w);
-            __threadfence();  // the softmax warps' partial rows (seen through job_full) before the count
-            const bool done = split && split_done(p, sh, nps);
-            unsigned todo = __ballot_sync(0xffffffffu, done);
-            if (todo) __threadfence();
+            if (lane == 0) mbar_arrive(&st_empty[es]);
+            if (i_cur < 0) break;
+            const TcItem it = tc_item(p, i_cur);
+            const bool member = lane < it.gmv;
+            const float mref = stv.x, l = stv.y;
+            const int npv = __float_as_int(stv.z), ctx = __float_as_int(stv.w);
+            TC_EP(e, 0);
+            if (npv > 0) {
+                mbar_wait(o_last, ocount & 1);  // one phase per item with tiles
+                ++ocount;
+                tc_fence_after();
+            }
+            TC_EP(e, 1);
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            // split context (a6): parts holding this member's tokens; with more than one,
+            // each part publishes (m, L, O / L) and the last to finish merges
+            const int nps = max(1, min((ctx + (16 << p.part_log) - 1) >> (4 + p.part_log), p.NPt));
+            const bool mine = member && ((it.st >> hh) & 1u) && it.part < nps;
+            const bool split = mine && nps > 1;
+            const bool store = mine && !split;
+            const int64_t sh = (int64_t)(it.s0 + lane) * p.H + sel4(it.h, hh);
+            T* orow = static_cast<T*>(p.out) + sh * 128;
+            float* prow = p.part_o + (sh * p.NPt + it.part) * 128;
+            // O in two 64-column halves (one wait each); tensor memory is released to the next
+            // item's P V once both are in registers, before the second half's stores
+            auto emit = [&](const float (&v)[32], int c0) {
+                if (split) {
+#pragma unroll
+                    for (int c1 = 0; c1 < 32; c1 += 4)
+                        *reinterpret_cast<float4*>(prow + c0 + c1) =
+                            make_float4(v[c1] * inv, v[c1 + 1] * inv, v[c1 + 2] * inv, v[c1 + 3] * inv);
+                }
+                if (store) {
+#pragma unroll
+                    for (int c1 = 0; c1 < 32; c1 += 8) {
+                        uint4 w;
+                        w.x = pack2<T>(v[c1] * inv, v[c1 + 1] * inv);
+                        w.y = pack2<T>(v[c1 + 2] * inv, v[c1 + 3] * inv);
+                        w.z = pack2<T>(v[c1 + 4] * inv, v[c1 + 5] * inv);
+                        w.w = pack2<T>(v[c1 + 6] * inv, v[c1 + 7] * inv);
+                        *reinterpret_cast<uint4*>(orow + c0 + c1) = w;
+                    }
+                }
+            };
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                float ov[2][32];
+                if (npv > 0) {
+                    tmem_ld32_nw(tO + 64 * hf, ov[0]);
+                    tmem_ld32_nw(tO + 64 * hf + 32, ov[1]);
+                    tmem_ld_wait();
+                    if (hf == 1) {
+                        TC_EP(e, 4);
+                        tc_fence_before();
+                        mbar_arrive(o_free);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) ov[c][u] = 0.f;
+                }
+                emit(ov[0], 64 * hf);
+                emit(ov[1], 64 * hf + 32);
+            }
+            TC_EP(e, 2);
+            // split rows (a6): (m, L) next to O / L, counted in; the part that completes a row's
+            // set merges it: o = sum_j L_j 2^(m_j - M) o~_j / sum_j L_j 2^(m_j - M), in part
+            // order (deterministic whichever CTA merges)
+            if (__any_sync(0xffffffffu, split)) {
+                bool done = false;
+                if (split) {
+                    p.part_ml[sh * p.NPt + it.part] = make_float2(mref, l);
+                    __threadfence();
+                    done = split_done(p, sh, nps);
+                }
+                unsigned todo = __ballot_sync(0xffffffffu, done);
+                if (todo) __threadfence();
             while (todo) {  // whole warp merges row r: lane = 4 dims
                 const int r = __ffs(todo) - 1;
                 todo &= todo - 1;
@@ -678,103 +754,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 st.y = pack2<T>(o.z * il, o.w * il);
                 *reinterpret_cast<uint2*>(static_cast<T*>(p.out) + shr * 128 + 4 * lane) = st;
             }
-        }
-    } else if (warp >= kEpi0) {
-        // ================================================================ epilogue ===
-        // Per item, after its last P V: O (this warp's lane quadrant = head hh) / L to `out`
-        // -- or, for rows with a split context, O / L and (m, L) for the merge warp -- so the
-        // softmax warps go straight on to the next item's scores
-        const int hh = warp - kEpi0;
-        const uint32_t tO = tmem + ((uint32_t)(32 * hh) << 16) + kTmO;
-        uint32_t ocount = 0;
-        uint32_t jcount = 0;
-        auto publish_job = [&](int item) {  // whole warp; the merge warp reads job_ring[slot]
-            const uint32_t js = jcount & 3;
-            if (lane == 0) {
-                if (jcount >= 4) mbar_wait(&job_empty[js], ((jcount >> 2) - 1) & 1);
-                if (hh == 0) job_ring[js] = item;
-                mbar_arrive(&job_full[js]);
-            }
-            ++jcount;
-            __syncwarp();
-        };
-        for (uint32_t e = 0;; ++e) {
-            const uint32_t es = e & 1;
-            mbar_wait(&st_full[es], (e >> 1) & 1);
-            const int i_cur = *reinterpret_cast<volatile int*>(&st_item[es]);
-            const volatile float* sv4 = reinterpret_cast<const volatile float*>(&stats[(es * kNH + hh) * 32 + lane]);
-            const float4 stv = make_float4(sv4[0], sv4[1], sv4[2], sv4[3]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&st_empty[es]);
-            if (i_cur < 0) break;
-            const TcItem it = tc_item(p, i_cur);
-            const bool member = lane < it.gmv;
-            const float mref = stv.x, l = stv.y;
-            const int npv = __float_as_int(stv.z), ctx = __float_as_int(stv.w);
-            TC_EP(e, 0);
-            if (npv > 0) {
-                mbar_wait(o_last, ocount & 1);  // one phase per item with tiles
-                ++ocount;
-                tc_fence_after();
-            }
-            TC_EP(e, 1);
-            const float inv = l > 0.f ? 1.f / l : 0.f;
-            // split context (a6): parts holding this member's tokens; with more than one,
-            // each part publishes (m, L, O / L) and the last to finish merges
-            const int nps = max(1, min((ctx + 511) >> 9, p.NPt));
-            const bool mine = member && ((it.st >> hh) & 1u) && it.part < nps;
-            const bool split = mine && nps > 1;
-            const bool store = mine && !split;
-            const int64_t sh = (int64_t)(it.s0 + lane) * p.H + sel4(it.h, hh);
-            T* orow = static_cast<T*>(p.out) + sh * 128;
-            float* prow = p.part_o + (sh * p.NPt + it.part) * 128;
-            // all of O in registers with one wait, then tensor memory is released to the next
-            // item's P V before the stores
-            float ov[4][32];
-            if (npv > 0) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_ld32_nw(tO + 32 * c, ov[c]);
-                tmem_ld_wait();
-                TC_EP(e, 4);
-                tc_fence_before();
-                mbar_arrive(o_free);
-            } else {
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) ov[c][u] = 0.f;
-            }
-#pragma unroll
-            for (int c0 = 0; c0 < 128; c0 += 32) {
-                const float (&v)[32] = ov[c0 >> 5];
-                if (split) {
-#pragma unroll
-                    for (int c1 = 0; c1 < 32; c1 += 4)
-                        *reinterpret_cast<float4*>(prow + c0 + c1) =
-                            make_float4(v[c1] * inv, v[c1 + 1] * inv, v[c1 + 2] * inv, v[c1 + 3] * inv);
-                }
-                if (store) {
-#pragma unroll
-                    for (int c1 = 0; c1 < 32; c1 += 8) {
-                        uint4 w;
-                        w.x = pack2<T>(v[c1] * inv, v[c1 + 1] * inv);
-                        w.y = pack2<T>(v[c1 + 2] * inv, v[c1 + 3] * inv);
-                        w.z = pack2<T>(v[c1 + 4] * inv, v[c1 + 5] * inv);
-                        w.w = pack2<T>(v[c1 + 6] * inv, v[c1 + 7] * inv);
-                        *reinterpret_cast<uint4*>(orow + c0 + c1) = w;
-                    }
-                }
-            }
-            TC_EP(e, 2);
-            // items with split members: (m, L) next to O / L, then a job for the merge warp
-            if (__any_sync(0xffffffffu, member && nps > 1 && it.part < nps)) {  // same in every epilogue warp
-                if (split) p.part_ml[sh * p.NPt + it.part] = make_float2(mref, l);
-                __syncwarp();
-                publish_job(i_cur);
             }
             TC_EP(e, 3);
         }
-        publish_job(-1);
     } else {
         // ================================================================ softmax ===
         const int hh = warp;  // head w of the quad = TMEM lane quadrant w
@@ -849,8 +831,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                         qnext = true;
                     }
                 }
-                const int b = (int)(tcount % kBuf);
-                mbar_wait(&tile_full[b], (tcount / kBuf) & 1);
+                const int b = (int)(tcount % kBV);
+                mbar_wait(&v_full[b], (tcount / kBV) & 1);  // V landed and the tile's meta written
                 ++tcount;
                 const int ns = *reinterpret_cast<volatile int*>(&meta[b].ns);
                 const int last = *reinterpret_cast<volatile int*>(&meta[b].last);
@@ -867,7 +849,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
                 for (int j = 0; j < kSlots; ++j) {
                     if (nr[j] < 16) {
-                        unsigned char* vb = sT + b * kTileBytes + kTensor + j * kQuad + hh * kPiece;
+                        unsigned char* vb = sV + b * kTensor + j * kQuad + hh * kPiece;
                         for (int u = lane; u < (16 - nr[j]) * 16; u += 32) {
                             const int row = nr[j] + (u >> 4), half = (u >> 3) & 1, ch = u & 7;
                             *reinterpret_cast<uint4*>(vb + half * kHalfReg + row * 128 + ch * 16) =
@@ -877,7 +859,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 }
                 fence_proxy_async_smem();  // before the P V product reads them (after p_full)
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tile_empty[b]);
+                if (lane == 0) mbar_arrive(&v_empty[b]);
                 if (ns > 0) {
                     const uint32_t t = scount++, sb = t & 1;
                     mbar_wait(&s_full[sb], (t >> 1) & 1);
@@ -1010,7 +992,8 @@ extern "C" int pa_debug_tc_trace(void* host_out, size_t bytes) {
 #endif
 
 size_t group_tc_smem_bytes() {
-    return 1024 + (size_t)kBuf * kTileBytes + kBuf * sizeof(TileMeta) + kNCh * kListCap * sizeof(int2) + 16 +
+    return 1024 + (size_t)(kBK + kBV) * kTensor + kBV * sizeof(TileMeta) + kBK * sizeof(int2) +
+           kNCh * kListCap * sizeof(int2) + 16 +
            kNCh * sizeof(int4) + kNumBars * 8 + 12 * 4 + 16 + 2 * kNH * 32 * sizeof(float4) + 16;
 }
 

@@ -115,7 +115,8 @@ struct GroupTcParams {
     unsigned long long* counters;      // [S*H] split-context completion words (epoch-tagged)
     float* part_o;                     // [S][H][NPt][128] O / L of each part
     float2* part_ml;                   // [S][H][NPt] (m, L) of each part, exp2 domain
-    int NPt;                           // parts per group (split context: 512 tokens each; the last to the end)
+    int NPt;                           // parts per group (split context; the last part to the end)
+    int part_log;                      // a part = 1 << part_log 16-token positions (4: 256 tokens, 5: 512)
     uint32_t epoch;
     float scale_log2;
     int log2B, H, H_kv, G, W, S;
