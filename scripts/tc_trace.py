@@ -18,12 +18,19 @@ from synth import make_config, materialize_torch, tables_torch  # noqa: E402
 
 name, gs = (sys.argv[1] if len(sys.argv) > 1 else "c5_beam"), int(sys.argv[2]) if len(sys.argv) > 2 else 4
 wl = make_config(name)
-x = materialize_torch(wl, "cuda")
+# bench.py's conditions: the traced launch reads a cache no recent launch touched (cold L2)
+R = int(os.environ.get("TC_TRACE_CACHES", "1"))
+xs = [materialize_torch(wl, "cuda") for _ in range(R)]
+x = xs[0]
 tb = tables_torch(wl, "cuda")
 out = torch.empty_like(x["query"])
 plan = pa.decode_plan(wl.context_lens)  # bench.py's longest-first order
 for _ in range(3):
     pa.paged_attention_decode_grouped(out, x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"],
+                                      tb["block_tables"], tb["context_lens"], wl.scale, gs,
+                                      max_context_len=wl.max_context_len, seq_order=plan)
+for y in xs[1:]:  # evict x's cache from L2 (each copy > L2 / R)
+    pa.paged_attention_decode_grouped(out, y["query"], y["key"], y["value"], y["key_cache"], y["value_cache"],
                                       tb["block_tables"], tb["context_lens"], wl.scale, gs,
                                       max_context_len=wl.max_context_len, seq_order=plan)
 torch.cuda.synchronize()
