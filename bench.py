@@ -658,9 +658,34 @@ def cpu_baseline(wl, target_s: float = 10.0):
         if el >= target_s:
             break
     per = el / reps
-    return {"value": sub.logical_kv_bytes() / per / 1e9, "unit": "GB/s", "cores": oracle.max_threads(),
-            "kind": "oracle", "sample": f"all {wl.S} sequences x {sub.H} of {wl.H} heads (heads {sub.q_head0}.."
-                                        f"{sub.q_head0 + sub.H - 1}), {reps} reps x {per:.3f} s (fp64 C, OpenMP)"}
+    res = {"value": sub.logical_kv_bytes() / per / 1e9, "unit": "GB/s", "cores": oracle.max_threads(),
+           "kind": "oracle", "sample": f"all {wl.S} sequences x {sub.H} of {wl.H} heads (heads {sub.q_head0}.."
+                                       f"{sub.q_head0 + sub.H - 1}), {reps} reps x {per:.3f} s (fp64 C, OpenMP)"}
+    # the same oracle on ONE host thread (one head of the sample, ~target_s / 4 seconds)
+    try:
+        import ctypes
+        gomp = ctypes.CDLL("libgomp.so.1")
+        n_all = oracle.max_threads()
+        gomp.omp_set_num_threads(1)
+        try:
+            one = shard(wl, 0, wl.H)  # one query head
+            x1 = materialize_numpy(one)
+            a1 = (x1["query"], x1["key_cache"], x1["value_cache"], one.block_tables, one.context_lens, one.scale,
+                  one.B, one.H_kv, one.dtype)
+            reps1, t1 = 0, time.perf_counter()
+            while True:
+                oracle.paged_attention(*a1)
+                reps1 += 1
+                el1 = time.perf_counter() - t1
+                if el1 >= target_s / 4:
+                    break
+            res["single_core"] = {"value": one.logical_kv_bytes() / (el1 / reps1) / 1e9, "unit": "GB/s", "cores": 1,
+                                  "sample": f"all {wl.S} sequences x 1 head, {reps1} reps"}
+        finally:
+            gomp.omp_set_num_threads(n_all)
+    except OSError:
+        pass
+    return res
 
 
 def main():
