@@ -42,7 +42,11 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 #endif
 // k is a constant after the callers' loop unrolling, so the choice folds at compile time.
 __device__ __forceinline__ float2 ex2_pair(float2 e, int k) {
-    if (PA_EXP_EMU > 0 && k % PA_EXP_EMU == PA_EXP_EMU - 1) return ex2_poly2(e);
+#if PA_EXP_EMU > 0
+    if (k % PA_EXP_EMU == PA_EXP_EMU - 1) return ex2_poly2(e);
+#else
+    (void)k;
+#endif
     return make_float2(ex2(e.x), ex2(e.y));
 }
 
