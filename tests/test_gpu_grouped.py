@@ -148,10 +148,12 @@ def test_grouped_decode_full_size_full_output(name, gs):
         assert np.array_equal(bits(x["value_cache"][:, h0:h0 + sh.H]), vc)
 
 
-def test_grouped_decode_plan_order_is_scheduling_only():
+@pytest.mark.parametrize("name,gs", [("c5_beam", 4), ("c3_parallel", 6)])
+def test_grouped_decode_plan_order_is_scheduling_only(name, gs):
     """Walking the groups longest first (pa_decode_plan) changes which CTA computes an item,
-    never a bit of it."""
-    wl = make_config("c5_beam")
+    never a bit of it -- also with split contexts (c3_parallel: few items per SM, so parts of
+    512 tokens, the empty parts skipped through the work counter, merges by the last part)."""
+    wl = make_config(name)
     x0 = materialize_torch(wl, "cuda")
     tb = tables_torch(wl, "cuda")
     outs = []
@@ -161,8 +163,9 @@ def test_grouped_decode_plan_order_is_scheduling_only():
             pa.copy_blocks([x["key_cache"]], [x["value_cache"]], tb["block_mapping"])
         out = torch.empty_like(x["query"])
         pa.paged_attention_decode_grouped(out, x["query"], x["key"], x["value"], x["key_cache"], x["value_cache"],
-                                          tb["block_tables"], tb["context_lens"], wl.scale, 4,
+                                          tb["block_tables"], tb["context_lens"], wl.scale, gs,
                                           max_context_len=wl.max_context_len, seq_order=order)
         torch.cuda.synchronize()
         outs.append(out)
     assert torch.equal(outs[0], outs[1])
+    assert not torch.isnan(outs[1]).any()
