@@ -166,9 +166,10 @@ pa_status_t pa_paged_attention_decode_shared(void* out, const void* query, const
  * tensor maps) and host_seq_order (as pa_paged_attention_ex: the groups are walked in the
  * order of their first sequence in it, e.g. pa_decode_plan's longest first; NULL =
  * natural order; scheduling only).  Persistent CTAs (one per SM) take work items =
- * (group, 4 query heads): a producer warp looks up the members' physical blocks, keeps
- * every DISTINCT 16-row block piece once (its owner set) and TMA-loads it for the 4 heads
- * in one 64-row box per tensor half; S = Q K^T and O += P V run as tcgen05.mma with Q, S,
+ * (group, split-context part, 4 query heads): a scheduler warp looks up the members'
+ * physical blocks, keeps every DISTINCT 16-row block piece once (its owner set), and two
+ * producer warps TMA-load K and V of each piece for the 4 heads (one 64-row box per tensor
+ * half); S = Q K^T and O += P V run as tcgen05.mma with Q, S,
  * P and O in tensor memory -- one set of products for the 4 heads, block-diagonal by
  * lane quadrant -- each member's scores masked to the pieces it owns and its context
  * (Eq.4; sharing P:295-332).  The new token's K/V is written to its
@@ -176,8 +177,15 @@ pa_status_t pa_paged_attention_decode_shared(void* out, const void* query, const
  * P is rounded to the storage dtype before P V (results match the oracle within the
  * stated tolerance; not bit-identical to the CUDA-core kernels).  Supports f16/bf16,
  * head_dim 128, power-of-two block_size >= 16, group_size in [1, 8]
- * (PA_ERR_UNSUPPORTED otherwise); NB*H_kv*B < 2^31.  workspace: >= 16 bytes, any
- * content (an epoch-tagged work counter; never reset by the host).
+ * (PA_ERR_UNSUPPORTED otherwise); NB*H_kv*B < 2^31.  Split context (a6, BJ:north_star):
+ * when the (group, head quad) items alone give fewer than 4 per SM, each group's context
+ * is cut into parts of 512 tokens (from max_context_len, <= 0: W * B; the last part takes
+ * every position past it, so a low bound costs balance, never tokens), a row with more
+ * than one part is merged in part order by the part that completes it (deterministic).
+ * workspace: >= pa_paged_attention_workspace_size(num_seqs, num_heads, head_dim,
+ * max_context_len, 0) bytes (PA_ERR_WORKSPACE otherwise), any content: an epoch-tagged
+ * work counter, epoch-tagged merge counters and the parts' partial rows; never reset by
+ * the host.
  * ---------------------------------------------------------------------------------- */
 pa_status_t pa_paged_attention_decode_grouped(void* out, const void* query, const void* key,
                                               const void* value, void* key_cache, void* value_cache,
