@@ -283,3 +283,33 @@ def test_seq_order_must_be_a_permutation(order):
     arr = (ctypes.c_int32 * 4)(*order)
     assert attn(order=arr, ws=FAKE, wsb=1 << 20) == INVALID
     assert "permutation" in _lib.last_error()
+
+
+def grouped(**kw):
+    a = dict(out=FAKE, q=FAKE, k=FAKE, v=FAKE, kc=FAKE, vc=FAKE, bt=FAKE, cl=FAKE, scale=0.125, B=16, hkv=8, NB=64,
+             S=8, H=8, D=128, W=128, mcl=2048, gs=4, dt=1, ws=FAKE, wsb=1 << 30)
+    a.update(kw)
+    return L.pa_paged_attention_decode_grouped(a["out"], a["q"], a["k"], a["v"], a["kc"], a["vc"], a["bt"], a["cl"],
+                                               a["scale"], a["B"], a["hkv"], a["NB"], a["S"], a["H"], a["D"], a["W"],
+                                               a["mcl"], a["gs"], a["dt"], None, a["ws"], a["wsb"], None)
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(dt=0), UNSUPPORTED),                 # f32: the tensor-core kernel is f16 / bf16
+    (dict(D=64), UNSUPPORTED),
+    (dict(B=8), UNSUPPORTED),                  # block_size >= 16
+    (dict(gs=9), INVALID),                     # group_size in [1, 8]
+    (dict(H=6, hkv=4), INVALID),               # H % H_kv
+    (dict(k=None), INVALID),                   # the step's new token is required
+    (dict(ws=None), WORKSPACE),
+    (dict(wsb=16), WORKSPACE),                 # split context: counters + partial rows, not only the work counter
+])
+def test_grouped_argument_validation(kw, status):
+    """pa_paged_attention_decode_grouped rejects bad arguments on the host (pa.h), incl. a
+    workspace below pa_paged_attention_workspace_size for its split context."""
+    assert grouped(**kw) == status
+    assert _lib.last_error() != ""
+
+
+def test_grouped_zero_seqs_is_noop():
+    assert grouped(S=0, out=None) == OK
