@@ -320,17 +320,9 @@ pa_status_t attention_impl(void* out, const void* query, const void* new_key, co
     // (sharing-aware: 48 KB of stages, so 4 CTAs fit in shared memory as in registers)
     int stg = (sched == 4 ? 48 * 1024 : 64 * 1024) / stage;
     stg = stg < 2 ? 2 : (stg > 8 ? 8 : stg);
-    // coop on a large unsplit batch (every context <= one partition, so a few tiles per
-    // CTA, and CTAs for several waves): ONE stage, so twice the CTAs fit an SM and their
-    // prologues (context length + block ids, then the first copy) overlap other CTAs'
-    // streaming -- c2_alpaca 63.9 -> 61.8 us (profiles/r02_coop_shape_ab.jsonl); a tiny
-    // batch keeps two (c1_tiny 10.7 vs 12.5 us).  Scheduling only: the arithmetic is unchanged
-    if (sched == 2 && NP == 1) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if ((int64_t)num_seqs * ((num_heads + nw - 1) / nw) >= 8LL * sms) stg = 1;
-    }
+    // (one stage per CTA on large unsplit batches measured 61.8 vs 63.9 us on c2_alpaca on
+    // one B200 but 68.1 vs 62.2 on another, and c2_sharegpt 371 vs 324 there: kept at two;
+    // DESIGN §11 item 5, profiles/r02_coop_stg_boxes.jsonl)
     if (tu.stg > 0) stg = tu.stg;
     // coop: partitions per CTA (scheduling only: the arithmetic partition stays PT and a
     // CTA owning all partitions merges them in shared memory, bit-identically).  Measured

@@ -363,7 +363,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 template <typename T, int D>
-__global__ void __launch_bounds__(288) paged_attention_coop_kernel(const AttnParams p) {
+#ifndef PA_COOP_MINB
+#define PA_COOP_MINB 1
+#endif
+__global__ void __launch_bounds__(288, PA_COOP_MINB) paged_attention_coop_kernel(const AttnParams p) {
     using C = AttnCfg<T, D>;
     constexpr int RB = C::RB, LT = C::LT, EPC = C::EPC;
     extern __shared__ __align__(128) unsigned char smem[];
