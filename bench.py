@@ -292,6 +292,31 @@ def run_ours(a, wl_full, world, rank, local):
     # (every layer reuses it, like the block tables): scheduling only, bit-identical output
     use_plan = not a.no_plan and not shared_g
     plan = pa.decode_plan(wl.context_lens) if use_plan else None
+    if ftp is not None:
+        # the fused gather (N2) is checked once against the NCCL all-gather of the same step on
+        # every rank before anything is timed: a bitwise mismatch or a flag-wait timeout on this
+        # node's peer links makes every rank fall back to NCCL (the decision is all-reduced)
+        L0 = layers[0]
+        bad = 0
+        try:
+            got = ftp.decode(L0["query"], L0["key"], L0["value"], L0["key_cache"], L0["value_cache"], bt, cl, wl.scale,
+                             max_context_len=mcl, workspace=ws, seq_order=plan).clone()
+            torch.cuda.synchronize(dev)
+            pa.paged_attention_decode(out, L0["query"], L0["key"], L0["value"], L0["key_cache"], L0["value_cache"], bt,
+                                      cl, wl.scale, max_context_len=mcl, workspace=ws, seq_order=plan)
+            want = gather_heads(out, buffer=gathered)
+            torch.cuda.synchronize(dev)
+            bad = int(int(ftp.status.item()) != 0 or not torch.equal(got, want))
+        except Exception as exc:  # noqa: BLE001 -- any failure of the fused path means: use NCCL
+            print(f"rank {rank}: fused TP gather check failed: {type(exc).__name__}: {exc}", file=sys.stderr)
+            bad = 1
+        flag = torch.tensor([bad], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        if int(flag.item()) != 0:
+            if a.tp_gather == "fused":
+                raise SystemExit("--tp-gather fused: the fused gather does not match the NCCL all-gather here")
+            ftp = None
+            tp_gather = "nccl (the fused gather's check against NCCL failed on this node)"
     # every launch of the step prepared once per layer cache (pa.prepare: Python checks and
     # argument marshalling done up front), so the timed loop is not bound by host overhead
     def layer_calls(L):
