@@ -268,14 +268,12 @@ def run_ours(a, wl_full, world, rank, local):
                     raise
                 tp_gather = f"nccl (fused setup failed: {type(exc).__name__}: {exc})"
     has_pairs = len(wl.block_mapping) > 0
-    # the tcgen05 N1 kernel's persistent CTAs need work items (group, 4 heads) for at least two
-    # rounds over the SMs; a TP=8 shard of C5 (12 heads per rank) has too few and runs coop
-    # (measured: profiles/r02_tp_shard_tune.jsonl)
-    # c3_fork (samples right after the fork share all but their last block) runs it too;
-    # c3_parallel (samples diverged: unique/logical 0.72) stays on coop (258 vs 328 us)
+    # the tcgen05 N1 kernel on the sharing configs: C5's beams, and c3_fork (samples right
+    # after the fork share all but their last block); c3_parallel (samples diverged:
+    # unique/logical 0.72) stays on coop (258 vs 328 us).  TP shards of C5 have few (group,
+    # 4 heads) items per SM, which the kernel's split context covers: TP=8/4/2 shards 66.6 /
+    # 102 / 174 us vs coop 76.7 / 141 / 275 (profiles/r02_tp_shard_n1_split.jsonl)
     auto_grouped = {"c5_beam": 4, "c3_fork": 6}.get(wl_full.name, 0)
-    if auto_grouped and (wl.S // auto_grouped) * ((wl.H + 3) // 4) < 2 * props.multi_processor_count:
-        auto_grouped = 0
     grouped = a.grouped if a.grouped >= 0 else auto_grouped
     if a.shared > 0 or ftp is not None or a.unfused:
         grouped = 0 if a.grouped < 0 else grouped
