@@ -169,3 +169,31 @@ def test_grouped_decode_plan_order_is_scheduling_only(name, gs):
         outs.append(out)
     assert torch.equal(outs[0], outs[1])
     assert not torch.isnan(outs[1]).any()
+
+
+def _fuzz_cases(n=10, seed=2309):
+    rs = np.random.default_rng(seed)
+    cases = []
+    for i in range(n):
+        name = ["c5_beam", "c3_parallel", "c3_fork"][i % 3]
+        H = int(rs.choice([1, 2, 3, 4, 5, 6, 8]))
+        H_kv = int(rs.choice([d for d in (1, 2, 4, 8) if H % d == 0 and d <= H]))
+        S = 4 * int(rs.integers(1, 9)) if name == "c5_beam" else 6 * int(rs.integers(1, 6))  # whole requests (k=4 / n=6)
+        over = dict(S=S, H=H, H_kv=H_kv, B=int(rs.choice([16, 32])), seed=int(rs.integers(1, 1 << 30)))
+        if name == "c5_beam":
+            over["stickiness"] = float(rs.choice([0.0, 0.5, 0.9]))
+        cases.append((name, over, int(rs.integers(1, 9))))
+    return cases
+
+
+@pytest.mark.parametrize("name,over,gs", _fuzz_cases())
+def test_grouped_decode_fuzz_vs_oracle(name, over, gs):
+    """Seeded random shapes through the tcgen05 N1 kernel: group sizes 1..8 not aligned with
+    the requests, 1..8 query heads (ragged head quads), GQA, block size 16 / 32, beam
+    stickiness, ragged last groups -- every output vs the fp64 oracle, caches bit-exact."""
+    wl = make_config(name, **over)
+    out, x = grouped_step(wl, gs)
+    ref, rkc, rvc = oracle_step(wl)
+    assert np.array_equal(bits(x["key_cache"]), rkc) and np.array_equal(bits(x["value_cache"]), rvc)
+    assert not torch.isnan(out).any()
+    assert max_abs(out, ref) <= TOL[wl.dtype]
