@@ -280,3 +280,34 @@ def test_packed_prefill_full_size_sampled():
             rr = oracle.paged_attention(qb[row:row + 1], kb, vb, btn[s:s + 1], np.array([pos + 1], np.int32),
                                         D ** -0.5, B, H_kv, "f16")
             assert max_abs(out[row:row + 1], rr) <= TOL["f16"], (name, row)
+
+
+def _packed_fuzz(n=6, seed=6180):
+    rs = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        groups = []
+        for _ in range(int(rs.integers(1, 5))):
+            P = int(rs.choice([0, 16, 64, 100, 128, 341, 600]))
+            members = []
+            for _ in range(int(rs.integers(1, 12))):
+                own = int(rs.integers(0, 140))
+                members.append((own, int(rs.integers(0, own + 1))))
+            groups.append((P, members))
+        out.append((groups, ["f16", "bf16"][i % 2], int(rs.choice([1, 2, 4])), int(rs.integers(1, 1 << 20))))
+    return out
+
+
+@pytest.mark.parametrize("groups,dtype,G,seed", _packed_fuzz())
+def test_packed_prefill_fuzz_vs_oracle(groups, dtype, G, seed):
+    """Seeded random shared-prefix problems through the packed (cascade) prompt kernel:
+    prefixes 0..600 tokens (block-aligned or not), 1..11 members per group with 0..139 own
+    tokens and 0..own query rows, GQA ratios 1/2/4 -- every row vs the fp64 oracle."""
+    H_kv = 2
+    q, kc, vc, bt, cl, qs, hqs, hcl, hsp = shared_prefix_problem(groups, 16, H_kv * G, H_kv, dtype, seed=seed)
+    if q.shape[0] == 0:
+        pytest.skip("no query rows drawn")
+    out = run_packed(q, kc, vc, bt, cl, qs, 0.088, hqs, hcl, hsp)
+    r = ref(q, kc, vc, bt, cl, qs, 0.088, 16, H_kv, dtype)
+    assert not torch.isnan(out).any()
+    assert max_abs(out, r) <= TOL[dtype]
