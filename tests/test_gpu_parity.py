@@ -627,3 +627,30 @@ def test_grid_order_is_scheduling_only_bitwise(name):
     if not name.endswith("_full"):
         ref, *_ = oracle_step(wl)
         assert max_abs(outs[1], ref) <= TOL[wl.dtype]
+
+
+def _decode_fuzz(n=12, seed=180):
+    rs = np.random.default_rng(seed)
+    cases = []
+    for i in range(n):
+        dtype, D = [("f16", 128), ("bf16", 128), ("f32", 64), ("f16", 64), ("bf16", 64), ("f32", 128)][i % 6]
+        H = int(rs.choice([1, 2, 3, 4, 5, 8]))
+        H_kv = int(rs.choice([d for d in (1, 2, 4, 8) if H % d == 0 and d <= H]))
+        S = int(rs.integers(1, 40))
+        ctx = [int(c) for c in rs.choice([0, 1, 15, 16, 17, 200, 511, 512, 513, 1100, 2048], S)]
+        cases.append((dict(ctx=ctx, H=H, H_kv=H_kv, D=D, B=int(rs.choice([1, 8, 16, 32])), dtype=dtype,
+                           seed=int(rs.integers(1, 1 << 20))), bool(i % 2)))
+    return cases
+
+
+@pytest.mark.parametrize("over,fused", _decode_fuzz())
+def test_decode_fuzz_vs_oracle(over, fused):
+    """Seeded random decode steps through the coop kernel (fused cache write or not): 1..39
+    sequences with contexts at the tile / partition edges (0, 1, 15-17, 511-513, 2048), 1..8
+    query heads, GQA, head_dim 64 / 128, block size 1..32, f32 / f16 / bf16 -- every output
+    vs the fp64 oracle, caches bit-exact."""
+    wl = make_config("explicit", **over)
+    out, kc, vc, _ = gpu_step(wl, fused=fused)
+    ref, rkc, rvc = oracle_step(wl)
+    assert np.array_equal(bits(kc), rkc) and np.array_equal(bits(vc), rvc)
+    assert max_abs(out, ref) <= TOL[wl.dtype]
