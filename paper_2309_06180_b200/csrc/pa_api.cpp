@@ -80,6 +80,7 @@ struct Tuning {
     int tc_split = 1;                      // PA_TC_SPLIT: N1 tcgen05 split context 0 never, 1 auto, 2 always
     int tc_part_log = 5;                   // split part = 512 tokens (the workspace's partition; 256 measured no faster)
     int prefill = 0;                       // PA_PREFILL=2|3 forces a prompt kernel (0 = auto)
+    int packed = 7;                        // PA_PACKED=6: the one-query-tile packed kernel (ablation)
     bool e2e_zero_copy = false;            // PA_E2E_MODE=zerocopy
     int e2e_chunks = 4;                    // PA_E2E_CHUNKS
     int e2e_split[16] = {};                // PA_E2E_SPLIT="1,2,4,1"
@@ -107,6 +108,7 @@ Tuning load_tuning() {
     if (const char* v = getenv("PA_PDL")) t.pdl = v[0] != '0';
     if (const char* v = getenv("PA_TC_SPLIT")) t.tc_split = std::max(0, std::min(2, atoi(v)));
     t.prefill = env_int("PA_PREFILL", 0);
+    t.packed = env_int("PA_PACKED", 7) == 6 ? 6 : 7;
     if (const char* v = getenv("PA_E2E_MODE")) t.e2e_zero_copy = std::strcmp(v, "zerocopy") == 0;
     t.e2e_chunks = env_int("PA_E2E_CHUNKS", 4);
     if (const char* ev = getenv("PA_E2E_SPLIT")) {
@@ -677,7 +679,8 @@ static pa_status_t prefill_impl(void* out, const void* query, const void* key_ca
     p.G = num_heads / num_kv_heads;
     p.W = max_blocks_per_seq;
     cudaError_t e = pack != nullptr
-                        ? pa::launch_prefill_packed(p, *pack, (int)dtype, (cudaStream_t)stream)
+                        ? (tuning().packed == 6 ? pa::launch_prefill_packed(p, *pack, (int)dtype, (cudaStream_t)stream)
+                                                : pa::launch_prefill_packed2(p, *pack, (int)dtype, (cudaStream_t)stream))
                         : pa::launch_prefill(p, (int)dtype, num_seqs, max_query_len, tuning().prefill,
                                              (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "paged_prefill_kernel launch");
@@ -708,13 +711,15 @@ pa_status_t pa_paged_prefill_attention_packed(
     REQUIRE(num_seqs >= 0, "num_seqs must be >= 0");
     REQUIRE(num_seqs == 0 || (host_query_start && host_context_lens && host_shared_prefix),
             "host_query_start / host_context_lens / host_shared_prefix are NULL");
-    // Pack consecutive sequences into query tiles of <= 128 rows that share a cached prefix
+    // Pack consecutive sequences into query tiles of <= 256 rows (v7: two 128-row tiles per
+    // item; 128 for the v6 ablation, PA_PACKED=6) that share a cached prefix
     // P (a multiple of the block size, <= every member's first query position): greedy, in
-    // order, a member joining while the tile stays <= 128 rows and its packed own-token
-    // columns (sum of ctx - P) stay <= 256 (two key tiles).  A query longer than 128 rows
-    // takes ceil(q_len / 128) tiles of its own.  Falls back to the per-sequence kernels
+    // order, a member joining while the tile stays within its rows and its packed own-token
+    // columns (sum of ctx - P) stay <= 256 (two key tiles).  A longer query takes tiles of
+    // its own.  Falls back to the per-sequence kernels
     // when the block size is below 16 or the table would overflow.
     static thread_local pa::PackTable t;
+    const int tile_rows = tuning().packed == 6 ? 128 : 256;  // v7: two 128-row query tiles per item
     bool ok = block_size >= 16 && num_seqs > 0;
     t.n_tiles = 0;
     auto add_tile = [&](int s0, int nm, int P, int r0) {
@@ -734,9 +739,9 @@ pa_status_t pa_paged_prefill_attention_packed(
         REQUIRE(q0 >= 0 && q0 <= host_context_lens[s], "sequence %d: q_len %d must be in [0, ctx %d]", s, q0,
                 host_context_lens[s]);
         const int P0 = ((host_context_lens[s] - q0) / block_size) * block_size;
-        if (q0 > 128) {  // a long query: its own tiles of 128 rows
-            REQUIRE(q0 < 65536 + 128, "q_len %d too long for the packed table", q0);
-            for (int r0 = 0; ok && r0 < q0; r0 += 128) ok = add_tile(s, 1, P0, r0);
+        if (q0 > tile_rows) {  // a long query: its own tiles
+            REQUIRE(q0 < 65536, "q_len %d too long for the packed table", q0);
+            for (int r0 = 0; ok && r0 < q0; r0 += tile_rows) ok = add_tile(s, 1, P0, r0);
             ++s;
             continue;
         }
@@ -746,7 +751,7 @@ pa_status_t pa_paged_prefill_attention_packed(
             const int qe = host_query_start[e + 1] - host_query_start[e];
             REQUIRE(qe >= 0 && qe <= host_context_lens[e], "sequence %d: q_len %d must be in [0, ctx %d]", e, qe,
                     host_context_lens[e]);
-            if (qe > 128 || rows + qe > 128 || e - s >= 128) break;
+            if (qe > tile_rows || rows + qe > tile_rows || e - s >= 128) break;
             const int Pe = std::min({P, (host_shared_prefix[e] / block_size) * block_size,
                                      ((host_context_lens[e] - qe) / block_size) * block_size});
             const int64_t cols_e = cols + (int64_t)(e - s) * (P - Pe) + (host_context_lens[e] - Pe);

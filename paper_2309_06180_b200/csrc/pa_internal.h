@@ -199,6 +199,8 @@ cudaError_t launch_group_tc(const GroupTcParams& p, int dtype, cudaStream_t stre
 cudaError_t launch_prefill(const PrefillParams& p, int dtype, int num_seqs, int max_query_len, int variant,
                            cudaStream_t stream);
 cudaError_t launch_prefill_packed(const PrefillParams& p, const PackTable& t, int dtype, cudaStream_t stream);
+// v7: two 128-row query tiles per item (tables packed with <= 256 rows per tile)
+cudaError_t launch_prefill_packed2(const PrefillParams& p, const PackTable& t, int dtype, cudaStream_t stream);
 // N2: rank `rank` publishes `epoch` to every peer's flag array, then waits (bounded) until
 // every peer has published it to this rank; status = 1 on timeout
 cudaError_t launch_tp_signal_wait(int32_t* const* flag_peers, int world, int rank, int32_t epoch, int32_t* status,

@@ -1377,6 +1377,503 @@ __global__ void __launch_bounds__(kThreadsV6, 1)
     }
 }
 
+
+// ---- v7: packed shared-prefix suffixes, two query tiles per item (default packed kernel) ----
+// As v6, but an item's packed rows fill TWO 128-row query tiles (<= 256 rows of members of one
+// shared prefix), and both tiles walk the same key tiles (the prefix, then every member's own
+// tokens packed back to back): v2's pipeline -- softmax warps 0-3 take tile 0, 4-7 tile 1
+// (thread = row, all 128 columns, no cross-group exchange), S_t and O_t per tile in tensor
+// memory, the MMA warp alternating P V_0(j), S_0(j+1), P V_1(j), S_1(j+1) so one tile's
+// softmax overlaps the other tile's products -- and every key tile is copied once for both.
+#ifndef PA_PF_PROD_V7
+#define PA_PF_PROD_V7 2  // 128 S registers per softmax thread: 4 producers would cap registers at 144
+#endif
+constexpr int kProdV7 = PA_PF_PROD_V7;
+constexpr int kThreadsV7 = kThreadsV2 + 32 * kProdV7;  // + scheduler warp 10, producers 11..
+
+template <typename T>
+__global__ void __launch_bounds__(kThreadsV7, 1)
+    paged_prefill_packed2_kernel(const __grid_constant__ PrefillParams p, const __grid_constant__ PackTable pt) {
+    constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = tc::smem_align1024(smem_raw);
+    unsigned char* sQ = smem;                          // [2 tiles][2 halves][128][64]
+    unsigned char* sK = smem + 4 * kHalf;              // [2 stages][2 halves][128][64]
+    unsigned char* sV = sK + 2 * kKStages * kHalf;     // [2 stages][2 halves][128][64]
+    unsigned char* stage = sV + 2 * kVStages * kHalf;  // [8 softmax warps][32 rows][64 B] output staging
+    PackSlot* slots = reinterpret_cast<PackSlot*>(stage + 8 * 2048);  // [2 parity]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(slots + 2);
+    uint64_t* q_full = bars;                 // 1
+    uint64_t* q_empty = bars + 1;            // 1: every S of the item issued
+    uint64_t* k_full = bars + 2;             // 2
+    uint64_t* k_empty = bars + 4;            // 2
+    uint64_t* v_full = bars + 6;             // 2
+    uint64_t* v_empty = bars + 8;            // 2
+    uint64_t* s_full = bars + 10;            // 2 (per query tile)
+    uint64_t* p_full = bars + 12;            // 2 (per query tile)
+    uint64_t* o_done = bars + 14;            // 2 (per query tile)
+    uint64_t* o_free = bars + 16;            // 2 (per query tile)
+    uint64_t* m_full = bars + 18;            // 2: item table published (scheduler warp)
+    uint64_t* m_empty = bars + 20;           // 2: item table read (8 softmax warps, MMA, producers)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n_items = pt.n_tiles * p.H;
+    pdl_wait();
+
+    if (tid == 0) {
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], kQ);
+            mbar_init(&o_done[i], 1);
+            mbar_init(&o_free[i], kQ);
+            mbar_init(&m_full[i], 1);
+            mbar_init(&m_empty[i], 9 + kProdV7);
+        }
+        fence_mbar_init();
+    }
+    // V stages start zeroed: columns of a last tile past its tokens are never loaded
+    for (int i = tid; i < 2 * kVStages * kHalf / 16; i += kThreadsV7)
+        reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+    if (warp == 0) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int B = 1 << p.log2B;
+
+    if (warp == 10) {
+        // ---------------- scheduler: each item's table, one item ahead ----------------
+        uint32_t nq = 0;
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++nq) {
+            int tile, h, s0, nm, P, r0;
+            packed_item(pt, p, i, tile, h, s0, nm, P, r0);
+            const int qb = nq & 1;
+            if (nq >= 2) mbar_wait(&m_empty[qb], ((nq - 2) >> 1) & 1);
+            PackSlot& sl = slots[qb];
+            PackMem* mt = sl.mem;
+            const int qs0 = __ldg(p.query_start + s0) + r0;
+            int col = 0, pcs = 0;
+            for (int k0 = 0; k0 < nm; k0 += 32) {
+                const int k = k0 + lane;
+                int len = 0, np = 0, ro = 0, cx = 0, ql = 0;
+                if (k < nm) {
+                    const int a0 = __ldg(p.query_start + s0 + k);
+                    ro = a0 - qs0;
+                    ql = __ldg(p.query_start + s0 + k + 1) - a0;
+                    cx = __ldg(p.context_lens + s0 + k);
+                    len = cx - P;
+                    np = (len + 15) >> 4;
+                }
+                int il = len, ip = np;  // inclusive scans over the lanes
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int a = __shfl_up_sync(0xffffffffu, il, off), b2 = __shfl_up_sync(0xffffffffu, ip, off);
+                    if (lane >= off) {
+                        il += a;
+                        ip += b2;
+                    }
+                }
+                if (k < nm) mt[k] = PackMem{ro, cx, col + il - len, pcs + ip - np, ql};
+                col += __shfl_sync(0xffffffffu, il, 31);
+                pcs += __shfl_sync(0xffffffffu, ip, 31);
+            }
+            const int rows = min(2 * kQ, __ldg(p.query_start + s0 + nm) - qs0);
+            __syncwarp();
+            {   // packed columns the tile's rows can see: the last member's causal range ends
+                // at its last row in this tile (a long query spans several tiles)
+                const PackMem ml = mt[nm - 1];
+                const int pos_max = ml.ctx - ml.qlen + (rows - 1 - ml.row_off);
+                col = ml.col_off + min(ml.ctx - P, pos_max - P + 1);
+            }
+            // physical blocks: every 16-token position of the prefix (through s0's table) and
+            // every own-token piece of every member
+            const int32_t* bt0 = p.block_tables + (int64_t)s0 * p.W;
+            for (int q = lane; q < ((P + 15) >> 4); q += 32) sl.pre_blk[q] = __ldg(bt0 + ((q << 4) >> p.log2B));
+            for (int gp = lane; gp < pcs; gp += 32) {
+                int lo = 0, hi = nm - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (mt[mid].piece_off <= gp) lo = mid; else hi = mid - 1;
+                }
+                const int tt0 = P + 16 * (gp - mt[lo].piece_off);
+                sl.piece_blk[gp] = __ldg(p.block_tables + (int64_t)(s0 + lo) * p.W + (tt0 >> p.log2B));
+            }
+            const int n_pre = (P + kN - 1) / kN, n_suf = (col + kN - 1) / kN;
+            if (lane == 0) {
+                mt[nm] = PackMem{rows, 0, col, pcs, 0};
+                sl.hdr[0] = rows;
+                sl.hdr[1] = col;
+                sl.hdr[2] = n_pre;
+                sl.hdr[3] = n_pre + n_suf;
+                sl.hdr[4] = nm;  // the item's fields for the other warps (no dynamically indexed
+                sl.hdr[5] = P;   // parameter loads there)
+                sl.hdr[6] = qs0;
+                sl.hdr[7] = h;
+                sl.hdr[8] = s0;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&m_full[qb]);  // release: the table writes above
+        }
+    } else if (warp == 8 || warp > 10) {  // (v7: warps 8, 11..)
+        // ---------------- TMA producers (pw 0 = warp 8) ----------------
+        const int pw = warp == 8 ? 0 : warp - 10;
+        const int br = p.box_rows;
+        uint32_t g = 0, nq = 0;
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++nq) {
+            const int qb = nq & 1;
+            mbar_wait(&m_full[qb], (nq >> 1) & 1);
+            const PackSlot& sl = slots[qb];
+            const PackMem* mt = sl.mem;
+            const int col = sl.hdr[1], n_pre = sl.hdr[2], n = sl.hdr[3];
+            const int nm = sl.hdr[4], P = sl.hdr[5], qs0 = sl.hdr[6], h = sl.hdr[7];
+            const int kvh = h / p.G;
+            const int pcs = mt[nm].piece_off;
+            // ---- the item's two query tiles (rows past the queries: zero fill / masked)
+            if (pw == 0 && nq >= 1) mbar_wait(q_empty, (nq - 1) & 1);
+            if (pw == 0 && lane == 0) {
+                mbar_arrive_expect_tx(q_full, 4u * kHalf);
+                tma_load_3d(sQ, &p.tmap_q, 0, h, qs0, q_full);
+                tma_load_3d(sQ + kHalf, &p.tmap_q, 64, h, qs0, q_full);
+                tma_load_3d(sQ + 2 * kHalf, &p.tmap_q, 0, h, qs0 + kQ, q_full);
+                tma_load_3d(sQ + 3 * kHalf, &p.tmap_q, 64, h, qs0 + kQ, q_full);
+            }
+            __syncwarp();
+            for (int j = 0; j < n; ++j, ++g) {
+                const uint32_t ks = g % kKStages, vs = g & 1;
+                for (int tsr = 0; tsr < 2; ++tsr) {  // K then V
+                    uint64_t* bar = tsr ? &v_full[vs] : &k_full[ks];
+                    if (tsr == 0 && g >= kKStages) mbar_wait(&k_empty[ks], ((g - kKStages) / kKStages) & 1);
+                    if (tsr == 1 && g >= 2) mbar_wait(&v_empty[vs], ((g - 2) >> 1) & 1);
+                    unsigned char* dst0 = tsr ? sV + vs * 2 * kHalf : sK + ks * 2 * kHalf;
+                    const CUtensorMap* map = tsr ? &p.tmap_v : &p.tmap_k;
+                    const CUtensorMap* map1 = tsr ? &p.tmap_v1 : &p.tmap_k1;
+                    if (j < n_pre) {
+                        // shared prefix tokens [128 j, min(P, 128 j + 128)) through s0's table
+                        const int t0 = j * kN, len = min(P, t0 + kN) - t0;
+                        const int nf = len / br, nb = nf + len % br;
+                        if (pw == 0 && lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)len * 256u);
+                        __syncwarp();
+                        for (int b2 = pw + kProdV7 * lane; b2 < nb; b2 += 32 * kProdV7) {
+                            const int tt = t0 + (b2 < nf ? b2 * br : nf * br + (b2 - nf));
+                            const int blk = sl.pre_blk[tt >> 4];
+                            const int row = (blk * p.H_kv + kvh) * B + (tt & (B - 1));
+                            const int off = (tt - t0) * 128;
+                            const CUtensorMap* m = b2 < nf ? map : map1;
+                            tma_load_2d(dst0 + off, m, 0, row, bar);
+                            tma_load_2d(dst0 + kHalf + off, m, 64, row, bar);
+                        }
+                    } else {
+                        // packed members' own tokens: packed columns [c_lo, c_hi) of this tile;
+                        // lane = one 16-token piece of one member (pieces are block-aligned
+                        // because P is), split into single rows where it crosses the tile
+                        const int c_lo = (j - n_pre) * kN, c_hi = min(col, c_lo + kN);
+                        if (pw == 0 && lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(c_hi - c_lo) * 256u);
+                        __syncwarp();
+                        for (int gp = pw + kProdV7 * lane; gp < pcs; gp += 32 * kProdV7) {
+                            int lo = 0, hi = nm - 1;  // member k of piece gp: last piece_off <= gp
+                            while (lo < hi) {
+                                const int mid = (lo + hi + 1) >> 1;
+                                if (mt[mid].piece_off <= gp) lo = mid; else hi = mid - 1;
+                            }
+                            const PackMem mk = mt[lo];
+                            const int q = gp - mk.piece_off;
+                            const int len_k = mk.ctx - P;
+                            const int pc0 = mk.col_off + 16 * q, pc1 = mk.col_off + min(16 * q + 16, len_k);
+                            const int a = max(pc0, c_lo), b3 = min(pc1, c_hi);
+                            if (a >= b3) continue;
+                            const int tt0 = P + 16 * q;  // first token of the piece
+                            const int blk = sl.piece_blk[gp];
+                            const int row0 = (blk * p.H_kv + kvh) * B + (tt0 & (B - 1));
+                            if (a == pc0 && b3 == pc1 && pc1 - pc0 == 16 && br == 16) {
+                                tma_load_2d(dst0 + (a - c_lo) * 128, map, 0, row0, bar);
+                                tma_load_2d(dst0 + kHalf + (a - c_lo) * 128, map, 64, row0, bar);
+                            } else {
+                                // rows [a, b3) of the piece as 8-row boxes, then 4/2/1
+                                int c = a;
+                                for (int rb = 8, mi = 0; rb >= 1; rb >>= 1, ++mi) {
+                                    const CUtensorMap* mr = rb == 1 ? map1 : (tsr ? &p.tmap_vr[mi] : &p.tmap_kr[mi]);
+                                    while (b3 - c >= rb && (rb == 8 || ((b3 - c) & rb))) {
+                                        tma_load_2d(dst0 + (c - c_lo) * 128, mr, 0, row0 + (c - pc0), bar);
+                                        tma_load_2d(dst0 + kHalf + (c - c_lo) * 128, mr, 64, row0 + (c - pc0), bar);
+                                        c += rb;
+                                    }
+                                }
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            if (lane == 0) mbar_arrive(&m_empty[qb]);  // this item's table is no longer read here
+        }
+    } else if (warp == 9) {
+        // ---------------- MMA issuer: v2's order over the two query tiles ----------------
+        const uint32_t idesc_s = umma_idesc(kBF16, false), idesc_o = umma_idesc(kBF16, true);
+        uint32_t g = 0, nq = 0, np[2] = {0u, 0u}, nf[2] = {0u, 0u};
+        auto issue_S = [&](int t, uint32_t gg) {  // S_t = Q_t K(gg)^T
+            if (lane == 0) {
+                const uint32_t q = smem_u32(sQ) + t * 2 * kHalf, k = smem_u32(sK) + (gg % kKStages) * 2 * kHalf;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+                    umma_f16(tmem + t * 128, umma_desc_sw128(q + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024),
+                             idesc_s, kk > 0);
+                }
+                umma_commit(&s_full[t]);
+            }
+            __syncwarp();
+        };
+        auto issue_PV = [&](int t, uint32_t gg, bool first) {  // O_t (+)= P_t V(gg)
+            mbar_wait(&p_full[t], np[t]++ & 1);
+            if (first && nf[t]++ > 0) mbar_wait(&o_free[t], (nf[t] - 2) & 1);  // the last item's O_t was read
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t v = smem_u32(sV) + (gg & 1) * 2 * kHalf;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                                umma_desc_sw128(v + kk * 2048, kHalf, 1024), idesc_o, (first ? 0u : 1u) | (kk > 0));
+                umma_commit(&o_done[t]);
+            }
+            __syncwarp();
+        };
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+            const uint32_t qb = nq & 1;
+            mbar_wait(&m_full[qb], (nq >> 1) & 1);
+            const int rows = *reinterpret_cast<volatile int*>(&slots[qb].hdr[0]);
+            const int n = *reinterpret_cast<volatile int*>(&slots[qb].hdr[3]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&m_empty[qb]);
+            mbar_wait(q_full, nq & 1);
+            ++nq;
+            const bool two = rows > kQ;  // the second query tile has rows
+            if (n == 0) {
+                if (lane == 0) umma_commit(q_empty);
+                __syncwarp();
+                continue;
+            }
+            mbar_wait(&k_full[g % kKStages], (g / kKStages) & 1);
+            tc_fence_after();
+            issue_S(0, g);
+            if (two) issue_S(1, g);
+            if (lane == 0) {
+                umma_commit(&k_empty[g % kKStages]);
+                if (n == 1) umma_commit(q_empty);
+            }
+            __syncwarp();
+            for (int j = 0; j < n; ++j, ++g) {
+                mbar_wait(&v_full[g & 1], (g >> 1) & 1);
+                issue_PV(0, g, j == 0);
+                const bool more = j + 1 < n;
+                if (more) {
+                    mbar_wait(&k_full[(g + 1) % kKStages], ((g + 1) / kKStages) & 1);
+                    tc_fence_after();
+                    issue_S(0, g + 1);
+                }
+                if (two) issue_PV(1, g, j == 0);
+                if (lane == 0) umma_commit(&v_empty[g & 1]);
+                if (more) {
+                    if (two) issue_S(1, g + 1);
+                    if (lane == 0) {
+                        umma_commit(&k_empty[(g + 1) % kKStages]);
+                        if (j + 2 == n) umma_commit(q_empty);  // every S of this item issued
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ---------------- softmax: warps 0-3 query tile 0, 4-7 tile 1 (thread = row) ----------------
+        const int t = warp >> 2;
+        const int rt = tid & (kQ - 1);                    // row within the tile
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + 256 + t * 128 + lane_off;
+        unsigned char* stg = stage + (warp & 7) * 2048;  // this warp's 32 rows x 32 columns staging
+        const int rw0 = t * kQ + (warp & 3) * 32;         // the warp's first row in the item
+        uint32_t ns = 0, nq = 0;
+        for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++nq) {
+            const uint32_t qb = nq & 1;
+            mbar_wait(&m_full[qb], (nq >> 1) & 1);
+            const PackMem* mt = slots[qb].mem;
+            const int rows = slots[qb].hdr[0], n_pre = slots[qb].hdr[2], n = slots[qb].hdr[3];
+            const int nm = slots[qb].hdr[4], P = slots[qb].hdr[5], qs0 = slots[qb].hdr[6], h = slots[qb].hdr[7];
+            const int r = t * kQ + rt;  // row within the item
+            const bool row_valid = r < rows;
+            int k = 0;
+            {
+                int lo = 0, hi = nm - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (mt[mid].row_off <= r) lo = mid; else hi = mid - 1;
+                }
+                k = lo;
+            }
+            const PackMem mk = mt[k];
+            const int pos = mk.ctx - mk.qlen + (r - mk.row_off);
+            const int seg_hi = mk.col_off + (pos - P) + 1;  // packed columns [col_off, seg_hi)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&m_empty[qb]);
+            const bool active = t == 0 || rows > kQ;
+            if (!active) continue;
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < n; ++j, ++ns) {
+                mbar_wait(&s_full[t], ns & 1);
+                tc_fence_after();
+                float sv[4][32];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld32_nw(tS + 32 * c, sv[c]);
+                tmem_ld_wait();
+                // valid columns [lo, lim) of this key tile
+                int lo, lim;
+                if (!row_valid) {
+                    lo = 0;
+                    lim = 0;
+                } else if (j < n_pre) {
+                    lo = 0;
+                    lim = min(P - j * kN, kN);
+                } else {
+                    const int c0 = (j - n_pre) * kN;
+                    lo = mk.col_off - c0;
+                    lim = seg_hi - c0;
+                }
+                const bool partial = !__all_sync(0xffffffffu, lo <= 0 && lim >= kN);
+                bool live[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    live[c] = !partial || __any_sync(0xffffffffu, lo < 32 * c + 32 && lim > 32 * c && lim > lo);
+                if (partial) {
+                    const uint32_t w = (uint32_t)max(lim - lo, 0);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) sv[c][u] = (uint32_t)(32 * c + u - lo) < w ? sv[c][u] : -INFINITY;
+                }
+                float mo = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int u = 0; u < 32; u += 2) mo = fmaxf(mo, fmaxf(sv[c][u], sv[c][u + 1]));
+                const float mt2 = mo * p.scale_log2;
+                const bool bump = __any_sync(0xffffffffu, mt2 > m + kLazy);
+                const float mn = bump ? fmaxf(m, mt2) : m;
+                const float ms = (mn == -INFINITY) ? 0.f : mn;
+                const float alpha = bump ? ex2(m - ms) : 1.f;
+                float2 rs2 = make_float2(0.f, 0.f);
+                const float2 c2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-ms, -ms);
+                const uint32_t zero[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    if (live[c]) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int u = 0; u < 32; u += 2) {
+                            const float2 e = ffma2(make_float2(sv[c][u], sv[c][u + 1]), c2, nm2);
+                            const float2 a = ex2_pair(e, u / 2);
+                            rs2 = __fadd2_rn(rs2, a);
+                            pk[u / 2] = pack2<T>(a.x, a.y);
+                        }
+                        tmem_st16(tS + 16 * c, pk);
+                    } else {
+                        tmem_st16(tS + 16 * c, zero);
+                    }
+                }
+                if (j > 0) {  // P V_t of the previous key tile completed (every o_done phase is waited)
+                    mbar_wait(&o_done[t], (ns - 1) & 1);
+                    tc_fence_after();
+                }
+                if (j > 0 && bump) {
+#pragma unroll
+                    for (int c0 = 0; c0 < 128; c0 += 32) {
+                        float v[32];
+                        tmem_ld32_nw(tO + c0, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) v[u] *= alpha;
+                        tmem_st32(tO + c0, v);
+                    }
+                }
+                l = l * alpha + (rs2.x + rs2.y);
+                m = mn;
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&p_full[t]);
+            }
+            // epilogue: out rows = O_t / l through the warp's staging buffer (coalesced stores)
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            if (n > 0) {
+                mbar_wait(&o_done[t], (ns - 1) & 1);
+                tc_fence_after();
+            }
+#pragma unroll
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+                float v[32];
+                if (n > 0) {
+                    tmem_ld32_nw(tO + c0, v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) v[u] = 0.f;
+                }
+#pragma unroll
+                for (int c1 = 0; c1 < 4; ++c1) {
+                    alignas(16) T w[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) w[u] = Elem<T>::from_f32(v[c1 * 8 + u] * inv);
+                    *reinterpret_cast<uint4*>(stg + lane * 64 + ((c1 ^ ((lane >> 1) & 3)) * 16)) =
+                        *reinterpret_cast<const uint4*>(w);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int kq = 0; kq < 4; ++kq) {
+                    const int rr = kq * 8 + (lane >> 2), ch = lane & 3;
+                    if (rw0 + rr < rows) {
+                        const uint4 x = *reinterpret_cast<const uint4*>(stg + rr * 64 + ((ch ^ ((rr >> 1) & 3)) * 16));
+                        T* dst = static_cast<T*>(p.out) + ((int64_t)(qs0 + rw0 + rr) * p.H + h) * 128 + c0 + ch * 8;
+                        *reinterpret_cast<uint4*>(dst) = x;
+                    }
+                }
+                __syncwarp();
+            }
+            if (n > 0) {
+                tc_fence_before();
+                mbar_arrive(&o_free[t]);  // O_t may take the next item
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+size_t prefill_packed2_smem_bytes() {
+    return 1024 + (4 + 2 * kKStages + 2 * kVStages) * (size_t)kHalf + 8 * 2048 + 2 * sizeof(PackSlot) + 22 * 8 + 16;
+}
+
+cudaError_t launch_prefill_packed2(const PrefillParams& p, const PackTable& t, int dtype, cudaStream_t stream) {
+    int dev = 0, num_sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (num_sms <= 0) num_sms = 148;
+    const size_t smem = prefill_packed2_smem_bytes();
+    const long long items = (long long)t.n_tiles * p.H;
+    const dim3 grid((unsigned)std::min<long long>(items, num_sms));
+    auto kern = dtype == 1 ? paged_prefill_packed2_kernel<__half> : paged_prefill_packed2_kernel<__nv_bfloat16>;
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem);
+    if (e != cudaSuccess) return e;
+    return launch_k(kern, grid, dim3(kThreadsV7), smem, stream, p, t);
+}
+
 size_t prefill_packed_smem_bytes() {
     return 1024 + (4 + 2 * kKStages + 2 * kVStages) * (size_t)kHalf + 8 * 2048 + (512 + 256) * 4 + 2 * sizeof(PackSlot) +
            21 * 8 + 16;
