@@ -81,6 +81,7 @@ struct Tuning {
     int tc_part_log = 5;                   // split part = 512 tokens (the workspace's partition; 256 measured no faster)
     int prefill = 0;                       // PA_PREFILL=2|3 forces a prompt kernel (0 = auto)
     int packed = 7;                        // PA_PACKED=6: the one-query-tile packed kernel (ablation)
+    int pack_cols = 256;                   // PA_PACK_COLS: packed own-token columns per tile (multiple of 128)
     bool e2e_zero_copy = false;            // PA_E2E_MODE=zerocopy
     int e2e_chunks = 4;                    // PA_E2E_CHUNKS
     int e2e_split[16] = {};                // PA_E2E_SPLIT="1,2,4,1"
@@ -109,6 +110,7 @@ Tuning load_tuning() {
     if (const char* v = getenv("PA_TC_SPLIT")) t.tc_split = std::max(0, std::min(2, atoi(v)));
     t.prefill = env_int("PA_PREFILL", 0);
     t.packed = env_int("PA_PACKED", 7) == 6 ? 6 : 7;
+    t.pack_cols = std::max(128, std::min(1024, env_int("PA_PACK_COLS", 256) / 128 * 128));
     if (const char* v = getenv("PA_E2E_MODE")) t.e2e_zero_copy = std::strcmp(v, "zerocopy") == 0;
     t.e2e_chunks = env_int("PA_E2E_CHUNKS", 4);
     if (const char* ev = getenv("PA_E2E_SPLIT")) {
@@ -755,7 +757,7 @@ pa_status_t pa_paged_prefill_attention_packed(
             const int Pe = std::min({P, (host_shared_prefix[e] / block_size) * block_size,
                                      ((host_context_lens[e] - qe) / block_size) * block_size});
             const int64_t cols_e = cols + (int64_t)(e - s) * (P - Pe) + (host_context_lens[e] - Pe);
-            if (cols_e > 256) break;
+            if (cols_e > tuning().pack_cols) break;
             rows += qe;
             cols = cols_e;
             P = Pe;
