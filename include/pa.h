@@ -237,17 +237,18 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
  * pa_paged_prefill_attention_packed -- pa_paged_prefill_attention for batches whose
  * requests share a cached prefix (the shared-prefix workload of P:334-338):
  * the query rows of consecutive sequences that share their first P cached tokens are
- * packed into one 128-row query tile, the shared prefix is attended ONCE for all of them
+ * packed into one item of up to 256 rows (two 128-row query tiles on the tensor cores that
+ * walk the same key tiles), the shared prefix is attended ONCE for all of them
  * and each row's own tokens [P, ctx) are attended causally in packed key tiles (cascade
  * attention; same results as pa_paged_prefill_attention within the tolerance, different
  * accumulation order).  Extra HOST arrays, which the scheduler already holds:
  * host_query_start [S+1] and host_context_lens [S] (copies of the device arrays), and
  * host_shared_prefix [S]: the number of leading cached tokens sequence s shares -- the
  * same physical blocks -- with sequence s-1 (0 when none; only its multiple of the block
- * size is used).  The library packs greedily in order: a tile grows while it stays <= 128
+ * size is used).  The library packs greedily in order: an item grows while it stays <= 256
  * rows and its members' own tokens past the shared prefix P (P a multiple of the block
  * size, at most every member's first query position) stay <= 256 packed key columns; a
- * query longer than 128 rows takes tiles of its own.  Falls back to
+ * query longer than 256 rows takes items of its own.  Falls back to
  * pa_paged_prefill_attention's kernels when block_size < 16 or more than 1024 tiles would
  * be needed.  Other arguments, layouts and errors as pa_paged_prefill_attention.
  * ---------------------------------------------------------------------------------- */
