@@ -139,7 +139,7 @@ __device__ __forceinline__ bool split_done(const GroupTcParams& p, int64_t sh, i
 #ifdef PA_TC_TRACE  // timing experiments (variant build): clock64 per tile of CTAs 0..7
 constexpr int kTrTiles = 1024;
 __device__ long long g_tc_trace[8 * kTrTiles * 8];
-__device__ unsigned long long g_tc_span[1024 * 4];
+__device__ unsigned long long g_tc_span[1024 * 8];
 __device__ long long g_tc_ep[8 * 64 * 8];  // CTAs 0..7, items 0..63: epilogue start, o_last seen, O stored, done
 #define TC_EP(item, ev)                                                                                      \
     do {                                                                                                     \
@@ -152,7 +152,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define TC_SPAN(ev, v)                                                     \
     do {                                                                   \
-        if (blockIdx.x < 1024) g_tc_span[blockIdx.x * 4 + (ev)] = (v);    \
+        if (blockIdx.x < 1024) g_tc_span[blockIdx.x * 8 + (ev)] = (v);    \
     } while (0)
 #define TC_T(tile, ev)                                                                               \
     do {                                                                                             \
@@ -424,6 +424,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             tb = base + b * kTensor;
         };
         auto publish = [&](int ns, int last) {  // lane 0
+#ifdef PA_TC_TRACE
+            if (!isv && tcount == 0) TC_SPAN(5, gtimer());
+#endif
             if (isv) {
                 meta[b].ns = ns;
                 meta[b].last = last;
@@ -438,7 +441,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             mbar_wait(&chunk_full[c], (ccount / kNCh) & 1);
             const volatile int* hv = reinterpret_cast<const volatile int*>(&chdr[c]);
             const int i = hv[0], total = hv[1], last_chunk = hv[2];
-            if (i >= p.n_items) break;
+            if (i >= p.n_items) {
+#ifdef PA_TC_TRACE
+                if (!isv && lane == 0) TC_SPAN(4, tcount);
+#endif
+                break;
+            }
             const TcItem it = tc_item(p, i);
             const int2* list = clist + c * kListCap;
             const bool quad_box = it.quad && p.log2B == 4;  // the 4 kv heads' pieces are 64 adjacent rows

@@ -45,17 +45,21 @@ pa.paged_attention_decode_grouped(out, x["query"], x["key"], x["value"], x["key_
                                   max_context_len=wl.max_context_len, seq_order=plan)
 e1.record()
 torch.cuda.synchronize()
-span = np.zeros(1024 * 4, np.uint64)
+span = np.zeros(1024 * 8, np.uint64)
 L.pa_debug_tc_span.restype = ctypes.c_int
 assert L.pa_debug_tc_span(span.ctypes.data, span.nbytes) == 0
-sp = span.reshape(1024, 4).astype(np.int64)
+sp = span.reshape(1024, 8).astype(np.int64)
 sp = sp[sp[:, 0] > 0]
 t0 = sp[:, 0].min()
 print(json.dumps({"launch_event_us": e0.elapsed_time(e1) * 1e3, "ctas": len(sp),
                   "entry_us_max": float((sp[:, 0].max() - t0) / 1e3),
                   "pdl_wait_us_max": float((sp[:, 1] - sp[:, 0]).max() / 1e3),
                   "exit_us": [float(np.percentile(sp[:, 2] - t0, q) / 1e3) for q in (0, 10, 50, 90, 100)],
-                  "items_per_cta": [int(np.percentile(sp[:, 3], q)) for q in (0, 50, 100)]}))
+                  "items_per_cta": [int(np.percentile(sp[:, 3], q)) for q in (0, 50, 100)],
+                  "tiles_per_cta": [int(np.percentile(sp[:, 4], q)) for q in (0, 10, 50, 90, 100)],
+                  "first_tile_published_us": [float(np.percentile(sp[:, 5] - t0, q) / 1e3) for q in (0, 50, 100)],
+                  "exit_us_vs_tiles": [[int(a), float((b - t0) / 1e3)] for a, b in
+                                       sorted(zip(sp[:, 4], sp[:, 2]))[:: max(1, len(sp) // 12)]]}))
 NT = 1024
 buf = np.zeros(8 * NT * 8, np.int64)
 L.pa_debug_tc_trace.restype = ctypes.c_int
