@@ -213,6 +213,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     volatile int* pv_done = reinterpret_cast<volatile int*>(tmem_slot + 1);  // last completed P V (tile index)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef PA_TC_TRACE
+    if (tid == 0) TC_SPAN(6, gtimer());  // kernel entry
+#endif
     if (tid == 0) {
         for (int i = 0; i < kBK; ++i) {
             mbar_init(&k_full[i], 1);
@@ -396,6 +399,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 }
                 __syncwarp();
                 if (lane == 0) {
+#ifdef PA_TC_TRACE
+                    if (ccount == 0) TC_SPAN(7, gtimer());
+#endif
                     chdr[c] = make_int4(i, total, p0 + 32 >= pend ? 1 : 0, 0);
                     mbar_arrive(&chunk_full[c]);
                 }

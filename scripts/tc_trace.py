@@ -58,6 +58,9 @@ print(json.dumps({"launch_event_us": e0.elapsed_time(e1) * 1e3, "ctas": len(sp),
                   "items_per_cta": [int(np.percentile(sp[:, 3], q)) for q in (0, 50, 100)],
                   "tiles_per_cta": [int(np.percentile(sp[:, 4], q)) for q in (0, 10, 50, 90, 100)],
                   "first_tile_published_us": [float(np.percentile(sp[:, 5] - t0, q) / 1e3) for q in (0, 50, 100)],
+                  "kernel_entry_us": [float(np.percentile(sp[:, 6] - t0, q) / 1e3) for q in (0, 50, 100)],
+                  "prologue_done_us": [float(np.percentile(sp[:, 1] - t0, q) / 1e3) for q in (0, 50, 100)],
+                  "first_list_published_us": [float(np.percentile(sp[:, 7] - t0, q) / 1e3) for q in (0, 50, 100)],
                   "exit_us_vs_tiles": [[int(a), float((b - t0) / 1e3)] for a, b in
                                        sorted(zip(sp[:, 4], sp[:, 2]))[:: max(1, len(sp) // 12)]]}))
 NT = 1024
