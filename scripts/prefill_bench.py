@@ -94,6 +94,8 @@ def main():
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--block-size", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--packed-all", action="store_true",
+                    help="also time the packed entry on workloads without a shared prefix (shared = 0)")
     args = ap.parse_args()
     peak, peak_src = peaks()
     for name in args.configs.split(","):
@@ -114,10 +116,11 @@ def main():
                "mean_ctx": round(float(c["ctx"].mean()), 1), "ms": round(t * 1e3, 4),
                "tflops": round(tf, 1), "peak_tflops": peak, "peak_src": peak_src, "frac": round(tf / peak, 3),
                "query_tokens_per_s": round(c["qlen"].sum() / t, 0), "launches_per_call": launches}
-        if c["kind"] == "prefix":  # the packed (cascade) entry on the same workload
+        if c["kind"] == "prefix" or args.packed_all:  # the packed (cascade) entry on the same workload
             hqs = np.concatenate([[0], np.cumsum(c["qlen"])]).astype(np.int32)
+            shared = c["shared"] if "shared" in c else np.zeros(len(c["ctx"]), np.int32)
             fnp = lambda: pa.paged_prefill_attention_packed(  # noqa: E731
-                out, q, kc, vc, bt, cl, qs, scale, hqs, c["ctx"].astype(np.int32), c["shared"].astype(np.int32),
+                out, q, kc, vc, bt, cl, qs, scale, hqs, c["ctx"].astype(np.int32), shared.astype(np.int32),
                 max_query_len=mql, workspace=ws)
             tp = time_it(fnp, args.iters)
             res["packed_ms"] = round(tp * 1e3, 4)
