@@ -248,7 +248,8 @@ pa_status_t pa_paged_prefill_attention(void* out, const void* query, const void*
  * size is used).  The library packs greedily in order: an item grows while it stays <= 256
  * rows and its members' own tokens past the shared prefix P (P a multiple of the block
  * size, at most every member's first query position) stay <= 256 packed key columns; a
- * query longer than 256 rows takes items of its own.  Falls back to
+ * query longer than 256 rows takes items of its own.  A batch whose items would each hold
+ * one sequence (nothing packs) runs pa_paged_prefill_attention's kernels.  Falls back to
  * pa_paged_prefill_attention's kernels when block_size < 16 or more than 1024 tiles would
  * be needed.  Other arguments, layouts and errors as pa_paged_prefill_attention.
  * ---------------------------------------------------------------------------------- */
